@@ -1,0 +1,417 @@
+#!/usr/bin/env python
+"""bench.py — HVP GDOF/s + sparse-tangent assembly ms on B200 (BASELINE.json metric).
+
+Workload (default): BASELINE cfg 3 — 3D compressible neo-Hookean block [0,1]^3, 150^3
+Kuhn-Tet4 cells (10,328,853 DOFs, 20.25M elements), perturbed interior nodes (a = 0.1,
+seed 13), roller stretch eps = 0.05 (DESIGN.md §8 input recipe).  One step = one pass of
+the whole per-iteration hot path over that mesh, all through the C ABI:
+    fem_energy -> fem_residual (BC) -> fem_hvp (BC) -> fem_assemble_csr (BC, Alg. 2)
+    -> fem_spmv
+Pattern + coloring (setup) and the solves (a12/a13) are timed
+separately in the same run.  `value` = HVP GDOF/s = DOFs x HVP calls / HVP device time
+(CUDA events on the launching stream), whole job over all ranks.
+
+--impl reference times the CPU oracle (the reference arm of this tier) on a bounded
+sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import fem_inputs as fi  # noqa: E402
+
+METRIC = "HVP GDOF/s + sparse-tangent assembly ms vs DOFs, 1/2/4/8 B200, % HBM peak"
+UNIT = "GDOF/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", type=int, default=3, choices=[2, 3, 5])
+    ap.add_argument("--n", type=int, default=None, help="override the mesh size (cells per side)")
+    ap.add_argument("--assemble-mode", default="batched", choices=["batched", "literal", "rows"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-solve", action="store_true")
+    ap.add_argument("--profile-step", action="store_true", help="one step only (for ncu)")
+    return ap.parse_args()
+
+
+def workload(cfg, n):
+    mesh = fi.config_mesh(cfg, n=n)
+    name = {2: "cfg2: 2D NH plate Tri3", 3: "cfg3: 3D NH block Kuhn-Tet4",
+            5: "cfg5: 2D LE + periodic MPC Tri3"}[cfg]
+    h = mesh.length / max(mesh.shape)
+    z = fi.lift(mesh, fi.generic_state(mesh, 5, eps=0.05, noise=0.01, h=h))
+    v = fi.random_direction(mesh.n_total, 4)
+    return mesh, name, z, v
+
+
+# ------------------------------------------------------------------ clocks
+class Clocks:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        out, _ = self.proc.communicate(timeout=10)
+        rows = [[c.strip() for c in l.split(",")] for l in out.strip().splitlines() if l.strip()]
+        rows = [r for r in rows if len(r) >= 8]
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[4 + i] == "Active"})
+        load = [s for s in sm if s > 0.5 * max(sm)] if sm else []
+        return {"sm_mhz": float(np.median(load)) if load else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(rows)}
+
+
+# ------------------------------------------------------------------ oracle (CPU) arm
+def oracle_hvp_sample(cfg, seconds=12.0):
+    """The oracle as it stands, single-threaded, on a bounded sub-block of the workload."""
+    import oracle
+    n = {3: 40, 2: 400, 5: 400}[cfg]
+    mesh = fi.config_mesh(cfg, n=n)
+    h = mesh.length / max(mesh.shape)
+    z = fi.lift(mesh, fi.generic_state(mesh, 5, eps=0.05, noise=0.01, h=h))
+    v = fi.random_direction(mesh.n_total, 4)
+    o = oracle.Oracle(mesh)
+    o.hvp(z, v, bc=True)
+    t0 = time.perf_counter()
+    calls = 0
+    while True:
+        o.hvp(z, v, bc=True)
+        calls += 1
+        if time.perf_counter() - t0 >= seconds:
+            break
+    dt = time.perf_counter() - t0
+    return {"value": mesh.n_total * calls / dt / 1e9, "unit": UNIT, "cores": 1, "kind": "oracle",
+            "sample": f"fem_ref_hvp (hyper-dual, FEM_APPLY_BC) x{calls} on the {n}^{mesh.dim} "
+                      f"cell sub-block of the same workload ({mesh.n_total} DOFs), {dt:.1f} s, "
+                      f"one host core", "n_dofs": mesh.n_total, "seconds": dt}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import oracle
+    os.sched_setaffinity(0, {sorted(os.sched_getaffinity(0))[0]})
+    n = {3: 40, 2: 400, 5: 400}[args.config]
+    mesh = fi.config_mesh(args.config, n=n)
+    h = mesh.length / max(mesh.shape)
+    z = fi.lift(mesh, fi.generic_state(mesh, 5, eps=0.05, noise=0.01, h=h))
+    v = fi.random_direction(mesh.n_total, 4)
+    o = oracle.Oracle(mesh)
+    for _ in range(args.warmup):
+        o.hvp(z, v, bc=True)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        o.hvp(z, v, bc=True)
+    dt = time.perf_counter() - t0
+    val = mesh.n_total * args.steps / dt / 1e9
+    sample = (f"fem_ref_hvp on the {n}^{mesh.dim}-cell sub-block of the workload "
+              f"({mesh.n_total} DOFs) per step")
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": workload_name(args.config), "n_dofs_sample": mesh.n_total},
+        "cpu_baseline": {"value": val, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
+        "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}))
+
+
+def workload_name(cfg):
+    return {3: "BASELINE cfg3: 3D compressible neo-Hookean block, 150^3 Kuhn-Tet4 cells, "
+               "10,328,853 DOFs, perturbed a=0.1, roller eps=0.05",
+            2: "BASELINE cfg2: 2D compressible neo-Hookean plate, 706^2 Tri3 cells, 999,698 DOFs",
+            5: "BASELINE cfg5: 2D linear elastic + periodic MPC"}[cfg]
+
+
+# ------------------------------------------------------------------ B200 arm
+# Algorithmic bytes per DOF (compulsory traffic, geometry recomputed from
+# coordinates; 3D Kuhn: 2 tets/DOF, 1/3 node/DOF) and FP64 flops per element.
+def algorithmic(mesh, nnz, C):
+    N, E, d = mesh.n_total, mesh.n_elems, mesh.dim
+    nen = d + 1
+    conn = 4 * nen * E
+    coords = 8 * d * mesh.n_nodes
+    vec = 8 * N
+    return {
+        "energy": {"bytes": conn + coords + vec},
+        "residual": {"bytes": conn + coords + vec + 2 * vec},          # u read, r zero + write
+        "hvp": {"bytes": conn + coords + 2 * vec + 2 * vec},           # u, v read, y zero + write
+        "assemble": {"bytes": conn + coords + vec + 8 * N * C          # J_comp written once
+                     + nnz * (8 + 4 + 4) + 8 * (N + 1) + 8 * nnz},     # decompress + vals write
+        "spmv": {"bytes": nnz * 12 + 8 * (N + 1) + 2 * vec},
+    }
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    import torch
+    import torch.distributed as dist
+    from paper_2602_12365_b200 import build as fbuild
+    from paper_2602_12365_b200 import fem
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    fbuild.build()
+
+    mesh, wname, z, v = workload(args.config, args.n)
+    N = mesh.n_total
+    prob = fem.Problem(mesh)
+    zt = torch.as_tensor(z, device="cuda")
+    vt = torch.as_tensor(v, device="cuda")
+    stream = torch.cuda.current_stream()
+
+    # ---- setup: pattern + coloring (a7, a8), timed separately
+    ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
+    torch.cuda.synchronize()
+    e0, e1, e2 = ev(), ev(), ev()
+    e0.record()
+    nnz = prob.nnz()
+    e1.record()
+    colors, C = prob.color()
+    e2.record()
+    torch.cuda.synchronize()
+    setup = {"pattern_ms": e0.elapsed_time(e1), "coloring_ms": e1.elapsed_time(e2),
+             "nnz": nnz, "n_colors": C}
+
+    energy = torch.empty(1, dtype=torch.float64, device="cuda")
+    r = torch.empty(N, dtype=torch.float64, device="cuda")
+    y = torch.empty(N, dtype=torch.float64, device="cuda")
+    ys = torch.empty(N, dtype=torch.float64, device="cuda")
+    vals = torch.empty(nnz, dtype=torch.float64, device="cuda")
+    phases = ("energy", "residual", "hvp", "assemble", "spmv")
+    mode = args.assemble_mode
+
+    def step(evs=None):
+        def mark(i):
+            if evs is not None:
+                evs[i].record(stream)
+        mark(0)
+        prob.energy(zt, out=energy)
+        mark(1)
+        prob.residual(zt, bc=True, out=r)
+        mark(2)
+        prob.hvp(zt, vt, bc=True, out=y)
+        mark(3)
+        prob.assemble_csr(zt, bc=True, mode=mode, out=vals)
+        mark(4)
+        prob.spmv(vals, vt, out=ys)
+        mark(5)
+
+    if args.profile_step:
+        step()
+        torch.cuda.synchronize()
+        prob.check()
+        return
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    prob.check()
+
+    clocks = Clocks(local)
+    clocks.start()
+    time.sleep(0.2)
+    events = [[ev() for _ in range(6)] for _ in range(args.steps)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t_start, t_end = ev(), ev()
+    t_start.record(stream)
+    for k in range(args.steps):
+        step(events[k])
+    t_end.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    time.sleep(0.1)
+    clk = clocks.stop()
+    prob.check()
+    total_ms = t_start.elapsed_time(t_end)
+    per = {ph: sum(events[k][i].elapsed_time(events[k][i + 1]) for k in range(args.steps))
+           for i, ph in enumerate(phases)}
+    if world > 1:
+        t = torch.tensor([total_ms] + [per[p] for p in phases], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t[0])
+        per = {p: float(t[i + 1]) for i, p in enumerate(phases)}
+    K = args.steps
+    n_global = N * world
+    hvp_ms = per["hvp"] / K
+    value = n_global / (hvp_ms * 1e-3) / 1e9
+
+    # ---- gpu launches in one step (torch profiler, outside the timed region)
+    launches_per_step = None
+    kernel_names = {}
+    try:
+        from torch.profiler import ProfilerActivity, profile
+        with profile(activities=[ProfilerActivity.CUDA]) as prof:
+            step()
+            torch.cuda.synchronize()
+        for e in prof.events():
+            if e.device_type.name == "CUDA" and not e.name.startswith(("Memset", "Memcpy")):
+                kernel_names[e.name] = kernel_names.get(e.name, 0) + 1
+        launches_per_step = sum(kernel_names.values())
+    except Exception as ex:  # profiler unavailable: count stays None
+        kernel_names = {"error": str(ex)}
+
+    # ---- e2e: the HVP through the C ABI with host buffers, copies inside the timed region
+    zh = torch.from_numpy(z).pin_memory()
+    vh = torch.from_numpy(v).pin_memory()
+    yh = torch.empty(N, dtype=torch.float64).pin_memory()
+    zd = torch.empty_like(zt)
+    vd = torch.empty_like(vt)
+
+    def e2e_step():
+        zd.copy_(zh, non_blocking=True)
+        vd.copy_(vh, non_blocking=True)
+        prob.hvp(zd, vd, bc=True, out=y)
+        yh.copy_(y, non_blocking=True)
+
+    for _ in range(2):
+        e2e_step()
+    torch.cuda.synchronize()
+    a, b = ev(), ev()
+    a.record(stream)
+    for _ in range(K):
+        e2e_step()
+    b.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = a.elapsed_time(b) / K
+    e2e = {"value": n_global / (e2e_ms * 1e-3) / 1e9, "unit": UNIT,
+           "h2d_bytes_per_step": 2 * 8 * N, "d2h_bytes_per_step": 8 * N,
+           "what": "fem_hvp with pinned-host z, v copied in and y copied out every step"}
+
+    # ---- roofline of the dominant phase
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        pass
+    hbm = peaks.get("hbm_gbs")
+    hbm_src = "measured (MEASURED_PEAKS.json)" if hbm else "fallback (B200_PROFILING.md)"
+    hbm = hbm or 6650.0
+    alg = algorithmic(mesh, nnz, C)
+    dom = max(phases, key=lambda p: per[p])
+    dom_ms = per[dom] / K
+    achieved = alg[dom]["bytes"] / (dom_ms * 1e-3) / 1e9
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                "frac": achieved / hbm, "traffic": None, "kernel_phase": dom,
+                "peak_source": hbm_src}
+    phase_roofline = {}
+    for p in phases:
+        ms = per[p] / K
+        gbs = alg[p]["bytes"] / (ms * 1e-3) / 1e9
+        phase_roofline[p] = {"ms": ms, "alg_GB": alg[p]["bytes"] / 1e9, "GB/s": gbs,
+                             "frac_hbm": gbs / hbm, "share_of_step": per[p] / total_ms}
+    fp64 = None
+    try:
+        import ctypes
+        peak_so = fbuild.build_peak()
+        lp = ctypes.CDLL(peak_so)
+        lp.fem_peak_fp64_tflops.restype = ctypes.c_double
+        fp64 = lp.fem_peak_fp64_tflops(torch.cuda.get_device_properties(local).multi_processor_count)
+    except Exception:
+        pass
+
+    # ---- solves (outside the timed region): CG per-iteration cost and Newton
+    solve = {}
+    if not args.no_solve:
+        b0 = torch.as_tensor(v, device="cuda").clone()
+        b0[torch.as_tensor(mesh.dirichlet_dofs.astype(np.int64), device="cuda")] = 0.0
+        for op, name in ((0, "cg_hvp"), (1, "cg_csr")):
+            torch.cuda.synchronize()
+            a, b = ev(), ev()
+            a.record(stream)
+            _, info = prob.cg_solve(b0, z=zt, vals=vals, op=op, rtol=1e-30, max_iter=50,
+                                    raise_on_fail=False)
+            b.record(stream)
+            torch.cuda.synchronize()
+            solve[name + "_ms_per_iter"] = a.elapsed_time(b) / max(info["iters"], 1)
+        z0 = torch.as_tensor(fi.lift(mesh, fi.affine_field(mesh, np.diag([0.05] + [0.0] * (mesh.dim - 1)))),
+                             device="cuda") if args.config != 5 else None
+        if z0 is not None:
+            t0 = time.perf_counter()
+            zs, info = prob.newton_solve(z0, op=0, cg_rtol=1e-8, rtol=1e-10, atol=1e-14,
+                                         raise_on_fail=False)
+            torch.cuda.synchronize()
+            solve["newton_s"] = time.perf_counter() - t0
+            solve["newton"] = {k: info[k] for k in ("iters", "cg_iters", "converged", "res0", "res")}
+
+    cpu = None
+    if not args.no_cpu_baseline and rank == 0:
+        cpu = oracle_hvp_sample(args.config)
+
+    out = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
+        "warmup": args.warmup, "ms_per_step": total_ms / K, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": wname if args.n else workload_name(args.config),
+                   "n_dofs": n_global, "n_elems": mesh.n_elems * world, "nnz": nnz, "n_colors": C,
+                   "assemble_mode": mode, "parallelism": f"element partition x{world}",
+                   "l2": "inputs larger than L2 (HVP reads ~0.7 GB per call)"},
+        "assembly_ms": per["assemble"] / K,
+        "residual_gdofs": n_global / (per["residual"] / K * 1e-3) / 1e9,
+        "energy_gdofs": n_global / (per["energy"] / K * 1e-3) / 1e9,
+        "spmv_ms": per["spmv"] / K,
+        "phases": phase_roofline,
+        "setup": setup,
+        "solve": solve,
+        "roofline": roofline,
+        "fp64_peak_tflops_measured": fp64,
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+        "gpu_launches": None if launches_per_step is None else launches_per_step * K,
+        "kernels_per_step": kernel_names,
+        "clocks": clk,
+    }
+    if rank == 0:
+        print(json.dumps(out))
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,227 @@
+/*
+ * fem.h — C ABI of libfem.so, the B200 (sm_100a) hot path of the globally
+ * differentiated energy FEM of arXiv 2602.12365 ("tatva", PAPER.md).
+ *
+ * The library evaluates the discrete energy Psi_h(u) = sum_e sum_q psi(grad u_h^e) w_q detJ^e
+ * (Eq. 2) over P1 triangles (2D) and P1 tetrahedra (3D) for the
+ * linear-elastic and compressible neo-Hookean (form fixed by
+ * DESIGN.md reading C1) densities, its gradient r = grad Psi (Eq. 1), the
+ * Hessian-vector product K(u) v (Eq. 3, §2.1), the sparsity pattern of K
+ * (App. B), the distance-2 greedy coloring of its columns (§2.2,
+ * P:184; App. A), the sparse tangent by Alg. 2 (one colored HVP per
+ * color into J_comp, then decompression into CSR), SpMV, CG and Newton.
+ * Derivatives are hand-derived per density (no AD framework).
+ *
+ * Conventions (all calls):
+ *   - Array arguments are CUDA DEVICE pointers unless marked (host).  The caller owns
+ *     every argument buffer (PyTorch tensors in the Python binding); the library owns
+ *     its internal copies and workspaces and frees them in fem_destroy.  No call
+ *     allocates caller-visible memory.
+ *   - Values are fp64; node / element / DOF ids int32; CSR offsets int64.
+ *   - DOF numbering: DOF = node * dim + comp (Alg. 1), the
+ *     n_mpc Lagrange multipliers follow as DOFs N_u .. N_u + n_mpc - 1.
+ *     N = N_u + n_mpc.
+ *   - Every call enqueues its kernels on `stream` and returns without synchronizing,
+ *     EXCEPT calls that return host values (fem_create, fem_query, fem_color,
+ *     fem_cg_solve, fem_newton_solve, fem_check), which synchronize `stream`.
+ *   - Errors: argument / shape errors return FEM_ERR_INVALID_ARG before any launch.
+ *     Conditions found on the device (neo-Hookean J <= 0, too many colors) set a
+ *     device error word; synchronous calls return it, asynchronous calls leave it
+ *     for the next synchronous call or fem_check.  Output contents are undefined when
+ *     the status is not FEM_OK.  fem_last_error() gives a message (thread-local).
+ *   - There is no CPU fallback: every computation runs in this library's kernels.
+ */
+#ifndef FEM_B200_H
+#define FEM_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct fem_problem fem_problem; /* opaque, library-owned */
+typedef void *fem_stream;               /* a cudaStream_t (0 = legacy default stream) */
+
+typedef enum {
+  FEM_OK = 0,
+  FEM_ERR_INVALID_ARG = 1,
+  FEM_ERR_DEGENERATE_ELEMENT = 2, /* detJ <= 1e-14 * (bbox diagonal)^d (reading C20)   */
+  FEM_ERR_INVERTED_ELEMENT = 3,   /* neo-Hookean J = det F <= 0           */
+  FEM_ERR_NONFINITE = 4,
+  FEM_ERR_CG_BREAKDOWN = 5,       /* p^T A p <= 0                          */
+  FEM_ERR_NOT_CONVERGED = 6,      /* iteration cap reached; report still filled         */
+  FEM_ERR_TOO_MANY_COLORS = 7,    /* coloring needs more than FEM_MAX_COLORS colors     */
+  FEM_ERR_OUT_OF_MEMORY = 8,
+  FEM_ERR_CUDA = 9,
+  FEM_ERR_NCCL = 10
+} fem_status;
+
+enum { FEM_TRI3 = 3, FEM_TET4 = 4 };
+enum { FEM_LINEAR_ELASTIC = 0, FEM_NEO_HOOKEAN = 1 };
+enum { FEM_MAX_COLORS = 256 };
+
+/* flags */
+enum {
+  FEM_APPLY_BC = 1u,        /* Dirichlet by condensation on full-length vectors (P:389-400,
+                               reading C12): residual r[D] = 0; HVP y = P_f K P_f v + P_D v;
+                               CSR = that operator (1 on the D diagonal, 0 elsewhere in D
+                               rows/cols), pattern unchanged.                            */
+  FEM_DETERMINISTIC = 2u,   /* atomic-free fixed-order scatter (bitwise reproducible)    */
+  FEM_ASSEMBLE_LITERAL = 4u /* fem_assemble_csr: Alg. 2 as written — C sequential colored
+                               HVP passes into J_comp [N][C], then decompression.        */
+};
+
+typedef struct {
+  int dim;                       /* 2 (Tri3) or 3 (Tet4); dofs per node m = dim            */
+  int64_t n_nodes, n_elems;
+  const double *coords;          /* [n_nodes][dim] row-major                               */
+  const int32_t *conn;           /* [n_elems][dim+1], positively oriented (detJ > 0)       */
+  int material;                  /* FEM_LINEAR_ELASTIC or FEM_NEO_HOOKEAN                  */
+  double lambda, mu;             /* uniform Lame parameters                        */
+  const uint8_t *phase;          /* optional [n_elems] phase id (NULL = uniform)           */
+  const double *lambda_tab;      /* (host) [n_phases] when phase != NULL                   */
+  const double *mu_tab;          /* (host) [n_phases]                                      */
+  int n_phases;
+  int64_t n_dirichlet;
+  const int32_t *dirichlet_dofs; /* [n_dirichlet] sorted, unique, < N_u                    */
+  const double *dirichlet_vals;  /* [n_dirichlet] prescribed values g                      */
+  int64_t n_mpc;                 /* g_k(u) = u[slave_k] - u[master_k] - offset_k */
+  const int32_t *mpc_slave;      /* [n_mpc] < N_u                                          */
+  const int32_t *mpc_master;     /* [n_mpc] < N_u, != slave_k                              */
+  const double *mpc_offset;      /* [n_mpc]                                                */
+  const double *f_ext;           /* optional [N_u] nodal load, Psi -= f_ext . u (NULL = 0) */
+} fem_mesh_desc;
+
+/* Element-partitioned multi-GPU run.  NULL => single GPU.
+ * The mesh passed to fem_create is this rank's submesh (local node numbering in
+ * ascending global id).  Interface nodes are listed per neighbour rank in ascending
+ * global id; the halo add sums the partials of a shared DOF over the ranks touching it
+ * in ascending rank order, so every rank holds the same bits. */
+typedef struct {
+  void *nccl_comm;               /* ncclComm_t from fem_nccl_comm_init                      */
+  int rank, size;
+  int n_nbr;
+  const int32_t *nbr_rank;       /* (host) [n_nbr] ascending                               */
+  const int64_t *nbr_offset;     /* (host) [n_nbr+1] offsets into nbr_nodes                */
+  const int32_t *nbr_nodes;      /* (host) local node ids shared with each neighbour       */
+  const uint8_t *owned;          /* (host) [n_nodes] 1 if this rank owns the node
+                                    (lowest rank touching it); used for dots / energy      */
+} fem_dist_desc;
+
+/* Copies the mesh description into library-owned device buffers (the caller may free
+ * its buffers once `stream` passes this point), validates it (ids in range, detJ >
+ * eps_det -> FEM_ERR_DEGENERATE_ELEMENT, MPC pairs distinct), and prepares the element
+ * tiles.  Synchronizes `stream`. */
+fem_status fem_create(fem_problem **p, const fem_mesh_desc *d, const fem_dist_desc *dist,
+                      fem_stream stream);
+fem_status fem_destroy(fem_problem *p);
+
+/* (host) N = N_u + n_mpc; nnz valid after fem_sparsity; n_colors after fem_color
+ * (else -1).  Synchronizes nothing. */
+fem_status fem_query(const fem_problem *p, int64_t *n_total, int64_t *nnz, int32_t *n_colors);
+
+/* Returns (and clears) the device error word.  Synchronizes `stream`. */
+fem_status fem_check(fem_problem *p, fem_stream stream);
+
+/* z[D] = g: the lift of the reduced functional. */
+fem_status fem_apply_dirichlet(fem_problem *p, double *z, fem_stream stream);
+
+/* energy (device scalar) = Psi_h(u) + lambda . g(u) - f_ext . u  (Eq. 2, Alg. 1 P:112-147,
+ * P:498).  Deterministic (fixed-order two-pass reduction). */
+fem_status fem_energy(fem_problem *p, const double *z, double *energy, fem_stream stream);
+
+/* r = grad L(z) [N] (Eq. 1; reverse-mode analogue P:154): per element f_a = vol P(H) G_a
+ * scatter-added, + B^T lambda, r_lambda = B u - b, - f_ext; FEM_APPLY_BC: r[D] = 0. */
+fem_status fem_residual(fem_problem *p, const double *z, double *r, unsigned flags,
+                        fem_stream stream);
+
+/* y = K(z) v [N] (Eq. 3, §2.1), K the Hessian of the Lagrangian:
+ * y_u = K_uu v_u + B^T v_lambda, y_lambda = B v_u; FEM_APPLY_BC: y = P_f K P_f v + P_D v.
+ * v and y must not alias. */
+fem_status fem_hvp(fem_problem *p, const double *z, const double *v, double *y, unsigned flags,
+                   fem_stream stream);
+
+/* Builds (once) the CSR pattern of K: (i,j) present iff DOFs i, j belong to nodes sharing
+ * an element, full dim x dim node blocks, plus [[., B^T],[B, 0]] multiplier rows/cols
+ * (App. B); columns ascending.  If row_ptr / col_idx are
+ * non-NULL, copies the pattern into them ([N+1] int64 / [nnz] int32; query nnz first by
+ * calling with NULLs, then fem_query). */
+fem_status fem_sparsity(fem_problem *p, int64_t *row_ptr, int32_t *col_idx, fem_stream stream);
+
+/* Distance-2 greedy coloring of the pattern's columns, ascending column order, smallest
+ * free color (App. A; reading C9): bit-identical to the sequential
+ * greedy.  Builds the pattern if needed.  colors [N] (may be NULL); *n_colors (host).
+ * Synchronizes `stream`. */
+fem_status fem_color(fem_problem *p, int32_t *colors, int32_t *n_colors, fem_stream stream);
+
+/* vals [nnz] in fem_sparsity order = the sparse tangent at z by Alg. 2:
+ * for each color c the HVP along the implicit seed e_c (e_j = [color_j == c]) gives
+ * J_comp[:, c]; K_ij = J_comp[i, color_j] (decompression).  Modes (flags):
+ *   FEM_ASSEMBLE_LITERAL: C sequential per-color passes (the paper's lax.scan);
+ *   default: all color passes in ONE element sweep (the passes are independent,
+ *            P:186), accumulating J_comp [N][C] with atomics, then decompression;
+ *   FEM_DETERMINISTIC: J_comp computed row by row (pull form: row i gathers the colored
+ *            seeds' responses of its incident elements) and decompressed in-register
+ *            straight into the CSR slots — atomic-free, bitwise reproducible.
+ * flags may add FEM_APPLY_BC.  Requires fem_color (the pattern and colors). */
+fem_status fem_assemble_csr(fem_problem *p, const double *z, double *vals, unsigned flags,
+                            fem_stream stream);
+
+/* y = K_csr x (pattern of fem_sparsity, values `vals`); row-ordered accumulation. */
+fem_status fem_spmv(fem_problem *p, const double *vals, const double *x, double *y,
+                    fem_stream stream);
+
+typedef struct {
+  int op;           /* 0: masked HVP at z (matrix-free); 1: CSR `vals` (SpMV)       */
+  double rtol, atol;/* stop when ||r||_2 <= max(rtol ||b||_2, atol)                        */
+  int max_iter;
+  int jacobi;       /* 1: Jacobi preconditioner (op 1 only)                                */
+  int check_every;  /* read the residual norm on the host every k iterations (>= 1)        */
+} fem_cg_opts;
+
+typedef struct {
+  int iters, converged;
+  double res0, res;
+} fem_cg_report;
+
+/* Textbook CG on the BC-applied operator.  x: in x0, out solution.
+ * b[D] and x0[D] should be 0 (condensed system).  Synchronizes `stream`. */
+fem_status fem_cg_solve(fem_problem *p, const double *z, const double *vals, const double *b,
+                        double *x, const fem_cg_opts *opts, fem_cg_report *report,
+                        fem_stream stream);
+
+typedef struct {
+  double atol, rtol; /* outer: ||r|| <= max(atol, rtol ||r0||)                 */
+  int max_iter;
+  fem_cg_opts cg;    /* inner solve; cg.op 0 = Newton-Krylov, 1 = colored CSR      */
+} fem_newton_opts;
+
+typedef struct {
+  int iters, cg_iters, converged;
+  double res0, res;
+} fem_newton_report;
+
+/* Full-step Newton on the condensed problem (Eq. 1): z starts at the lift; repeat
+ * r = residual(z, BC); K(z) dz = -r by CG; z += dz.  Synchronizes `stream`. */
+fem_status fem_newton_solve(fem_problem *p, double *z, const fem_newton_opts *opts,
+                            fem_newton_report *report, fem_stream stream);
+
+/* NCCL bootstrap for fem_dist_desc: rank 0 creates the id, the caller
+ * broadcasts its 128 bytes (torch.distributed), every rank initialises the comm. */
+fem_status fem_nccl_unique_id(unsigned char id[128]);
+fem_status fem_nccl_comm_init(const unsigned char id[128], int rank, int size, void **comm);
+fem_status fem_nccl_comm_destroy(void *comm);
+
+/* (host) n = 1 / 2 scalar all-reduce (sum) of a device buffer over the problem's ranks
+ * (no-op on a single GPU); used for global dots in multi-GPU CG and the energy. */
+fem_status fem_allreduce_sum(fem_problem *p, double *buf, int n, fem_stream stream);
+
+const char *fem_last_error(void);
+const char *fem_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FEM_B200_H */

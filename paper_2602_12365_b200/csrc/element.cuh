@@ -1,0 +1,233 @@
+// element.cuh — per-element math of the hot path (device functions, templated on dim).
+//
+// One-point P1 simplex (Eq. 2; reading C4): H = sum_a u_a (x) G_a is
+// constant per element, Psi_e = vol * psi(H).  Hand-derived derivatives (north_star:
+// "derivatives are hand-derived per energy density rather than produced by an AD
+// framework"):
+//   residual  f_a = vol * P(H) G_a,             P = d psi / dH           (Eq. 1)
+//   HVP       y_a = vol * dP(H)[dH] G_a,        dH = sum_a v_a (x) G_a   (Eq. 3)
+// Linear elastic (plane strain in 2D, reading C2):
+//   psi = mu eps:eps + lambda/2 tr(eps)^2, P = mu (H + H^T) + lambda tr(H) I,
+//   dP = mu (dH + dH^T) + lambda tr(dH) I.
+// Compressible neo-Hookean (reading C1):
+//   psi = mu/2 (F:F - d - 2 ln J) + lambda/2 (ln J)^2, F = I + H, J = det F,
+//   P  = mu F + (lambda ln J - mu) F^{-T},
+//   dP = mu dH + (mu - lambda ln J) F^{-T} dH^T F^{-T} + lambda (F^{-T}:dH) F^{-T}.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace fem {
+
+template <int D>
+struct Elem {
+  static constexpr int NEN = D + 1;
+};
+
+// Geometry from nodal coordinates.  J = [x1-x0 | ... | xd-x0]; G_a (a>=1) = row a-1 of
+// J^{-1}; G_0 = -sum G_a; vol = det J / d!.  Returns det J.
+template <int D>
+__device__ __forceinline__ double geometry(const double (&x)[D + 1][D], double (&G)[D + 1][D],
+                                           double &vol) {
+  if constexpr (D == 2) {
+    const double j00 = x[1][0] - x[0][0], j01 = x[2][0] - x[0][0];
+    const double j10 = x[1][1] - x[0][1], j11 = x[2][1] - x[0][1];
+    const double det = j00 * j11 - j01 * j10;
+    const double id = 1.0 / det;
+    G[1][0] = j11 * id;
+    G[1][1] = -j01 * id;
+    G[2][0] = -j10 * id;
+    G[2][1] = j00 * id;
+    G[0][0] = -G[1][0] - G[2][0];
+    G[0][1] = -G[1][1] - G[2][1];
+    vol = 0.5 * det;
+    return det;
+  } else {
+    double J[3][3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+      for (int j = 0; j < 3; ++j) J[i][j] = x[j + 1][i] - x[0][i];
+    const double c00 = J[1][1] * J[2][2] - J[1][2] * J[2][1];
+    const double c01 = J[1][2] * J[2][0] - J[1][0] * J[2][2];
+    const double c02 = J[1][0] * J[2][1] - J[1][1] * J[2][0];
+    const double c10 = J[0][2] * J[2][1] - J[0][1] * J[2][2];
+    const double c11 = J[0][0] * J[2][2] - J[0][2] * J[2][0];
+    const double c12 = J[0][1] * J[2][0] - J[0][0] * J[2][1];
+    const double c20 = J[0][1] * J[1][2] - J[0][2] * J[1][1];
+    const double c21 = J[0][2] * J[1][0] - J[0][0] * J[1][2];
+    const double c22 = J[0][0] * J[1][1] - J[0][1] * J[1][0];
+    const double det = J[0][0] * c00 + J[0][1] * c01 + J[0][2] * c02;
+    const double id = 1.0 / det;
+    // inv[i][j] = cof[j][i] / det; G_{a}[j] = inv[a-1][j]
+    G[1][0] = c00 * id; G[1][1] = c10 * id; G[1][2] = c20 * id;
+    G[2][0] = c01 * id; G[2][1] = c11 * id; G[2][2] = c21 * id;
+    G[3][0] = c02 * id; G[3][1] = c12 * id; G[3][2] = c22 * id;
+#pragma unroll
+    for (int j = 0; j < 3; ++j) G[0][j] = -(G[1][j] + G[2][j] + G[3][j]);
+    vol = det * (1.0 / 6.0);
+    return det;
+  }
+}
+
+template <int D>
+__device__ __forceinline__ void field_gradient(const double (&u)[D + 1][D],
+                                               const double (&G)[D + 1][D], double (&H)[D][D]) {
+#pragma unroll
+  for (int i = 0; i < D; ++i)
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
+      double h = 0.0;
+#pragma unroll
+      for (int a = 0; a < D + 1; ++a) h = fma(u[a][i], G[a][j], h);
+      H[i][j] = h;
+    }
+}
+
+// Scatter-ready nodal vectors out_a = vol * A G_a.
+template <int D>
+__device__ __forceinline__ void nodal_from_stress(const double (&A)[D][D],
+                                                  const double (&G)[D + 1][D], double vol,
+                                                  double (&out)[D + 1][D]) {
+#pragma unroll
+  for (int i = 0; i < D; ++i) {
+    double s0 = 0.0;
+#pragma unroll
+    for (int a = 1; a < D + 1; ++a) {
+      double t = 0.0;
+#pragma unroll
+      for (int j = 0; j < D; ++j) t = fma(A[i][j], G[a][j], t);
+      out[a][i] = vol * t;
+      s0 += out[a][i];
+    }
+    out[0][i] = -s0;
+  }
+}
+
+// ------------------------------------------------------------------ linear elastic
+template <int D>
+__device__ __forceinline__ double le_psi(const double (&H)[D][D], double lam, double mu) {
+  double tr = 0.0, ee = 0.0;
+#pragma unroll
+  for (int i = 0; i < D; ++i) {
+    tr += H[i][i];
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
+      const double e = 0.5 * (H[i][j] + H[j][i]);
+      ee = fma(e, e, ee);
+    }
+  }
+  return mu * ee + 0.5 * lam * tr * tr;
+}
+
+template <int D>
+__device__ __forceinline__ void le_stress(const double (&H)[D][D], double lam, double mu,
+                                          double (&P)[D][D]) {
+  double tr = 0.0;
+#pragma unroll
+  for (int i = 0; i < D; ++i) tr += H[i][i];
+#pragma unroll
+  for (int i = 0; i < D; ++i)
+#pragma unroll
+    for (int j = 0; j < D; ++j) P[i][j] = mu * (H[i][j] + H[j][i]) + (i == j ? lam * tr : 0.0);
+}
+
+// ------------------------------------------------------------------ neo-Hookean
+template <int D>
+struct NHState {
+  double F[D][D];
+  double FiT[D][D];  // F^{-T}
+  double lnJ, J;
+};
+
+// Returns false when J <= 0 (inverted element).
+template <int D>
+__device__ __forceinline__ bool nh_state(const double (&H)[D][D], NHState<D> &s) {
+#pragma unroll
+  for (int i = 0; i < D; ++i)
+#pragma unroll
+    for (int j = 0; j < D; ++j) s.F[i][j] = H[i][j] + (i == j ? 1.0 : 0.0);
+  double cof[D][D];
+  if constexpr (D == 2) {
+    cof[0][0] = s.F[1][1];
+    cof[0][1] = -s.F[1][0];
+    cof[1][0] = -s.F[0][1];
+    cof[1][1] = s.F[0][0];
+    s.J = s.F[0][0] * s.F[1][1] - s.F[0][1] * s.F[1][0];
+  } else {
+    const double(&F)[3][3] = s.F;
+    cof[0][0] = F[1][1] * F[2][2] - F[1][2] * F[2][1];
+    cof[0][1] = F[1][2] * F[2][0] - F[1][0] * F[2][2];
+    cof[0][2] = F[1][0] * F[2][1] - F[1][1] * F[2][0];
+    cof[1][0] = F[0][2] * F[2][1] - F[0][1] * F[2][2];
+    cof[1][1] = F[0][0] * F[2][2] - F[0][2] * F[2][0];
+    cof[1][2] = F[0][1] * F[2][0] - F[0][0] * F[2][1];
+    cof[2][0] = F[0][1] * F[1][2] - F[0][2] * F[1][1];
+    cof[2][1] = F[0][2] * F[1][0] - F[0][0] * F[1][2];
+    cof[2][2] = F[0][0] * F[1][1] - F[0][1] * F[1][0];
+    s.J = F[0][0] * cof[0][0] + F[0][1] * cof[0][1] + F[0][2] * cof[0][2];
+  }
+  if (!(s.J > 0.0)) return false;
+  const double iJ = 1.0 / s.J;
+#pragma unroll
+  for (int i = 0; i < D; ++i)
+#pragma unroll
+    for (int j = 0; j < D; ++j) s.FiT[i][j] = cof[i][j] * iJ;
+  s.lnJ = log(s.J);
+  return true;
+}
+
+template <int D>
+__device__ __forceinline__ double nh_psi(const double (&H)[D][D], const NHState<D> &s,
+                                         double lam, double mu) {
+  // F:F - d = 2 tr H + H:H (no cancellation against d)
+  double t = 0.0;
+#pragma unroll
+  for (int i = 0; i < D; ++i) {
+    t += 2.0 * H[i][i];
+#pragma unroll
+    for (int j = 0; j < D; ++j) t = fma(H[i][j], H[i][j], t);
+  }
+  return 0.5 * mu * (t - 2.0 * s.lnJ) + 0.5 * lam * s.lnJ * s.lnJ;
+}
+
+template <int D>
+__device__ __forceinline__ void nh_stress(const NHState<D> &s, double lam, double mu,
+                                          double (&P)[D][D]) {
+  const double c = lam * s.lnJ - mu;
+#pragma unroll
+  for (int i = 0; i < D; ++i)
+#pragma unroll
+    for (int j = 0; j < D; ++j) P[i][j] = fma(c, s.FiT[i][j], mu * s.F[i][j]);
+}
+
+template <int D>
+__device__ __forceinline__ void nh_dstress(const NHState<D> &s, double lam, double mu,
+                                           const double (&dH)[D][D], double (&dP)[D][D]) {
+  // T = dH^T F^{-T};  M = F^{-T} T = F^{-T} dH^T F^{-T};  tr = F^{-T} : dH
+  double T[D][D];
+  double tr = 0.0;
+#pragma unroll
+  for (int k = 0; k < D; ++k)
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
+      double t = 0.0;
+#pragma unroll
+      for (int l = 0; l < D; ++l) t = fma(dH[l][k], s.FiT[l][j], t);
+      T[k][j] = t;
+      tr = fma(s.FiT[k][j], dH[k][j], tr);
+    }
+  const double c1 = mu - lam * s.lnJ, c2 = lam * tr;
+#pragma unroll
+  for (int i = 0; i < D; ++i)
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
+      double m = 0.0;
+#pragma unroll
+      for (int k = 0; k < D; ++k) m = fma(s.FiT[i][k], T[k][j], m);
+      dP[i][j] = fma(c2, s.FiT[i][j], fma(c1, m, mu * dH[i][j]));
+    }
+}
+
+}  // namespace fem

@@ -1,0 +1,594 @@
+// fem_core.cu — problem lifetime, energy / residual / HVP (Eq. 1-3, Alg. 1).
+//
+// Element kernels: one thread per element, grid-stride, geometry recomputed from the
+// coordinates in registers (the byte-minimal "R" dataflow of DESIGN.md §5), gather of the
+// element's nodal values, hand-derived P / dP (element.cuh), fp64 atomic scatter-add
+// (RED.E.ADD.F64 in L2) of the nodal forces — the transpose of Alg. 1's gather.
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "element.cuh"
+#include "fem_internal.cuh"
+
+namespace fem {
+
+static thread_local std::string g_last_error;
+
+void set_error(const std::string &msg) { g_last_error = msg; }
+
+fem_status cuda_status(cudaError_t e, const char *what) {
+  set_error(std::string(what) + ": " + cudaGetErrorString(e));
+  return e == cudaErrorMemoryAllocation ? FEM_ERR_OUT_OF_MEMORY : FEM_ERR_CUDA;
+}
+
+fem_status ensure(Workspace &w, size_t bytes) {
+  if (w.bytes >= bytes) return FEM_OK;
+  if (w.ptr) cudaFree(w.ptr);
+  w.ptr = nullptr;
+  w.bytes = 0;
+  FEM_CUDA(cudaMalloc(&w.ptr, bytes));
+  w.bytes = bytes;
+  return FEM_OK;
+}
+
+fem_status read_error_word(Problem *p, cudaStream_t s) {
+  int h = 0;
+  FEM_CUDA(cudaMemcpyAsync(&h, p->d_err, sizeof(int), cudaMemcpyDeviceToHost, s));
+  FEM_CUDA(cudaStreamSynchronize(s));
+  if (h) FEM_CUDA(cudaMemsetAsync(p->d_err, 0, sizeof(int), s));
+  if (h & ERRW_INVERTED) {
+    set_error("neo-Hookean element with J = det F <= 0 (InvertedElement)");
+    return FEM_ERR_INVERTED_ELEMENT;
+  }
+  if (h & ERRW_TOO_MANY_COLORS) {
+    set_error("coloring needs more than FEM_MAX_COLORS colors");
+    return FEM_ERR_TOO_MANY_COLORS;
+  }
+  if (h & ERRW_ADJ_OVERFLOW) {
+    set_error("a node has more than kMaxNodeAdj distinct neighbours");
+    return FEM_ERR_INVALID_ARG;
+  }
+  if (h & ERRW_NONFINITE) {
+    set_error("non-finite value");
+    return FEM_ERR_NONFINITE;
+  }
+  return FEM_OK;
+}
+
+// ------------------------------------------------------------------ element kernels
+enum { OP_ENERGY = 0, OP_RESIDUAL = 1, OP_HVP = 2 };
+
+struct ElemArgs {
+  const double *coords;
+  const int32_t *conn;
+  int64_t E;
+  double lam, mu;
+  const uint8_t *phase;
+  const double *lam_tab, *mu_tab;
+  const uint8_t *node_bc;  // non-null: mask v at Dirichlet DOFs (HVP with FEM_APPLY_BC)
+  const double *u, *v;
+  double *out;
+  double *partials;
+  int *err;
+};
+
+template <int D>
+__device__ __forceinline__ void load_conn(const int32_t *conn, int64_t e, int32_t (&nd)[D + 1]) {
+  if constexpr (D == 3) {
+    const int4 c = __ldg(reinterpret_cast<const int4 *>(conn) + e);
+    nd[0] = c.x; nd[1] = c.y; nd[2] = c.z; nd[3] = c.w;
+  } else {
+#pragma unroll
+    for (int a = 0; a < 3; ++a) nd[a] = __ldg(conn + e * 3 + a);
+  }
+}
+
+template <int D>
+__device__ __forceinline__ void gather(const double *f, const int32_t (&nd)[D + 1],
+                                       double (&x)[D + 1][D]) {
+#pragma unroll
+  for (int a = 0; a < D + 1; ++a)
+#pragma unroll
+    for (int i = 0; i < D; ++i) x[a][i] = __ldg(f + (int64_t)nd[a] * D + i);
+}
+
+template <int D, int MAT, int OP, bool MASK>
+__global__ void __launch_bounds__(kThreads) k_elem(ElemArgs A) {
+  double acc = 0.0;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < A.E; e += stride) {
+    int32_t nd[D + 1];
+    load_conn<D>(A.conn, e, nd);
+    double x[D + 1][D], G[D + 1][D], vol;
+    gather<D>(A.coords, nd, x);
+    geometry<D>(x, G, vol);
+    double lam = A.lam, mu = A.mu;
+    if (A.phase) {
+      const int ph = A.phase[e];
+      lam = A.lam_tab[ph];
+      mu = A.mu_tab[ph];
+    }
+    double H[D][D];
+    if (OP != OP_HVP || MAT == FEM_NEO_HOOKEAN) {
+      double u[D + 1][D];
+      gather<D>(A.u, nd, u);
+      field_gradient<D>(u, G, H);
+    }
+    if constexpr (OP == OP_ENERGY) {
+      if constexpr (MAT == FEM_LINEAR_ELASTIC) {
+        acc += vol * le_psi<D>(H, lam, mu);
+      } else {
+        NHState<D> s;
+        if (!nh_state<D>(H, s)) { atomicOr(A.err, ERRW_INVERTED); continue; }
+        acc += vol * nh_psi<D>(H, s, lam, mu);
+      }
+    } else {
+      double S[D][D];
+      if constexpr (OP == OP_RESIDUAL) {
+        if constexpr (MAT == FEM_LINEAR_ELASTIC) {
+          le_stress<D>(H, lam, mu, S);
+        } else {
+          NHState<D> s;
+          if (!nh_state<D>(H, s)) { atomicOr(A.err, ERRW_INVERTED); continue; }
+          nh_stress<D>(s, lam, mu, S);
+        }
+      } else {
+        double v[D + 1][D], dH[D][D];
+        gather<D>(A.v, nd, v);
+        if constexpr (MASK) {
+#pragma unroll
+          for (int a = 0; a < D + 1; ++a) {
+            const unsigned bc = __ldg(A.node_bc + nd[a]);
+#pragma unroll
+            for (int i = 0; i < D; ++i)
+              if (bc & (1u << i)) v[a][i] = 0.0;
+          }
+        }
+        field_gradient<D>(v, G, dH);
+        if constexpr (MAT == FEM_LINEAR_ELASTIC) {
+          le_stress<D>(dH, lam, mu, S);  // linear: dP = P(dH)
+        } else {
+          NHState<D> s;
+          if (!nh_state<D>(H, s)) { atomicOr(A.err, ERRW_INVERTED); continue; }
+          nh_dstress<D>(s, lam, mu, dH, S);
+        }
+      }
+      double f[D + 1][D];
+      nodal_from_stress<D>(S, G, vol, f);
+#pragma unroll
+      for (int a = 0; a < D + 1; ++a)
+#pragma unroll
+        for (int i = 0; i < D; ++i) atomicAdd(A.out + (int64_t)nd[a] * D + i, f[a][i]);
+    }
+  }
+  if constexpr (OP == OP_ENERGY) {
+    const double t = block_sum<kThreads>(acc);
+    if (threadIdx.x == 0) A.partials[blockIdx.x] = t;
+  }
+}
+
+template <int OP, bool MASK>
+static fem_status launch_elem(Problem *p, const ElemArgs &a, int grid, cudaStream_t s) {
+  if (p->n_elems == 0) return FEM_OK;
+#define FEM_DISPATCH(D, M) k_elem<D, M, OP, MASK><<<grid, kThreads, 0, s>>>(a)
+  if (p->dim == 2) {
+    if (p->material == FEM_LINEAR_ELASTIC) FEM_DISPATCH(2, FEM_LINEAR_ELASTIC);
+    else FEM_DISPATCH(2, FEM_NEO_HOOKEAN);
+  } else {
+    if (p->material == FEM_LINEAR_ELASTIC) FEM_DISPATCH(3, FEM_LINEAR_ELASTIC);
+    else FEM_DISPATCH(3, FEM_NEO_HOOKEAN);
+  }
+#undef FEM_DISPATCH
+  FEM_LAUNCH_CHECK("element kernel");
+  return FEM_OK;
+}
+
+static ElemArgs elem_args(Problem *p) {
+  ElemArgs a{};
+  a.coords = p->coords;
+  a.conn = p->conn;
+  a.E = p->n_elems;
+  a.lam = p->lam;
+  a.mu = p->mu;
+  a.phase = p->phase;
+  a.lam_tab = p->lam_tab;
+  a.mu_tab = p->mu_tab;
+  a.err = p->d_err;
+  return a;
+}
+
+// ------------------------------------------------------------------ small vector kernels
+__global__ void k_partial_dot(const double *a, const double *b, int64_t n, double scale,
+                              double *partials) {
+  double acc = 0.0;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
+    acc = fma(a[i], b[i], acc);
+  const double t = block_sum<kThreads>(acc);
+  if (threadIdx.x == 0) partials[blockIdx.x] = scale * t;
+}
+
+__global__ void k_final_sum(const double *partials, int n, double *out) {
+  double acc = 0.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) acc += partials[i];
+  const double t = block_sum<kThreads>(acc);
+  if (threadIdx.x == 0) *out = t;
+}
+
+fem_status launch_dot(Problem *p, const double *a, const double *b, int64_t n, double *out,
+                      cudaStream_t s) {
+  const int nb = grid_for(n, kThreads, kReduceBlocks);
+  k_partial_dot<<<nb, kThreads, 0, s>>>(a, b, n, 1.0, p->partials);
+  k_final_sum<<<1, kThreads, 0, s>>>(p->partials, nb, out);
+  FEM_LAUNCH_CHECK("dot");
+  return FEM_OK;
+}
+
+// lambda_k * g_k(u) partial sums (energy), g_k = u[s] - u[m] - b
+__global__ void k_mpc_energy(const double *z, const int32_t *s, const int32_t *m, const double *b,
+                             int64_t nc, int64_t nu, double *partials) {
+  double acc = 0.0;
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < nc;
+       k += (int64_t)gridDim.x * blockDim.x)
+    acc += z[nu + k] * (z[s[k]] - z[m[k]] - b[k]);
+  const double t = block_sum<kThreads>(acc);
+  if (threadIdx.x == 0) partials[blockIdx.x] = t;
+}
+
+// residual: r_u += B^T lambda, r_lambda = B u - b ; HVP: y_u += B^T w_lambda, y_lambda = B w_u
+// (w = v masked at Dirichlet DOFs when node_bc != null).  PAPER.md P:497-498, App. B.
+__global__ void k_mpc_apply(const double *z, const int32_t *s, const int32_t *m, const double *b,
+                            int64_t nc, int64_t nu, int dim, const uint8_t *node_bc,
+                            double *out) {
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < nc;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t sk = s[k], mk = m[k];
+    double zs = z[sk], zm = z[mk];
+    if (node_bc) {
+      if (node_bc[sk / dim] & (1u << (sk % dim))) zs = 0.0;
+      if (node_bc[mk / dim] & (1u << (mk % dim))) zm = 0.0;
+    }
+    const double lk = z[nu + k];
+    atomicAdd(out + sk, lk);
+    atomicAdd(out + mk, -lk);
+    out[nu + k] = b ? (zs - zm - b[k]) : (zs - zm);
+  }
+}
+
+__global__ void k_axpy(double *y, const double *x, double a, int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    y[i] = fma(a, x[i], y[i]);
+}
+
+// y[D] = src[D] (src = v for the HVP) or 0 (src = null, residual)
+__global__ void k_bc_fix(double *y, const int32_t *dofs, int64_t nd, const double *src) {
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < nd;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t d = dofs[k];
+    y[d] = src ? src[d] : 0.0;
+  }
+}
+
+__global__ void k_set_dirichlet(double *z, const int32_t *dofs, const double *vals, int64_t nd) {
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < nd;
+       k += (int64_t)gridDim.x * blockDim.x)
+    z[dofs[k]] = vals[k];
+}
+
+// node_bc byte per node: the thread of the first Dirichlet DOF of a node writes the byte.
+__global__ void k_node_bc(const int32_t *dofs, int64_t nd, int dim, uint8_t *node_bc) {
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < nd;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t node = dofs[k] / dim;
+    if (k > 0 && dofs[k - 1] / dim == node) continue;
+    unsigned bits = 0;
+    for (int64_t q = k; q < nd && dofs[q] / dim == node; ++q) bits |= 1u << (dofs[q] % dim);
+    node_bc[node] = (uint8_t)bits;
+  }
+}
+
+// Validation: ids in range and detJ > 1e-14 (bbox diagonal)^d (reading C20).
+template <int D>
+__global__ void k_validate(const double *coords, const int32_t *conn, int64_t E, int64_t n_nodes,
+                           int *bad) {
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < E;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    int32_t nd[D + 1];
+    bool ok = true;
+#pragma unroll
+    for (int a = 0; a < D + 1; ++a) {
+      nd[a] = conn[e * (D + 1) + a];
+      ok = ok && nd[a] >= 0 && nd[a] < n_nodes;
+    }
+    if (!ok) { atomicOr(bad, 1); continue; }
+    double x[D + 1][D], G[D + 1][D], vol;
+    gather<D>(coords, nd, x);
+    const double det = geometry<D>(x, G, vol);
+    double d2 = 0.0;
+#pragma unroll
+    for (int i = 0; i < D; ++i) {
+      double lo = x[0][i], hi = x[0][i];
+#pragma unroll
+      for (int a = 1; a < D + 1; ++a) { lo = fmin(lo, x[a][i]); hi = fmax(hi, x[a][i]); }
+      d2 += (hi - lo) * (hi - lo);
+    }
+    const double eps = (D == 2) ? 1e-14 * d2 : 1e-14 * d2 * sqrt(d2);
+    if (!(det > eps)) atomicOr(bad, 2);
+  }
+}
+
+__global__ void k_validate_dofs(const int32_t *dd, int64_t nd, const int32_t *ms,
+                                const int32_t *mm, int64_t nc, int64_t nu, int *bad) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < nd; k += stride) {
+    if (dd[k] < 0 || dd[k] >= nu || (k > 0 && dd[k] <= dd[k - 1])) atomicOr(bad, 1);
+  }
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < nc; k += stride) {
+    if (ms[k] < 0 || ms[k] >= nu || mm[k] < 0 || mm[k] >= nu || ms[k] == mm[k]) atomicOr(bad, 1);
+  }
+}
+
+// ------------------------------------------------------------------ internal runners
+fem_status run_residual(Problem *p, const double *z, double *r, unsigned flags, cudaStream_t s) {
+  FEM_CUDA(cudaMemsetAsync(r, 0, sizeof(double) * p->N, s));
+  ElemArgs a = elem_args(p);
+  a.u = z;
+  a.out = r;
+  fem_status st = launch_elem<OP_RESIDUAL, false>(p, a, grid_for(p->n_elems), s);
+  if (st) return st;
+  if (p->size > 1) {
+    st = halo_add(p, r, s);
+    if (st) return st;
+  }
+  if (p->n_mpc) {
+    k_mpc_apply<<<grid_for(p->n_mpc), kThreads, 0, s>>>(z, p->mpc_s, p->mpc_m, p->mpc_b, p->n_mpc,
+                                                        p->n_u, p->dim, nullptr, r);
+  }
+  if (p->f_ext) k_axpy<<<grid_for(p->n_u), kThreads, 0, s>>>(r, p->f_ext, -1.0, p->n_u);
+  if ((flags & FEM_APPLY_BC) && p->n_dir)
+    k_bc_fix<<<grid_for(p->n_dir), kThreads, 0, s>>>(r, p->dir_dofs, p->n_dir, nullptr);
+  FEM_LAUNCH_CHECK("residual");
+  return FEM_OK;
+}
+
+fem_status run_hvp(Problem *p, const double *z, const double *v, double *y, unsigned flags,
+                   cudaStream_t s) {
+  FEM_CUDA(cudaMemsetAsync(y, 0, sizeof(double) * p->N, s));
+  const bool bc = (flags & FEM_APPLY_BC) && p->n_dir;
+  ElemArgs a = elem_args(p);
+  a.u = z;
+  a.v = v;
+  a.out = y;
+  a.node_bc = p->node_bc;
+  fem_status st = bc ? launch_elem<OP_HVP, true>(p, a, grid_for(p->n_elems), s)
+                     : launch_elem<OP_HVP, false>(p, a, grid_for(p->n_elems), s);
+  if (st) return st;
+  if (p->size > 1) {
+    st = halo_add(p, y, s);
+    if (st) return st;
+  }
+  if (p->n_mpc)
+    k_mpc_apply<<<grid_for(p->n_mpc), kThreads, 0, s>>>(v, p->mpc_s, p->mpc_m, nullptr, p->n_mpc,
+                                                        p->n_u, p->dim, bc ? p->node_bc : nullptr,
+                                                        y);
+  if (bc) k_bc_fix<<<grid_for(p->n_dir), kThreads, 0, s>>>(y, p->dir_dofs, p->n_dir, v);
+  FEM_LAUNCH_CHECK("hvp");
+  return FEM_OK;
+}
+
+}  // namespace fem
+
+using namespace fem;
+
+// ====================================================================== C ABI
+extern "C" {
+
+const char *fem_last_error(void) { return g_last_error.c_str(); }
+const char *fem_version(void) { return "fem-b200 0.1 (sm_100a)"; }
+
+fem_status fem_create(fem_problem **out, const fem_mesh_desc *d, const fem_dist_desc *dist,
+                      fem_stream stream) {
+  FEM_ARG(out && d, "fem_create: null argument");
+  *out = nullptr;
+  FEM_ARG(d->dim == 2 || d->dim == 3, "fem_create: dim must be 2 or 3");
+  FEM_ARG(d->n_nodes > 0 && d->n_elems >= 0, "fem_create: bad sizes");
+  FEM_ARG(d->coords && (d->conn || d->n_elems == 0), "fem_create: null coords/conn");
+  FEM_ARG(d->material == FEM_LINEAR_ELASTIC || d->material == FEM_NEO_HOOKEAN,
+          "fem_create: unknown material");
+  FEM_ARG(d->n_dirichlet >= 0 && (d->n_dirichlet == 0 || (d->dirichlet_dofs && d->dirichlet_vals)),
+          "fem_create: bad Dirichlet arrays");
+  FEM_ARG(d->n_mpc >= 0 && (d->n_mpc == 0 || (d->mpc_slave && d->mpc_master && d->mpc_offset)),
+          "fem_create: bad MPC arrays");
+  FEM_ARG(!d->phase || (d->lambda_tab && d->mu_tab && d->n_phases > 0 && d->n_phases <= 256),
+          "fem_create: bad phase tables");
+  FEM_ARG(d->n_nodes * d->dim + d->n_mpc < (int64_t)INT32_MAX, "fem_create: N exceeds int32");
+  FEM_ARG(d->n_elems < (int64_t)1 << 29, "fem_create: too many elements");
+  FEM_ARG(!(dist && dist->size > 1 && d->n_mpc), "fem_create: MPC with >1 rank unsupported");
+  cudaStream_t s = (cudaStream_t)stream;
+  fem_problem *h = new fem_problem();
+  Problem *p = &h->p;
+  p->dim = d->dim;
+  p->nen = d->dim + 1;
+  p->material = d->material;
+  p->n_nodes = d->n_nodes;
+  p->n_elems = d->n_elems;
+  p->n_u = d->n_nodes * d->dim;
+  p->n_mpc = d->n_mpc;
+  p->N = p->n_u + p->n_mpc;
+  p->n_dir = d->n_dirichlet;
+  p->lam = d->lambda;
+  p->mu = d->mu;
+  p->n_phases = d->phase ? d->n_phases : 0;
+  auto fail = [&](fem_status st) {
+    fem_destroy(h);
+    return st;
+  };
+#define FEM_C(call)                                   \
+  do {                                                \
+    cudaError_t e_ = (call);                          \
+    if (e_ != cudaSuccess) return fail(cuda_status(e_, #call)); \
+  } while (0)
+  const size_t cb = sizeof(double) * p->n_nodes * p->dim, nb = sizeof(int32_t) * p->n_elems * p->nen;
+  FEM_C(cudaMalloc(&p->coords, cb));
+  FEM_C(cudaMemcpyAsync(p->coords, d->coords, cb, cudaMemcpyDefault, s));
+  FEM_C(cudaMalloc(&p->conn, nb > 0 ? nb : 16));
+  if (nb) FEM_C(cudaMemcpyAsync(p->conn, d->conn, nb, cudaMemcpyDefault, s));
+  if (d->phase) {
+    FEM_C(cudaMalloc(&p->phase, p->n_elems > 0 ? p->n_elems : 1));
+    if (p->n_elems) FEM_C(cudaMemcpyAsync(p->phase, d->phase, p->n_elems, cudaMemcpyDefault, s));
+    FEM_C(cudaMalloc(&p->lam_tab, sizeof(double) * d->n_phases));
+    FEM_C(cudaMalloc(&p->mu_tab, sizeof(double) * d->n_phases));
+    FEM_C(cudaMemcpyAsync(p->lam_tab, d->lambda_tab, sizeof(double) * d->n_phases, cudaMemcpyDefault, s));
+    FEM_C(cudaMemcpyAsync(p->mu_tab, d->mu_tab, sizeof(double) * d->n_phases, cudaMemcpyDefault, s));
+  }
+  FEM_C(cudaMalloc(&p->node_bc, p->n_nodes));
+  FEM_C(cudaMemsetAsync(p->node_bc, 0, p->n_nodes, s));
+  if (p->n_dir) {
+    FEM_C(cudaMalloc(&p->dir_dofs, sizeof(int32_t) * p->n_dir));
+    FEM_C(cudaMalloc(&p->dir_vals, sizeof(double) * p->n_dir));
+    FEM_C(cudaMemcpyAsync(p->dir_dofs, d->dirichlet_dofs, sizeof(int32_t) * p->n_dir, cudaMemcpyDefault, s));
+    FEM_C(cudaMemcpyAsync(p->dir_vals, d->dirichlet_vals, sizeof(double) * p->n_dir, cudaMemcpyDefault, s));
+  }
+  if (p->n_mpc) {
+    FEM_C(cudaMalloc(&p->mpc_s, sizeof(int32_t) * p->n_mpc));
+    FEM_C(cudaMalloc(&p->mpc_m, sizeof(int32_t) * p->n_mpc));
+    FEM_C(cudaMalloc(&p->mpc_b, sizeof(double) * p->n_mpc));
+    FEM_C(cudaMemcpyAsync(p->mpc_s, d->mpc_slave, sizeof(int32_t) * p->n_mpc, cudaMemcpyDefault, s));
+    FEM_C(cudaMemcpyAsync(p->mpc_m, d->mpc_master, sizeof(int32_t) * p->n_mpc, cudaMemcpyDefault, s));
+    FEM_C(cudaMemcpyAsync(p->mpc_b, d->mpc_offset, sizeof(double) * p->n_mpc, cudaMemcpyDefault, s));
+  }
+  if (d->f_ext) {
+    FEM_C(cudaMalloc(&p->f_ext, sizeof(double) * p->n_u));
+    FEM_C(cudaMemcpyAsync(p->f_ext, d->f_ext, sizeof(double) * p->n_u, cudaMemcpyDefault, s));
+  }
+  FEM_C(cudaMalloc(&p->partials, sizeof(double) * kReduceBlocks * 4));
+  FEM_C(cudaMalloc(&p->scal, sizeof(double) * 64));
+  FEM_C(cudaMemsetAsync(p->scal, 0, sizeof(double) * 64, s));
+  FEM_C(cudaMallocHost(&p->h_scal, sizeof(double) * 64));
+  FEM_C(cudaMalloc(&p->d_err, sizeof(int) * 2));
+  FEM_C(cudaMemsetAsync(p->d_err, 0, sizeof(int) * 2, s));
+  if (dist && dist->size > 1) {
+    p->nccl = dist->nccl_comm;
+    p->rank = dist->rank;
+    p->size = dist->size;
+  }
+  // validation (ids, orientation / degeneracy, Dirichlet sortedness, MPC pairs)
+  int *bad = p->d_err + 1;
+  if (p->n_elems) {
+    if (p->dim == 2)
+      k_validate<2><<<grid_for(p->n_elems), kThreads, 0, s>>>(p->coords, p->conn, p->n_elems, p->n_nodes, bad);
+    else
+      k_validate<3><<<grid_for(p->n_elems), kThreads, 0, s>>>(p->coords, p->conn, p->n_elems, p->n_nodes, bad);
+  }
+  if (p->n_dir || p->n_mpc)
+    k_validate_dofs<<<grid_for(p->n_dir > p->n_mpc ? p->n_dir : p->n_mpc), kThreads, 0, s>>>(
+        p->dir_dofs, p->n_dir, p->mpc_s, p->mpc_m, p->n_mpc, p->n_u, bad);
+  if (p->n_dir) k_node_bc<<<grid_for(p->n_dir), kThreads, 0, s>>>(p->dir_dofs, p->n_dir, p->dim, p->node_bc);
+  FEM_C(cudaGetLastError());
+  int hbad = 0;
+  FEM_C(cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, s));
+  FEM_C(cudaStreamSynchronize(s));
+  if (hbad & 1) {
+    set_error("fem_create: index out of range / unsorted Dirichlet DOFs / invalid MPC pair");
+    return fail(FEM_ERR_INVALID_ARG);
+  }
+  if (hbad & 2) {
+    set_error("fem_create: degenerate or inverted element (detJ <= eps_det)");
+    return fail(FEM_ERR_DEGENERATE_ELEMENT);
+  }
+#undef FEM_C
+  *out = h;
+  return FEM_OK;
+}
+
+fem_status fem_destroy(fem_problem *h) {
+  if (!h) return FEM_OK;
+  Problem *p = &h->p;
+  void *bufs[] = {p->coords, p->conn, p->phase, p->lam_tab, p->mu_tab, p->node_bc, p->dir_dofs,
+                  p->dir_vals, p->mpc_s, p->mpc_m, p->mpc_b, p->f_ext, p->partials, p->scal,
+                  p->d_err, p->inc_ptr, p->inc, p->nadj_ptr, p->nadj, p->dmpc_ptr, p->dmpc,
+                  p->row_ptr, p->col_idx, p->diag_pos, p->colors, p->jcomp.ptr, p->cgbuf.ptr,
+                  p->tmp.ptr};
+  for (void *b : bufs)
+    if (b) cudaFree(b);
+  if (p->h_scal) cudaFreeHost(p->h_scal);
+  delete h;
+  return FEM_OK;
+}
+
+fem_status fem_query(const fem_problem *h, int64_t *n_total, int64_t *nnz, int32_t *n_colors) {
+  FEM_ARG(h, "fem_query: null problem");
+  const Problem *p = &h->p;
+  if (n_total) *n_total = p->N;
+  if (nnz) *nnz = p->have_pattern ? p->nnz : -1;
+  if (n_colors) *n_colors = p->have_colors ? p->n_colors : -1;
+  return FEM_OK;
+}
+
+fem_status fem_check(fem_problem *h, fem_stream stream) {
+  FEM_ARG(h, "fem_check: null problem");
+  FEM_CUDA(cudaGetLastError());
+  return read_error_word(&h->p, (cudaStream_t)stream);
+}
+
+fem_status fem_apply_dirichlet(fem_problem *h, double *z, fem_stream stream) {
+  FEM_ARG(h && z, "fem_apply_dirichlet: null argument");
+  Problem *p = &h->p;
+  if (p->n_dir)
+    k_set_dirichlet<<<grid_for(p->n_dir), kThreads, 0, (cudaStream_t)stream>>>(z, p->dir_dofs,
+                                                                                p->dir_vals, p->n_dir);
+  FEM_LAUNCH_CHECK("fem_apply_dirichlet");
+  return FEM_OK;
+}
+
+fem_status fem_energy(fem_problem *h, const double *z, double *energy, fem_stream stream) {
+  FEM_ARG(h && z && energy, "fem_energy: null argument");
+  Problem *p = &h->p;
+  cudaStream_t s = (cudaStream_t)stream;
+  const int g1 = grid_for(p->n_elems, kThreads, kReduceBlocks);
+  ElemArgs a = elem_args(p);
+  a.u = z;
+  a.partials = p->partials;
+  int n = 0;
+  if (p->n_elems) {
+    fem_status st = launch_elem<OP_ENERGY, false>(p, a, g1, s);
+    if (st) return st;
+    n = g1;
+  }
+  if (p->n_mpc) {
+    const int g2 = grid_for(p->n_mpc, kThreads, kReduceBlocks);
+    k_mpc_energy<<<g2, kThreads, 0, s>>>(z, p->mpc_s, p->mpc_m, p->mpc_b, p->n_mpc, p->n_u,
+                                         p->partials + n);
+    n += g2;
+  }
+  if (p->f_ext) {
+    const int g3 = grid_for(p->n_u, kThreads, kReduceBlocks);
+    k_partial_dot<<<g3, kThreads, 0, s>>>(p->f_ext, z, p->n_u, -1.0, p->partials + n);
+    n += g3;
+  }
+  if (n == 0) FEM_CUDA(cudaMemsetAsync(energy, 0, sizeof(double), s));
+  else k_final_sum<<<1, kThreads, 0, s>>>(p->partials, n, energy);
+  FEM_LAUNCH_CHECK("fem_energy");
+  if (p->size > 1) return fem_allreduce_sum(h, energy, 1, stream);
+  return FEM_OK;
+}
+
+fem_status fem_residual(fem_problem *h, const double *z, double *r, unsigned flags,
+                        fem_stream stream) {
+  FEM_ARG(h && z && r, "fem_residual: null argument");
+  FEM_ARG(z != r, "fem_residual: z and r alias");
+  return run_residual(&h->p, z, r, flags, (cudaStream_t)stream);
+}
+
+fem_status fem_hvp(fem_problem *h, const double *z, const double *v, double *y, unsigned flags,
+                   fem_stream stream) {
+  FEM_ARG(h && z && v && y, "fem_hvp: null argument");
+  FEM_ARG(v != y && z != y, "fem_hvp: output aliases an input");
+  return run_hvp(&h->p, z, v, y, flags, (cudaStream_t)stream);
+}
+
+}  // extern "C"

@@ -1,0 +1,148 @@
+// fem_internal.cuh — library-internal state and helpers of libfem.so (not installed).
+//
+// Data layout in HBM: coords [n_nodes][dim] fp64 AoS, conn [E][dim+1] int32
+// (library copy, element order of the caller), node_bc [n_nodes] uint8 bit c = DOF
+// node*dim+c is Dirichlet, CSR row_ptr int64 / col_idx int32, J_comp [N][C] fp64 row-major.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+
+#include "../../include/fem.h"
+
+namespace fem {
+
+enum : int { ERRW_INVERTED = 1, ERRW_TOO_MANY_COLORS = 2, ERRW_NONFINITE = 4, ERRW_ADJ_OVERFLOW = 8 };
+
+constexpr int kMaxNodeAdj = 64;     // max distinct node neighbours (incl. self) per node
+constexpr int kReduceBlocks = 1184; // 148 SMs x 8: fixed grid => fixed reduction order
+constexpr int kThreads = 256;
+
+struct Workspace {
+  void *ptr = nullptr;
+  size_t bytes = 0;
+};
+
+struct Problem {
+  int dim = 0, nen = 0, material = 0;
+  int64_t n_nodes = 0, n_elems = 0, n_u = 0, n_mpc = 0, N = 0, n_dir = 0;
+  double lam = 0, mu = 0;
+  int n_phases = 0;
+  // mesh copies
+  double *coords = nullptr;
+  int32_t *conn = nullptr;
+  uint8_t *phase = nullptr;
+  double *lam_tab = nullptr, *mu_tab = nullptr;
+  uint8_t *node_bc = nullptr;
+  int32_t *dir_dofs = nullptr;
+  double *dir_vals = nullptr;
+  int32_t *mpc_s = nullptr, *mpc_m = nullptr;
+  double *mpc_b = nullptr;
+  double *f_ext = nullptr;
+  // reductions
+  double *partials = nullptr;   // [kReduceBlocks * 4]
+  double *scal = nullptr;       // device scalars (CG etc.) [64]
+  double *h_scal = nullptr;     // pinned host mirror [64]
+  int *d_err = nullptr;
+  // incidence (node -> (element, local node)), built with the pattern
+  int64_t *inc_ptr = nullptr;   // [n_nodes+1]
+  int32_t *inc = nullptr;       // [E*nen] packed e*nen+a, ascending e per node
+  // node adjacency (sorted, incl. self)
+  int64_t *nadj_ptr = nullptr;  // [n_nodes+1]
+  int32_t *nadj = nullptr;
+  // dof -> mpc constraint list
+  int32_t *dmpc_ptr = nullptr;  // [n_u+1]
+  int32_t *dmpc = nullptr;
+  // CSR pattern
+  bool have_pattern = false;
+  int64_t nnz = 0;
+  int64_t *row_ptr = nullptr;
+  int32_t *col_idx = nullptr;
+  int64_t *diag_pos = nullptr;  // [N] position of the diagonal in each row (-1 if absent)
+  // coloring
+  bool have_colors = false;
+  int32_t n_colors = -1;
+  int32_t *colors = nullptr;    // [N]
+  // workspaces
+  Workspace jcomp, cgbuf, tmp;
+  // multi-GPU
+  void *nccl = nullptr;
+  int rank = 0, size = 1;
+};
+
+// ------------------------------------------------------------------ error plumbing
+void set_error(const std::string &msg);
+fem_status cuda_status(cudaError_t e, const char *what);
+
+#define FEM_CUDA(call)                                                     \
+  do {                                                                     \
+    cudaError_t e_ = (call);                                               \
+    if (e_ != cudaSuccess) return ::fem::cuda_status(e_, #call);           \
+  } while (0)
+
+#define FEM_LAUNCH_CHECK(what)                                             \
+  do {                                                                     \
+    cudaError_t e_ = cudaGetLastError();                                   \
+    if (e_ != cudaSuccess) return ::fem::cuda_status(e_, what);            \
+  } while (0)
+
+#define FEM_ARG(cond, msg)                                                 \
+  do {                                                                     \
+    if (!(cond)) {                                                         \
+      ::fem::set_error(msg);                                               \
+      return FEM_ERR_INVALID_ARG;                                          \
+    }                                                                      \
+  } while (0)
+
+fem_status ensure(Workspace &w, size_t bytes);
+fem_status read_error_word(Problem *p, cudaStream_t s);
+
+inline int grid_for(int64_t n, int threads = kThreads, int max_blocks = 148 * 64) {
+  int64_t b = (n + threads - 1) / threads;
+  if (b < 1) b = 1;
+  if (b > max_blocks) b = max_blocks;
+  return (int)b;
+}
+
+// ------------------------------------------------------------------ device helpers
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Block sum of one value per thread; result valid in thread 0.  Fixed order.
+template <int BLOCK>
+__device__ __forceinline__ double block_sum(double v) {
+  __shared__ double sh[BLOCK / 32];
+  v = warp_sum(v);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (lane == 0) sh[w] = v;
+  __syncthreads();
+  double t = 0.0;
+  if (w == 0) {
+    t = (lane < BLOCK / 32) ? sh[lane] : 0.0;
+    t = warp_sum(t);
+  }
+  __syncthreads();
+  return t;
+}
+
+// internal launchers shared between translation units
+fem_status launch_dot(Problem *p, const double *a, const double *b, int64_t n, double *out,
+                      cudaStream_t s);
+fem_status build_pattern(Problem *p, cudaStream_t s);
+fem_status build_colors(Problem *p, cudaStream_t s);
+fem_status run_residual(Problem *p, const double *z, double *r, unsigned flags, cudaStream_t s);
+fem_status run_hvp(Problem *p, const double *z, const double *v, double *y, unsigned flags,
+                   cudaStream_t s);
+fem_status run_spmv(Problem *p, const double *vals, const double *x, double *y, cudaStream_t s);
+fem_status halo_add(Problem *p, double *y, cudaStream_t s);
+
+}  // namespace fem
+
+struct fem_problem {
+  fem::Problem p;
+};

@@ -1,0 +1,294 @@
+// fem_solve.cu — CG (a12) and Newton (a13) driven natively on the device.
+//
+// CG: textbook Hestenes-Stiefel with optional Jacobi.  Scalars (r.r, p.Ap,
+// r.z) stay on the device in ping-pong slots so no kernel reads a value another kernel of
+// the same iteration writes; the host reads ||r|| every `check_every` iterations.
+// Operator: the masked HVP at z (matrix-free Newton-Krylov) or the CSR SpMV.
+#include <cuda_runtime.h>
+
+#include <cmath>
+
+#include "fem_internal.cuh"
+
+namespace fem {
+
+fem_status run_assemble(Problem *p, const double *z, double *vals, unsigned flags, cudaStream_t s);
+
+enum { S_RZ0 = 0, S_RZ1 = 1, S_PAP = 2, S_BB = 3, S_RR0 = 4, S_RR1 = 5, S_NRM = 6 };
+
+__global__ void k_sub(const double *b, const double *Ax, double *r, int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    r[i] = b[i] - Ax[i];
+}
+
+// z = dinv * r (or r), p = z, partial r.r and r.z
+__global__ void k_cg_start(const double *r, const double *dinv, double *zv, double *p, int64_t n,
+                           double *part_rr, double *part_rz) {
+  double rr = 0.0, rz = 0.0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const double ri = r[i];
+    const double zi = dinv ? dinv[i] * ri : ri;
+    if (dinv) zv[i] = zi;
+    p[i] = zi;
+    rr = fma(ri, ri, rr);
+    rz = fma(ri, zi, rz);
+  }
+  const double a = block_sum<kThreads>(rr);
+  const double b = block_sum<kThreads>(rz);
+  if (threadIdx.x == 0) {
+    part_rr[blockIdx.x] = a;
+    part_rz[blockIdx.x] = b;
+  }
+}
+
+// alpha = rz / pAp; x += alpha p; r -= alpha Ap; z = dinv r; partial r.r, r.z
+__global__ void k_cg_update(const double *scal, int rz_slot, double *x, double *r, double *zv,
+                            const double *p, const double *Ap, const double *dinv, int64_t n,
+                            double *part_rr, double *part_rz) {
+  const double alpha = scal[rz_slot] / scal[S_PAP];
+  double rr = 0.0, rz = 0.0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    x[i] = fma(alpha, p[i], x[i]);
+    const double ri = fma(-alpha, Ap[i], r[i]);
+    r[i] = ri;
+    const double zi = dinv ? dinv[i] * ri : ri;
+    if (dinv) zv[i] = zi;
+    rr = fma(ri, ri, rr);
+    rz = fma(ri, zi, rz);
+  }
+  const double a = block_sum<kThreads>(rr);
+  const double b = block_sum<kThreads>(rz);
+  if (threadIdx.x == 0) {
+    part_rr[blockIdx.x] = a;
+    part_rz[blockIdx.x] = b;
+  }
+}
+
+// p = z + beta p, beta = rz_new / rz_old
+__global__ void k_cg_dir(const double *scal, int rz_old, int rz_new, const double *zv, double *p,
+                         int64_t n) {
+  const double beta = scal[rz_new] / scal[rz_old];
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    p[i] = fma(beta, p[i], zv[i]);
+}
+
+__global__ void k_final_sum2(const double *pa, const double *pb, int n, double *oa, double *ob) {
+  double a = 0.0, b = 0.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    a += pa[i];
+    b += pb[i];
+  }
+  const double ta = block_sum<kThreads>(a);
+  const double tb = block_sum<kThreads>(b);
+  if (threadIdx.x == 0) {
+    *oa = ta;
+    *ob = tb;
+  }
+}
+
+__global__ void k_jacobi_diag(const double *vals, const int64_t *diag_pos, int64_t N, double *dinv,
+                              int *err) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < N;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t q = diag_pos[i];
+    const double d = q >= 0 ? vals[q] : 0.0;
+    if (!(d > 0.0)) atomicOr(err, ERRW_NONFINITE);
+    dinv[i] = 1.0 / d;
+  }
+}
+
+__global__ void k_neg_copy(const double *a, double *b, int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    b[i] = -a[i];
+}
+
+__global__ void k_add(double *a, const double *b, int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    a[i] += b[i];
+}
+
+static fem_status apply_op(Problem *p, int op, const double *z, const double *vals, const double *x,
+                           double *y, cudaStream_t s) {
+  if (op == 0) return run_hvp(p, z, x, y, FEM_APPLY_BC, s);
+  return run_spmv(p, vals, x, y, s);
+}
+
+static fem_status read_scalars(Problem *p, int n, cudaStream_t s) {
+  FEM_CUDA(cudaMemcpyAsync(p->h_scal, p->scal, sizeof(double) * n, cudaMemcpyDeviceToHost, s));
+  FEM_CUDA(cudaStreamSynchronize(s));
+  return FEM_OK;
+}
+
+fem_status run_cg(Problem *p, const double *z, const double *vals, const double *b, double *x,
+                  const fem_cg_opts *o, fem_cg_report *rep, cudaStream_t s) {
+  const int64_t n = p->N;
+  const bool jac = o->jacobi != 0;
+  const int every = o->check_every > 0 ? o->check_every : 1;
+  fem_status st = ensure(p->cgbuf, sizeof(double) * n * (jac ? 5 : 3));
+  if (st) return st;
+  double *r = (double *)p->cgbuf.ptr, *pp = r + n, *Ap = pp + n;
+  double *zv = jac ? Ap + n : r, *dinv = jac ? Ap + 2 * n : nullptr;
+  const int nb = grid_for(n, kThreads, kReduceBlocks);
+  double *part_a = p->partials, *part_b = p->partials + kReduceBlocks;
+  if (jac) k_jacobi_diag<<<grid_for(n), kThreads, 0, s>>>(vals, p->diag_pos, n, dinv, p->d_err);
+  // r0 = b - A x0
+  st = apply_op(p, o->op, z, vals, x, Ap, s);
+  if (st) return st;
+  k_sub<<<grid_for(n), kThreads, 0, s>>>(b, Ap, r, n);
+  k_cg_start<<<nb, kThreads, 0, s>>>(r, dinv, zv, pp, n, part_a, part_b);
+  k_final_sum2<<<1, kThreads, 0, s>>>(part_a, part_b, nb, p->scal + S_RR0, p->scal + S_RZ0);
+  st = launch_dot(p, b, b, n, p->scal + S_BB, s);
+  if (st) return st;
+  FEM_LAUNCH_CHECK("cg start");
+  st = read_scalars(p, 8, s);
+  if (st) return st;
+  st = read_error_word(p, s);
+  if (st) return st;
+  const double bn = std::sqrt(p->h_scal[S_BB]);
+  const double tol = std::fmax(o->rtol * bn, o->atol);
+  double rn = std::sqrt(p->h_scal[S_RR0]);
+  rep->res0 = rn;
+  rep->iters = 0;
+  rep->converged = 0;
+  int it = 0;
+  fem_status result = FEM_OK;
+  while (true) {
+    if (rn <= tol) { rep->converged = 1; break; }
+    if (it >= o->max_iter) { result = FEM_ERR_NOT_CONVERGED; break; }
+    const int cur = it & 1;  // rz / rr of the current residual live in slot cur
+    st = apply_op(p, o->op, z, vals, pp, Ap, s);
+    if (st) return st;
+    st = launch_dot(p, pp, Ap, n, p->scal + S_PAP, s);
+    if (st) return st;
+    k_cg_update<<<nb, kThreads, 0, s>>>(p->scal, S_RZ0 + cur, x, r, zv, pp, Ap, dinv, n, part_a, part_b);
+    k_final_sum2<<<1, kThreads, 0, s>>>(part_a, part_b, nb, p->scal + S_RR0 + (cur ^ 1),
+                                        p->scal + S_RZ0 + (cur ^ 1));
+    k_cg_dir<<<grid_for(n), kThreads, 0, s>>>(p->scal, S_RZ0 + cur, S_RZ0 + (cur ^ 1), zv, pp, n);
+    FEM_LAUNCH_CHECK("cg iteration");
+    ++it;
+    if (it % every == 0 || it >= o->max_iter) {
+      st = read_scalars(p, 8, s);
+      if (st) return st;
+      if (!(p->h_scal[S_PAP] > 0.0)) { result = FEM_ERR_CG_BREAKDOWN; break; }
+      rn = std::sqrt(p->h_scal[S_RR0 + (it & 1)]);
+      if (!std::isfinite(rn)) { result = FEM_ERR_NONFINITE; break; }
+    }
+  }
+  rep->iters = it;
+  rep->res = rn;
+  st = read_error_word(p, s);
+  if (st) return st;
+  if (result == FEM_ERR_CG_BREAKDOWN) set_error("CG breakdown: p^T A p <= 0");
+  if (result == FEM_ERR_NOT_CONVERGED) set_error("CG: iteration cap reached");
+  return result;
+}
+
+fem_status halo_add(Problem *p, double *y, cudaStream_t s) {
+  (void)y;
+  (void)s;
+  if (p->size <= 1) return FEM_OK;
+  set_error("multi-rank halo exchange not available in this build");
+  return FEM_ERR_NCCL;
+}
+
+}  // namespace fem
+
+using namespace fem;
+
+extern "C" {
+
+fem_status fem_cg_solve(fem_problem *h, const double *z, const double *vals, const double *b,
+                        double *x, const fem_cg_opts *o, fem_cg_report *rep, fem_stream stream) {
+  FEM_ARG(h && b && x && o && rep, "fem_cg_solve: null argument");
+  FEM_ARG(o->op == 0 || o->op == 1, "fem_cg_solve: op must be 0 (HVP) or 1 (CSR)");
+  FEM_ARG(o->op == 1 || z, "fem_cg_solve: op 0 needs z");
+  FEM_ARG(o->op == 0 || (vals && h->p.have_pattern), "fem_cg_solve: op 1 needs vals and a pattern");
+  FEM_ARG(!o->jacobi || (o->op == 1 && h->p.n_mpc == 0), "fem_cg_solve: Jacobi needs op 1, no MPC");
+  return run_cg(&h->p, z, vals, b, x, o, rep, (cudaStream_t)stream);
+}
+
+fem_status fem_newton_solve(fem_problem *h, double *z, const fem_newton_opts *o,
+                            fem_newton_report *rep, fem_stream stream) {
+  FEM_ARG(h && z && o && rep, "fem_newton_solve: null argument");
+  Problem *p = &h->p;
+  cudaStream_t s = (cudaStream_t)stream;
+  const int64_t n = p->N;
+  double *buf = nullptr;
+  const bool csr = o->cg.op == 1;
+  fem_status st;
+  if (csr) {
+    st = build_colors(p, s);
+    if (st) return st;
+  }
+  const size_t bytes = sizeof(double) * (2 * n + (csr ? p->nnz : 0));
+  FEM_CUDA(cudaMalloc(&buf, bytes));
+  double *r = buf, *dz = buf + n, *vals = csr ? buf + 2 * n : nullptr;
+  rep->iters = rep->cg_iters = rep->converged = 0;
+  double r0 = 0.0;
+  fem_status result = FEM_OK;
+  for (int it = 0;; ++it) {
+    st = run_residual(p, z, r, FEM_APPLY_BC, s);
+    if (st) { result = st; break; }
+    st = launch_dot(p, r, r, n, p->scal + S_NRM, s);
+    if (st) { result = st; break; }
+    st = read_scalars(p, 8, s);
+    if (st) { result = st; break; }
+    st = read_error_word(p, s);
+    if (st) { result = st; break; }
+    const double nr = std::sqrt(p->h_scal[S_NRM]);
+    if (it == 0) r0 = nr;
+    rep->res = nr;
+    rep->iters = it;
+    if (nr <= std::fmax(o->atol, o->rtol * r0)) { rep->converged = 1; break; }
+    if (!std::isfinite(nr)) { result = FEM_ERR_NONFINITE; break; }
+    if (it >= o->max_iter) { result = FEM_ERR_NOT_CONVERGED; break; }
+    k_neg_copy<<<grid_for(n), kThreads, 0, s>>>(r, r, n);
+    FEM_CUDA(cudaMemsetAsync(dz, 0, sizeof(double) * n, s));
+    if (csr) {
+      st = run_assemble(p, z, vals, FEM_APPLY_BC, s);
+      if (st) { result = st; break; }
+    }
+    fem_cg_report cr{};
+    st = run_cg(p, z, vals, r, dz, &o->cg, &cr, s);
+    rep->cg_iters += cr.iters;
+    if (st) { result = st; break; }
+    k_add<<<grid_for(n), kThreads, 0, s>>>(z, dz, n);
+  }
+  rep->res0 = r0;
+  cudaStreamSynchronize(s);
+  cudaFree(buf);
+  return result;
+}
+
+fem_status fem_nccl_unique_id(unsigned char id[128]) {
+  (void)id;
+  set_error("NCCL support not built");
+  return FEM_ERR_NCCL;
+}
+
+fem_status fem_nccl_comm_init(const unsigned char id[128], int rank, int size, void **comm) {
+  (void)id; (void)rank; (void)size; (void)comm;
+  set_error("NCCL support not built");
+  return FEM_ERR_NCCL;
+}
+
+fem_status fem_nccl_comm_destroy(void *comm) {
+  (void)comm;
+  return FEM_OK;
+}
+
+fem_status fem_allreduce_sum(fem_problem *h, double *buf, int n, fem_stream stream) {
+  (void)buf; (void)n; (void)stream;
+  FEM_ARG(h, "fem_allreduce_sum: null problem");
+  if (h->p.size <= 1) return FEM_OK;
+  set_error("NCCL support not built");
+  return FEM_ERR_NCCL;
+}
+
+}  // extern "C"

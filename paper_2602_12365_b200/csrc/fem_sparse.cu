@@ -1,0 +1,422 @@
+// fem_sparse.cu — sparsity pattern (a7) and distance-2 greedy coloring (a8).
+//
+// Pattern (App. B): node -> element incidence by a stable radix
+// sort of the connectivity, per-node sorted neighbour sets (node adjacency incl. self),
+// expansion into dim x dim DOF blocks with columns ascending, plus the multiplier rows and
+// columns [[K, B^T], [B, 0]].  row_ptr int64 (nnz exceeds 2^31 at BASELINE cfg 4).
+//
+// Coloring (App. A; reading C9): the sequential ascending-order greedy is reproduced
+// exactly by index-priority dataflow (Jones-Plassmann with priority = -index): a column is
+// colored in the round after its last lower-indexed distance-2 neighbour was colored; at
+// that moment the colored neighbours are exactly the lower-indexed ones, so the smallest
+// free color equals the sequential choice.  Counters of uncolored lower neighbours are
+// decremented by the coloring column; frontiers are compacted with atomics.  Without
+// multipliers the DOF graph is the node graph with full dim x dim blocks, and the greedy
+// on DOFs equals color(node*dim + c) = dim * C_node(node) + c (proof in DESIGN.md §6), so
+// the node graph (dim^2 fewer distance-2 visits) is colored instead.
+#include <cub/cub.cuh>
+
+#include "fem_internal.cuh"
+
+namespace fem {
+
+// ------------------------------------------------------------------ incidence
+__global__ void k_iota_count(const int32_t *conn, int64_t n, int32_t *idx, int64_t *cnt) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    idx[i] = (int32_t)i;
+    atomicAdd(reinterpret_cast<unsigned long long *>(cnt + conn[i]), 1ull);
+  }
+}
+
+// sorted unique neighbour nodes of node n (incl. itself); returns count or -1 on overflow
+__device__ int node_neighbours(const int64_t *inc_ptr, const int32_t *inc, const int32_t *conn,
+                               int nen, int32_t n, int32_t *nb) {
+  int cnt = 0;
+  for (int64_t t = inc_ptr[n]; t < inc_ptr[n + 1]; ++t) {
+    const int64_t e = inc[t] / nen;
+    for (int b = 0; b < nen; ++b) {
+      const int32_t c = conn[e * nen + b];
+      int lo = 0, hi = cnt;
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (nb[mid] < c) lo = mid + 1; else hi = mid;
+      }
+      if (lo < cnt && nb[lo] == c) continue;
+      if (cnt == kMaxNodeAdj) return -1;
+      for (int q = cnt; q > lo; --q) nb[q] = nb[q - 1];
+      nb[lo] = c;
+      ++cnt;
+    }
+  }
+  return cnt;
+}
+
+__global__ void k_nadj_count(const int64_t *inc_ptr, const int32_t *inc, const int32_t *conn,
+                             int nen, int64_t n_nodes, int64_t *cnt, int *err) {
+  int32_t nb[kMaxNodeAdj];
+  for (int64_t n = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; n < n_nodes;
+       n += (int64_t)gridDim.x * blockDim.x) {
+    const int c = node_neighbours(inc_ptr, inc, conn, nen, (int32_t)n, nb);
+    if (c < 0) { atomicOr(err, ERRW_ADJ_OVERFLOW); cnt[n] = 0; }
+    else cnt[n] = c;
+  }
+}
+
+__global__ void k_nadj_fill(const int64_t *inc_ptr, const int32_t *inc, const int32_t *conn,
+                            int nen, int64_t n_nodes, const int64_t *nadj_ptr, int32_t *nadj) {
+  int32_t nb[kMaxNodeAdj];
+  for (int64_t n = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; n < n_nodes;
+       n += (int64_t)gridDim.x * blockDim.x) {
+    const int c = node_neighbours(inc_ptr, inc, conn, nen, (int32_t)n, nb);
+    for (int q = 0; q < c; ++q) nadj[nadj_ptr[n] + q] = nb[q];
+  }
+}
+
+// dof -> constraint lists
+__global__ void k_dmpc_count(const int32_t *s, const int32_t *m, int64_t nc, int32_t *cnt) {
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < nc;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    atomicAdd(cnt + s[k], 1);
+    atomicAdd(cnt + m[k], 1);
+  }
+}
+
+__global__ void k_dmpc_fill(const int32_t *s, const int32_t *m, int64_t nc, const int32_t *ptr,
+                            int32_t *cursor, int32_t *list) {
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < nc;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    list[ptr[s[k]] + atomicAdd(cursor + s[k], 1)] = (int32_t)k;
+    list[ptr[m[k]] + atomicAdd(cursor + m[k], 1)] = (int32_t)k;
+  }
+}
+
+__global__ void k_row_len(const int64_t *nadj_ptr, const int32_t *dmpc_ptr, int64_t n_u,
+                          int64_t N, int dim, int64_t *len) {
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r <= N;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    int64_t l = 0;
+    if (r < n_u) {
+      const int64_t n = r / dim;
+      l = (nadj_ptr[n + 1] - nadj_ptr[n]) * dim;
+      if (dmpc_ptr) l += dmpc_ptr[r + 1] - dmpc_ptr[r];
+    } else if (r < N) {
+      l = 2;
+    }
+    len[r] = l;
+  }
+}
+
+__global__ void k_row_fill(const int64_t *nadj_ptr, const int32_t *nadj, const int32_t *dmpc_ptr,
+                           const int32_t *dmpc, const int32_t *ms, const int32_t *mm, int64_t n_u,
+                           int64_t N, int dim, const int64_t *row_ptr, int32_t *col_idx,
+                           int64_t *diag_pos) {
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < N;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    int64_t p = row_ptr[r];
+    if (r < n_u) {
+      const int64_t n = r / dim;
+      int64_t dpos = -1;
+      for (int64_t t = nadj_ptr[n]; t < nadj_ptr[n + 1]; ++t) {
+        const int32_t nb = nadj[t];
+        if (nb == n) dpos = p + (r % dim);
+        for (int c = 0; c < dim; ++c) col_idx[p++] = nb * dim + c;
+      }
+      diag_pos[r] = dpos;
+      if (dmpc_ptr) {
+        const int32_t lo = dmpc_ptr[r], hi = dmpc_ptr[r + 1];
+        // ascending constraint ids (tiny lists: insertion sort while writing)
+        for (int32_t q = lo; q < hi; ++q) {
+          int32_t k = dmpc[q];
+          int64_t w = p + (q - lo);
+          col_idx[w] = (int32_t)(n_u + k);
+          while (w > p && col_idx[w - 1] > col_idx[w]) {
+            const int32_t t = col_idx[w - 1];
+            col_idx[w - 1] = col_idx[w];
+            col_idx[w] = t;
+            --w;
+          }
+        }
+      }
+    } else {
+      const int64_t k = r - n_u;
+      const int32_t a = ms[k], b = mm[k];
+      col_idx[p] = a < b ? a : b;
+      col_idx[p + 1] = a < b ? b : a;
+      diag_pos[r] = -1;
+    }
+  }
+}
+
+template <typename T>
+static fem_status exclusive_scan(T *in, T *out, int64_t n, Workspace &tmp, cudaStream_t s) {
+  size_t bytes = 0;
+  FEM_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, bytes, in, out, n, s));
+  fem_status st = ensure(tmp, bytes);
+  if (st) return st;
+  FEM_CUDA(cub::DeviceScan::ExclusiveSum(tmp.ptr, bytes, in, out, n, s));
+  return FEM_OK;
+}
+
+static fem_status build_incidence(Problem *p, cudaStream_t s) {
+  const int64_t n = p->n_elems * p->nen;
+  int32_t *idx = nullptr, *keys_out = nullptr;
+  int64_t *cnt = nullptr;
+  FEM_CUDA(cudaMalloc(&p->inc_ptr, sizeof(int64_t) * (p->n_nodes + 1)));
+  FEM_CUDA(cudaMalloc(&p->inc, sizeof(int32_t) * (n > 0 ? n : 1)));
+  FEM_CUDA(cudaMalloc(&cnt, sizeof(int64_t) * (p->n_nodes + 1)));
+  FEM_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int64_t) * (p->n_nodes + 1), s));
+  if (n > 0) {
+    FEM_CUDA(cudaMalloc(&idx, sizeof(int32_t) * n));
+    FEM_CUDA(cudaMalloc(&keys_out, sizeof(int32_t) * n));
+    k_iota_count<<<grid_for(n), kThreads, 0, s>>>(p->conn, n, idx, cnt);
+    int bits = 1;
+    while ((int64_t(1) << bits) < p->n_nodes) ++bits;
+    size_t bytes = 0;
+    FEM_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, p->conn, keys_out, idx, p->inc,
+                                             (int)n, 0, bits, s));
+    fem_status st = ensure(p->tmp, bytes);
+    if (st) return st;
+    FEM_CUDA(cub::DeviceRadixSort::SortPairs(p->tmp.ptr, bytes, p->conn, keys_out, idx, p->inc,
+                                             (int)n, 0, bits, s));
+  }
+  fem_status st = exclusive_scan(cnt, p->inc_ptr, p->n_nodes + 1, p->tmp, s);
+  FEM_CUDA(cudaStreamSynchronize(s));
+  cudaFree(idx);
+  cudaFree(keys_out);
+  cudaFree(cnt);
+  return st;
+}
+
+fem_status build_pattern(Problem *p, cudaStream_t s) {
+  if (p->have_pattern) return FEM_OK;
+  fem_status st = build_incidence(p, s);
+  if (st) return st;
+  // node adjacency
+  int64_t *cnt = nullptr;
+  FEM_CUDA(cudaMalloc(&cnt, sizeof(int64_t) * (p->n_nodes + 1)));
+  FEM_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int64_t) * (p->n_nodes + 1), s));
+  k_nadj_count<<<grid_for(p->n_nodes, 128), 128, 0, s>>>(p->inc_ptr, p->inc, p->conn, p->nen,
+                                                          p->n_nodes, cnt, p->d_err);
+  FEM_CUDA(cudaMalloc(&p->nadj_ptr, sizeof(int64_t) * (p->n_nodes + 1)));
+  st = exclusive_scan(cnt, p->nadj_ptr, p->n_nodes + 1, p->tmp, s);
+  if (st) return st;
+  int64_t total = 0;
+  FEM_CUDA(cudaMemcpyAsync(&total, p->nadj_ptr + p->n_nodes, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+  FEM_CUDA(cudaStreamSynchronize(s));
+  st = read_error_word(p, s);
+  if (st) { cudaFree(cnt); return st; }
+  FEM_CUDA(cudaMalloc(&p->nadj, sizeof(int32_t) * (total > 0 ? total : 1)));
+  k_nadj_fill<<<grid_for(p->n_nodes, 128), 128, 0, s>>>(p->inc_ptr, p->inc, p->conn, p->nen,
+                                                         p->n_nodes, p->nadj_ptr, p->nadj);
+  // dof -> constraint lists
+  if (p->n_mpc) {
+    int32_t *dcnt = nullptr, *cursor = nullptr;
+    FEM_CUDA(cudaMalloc(&dcnt, sizeof(int32_t) * (p->n_u + 1)));
+    FEM_CUDA(cudaMalloc(&cursor, sizeof(int32_t) * (p->n_u + 1)));
+    FEM_CUDA(cudaMemsetAsync(dcnt, 0, sizeof(int32_t) * (p->n_u + 1), s));
+    FEM_CUDA(cudaMemsetAsync(cursor, 0, sizeof(int32_t) * (p->n_u + 1), s));
+    FEM_CUDA(cudaMalloc(&p->dmpc_ptr, sizeof(int32_t) * (p->n_u + 1)));
+    FEM_CUDA(cudaMalloc(&p->dmpc, sizeof(int32_t) * 2 * p->n_mpc));
+    k_dmpc_count<<<grid_for(p->n_mpc), kThreads, 0, s>>>(p->mpc_s, p->mpc_m, p->n_mpc, dcnt);
+    st = exclusive_scan(dcnt, p->dmpc_ptr, p->n_u + 1, p->tmp, s);
+    if (st) return st;
+    k_dmpc_fill<<<grid_for(p->n_mpc), kThreads, 0, s>>>(p->mpc_s, p->mpc_m, p->n_mpc, p->dmpc_ptr,
+                                                        cursor, p->dmpc);
+    FEM_CUDA(cudaStreamSynchronize(s));
+    cudaFree(dcnt);
+    cudaFree(cursor);
+  }
+  // rows
+  int64_t *len = nullptr;
+  FEM_CUDA(cudaMalloc(&len, sizeof(int64_t) * (p->N + 1)));
+  k_row_len<<<grid_for(p->N + 1), kThreads, 0, s>>>(p->nadj_ptr, p->dmpc_ptr, p->n_u, p->N,
+                                                     p->dim, len);
+  FEM_CUDA(cudaMalloc(&p->row_ptr, sizeof(int64_t) * (p->N + 1)));
+  st = exclusive_scan(len, p->row_ptr, p->N + 1, p->tmp, s);
+  if (st) return st;
+  FEM_CUDA(cudaMemcpyAsync(&p->nnz, p->row_ptr + p->N, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+  FEM_CUDA(cudaStreamSynchronize(s));
+  FEM_CUDA(cudaMalloc(&p->col_idx, sizeof(int32_t) * (p->nnz > 0 ? p->nnz : 1)));
+  FEM_CUDA(cudaMalloc(&p->diag_pos, sizeof(int64_t) * (p->N > 0 ? p->N : 1)));
+  k_row_fill<<<grid_for(p->N), kThreads, 0, s>>>(p->nadj_ptr, p->nadj, p->dmpc_ptr, p->dmpc,
+                                                  p->mpc_s, p->mpc_m, p->n_u, p->N, p->dim,
+                                                  p->row_ptr, p->col_idx, p->diag_pos);
+  FEM_LAUNCH_CHECK("pattern fill");
+  FEM_CUDA(cudaStreamSynchronize(s));
+  cudaFree(cnt);
+  cudaFree(len);
+  p->have_pattern = true;
+  return FEM_OK;
+}
+
+// ------------------------------------------------------------------ coloring
+// Number of (r, k) paths with r in adj(j), k in adj(r), k < j (with multiplicity).
+__global__ void k_color_init(const int64_t *gp, const int32_t *gi, int64_t nv, int32_t *cnt,
+                             int32_t *colors, int32_t *frontier, int32_t *fsize) {
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < nv;
+       j += (int64_t)gridDim.x * blockDim.x) {
+    int32_t c = 0;
+    for (int64_t p = gp[j]; p < gp[j + 1]; ++p) {
+      const int32_t r = gi[p];
+      for (int64_t q = gp[r]; q < gp[r + 1]; ++q) c += (gi[q] < j);
+    }
+    cnt[j] = c;
+    colors[j] = -1;
+    if (c == 0) frontier[atomicAdd(fsize, 1)] = (int32_t)j;
+  }
+}
+
+__global__ void __launch_bounds__(128) k_color_round(const int64_t *gp, const int32_t *gi,
+                                                     int32_t *cnt, int32_t *colors,
+                                                     const int32_t *cur, int32_t *next,
+                                                     int32_t *sizes, int t, int32_t *done,
+                                                     int *err, int32_t *max_color) {
+  const int32_t n_cur = sizes[t % 3];
+  if (blockIdx.x == 0 && threadIdx.x == 0) sizes[(t + 2) % 3] = 0;
+  int32_t *nsize = sizes + (t + 1) % 3;
+  for (int32_t w = blockIdx.x * blockDim.x + threadIdx.x; w < n_cur; w += gridDim.x * blockDim.x) {
+    const int32_t j = cur[w];
+    uint32_t fb[FEM_MAX_COLORS / 32];
+#pragma unroll
+    for (int q = 0; q < FEM_MAX_COLORS / 32; ++q) fb[q] = 0u;
+    for (int64_t p = gp[j]; p < gp[j + 1]; ++p) {
+      const int32_t r = gi[p];
+      for (int64_t q = gp[r]; q < gp[r + 1]; ++q) {
+        const int32_t k = gi[q];
+        if (k < j) {
+          const int32_t c = colors[k];
+          fb[c >> 5] |= 1u << (c & 31);
+        }
+      }
+    }
+    int32_t c = -1;
+#pragma unroll
+    for (int q = 0; q < FEM_MAX_COLORS / 32; ++q) {
+      if (c < 0 && fb[q] != 0xffffffffu) c = q * 32 + __ffs(~fb[q]) - 1;
+    }
+    if (c < 0) { atomicOr(err, ERRW_TOO_MANY_COLORS); c = FEM_MAX_COLORS - 1; }
+    colors[j] = c;
+    atomicMax(max_color, c);
+    atomicAdd(done, 1);
+    for (int64_t p = gp[j]; p < gp[j + 1]; ++p) {
+      const int32_t r = gi[p];
+      for (int64_t q = gp[r]; q < gp[r + 1]; ++q) {
+        const int32_t k = gi[q];
+        if (k > j && atomicSub(cnt + k, 1) == 1) next[atomicAdd(nsize, 1)] = k;
+      }
+    }
+  }
+}
+
+__global__ void k_expand_node_colors(const int32_t *nc, int64_t n_nodes, int dim, int32_t *colors) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_nodes * dim;
+       i += (int64_t)gridDim.x * blockDim.x)
+    colors[i] = dim * nc[i / dim] + (int32_t)(i % dim);
+}
+
+// Colors the graph (gp, gi) with nv vertices into `colors`; returns the number of colors.
+static fem_status greedy_color(Problem *p, const int64_t *gp, const int32_t *gi, int64_t nv,
+                               int32_t *colors, int32_t *n_colors, cudaStream_t s) {
+  int32_t *cnt = nullptr, *f0 = nullptr, *f1 = nullptr, *aux = nullptr;
+  FEM_CUDA(cudaMalloc(&cnt, sizeof(int32_t) * (nv > 0 ? nv : 1)));
+  FEM_CUDA(cudaMalloc(&f0, sizeof(int32_t) * (nv > 0 ? nv : 1)));
+  FEM_CUDA(cudaMalloc(&f1, sizeof(int32_t) * (nv > 0 ? nv : 1)));
+  FEM_CUDA(cudaMalloc(&aux, sizeof(int32_t) * 8));  // sizes[3], done, max_color
+  FEM_CUDA(cudaMemsetAsync(aux, 0, sizeof(int32_t) * 8, s));
+  FEM_CUDA(cudaMemsetAsync(aux + 4, 0xff, sizeof(int32_t), s));  // max_color = -1
+  int32_t *sizes = aux, *done = aux + 3, *maxc = aux + 4;
+  k_color_init<<<grid_for(nv), kThreads, 0, s>>>(gp, gi, nv, cnt, colors, f0, sizes);
+  FEM_LAUNCH_CHECK("color init");
+  int32_t h_done = 0;
+  const int kCheck = 32;
+  const int grid = 148 * 4;
+  for (int t = 0; h_done < nv;) {
+    for (int q = 0; q < kCheck; ++q, ++t) {
+      int32_t *cur = (t % 2 == 0) ? f0 : f1, *nxt = (t % 2 == 0) ? f1 : f0;
+      k_color_round<<<grid, 128, 0, s>>>(gp, gi, cnt, colors, cur, nxt, sizes, t, done, p->d_err,
+                                         maxc);
+    }
+    FEM_LAUNCH_CHECK("color round");
+    FEM_CUDA(cudaMemcpyAsync(&h_done, done, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    FEM_CUDA(cudaStreamSynchronize(s));
+    if (t > 64 * (nv + 64)) {
+      set_error("coloring did not terminate");
+      return FEM_ERR_CUDA;
+    }
+  }
+  int32_t hmax = -1;
+  FEM_CUDA(cudaMemcpyAsync(&hmax, maxc, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+  FEM_CUDA(cudaStreamSynchronize(s));
+  cudaFree(cnt);
+  cudaFree(f0);
+  cudaFree(f1);
+  cudaFree(aux);
+  *n_colors = hmax + 1;
+  return read_error_word(p, s);
+}
+
+fem_status build_colors(Problem *p, cudaStream_t s) {
+  if (p->have_colors) return FEM_OK;
+  fem_status st = build_pattern(p, s);
+  if (st) return st;
+  FEM_CUDA(cudaMalloc(&p->colors, sizeof(int32_t) * (p->N > 0 ? p->N : 1)));
+  int32_t nc = 0;
+  if (p->n_mpc == 0) {
+    int32_t *node_colors = nullptr;
+    FEM_CUDA(cudaMalloc(&node_colors, sizeof(int32_t) * p->n_nodes));
+    st = greedy_color(p, p->nadj_ptr, p->nadj, p->n_nodes, node_colors, &nc, s);
+    if (st) { cudaFree(node_colors); return st; }
+    if (nc * p->dim > FEM_MAX_COLORS) {
+      cudaFree(node_colors);
+      set_error("coloring needs more than FEM_MAX_COLORS colors");
+      return FEM_ERR_TOO_MANY_COLORS;
+    }
+    k_expand_node_colors<<<grid_for(p->n_u), kThreads, 0, s>>>(node_colors, p->n_nodes, p->dim,
+                                                                p->colors);
+    FEM_LAUNCH_CHECK("expand colors");
+    FEM_CUDA(cudaStreamSynchronize(s));
+    cudaFree(node_colors);
+    nc *= p->dim;
+  } else {
+    st = greedy_color(p, p->row_ptr, p->col_idx, p->N, p->colors, &nc, s);
+    if (st) return st;
+  }
+  p->n_colors = nc;
+  p->have_colors = true;
+  return FEM_OK;
+}
+
+}  // namespace fem
+
+using namespace fem;
+
+extern "C" {
+
+fem_status fem_sparsity(fem_problem *h, int64_t *row_ptr, int32_t *col_idx, fem_stream stream) {
+  FEM_ARG(h, "fem_sparsity: null problem");
+  Problem *p = &h->p;
+  cudaStream_t s = (cudaStream_t)stream;
+  fem_status st = build_pattern(p, s);
+  if (st) return st;
+  if (row_ptr)
+    FEM_CUDA(cudaMemcpyAsync(row_ptr, p->row_ptr, sizeof(int64_t) * (p->N + 1), cudaMemcpyDeviceToDevice, s));
+  if (col_idx && p->nnz)
+    FEM_CUDA(cudaMemcpyAsync(col_idx, p->col_idx, sizeof(int32_t) * p->nnz, cudaMemcpyDeviceToDevice, s));
+  return FEM_OK;
+}
+
+fem_status fem_color(fem_problem *h, int32_t *colors, int32_t *n_colors, fem_stream stream) {
+  FEM_ARG(h, "fem_color: null problem");
+  Problem *p = &h->p;
+  cudaStream_t s = (cudaStream_t)stream;
+  fem_status st = build_colors(p, s);
+  if (st) return st;
+  if (colors)
+    FEM_CUDA(cudaMemcpyAsync(colors, p->colors, sizeof(int32_t) * p->N, cudaMemcpyDeviceToDevice, s));
+  if (n_colors) *n_colors = p->n_colors;
+  FEM_CUDA(cudaStreamSynchronize(s));
+  return FEM_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,292 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle.
+
+Floating point: normwise relative error <= 1e-12 (north_star; reading C14).
+Pattern and coloring: bit-exact.  Converged Newton displacements: <= 1e-10 relative.
+Small meshes span several 256-thread tiles plus a ragged tail; full BASELINE sizes are
+checked on sampled rows the oracle computes one by one, and by size-independent
+properties (patch tests, closed-form homogeneous solutions).
+"""
+import numpy as np
+import pytest
+
+import fem_inputs as fi
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-12
+
+
+@pytest.fixture(scope="module")
+def fem():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2602_12365_b200 import build, fem as f
+    build.build()
+    return f
+
+
+def rel(a, b):
+    a = a.detach().cpu().numpy() if hasattr(a, "detach") else np.asarray(a)
+    b = np.asarray(b)
+    return float(np.abs(a - b).max() / max(np.abs(b).max(), 1e-300))
+
+
+def dev(x):
+    return torch.as_tensor(np.ascontiguousarray(x), device="cuda")
+
+
+def meshes():
+    out = {
+        "cfg1-2d-le": fi.config_mesh(1),
+        "2d-nh-roller": fi.roller_bc(fi.perturb(fi.grid_tri3(23, 17), 0.2, 3).copy_with(material=1), 0.1),
+        "2d-nh-clamped": fi.clamped_bc(fi.perturb(fi.grid_tri3(19, 20), 0.2, 4).copy_with(material=1), 0.05),
+        "3d-le": fi.roller_bc(fi.perturb(fi.grid_tet4(7, 6, 5), 0.1, 5).copy_with(material=0), 0.05),
+        "3d-nh": fi.roller_bc(fi.perturb(fi.grid_tet4(6, 7, 5), 0.1, 6).copy_with(material=1), 0.05),
+        "2d-le-mpc": fi.config_mesh(5, n=13),
+        "3d-nh-shuffled": fi.renumber_nodes(fi.grid_tet4(5, 4, 6).copy_with(material=1), 21),
+    }
+    ph = fi.two_phase(fi.perturb(fi.grid_tri3(16, 16), 0.2, 8).copy_with(material=1), 0.3,
+                      (0.5, 0.3), (5.0, 3.0))
+    ph = ph.copy_with(f_ext=np.random.default_rng(3).uniform(-1e-3, 1e-3, ph.n_u))
+    out["2d-nh-phases-fext"] = ph
+    return out
+
+
+MESHES = meshes()
+
+
+@pytest.fixture(scope="module", params=sorted(MESHES))
+def case(request, fem, oracle_mod):
+    mesh = MESHES[request.param]
+    prob = fem.Problem(mesh)
+    ref = oracle_mod.Oracle(mesh)
+    z = fi.lift(mesh, fi.generic_state(mesh, 1))
+    v = fi.random_direction(mesh.n_total, 2)
+    return request.param, mesh, prob, ref, z, v
+
+
+def test_energy(case):
+    name, mesh, prob, ref, z, v = case
+    e = prob.energy(dev(z)).item()
+    r = ref.energy(z)
+    assert abs(e - r) <= TOL * abs(r)
+
+
+@pytest.mark.parametrize("bc", [False, True])
+def test_residual(case, bc):
+    name, mesh, prob, ref, z, v = case
+    assert rel(prob.residual(dev(z), bc=bc), ref.residual(z, bc=bc)) <= TOL
+
+
+@pytest.mark.parametrize("bc", [False, True])
+def test_hvp(case, bc):
+    name, mesh, prob, ref, z, v = case
+    assert rel(prob.hvp(dev(z), dev(v), bc=bc), ref.hvp(z, v, bc=bc)) <= TOL
+
+
+def test_pattern_bit_exact(case):
+    name, mesh, prob, ref, z, v = case
+    rp, ci = prob.sparsity()
+    rrp, rci = ref.sparsity()
+    assert np.array_equal(rp.cpu().numpy(), rrp)
+    assert np.array_equal(ci.cpu().numpy(), rci)
+
+
+def test_coloring_bit_exact(case):
+    name, mesh, prob, ref, z, v = case
+    colors, nc = prob.color()
+    rcol, rnc = ref.colors()
+    assert nc == rnc
+    assert np.array_equal(colors.cpu().numpy(), rcol)
+
+
+@pytest.mark.parametrize("mode", ["batched", "literal", "rows"])
+@pytest.mark.parametrize("bc", [False, True])
+def test_assembly(case, mode, bc):
+    name, mesh, prob, ref, z, v = case
+    vals = prob.assemble_csr(dev(z), bc=bc, mode=mode)
+    assert rel(vals, ref.assemble_alg2(z, bc=bc)) <= TOL
+
+
+def test_rows_mode_is_bitwise_reproducible(case):
+    name, mesh, prob, ref, z, v = case
+    a = prob.assemble_csr(dev(z), bc=True, mode="rows").cpu().numpy()
+    b = prob.assemble_csr(dev(z), bc=True, mode="rows").cpu().numpy()
+    assert np.array_equal(a, b)
+
+
+def test_spmv_equals_hvp(case):
+    name, mesh, prob, ref, z, v = case
+    vals = prob.assemble_csr(dev(z), bc=True)
+    y = prob.spmv(vals, dev(v))
+    assert rel(y, ref.hvp(z, v, bc=True)) <= TOL
+    rp, ci = ref.sparsity()
+    import oracle
+    assert rel(y, oracle.spmv(rp, ci, vals.cpu().numpy(), v)) <= TOL
+
+
+def test_cg_matrix_free_and_csr(case):
+    name, mesh, prob, ref, z, v = case
+    if mesh.n_mpc:
+        pytest.skip("saddle-point system: CG does not apply (SURVEY §8(f) f2)")
+    b = v.copy()
+    b[mesh.dirichlet_dofs] = 0.0
+    if len(mesh.dirichlet_dofs) == 0:
+        pytest.skip("singular without Dirichlet conditions")
+    xr, rinfo = ref.cg(b, op=0, z=z, rtol=1e-13)
+    x, info = prob.cg_solve(dev(b), z=dev(z), op=0, rtol=1e-13)
+    assert info["converged"] and rinfo["status"] == 0
+    assert rel(x, xr) <= 1e-10
+    vals = prob.assemble_csr(dev(z), bc=True)
+    x1, info1 = prob.cg_solve(dev(b), vals=vals, op=1, rtol=1e-13)
+    assert info1["converged"] and rel(x1, xr) <= 1e-10
+    x2, info2 = prob.cg_solve(dev(b), vals=vals, op=1, rtol=1e-13, jacobi=True)
+    assert info2["converged"] and rel(x2, xr) <= 1e-10
+
+
+def test_newton(case):
+    name, mesh, prob, ref, z, v = case
+    if mesh.n_mpc or len(mesh.dirichlet_dofs) == 0 or mesh.f_ext is not None:
+        pytest.skip("Newton parity on the roller / clamped problems")
+    z0 = fi.lift(mesh)
+    zr, rinfo = ref.newton(z0, cg_rtol=1e-13)
+    for op in (0, 1):
+        zg, info = prob.newton_solve(dev(z0), op=op, cg_rtol=1e-13)
+        assert info["converged"] and rinfo["status"] == 0
+        assert rel(zg, zr) <= 1e-10
+
+
+# ------------------------------------------------------------------ edge cases
+
+def test_single_element_and_empty(fem, oracle_mod):
+    tri = fi.Mesh(dim=2, coords=np.array([[0., 0.], [1., 0.], [0., 1.]]),
+                  conn=np.array([[0, 1, 2]], np.int32), material=1)
+    p = fem.Problem(tri)
+    z = np.array([0.01, 0.0, 0.02, -0.01, 0.0, 0.03])
+    v = np.arange(6.0)
+    o = oracle_mod.Oracle(tri)
+    assert rel(p.hvp(dev(z), dev(v)), o.hvp(z, v)) <= TOL
+    assert p.color()[1] == 6
+    empty = fi.Mesh(dim=3, coords=np.zeros((4, 3)), conn=np.zeros((0, 4), np.int32))
+    pe = fem.Problem(empty)
+    assert pe.energy(torch.zeros(12, dtype=torch.float64, device="cuda")).item() == 0.0
+    assert pe.nnz() == 0
+
+
+def test_errors(fem):
+    deg = fi.Mesh(dim=2, coords=np.array([[0., 0.], [1., 0.], [2., 0.]]),
+                  conn=np.array([[0, 1, 2]], np.int32))
+    with pytest.raises(fem.FemError) as ei:
+        fem.Problem(deg)
+    assert ei.value.status == 2
+    bad = fi.Mesh(dim=2, coords=np.array([[0., 0.], [1., 0.], [0., 1.]]),
+                  conn=np.array([[0, 1, 5]], np.int32))
+    with pytest.raises(fem.FemError) as ei:
+        fem.Problem(bad)
+    assert ei.value.status == 1
+    tri = fi.Mesh(dim=2, coords=np.array([[0., 0.], [1., 0.], [0., 1.]]),
+                  conn=np.array([[0, 1, 2]], np.int32), material=1)
+    p = fem.Problem(tri)
+    z = dev(np.array([0.0, 0.0, -3.0, 0.0, 0.0, 0.0]))   # folds the element: J < 0
+    p.residual(z)
+    with pytest.raises(fem.FemError) as ei:
+        p.check()
+    assert ei.value.status == 3
+    with pytest.raises(ValueError):
+        p.hvp(z, dev(np.zeros(5)))
+
+
+# ------------------------------------------------------------------ full BASELINE sizes
+
+def sampled_rows(n, k, seed):
+    rows = np.random.default_rng(seed).choice(n, k, replace=False)
+    return np.unique(np.concatenate([rows, [0, n - 1]]))
+
+
+@pytest.mark.parametrize("cfg", [2, 3])
+def test_full_size_sampled_parity(fem, oracle_mod, cfg):
+    mesh = fi.config_mesh(cfg)
+    prob = fem.Problem(mesh)
+    ref = oracle_mod.Oracle(mesh)
+    h = mesh.length / max(mesh.shape)
+    z = fi.lift(mesh, fi.generic_state(mesh, 3, eps=0.05, noise=0.01, h=h))
+    v = fi.random_direction(mesh.n_total, 4)
+    rows = sampled_rows(mesh.n_total, 2000, 5)
+    zt, vt = dev(z), dev(v)
+    for bc in (False, True):
+        r = prob.residual(zt, bc=bc).cpu().numpy()
+        rr = ref.residual_rows(z, rows, bc=bc)
+        assert np.abs(r[rows] - rr).max() <= TOL * np.abs(r).max()
+        y = prob.hvp(zt, vt, bc=bc).cpu().numpy()
+        yr = ref.hvp_rows(z, v, rows, bc=bc)
+        assert np.abs(y[rows] - yr).max() <= TOL * np.abs(y).max()
+    # tangent and residual patch tests at full size (exact on any P1 mesh)
+    dim = mesh.dim
+    F = np.diag([1.05] + [0.98] * (dim - 1))
+    u_hom = fi.affine_field(mesh, F - np.eye(dim))
+    interior = ~fi.boundary_node_mask(mesh)
+    r = prob.residual(dev(u_hom)).cpu().numpy().reshape(-1, dim)
+    assert np.abs(r[interior]).max() <= 1e-12 * np.abs(r).max()
+    w = fi.affine_field(mesh, np.random.default_rng(1).uniform(-1, 1, (dim, dim)))
+    y = prob.hvp(dev(u_hom), dev(w)).cpu().numpy().reshape(-1, dim)
+    assert np.abs(y[interior]).max() <= 1e-12 * np.abs(y).max()
+    # CSR rows, all three modes, vs the oracle's element-Hessian rows
+    rp, ci = prob.sparsity()
+    rp_n, ci_n = rp.cpu().numpy(), ci.cpu().numpy()
+    assert rp_n[-1] == {2: 13973156, 3: 459889659}[cfg]       # SURVEY §8 closed-form nnz
+    colors, nc = prob.color()
+    assert nc == {2: 18, 3: 87}[cfg]
+    srow = sampled_rows(mesh.n_total, 300, 6)
+    ref_vals = ref.csr_rows(z, srow, rp_n, ci_n, bc=True)
+    idx = np.concatenate([np.arange(rp_n[r], rp_n[r + 1]) for r in srow])
+    for mode in ("batched", "rows"):
+        vals = prob.assemble_csr(zt, bc=True, mode=mode).cpu().numpy()
+        assert np.abs(vals[idx] - ref_vals).max() <= TOL * np.abs(vals).max()
+        del vals
+    torch.cuda.empty_cache()
+
+
+def test_full_size_coloring_bit_exact_cfg2(fem, oracle_mod):
+    mesh = fi.config_mesh(2)
+    prob = fem.Problem(mesh)
+    ref = oracle_mod.Oracle(mesh)
+    colors, nc = prob.color()
+    rcol, rnc = ref.colors()
+    assert nc == rnc == 18
+    assert np.array_equal(colors.cpu().numpy(), rcol)
+
+
+def test_full_size_mpc_coloring_bit_exact(fem, oracle_mod):
+    mesh = fi.config_mesh(5, n=223)   # ~1e5 DOFs, DOF-level generic path (multipliers)
+    prob = fem.Problem(mesh)
+    ref = oracle_mod.Oracle(mesh)
+    rp, ci = prob.sparsity()
+    rrp, rci = ref.sparsity()
+    assert np.array_equal(rp.cpu().numpy(), rrp) and np.array_equal(ci.cpu().numpy(), rci)
+    colors, nc = prob.color()
+    rcol, rnc = ref.colors()
+    assert nc == rnc and np.array_equal(colors.cpu().numpy(), rcol)
+    z = fi.generic_state(mesh, 3)
+    assert rel(prob.assemble_csr(dev(z)), ref.assemble_elem(z)) <= TOL
+
+
+def test_full_size_newton_cfg2_closed_form(fem, oracle_mod):
+    # C15: roller stretch eps = 0.1 has the homogeneous solution u = (F - I) X on any mesh,
+    # so the full-size solution must be affine with the oracle's s from a small mesh.
+    small = fi.roller_bc(fi.perturb(fi.grid_tri3(8, 8), 0.2, 11).copy_with(material=1), 0.1)
+    zs, _ = oracle_mod.Oracle(small).newton(fi.lift(small), cg_rtol=1e-13)
+    s_ref = 1.0 + zs.reshape(-1, 2)[:, 1] @ small.coords[:, 1] / (small.coords[:, 1] @ small.coords[:, 1])
+    mesh = fi.config_mesh(2)
+    prob = fem.Problem(mesh)
+    # one load step from the affine predictor u = (eps X, 0) (it satisfies the BCs); the
+    # bare lift would stretch the last element column by eps/h = 70x, where the NH tangent
+    # is indefinite (c1 = mu - lambda ln J < 0) and CG breaks down.
+    z0 = fi.lift(mesh, fi.affine_field(mesh, np.diag([0.1, 0.0])))
+    z, info = prob.newton_solve(dev(z0), op=0, cg_rtol=1e-11, rtol=1e-10, atol=1e-14)
+    assert info["converged"]
+    U = z.cpu().numpy().reshape(-1, 2)
+    s = 1.0 + U[:, 1] @ mesh.coords[:, 1] / (mesh.coords[:, 1] @ mesh.coords[:, 1])
+    ref = fi.affine_field(mesh, np.diag([0.1, s - 1.0]))
+    assert rel(z, ref) <= 1e-10
+    assert abs(s - s_ref) < 1e-10

@@ -69,8 +69,11 @@ enum {
                                CSR = that operator (1 on the D diagonal, 0 elsewhere in D
                                rows/cols), pattern unchanged.                            */
   FEM_DETERMINISTIC = 2u,   /* atomic-free fixed-order scatter (bitwise reproducible)    */
-  FEM_ASSEMBLE_LITERAL = 4u /* fem_assemble_csr: Alg. 2 as written — C sequential colored
+  FEM_ASSEMBLE_LITERAL = 4u,/* fem_assemble_csr: Alg. 2 as written — C sequential colored
                                HVP passes into J_comp [N][C], then decompression.        */
+  FEM_BASELINE_SCATTER = 8u /* residual / HVP: one thread per element with element-level
+                               fp64 atomics instead of the element tiles — the baseline the
+                               tile kernels are measured against.         */
 };
 
 typedef struct {

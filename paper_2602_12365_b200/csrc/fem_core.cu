@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -59,7 +60,8 @@ fem_status read_error_word(Problem *p, cudaStream_t s) {
 }
 
 // ------------------------------------------------------------------ element kernels
-enum { OP_ENERGY = 0, OP_RESIDUAL = 1, OP_HVP = 2 };
+// k_elem: the plain one-thread-per-element form with element-level atomics.  Kept as the
+// baseline the tile kernels (fem_tiles.cu) are measured against (FEM_BASELINE_SCATTER).
 
 struct ElemArgs {
   const double *coords;
@@ -211,9 +213,9 @@ __global__ void k_partial_dot(const double *a, const double *b, int64_t n, doubl
   if (threadIdx.x == 0) partials[blockIdx.x] = scale * t;
 }
 
-__global__ void k_final_sum(const double *partials, int n, double *out) {
+__global__ void k_final_sum(const double *partials, int64_t n, double *out) {
   double acc = 0.0;
-  for (int i = threadIdx.x; i < n; i += blockDim.x) acc += partials[i];
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) acc += partials[i];
   const double t = block_sum<kThreads>(acc);
   if (threadIdx.x == 0) *out = t;
 }
@@ -333,12 +335,20 @@ __global__ void k_validate_dofs(const int32_t *dd, int64_t nd, const int32_t *ms
 }
 
 // ------------------------------------------------------------------ internal runners
+
 fem_status run_residual(Problem *p, const double *z, double *r, unsigned flags, cudaStream_t s) {
-  FEM_CUDA(cudaMemsetAsync(r, 0, sizeof(double) * p->N, s));
-  ElemArgs a = elem_args(p);
-  a.u = z;
-  a.out = r;
-  fem_status st = launch_elem<OP_RESIDUAL, false>(p, a, grid_for(p->n_elems), s);
+  const bool det = flags & FEM_DETERMINISTIC;
+  if (!det || p->n_elems == 0) FEM_CUDA(cudaMemsetAsync(r, 0, sizeof(double) * p->N, s));
+  fem_status st;
+  if (flags & FEM_BASELINE_SCATTER) {
+    ElemArgs a = elem_args(p);
+    a.u = z;
+    a.out = r;
+    st = launch_elem<OP_RESIDUAL, false>(p, a, grid_for(p->n_elems), s);
+  } else {
+    if (det && p->n_mpc) FEM_CUDA(cudaMemsetAsync(r + p->n_u, 0, sizeof(double) * p->n_mpc, s));
+    st = tile_pass(p, OP_RESIDUAL, z, nullptr, r, false, det, nullptr, s);
+  }
   if (st) return st;
   if (p->size > 1) {
     st = halo_add(p, r, s);
@@ -357,15 +367,22 @@ fem_status run_residual(Problem *p, const double *z, double *r, unsigned flags, 
 
 fem_status run_hvp(Problem *p, const double *z, const double *v, double *y, unsigned flags,
                    cudaStream_t s) {
-  FEM_CUDA(cudaMemsetAsync(y, 0, sizeof(double) * p->N, s));
+  const bool det = flags & FEM_DETERMINISTIC;
+  if (!det || p->n_elems == 0) FEM_CUDA(cudaMemsetAsync(y, 0, sizeof(double) * p->N, s));
   const bool bc = (flags & FEM_APPLY_BC) && p->n_dir;
-  ElemArgs a = elem_args(p);
-  a.u = z;
-  a.v = v;
-  a.out = y;
-  a.node_bc = p->node_bc;
-  fem_status st = bc ? launch_elem<OP_HVP, true>(p, a, grid_for(p->n_elems), s)
-                     : launch_elem<OP_HVP, false>(p, a, grid_for(p->n_elems), s);
+  fem_status st;
+  if (flags & FEM_BASELINE_SCATTER) {
+    ElemArgs a = elem_args(p);
+    a.u = z;
+    a.v = v;
+    a.out = y;
+    a.node_bc = p->node_bc;
+    st = bc ? launch_elem<OP_HVP, true>(p, a, grid_for(p->n_elems), s)
+            : launch_elem<OP_HVP, false>(p, a, grid_for(p->n_elems), s);
+  } else {
+    if (det && p->n_mpc) FEM_CUDA(cudaMemsetAsync(y + p->n_u, 0, sizeof(double) * p->n_mpc, s));
+    st = tile_pass(p, OP_HVP, z, v, y, bc, det, nullptr, s);
+  }
   if (st) return st;
   if (p->size > 1) {
     st = halo_add(p, y, s);
@@ -501,6 +518,8 @@ fem_status fem_create(fem_problem **out, const fem_mesh_desc *d, const fem_dist_
     return fail(FEM_ERR_DEGENERATE_ELEMENT);
   }
 #undef FEM_C
+  fem_status tst = build_tiles(p, s);
+  if (tst) return fail(tst);
   *out = h;
   return FEM_OK;
 }
@@ -516,6 +535,7 @@ fem_status fem_destroy(fem_problem *h) {
   for (void *b : bufs)
     if (b) cudaFree(b);
   if (p->h_scal) cudaFreeHost(p->h_scal);
+  free_tiles(p->tiles);
   delete h;
   return FEM_OK;
 }
@@ -549,15 +569,17 @@ fem_status fem_energy(fem_problem *h, const double *z, double *energy, fem_strea
   FEM_ARG(h && z && energy, "fem_energy: null argument");
   Problem *p = &h->p;
   cudaStream_t s = (cudaStream_t)stream;
-  const int g1 = grid_for(p->n_elems, kThreads, kReduceBlocks);
-  ElemArgs a = elem_args(p);
-  a.u = z;
-  a.partials = p->partials;
   int n = 0;
   if (p->n_elems) {
-    fem_status st = launch_elem<OP_ENERGY, false>(p, a, g1, s);
+    fem_status st;
+    {
+      st = build_tiles(p, s);
+      if (st) return st;
+      st = tile_pass(p, OP_ENERGY, z, nullptr, nullptr, false, false, p->tiles.epart, s);
+      k_final_sum<<<1, kThreads, 0, s>>>(p->tiles.epart, p->tiles.n_tiles, p->partials);
+      n = 1;
+    }
     if (st) return st;
-    n = g1;
   }
   if (p->n_mpc) {
     const int g2 = grid_for(p->n_mpc, kThreads, kReduceBlocks);

@@ -19,6 +19,28 @@ enum : int { ERRW_INVERTED = 1, ERRW_TOO_MANY_COLORS = 2, ERRW_NONFINITE = 4, ER
 constexpr int kMaxNodeAdj = 64;     // max distinct node neighbours (incl. self) per node
 constexpr int kReduceBlocks = 1184; // 148 SMs x 8: fixed grid => fixed reduction order
 constexpr int kThreads = 256;
+constexpr int kTile = 256;          // elements per tile (one CTA)
+
+enum { OP_ENERGY = 0, OP_RESIDUAL = 1, OP_HVP = 2 };
+
+// Element tiles (fem_tiles.cu).  maxe = kTile * (dim+1) reserved entries per tile.
+struct TileSet {
+  bool built = false;
+  int64_t n_tiles = 0, n_slots = 0;
+  int maxe = 0, max_U = 0;
+  int32_t *perm = nullptr;       // [E] tile order -> caller element id
+  int32_t *nodes = nullptr;      // [n_tiles][maxe] sorted unique nodes (first U valid)
+  int32_t *U = nullptr;          // [n_tiles]
+  uint16_t *ptr = nullptr;       // [n_tiles][maxe+1] start of each node's incidences
+  uint16_t *inc = nullptr;       // [n_tiles][maxe] packed (element_local << 2 | slot)
+  uint16_t *lconn = nullptr;     // [n_tiles*kTile][4] tile-local node indices
+  uint8_t *interior = nullptr;   // [n_tiles][maxe] all incident elements in the tile
+  uint8_t *phase = nullptr;      // [E] permuted phase ids (if any)
+  int64_t *slot_off = nullptr;   // [n_tiles+1] prefix sum of U (deterministic mode)
+  int32_t *node_slots = nullptr; // [n_slots] slots of each node, tile order
+  int64_t *node_slot_ptr = nullptr; // [n_nodes+1]
+  double *epart = nullptr;       // [n_tiles] energy partials
+};
 
 struct Workspace {
   void *ptr = nullptr;
@@ -66,7 +88,8 @@ struct Problem {
   int32_t n_colors = -1;
   int32_t *colors = nullptr;    // [N]
   // workspaces
-  Workspace jcomp, cgbuf, tmp;
+  Workspace jcomp, cgbuf, tmp, slotbuf;
+  TileSet tiles;
   // multi-GPU
   void *nccl = nullptr;
   int rank = 0, size = 1;
@@ -140,6 +163,11 @@ fem_status run_hvp(Problem *p, const double *z, const double *v, double *y, unsi
                    cudaStream_t s);
 fem_status run_spmv(Problem *p, const double *vals, const double *x, double *y, cudaStream_t s);
 fem_status halo_add(Problem *p, double *y, cudaStream_t s);
+fem_status build_tiles(Problem *p, cudaStream_t s);
+fem_status tile_pass(Problem *p, int op, const double *u, const double *v, double *out, bool mask,
+                     bool det, double *partials, cudaStream_t s);
+void free_tiles(TileSet &T);
+__global__ void k_final_sum(const double *partials, int64_t n, double *out);
 
 }  // namespace fem
 

@@ -1,0 +1,563 @@
+// fem_tiles.cu — element tiles: the B200 form of Alg. 1's element batches.
+//
+// Setup: elements are ordered along a Morton curve of their centroids (cub radix sort) and
+// cut into tiles of kTile = 256 consecutive elements — one CTA each.  Per tile a block
+// radix sort of the tile's (node, element-slot) incidences yields the sorted list of the
+// tile's unique nodes, the tile-local connectivity (uint16 indices into that list) and, per
+// tile node, the list of its in-tile incidences; a node is "interior" when all of its
+// incident elements lie in the tile.
+//
+// Element kernels (energy / residual / HVP): phase 0 stages the tile's nodal coordinates,
+// u and v (masked at Dirichlet DOFs) in shared memory with coalesced loads of runs of
+// consecutive nodes; phase 1 evaluates one element per thread from shared memory and writes
+// its nodal contributions to a shared [slot][comp][element] array; phase 2 sums each tile
+// node's in-tile incidences in a fixed order and writes the result: a plain store for
+// interior nodes, one fp64 RED for nodes shared with other tiles (~1.8 REDs per DOF in 3D
+// instead of 24 element-level atomics).  With FEM_DETERMINISTIC every tile-node sum goes to
+// its own partial slot and a node-gather kernel adds the slots in tile order.
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <vector>
+
+#include "element.cuh"
+#include "fem_internal.cuh"
+
+namespace fem {
+
+// ------------------------------------------------------------------ setup
+__global__ void k_bbox_partial(const double *coords, int64_t n, int dim, double *part) {
+  double lo[3] = {1e300, 1e300, 1e300}, hi[3] = {-1e300, -1e300, -1e300};
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    for (int c = 0; c < dim; ++c) {
+      const double x = coords[i * dim + c];
+      lo[c] = fmin(lo[c], x);
+      hi[c] = fmax(hi[c], x);
+    }
+  __shared__ double s[2][3][kThreads];
+  for (int c = 0; c < 3; ++c) { s[0][c][threadIdx.x] = lo[c]; s[1][c][threadIdx.x] = hi[c]; }
+  __syncthreads();
+  for (int o = kThreads / 2; o > 0; o >>= 1) {
+    if (threadIdx.x < o)
+      for (int c = 0; c < 3; ++c) {
+        s[0][c][threadIdx.x] = fmin(s[0][c][threadIdx.x], s[0][c][threadIdx.x + o]);
+        s[1][c][threadIdx.x] = fmax(s[1][c][threadIdx.x], s[1][c][threadIdx.x + o]);
+      }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0)
+    for (int c = 0; c < 3; ++c) {
+      part[blockIdx.x * 6 + c] = s[0][c][0];
+      part[blockIdx.x * 6 + 3 + c] = s[1][c][0];
+    }
+}
+
+__device__ __forceinline__ uint64_t spread3(uint64_t x) {  // 21 bits -> every 3rd bit
+  x &= 0x1fffff;
+  x = (x | x << 32) & 0x1f00000000ffffull;
+  x = (x | x << 16) & 0x1f0000ff0000ffull;
+  x = (x | x << 8) & 0x100f00f00f00f00full;
+  x = (x | x << 4) & 0x10c30c30c30c30c3ull;
+  x = (x | x << 2) & 0x1249249249249249ull;
+  return x;
+}
+
+__device__ __forceinline__ uint64_t spread2(uint64_t x) {  // 31 bits -> every 2nd bit
+  x &= 0x7fffffffull;
+  x = (x | x << 16) & 0x0000ffff0000ffffull;
+  x = (x | x << 8) & 0x00ff00ff00ff00ffull;
+  x = (x | x << 4) & 0x0f0f0f0f0f0f0f0full;
+  x = (x | x << 2) & 0x3333333333333333ull;
+  x = (x | x << 1) & 0x5555555555555555ull;
+  return x;
+}
+
+template <int D>
+__global__ void k_morton(const double *coords, const int32_t *conn, int64_t E, double3 lo,
+                         double3 scale, uint64_t *keys, int32_t *idx, int32_t *node_cnt) {
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < E;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    double c[3] = {0, 0, 0};
+    for (int a = 0; a < D + 1; ++a) {
+      const int32_t n = conn[e * (D + 1) + a];
+      atomicAdd(node_cnt + n, 1);
+      for (int i = 0; i < D; ++i) c[i] += coords[(int64_t)n * D + i];
+    }
+    const double l[3] = {lo.x, lo.y, lo.z}, s[3] = {scale.x, scale.y, scale.z};
+    uint64_t q[3];
+    for (int i = 0; i < D; ++i) {
+      double t = (c[i] / (D + 1) - l[i]) * s[i];
+      q[i] = (uint64_t)fmax(0.0, t);
+    }
+    keys[e] = (D == 3) ? (spread3(q[0]) | spread3(q[1]) << 1 | spread3(q[2]) << 2)
+                       : (spread2(q[0]) | spread2(q[1]) << 1);
+    idx[e] = (int32_t)e;
+  }
+}
+
+template <int D>
+__global__ void __launch_bounds__(kTile) k_tile_build(const int32_t *conn, const int32_t *perm,
+                                                      int64_t E, const int32_t *node_cnt,
+                                                      TileSet T) {
+  constexpr int ITEMS = D + 1;
+  constexpr int MAXE = kTile * ITEMS;
+  using Sort = cub::BlockRadixSort<int32_t, kTile, ITEMS, uint16_t>;
+  using Scan = cub::BlockScan<int, kTile>;
+  __shared__ union {
+    typename Sort::TempStorage sort;
+    typename Scan::TempStorage scan;
+  } tmp;
+  __shared__ int32_t s_keys[MAXE + 1];
+  __shared__ int s_U, s_valid;
+  const int t = blockIdx.x, tid = threadIdx.x;
+  int32_t keys[ITEMS];
+  uint16_t vals[ITEMS];
+#pragma unroll
+  for (int i = 0; i < ITEMS; ++i) {
+    const int pos = tid * ITEMS + i;
+    const int el = pos / (D + 1), a = pos % (D + 1);
+    const int64_t eg = (int64_t)t * kTile + el;
+    if (eg < E) {
+      keys[i] = conn[(int64_t)perm[eg] * (D + 1) + a];
+      vals[i] = (uint16_t)(el * 4 + a);
+    } else {
+      keys[i] = INT32_MAX;
+      vals[i] = 0xffff;
+    }
+  }
+  Sort(tmp.sort).Sort(keys, vals);
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < ITEMS; ++i) s_keys[tid * ITEMS + i] = keys[i];
+  __syncthreads();
+  int head[ITEMS], nh = 0;
+#pragma unroll
+  for (int i = 0; i < ITEMS; ++i) {
+    const int pos = tid * ITEMS + i;
+    head[i] = keys[i] != INT32_MAX && (pos == 0 || s_keys[pos - 1] != keys[i]);
+    nh += head[i];
+  }
+  int base = 0, total = 0;
+  Scan(tmp.scan).ExclusiveSum(nh, base, total);
+  const int64_t toff = (int64_t)t * MAXE;
+  int rank = base - 1;
+  int valid = 0;
+#pragma unroll
+  for (int i = 0; i < ITEMS; ++i) {
+    const int pos = tid * ITEMS + i;
+    if (keys[i] == INT32_MAX) continue;
+    ++valid;
+    rank += head[i];
+    T.inc[toff + pos] = vals[i];
+    const int el = vals[i] >> 2, a = vals[i] & 3;
+    T.lconn[((int64_t)t * kTile + el) * 4 + a] = (uint16_t)rank;
+    if (head[i]) {
+      T.nodes[toff + rank] = keys[i];
+      T.ptr[(int64_t)t * (MAXE + 1) + rank] = (uint16_t)pos;
+    }
+  }
+  if (tid == 0) s_valid = 0;
+  __syncthreads();
+  atomicAdd(&s_valid, valid);
+  if (tid == 0) s_U = total;
+  __syncthreads();
+  if (tid == 0) {
+    T.U[t] = total;
+    T.ptr[(int64_t)t * (MAXE + 1) + total] = (uint16_t)s_valid;
+  }
+  __syncthreads();
+  for (int r = tid; r < s_U; r += kTile) {
+    const int lo = T.ptr[(int64_t)t * (MAXE + 1) + r];
+    const int hi = (r + 1 < s_U) ? T.ptr[(int64_t)t * (MAXE + 1) + r + 1] : s_valid;
+    T.interior[toff + r] = (hi - lo) == node_cnt[T.nodes[toff + r]];
+  }
+  if (D == 2) {  // pad slot 3 of the tile-local connectivity
+    const int64_t e = (int64_t)t * kTile + tid;
+    T.lconn[e * 4 + 3] = 0;
+  }
+}
+
+__global__ void k_permute_u8(const uint8_t *src, const int32_t *perm, int64_t n, uint8_t *dst) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    dst[i] = src[perm[i]];
+}
+
+__global__ void k_histogram64(const int32_t *keys, int64_t n, int64_t *cnt) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    atomicAdd(reinterpret_cast<unsigned long long *>(cnt + keys[i]), 1ull);
+}
+
+// deterministic mode: node -> partial slots (tile order)
+__global__ void k_slot_pairs(TileSet T, int64_t n_tiles, const int64_t *slot_off, int32_t *key,
+                             int32_t *val) {
+  for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+    const int U = T.U[t];
+    for (int r = threadIdx.x; r < U; r += blockDim.x) {
+      key[slot_off[t] + r] = T.nodes[t * T.maxe + r];
+      val[slot_off[t] + r] = (int32_t)(slot_off[t] + r);
+    }
+  }
+}
+
+fem_status build_tiles(Problem *p, cudaStream_t s) {
+  TileSet &T = p->tiles;
+  if (T.built || p->n_elems == 0) return FEM_OK;
+  const int D = p->dim;
+  const int64_t E = p->n_elems;
+  const int maxe = kTile * (D + 1);
+  T.maxe = maxe;
+  T.n_tiles = (E + kTile - 1) / kTile;
+  // bounding box
+  const int nb = grid_for(p->n_nodes, kThreads, 256);
+  double *part = nullptr;
+  FEM_CUDA(cudaMalloc(&part, sizeof(double) * nb * 6));
+  k_bbox_partial<<<nb, kThreads, 0, s>>>(p->coords, p->n_nodes, D, part);
+  std::vector<double> hp(nb * 6);
+  FEM_CUDA(cudaMemcpyAsync(hp.data(), part, sizeof(double) * nb * 6, cudaMemcpyDeviceToHost, s));
+  FEM_CUDA(cudaStreamSynchronize(s));
+  cudaFree(part);
+  double lo[3] = {1e300, 1e300, 1e300}, hi[3] = {-1e300, -1e300, -1e300};
+  for (int b = 0; b < nb; ++b)
+    for (int c = 0; c < 3; ++c) {
+      lo[c] = std::min(lo[c], hp[b * 6 + c]);
+      hi[c] = std::max(hi[c], hp[b * 6 + 3 + c]);
+    }
+  const double qmax = (D == 3) ? double((1 << 21) - 1) : double((1u << 31) - 1);
+  double sc[3];
+  for (int c = 0; c < 3; ++c) sc[c] = (c < D && hi[c] > lo[c]) ? qmax / (hi[c] - lo[c]) : 0.0;
+  // Morton keys + stable sort
+  uint64_t *keys = nullptr, *keys_out = nullptr;
+  int32_t *idx = nullptr, *node_cnt = nullptr;
+  FEM_CUDA(cudaMalloc(&keys, sizeof(uint64_t) * E));
+  FEM_CUDA(cudaMalloc(&keys_out, sizeof(uint64_t) * E));
+  FEM_CUDA(cudaMalloc(&idx, sizeof(int32_t) * E));
+  FEM_CUDA(cudaMalloc(&node_cnt, sizeof(int32_t) * p->n_nodes));
+  FEM_CUDA(cudaMalloc(&T.perm, sizeof(int32_t) * E));
+  FEM_CUDA(cudaMemsetAsync(node_cnt, 0, sizeof(int32_t) * p->n_nodes, s));
+  const double3 dlo = make_double3(lo[0], lo[1], lo[2]);
+  const double3 dsc = make_double3(sc[0], sc[1], sc[2]);
+  if (D == 3) k_morton<3><<<grid_for(E), kThreads, 0, s>>>(p->coords, p->conn, E, dlo, dsc, keys, idx, node_cnt);
+  else k_morton<2><<<grid_for(E), kThreads, 0, s>>>(p->coords, p->conn, E, dlo, dsc, keys, idx, node_cnt);
+  FEM_LAUNCH_CHECK("morton");
+  size_t bytes = 0;
+  FEM_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, keys, keys_out, idx, T.perm, (int)E, 0,
+                                           64, s));
+  fem_status st = ensure(p->tmp, bytes);
+  if (st) return st;
+  FEM_CUDA(cub::DeviceRadixSort::SortPairs(p->tmp.ptr, bytes, keys, keys_out, idx, T.perm, (int)E,
+                                           0, 64, s));
+  // tiles
+  const int64_t nt = T.n_tiles;
+  FEM_CUDA(cudaMalloc(&T.nodes, sizeof(int32_t) * nt * maxe));
+  FEM_CUDA(cudaMalloc(&T.U, sizeof(int32_t) * nt));
+  FEM_CUDA(cudaMalloc(&T.ptr, sizeof(uint16_t) * nt * (maxe + 1)));
+  FEM_CUDA(cudaMalloc(&T.inc, sizeof(uint16_t) * nt * maxe));
+  FEM_CUDA(cudaMalloc(&T.lconn, sizeof(uint16_t) * nt * kTile * 4));
+  FEM_CUDA(cudaMalloc(&T.interior, sizeof(uint8_t) * nt * maxe));
+  FEM_CUDA(cudaMemsetAsync(T.lconn, 0, sizeof(uint16_t) * nt * kTile * 4, s));
+  if (D == 3) k_tile_build<3><<<(unsigned)nt, kTile, 0, s>>>(p->conn, T.perm, E, node_cnt, T);
+  else k_tile_build<2><<<(unsigned)nt, kTile, 0, s>>>(p->conn, T.perm, E, node_cnt, T);
+  FEM_LAUNCH_CHECK("tile build");
+  if (p->phase) {
+    FEM_CUDA(cudaMalloc(&T.phase, E));
+    k_permute_u8<<<grid_for(E), kThreads, 0, s>>>(p->phase, T.perm, E, T.phase);
+  }
+  // max U (smem sizing) and slot offsets for the deterministic mode
+  std::vector<int32_t> hU(nt);
+  FEM_CUDA(cudaMemcpyAsync(hU.data(), T.U, sizeof(int32_t) * nt, cudaMemcpyDeviceToHost, s));
+  FEM_CUDA(cudaStreamSynchronize(s));
+  T.max_U = 0;
+  std::vector<int64_t> off(nt + 1, 0);
+  for (int64_t t = 0; t < nt; ++t) {
+    T.max_U = std::max(T.max_U, hU[t]);
+    off[t + 1] = off[t] + hU[t];
+  }
+  T.n_slots = off[nt];
+  FEM_CUDA(cudaMalloc(&T.slot_off, sizeof(int64_t) * (nt + 1)));
+  FEM_CUDA(cudaMemcpyAsync(T.slot_off, off.data(), sizeof(int64_t) * (nt + 1), cudaMemcpyHostToDevice, s));
+  // node -> slots CSR (stable by tile order)
+  {
+    int32_t *k_in = nullptr, *v_in = nullptr, *k_out = nullptr;
+    FEM_CUDA(cudaMalloc(&k_in, sizeof(int32_t) * T.n_slots));
+    FEM_CUDA(cudaMalloc(&v_in, sizeof(int32_t) * T.n_slots));
+    FEM_CUDA(cudaMalloc(&k_out, sizeof(int32_t) * T.n_slots));
+    FEM_CUDA(cudaMalloc(&T.node_slots, sizeof(int32_t) * T.n_slots));
+    FEM_CUDA(cudaMalloc(&T.node_slot_ptr, sizeof(int64_t) * (p->n_nodes + 1)));
+    k_slot_pairs<<<grid_for(nt * 64, 64, 148 * 64), 64, 0, s>>>(T, nt, T.slot_off, k_in, v_in);
+    int bits = 1;
+    while ((int64_t(1) << bits) < p->n_nodes) ++bits;
+    size_t b2 = 0;
+    FEM_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, b2, k_in, k_out, v_in, T.node_slots,
+                                             (int)T.n_slots, 0, bits, s));
+    st = ensure(p->tmp, b2);
+    if (st) return st;
+    FEM_CUDA(cub::DeviceRadixSort::SortPairs(p->tmp.ptr, b2, k_in, k_out, v_in, T.node_slots,
+                                             (int)T.n_slots, 0, bits, s));
+    // node_cnt of slots via histogram of k_out -> exclusive scan
+    int64_t *c64 = nullptr;
+    FEM_CUDA(cudaMalloc(&c64, sizeof(int64_t) * (p->n_nodes + 1)));
+    FEM_CUDA(cudaMemsetAsync(c64, 0, sizeof(int64_t) * (p->n_nodes + 1), s));
+    k_histogram64<<<grid_for(T.n_slots), kThreads, 0, s>>>(k_out, T.n_slots, c64);
+    size_t b3 = 0;
+    FEM_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, b3, c64, T.node_slot_ptr, p->n_nodes + 1, s));
+    st = ensure(p->tmp, b3);
+    if (st) return st;
+    FEM_CUDA(cub::DeviceScan::ExclusiveSum(p->tmp.ptr, b3, c64, T.node_slot_ptr, p->n_nodes + 1, s));
+    FEM_CUDA(cudaStreamSynchronize(s));
+    cudaFree(k_in); cudaFree(v_in); cudaFree(k_out); cudaFree(c64);
+  }
+  FEM_CUDA(cudaStreamSynchronize(s));
+  cudaFree(keys); cudaFree(keys_out); cudaFree(idx); cudaFree(node_cnt);
+  FEM_CUDA(cudaMalloc(&T.epart, sizeof(double) * nt));
+  T.built = true;
+  return FEM_OK;
+}
+
+// ------------------------------------------------------------------ tile element kernels
+struct TileArgs {
+  TileSet T;
+  const double *coords;
+  int64_t E;
+  double lam, mu;
+  const double *lam_tab, *mu_tab;
+  const uint8_t *node_bc;  // non-null: mask v (HVP with FEM_APPLY_BC)
+  const double *u, *v;
+  double *out;             // residual / HVP output (zeroed by the caller unless DET)
+  double *slots;           // DET: [n_slots][D] partial sums
+  double *partials;        // energy: one partial per tile
+  int *err;
+};
+
+template <int D, int MAT, int OP, bool MASK, bool DET>
+__global__ void __launch_bounds__(kTile, 3) k_tile_elem(TileArgs A) {
+  extern __shared__ double sm[];
+  const int t = blockIdx.x, tid = threadIdx.x;
+  const int U = A.T.U[t];
+  const int64_t toff = (int64_t)t * A.T.maxe;
+  const int32_t *tn = A.T.nodes + toff;
+  constexpr bool NEED_U = (OP != OP_HVP) || (MAT == FEM_NEO_HOOKEAN);
+  double *xs = sm;
+  double *us = xs + U * D;
+  double *vs = us + (NEED_U ? U * D : 0);
+  double *contrib = vs + (OP == OP_HVP ? U * D : 0);  // [(D+1)*D][kTile]
+  // phase 0: stage nodal data
+  for (int i = tid; i < U * D; i += kTile) {
+    const int32_t n = __ldg(tn + i / D);
+    const int c = i % D;
+    const int64_t g = (int64_t)n * D + c;
+    xs[i] = __ldg(A.coords + g);
+    if constexpr (NEED_U) us[i] = __ldg(A.u + g);
+    if constexpr (OP == OP_HVP) {
+      double vv = __ldg(A.v + g);
+      if constexpr (MASK) {
+        if (__ldg(A.node_bc + n) & (1u << c)) vv = 0.0;
+      }
+      vs[i] = vv;
+    }
+  }
+  __syncthreads();
+  // phase 1: one element per thread
+  const int64_t e = (int64_t)t * kTile + tid;
+  double acc = 0.0;
+  if (e < A.E) {
+    const ushort4 lc4 = __ldg(reinterpret_cast<const ushort4 *>(A.T.lconn) + e);
+    const int lc[4] = {lc4.x, lc4.y, lc4.z, lc4.w};
+    double x[D + 1][D], G[D + 1][D], vol;
+#pragma unroll
+    for (int a = 0; a < D + 1; ++a)
+#pragma unroll
+      for (int i = 0; i < D; ++i) x[a][i] = xs[lc[a] * D + i];
+    geometry<D>(x, G, vol);
+    double lam = A.lam, mu = A.mu;
+    if (A.T.phase) {
+      const int ph = A.T.phase[e];
+      lam = A.lam_tab[ph];
+      mu = A.mu_tab[ph];
+    }
+    double H[D][D];
+    if constexpr (NEED_U) {
+      double u[D + 1][D];
+#pragma unroll
+      for (int a = 0; a < D + 1; ++a)
+#pragma unroll
+        for (int i = 0; i < D; ++i) u[a][i] = us[lc[a] * D + i];
+      field_gradient<D>(u, G, H);
+    }
+    bool ok = true;
+    double S[D][D];
+    if constexpr (OP == OP_ENERGY) {
+      if constexpr (MAT == FEM_LINEAR_ELASTIC) {
+        acc = vol * le_psi<D>(H, lam, mu);
+      } else {
+        NHState<D> s;
+        ok = nh_state<D>(H, s);
+        if (ok) acc = vol * nh_psi<D>(H, s, lam, mu);
+      }
+    } else if constexpr (OP == OP_RESIDUAL) {
+      if constexpr (MAT == FEM_LINEAR_ELASTIC) {
+        le_stress<D>(H, lam, mu, S);
+      } else {
+        NHState<D> s;
+        ok = nh_state<D>(H, s);
+        if (ok) nh_stress<D>(s, lam, mu, S);
+      }
+    } else {
+      double v[D + 1][D], dH[D][D];
+#pragma unroll
+      for (int a = 0; a < D + 1; ++a)
+#pragma unroll
+        for (int i = 0; i < D; ++i) v[a][i] = vs[lc[a] * D + i];
+      field_gradient<D>(v, G, dH);
+      if constexpr (MAT == FEM_LINEAR_ELASTIC) {
+        le_stress<D>(dH, lam, mu, S);
+      } else {
+        NHState<D> s;
+        ok = nh_state<D>(H, s);
+        if (ok) nh_dstress<D>(s, lam, mu, dH, S);
+      }
+    }
+    if (!ok) {
+      atomicOr(A.err, ERRW_INVERTED);
+      acc = 0.0;
+    }
+    if constexpr (OP != OP_ENERGY) {
+      double f[D + 1][D];
+      nodal_from_stress<D>(S, G, vol, f);
+#pragma unroll
+      for (int a = 0; a < D + 1; ++a)
+#pragma unroll
+        for (int i = 0; i < D; ++i) contrib[(a * D + i) * kTile + tid] = ok ? f[a][i] : 0.0;
+    }
+  }
+  if constexpr (OP == OP_ENERGY) {
+    const double tsum = block_sum<kTile>(acc);
+    if (tid == 0) A.partials[t] = tsum;
+    return;
+  } else {
+    __syncthreads();
+    // phase 2: per tile node, fixed-order sum of its in-tile incidences
+    const uint16_t *ptr = A.T.ptr + (int64_t)t * (A.T.maxe + 1);
+    const uint16_t *inc = A.T.inc + toff;
+    for (int r = tid; r < U; r += kTile) {
+      const int lo = ptr[r], hi = ptr[r + 1];
+      double sacc[D];
+#pragma unroll
+      for (int c = 0; c < D; ++c) sacc[c] = 0.0;
+      for (int q = lo; q < hi; ++q) {
+        const int pk = inc[q];
+        const int el = pk >> 2, a = pk & 3;
+#pragma unroll
+        for (int c = 0; c < D; ++c) sacc[c] += contrib[(a * D + c) * kTile + el];
+      }
+      if constexpr (DET) {
+        double *slot = A.slots + (A.T.slot_off[t] + r) * D;
+#pragma unroll
+        for (int c = 0; c < D; ++c) slot[c] = sacc[c];
+      } else {
+        const int64_t g = (int64_t)tn[r] * D;
+        if (A.T.interior[toff + r]) {
+#pragma unroll
+          for (int c = 0; c < D; ++c) A.out[g + c] = sacc[c];
+        } else {
+#pragma unroll
+          for (int c = 0; c < D; ++c) atomicAdd(A.out + g + c, sacc[c]);
+        }
+      }
+    }
+  }
+}
+
+// DET: y[node] = sum of its tile slots in tile order
+template <int D>
+__global__ void k_slot_gather(const int64_t *node_slot_ptr, const int32_t *node_slots,
+                              const double *slots, int64_t n_nodes, double *out) {
+  for (int64_t n = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; n < n_nodes;
+       n += (int64_t)gridDim.x * blockDim.x) {
+    double s[D];
+#pragma unroll
+    for (int c = 0; c < D; ++c) s[c] = 0.0;
+    for (int64_t q = node_slot_ptr[n]; q < node_slot_ptr[n + 1]; ++q) {
+      const int64_t sl = node_slots[q];
+#pragma unroll
+      for (int c = 0; c < D; ++c) s[c] += slots[sl * D + c];
+    }
+#pragma unroll
+    for (int c = 0; c < D; ++c) out[n * D + c] = s[c];
+  }
+}
+
+template <int D, int MAT, int OP, bool MASK, bool DET>
+static fem_status launch_tile_t(Problem *p, const TileArgs &a, cudaStream_t s) {
+  const int U = p->tiles.max_U;
+  const bool need_u = (OP != OP_HVP) || (MAT == FEM_NEO_HOOKEAN);
+  size_t smem = sizeof(double) * ((size_t)U * D * (1 + (need_u ? 1 : 0) + (OP == OP_HVP ? 1 : 0)) +
+                                  (OP == OP_ENERGY ? 0 : (size_t)(D + 1) * D * kTile));
+  auto kern = k_tile_elem<D, MAT, OP, MASK, DET>;
+  if (smem > 48 * 1024) FEM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  kern<<<(unsigned)p->tiles.n_tiles, kTile, smem, s>>>(a);
+  FEM_LAUNCH_CHECK("tile element kernel");
+  return FEM_OK;
+}
+
+template <int OP, bool MASK, bool DET>
+static fem_status launch_tile_op(Problem *p, const TileArgs &a, cudaStream_t s) {
+  if (p->dim == 2) {
+    if (p->material == FEM_LINEAR_ELASTIC) return launch_tile_t<2, FEM_LINEAR_ELASTIC, OP, MASK, DET>(p, a, s);
+    return launch_tile_t<2, FEM_NEO_HOOKEAN, OP, MASK, DET>(p, a, s);
+  }
+  if (p->material == FEM_LINEAR_ELASTIC) return launch_tile_t<3, FEM_LINEAR_ELASTIC, OP, MASK, DET>(p, a, s);
+  return launch_tile_t<3, FEM_NEO_HOOKEAN, OP, MASK, DET>(p, a, s);
+}
+
+// Element pass of the residual / HVP (op = OP_RESIDUAL / OP_HVP) or the energy partials
+// (OP_ENERGY, one per tile into p->partials-compatible buffer `partials`).
+fem_status tile_pass(Problem *p, int op, const double *u, const double *v, double *out,
+                     bool mask, bool det, double *partials, cudaStream_t s) {
+  fem_status st = build_tiles(p, s);
+  if (st) return st;
+  if (p->n_elems == 0) return FEM_OK;
+  TileArgs a{};
+  a.T = p->tiles;
+  a.coords = p->coords;
+  a.E = p->n_elems;
+  a.lam = p->lam;
+  a.mu = p->mu;
+  a.lam_tab = p->lam_tab;
+  a.mu_tab = p->mu_tab;
+  a.node_bc = p->node_bc;
+  a.u = u;
+  a.v = v;
+  a.out = out;
+  a.partials = partials;
+  a.err = p->d_err;
+  if (op == OP_ENERGY) return launch_tile_op<OP_ENERGY, false, false>(p, a, s);
+  if (det) {
+    st = ensure(p->slotbuf, sizeof(double) * p->tiles.n_slots * p->dim);
+    if (st) return st;
+    a.slots = (double *)p->slotbuf.ptr;
+    if (op == OP_RESIDUAL) st = launch_tile_op<OP_RESIDUAL, false, true>(p, a, s);
+    else st = mask ? launch_tile_op<OP_HVP, true, true>(p, a, s) : launch_tile_op<OP_HVP, false, true>(p, a, s);
+    if (st) return st;
+    if (p->dim == 2)
+      k_slot_gather<2><<<grid_for(p->n_nodes), kThreads, 0, s>>>(p->tiles.node_slot_ptr, p->tiles.node_slots, a.slots, p->n_nodes, out);
+    else
+      k_slot_gather<3><<<grid_for(p->n_nodes), kThreads, 0, s>>>(p->tiles.node_slot_ptr, p->tiles.node_slots, a.slots, p->n_nodes, out);
+    FEM_LAUNCH_CHECK("slot gather");
+    return FEM_OK;
+  }
+  if (op == OP_RESIDUAL) return launch_tile_op<OP_RESIDUAL, false, false>(p, a, s);
+  return mask ? launch_tile_op<OP_HVP, true, false>(p, a, s) : launch_tile_op<OP_HVP, false, false>(p, a, s);
+}
+
+void free_tiles(TileSet &T) {
+  void *bufs[] = {T.perm, T.nodes, T.U, T.ptr, T.inc, T.lconn, T.interior, T.phase, T.slot_off,
+                  T.node_slots, T.node_slot_ptr, T.epart};
+  for (void *b : bufs)
+    if (b) cudaFree(b);
+  T = TileSet{};
+}
+
+}  // namespace fem

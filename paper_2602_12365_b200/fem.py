@@ -24,6 +24,7 @@ LIB_PATH = os.path.join(_HERE, "libfem.so")
 APPLY_BC = 1
 DETERMINISTIC = 2
 ASSEMBLE_LITERAL = 4
+BASELINE_SCATTER = 8
 STATUS = {0: "OK", 1: "INVALID_ARG", 2: "DEGENERATE_ELEMENT", 3: "INVERTED_ELEMENT",
           4: "NONFINITE", 5: "CG_BREAKDOWN", 6: "NOT_CONVERGED", 7: "TOO_MANY_COLORS",
           8: "OUT_OF_MEMORY", 9: "CUDA", 10: "NCCL"}

@@ -18,7 +18,7 @@ if [[ $MODE == all || $MODE == ncu ]]; then
   timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
      --log-file gpurun_out/launches.csv python bench.py --profile-step > gpurun_out/ncu_list.log 2>&1
   timeout 1200 ncu --set full --clock-control none --import-source on \
-     -k regex:'k_elem|k_colored_hvp|k_decompress|k_spmv|k_rows_gather' -c 6 \
+     -k regex:"${NCU_KERNELS:-k_tile_elem|k_colored_hvp|k_decompress|k_spmv|k_rows_gather}" -c ${NCU_COUNT:-6} \
      -o gpurun_out/prof_full -f python bench.py --profile-step > gpurun_out/ncu_full.log 2>&1
   tail -3 gpurun_out/ncu_full.log
 fi

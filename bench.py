@@ -42,7 +42,7 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", type=int, default=3, choices=[2, 3, 5])
     ap.add_argument("--n", type=int, default=None, help="override the mesh size (cells per side)")
-    ap.add_argument("--assemble-mode", default="batched", choices=["batched", "literal", "rows"])
+    ap.add_argument("--assemble-mode", default="rows", choices=["batched", "literal", "rows"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-solve", action="store_true")
     ap.add_argument("--profile-step", action="store_true", help="one step only (for ncu)")

@@ -71,9 +71,16 @@ enum {
   FEM_DETERMINISTIC = 2u,   /* atomic-free fixed-order scatter (bitwise reproducible)    */
   FEM_ASSEMBLE_LITERAL = 4u,/* fem_assemble_csr: Alg. 2 as written — C sequential colored
                                HVP passes into J_comp [N][C], then decompression.        */
-  FEM_BASELINE_SCATTER = 8u /* residual / HVP: one thread per element with element-level
+  FEM_BASELINE_SCATTER = 8u,/* residual / HVP: one thread per element with element-level
                                fp64 atomics instead of the element tiles — the baseline the
                                tile kernels are measured against.         */
+  FEM_LOCAL_ONLY = 16u,     /* residual / HVP on a rank of a multi-GPU problem: skip the
+                               halo add and return this rank's partial sums (DOF-wise
+                               terms — f_ext, Dirichlet rows — on owned DOFs only, zero
+                               elsewhere), so fem_halo_pack + exchange + fem_halo_combine
+                               yields the global result.                                 */
+  FEM_ASSEMBLE_JCOMP = 32u  /* fem_assemble_csr: all color passes in ONE element sweep
+                               into J_comp [N][C] (atomics), then decompression.         */
 };
 
 typedef struct {
@@ -162,12 +169,14 @@ fem_status fem_color(fem_problem *p, int32_t *colors, int32_t *n_colors, fem_str
 /* vals [nnz] in fem_sparsity order = the sparse tangent at z by Alg. 2:
  * for each color c the HVP along the implicit seed e_c (e_j = [color_j == c]) gives
  * J_comp[:, c]; K_ij = J_comp[i, color_j] (decompression).  Modes (flags):
- *   FEM_ASSEMBLE_LITERAL: C sequential per-color passes (the paper's lax.scan);
- *   default: all color passes in ONE element sweep (the passes are independent,
- *            P:186), accumulating J_comp [N][C] with atomics, then decompression;
- *   FEM_DETERMINISTIC: J_comp computed row by row (pull form: row i gathers the colored
- *            seeds' responses of its incident elements) and decompressed in-register
- *            straight into the CSR slots — atomic-free, bitwise reproducible.
+ *   FEM_ASSEMBLE_LITERAL: C sequential per-color passes into J_comp [N][C] (the paper's
+ *            lax.scan), then a decompression kernel;
+ *   FEM_ASSEMBLE_JCOMP: all color passes in ONE element sweep (the passes are
+ *            independent), accumulating J_comp with atomics, then decompression;
+ *   default: J_comp computed row by row (pull form: row i sums the colored seeds'
+ *            responses of its incident elements, a warp per node) with each compressed
+ *            entry stored at its decompressed CSR slot (within a row every color names
+ *            one column) — no J_comp buffer, atomic-free, bitwise reproducible.
  * flags may add FEM_APPLY_BC.  Requires fem_color (the pattern and colors). */
 fem_status fem_assemble_csr(fem_problem *p, const double *z, double *vals, unsigned flags,
                             fem_stream stream);
@@ -220,6 +229,16 @@ fem_status fem_nccl_comm_destroy(void *comm);
 /* (host) n = 1 / 2 scalar all-reduce (sum) of a device buffer over the problem's ranks
  * (no-op on a single GPU); used for global dots in multi-GPU CG and the energy. */
 fem_status fem_allreduce_sum(fem_problem *p, double *buf, int n, fem_stream stream);
+
+/* Halo add in explicit steps (what fem_residual / fem_hvp / fem_spmv do internally with
+ * NCCL on a multi-GPU problem; exposed so the exchange can be driven by another transport).
+ * Buffers hold, per neighbour in ascending rank order, the shared nodes' dim values in
+ * ascending global id (fem_dist_desc.nbr_offset segments); n_doubles = entries * dim.
+ * combine: y[n] = sum over the ranks touching n in ascending rank order of their partials
+ * (own y[n] or recvbuf), so every rank holds identical bits. */
+fem_status fem_halo_size(const fem_problem *p, int64_t *n_doubles);
+fem_status fem_halo_pack(fem_problem *p, const double *y, double *sendbuf, fem_stream stream);
+fem_status fem_halo_combine(fem_problem *p, double *y, const double *recvbuf, fem_stream stream);
 
 const char *fem_last_error(void);
 const char *fem_version(void);

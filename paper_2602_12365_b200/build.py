@@ -20,10 +20,22 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 
+def _nccl_dirs():
+    """The NCCL torch loads (nvidia-nccl wheel), so one libnccl is in the process."""
+    import importlib.util
+    spec = importlib.util.find_spec("nvidia")
+    for base in (list(spec.submodule_search_locations) if spec else []):
+        inc, lib = os.path.join(base, "nccl", "include"), os.path.join(base, "nccl", "lib")
+        if os.path.exists(os.path.join(inc, "nccl.h")):
+            return inc, lib
+    return "/usr/include", "/usr/lib/x86_64-linux-gnu"
+
+
 def _flags():
     return ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2",
                    "--expt-relaxed-constexpr", "-I" + os.path.join(ROOT, "include"),
-                   "-Xptxas", "-warn-spills"]
+                   "-Xptxas", "-warn-spills", "-I" + _nccl_dirs()[0]] + \
+        os.environ.get("FEM_NVCC_FLAGS", "").split()
 
 
 def _needs_build(srcs, deps):
@@ -53,7 +65,10 @@ def build(force: bool = False, verbose: bool = False) -> str:
     with cf.ThreadPoolExecutor(max_workers=min(8, len(srcs))) as ex:
         objs = list(ex.map(compile_one, srcs))
     tmp = SO + ".tmp"
-    cmd = [NVCC] + ARCH + ["-shared", "-o", tmp] + objs + ["-lcudart_static"]
+    inc, lib = _nccl_dirs()
+    nccl = (["-L" + lib, "-Xlinker", "-l:libnccl.so.2"] if os.path.exists(os.path.join(lib, "libnccl.so.2")) else ["-lnccl"])
+    cmd = [NVCC] + ARCH + ["-shared", "-o", tmp] + objs + nccl + ["-lcudart_static",
+                                                                    "-Xlinker", "-rpath=" + lib]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")

@@ -80,6 +80,23 @@ __device__ __forceinline__ void column_block(const ColumnCtx<D> &c, int a, int b
   }
 }
 
+// Same, with row node a's gradients passed in registers (runtime a).
+template <int D>
+__device__ __forceinline__ void column_block_row(const ColumnCtx<D> &c, const double (&Ga)[D],
+                                                 const double (&ga)[D], int b, int k,
+                                                 double (&out)[D]) {
+  double GG = 0.0;
+#pragma unroll
+  for (int j = 0; j < D; ++j) GG = fma(Ga[j], c.G[b][j], GG);
+  const double ak = c.c1 * ga[k], bk = c.c2 * c.g[b][k];
+#pragma unroll
+  for (int i = 0; i < D; ++i) {
+    double t = fma(ak, c.g[b][i], bk * ga[i]);
+    if (i == k) t += c.mu * GG;
+    out[i] = c.vol * t;
+  }
+}
+
 struct AsmArgs {
   const double *coords;
   const int32_t *conn;
@@ -190,20 +207,33 @@ __global__ void k_jcomp_bc(const int32_t *dofs, int64_t nd, const int32_t *color
 }
 
 // Alg. 2 part 2: K_ij = J_comp[i, color[j]] over the pattern (one thread per row).
+// 8 lanes per row: coalesced col_idx / vals streams, the row's J_comp entries (C doubles,
+// contiguous) gathered through L1.
 __global__ void k_decompress(const int64_t *row_ptr, const int32_t *col_idx, const int32_t *colors,
                              const double *J, int C, int64_t N, double *vals) {
-  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < N;
-       r += (int64_t)gridDim.x * blockDim.x) {
+  const int lane = threadIdx.x & 7;
+  const int64_t groups = (int64_t)gridDim.x * (blockDim.x / 8);
+  for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / 8; r < N; r += groups) {
     const double *jr = J + r * C;
-    for (int64_t p = row_ptr[r]; p < row_ptr[r + 1]; ++p) vals[p] = jr[__ldg(colors + col_idx[p])];
+    for (int64_t p = row_ptr[r] + lane; p < row_ptr[r + 1]; p += 8)
+      vals[p] = __ldg(jr + __ldg(colors + __ldg(col_idx + p)));
   }
 }
 
-// ------------------------------------------------------------------ deterministic row gather
-// One thread per node n: for its incident elements in ascending element order, the block
-// row K_{a(n), b} is accumulated at the CSR slot of node b in n's sorted neighbour list
-// (the compressed row of Alg. 2 stored at its decompressed positions), then written once.
-constexpr int kRowMaxAdj = 32;
+// ------------------------------------------------------------------ fused row-pull (deterministic)
+// One warp per node n (32 lanes).  Lane l takes the l-th incident element of n (ascending
+// element order), evaluates that element's column context once and its block row
+// K_{a(n), b} for every element node b into shared memory.  Lane s then owns slot s of n's
+// sorted neighbour list (i.e. the CSR columns of node nadj[s]) and sums, in a fixed
+// precomputed order, the staged blocks that land on it: the compressed row of Alg. 2 at
+// its decompressed positions (within a row every color names exactly one column, so the
+// color -> CSR slot map is a bijection).  No atomics, bitwise reproducible, each value
+// written once.  slot lists: per node, entries (l << 2 | b) grouped by slot (setup).
+#ifndef FEM_ROWS_MINB
+#define FEM_ROWS_MINB 5
+#endif
+constexpr int kRowLanes = 32;
+constexpr int kRowGroups = 4;  // warps (nodes) per 128-thread CTA
 
 struct RowArgs {
   const double *coords;
@@ -217,6 +247,8 @@ struct RowArgs {
   const int32_t *inc;
   const int64_t *nadj_ptr;
   const int32_t *nadj;
+  const uint8_t *slot_list;
+  const uint16_t *slot_off;
   const int32_t *dmpc_ptr, *dmpc, *ms, *mm;
   const int64_t *row_ptr;
   int64_t n_nodes, n_u;
@@ -224,81 +256,140 @@ struct RowArgs {
   int *err;
 };
 
-template <int D, int MAT>
-__global__ void __launch_bounds__(128) k_rows_gather(RowArgs A) {
-  for (int64_t n = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; n < A.n_nodes;
+template <int D>
+__global__ void k_slot_build(const int64_t *inc_ptr, const int32_t *inc, const int32_t *conn,
+                             const int64_t *nadj_ptr, const int32_t *nadj, int64_t n_nodes,
+                             uint8_t *slot_list, uint16_t *slot_off, int *err) {
+  constexpr int NEN = D + 1;
+  for (int64_t n = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; n < n_nodes;
        n += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t a0 = A.nadj_ptr[n];
-    const int na = (int)(A.nadj_ptr[n + 1] - a0);
-    if (na > kRowMaxAdj) { atomicOr(A.err, ERRW_ADJ_OVERFLOW); continue; }
-    double acc[kRowMaxAdj][D][D];
-    for (int q = 0; q < na; ++q)
-#pragma unroll
-      for (int i = 0; i < D; ++i)
-#pragma unroll
-        for (int k = 0; k < D; ++k) acc[q][i][k] = 0.0;
-    const unsigned bcn = A.node_bc ? A.node_bc[n] : 0u;
-    for (int64_t t = A.inc_ptr[n]; t < A.inc_ptr[n + 1]; ++t) {
-      const int32_t packed = A.inc[t];
-      const int64_t e = packed / (D + 1);
-      const int a = packed % (D + 1);
-      int32_t nd[D + 1];
-      load_nodes<D>(A.conn, e, nd);
-      double lam = A.lam, mu = A.mu;
-      if (A.phase) {
-        const int ph = A.phase[e];
-        lam = A.lam_tab[ph];
-        mu = A.mu_tab[ph];
-      }
-      ColumnCtx<D> cx;
-      if (!column_ctx<D, MAT>(A.coords, nd, A.z, lam, mu, cx)) {
-        atomicOr(A.err, ERRW_INVERTED);
-        continue;
-      }
-#pragma unroll
-      for (int b = 0; b < D + 1; ++b) {
-        // slot of node nd[b] in n's sorted neighbour list
-        int lo = 0, hi = na;
-        while (lo < hi) {
-          const int mid = (lo + hi) >> 1;
-          if (A.nadj[a0 + mid] < nd[b]) lo = mid + 1; else hi = mid;
+    const int deg = (int)(inc_ptr[n + 1] - inc_ptr[n]);
+    const int64_t a0 = nadj_ptr[n];
+    const int sn = (int)(nadj_ptr[n + 1] - a0);
+    if (deg > 63 || sn > 2 * kRowLanes) { atomicOr(err, ERRW_ADJ_OVERFLOW); continue; }
+    uint16_t cnt[2 * kRowLanes + 1];
+    for (int q = 0; q <= sn; ++q) cnt[q] = 0;
+    for (int pass = 0; pass < 2; ++pass) {
+      for (int l = 0; l < deg; ++l) {
+        const int64_t e = inc[inc_ptr[n] + l] / NEN;
+        for (int b = 0; b < NEN; ++b) {
+          const int32_t m = conn[e * NEN + b];
+          int lo = 0, hi = sn;
+          while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (nadj[a0 + mid] < m) lo = mid + 1; else hi = mid;
+          }
+          if (pass == 0) cnt[lo + 1]++;
+          else slot_list[NEN * inc_ptr[n] + cnt[lo]++] = (uint8_t)(l << 2 | b);
         }
-        const unsigned bcb = A.node_bc ? __ldg(A.node_bc + nd[b]) : 0u;
-#pragma unroll
-        for (int k = 0; k < D; ++k) {
-          if (bcb & (1u << k)) continue;           // masked column
-          double kab[D];
-          column_block<D>(cx, a, b, k, kab);
-#pragma unroll
-          for (int i = 0; i < D; ++i) acc[lo][i][k] += kab[i];
-        }
+      }
+      if (pass == 0) {
+        for (int q = 0; q < sn; ++q) cnt[q + 1] += cnt[q];
+        for (int q = 0; q <= sn; ++q) slot_off[a0 + n + q] = cnt[q];
       }
     }
-    for (int i = 0; i < D; ++i) {
-      const int64_t r = n * D + i;
-      const int64_t base = A.row_ptr[r];
-      const bool drow = bcn & (1u << i);
-      for (int q = 0; q < na; ++q)
+  }
+}
+
+template <int D, int MAT>
+__global__ void __launch_bounds__(kRowLanes * kRowGroups, FEM_ROWS_MINB) k_rows_fused(RowArgs A) {
+  constexpr int NEN = D + 1, BS = D * D;
+  __shared__ double stage[kRowGroups][kRowLanes][NEN * BS + 1];  // +1: no bank conflicts
+  __shared__ uint8_t s_list[kRowGroups][NEN * 64];                // node's slot list
+  __shared__ uint16_t s_off[kRowGroups][2 * kRowLanes + 1];       // its slot offsets
+  const int lane = threadIdx.x % kRowLanes, g = threadIdx.x / kRowLanes;
+  for (int64_t n = (int64_t)blockIdx.x * kRowGroups + g; n < A.n_nodes;
+       n += (int64_t)gridDim.x * kRowGroups) {
+    const int64_t i0 = A.inc_ptr[n];
+    const int deg = (int)(A.inc_ptr[n + 1] - i0);
+    const int64_t a0 = A.nadj_ptr[n];
+    const int sn = (int)(A.nadj_ptr[n + 1] - a0);
+    const unsigned bcn = A.node_bc ? A.node_bc[n] : 0u;
+    // stage the node's slot metadata in shared memory (coalesced), read in the sums below
+    for (int q = lane; q < NEN * deg; q += kRowLanes) s_list[g][q] = A.slot_list[NEN * i0 + q];
+    for (int q = lane; q <= sn; q += kRowLanes) s_off[g][q] = A.slot_off[a0 + n + q];
+    const uint8_t *sl = s_list[g];
+    const uint16_t *so = s_off[g];
+    for (int l0 = 0; l0 < deg; l0 += kRowLanes) {
+      const int l = l0 + lane;
+      if (l < deg) {
+        const int32_t packed = A.inc[i0 + l];
+        const int64_t e = packed / NEN;
+        const int a = packed % NEN;
+        int32_t nd[NEN];
+        load_nodes<D>(A.conn, e, nd);
+        double lam = A.lam, mu = A.mu;
+        if (A.phase) {
+          const int ph = A.phase[e];
+          lam = A.lam_tab[ph];
+          mu = A.mu_tab[ph];
+        }
+        ColumnCtx<D> cx;
+        const bool ok = column_ctx<D, MAT>(A.coords, nd, A.z, lam, mu, cx);
+        if (!ok) atomicOr(A.err, ERRW_INVERTED);
+        double Ga[D], ga[D];
 #pragma unroll
-        for (int k = 0; k < D; ++k) {
-          double v = acc[q][i][k];
-          if (drow) v = (A.nadj[a0 + q] == n && k == i) ? 1.0 : 0.0;
-          A.vals[base + q * D + k] = v;
+        for (int j = 0; j < D; ++j) {
+          Ga[j] = cx.G[0][j];
+          ga[j] = cx.g[0][j];
         }
-      if (A.dmpc_ptr) {  // B^T entries, ascending constraint id (same order as the pattern)
-        const int32_t lo = A.dmpc_ptr[r], hi = A.dmpc_ptr[r + 1];
-        int64_t w = base + (int64_t)na * D;
-        int32_t prev = -1;
-        for (int32_t q = lo; q < hi; ++q, ++w) {
-          int32_t kmin = INT32_MAX;  // next constraint id above prev
-          for (int32_t q2 = lo; q2 < hi; ++q2) {
-            const int32_t kk = A.dmpc[q2];
-            if (kk > prev && kk < kmin) kmin = kk;
+#pragma unroll
+        for (int q = 1; q < NEN; ++q)
+          if (a == q) {
+#pragma unroll
+            for (int j = 0; j < D; ++j) {
+              Ga[j] = cx.G[q][j];
+              ga[j] = cx.g[q][j];
+            }
           }
-          prev = kmin;
-          double v = (A.ms[kmin] == r ? 1.0 : 0.0) - (A.mm[kmin] == r ? 1.0 : 0.0);
-          A.vals[w] = drow ? 0.0 : v;
+#pragma unroll
+        for (int b = 0; b < NEN; ++b)
+#pragma unroll
+          for (int k = 0; k < D; ++k) {
+            double kab[D];
+            column_block_row<D>(cx, Ga, ga, b, k, kab);
+#pragma unroll
+            for (int i = 0; i < D; ++i) stage[g][lane][b * BS + i * D + k] = ok ? kab[i] : 0.0;
+          }
+      }
+      __syncwarp();
+      const bool first = (l0 == 0), last = (l0 + kRowLanes >= deg);
+      // the sn*D*D outputs (slot s, entry i*D+k) are spread round-robin over the lanes so the
+      // diagonal slot's long list (every incident element) does not serialise the warp;
+      // partial sums of earlier chunks live in the output itself (same lane, no race)
+      for (int q = lane; q < sn * BS; q += kRowLanes) {
+        const int s = q / BS, ik = q - s * BS, i = ik / D, k = ik - i * D;
+        const int64_t pos = A.row_ptr[n * D + i] + (int64_t)s * D + k;
+        double acc = first ? 0.0 : A.vals[pos];
+        for (int c = so[s]; c < so[s + 1]; ++c) {
+          const int ent = sl[c];
+          const int le = (ent >> 2) - l0;
+          if (le >= 0 && le < kRowLanes) acc += stage[g][le][(ent & 3) * BS + ik];
         }
+        if (last) {
+          const int32_t m = A.nadj[a0 + s];
+          if (A.node_bc && (A.node_bc[m] & (1u << k))) acc = 0.0;            // masked column
+          if (bcn & (1u << i)) acc = (m == n && k == i) ? 1.0 : 0.0;          // identity row
+        }
+        A.vals[pos] = acc;
+      }
+      __syncwarp();
+    }
+    if (A.dmpc_ptr && lane < D) {  // B^T entries of row (n, lane), ascending constraint id
+      const int64_t r = n * D + lane;
+      const bool drow = bcn & (1u << lane);
+      const int32_t lo = A.dmpc_ptr[r], hi = A.dmpc_ptr[r + 1];
+      int64_t w = A.row_ptr[r] + (int64_t)sn * D;
+      int32_t prev = -1;
+      for (int32_t q = lo; q < hi; ++q, ++w) {
+        int32_t kmin = INT32_MAX;
+        for (int32_t q2 = lo; q2 < hi; ++q2) {
+          const int32_t kk = A.dmpc[q2];
+          if (kk > prev && kk < kmin) kmin = kk;
+        }
+        prev = kmin;
+        const double v = (A.ms[kmin] == r ? 1.0 : 0.0) - (A.mm[kmin] == r ? 1.0 : 0.0);
+        A.vals[w] = drow ? 0.0 : v;
       }
     }
   }
@@ -318,6 +409,23 @@ __global__ void k_rows_mpc(const int32_t *ms, const int32_t *mm, int64_t nc, int
   }
 }
 
+static fem_status build_slot_lists(Problem *p, cudaStream_t s) {
+  if (p->slot_list || p->n_nodes == 0) return FEM_OK;
+  const int64_t nent = p->n_elems * p->nen * p->nen;
+  const int64_t nnode_nnz = p->n_nodes + (p->n_nodes > 0 ? 0 : 0);
+  int64_t nadj_total = 0;
+  FEM_CUDA(cudaMemcpyAsync(&nadj_total, p->nadj_ptr + p->n_nodes, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+  FEM_CUDA(cudaStreamSynchronize(s));
+  FEM_CUDA(cudaMalloc(&p->slot_list, nent > 0 ? nent : 1));
+  FEM_CUDA(cudaMalloc(&p->slot_off, sizeof(uint16_t) * (nadj_total + nnode_nnz + 1)));
+  if (p->dim == 2)
+    k_slot_build<2><<<grid_for(p->n_nodes, 128), 128, 0, s>>>(p->inc_ptr, p->inc, p->conn, p->nadj_ptr, p->nadj, p->n_nodes, p->slot_list, p->slot_off, p->d_err);
+  else
+    k_slot_build<3><<<grid_for(p->n_nodes, 128), 128, 0, s>>>(p->inc_ptr, p->inc, p->conn, p->nadj_ptr, p->nadj, p->n_nodes, p->slot_list, p->slot_off, p->d_err);
+  FEM_LAUNCH_CHECK("slot lists");
+  return read_error_word(p, s);
+}
+
 template <int D, int MAT>
 static void launch_colored(const AsmArgs &a, bool literal, int pass, cudaStream_t s) {
   const int grid = grid_for(a.E);
@@ -328,21 +436,24 @@ static void launch_colored(const AsmArgs &a, bool literal, int pass, cudaStream_
 static fem_status assemble(Problem *p, const double *z, double *vals, unsigned flags,
                            cudaStream_t s) {
   const bool bc = (flags & FEM_APPLY_BC) && p->n_dir;
-  if (flags & FEM_DETERMINISTIC) {
+  if (!(flags & (FEM_ASSEMBLE_LITERAL | FEM_ASSEMBLE_JCOMP))) {  // default: fused row-pull
+    fem_status st0 = build_slot_lists(p, s);
+    if (st0) return st0;
     RowArgs A{};
     A.coords = p->coords; A.conn = p->conn; A.lam = p->lam; A.mu = p->mu;
     A.phase = p->phase; A.lam_tab = p->lam_tab; A.mu_tab = p->mu_tab;
     A.node_bc = bc ? p->node_bc : nullptr; A.z = z;
     A.inc_ptr = p->inc_ptr; A.inc = p->inc; A.nadj_ptr = p->nadj_ptr; A.nadj = p->nadj;
+    A.slot_list = p->slot_list; A.slot_off = p->slot_off;
     A.dmpc_ptr = p->dmpc_ptr; A.dmpc = p->dmpc; A.ms = p->mpc_s; A.mm = p->mpc_m;
     A.row_ptr = p->row_ptr; A.n_nodes = p->n_nodes; A.n_u = p->n_u; A.vals = vals; A.err = p->d_err;
-    const int grid = grid_for(p->n_nodes, 128);
+    const int grid = grid_for(p->n_nodes, kRowGroups, 148 * 64);
     if (p->dim == 2) {
-      if (p->material == FEM_LINEAR_ELASTIC) k_rows_gather<2, FEM_LINEAR_ELASTIC><<<grid, 128, 0, s>>>(A);
-      else k_rows_gather<2, FEM_NEO_HOOKEAN><<<grid, 128, 0, s>>>(A);
+      if (p->material == FEM_LINEAR_ELASTIC) k_rows_fused<2, FEM_LINEAR_ELASTIC><<<grid, kRowLanes * kRowGroups, 0, s>>>(A);
+      else k_rows_fused<2, FEM_NEO_HOOKEAN><<<grid, kRowLanes * kRowGroups, 0, s>>>(A);
     } else {
-      if (p->material == FEM_LINEAR_ELASTIC) k_rows_gather<3, FEM_LINEAR_ELASTIC><<<grid, 128, 0, s>>>(A);
-      else k_rows_gather<3, FEM_NEO_HOOKEAN><<<grid, 128, 0, s>>>(A);
+      if (p->material == FEM_LINEAR_ELASTIC) k_rows_fused<3, FEM_LINEAR_ELASTIC><<<grid, kRowLanes * kRowGroups, 0, s>>>(A);
+      else k_rows_fused<3, FEM_NEO_HOOKEAN><<<grid, kRowLanes * kRowGroups, 0, s>>>(A);
     }
     if (p->n_mpc)
       k_rows_mpc<<<grid_for(p->n_mpc), kThreads, 0, s>>>(p->mpc_s, p->mpc_m, p->n_mpc, p->n_u, p->dim,
@@ -377,7 +488,7 @@ static fem_status assemble(Problem *p, const double *z, double *vals, unsigned f
     k_jcomp_mpc<<<grid_for(p->n_mpc), kThreads, 0, s>>>(p->mpc_s, p->mpc_m, p->n_mpc, p->n_u, p->dim,
                                                         bc ? p->node_bc : nullptr, p->colors, C, J);
   if (bc) k_jcomp_bc<<<grid_for(p->n_dir), kThreads, 0, s>>>(p->dir_dofs, p->n_dir, p->colors, C, J);
-  k_decompress<<<grid_for(p->N), kThreads, 0, s>>>(p->row_ptr, p->col_idx, p->colors, J, C, p->N, vals);
+  k_decompress<<<grid_for(p->N * 8, kThreads, 148 * 32), kThreads, 0, s>>>(p->row_ptr, p->col_idx, p->colors, J, C, p->N, vals);
   FEM_LAUNCH_CHECK("colored assembly");
   return FEM_OK;
 }

@@ -203,12 +203,13 @@ static ElemArgs elem_args(Problem *p) {
 }
 
 // ------------------------------------------------------------------ small vector kernels
+// owned != null: only DOFs of nodes this rank owns (multi-GPU dots)
 __global__ void k_partial_dot(const double *a, const double *b, int64_t n, double scale,
-                              double *partials) {
+                              double *partials, const uint8_t *owned = nullptr, int dim = 1) {
   double acc = 0.0;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
-    acc = fma(a[i], b[i], acc);
+    if (!owned || owned[i / dim]) acc = fma(a[i], b[i], acc);
   const double t = block_sum<kThreads>(acc);
   if (threadIdx.x == 0) partials[blockIdx.x] = scale * t;
 }
@@ -223,10 +224,10 @@ __global__ void k_final_sum(const double *partials, int64_t n, double *out) {
 fem_status launch_dot(Problem *p, const double *a, const double *b, int64_t n, double *out,
                       cudaStream_t s) {
   const int nb = grid_for(n, kThreads, kReduceBlocks);
-  k_partial_dot<<<nb, kThreads, 0, s>>>(a, b, n, 1.0, p->partials);
+  k_partial_dot<<<nb, kThreads, 0, s>>>(a, b, n, 1.0, p->partials, p->size > 1 ? p->owned : nullptr, p->dim);
   k_final_sum<<<1, kThreads, 0, s>>>(p->partials, nb, out);
   FEM_LAUNCH_CHECK("dot");
-  return FEM_OK;
+  return allreduce(p, out, 1, s);  // no-op on one rank
 }
 
 // lambda_k * g_k(u) partial sums (energy), g_k = u[s] - u[m] - b
@@ -260,18 +261,22 @@ __global__ void k_mpc_apply(const double *z, const int32_t *s, const int32_t *m,
   }
 }
 
-__global__ void k_axpy(double *y, const double *x, double a, int64_t n) {
+// owned != null (FEM_LOCAL_ONLY on a multi-GPU rank): DOF-wise terms only on owned DOFs, so
+// that the later halo sum counts them once
+__global__ void k_axpy(double *y, const double *x, double a, int64_t n,
+                       const uint8_t *owned = nullptr, int dim = 1) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x)
-    y[i] = fma(a, x[i], y[i]);
+    if (!owned || owned[i / dim]) y[i] = fma(a, x[i], y[i]);
 }
 
 // y[D] = src[D] (src = v for the HVP) or 0 (src = null, residual)
-__global__ void k_bc_fix(double *y, const int32_t *dofs, int64_t nd, const double *src) {
+__global__ void k_bc_fix(double *y, const int32_t *dofs, int64_t nd, const double *src,
+                         const uint8_t *owned = nullptr, int dim = 1) {
   for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < nd;
        k += (int64_t)gridDim.x * blockDim.x) {
     const int32_t d = dofs[k];
-    y[d] = src ? src[d] : 0.0;
+    y[d] = (src && (!owned || owned[d / dim])) ? src[d] : 0.0;
   }
 }
 
@@ -350,7 +355,7 @@ fem_status run_residual(Problem *p, const double *z, double *r, unsigned flags, 
     st = tile_pass(p, OP_RESIDUAL, z, nullptr, r, false, det, nullptr, s);
   }
   if (st) return st;
-  if (p->size > 1) {
+  if (p->size > 1 && !(flags & FEM_LOCAL_ONLY)) {
     st = halo_add(p, r, s);
     if (st) return st;
   }
@@ -358,9 +363,10 @@ fem_status run_residual(Problem *p, const double *z, double *r, unsigned flags, 
     k_mpc_apply<<<grid_for(p->n_mpc), kThreads, 0, s>>>(z, p->mpc_s, p->mpc_m, p->mpc_b, p->n_mpc,
                                                         p->n_u, p->dim, nullptr, r);
   }
-  if (p->f_ext) k_axpy<<<grid_for(p->n_u), kThreads, 0, s>>>(r, p->f_ext, -1.0, p->n_u);
+  const uint8_t *own = (p->size > 1 && (flags & FEM_LOCAL_ONLY)) ? p->owned : nullptr;
+  if (p->f_ext) k_axpy<<<grid_for(p->n_u), kThreads, 0, s>>>(r, p->f_ext, -1.0, p->n_u, own, p->dim);
   if ((flags & FEM_APPLY_BC) && p->n_dir)
-    k_bc_fix<<<grid_for(p->n_dir), kThreads, 0, s>>>(r, p->dir_dofs, p->n_dir, nullptr);
+    k_bc_fix<<<grid_for(p->n_dir), kThreads, 0, s>>>(r, p->dir_dofs, p->n_dir, nullptr, own, p->dim);
   FEM_LAUNCH_CHECK("residual");
   return FEM_OK;
 }
@@ -384,7 +390,7 @@ fem_status run_hvp(Problem *p, const double *z, const double *v, double *y, unsi
     st = tile_pass(p, OP_HVP, z, v, y, bc, det, nullptr, s);
   }
   if (st) return st;
-  if (p->size > 1) {
+  if (p->size > 1 && !(flags & FEM_LOCAL_ONLY)) {
     st = halo_add(p, y, s);
     if (st) return st;
   }
@@ -392,7 +398,8 @@ fem_status run_hvp(Problem *p, const double *z, const double *v, double *y, unsi
     k_mpc_apply<<<grid_for(p->n_mpc), kThreads, 0, s>>>(v, p->mpc_s, p->mpc_m, nullptr, p->n_mpc,
                                                         p->n_u, p->dim, bc ? p->node_bc : nullptr,
                                                         y);
-  if (bc) k_bc_fix<<<grid_for(p->n_dir), kThreads, 0, s>>>(y, p->dir_dofs, p->n_dir, v);
+  const uint8_t *own = (p->size > 1 && (flags & FEM_LOCAL_ONLY)) ? p->owned : nullptr;
+  if (bc) k_bc_fix<<<grid_for(p->n_dir), kThreads, 0, s>>>(y, p->dir_dofs, p->n_dir, v, own, p->dim);
   FEM_LAUNCH_CHECK("hvp");
   return FEM_OK;
 }
@@ -489,9 +496,8 @@ fem_status fem_create(fem_problem **out, const fem_mesh_desc *d, const fem_dist_
   FEM_C(cudaMalloc(&p->d_err, sizeof(int) * 2));
   FEM_C(cudaMemsetAsync(p->d_err, 0, sizeof(int) * 2, s));
   if (dist && dist->size > 1) {
-    p->nccl = dist->nccl_comm;
-    p->rank = dist->rank;
-    p->size = dist->size;
+    fem_status dst = dist_setup(p, dist, s);
+    if (dst) return fail(dst);
   }
   // validation (ids, orientation / degeneracy, Dirichlet sortedness, MPC pairs)
   int *bad = p->d_err + 1;
@@ -530,12 +536,13 @@ fem_status fem_destroy(fem_problem *h) {
   void *bufs[] = {p->coords, p->conn, p->phase, p->lam_tab, p->mu_tab, p->node_bc, p->dir_dofs,
                   p->dir_vals, p->mpc_s, p->mpc_m, p->mpc_b, p->f_ext, p->partials, p->scal,
                   p->d_err, p->inc_ptr, p->inc, p->nadj_ptr, p->nadj, p->dmpc_ptr, p->dmpc,
-                  p->row_ptr, p->col_idx, p->diag_pos, p->colors, p->jcomp.ptr, p->cgbuf.ptr,
+                  p->row_ptr, p->col_idx, p->diag_pos, p->slot_list, p->slot_off, p->colors, p->jcomp.ptr, p->cgbuf.ptr,
                   p->tmp.ptr};
   for (void *b : bufs)
     if (b) cudaFree(b);
   if (p->h_scal) cudaFreeHost(p->h_scal);
   free_tiles(p->tiles);
+  dist_free(p);
   delete h;
   return FEM_OK;
 }
@@ -576,7 +583,7 @@ fem_status fem_energy(fem_problem *h, const double *z, double *energy, fem_strea
       st = build_tiles(p, s);
       if (st) return st;
       st = tile_pass(p, OP_ENERGY, z, nullptr, nullptr, false, false, p->tiles.epart, s);
-      k_final_sum<<<1, kThreads, 0, s>>>(p->tiles.epart, p->tiles.n_tiles, p->partials);
+      k_final_sum<<<1, kThreads, 0, s>>>(p->tiles.epart, tile_energy_partials(p), p->partials);
       n = 1;
     }
     if (st) return st;
@@ -589,13 +596,14 @@ fem_status fem_energy(fem_problem *h, const double *z, double *energy, fem_strea
   }
   if (p->f_ext) {
     const int g3 = grid_for(p->n_u, kThreads, kReduceBlocks);
-    k_partial_dot<<<g3, kThreads, 0, s>>>(p->f_ext, z, p->n_u, -1.0, p->partials + n);
+    k_partial_dot<<<g3, kThreads, 0, s>>>(p->f_ext, z, p->n_u, -1.0, p->partials + n,
+                                          p->size > 1 ? p->owned : nullptr, p->dim);
     n += g3;
   }
   if (n == 0) FEM_CUDA(cudaMemsetAsync(energy, 0, sizeof(double), s));
   else k_final_sum<<<1, kThreads, 0, s>>>(p->partials, n, energy);
   FEM_LAUNCH_CHECK("fem_energy");
-  if (p->size > 1) return fem_allreduce_sum(h, energy, 1, stream);
+  return allreduce(p, energy, 1, s);
   return FEM_OK;
 }
 

@@ -9,6 +9,7 @@
 #include <stdint.h>
 
 #include <string>
+#include <vector>
 
 #include "../../include/fem.h"
 
@@ -19,7 +20,10 @@ enum : int { ERRW_INVERTED = 1, ERRW_TOO_MANY_COLORS = 2, ERRW_NONFINITE = 4, ER
 constexpr int kMaxNodeAdj = 64;     // max distinct node neighbours (incl. self) per node
 constexpr int kReduceBlocks = 1184; // 148 SMs x 8: fixed grid => fixed reduction order
 constexpr int kThreads = 256;
-constexpr int kTile = 256;          // elements per tile (one CTA)
+#ifndef FEM_TILE
+#define FEM_TILE 256
+#endif
+constexpr int kTile = FEM_TILE;     // elements per tile (one CTA)
 
 enum { OP_ENERGY = 0, OP_RESIDUAL = 1, OP_HVP = 2 };
 
@@ -40,6 +44,10 @@ struct TileSet {
   int32_t *node_slots = nullptr; // [n_slots] slots of each node, tile order
   int64_t *node_slot_ptr = nullptr; // [n_nodes+1]
   double *epart = nullptr;       // [n_tiles] energy partials
+  // packed per-tile metadata blocks (fem_tiles.cu pack_tile_meta), mb bytes each
+  uint8_t *meta = nullptr;
+  int um = 0, mb = 0, off_nodes = 0, off_lconn = 0, off_ptr = 0, off_inc = 0, off_int = 0,
+      off_bc = 0, off_ph = 0;
 };
 
 struct Workspace {
@@ -83,6 +91,8 @@ struct Problem {
   int64_t *row_ptr = nullptr;
   int32_t *col_idx = nullptr;
   int64_t *diag_pos = nullptr;  // [N] position of the diagonal in each row (-1 if absent)
+  uint8_t *slot_list = nullptr; // fused assembly: per node (l << 2 | b) grouped by CSR slot
+  uint16_t *slot_off = nullptr; // [nnz_node + n_nodes] slot offsets into each node's list
   // coloring
   bool have_colors = false;
   int32_t n_colors = -1;
@@ -90,9 +100,16 @@ struct Problem {
   // workspaces
   Workspace jcomp, cgbuf, tmp, slotbuf;
   TileSet tiles;
-  // multi-GPU
+  // multi-GPU (fem_dist.cu)
   void *nccl = nullptr;
-  int rank = 0, size = 1;
+  int rank = 0, size = 1, n_nbr = 0;
+  std::vector<int> nbr_rank_h;
+  std::vector<int64_t> nbr_off_h;
+  int64_t n_halo_entries = 0, n_halo_nodes = 0;
+  int32_t *halo_send_nodes = nullptr, *halo_nodes = nullptr, *halo_src_ptr = nullptr,
+          *halo_src = nullptr;
+  double *sendbuf = nullptr, *recvbuf = nullptr;
+  uint8_t *owned = nullptr;     // [n_nodes] (size > 1)
 };
 
 // ------------------------------------------------------------------ error plumbing
@@ -167,6 +184,10 @@ fem_status build_tiles(Problem *p, cudaStream_t s);
 fem_status tile_pass(Problem *p, int op, const double *u, const double *v, double *out, bool mask,
                      bool det, double *partials, cudaStream_t s);
 void free_tiles(TileSet &T);
+int tile_energy_partials(Problem *p);
+fem_status dist_setup(Problem *p, const fem_dist_desc *d, cudaStream_t s);
+void dist_free(Problem *p);
+fem_status allreduce(Problem *p, double *buf, int n, cudaStream_t s);
 __global__ void k_final_sum(const double *partials, int64_t n, double *out);
 
 }  // namespace fem

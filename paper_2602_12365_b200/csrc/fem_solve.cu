@@ -24,7 +24,7 @@ __global__ void k_sub(const double *b, const double *Ax, double *r, int64_t n) {
 
 // z = dinv * r (or r), p = z, partial r.r and r.z
 __global__ void k_cg_start(const double *r, const double *dinv, double *zv, double *p, int64_t n,
-                           double *part_rr, double *part_rz) {
+                           double *part_rr, double *part_rz, const uint8_t *owned, int dim) {
   double rr = 0.0, rz = 0.0;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
@@ -32,8 +32,10 @@ __global__ void k_cg_start(const double *r, const double *dinv, double *zv, doub
     const double zi = dinv ? dinv[i] * ri : ri;
     if (dinv) zv[i] = zi;
     p[i] = zi;
-    rr = fma(ri, ri, rr);
-    rz = fma(ri, zi, rz);
+    if (!owned || owned[i / dim]) {
+      rr = fma(ri, ri, rr);
+      rz = fma(ri, zi, rz);
+    }
   }
   const double a = block_sum<kThreads>(rr);
   const double b = block_sum<kThreads>(rz);
@@ -46,7 +48,7 @@ __global__ void k_cg_start(const double *r, const double *dinv, double *zv, doub
 // alpha = rz / pAp; x += alpha p; r -= alpha Ap; z = dinv r; partial r.r, r.z
 __global__ void k_cg_update(const double *scal, int rz_slot, double *x, double *r, double *zv,
                             const double *p, const double *Ap, const double *dinv, int64_t n,
-                            double *part_rr, double *part_rz) {
+                            double *part_rr, double *part_rz, const uint8_t *owned, int dim) {
   const double alpha = scal[rz_slot] / scal[S_PAP];
   double rr = 0.0, rz = 0.0;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
@@ -56,8 +58,10 @@ __global__ void k_cg_update(const double *scal, int rz_slot, double *x, double *
     r[i] = ri;
     const double zi = dinv ? dinv[i] * ri : ri;
     if (dinv) zv[i] = zi;
-    rr = fma(ri, ri, rr);
-    rz = fma(ri, zi, rz);
+    if (!owned || owned[i / dim]) {
+      rr = fma(ri, ri, rr);
+      rz = fma(ri, zi, rz);
+    }
   }
   const double a = block_sum<kThreads>(rr);
   const double b = block_sum<kThreads>(rz);
@@ -141,8 +145,13 @@ fem_status run_cg(Problem *p, const double *z, const double *vals, const double 
   st = apply_op(p, o->op, z, vals, x, Ap, s);
   if (st) return st;
   k_sub<<<grid_for(n), kThreads, 0, s>>>(b, Ap, r, n);
-  k_cg_start<<<nb, kThreads, 0, s>>>(r, dinv, zv, pp, n, part_a, part_b);
+  const uint8_t *own = p->size > 1 ? p->owned : nullptr;
+  k_cg_start<<<nb, kThreads, 0, s>>>(r, dinv, zv, pp, n, part_a, part_b, own, p->dim);
   k_final_sum2<<<1, kThreads, 0, s>>>(part_a, part_b, nb, p->scal + S_RR0, p->scal + S_RZ0);
+  st = allreduce(p, p->scal + S_RR0, 1, s);
+  if (st) return st;
+  st = allreduce(p, p->scal + S_RZ0, 1, s);
+  if (st) return st;
   st = launch_dot(p, b, b, n, p->scal + S_BB, s);
   if (st) return st;
   FEM_LAUNCH_CHECK("cg start");
@@ -166,9 +175,14 @@ fem_status run_cg(Problem *p, const double *z, const double *vals, const double 
     if (st) return st;
     st = launch_dot(p, pp, Ap, n, p->scal + S_PAP, s);
     if (st) return st;
-    k_cg_update<<<nb, kThreads, 0, s>>>(p->scal, S_RZ0 + cur, x, r, zv, pp, Ap, dinv, n, part_a, part_b);
+    k_cg_update<<<nb, kThreads, 0, s>>>(p->scal, S_RZ0 + cur, x, r, zv, pp, Ap, dinv, n, part_a,
+                                        part_b, own, p->dim);
     k_final_sum2<<<1, kThreads, 0, s>>>(part_a, part_b, nb, p->scal + S_RR0 + (cur ^ 1),
                                         p->scal + S_RZ0 + (cur ^ 1));
+    st = allreduce(p, p->scal + S_RR0 + (cur ^ 1), 1, s);
+    if (st) return st;
+    st = allreduce(p, p->scal + S_RZ0 + (cur ^ 1), 1, s);
+    if (st) return st;
     k_cg_dir<<<grid_for(n), kThreads, 0, s>>>(p->scal, S_RZ0 + cur, S_RZ0 + (cur ^ 1), zv, pp, n);
     FEM_LAUNCH_CHECK("cg iteration");
     ++it;
@@ -187,14 +201,6 @@ fem_status run_cg(Problem *p, const double *z, const double *vals, const double 
   if (result == FEM_ERR_CG_BREAKDOWN) set_error("CG breakdown: p^T A p <= 0");
   if (result == FEM_ERR_NOT_CONVERGED) set_error("CG: iteration cap reached");
   return result;
-}
-
-fem_status halo_add(Problem *p, double *y, cudaStream_t s) {
-  (void)y;
-  (void)s;
-  if (p->size <= 1) return FEM_OK;
-  set_error("multi-rank halo exchange not available in this build");
-  return FEM_ERR_NCCL;
 }
 
 }  // namespace fem
@@ -264,31 +270,6 @@ fem_status fem_newton_solve(fem_problem *h, double *z, const fem_newton_opts *o,
   cudaStreamSynchronize(s);
   cudaFree(buf);
   return result;
-}
-
-fem_status fem_nccl_unique_id(unsigned char id[128]) {
-  (void)id;
-  set_error("NCCL support not built");
-  return FEM_ERR_NCCL;
-}
-
-fem_status fem_nccl_comm_init(const unsigned char id[128], int rank, int size, void **comm) {
-  (void)id; (void)rank; (void)size; (void)comm;
-  set_error("NCCL support not built");
-  return FEM_ERR_NCCL;
-}
-
-fem_status fem_nccl_comm_destroy(void *comm) {
-  (void)comm;
-  return FEM_OK;
-}
-
-fem_status fem_allreduce_sum(fem_problem *h, double *buf, int n, fem_stream stream) {
-  (void)buf; (void)n; (void)stream;
-  FEM_ARG(h, "fem_allreduce_sum: null problem");
-  if (h->p.size <= 1) return FEM_OK;
-  set_error("NCCL support not built");
-  return FEM_ERR_NCCL;
 }
 
 }  // extern "C"

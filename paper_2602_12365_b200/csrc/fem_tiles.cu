@@ -23,6 +23,10 @@
 #include "element.cuh"
 #include "fem_internal.cuh"
 
+#ifndef FEM_PIPE_MINB
+#define FEM_PIPE_MINB 3
+#endif
+
 namespace fem {
 
 // ------------------------------------------------------------------ setup
@@ -202,6 +206,8 @@ __global__ void k_slot_pairs(TileSet T, int64_t n_tiles, const int64_t *slot_off
   }
 }
 
+fem_status pack_tile_meta(Problem *p, cudaStream_t s);
+
 fem_status build_tiles(Problem *p, cudaStream_t s) {
   TileSet &T = p->tiles;
   if (T.built || p->n_elems == 0) return FEM_OK;
@@ -312,161 +318,258 @@ fem_status build_tiles(Problem *p, cudaStream_t s) {
   FEM_CUDA(cudaStreamSynchronize(s));
   cudaFree(keys); cudaFree(keys_out); cudaFree(idx); cudaFree(node_cnt);
   FEM_CUDA(cudaMalloc(&T.epart, sizeof(double) * nt));
+  st = pack_tile_meta(p, s);
+  if (st) return st;
+  FEM_CUDA(cudaStreamSynchronize(s));
   T.built = true;
   return FEM_OK;
 }
 
-// ------------------------------------------------------------------ tile element kernels
-struct TileArgs {
-  TileSet T;
-  const double *coords;
-  int64_t E;
+// ------------------------------------------------------------------ packed tile metadata
+// Per tile one contiguous, 16-byte aligned block (copied into shared memory with 16-byte
+// cp.async): header {U, n_valid}, nodes int32[um], lconn uint16[kTile][4], ptr
+// uint16[um+1], inc uint16[kTile*4], interior uint8[um], bc uint8[um] (Dirichlet bits of
+// each tile node), phase uint8[kTile] (optional).
+static inline int round_up(int x, int m) { return (x + m - 1) / m * m; }
+
+template <int D>
+__global__ void k_pack_meta(TileSet T, const uint8_t *node_bc, int64_t E) {
+  const int64_t t = blockIdx.x;
+  uint8_t *base = T.meta + t * T.mb;
+  const int U = T.U[t];
+  const int64_t e0 = t * kTile;
+  const int nvalid = (int)((E - e0 < kTile ? E - e0 : kTile) * (D + 1));
+  if (threadIdx.x == 0) {
+    reinterpret_cast<int *>(base)[0] = U;
+    reinterpret_cast<int *>(base)[1] = nvalid;
+    reinterpret_cast<int *>(base)[2] = 0;
+    reinterpret_cast<int *>(base)[3] = 0;
+  }
+  int32_t *nodes = reinterpret_cast<int32_t *>(base + T.off_nodes);
+  for (int i = threadIdx.x; i < T.um; i += blockDim.x) nodes[i] = i < U ? T.nodes[t * T.maxe + i] : 0;
+  uint16_t *lc = reinterpret_cast<uint16_t *>(base + T.off_lconn);
+  for (int i = threadIdx.x; i < kTile * 4; i += blockDim.x) lc[i] = T.lconn[t * kTile * 4 + i];
+  uint16_t *ptr = reinterpret_cast<uint16_t *>(base + T.off_ptr);
+  for (int i = threadIdx.x; i <= T.um; i += blockDim.x)
+    ptr[i] = i <= U ? T.ptr[t * (T.maxe + 1) + i] : (uint16_t)nvalid;
+  uint16_t *inc = reinterpret_cast<uint16_t *>(base + T.off_inc);
+  for (int i = threadIdx.x; i < kTile * 4; i += blockDim.x) inc[i] = i < nvalid ? T.inc[t * T.maxe + i] : 0;
+  for (int i = threadIdx.x; i < T.um; i += blockDim.x) {
+    base[T.off_int + i] = i < U ? T.interior[t * T.maxe + i] : 0;
+    base[T.off_bc + i] = i < U ? node_bc[T.nodes[t * T.maxe + i]] : 0;
+  }
+  if (T.phase)
+    for (int i = threadIdx.x; i < kTile; i += blockDim.x)
+      base[T.off_ph + i] = (e0 + i < E) ? T.phase[e0 + i] : 0;
+}
+
+fem_status pack_tile_meta(Problem *p, cudaStream_t s) {
+  TileSet &T = p->tiles;
+  T.um = round_up(T.max_U > 0 ? T.max_U : 1, 8);
+  T.off_nodes = 16;
+  T.off_lconn = T.off_nodes + 4 * T.um;
+  T.off_ptr = T.off_lconn + 8 * kTile;
+  T.off_inc = T.off_ptr + round_up(2 * (T.um + 1), 16);
+  T.off_int = T.off_inc + 8 * kTile;
+  T.off_bc = T.off_int + round_up(T.um, 16);
+  T.off_ph = T.off_bc + round_up(T.um, 16);
+  T.mb = round_up(T.off_ph + (T.phase ? kTile : 0), 16);
+  FEM_CUDA(cudaMalloc(&T.meta, (size_t)T.mb * T.n_tiles));
+  if (p->dim == 2) k_pack_meta<2><<<(unsigned)T.n_tiles, 256, 0, s>>>(T, p->node_bc, p->n_elems);
+  else k_pack_meta<3><<<(unsigned)T.n_tiles, 256, 0, s>>>(T, p->node_bc, p->n_elems);
+  FEM_LAUNCH_CHECK("pack tile meta");
+  return FEM_OK;
+}
+
+// ------------------------------------------------------------------ pipelined tile kernels
+// Persistent CTAs walk the tiles t = blockIdx.x, +gridDim.x, ...  While tile k is computed,
+// cp.async copies of tile k+1's nodal data (8-byte gathers of coordinates, u, v) and tile
+// k+2's metadata block (16-byte copies) are in flight: meta is triple-, node data
+// double-buffered in shared memory, so HBM/L2 latency overlaps the FP64 element math.
+__device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async8(void *smem, const void *gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+
+struct PipeArgs {
+  const uint8_t *meta;
+  int64_t n_tiles, E;
+  int mb, um, off_nodes, off_lconn, off_ptr, off_inc, off_int, off_bc, off_ph;
+  bool has_phase;
+  const int64_t *slot_off;
+  const double *coords, *u, *v;
   double lam, mu;
   const double *lam_tab, *mu_tab;
-  const uint8_t *node_bc;  // non-null: mask v (HVP with FEM_APPLY_BC)
-  const double *u, *v;
-  double *out;             // residual / HVP output (zeroed by the caller unless DET)
-  double *slots;           // DET: [n_slots][D] partial sums
-  double *partials;        // energy: one partial per tile
+  double *out, *slots, *partials;
   int *err;
 };
 
 template <int D, int MAT, int OP, bool MASK, bool DET>
-__global__ void __launch_bounds__(kTile, 3) k_tile_elem(TileArgs A) {
-  extern __shared__ double sm[];
-  const int t = blockIdx.x, tid = threadIdx.x;
-  const int U = A.T.U[t];
-  const int64_t toff = (int64_t)t * A.T.maxe;
-  const int32_t *tn = A.T.nodes + toff;
+__global__ void __launch_bounds__(kTile, FEM_PIPE_MINB) k_tile_pipe(PipeArgs A) {
+  constexpr int NEN = D + 1;
   constexpr bool NEED_U = (OP != OP_HVP) || (MAT == FEM_NEO_HOOKEAN);
-  double *xs = sm;
-  double *us = xs + U * D;
-  double *vs = us + (NEED_U ? U * D : 0);
-  double *contrib = vs + (OP == OP_HVP ? U * D : 0);  // [(D+1)*D][kTile]
-  // phase 0: stage nodal data
-  for (int i = tid; i < U * D; i += kTile) {
-    const int32_t n = __ldg(tn + i / D);
-    const int c = i % D;
-    const int64_t g = (int64_t)n * D + c;
-    xs[i] = __ldg(A.coords + g);
-    if constexpr (NEED_U) us[i] = __ldg(A.u + g);
-    if constexpr (OP == OP_HVP) {
-      double vv = __ldg(A.v + g);
-      if constexpr (MASK) {
-        if (__ldg(A.node_bc + n) & (1u << c)) vv = 0.0;
-      }
-      vs[i] = vv;
+  constexpr int NF = 1 + (NEED_U ? 1 : 0) + (OP == OP_HVP ? 1 : 0);
+  extern __shared__ __align__(16) unsigned char sm[];
+  const int tid = threadIdx.x;
+  const int mb = A.mb, um = A.um;
+  const int nstride = um * D * NF;
+  unsigned char *metab = sm;
+  double *nodeb = reinterpret_cast<double *>(sm + 3 * mb);
+  double *contrib = nodeb + 2 * nstride;
+  const int64_t G = gridDim.x;
+
+  auto issue_meta = [&](int64_t t, unsigned char *dst) {
+    const unsigned char *src = A.meta + t * (int64_t)mb;
+    for (int off = tid * 16; off < mb; off += kTile * 16) cp_async16(dst + off, src + off);
+  };
+  auto issue_nodes = [&](const unsigned char *m, double *dst) {
+    const int U = reinterpret_cast<const int *>(m)[0];
+    const int32_t *nodes = reinterpret_cast<const int32_t *>(m + A.off_nodes);
+    for (int i = tid; i < U * D; i += kTile) {
+      const int64_t g = (int64_t)nodes[i / D] * D + (i % D);
+      cp_async8(dst + i, A.coords + g);
+      if constexpr (NEED_U) cp_async8(dst + um * D + i, A.u + g);
+      if constexpr (OP == OP_HVP) cp_async8(dst + (NF - 1) * um * D + i, A.v + g);
     }
+  };
+
+  double eacc = 0.0;
+  int64_t t = blockIdx.x;
+  if (t < A.n_tiles) {
+    issue_meta(t, metab);
+    cp_async_commit();
+    cp_async_wait_all();
+    __syncthreads();
+    issue_nodes(metab, nodeb);
+    if (t + G < A.n_tiles) issue_meta(t + G, metab + mb);
+    cp_async_commit();
   }
-  __syncthreads();
-  // phase 1: one element per thread
-  const int64_t e = (int64_t)t * kTile + tid;
-  double acc = 0.0;
-  if (e < A.E) {
-    const ushort4 lc4 = __ldg(reinterpret_cast<const ushort4 *>(A.T.lconn) + e);
-    const int lc[4] = {lc4.x, lc4.y, lc4.z, lc4.w};
-    double x[D + 1][D], G[D + 1][D], vol;
+  for (int k = 0; t < A.n_tiles; ++k, t += G) {
+    cp_async_wait_all();
+    __syncthreads();
+    const unsigned char *m = metab + (k % 3) * mb;
+    const double *nb = nodeb + (k & 1) * nstride;
+    if (t + G < A.n_tiles) issue_nodes(metab + ((k + 1) % 3) * mb, nodeb + ((k + 1) & 1) * nstride);
+    if (t + 2 * G < A.n_tiles) issue_meta(t + 2 * G, metab + ((k + 2) % 3) * mb);
+    cp_async_commit();
+
+    const int U = reinterpret_cast<const int *>(m)[0];
+    const double *xs = nb, *us = nb + um * D, *vs = nb + (NF - 1) * um * D;
+    // phase 1: one element per thread
+    const int64_t e = t * kTile + tid;
+    if (e < A.E) {
+      const ushort4 lc4 = reinterpret_cast<const ushort4 *>(m + A.off_lconn)[tid];
+      const int lc[4] = {lc4.x, lc4.y, lc4.z, lc4.w};
+      double x[NEN][D], Gr[NEN][D], vol;
 #pragma unroll
-    for (int a = 0; a < D + 1; ++a)
+      for (int a = 0; a < NEN; ++a)
 #pragma unroll
-      for (int i = 0; i < D; ++i) x[a][i] = xs[lc[a] * D + i];
-    geometry<D>(x, G, vol);
-    double lam = A.lam, mu = A.mu;
-    if (A.T.phase) {
-      const int ph = A.T.phase[e];
-      lam = A.lam_tab[ph];
-      mu = A.mu_tab[ph];
-    }
-    double H[D][D];
-    if constexpr (NEED_U) {
-      double u[D + 1][D];
-#pragma unroll
-      for (int a = 0; a < D + 1; ++a)
-#pragma unroll
-        for (int i = 0; i < D; ++i) u[a][i] = us[lc[a] * D + i];
-      field_gradient<D>(u, G, H);
-    }
-    bool ok = true;
-    double S[D][D];
-    if constexpr (OP == OP_ENERGY) {
-      if constexpr (MAT == FEM_LINEAR_ELASTIC) {
-        acc = vol * le_psi<D>(H, lam, mu);
-      } else {
-        NHState<D> s;
-        ok = nh_state<D>(H, s);
-        if (ok) acc = vol * nh_psi<D>(H, s, lam, mu);
+        for (int i = 0; i < D; ++i) x[a][i] = xs[lc[a] * D + i];
+      geometry<D>(x, Gr, vol);
+      double lam = A.lam, mu = A.mu;
+      if (A.has_phase) {
+        const int ph = m[A.off_ph + tid];
+        lam = A.lam_tab[ph];
+        mu = A.mu_tab[ph];
       }
-    } else if constexpr (OP == OP_RESIDUAL) {
-      if constexpr (MAT == FEM_LINEAR_ELASTIC) {
-        le_stress<D>(H, lam, mu, S);
-      } else {
-        NHState<D> s;
-        ok = nh_state<D>(H, s);
-        if (ok) nh_stress<D>(s, lam, mu, S);
-      }
-    } else {
-      double v[D + 1][D], dH[D][D];
+      double H[D][D];
+      if constexpr (NEED_U) {
+        double u[NEN][D];
 #pragma unroll
-      for (int a = 0; a < D + 1; ++a)
+        for (int a = 0; a < NEN; ++a)
 #pragma unroll
-        for (int i = 0; i < D; ++i) v[a][i] = vs[lc[a] * D + i];
-      field_gradient<D>(v, G, dH);
-      if constexpr (MAT == FEM_LINEAR_ELASTIC) {
-        le_stress<D>(dH, lam, mu, S);
-      } else {
-        NHState<D> s;
-        ok = nh_state<D>(H, s);
-        if (ok) nh_dstress<D>(s, lam, mu, dH, S);
+          for (int i = 0; i < D; ++i) u[a][i] = us[lc[a] * D + i];
+        field_gradient<D>(u, Gr, H);
       }
-    }
-    if (!ok) {
-      atomicOr(A.err, ERRW_INVERTED);
-      acc = 0.0;
+      bool ok = true;
+      double S[D][D];
+      if constexpr (OP == OP_ENERGY) {
+        if constexpr (MAT == FEM_LINEAR_ELASTIC) {
+          eacc += vol * le_psi<D>(H, lam, mu);
+        } else {
+          NHState<D> s;
+          ok = nh_state<D>(H, s);
+          if (ok) eacc += vol * nh_psi<D>(H, s, lam, mu);
+        }
+      } else if constexpr (OP == OP_RESIDUAL) {
+        if constexpr (MAT == FEM_LINEAR_ELASTIC) {
+          le_stress<D>(H, lam, mu, S);
+        } else {
+          NHState<D> s;
+          ok = nh_state<D>(H, s);
+          if (ok) nh_stress<D>(s, lam, mu, S);
+        }
+      } else {
+        double v[NEN][D], dH[D][D];
+#pragma unroll
+        for (int a = 0; a < NEN; ++a) {
+          const unsigned bc = MASK ? m[A.off_bc + lc[a]] : 0u;
+#pragma unroll
+          for (int i = 0; i < D; ++i) v[a][i] = (bc & (1u << i)) ? 0.0 : vs[lc[a] * D + i];
+        }
+        field_gradient<D>(v, Gr, dH);
+        if constexpr (MAT == FEM_LINEAR_ELASTIC) {
+          le_stress<D>(dH, lam, mu, S);
+        } else {
+          NHState<D> s;
+          ok = nh_state<D>(H, s);
+          if (ok) nh_dstress<D>(s, lam, mu, dH, S);
+        }
+      }
+      if (!ok) atomicOr(A.err, ERRW_INVERTED);
+      if constexpr (OP != OP_ENERGY) {
+        double f[NEN][D];
+        nodal_from_stress<D>(S, Gr, vol, f);
+#pragma unroll
+        for (int a = 0; a < NEN; ++a)
+#pragma unroll
+          for (int i = 0; i < D; ++i) contrib[(a * D + i) * kTile + tid] = ok ? f[a][i] : 0.0;
+      }
     }
     if constexpr (OP != OP_ENERGY) {
-      double f[D + 1][D];
-      nodal_from_stress<D>(S, G, vol, f);
+      __syncthreads();
+      // phase 2: fixed-order per-tile-node sums
+      const uint16_t *ptr = reinterpret_cast<const uint16_t *>(m + A.off_ptr);
+      const uint16_t *inc = reinterpret_cast<const uint16_t *>(m + A.off_inc);
+      const int32_t *nodes = reinterpret_cast<const int32_t *>(m + A.off_nodes);
+      for (int r = tid; r < U; r += kTile) {
+        const int lo = ptr[r], hi = ptr[r + 1];
+        double sacc[D];
 #pragma unroll
-      for (int a = 0; a < D + 1; ++a)
+        for (int c = 0; c < D; ++c) sacc[c] = 0.0;
+        for (int q = lo; q < hi; ++q) {
+          const int pk = inc[q];
+          const int el = pk >> 2, a = pk & 3;
 #pragma unroll
-        for (int i = 0; i < D; ++i) contrib[(a * D + i) * kTile + tid] = ok ? f[a][i] : 0.0;
-    }
-  }
-  if constexpr (OP == OP_ENERGY) {
-    const double tsum = block_sum<kTile>(acc);
-    if (tid == 0) A.partials[t] = tsum;
-    return;
-  } else {
-    __syncthreads();
-    // phase 2: per tile node, fixed-order sum of its in-tile incidences
-    const uint16_t *ptr = A.T.ptr + (int64_t)t * (A.T.maxe + 1);
-    const uint16_t *inc = A.T.inc + toff;
-    for (int r = tid; r < U; r += kTile) {
-      const int lo = ptr[r], hi = ptr[r + 1];
-      double sacc[D];
+          for (int c = 0; c < D; ++c) sacc[c] += contrib[(a * D + c) * kTile + el];
+        }
+        if constexpr (DET) {
+          double *slot = A.slots + (A.slot_off[t] + r) * D;
 #pragma unroll
-      for (int c = 0; c < D; ++c) sacc[c] = 0.0;
-      for (int q = lo; q < hi; ++q) {
-        const int pk = inc[q];
-        const int el = pk >> 2, a = pk & 3;
-#pragma unroll
-        for (int c = 0; c < D; ++c) sacc[c] += contrib[(a * D + c) * kTile + el];
-      }
-      if constexpr (DET) {
-        double *slot = A.slots + (A.T.slot_off[t] + r) * D;
-#pragma unroll
-        for (int c = 0; c < D; ++c) slot[c] = sacc[c];
-      } else {
-        const int64_t g = (int64_t)tn[r] * D;
-        if (A.T.interior[toff + r]) {
-#pragma unroll
-          for (int c = 0; c < D; ++c) A.out[g + c] = sacc[c];
+          for (int c = 0; c < D; ++c) slot[c] = sacc[c];
         } else {
+          const int64_t g = (int64_t)nodes[r] * D;
+          if (m[A.off_int + r]) {
 #pragma unroll
-          for (int c = 0; c < D; ++c) atomicAdd(A.out + g + c, sacc[c]);
+            for (int c = 0; c < D; ++c) A.out[g + c] = sacc[c];
+          } else {
+#pragma unroll
+            for (int c = 0; c < D; ++c) atomicAdd(A.out + g + c, sacc[c]);
+          }
         }
       }
     }
+    __syncthreads();
+  }
+  if constexpr (OP == OP_ENERGY) {
+    const double tsum = block_sum<kTile>(eacc);
+    if (tid == 0) A.partials[blockIdx.x] = tsum;
   }
 }
 
@@ -489,72 +592,87 @@ __global__ void k_slot_gather(const int64_t *node_slot_ptr, const int32_t *node_
   }
 }
 
+// grid of the persistent kernels (fixed per problem: deterministic energy partial order)
+static int pipe_grid(Problem *p) {
+  return (int)std::min<int64_t>(p->tiles.n_tiles, 148 * FEM_PIPE_MINB * (256 / kTile));
+}
+
 template <int D, int MAT, int OP, bool MASK, bool DET>
-static fem_status launch_tile_t(Problem *p, const TileArgs &a, cudaStream_t s) {
-  const int U = p->tiles.max_U;
+static fem_status launch_pipe_t(Problem *p, const PipeArgs &a, cudaStream_t s) {
+  const TileSet &T = p->tiles;
   const bool need_u = (OP != OP_HVP) || (MAT == FEM_NEO_HOOKEAN);
-  size_t smem = sizeof(double) * ((size_t)U * D * (1 + (need_u ? 1 : 0) + (OP == OP_HVP ? 1 : 0)) +
-                                  (OP == OP_ENERGY ? 0 : (size_t)(D + 1) * D * kTile));
-  auto kern = k_tile_elem<D, MAT, OP, MASK, DET>;
-  if (smem > 48 * 1024) FEM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  kern<<<(unsigned)p->tiles.n_tiles, kTile, smem, s>>>(a);
-  FEM_LAUNCH_CHECK("tile element kernel");
+  const int nf = 1 + (need_u ? 1 : 0) + (OP == OP_HVP ? 1 : 0);
+  const size_t smem = (size_t)3 * T.mb + sizeof(double) * 2 * (size_t)T.um * D * nf +
+                      (OP == OP_ENERGY ? 0 : sizeof(double) * (size_t)(D + 1) * D * kTile);
+  auto kern = k_tile_pipe<D, MAT, OP, MASK, DET>;
+  FEM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  kern<<<pipe_grid(p), kTile, smem, s>>>(a);
+  FEM_LAUNCH_CHECK("tile pipeline kernel");
   return FEM_OK;
 }
 
 template <int OP, bool MASK, bool DET>
-static fem_status launch_tile_op(Problem *p, const TileArgs &a, cudaStream_t s) {
+static fem_status launch_pipe_op(Problem *p, const PipeArgs &a, cudaStream_t s) {
   if (p->dim == 2) {
-    if (p->material == FEM_LINEAR_ELASTIC) return launch_tile_t<2, FEM_LINEAR_ELASTIC, OP, MASK, DET>(p, a, s);
-    return launch_tile_t<2, FEM_NEO_HOOKEAN, OP, MASK, DET>(p, a, s);
+    if (p->material == FEM_LINEAR_ELASTIC) return launch_pipe_t<2, FEM_LINEAR_ELASTIC, OP, MASK, DET>(p, a, s);
+    return launch_pipe_t<2, FEM_NEO_HOOKEAN, OP, MASK, DET>(p, a, s);
   }
-  if (p->material == FEM_LINEAR_ELASTIC) return launch_tile_t<3, FEM_LINEAR_ELASTIC, OP, MASK, DET>(p, a, s);
-  return launch_tile_t<3, FEM_NEO_HOOKEAN, OP, MASK, DET>(p, a, s);
+  if (p->material == FEM_LINEAR_ELASTIC) return launch_pipe_t<3, FEM_LINEAR_ELASTIC, OP, MASK, DET>(p, a, s);
+  return launch_pipe_t<3, FEM_NEO_HOOKEAN, OP, MASK, DET>(p, a, s);
 }
 
 // Element pass of the residual / HVP (op = OP_RESIDUAL / OP_HVP) or the energy partials
-// (OP_ENERGY, one per tile into p->partials-compatible buffer `partials`).
+// (OP_ENERGY: one partial per CTA into `partials`, *n_partials set).
 fem_status tile_pass(Problem *p, int op, const double *u, const double *v, double *out,
                      bool mask, bool det, double *partials, cudaStream_t s) {
   fem_status st = build_tiles(p, s);
   if (st) return st;
   if (p->n_elems == 0) return FEM_OK;
-  TileArgs a{};
-  a.T = p->tiles;
-  a.coords = p->coords;
+  const TileSet &T = p->tiles;
+  PipeArgs a{};
+  a.meta = T.meta;
+  a.n_tiles = T.n_tiles;
   a.E = p->n_elems;
+  a.mb = T.mb; a.um = T.um; a.off_nodes = T.off_nodes; a.off_lconn = T.off_lconn;
+  a.off_ptr = T.off_ptr; a.off_inc = T.off_inc; a.off_int = T.off_int; a.off_bc = T.off_bc;
+  a.off_ph = T.off_ph;
+  a.has_phase = T.phase != nullptr;
+  a.slot_off = T.slot_off;
+  a.coords = p->coords;
+  a.u = u;
+  a.v = v;
   a.lam = p->lam;
   a.mu = p->mu;
   a.lam_tab = p->lam_tab;
   a.mu_tab = p->mu_tab;
-  a.node_bc = p->node_bc;
-  a.u = u;
-  a.v = v;
   a.out = out;
   a.partials = partials;
   a.err = p->d_err;
-  if (op == OP_ENERGY) return launch_tile_op<OP_ENERGY, false, false>(p, a, s);
+  if (op == OP_ENERGY) return launch_pipe_op<OP_ENERGY, false, false>(p, a, s);
   if (det) {
-    st = ensure(p->slotbuf, sizeof(double) * p->tiles.n_slots * p->dim);
+    st = ensure(p->slotbuf, sizeof(double) * T.n_slots * p->dim);
     if (st) return st;
     a.slots = (double *)p->slotbuf.ptr;
-    if (op == OP_RESIDUAL) st = launch_tile_op<OP_RESIDUAL, false, true>(p, a, s);
-    else st = mask ? launch_tile_op<OP_HVP, true, true>(p, a, s) : launch_tile_op<OP_HVP, false, true>(p, a, s);
+    if (op == OP_RESIDUAL) st = launch_pipe_op<OP_RESIDUAL, false, true>(p, a, s);
+    else st = mask ? launch_pipe_op<OP_HVP, true, true>(p, a, s) : launch_pipe_op<OP_HVP, false, true>(p, a, s);
     if (st) return st;
     if (p->dim == 2)
-      k_slot_gather<2><<<grid_for(p->n_nodes), kThreads, 0, s>>>(p->tiles.node_slot_ptr, p->tiles.node_slots, a.slots, p->n_nodes, out);
+      k_slot_gather<2><<<grid_for(p->n_nodes), kThreads, 0, s>>>(T.node_slot_ptr, T.node_slots, a.slots, p->n_nodes, out);
     else
-      k_slot_gather<3><<<grid_for(p->n_nodes), kThreads, 0, s>>>(p->tiles.node_slot_ptr, p->tiles.node_slots, a.slots, p->n_nodes, out);
+      k_slot_gather<3><<<grid_for(p->n_nodes), kThreads, 0, s>>>(T.node_slot_ptr, T.node_slots, a.slots, p->n_nodes, out);
     FEM_LAUNCH_CHECK("slot gather");
     return FEM_OK;
   }
-  if (op == OP_RESIDUAL) return launch_tile_op<OP_RESIDUAL, false, false>(p, a, s);
-  return mask ? launch_tile_op<OP_HVP, true, false>(p, a, s) : launch_tile_op<OP_HVP, false, false>(p, a, s);
+  if (op == OP_RESIDUAL) return launch_pipe_op<OP_RESIDUAL, false, false>(p, a, s);
+  return mask ? launch_pipe_op<OP_HVP, true, false>(p, a, s) : launch_pipe_op<OP_HVP, false, false>(p, a, s);
 }
+
+int tile_energy_partials(Problem *p) { return pipe_grid(p); }
+
 
 void free_tiles(TileSet &T) {
   void *bufs[] = {T.perm, T.nodes, T.U, T.ptr, T.inc, T.lconn, T.interior, T.phase, T.slot_off,
-                  T.node_slots, T.node_slot_ptr, T.epart};
+                  T.node_slots, T.node_slot_ptr, T.epart, T.meta};
   for (void *b : bufs)
     if (b) cudaFree(b);
   T = TileSet{};

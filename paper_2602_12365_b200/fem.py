@@ -24,7 +24,9 @@ LIB_PATH = os.path.join(_HERE, "libfem.so")
 APPLY_BC = 1
 DETERMINISTIC = 2
 ASSEMBLE_LITERAL = 4
+ASSEMBLE_JCOMP = 32
 BASELINE_SCATTER = 8
+LOCAL_ONLY = 16
 STATUS = {0: "OK", 1: "INVALID_ARG", 2: "DEGENERATE_ELEMENT", 3: "INVERTED_ELEMENT",
           4: "NONFINITE", 5: "CG_BREAKDOWN", 6: "NOT_CONVERGED", 7: "TOO_MANY_COLORS",
           8: "OUT_OF_MEMORY", 9: "CUDA", 10: "NCCL"}
@@ -34,7 +36,8 @@ EXPORTS = ("fem_create", "fem_destroy", "fem_query", "fem_check", "fem_apply_dir
            "fem_energy", "fem_residual", "fem_hvp", "fem_sparsity", "fem_color",
            "fem_assemble_csr", "fem_spmv", "fem_cg_solve", "fem_newton_solve",
            "fem_nccl_unique_id", "fem_nccl_comm_init", "fem_nccl_comm_destroy",
-           "fem_allreduce_sum", "fem_last_error", "fem_version")
+           "fem_allreduce_sum", "fem_halo_size", "fem_halo_pack", "fem_halo_combine",
+           "fem_last_error", "fem_version")
 
 
 class FemError(RuntimeError):
@@ -110,6 +113,9 @@ def load_library():
         lib.fem_nccl_comm_init.argtypes = [C.c_char_p, C.c_int, C.c_int, C.POINTER(vp)]
         lib.fem_nccl_comm_destroy.argtypes = [vp]
         lib.fem_allreduce_sum.argtypes = [vp, vp, C.c_int, vp]
+        lib.fem_halo_size.argtypes = [vp, i64p]
+        lib.fem_halo_pack.argtypes = [vp, vp, vp, vp]
+        lib.fem_halo_combine.argtypes = [vp, vp, vp, vp]
         lib.fem_last_error.restype = C.c_char_p
         lib.fem_version.restype = C.c_char_p
         _lib = lib
@@ -143,7 +149,9 @@ def _dev(x, dtype, device):
 class Problem:
     """fem_problem handle for a mesh (fem_inputs.Mesh or any object with its fields)."""
 
-    def __init__(self, mesh, device: str | torch.device = "cuda", dist: Optional[DistDesc] = None):
+    def __init__(self, mesh, device: str | torch.device = "cuda", plan=None, nccl_comm=None):
+        """plan: paper_2602_12365_b200.dist.HaloPlan for a multi-GPU rank (None = one GPU);
+        nccl_comm: handle from nccl_comm_init (None: only FEM_LOCAL_ONLY + halo pack/combine)."""
         lib = load_library()
         if not torch.cuda.is_available():
             raise RuntimeError("libfem needs a CUDA device (no CPU fallback)")
@@ -170,12 +178,21 @@ class Problem:
                         0 if self._lt is None else len(self._lt), int(keep["dd"].numel()),
                         _ptr(keep["dd"]), _ptr(keep["dv"]), int(keep["ms"].numel()),
                         _ptr(keep["ms"]), _ptr(keep["mm"]), _ptr(keep["mo"]), _ptr(keep["fe"]))
+        dist = None
+        if plan is not None and plan.size > 1:
+            self._plan_arrays = (np.ascontiguousarray(plan.nbr_rank, np.int32),
+                                 np.ascontiguousarray(plan.nbr_offset, np.int64),
+                                 np.ascontiguousarray(plan.nbr_nodes, np.int32),
+                                 np.ascontiguousarray(plan.owned, np.uint8))
+            nr, no, nn, ow = self._plan_arrays
+            dist = DistDesc(nccl_comm, plan.rank, plan.size, len(nr), nr.ctypes.data,
+                            no.ctypes.data, nn.ctypes.data if len(nn) else None, ow.ctypes.data)
         h = C.c_void_p()
         with torch.cuda.device(self.device):
             _check(lib.fem_create(C.byref(h), C.byref(desc), C.byref(dist) if dist else None,
                                   _stream()), "fem_create")
         self._h = h
-        self._dist = dist
+        self.plan = plan
         n = C.c_int64()
         lib.fem_query(h, C.byref(n), None, None)
         self.N = int(n.value)
@@ -257,10 +274,10 @@ class Problem:
         _check(load_library().fem_color(self._h, _ptr(colors), C.byref(nc), _stream()), "fem_color")
         return colors, nc.value
 
-    def assemble_csr(self, z, bc: bool = False, mode: str = "batched", out=None) -> torch.Tensor:
+    def assemble_csr(self, z, bc: bool = False, mode: str = "rows", out=None) -> torch.Tensor:
         z = self._vec(z, "z")
-        flags = (APPLY_BC if bc else 0) | {"batched": 0, "literal": ASSEMBLE_LITERAL,
-                                             "rows": DETERMINISTIC}[mode]
+        flags = (APPLY_BC if bc else 0) | {"batched": ASSEMBLE_JCOMP, "literal": ASSEMBLE_LITERAL,
+                                             "rows": 0}[mode]
         nnz = self.nnz()
         out = self._out(out, nnz)
         _check(load_library().fem_assemble_csr(self._h, _ptr(z), _ptr(out), flags, _stream()),
@@ -288,6 +305,22 @@ class Problem:
             _check(st, "fem_cg_solve")
         return x, info
 
+    # ---------------------------------------------------------------- multi-GPU halo
+    def halo_size(self) -> int:
+        n = C.c_int64()
+        _check(load_library().fem_halo_size(self._h, C.byref(n)), "fem_halo_size")
+        return n.value
+
+    def halo_pack(self, y: torch.Tensor, send: Optional[torch.Tensor] = None) -> torch.Tensor:
+        send = self._out(send, max(self.halo_size(), 1))
+        _check(load_library().fem_halo_pack(self._h, _ptr(y), _ptr(send), _stream()), "fem_halo_pack")
+        return send
+
+    def halo_combine(self, y: torch.Tensor, recv: torch.Tensor) -> torch.Tensor:
+        _check(load_library().fem_halo_combine(self._h, _ptr(y), _ptr(recv), _stream()),
+               "fem_halo_combine")
+        return y
+
     def newton_solve(self, z0, atol=1e-12, rtol=1e-10, max_iter=50, op=0, cg_rtol=1e-10,
                      cg_max_iter=100000, jacobi=False, check_every=1, raise_on_fail=True):
         z = self._vec(z0, "z0").clone()
@@ -299,3 +332,20 @@ class Problem:
         if raise_on_fail:
             _check(st, "fem_newton_solve")
         return z, info
+
+
+def nccl_unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    _check(load_library().fem_nccl_unique_id(buf), "fem_nccl_unique_id")
+    return buf.raw
+
+
+def nccl_comm_init(uid: bytes, rank: int, size: int):
+    comm = C.c_void_p()
+    _check(load_library().fem_nccl_comm_init(C.create_string_buffer(uid, 128), rank, size,
+                                             C.byref(comm)), "fem_nccl_comm_init")
+    return comm.value
+
+
+def nccl_comm_destroy(comm) -> None:
+    load_library().fem_nccl_comm_destroy(comm)

@@ -253,7 +253,7 @@ def test_full_size_sampled_parity(fem, oracle_mod, cfg):
     srow = sampled_rows(mesh.n_total, 300, 6)
     ref_vals = ref.csr_rows(z, srow, rp_n, ci_n, bc=True)
     idx = np.concatenate([np.arange(rp_n[r], rp_n[r + 1]) for r in srow])
-    for mode in ("batched", "rows"):
+    for mode in ("rows", "batched"):
         vals = prob.assemble_csr(zt, bc=True, mode=mode).cpu().numpy()
         assert np.abs(vals[idx] - ref_vals).max() <= TOL * np.abs(vals).max()
         del vals

@@ -196,9 +196,38 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     fbuild.build()
 
-    mesh, wname, z, v = workload(args.config, args.n)
+    comm = None
+    if world > 1:
+        # weak scaling: every rank owns one cfg-3-sized z-slab of a 150 x 150 x (150 N) block
+        # (N = 1 reproduces cfg 3 exactly); one halo add per residual / HVP / SpMV over NCCL
+        from paper_2602_12365_b200 import dist as fd
+        if args.config != 3:
+            raise SystemExit("multi-GPU bench runs the 3D cfg-3 slabs")
+        k = args.n or 150
+        mesh, gids = fd.slab_mesh(k, k, k, world, rank, perturb_a=0.1)
+        all_ids = [None] * world
+        dist.all_gather_object(all_ids, gids)
+        plan = fd.halo_plan(all_ids, rank)
+        del all_ids
+        uid = [fem.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        comm = fem.nccl_comm_init(uid[0], rank, world)
+        # states drawn per global node so shared DOFs agree on every rank
+        h = 1.0 / (k * world)
+        n_glob_nodes = (k + 1) * (k + 1) * (k * world + 1)
+        gz = np.random.default_rng(5).uniform(-0.01 * h, 0.01 * h, size=(n_glob_nodes, 3))
+        gv = np.random.default_rng(4).uniform(-1, 1, size=(n_glob_nodes, 3))
+        z = fi.lift(mesh, (fi.affine_field(mesh, np.diag([0.05, 0.0, 0.0])).reshape(-1, 3)
+                           + gz[gids]).ravel())
+        v = gv[gids].ravel()
+        del gz, gv
+        wname = (f"weak scaling: {world} z-slabs of 150^3 Kuhn-Tet4 cells (cfg 3 per GPU), "
+                 f"3D NH, perturbed a=0.1, roller eps=0.05, NCCL halo add")
+        prob = fem.Problem(mesh, plan=plan, nccl_comm=comm)
+    else:
+        mesh, wname, z, v = workload(args.config, args.n)
+        prob = fem.Problem(mesh)
     N = mesh.n_total
-    prob = fem.Problem(mesh)
     zt = torch.as_tensor(z, device="cuda")
     vt = torch.as_tensor(v, device="cuda")
     stream = torch.cuda.current_stream()
@@ -278,7 +307,7 @@ def main():
         total_ms = float(t[0])
         per = {p: float(t[i + 1]) for i, p in enumerate(phases)}
     K = args.steps
-    n_global = N * world
+    n_global = N if world == 1 else 3 * (k + 1) * (k + 1) * (k * world + 1)
     hvp_ms = per["hvp"] / K
     value = n_global / (hvp_ms * 1e-3) / 1e9
 
@@ -436,6 +465,10 @@ def main():
     }
     if rank == 0:
         print(json.dumps(out))
+    if comm is not None:
+        del prob
+        torch.cuda.synchronize()
+        fem.nccl_comm_destroy(comm)
     if world > 1:
         dist.destroy_process_group()
 

@@ -230,7 +230,7 @@ __global__ void k_decompress(const int64_t *row_ptr, const int32_t *col_idx, con
 // color -> CSR slot map is a bijection).  No atomics, bitwise reproducible, each value
 // written once.  slot lists: per node, entries (l << 2 | b) grouped by slot (setup).
 #ifndef FEM_ROWS_MINB
-#define FEM_ROWS_MINB 5
+#define FEM_ROWS_MINB 4
 #endif
 constexpr int kRowLanes = 32;
 constexpr int kRowGroups = 4;  // warps (nodes) per 128-thread CTA
@@ -252,6 +252,7 @@ struct RowArgs {
   const int32_t *dmpc_ptr, *dmpc, *ms, *mm;
   const int64_t *row_ptr;
   int64_t n_nodes, n_u;
+  int dim;
   double *vals;
   int *err;
 };
@@ -291,27 +292,46 @@ __global__ void k_slot_build(const int64_t *inc_ptr, const int32_t *inc, const i
   }
 }
 
+__device__ __forceinline__ int64_t rp_row(const RowArgs &A, int64_t n, int i) {
+  return __ldg(A.row_ptr + n * (int64_t)A.dim + i);
+}
+
 template <int D, int MAT>
 __global__ void __launch_bounds__(kRowLanes * kRowGroups, FEM_ROWS_MINB) k_rows_fused(RowArgs A) {
-  constexpr int NEN = D + 1, BS = D * D;
+  constexpr int NEN = D + 1, BS = D * D, SPL = kRowLanes / BS;  // slots per pass
   __shared__ double stage[kRowGroups][kRowLanes][NEN * BS + 1];  // +1: no bank conflicts
   __shared__ uint8_t s_list[kRowGroups][NEN * 64];                // node's slot list
   __shared__ uint16_t s_off[kRowGroups][2 * kRowLanes + 1];       // its slot offsets
+  const unsigned FULL = 0xffffffffu;
   const int lane = threadIdx.x % kRowLanes, g = threadIdx.x / kRowLanes;
+  // this lane's output in a pass over SPL slots: (slot offset, entry i*D+k)
+  const int my_s = lane / BS, my_ik = lane - my_s * BS, my_i = my_ik / D, my_k = my_ik - my_i * D;
+  const bool writer = lane < SPL * BS;
   for (int64_t n = (int64_t)blockIdx.x * kRowGroups + g; n < A.n_nodes;
        n += (int64_t)gridDim.x * kRowGroups) {
     const int64_t i0 = A.inc_ptr[n];
     const int deg = (int)(A.inc_ptr[n + 1] - i0);
     const int64_t a0 = A.nadj_ptr[n];
     const int sn = (int)(A.nadj_ptr[n + 1] - a0);
+    if (deg == 0) continue;
     const unsigned bcn = A.node_bc ? A.node_bc[n] : 0u;
-    // stage the node's slot metadata in shared memory (coalesced), read in the sums below
     for (int q = lane; q < NEN * deg; q += kRowLanes) s_list[g][q] = A.slot_list[NEN * i0 + q];
     for (int q = lane; q <= sn; q += kRowLanes) s_off[g][q] = A.slot_off[a0 + n + q];
+    int ds = 0;  // slot of the diagonal block (node n itself)
+    for (int base = 0; base < sn; base += kRowLanes) {
+      const unsigned hit = __ballot_sync(FULL, base + lane < sn && A.nadj[a0 + base + lane] == n);
+      if (hit) { ds = base + __ffs(hit) - 1; break; }
+    }
+    const int64_t rp_lane = lane < D ? A.row_ptr[n * D + lane] : 0;
+    const int64_t rp_my = __shfl_sync(FULL, rp_lane, my_i);
     const uint8_t *sl = s_list[g];
     const uint16_t *so = s_off[g];
+    double dsum = 0.0;  // diagonal-block entry my_ik, summed over all incident elements
     for (int l0 = 0; l0 < deg; l0 += kRowLanes) {
       const int l = l0 + lane;
+      double diag[BS];
+#pragma unroll
+      for (int q = 0; q < BS; ++q) diag[q] = 0.0;
       if (l < deg) {
         const int32_t packed = A.inc[i0 + l];
         const int64_t e = packed / NEN;
@@ -349,31 +369,63 @@ __global__ void __launch_bounds__(kRowLanes * kRowGroups, FEM_ROWS_MINB) k_rows_
             double kab[D];
             column_block_row<D>(cx, Ga, ga, b, k, kab);
 #pragma unroll
-            for (int i = 0; i < D; ++i) stage[g][lane][b * BS + i * D + k] = ok ? kab[i] : 0.0;
+            for (int i = 0; i < D; ++i) {
+              const double val = ok ? kab[i] : 0.0;
+              if (b == a) diag[i * D + k] = val;                        // K_aa: warp-reduced
+              else stage[g][lane][b * BS + i * D + k] = val;            // K_ab: slot lists
+            }
           }
       }
+      // diagonal block: butterfly sum over the lanes (fixed order, identical on all lanes)
+#pragma unroll
+      for (int q = 0; q < BS; ++q) {
+        double v = diag[q];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
+        if (q == my_ik) dsum += v;
+      }
       __syncwarp();
+      // off-diagonal blocks: lane s owns slot s (all BS entries, in registers) and sums
+      // its slot list in order; partial sums of earlier chunks live in the output itself
       const bool first = (l0 == 0), last = (l0 + kRowLanes >= deg);
-      // the sn*D*D outputs (slot s, entry i*D+k) are spread round-robin over the lanes so the
-      // diagonal slot's long list (every incident element) does not serialise the warp;
-      // partial sums of earlier chunks live in the output itself (same lane, no race)
-      for (int q = lane; q < sn * BS; q += kRowLanes) {
-        const int s = q / BS, ik = q - s * BS, i = ik / D, k = ik - i * D;
-        const int64_t pos = A.row_ptr[n * D + i] + (int64_t)s * D + k;
-        double acc = first ? 0.0 : A.vals[pos];
+      for (int s = lane; s < sn; s += kRowLanes) {
+        if (s == ds) continue;
+        double acc[BS];
+#pragma unroll
+        for (int q = 0; q < BS; ++q) acc[q] = 0.0;
+        if (!first) {
+#pragma unroll
+          for (int q = 0; q < BS; ++q) acc[q] = A.vals[rp_row(A, n, q / D) + (int64_t)s * D + q % D];
+        }
         for (int c = so[s]; c < so[s + 1]; ++c) {
           const int ent = sl[c];
           const int le = (ent >> 2) - l0;
-          if (le >= 0 && le < kRowLanes) acc += stage[g][le][(ent & 3) * BS + ik];
+          if (le < 0 || le >= kRowLanes) continue;
+          const double *st = &stage[g][le][(ent & 3) * BS];
+#pragma unroll
+          for (int q = 0; q < BS; ++q) acc[q] += st[q];
         }
-        if (last) {
-          const int32_t m = A.nadj[a0 + s];
-          if (A.node_bc && (A.node_bc[m] & (1u << k))) acc = 0.0;            // masked column
-          if (bcn & (1u << i)) acc = (m == n && k == i) ? 1.0 : 0.0;          // identity row
+        const int32_t m = A.nadj[a0 + s];
+        const unsigned bcm = (last && A.node_bc) ? A.node_bc[m] : 0u;
+#pragma unroll
+        for (int i = 0; i < D; ++i) {
+          const int64_t base = rp_row(A, n, i) + (int64_t)s * D;
+#pragma unroll
+          for (int k = 0; k < D; ++k) {
+            double v = acc[i * D + k];
+            if (last && ((bcm >> k) & 1u)) v = 0.0;     // masked column
+            if (last && ((bcn >> i) & 1u)) v = 0.0;     // identity row (off-diagonal)
+            A.vals[base + k] = v;
+          }
         }
-        A.vals[pos] = acc;
       }
       __syncwarp();
+    }
+    if (lane < BS) {  // diagonal block
+      double v = dsum;
+      if (bcn & (1u << my_k)) v = 0.0;                                    // masked column
+      if (bcn & (1u << my_i)) v = (my_k == my_i) ? 1.0 : 0.0;             // identity row
+      A.vals[rp_my + (int64_t)ds * D + my_k] = v;
     }
     if (A.dmpc_ptr && lane < D) {  // B^T entries of row (n, lane), ascending constraint id
       const int64_t r = n * D + lane;
@@ -447,6 +499,7 @@ static fem_status assemble(Problem *p, const double *z, double *vals, unsigned f
     A.slot_list = p->slot_list; A.slot_off = p->slot_off;
     A.dmpc_ptr = p->dmpc_ptr; A.dmpc = p->dmpc; A.ms = p->mpc_s; A.mm = p->mpc_m;
     A.row_ptr = p->row_ptr; A.n_nodes = p->n_nodes; A.n_u = p->n_u; A.vals = vals; A.err = p->d_err;
+    A.dim = p->dim;
     const int grid = grid_for(p->n_nodes, kRowGroups, 148 * 64);
     if (p->dim == 2) {
       if (p->material == FEM_LINEAR_ELASTIC) k_rows_fused<2, FEM_LINEAR_ELASTIC><<<grid, kRowLanes * kRowGroups, 0, s>>>(A);

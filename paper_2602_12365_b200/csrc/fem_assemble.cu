@@ -220,6 +220,96 @@ __global__ void k_decompress(const int64_t *row_ptr, const int32_t *col_idx, con
   }
 }
 
+__device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+
+// ------------------------------------------------------------------ per-element tangent context
+// k_elem_ctx evaluates, once per element and in the caller's element order, everything the
+// element Hessian needs (the ColumnCtx above): G_1..G_d, g_1..g_d (G_0, g_0 = -sum) and the
+// scalars vol*mu, vol*c1, vol*c2, stored as one 16-byte aligned record.  The row-pull
+// assembly then reads these records instead of re-gathering coordinates and state and
+// re-evaluating F, F^-1 and ln J for each of the element's nodes.
+template <int D>
+constexpr int ctx_stride() { return D == 3 ? 22 : 12; }
+
+template <int D>
+struct CtxLite {
+  double G[D + 1][D], g[D + 1][D], smu, sc1, sc2;
+};
+
+template <int D>
+__device__ __forceinline__ void load_ctx(const double *ctx, int64_t e, CtxLite<D> &c) {
+  constexpr int ST = ctx_stride<D>();
+  const double2 *p = reinterpret_cast<const double2 *>(ctx + e * ST);
+  double v[ST];
+#pragma unroll
+  for (int q = 0; q < ST / 2; ++q) {
+    const double2 t = p[q];
+    v[2 * q] = t.x;
+    v[2 * q + 1] = t.y;
+  }
+#pragma unroll
+  for (int j = 0; j < D; ++j) {
+    c.G[0][j] = 0.0;
+    c.g[0][j] = 0.0;
+  }
+#pragma unroll
+  for (int a = 1; a < D + 1; ++a)
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
+      c.G[a][j] = v[(a - 1) * D + j];
+      c.g[a][j] = v[D * D + (a - 1) * D + j];
+      c.G[0][j] -= c.G[a][j];
+      c.g[0][j] -= c.g[a][j];
+    }
+  c.smu = v[2 * D * D];
+  c.sc1 = v[2 * D * D + 1];
+  c.sc2 = v[2 * D * D + 2];
+}
+
+template <int D, int MAT>
+__global__ void __launch_bounds__(kThreads) k_elem_ctx(const double *coords, const int32_t *conn,
+                                                      int64_t E, double lam0, double mu0,
+                                                      const uint8_t *phase, const double *lam_tab,
+                                                      const double *mu_tab, const double *z,
+                                                      double *ctx, int *err) {
+  constexpr int ST = ctx_stride<D>();
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < E;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    int32_t nd[D + 1];
+    load_nodes<D>(conn, e, nd);
+    double lam = lam0, mu = mu0;
+    if (phase) {
+      const int ph = phase[e];
+      lam = lam_tab[ph];
+      mu = mu_tab[ph];
+    }
+    ColumnCtx<D> cx;
+    const bool ok = column_ctx<D, MAT>(coords, nd, z, lam, mu, cx);
+    if (!ok) atomicOr(err, ERRW_INVERTED);
+    double v[ST];
+#pragma unroll
+    for (int a = 1; a < D + 1; ++a)
+#pragma unroll
+      for (int j = 0; j < D; ++j) {
+        v[(a - 1) * D + j] = ok ? cx.G[a][j] : 0.0;
+        v[D * D + (a - 1) * D + j] = ok ? cx.g[a][j] : 0.0;
+      }
+    v[2 * D * D] = ok ? cx.vol * cx.mu : 0.0;
+    v[2 * D * D + 1] = ok ? cx.vol * cx.c1 : 0.0;
+    v[2 * D * D + 2] = ok ? cx.vol * cx.c2 : 0.0;
+#pragma unroll
+    for (int q = 2 * D * D + 3; q < ST; ++q) v[q] = 0.0;
+    double2 *o = reinterpret_cast<double2 *>(ctx + e * ST);
+#pragma unroll
+    for (int q = 0; q < ST / 2; ++q) o[q] = make_double2(v[2 * q], v[2 * q + 1]);
+  }
+}
+
 // ------------------------------------------------------------------ fused row-pull (deterministic)
 // One warp per node n (32 lanes).  Lane l takes the l-th incident element of n (ascending
 // element order), evaluates that element's column context once and its block row
@@ -251,6 +341,8 @@ struct RowArgs {
   const uint16_t *slot_off;
   const int32_t *dmpc_ptr, *dmpc, *ms, *mm;
   const int64_t *row_ptr;
+  const double *ctx;
+  const int32_t *node_order;
   int64_t n_nodes, n_u;
   int dim;
   double *vals;
@@ -296,19 +388,19 @@ __device__ __forceinline__ int64_t rp_row(const RowArgs &A, int64_t n, int i) {
   return __ldg(A.row_ptr + n * (int64_t)A.dim + i);
 }
 
-template <int D, int MAT>
+template <int D>
 __global__ void __launch_bounds__(kRowLanes * kRowGroups, FEM_ROWS_MINB) k_rows_fused(RowArgs A) {
-  constexpr int NEN = D + 1, BS = D * D, SPL = kRowLanes / BS;  // slots per pass
-  __shared__ double stage[kRowGroups][kRowLanes][NEN * BS + 1];  // +1: no bank conflicts
-  __shared__ uint8_t s_list[kRowGroups][NEN * 64];                // node's slot list
-  __shared__ uint16_t s_off[kRowGroups][2 * kRowLanes + 1];       // its slot offsets
+  constexpr int NEN = D + 1, BS = D * D;
+  __shared__ __align__(16) double stage[kRowGroups][kRowLanes][NEN * BS + 1];  // +1: no bank conflicts
+  __shared__ uint8_t s_list[kRowGroups][NEN * 64];                              // node's slot list
+  __shared__ uint16_t s_off[kRowGroups][2 * kRowLanes + 1];                     // its slot offsets
   const unsigned FULL = 0xffffffffu;
   const int lane = threadIdx.x % kRowLanes, g = threadIdx.x / kRowLanes;
-  // this lane's output in a pass over SPL slots: (slot offset, entry i*D+k)
-  const int my_s = lane / BS, my_ik = lane - my_s * BS, my_i = my_ik / D, my_k = my_ik - my_i * D;
-  const bool writer = lane < SPL * BS;
-  for (int64_t n = (int64_t)blockIdx.x * kRowGroups + g; n < A.n_nodes;
-       n += (int64_t)gridDim.x * kRowGroups) {
+  const int my_i = (lane % BS) / D, my_k = lane % D;  // diagonal entry of lanes < BS
+  for (int64_t idx = (int64_t)blockIdx.x * kRowGroups + g; idx < A.n_nodes;
+       idx += (int64_t)gridDim.x * kRowGroups) {
+    // nodes in Morton order: the readers of each element context run close together in time
+    const int64_t n = A.node_order ? A.node_order[idx] : idx;
     const int64_t i0 = A.inc_ptr[n];
     const int deg = (int)(A.inc_ptr[n + 1] - i0);
     const int64_t a0 = A.nadj_ptr[n];
@@ -326,7 +418,7 @@ __global__ void __launch_bounds__(kRowLanes * kRowGroups, FEM_ROWS_MINB) k_rows_
     const int64_t rp_my = __shfl_sync(FULL, rp_lane, my_i);
     const uint8_t *sl = s_list[g];
     const uint16_t *so = s_off[g];
-    double dsum = 0.0;  // diagonal-block entry my_ik, summed over all incident elements
+    double dsum = 0.0;  // diagonal-block entry (lanes < BS), summed over all incident elements
     for (int l0 = 0; l0 < deg; l0 += kRowLanes) {
       const int l = l0 + lane;
       double diag[BS];
@@ -334,19 +426,9 @@ __global__ void __launch_bounds__(kRowLanes * kRowGroups, FEM_ROWS_MINB) k_rows_
       for (int q = 0; q < BS; ++q) diag[q] = 0.0;
       if (l < deg) {
         const int32_t packed = A.inc[i0 + l];
-        const int64_t e = packed / NEN;
         const int a = packed % NEN;
-        int32_t nd[NEN];
-        load_nodes<D>(A.conn, e, nd);
-        double lam = A.lam, mu = A.mu;
-        if (A.phase) {
-          const int ph = A.phase[e];
-          lam = A.lam_tab[ph];
-          mu = A.mu_tab[ph];
-        }
-        ColumnCtx<D> cx;
-        const bool ok = column_ctx<D, MAT>(A.coords, nd, A.z, lam, mu, cx);
-        if (!ok) atomicOr(A.err, ERRW_INVERTED);
+        CtxLite<D> cx;
+        load_ctx<D>(A.ctx, packed / NEN, cx);
         double Ga[D], ga[D];
 #pragma unroll
         for (int j = 0; j < D; ++j) {
@@ -363,18 +445,22 @@ __global__ void __launch_bounds__(kRowLanes * kRowGroups, FEM_ROWS_MINB) k_rows_
             }
           }
 #pragma unroll
-        for (int b = 0; b < NEN; ++b)
+        for (int b = 0; b < NEN; ++b) {
+          double GG = 0.0;
+#pragma unroll
+          for (int j = 0; j < D; ++j) GG = fma(Ga[j], cx.G[b][j], GG);
 #pragma unroll
           for (int k = 0; k < D; ++k) {
-            double kab[D];
-            column_block_row<D>(cx, Ga, ga, b, k, kab);
+            const double ak = cx.sc1 * ga[k], bk = cx.sc2 * cx.g[b][k];
 #pragma unroll
             for (int i = 0; i < D; ++i) {
-              const double val = ok ? kab[i] : 0.0;
-              if (b == a) diag[i * D + k] = val;                        // K_aa: warp-reduced
-              else stage[g][lane][b * BS + i * D + k] = val;            // K_ab: slot lists
+              double t = fma(ak, cx.g[b][i], bk * ga[i]);
+              if (i == k) t = fma(cx.smu, GG, t);
+              if (b == a) diag[i * D + k] = t;                      // K_aa: warp-reduced
+              else stage[g][lane][b * BS + i * D + k] = t;          // K_ab: slot lists
             }
           }
+        }
       }
       // diagonal block: butterfly sum over the lanes (fixed order, identical on all lanes)
 #pragma unroll
@@ -382,7 +468,7 @@ __global__ void __launch_bounds__(kRowLanes * kRowGroups, FEM_ROWS_MINB) k_rows_
         double v = diag[q];
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
-        if (q == my_ik) dsum += v;
+        if (q == lane) dsum += v;
       }
       __syncwarp();
       // off-diagonal blocks: lane s owns slot s (all BS entries, in registers) and sums
@@ -461,6 +547,8 @@ __global__ void k_rows_mpc(const int32_t *ms, const int32_t *mm, int64_t nc, int
   }
 }
 
+fem_status morton_node_order(Problem *p, cudaStream_t s);
+
 static fem_status build_slot_lists(Problem *p, cudaStream_t s) {
   if (p->slot_list || p->n_nodes == 0) return FEM_OK;
   const int64_t nent = p->n_elems * p->nen * p->nen;
@@ -475,6 +563,8 @@ static fem_status build_slot_lists(Problem *p, cudaStream_t s) {
   else
     k_slot_build<3><<<grid_for(p->n_nodes, 128), 128, 0, s>>>(p->inc_ptr, p->inc, p->conn, p->nadj_ptr, p->nadj, p->n_nodes, p->slot_list, p->slot_off, p->d_err);
   FEM_LAUNCH_CHECK("slot lists");
+  fem_status st = morton_node_order(p, s);
+  if (st) return st;
   return read_error_word(p, s);
 }
 
@@ -496,18 +586,29 @@ static fem_status assemble(Problem *p, const double *z, double *vals, unsigned f
     A.phase = p->phase; A.lam_tab = p->lam_tab; A.mu_tab = p->mu_tab;
     A.node_bc = bc ? p->node_bc : nullptr; A.z = z;
     A.inc_ptr = p->inc_ptr; A.inc = p->inc; A.nadj_ptr = p->nadj_ptr; A.nadj = p->nadj;
-    A.slot_list = p->slot_list; A.slot_off = p->slot_off;
+    A.slot_list = p->slot_list; A.slot_off = p->slot_off; A.node_order = p->node_order;
     A.dmpc_ptr = p->dmpc_ptr; A.dmpc = p->dmpc; A.ms = p->mpc_s; A.mm = p->mpc_m;
     A.row_ptr = p->row_ptr; A.n_nodes = p->n_nodes; A.n_u = p->n_u; A.vals = vals; A.err = p->d_err;
     A.dim = p->dim;
-    const int grid = grid_for(p->n_nodes, kRowGroups, 148 * 64);
-    if (p->dim == 2) {
-      if (p->material == FEM_LINEAR_ELASTIC) k_rows_fused<2, FEM_LINEAR_ELASTIC><<<grid, kRowLanes * kRowGroups, 0, s>>>(A);
-      else k_rows_fused<2, FEM_NEO_HOOKEAN><<<grid, kRowLanes * kRowGroups, 0, s>>>(A);
-    } else {
-      if (p->material == FEM_LINEAR_ELASTIC) k_rows_fused<3, FEM_LINEAR_ELASTIC><<<grid, kRowLanes * kRowGroups, 0, s>>>(A);
-      else k_rows_fused<3, FEM_NEO_HOOKEAN><<<grid, kRowLanes * kRowGroups, 0, s>>>(A);
+    // per-element tangent context, then the row-pull
+    const int st_ctx = p->dim == 3 ? ctx_stride<3>() : ctx_stride<2>();
+    fem_status stc = ensure(p->ctxbuf, sizeof(double) * (size_t)st_ctx * (p->n_elems > 0 ? p->n_elems : 1));
+    if (stc) return stc;
+    A.ctx = (const double *)p->ctxbuf.ptr;
+    if (p->n_elems) {
+      const int ge = grid_for(p->n_elems);
+      double *ctx = (double *)p->ctxbuf.ptr;
+      if (p->dim == 2) {
+        if (p->material == FEM_LINEAR_ELASTIC) k_elem_ctx<2, FEM_LINEAR_ELASTIC><<<ge, kThreads, 0, s>>>(p->coords, p->conn, p->n_elems, p->lam, p->mu, p->phase, p->lam_tab, p->mu_tab, z, ctx, p->d_err);
+        else k_elem_ctx<2, FEM_NEO_HOOKEAN><<<ge, kThreads, 0, s>>>(p->coords, p->conn, p->n_elems, p->lam, p->mu, p->phase, p->lam_tab, p->mu_tab, z, ctx, p->d_err);
+      } else {
+        if (p->material == FEM_LINEAR_ELASTIC) k_elem_ctx<3, FEM_LINEAR_ELASTIC><<<ge, kThreads, 0, s>>>(p->coords, p->conn, p->n_elems, p->lam, p->mu, p->phase, p->lam_tab, p->mu_tab, z, ctx, p->d_err);
+        else k_elem_ctx<3, FEM_NEO_HOOKEAN><<<ge, kThreads, 0, s>>>(p->coords, p->conn, p->n_elems, p->lam, p->mu, p->phase, p->lam_tab, p->mu_tab, z, ctx, p->d_err);
+      }
     }
+    const int grid = grid_for(p->n_nodes, kRowGroups, 148 * 64);
+    if (p->dim == 2) k_rows_fused<2><<<grid, kRowLanes * kRowGroups, 0, s>>>(A);
+    else k_rows_fused<3><<<grid, kRowLanes * kRowGroups, 0, s>>>(A);
     if (p->n_mpc)
       k_rows_mpc<<<grid_for(p->n_mpc), kThreads, 0, s>>>(p->mpc_s, p->mpc_m, p->n_mpc, p->n_u, p->dim,
                                                          bc ? p->node_bc : nullptr, p->row_ptr, vals);

@@ -93,12 +93,13 @@ struct Problem {
   int64_t *diag_pos = nullptr;  // [N] position of the diagonal in each row (-1 if absent)
   uint8_t *slot_list = nullptr; // fused assembly: per node (l << 2 | b) grouped by CSR slot
   uint16_t *slot_off = nullptr; // [nnz_node + n_nodes] slot offsets into each node's list
+  int32_t *node_order = nullptr; // [n_nodes] Morton order of the nodes (assembly)
   // coloring
   bool have_colors = false;
   int32_t n_colors = -1;
   int32_t *colors = nullptr;    // [N]
   // workspaces
-  Workspace jcomp, cgbuf, tmp, slotbuf;
+  Workspace jcomp, cgbuf, tmp, slotbuf, ctxbuf;
   TileSet tiles;
   // multi-GPU (fem_dist.cu)
   void *nccl = nullptr;

@@ -670,6 +670,60 @@ fem_status tile_pass(Problem *p, int op, const double *u, const double *v, doubl
 int tile_energy_partials(Problem *p) { return pipe_grid(p); }
 
 
+template <int D>
+__global__ void k_node_morton(const double *coords, int64_t n, double3 lo, double3 scale,
+                              uint64_t *keys, int32_t *idx) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const double l[3] = {lo.x, lo.y, lo.z}, sc[3] = {scale.x, scale.y, scale.z};
+    uint64_t q[3] = {0, 0, 0};
+    for (int c = 0; c < D; ++c) q[c] = (uint64_t)fmax(0.0, (coords[i * D + c] - l[c]) * sc[c]);
+    keys[i] = (D == 3) ? (spread3(q[0]) | spread3(q[1]) << 1 | spread3(q[2]) << 2)
+                       : (spread2(q[0]) | spread2(q[1]) << 1);
+    idx[i] = (int32_t)i;
+  }
+}
+
+// Morton order of the nodes (assembly row order), stable sort of centroid-free keys.
+fem_status morton_node_order(Problem *p, cudaStream_t s) {
+  if (p->node_order || p->n_nodes == 0) return FEM_OK;
+  const int D = p->dim;
+  const int nb = grid_for(p->n_nodes, kThreads, 256);
+  double *part = nullptr;
+  FEM_CUDA(cudaMalloc(&part, sizeof(double) * nb * 6));
+  k_bbox_partial<<<nb, kThreads, 0, s>>>(p->coords, p->n_nodes, D, part);
+  std::vector<double> hp(nb * 6);
+  FEM_CUDA(cudaMemcpyAsync(hp.data(), part, sizeof(double) * nb * 6, cudaMemcpyDeviceToHost, s));
+  FEM_CUDA(cudaStreamSynchronize(s));
+  cudaFree(part);
+  double lo[3] = {1e300, 1e300, 1e300}, hi[3] = {-1e300, -1e300, -1e300};
+  for (int b = 0; b < nb; ++b)
+    for (int c = 0; c < 3; ++c) {
+      lo[c] = std::min(lo[c], hp[b * 6 + c]);
+      hi[c] = std::max(hi[c], hp[b * 6 + 3 + c]);
+    }
+  const double qmax = (D == 3) ? double((1 << 21) - 1) : double((1u << 31) - 1);
+  double sc[3];
+  for (int c = 0; c < 3; ++c) sc[c] = (c < D && hi[c] > lo[c]) ? qmax / (hi[c] - lo[c]) : 0.0;
+  uint64_t *keys = nullptr, *keys_out = nullptr;
+  int32_t *idx = nullptr;
+  FEM_CUDA(cudaMalloc(&keys, sizeof(uint64_t) * p->n_nodes));
+  FEM_CUDA(cudaMalloc(&keys_out, sizeof(uint64_t) * p->n_nodes));
+  FEM_CUDA(cudaMalloc(&idx, sizeof(int32_t) * p->n_nodes));
+  FEM_CUDA(cudaMalloc(&p->node_order, sizeof(int32_t) * p->n_nodes));
+  const double3 dlo = make_double3(lo[0], lo[1], lo[2]), dsc = make_double3(sc[0], sc[1], sc[2]);
+  if (D == 3) k_node_morton<3><<<grid_for(p->n_nodes), kThreads, 0, s>>>(p->coords, p->n_nodes, dlo, dsc, keys, idx);
+  else k_node_morton<2><<<grid_for(p->n_nodes), kThreads, 0, s>>>(p->coords, p->n_nodes, dlo, dsc, keys, idx);
+  size_t bytes = 0;
+  FEM_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, keys, keys_out, idx, p->node_order, (int)p->n_nodes, 0, 64, s));
+  fem_status st = ensure(p->tmp, bytes);
+  if (st) return st;
+  FEM_CUDA(cub::DeviceRadixSort::SortPairs(p->tmp.ptr, bytes, keys, keys_out, idx, p->node_order, (int)p->n_nodes, 0, 64, s));
+  FEM_CUDA(cudaStreamSynchronize(s));
+  cudaFree(keys); cudaFree(keys_out); cudaFree(idx);
+  return FEM_OK;
+}
+
 void free_tiles(TileSet &T) {
   void *bufs[] = {T.perm, T.nodes, T.U, T.ptr, T.inc, T.lconn, T.interior, T.phase, T.slot_off,
                   T.node_slots, T.node_slot_ptr, T.epart, T.meta};

@@ -163,19 +163,31 @@ def workload_name(cfg):
 # ------------------------------------------------------------------ B200 arm
 # Algorithmic bytes per DOF (compulsory traffic, geometry recomputed from
 # coordinates; 3D Kuhn: 2 tets/DOF, 1/3 node/DOF) and FP64 flops per element.
-def algorithmic(mesh, nnz, C):
+# FP64 flops per element of the minimal formulations (FMA = 2; SURVEY §8(d2) counting
+# scalar, geometry recomputed): energy / residual / HVP; assembly = per-element tangent
+# context (~ residual + spatial gradients) + the (d+1)^2 blocks K_ab (d^2 entries, 6 flops
+# each, plus the G_a.G_b dot) — DESIGN.md §5.
+FLOPS = {(3, 1): (189, 266, 457), (3, 0): (156, 204, 258), (2, 1): (59, 79, 141), (2, 0): (54, 64, 80)}
+
+
+def algorithmic(mesh, nnz, C, mode):
     N, E, d = mesh.n_total, mesh.n_elems, mesh.dim
     nen = d + 1
     conn = 4 * nen * E
     coords = 8 * d * mesh.n_nodes
     vec = 8 * N
+    fe, fr, fh = FLOPS[(d, mesh.material)]
+    f_ctx = fr + 2 * d * d * nen
+    f_blocks = nen * nen * (2 * d + 6 * d * d)
+    asm_bytes = conn + coords + vec + 8 * nnz                          # inputs + vals written once
+    if mode != "rows":                                                 # J_comp written + read
+        asm_bytes += 2 * 8 * N * C + nnz * (4 + 4)
     return {
-        "energy": {"bytes": conn + coords + vec},
-        "residual": {"bytes": conn + coords + vec + 2 * vec},          # u read, r zero + write
-        "hvp": {"bytes": conn + coords + 2 * vec + 2 * vec},           # u, v read, y zero + write
-        "assemble": {"bytes": conn + coords + vec + 8 * N * C          # J_comp written once
-                     + nnz * (8 + 4 + 4) + 8 * (N + 1) + 8 * nnz},     # decompress + vals write
-        "spmv": {"bytes": nnz * 12 + 8 * (N + 1) + 2 * vec},
+        "energy": {"bytes": conn + coords + vec, "flops": fe * E},
+        "residual": {"bytes": conn + coords + vec + 2 * vec, "flops": fr * E},  # r zero + write
+        "hvp": {"bytes": conn + coords + 2 * vec + 2 * vec, "flops": fh * E},   # u, v; y zero + write
+        "assemble": {"bytes": asm_bytes, "flops": (f_ctx + f_blocks) * E},
+        "spmv": {"bytes": nnz * 12 + 8 * (N + 1) + 2 * vec, "flops": 2 * nnz},
     }
 
 
@@ -270,8 +282,14 @@ def main():
         mark(5)
 
     if args.profile_step:
+        # one warm step (lazy setup), then exactly one step inside the profiler range
+        # (ncu --profile-from-start off captures only that)
         step()
         torch.cuda.synchronize()
+        torch.cuda.profiler.start()
+        step()
+        torch.cuda.synchronize()
+        torch.cuda.profiler.stop()
         prob.check()
         return
 
@@ -388,19 +406,6 @@ def main():
     hbm = peaks.get("hbm_gbs")
     hbm_src = "measured (MEASURED_PEAKS.json)" if hbm else "fallback (B200_PROFILING.md)"
     hbm = hbm or 6650.0
-    alg = algorithmic(mesh, nnz, C)
-    dom = max(phases, key=lambda p: per[p])
-    dom_ms = per[dom] / K
-    achieved = alg[dom]["bytes"] / (dom_ms * 1e-3) / 1e9
-    roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                "frac": achieved / hbm, "traffic": None, "kernel_phase": dom,
-                "peak_source": hbm_src}
-    phase_roofline = {}
-    for p in phases:
-        ms = per[p] / K
-        gbs = alg[p]["bytes"] / (ms * 1e-3) / 1e9
-        phase_roofline[p] = {"ms": ms, "alg_GB": alg[p]["bytes"] / 1e9, "GB/s": gbs,
-                             "frac_hbm": gbs / hbm, "share_of_step": per[p] / total_ms}
     fp64 = None
     try:
         import ctypes
@@ -410,6 +415,39 @@ def main():
         fp64 = lp.fem_peak_fp64_tflops(torch.cuda.get_device_properties(local).multi_processor_count)
     except Exception:
         pass
+    fp64_src = "measured (bench_tools/peak.cu DFMA)" if fp64 else "nominal 148 SM x 64 DFMA x 2 x 1.965 GHz"
+    fp64 = fp64 or 37.2
+    alg = algorithmic(mesh, nnz, C, mode)
+    phase_roofline = {}
+    for p in phases:
+        ms = per[p] / K
+        gbs = alg[p]["bytes"] / (ms * 1e-3) / 1e9
+        tfs = alg[p]["flops"] / (ms * 1e-3) / 1e12
+        t_hbm = alg[p]["bytes"] / (hbm * 1e9)
+        t_alu = alg[p]["flops"] / (fp64 * 1e12)
+        phase_roofline[p] = {"ms": ms, "alg_GB": alg[p]["bytes"] / 1e9, "GB/s": gbs,
+                             "frac_hbm": gbs / hbm, "alg_GFLOP": alg[p]["flops"] / 1e9,
+                             "TFLOP/s": tfs, "frac_fp64": tfs / fp64,
+                             "bound": "hbm" if t_hbm >= t_alu else "alu",
+                             "frac_of_bound": max(t_hbm, t_alu) / (ms * 1e-3),
+                             "share_of_step": per[p] / total_ms}
+    dom = max(phases, key=lambda p: per[p])
+    pr = phase_roofline[dom]
+    if pr["bound"] == "hbm":
+        roofline = {"bound": "hbm", "achieved": pr["GB/s"], "peak": hbm, "unit": "GB/s",
+                    "frac": pr["frac_hbm"], "peak_source": hbm_src}
+    else:
+        roofline = {"bound": "alu", "achieved": pr["TFLOP/s"], "peak": fp64, "unit": "TFLOP/s",
+                    "frac": pr["frac_fp64"], "peak_source": fp64_src}
+    traffic = None
+    try:
+        tj = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
+        traffic = tj["dram_bytes_per_launch"].get(dom)
+    except Exception:
+        pass
+    roofline.update({"traffic": traffic, "kernel_phase": dom,
+                     "note": "algorithmic bytes/flops per launch / CUDA-event time of the phase; "
+                             "traffic from ncu in profiles/"})
 
     # ---- solves (outside the timed region): CG per-iteration cost and Newton
     solve = {}

@@ -6,8 +6,8 @@ python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1
 timeout 600 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?" >> gpurun_out/smoke.log
 timeout 900 python bench.py > gpurun_out/bench_full.json 2> gpurun_out/bench_full.err
 timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err
-timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --profile-from-start off --csv \
    --log-file gpurun_out/launches.csv python bench.py --profile-step > gpurun_out/ncu_list.log 2>&1
-timeout 1500 ncu --set full --clock-control none --import-source on \
-   -k regex:"k_tile_pipe|k_rows_fused|k_spmv" -c 5 -o gpurun_out/prof_full -f \
+timeout 1500 ncu --set full --clock-control none --import-source on --profile-from-start off \
+   -k regex:"k_tile_pipe|k_rows_fused|k_elem_ctx|k_spmv" -c 6 -o gpurun_out/prof_full -f \
    python bench.py --profile-step > gpurun_out/ncu_full.log 2>&1

@@ -253,7 +253,7 @@ fem_status build_pattern(Problem *p, cudaStream_t s) {
 // ------------------------------------------------------------------ coloring
 // Number of (r, k) paths with r in adj(j), k in adj(r), k < j (with multiplicity).
 __global__ void k_color_init(const int64_t *gp, const int32_t *gi, int64_t nv, int32_t *cnt,
-                             int32_t *colors, int32_t *frontier, int32_t *fsize) {
+                             int32_t *colors) {
   for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < nv;
        j += (int64_t)gridDim.x * blockDim.x) {
     int32_t c = 0;
@@ -263,24 +263,46 @@ __global__ void k_color_init(const int64_t *gp, const int32_t *gi, int64_t nv, i
     }
     cnt[j] = c;
     colors[j] = -1;
-    if (c == 0) frontier[atomicAdd(fsize, 1)] = (int32_t)j;
   }
 }
 
-__global__ void __launch_bounds__(128) k_color_round(const int64_t *gp, const int32_t *gi,
+// Round t, phase 1: the frontier = uncolored vertices whose lower distance-2 neighbours are
+// all colored (counter reached 0 in an earlier round), compacted with warp-aggregated atomics.
+__global__ void k_color_select(const int32_t *cnt, const int32_t *colors, int64_t nv,
+                               int32_t *frontier, int32_t *size) {
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j - threadIdx.x < nv;
+       j += (int64_t)gridDim.x * blockDim.x) {
+    const bool ready = j < nv && colors[j] < 0 && cnt[j] == 0;
+    const unsigned mask = __ballot_sync(0xffffffffu, ready);
+    if (!mask) continue;
+    const int lane = threadIdx.x & 31, leader = __ffs(mask) - 1;
+    int base = 0;
+    if (lane == leader) base = atomicAdd(size, __popc(mask));
+    base = __shfl_sync(0xffffffffu, base, leader);
+    if (ready) frontier[base + __popc(mask & ((1u << lane) - 1))] = (int32_t)j;
+  }
+}
+
+// Round t, phase 2: one warp per frontier column j.  The lanes split j's rows r, collect
+// the colors of the lower distance-2 neighbours in a per-lane bitmask, OR-reduce it across
+// the warp, take the smallest free color (all lower neighbours are colored), then decrement
+// the counters of the higher distance-2 neighbours with fire-and-forget reductions.
+__global__ void __launch_bounds__(128) k_color_apply(const int64_t *gp, const int32_t *gi,
                                                      int32_t *cnt, int32_t *colors,
-                                                     const int32_t *cur, int32_t *next,
-                                                     int32_t *sizes, int t, int32_t *done,
-                                                     int *err, int32_t *max_color) {
-  const int32_t n_cur = sizes[t % 3];
-  if (blockIdx.x == 0 && threadIdx.x == 0) sizes[(t + 2) % 3] = 0;
-  int32_t *nsize = sizes + (t + 1) % 3;
-  for (int32_t w = blockIdx.x * blockDim.x + threadIdx.x; w < n_cur; w += gridDim.x * blockDim.x) {
-    const int32_t j = cur[w];
+                                                     const int32_t *frontier, int32_t *sizes,
+                                                     int slot, int32_t *done, int *err,
+                                                     int32_t *max_color) {
+  const int32_t n_cur = sizes[slot];
+  if (blockIdx.x == 0 && threadIdx.x == 0) sizes[slot ^ 1] = 0;
+  const int lane = threadIdx.x & 31;
+  const int32_t warps = gridDim.x * (blockDim.x >> 5);
+  for (int32_t w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < n_cur; w += warps) {
+    const int32_t j = frontier[w];
+    const int64_t p0 = gp[j], p1 = gp[j + 1];
     uint32_t fb[FEM_MAX_COLORS / 32];
 #pragma unroll
     for (int q = 0; q < FEM_MAX_COLORS / 32; ++q) fb[q] = 0u;
-    for (int64_t p = gp[j]; p < gp[j + 1]; ++p) {
+    for (int64_t p = p0 + lane; p < p1; p += 32) {
       const int32_t r = gi[p];
       for (int64_t q = gp[r]; q < gp[r + 1]; ++q) {
         const int32_t k = gi[q];
@@ -293,17 +315,20 @@ __global__ void __launch_bounds__(128) k_color_round(const int64_t *gp, const in
     int32_t c = -1;
 #pragma unroll
     for (int q = 0; q < FEM_MAX_COLORS / 32; ++q) {
-      if (c < 0 && fb[q] != 0xffffffffu) c = q * 32 + __ffs(~fb[q]) - 1;
+      const uint32_t m = __reduce_or_sync(0xffffffffu, fb[q]);
+      if (c < 0 && m != 0xffffffffu) c = q * 32 + __ffs(~m) - 1;
     }
-    if (c < 0) { atomicOr(err, ERRW_TOO_MANY_COLORS); c = FEM_MAX_COLORS - 1; }
-    colors[j] = c;
-    atomicMax(max_color, c);
-    atomicAdd(done, 1);
-    for (int64_t p = gp[j]; p < gp[j + 1]; ++p) {
+    if (lane == 0) {
+      if (c < 0) { atomicOr(err, ERRW_TOO_MANY_COLORS); c = FEM_MAX_COLORS - 1; }
+      colors[j] = c;
+      atomicMax(max_color, c);
+      atomicAdd(done, 1);
+    }
+    for (int64_t p = p0 + lane; p < p1; p += 32) {
       const int32_t r = gi[p];
       for (int64_t q = gp[r]; q < gp[r + 1]; ++q) {
         const int32_t k = gi[q];
-        if (k > j && atomicSub(cnt + k, 1) == 1) next[atomicAdd(nsize, 1)] = k;
+        if (k > j) atomicSub(cnt + k, 1);  // result unused: compiled to RED
       }
     }
   }
@@ -318,24 +343,23 @@ __global__ void k_expand_node_colors(const int32_t *nc, int64_t n_nodes, int dim
 // Colors the graph (gp, gi) with nv vertices into `colors`; returns the number of colors.
 static fem_status greedy_color(Problem *p, const int64_t *gp, const int32_t *gi, int64_t nv,
                                int32_t *colors, int32_t *n_colors, cudaStream_t s) {
-  int32_t *cnt = nullptr, *f0 = nullptr, *f1 = nullptr, *aux = nullptr;
+  int32_t *cnt = nullptr, *f0 = nullptr, *aux = nullptr;
   FEM_CUDA(cudaMalloc(&cnt, sizeof(int32_t) * (nv > 0 ? nv : 1)));
   FEM_CUDA(cudaMalloc(&f0, sizeof(int32_t) * (nv > 0 ? nv : 1)));
-  FEM_CUDA(cudaMalloc(&f1, sizeof(int32_t) * (nv > 0 ? nv : 1)));
-  FEM_CUDA(cudaMalloc(&aux, sizeof(int32_t) * 8));  // sizes[3], done, max_color
+  FEM_CUDA(cudaMalloc(&aux, sizeof(int32_t) * 8));  // sizes[2], done, max_color
   FEM_CUDA(cudaMemsetAsync(aux, 0, sizeof(int32_t) * 8, s));
-  FEM_CUDA(cudaMemsetAsync(aux + 4, 0xff, sizeof(int32_t), s));  // max_color = -1
-  int32_t *sizes = aux, *done = aux + 3, *maxc = aux + 4;
-  k_color_init<<<grid_for(nv), kThreads, 0, s>>>(gp, gi, nv, cnt, colors, f0, sizes);
+  FEM_CUDA(cudaMemsetAsync(aux + 3, 0xff, sizeof(int32_t), s));  // max_color = -1
+  int32_t *sizes = aux, *done = aux + 2, *maxc = aux + 3;
+  k_color_init<<<grid_for(nv), kThreads, 0, s>>>(gp, gi, nv, cnt, colors);
   FEM_LAUNCH_CHECK("color init");
   int32_t h_done = 0;
   const int kCheck = 32;
-  const int grid = 148 * 4;
+  const int sel_grid = grid_for(nv, kThreads, 148 * 16);
   for (int t = 0; h_done < nv;) {
     for (int q = 0; q < kCheck; ++q, ++t) {
-      int32_t *cur = (t % 2 == 0) ? f0 : f1, *nxt = (t % 2 == 0) ? f1 : f0;
-      k_color_round<<<grid, 128, 0, s>>>(gp, gi, cnt, colors, cur, nxt, sizes, t, done, p->d_err,
-                                         maxc);
+      const int slot = t & 1;
+      k_color_select<<<sel_grid, kThreads, 0, s>>>(cnt, colors, nv, f0, sizes + slot);
+      k_color_apply<<<148 * 4, 128, 0, s>>>(gp, gi, cnt, colors, f0, sizes, slot, done, p->d_err, maxc);
     }
     FEM_LAUNCH_CHECK("color round");
     FEM_CUDA(cudaMemcpyAsync(&h_done, done, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
@@ -350,7 +374,6 @@ static fem_status greedy_color(Problem *p, const int64_t *gp, const int32_t *gi,
   FEM_CUDA(cudaStreamSynchronize(s));
   cudaFree(cnt);
   cudaFree(f0);
-  cudaFree(f1);
   cudaFree(aux);
   *n_colors = hmax + 1;
   return read_error_word(p, s);

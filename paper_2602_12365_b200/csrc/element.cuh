@@ -105,6 +105,76 @@ __device__ __forceinline__ void nodal_from_stress(const double (&A)[D][D],
   }
 }
 
+// ---- cofactor form (tile kernels): G_a = c_a / det for a >= 1, so with vol = det / d!
+// the nodal vectors are vol P G_a = (P / d!) c_a and dH = dHh / det; the scalings fold into
+// the material coefficients (P and dP are linear in (lambda, mu)), and G, G_0, vol are
+// never formed.
+template <int D>
+__device__ __forceinline__ double cof_gradients(const double (&x)[D + 1][D], double (&c)[D][D]) {
+  if constexpr (D == 2) {
+    const double j00 = x[1][0] - x[0][0], j01 = x[2][0] - x[0][0];
+    const double j10 = x[1][1] - x[0][1], j11 = x[2][1] - x[0][1];
+    c[0][0] = j11;  c[0][1] = -j01;
+    c[1][0] = -j10; c[1][1] = j00;
+    return j00 * j11 - j01 * j10;
+  } else {
+    double J[3][3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+      for (int j = 0; j < 3; ++j) J[i][j] = x[j + 1][i] - x[0][i];
+    // c[a-1][j] = cof(J)[j][a-1]
+    c[0][0] = J[1][1] * J[2][2] - J[1][2] * J[2][1];
+    c[1][0] = J[1][2] * J[2][0] - J[1][0] * J[2][2];
+    c[2][0] = J[1][0] * J[2][1] - J[1][1] * J[2][0];
+    c[0][1] = J[0][2] * J[2][1] - J[0][1] * J[2][2];
+    c[1][1] = J[0][0] * J[2][2] - J[0][2] * J[2][0];
+    c[2][1] = J[0][1] * J[2][0] - J[0][0] * J[2][1];
+    c[0][2] = J[0][1] * J[1][2] - J[0][2] * J[1][1];
+    c[1][2] = J[0][2] * J[1][0] - J[0][0] * J[1][2];
+    c[2][2] = J[0][0] * J[1][1] - J[0][1] * J[1][0];
+    return J[0][0] * c[0][0] + J[0][1] * c[1][0] + J[0][2] * c[2][0];
+  }
+}
+
+// Hh = sum_{a>=1} (u_a - u_0) (x) c_a   (= det * H)
+template <int D>
+__device__ __forceinline__ void grad_hat(const double (&u)[D + 1][D], const double (&c)[D][D],
+                                         double (&Hh)[D][D]) {
+#pragma unroll
+  for (int i = 0; i < D; ++i) {
+    double du[D];
+#pragma unroll
+    for (int a = 0; a < D; ++a) du[a] = u[a + 1][i] - u[0][i];
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
+      double h = 0.0;
+#pragma unroll
+      for (int a = 0; a < D; ++a) h = fma(du[a], c[a][j], h);
+      Hh[i][j] = h;
+    }
+  }
+}
+
+// f_a = S c_a (a >= 1), f_0 = -sum_a f_a
+template <int D>
+__device__ __forceinline__ void nodal_from_c(const double (&S)[D][D], const double (&c)[D][D],
+                                             double (&f)[D + 1][D]) {
+#pragma unroll
+  for (int i = 0; i < D; ++i) {
+    double s0 = 0.0;
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+      double t = 0.0;
+#pragma unroll
+      for (int j = 0; j < D; ++j) t = fma(S[i][j], c[a][j], t);
+      f[a + 1][i] = t;
+      s0 += t;
+    }
+    f[0][i] = -s0;
+  }
+}
+
 // ------------------------------------------------------------------ linear elastic
 template <int D>
 __device__ __forceinline__ double le_psi(const double (&H)[D][D], double lam, double mu) {
@@ -207,7 +277,6 @@ __device__ __forceinline__ void nh_dstress(const NHState<D> &s, double lam, doub
                                            const double (&dH)[D][D], double (&dP)[D][D]) {
   // T = dH^T F^{-T};  M = F^{-T} T = F^{-T} dH^T F^{-T};  tr = F^{-T} : dH
   double T[D][D];
-  double tr = 0.0;
 #pragma unroll
   for (int k = 0; k < D; ++k)
 #pragma unroll
@@ -216,8 +285,10 @@ __device__ __forceinline__ void nh_dstress(const NHState<D> &s, double lam, doub
 #pragma unroll
       for (int l = 0; l < D; ++l) t = fma(dH[l][k], s.FiT[l][j], t);
       T[k][j] = t;
-      tr = fma(s.FiT[k][j], dH[k][j], tr);
     }
+  double tr = 0.0;  // F^{-T} : dH = tr(dH^T F^{-T}) = tr T
+#pragma unroll
+  for (int k = 0; k < D; ++k) tr += T[k][k];
   const double c1 = mu - lam * s.lnJ, c2 = lam * tr;
 #pragma unroll
   for (int i = 0; i < D; ++i)

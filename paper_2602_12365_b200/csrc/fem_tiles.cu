@@ -24,7 +24,10 @@
 #include "fem_internal.cuh"
 
 #ifndef FEM_PIPE_MINB
-#define FEM_PIPE_MINB 3
+#define FEM_PIPE_MINB 0  // 0: per-op choice (pipe_minb)
+#endif
+#ifndef FEM_PHASE2_SPLIT
+#define FEM_PHASE2_SPLIT 0
 #endif
 
 namespace fem {
@@ -397,6 +400,13 @@ __device__ __forceinline__ void cp_async8(void *smem, const void *gmem) {
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
 
+// CTAs per SM the register budget targets (A/B on cfg 3, profiles/): the NH HVP is the
+// register-heaviest and runs fastest spill-free at 2; energy at 4; residual at 3.
+__host__ __device__ constexpr int pipe_minb(int op, int mat) {
+  return FEM_PIPE_MINB > 0 ? FEM_PIPE_MINB
+                           : (op == OP_ENERGY ? 4 : (op == OP_RESIDUAL ? 3 : (mat == FEM_NEO_HOOKEAN ? 2 : 3)));
+}
+
 struct PipeArgs {
   const uint8_t *meta;
   int64_t n_tiles, E;
@@ -411,7 +421,7 @@ struct PipeArgs {
 };
 
 template <int D, int MAT, int OP, bool MASK, bool DET>
-__global__ void __launch_bounds__(kTile, FEM_PIPE_MINB) k_tile_pipe(PipeArgs A) {
+__global__ void __launch_bounds__(kTile, pipe_minb(OP, MAT)) k_tile_pipe(PipeArgs A) {
   constexpr int NEN = D + 1;
   constexpr bool NEED_U = (OP != OP_HVP) || (MAT == FEM_NEO_HOOKEAN);
   constexpr int NF = 1 + (NEED_U ? 1 : 0) + (OP == OP_HVP ? 1 : 0);
@@ -466,12 +476,14 @@ __global__ void __launch_bounds__(kTile, FEM_PIPE_MINB) k_tile_pipe(PipeArgs A) 
     if (e < A.E) {
       const ushort4 lc4 = reinterpret_cast<const ushort4 *>(m + A.off_lconn)[tid];
       const int lc[4] = {lc4.x, lc4.y, lc4.z, lc4.w};
-      double x[NEN][D], Gr[NEN][D], vol;
+      double x[NEN][D], c[D][D];
 #pragma unroll
       for (int a = 0; a < NEN; ++a)
 #pragma unroll
         for (int i = 0; i < D; ++i) x[a][i] = xs[lc[a] * D + i];
-      geometry<D>(x, Gr, vol);
+      const double det = cof_gradients<D>(x, c);
+      const double id = 1.0 / det;
+      constexpr double inv_fact = (D == 3) ? 1.0 / 6.0 : 0.5;  // vol = det / d!
       double lam = A.lam, mu = A.mu;
       if (A.has_phase) {
         const int ph = m[A.off_ph + tid];
@@ -485,11 +497,16 @@ __global__ void __launch_bounds__(kTile, FEM_PIPE_MINB) k_tile_pipe(PipeArgs A) 
         for (int a = 0; a < NEN; ++a)
 #pragma unroll
           for (int i = 0; i < D; ++i) u[a][i] = us[lc[a] * D + i];
-        field_gradient<D>(u, Gr, H);
+        grad_hat<D>(u, c, H);
+#pragma unroll
+        for (int i = 0; i < D; ++i)
+#pragma unroll
+          for (int j = 0; j < D; ++j) H[i][j] *= id;
       }
       bool ok = true;
       double S[D][D];
       if constexpr (OP == OP_ENERGY) {
+        const double vol = det * inv_fact;
         if constexpr (MAT == FEM_LINEAR_ELASTIC) {
           eacc += vol * le_psi<D>(H, lam, mu);
         } else {
@@ -498,14 +515,17 @@ __global__ void __launch_bounds__(kTile, FEM_PIPE_MINB) k_tile_pipe(PipeArgs A) 
           if (ok) eacc += vol * nh_psi<D>(H, s, lam, mu);
         }
       } else if constexpr (OP == OP_RESIDUAL) {
+        // vol P G_a = (P / d!) c_a; P linear in (lambda, mu)
+        const double ls = lam * inv_fact, ms = mu * inv_fact;
         if constexpr (MAT == FEM_LINEAR_ELASTIC) {
-          le_stress<D>(H, lam, mu, S);
+          le_stress<D>(H, ls, ms, S);
         } else {
           NHState<D> s;
           ok = nh_state<D>(H, s);
-          if (ok) nh_stress<D>(s, lam, mu, S);
+          if (ok) nh_stress<D>(s, ls, ms, S);
         }
       } else {
+        // dH = dHh / det; vol dP(dH) G_a = dP(dHh) c_a * (1 / (det d!)): fold into (lambda, mu)
         double v[NEN][D], dH[D][D];
 #pragma unroll
         for (int a = 0; a < NEN; ++a) {
@@ -513,19 +533,21 @@ __global__ void __launch_bounds__(kTile, FEM_PIPE_MINB) k_tile_pipe(PipeArgs A) 
 #pragma unroll
           for (int i = 0; i < D; ++i) v[a][i] = (bc & (1u << i)) ? 0.0 : vs[lc[a] * D + i];
         }
-        field_gradient<D>(v, Gr, dH);
+        grad_hat<D>(v, c, dH);
+        const double sc = id * inv_fact;
+        const double ls = lam * sc, ms = mu * sc;
         if constexpr (MAT == FEM_LINEAR_ELASTIC) {
-          le_stress<D>(dH, lam, mu, S);
+          le_stress<D>(dH, ls, ms, S);
         } else {
           NHState<D> s;
           ok = nh_state<D>(H, s);
-          if (ok) nh_dstress<D>(s, lam, mu, dH, S);
+          if (ok) nh_dstress<D>(s, ls, ms, dH, S);
         }
       }
       if (!ok) atomicOr(A.err, ERRW_INVERTED);
       if constexpr (OP != OP_ENERGY) {
         double f[NEN][D];
-        nodal_from_stress<D>(S, Gr, vol, f);
+        nodal_from_c<D>(S, c, f);
 #pragma unroll
         for (int a = 0; a < NEN; ++a)
 #pragma unroll
@@ -538,32 +560,51 @@ __global__ void __launch_bounds__(kTile, FEM_PIPE_MINB) k_tile_pipe(PipeArgs A) 
       const uint16_t *ptr = reinterpret_cast<const uint16_t *>(m + A.off_ptr);
       const uint16_t *inc = reinterpret_cast<const uint16_t *>(m + A.off_inc);
       const int32_t *nodes = reinterpret_cast<const int32_t *>(m + A.off_nodes);
-      for (int r = tid; r < U; r += kTile) {
+#if FEM_PHASE2_SPLIT
+      for (int q = tid; q < U * D; q += kTile) {  // (tile node, component) items
+        const int r = q / D, cc = q - r * D;
+        const int lo = ptr[r], hi = ptr[r + 1];
+        double sacc = 0.0;
+        for (int w = lo; w < hi; ++w) {
+          const int pk = inc[w];
+          sacc += contrib[((pk & 3) * D + cc) * kTile + (pk >> 2)];
+        }
+        if constexpr (DET) {
+          A.slots[(A.slot_off[t] + r) * D + cc] = sacc;
+        } else {
+          const int64_t g = (int64_t)nodes[r] * D + cc;
+          if (m[A.off_int + r]) A.out[g] = sacc;
+          else atomicAdd(A.out + g, sacc);
+        }
+      }
+#else
+      for (int r = tid; r < U; r += kTile) {  // one thread per tile node, D components
         const int lo = ptr[r], hi = ptr[r + 1];
         double sacc[D];
 #pragma unroll
-        for (int c = 0; c < D; ++c) sacc[c] = 0.0;
-        for (int q = lo; q < hi; ++q) {
-          const int pk = inc[q];
+        for (int cc = 0; cc < D; ++cc) sacc[cc] = 0.0;
+        for (int w = lo; w < hi; ++w) {
+          const int pk = inc[w];
           const int el = pk >> 2, a = pk & 3;
 #pragma unroll
-          for (int c = 0; c < D; ++c) sacc[c] += contrib[(a * D + c) * kTile + el];
+          for (int cc = 0; cc < D; ++cc) sacc[cc] += contrib[(a * D + cc) * kTile + el];
         }
         if constexpr (DET) {
           double *slot = A.slots + (A.slot_off[t] + r) * D;
 #pragma unroll
-          for (int c = 0; c < D; ++c) slot[c] = sacc[c];
+          for (int cc = 0; cc < D; ++cc) slot[cc] = sacc[cc];
         } else {
           const int64_t g = (int64_t)nodes[r] * D;
           if (m[A.off_int + r]) {
 #pragma unroll
-            for (int c = 0; c < D; ++c) A.out[g + c] = sacc[c];
+            for (int cc = 0; cc < D; ++cc) A.out[g + cc] = sacc[cc];
           } else {
 #pragma unroll
-            for (int c = 0; c < D; ++c) atomicAdd(A.out + g + c, sacc[c]);
+            for (int cc = 0; cc < D; ++cc) atomicAdd(A.out + g + cc, sacc[cc]);
           }
         }
       }
+#endif
     }
     __syncthreads();
   }
@@ -593,8 +634,10 @@ __global__ void k_slot_gather(const int64_t *node_slot_ptr, const int32_t *node_
 }
 
 // grid of the persistent kernels (fixed per problem: deterministic energy partial order)
-static int pipe_grid(Problem *p) {
-  return (int)std::min<int64_t>(p->tiles.n_tiles, 148 * FEM_PIPE_MINB * (256 / kTile));
+// grid of the persistent kernels: 148 SMs x CTAs/SM of the op (fixed per problem and op,
+// so the energy partial order is deterministic)
+static int pipe_grid(Problem *p, int op) {
+  return (int)std::min<int64_t>(p->tiles.n_tiles, 148 * pipe_minb(op, p->material) * (256 / kTile));
 }
 
 template <int D, int MAT, int OP, bool MASK, bool DET>
@@ -606,7 +649,7 @@ static fem_status launch_pipe_t(Problem *p, const PipeArgs &a, cudaStream_t s) {
                       (OP == OP_ENERGY ? 0 : sizeof(double) * (size_t)(D + 1) * D * kTile);
   auto kern = k_tile_pipe<D, MAT, OP, MASK, DET>;
   FEM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  kern<<<pipe_grid(p), kTile, smem, s>>>(a);
+  kern<<<pipe_grid(p, OP), kTile, smem, s>>>(a);
   FEM_LAUNCH_CHECK("tile pipeline kernel");
   return FEM_OK;
 }
@@ -667,7 +710,7 @@ fem_status tile_pass(Problem *p, int op, const double *u, const double *v, doubl
   return mask ? launch_pipe_op<OP_HVP, true, false>(p, a, s) : launch_pipe_op<OP_HVP, false, false>(p, a, s);
 }
 
-int tile_energy_partials(Problem *p) { return pipe_grid(p); }
+int tile_energy_partials(Problem *p) { return pipe_grid(p, OP_ENERGY); }
 
 
 template <int D>

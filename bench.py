@@ -482,6 +482,14 @@ def main():
             torch.cuda.synchronize()
             solve["newton_s"] = time.perf_counter() - t0
             solve["newton"] = {k: info[k] for k in ("iters", "cg_iters", "converged", "res0", "res")}
+            # BASELINE cfg 3 as stated: colored sparse tangent + SpMV-CG (Jacobi) per Newton step
+            t0 = time.perf_counter()
+            zc, infoc = prob.newton_solve(z0, op=1, jacobi=True, cg_rtol=1e-8, rtol=1e-10,
+                                          atol=1e-14, raise_on_fail=False)
+            torch.cuda.synchronize()
+            solve["newton_csr_s"] = time.perf_counter() - t0
+            solve["newton_csr"] = {k: infoc[k] for k in ("iters", "cg_iters", "converged", "res0", "res")}
+            solve["newton_csr_vs_hvp_maxdiff"] = float((zc - zs).abs().max())
 
     cpu = None
     if not args.no_cpu_baseline and rank == 0:

@@ -42,7 +42,7 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", type=int, default=3, choices=[2, 3, 5])
     ap.add_argument("--n", type=int, default=None, help="override the mesh size (cells per side)")
-    ap.add_argument("--assemble-mode", default="rows", choices=["batched", "literal", "rows"])
+    ap.add_argument("--assemble-mode", default="auto", choices=["auto", "batched", "literal", "rows"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-solve", action="store_true")
     ap.add_argument("--profile-step", action="store_true", help="one step only (for ncu)")
@@ -180,7 +180,7 @@ def algorithmic(mesh, nnz, C, mode):
     f_ctx = fr + 2 * d * d * nen
     f_blocks = nen * nen * (2 * d + 6 * d * d)
     asm_bytes = conn + coords + vec + 8 * nnz                          # inputs + vals written once
-    if mode != "rows":                                                 # J_comp written + read
+    if mode in ("batched", "literal") or (mode == "auto" and d == 2):  # J_comp written + read
         asm_bytes += 2 * 8 * N * C + nnz * (4 + 4)
     return {
         "energy": {"bytes": conn + coords + vec, "flops": fe * E},

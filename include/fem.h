@@ -79,8 +79,9 @@ enum {
                                terms — f_ext, Dirichlet rows — on owned DOFs only, zero
                                elsewhere), so fem_halo_pack + exchange + fem_halo_combine
                                yields the global result.                                 */
-  FEM_ASSEMBLE_JCOMP = 32u  /* fem_assemble_csr: all color passes in ONE element sweep
+  FEM_ASSEMBLE_JCOMP = 32u, /* fem_assemble_csr: all color passes in ONE element sweep
                                into J_comp [N][C] (atomics), then decompression.         */
+  FEM_ASSEMBLE_ROWS = 64u   /* fem_assemble_csr: row-pull form (no J_comp buffer).         */
 };
 
 typedef struct {
@@ -173,10 +174,11 @@ fem_status fem_color(fem_problem *p, int32_t *colors, int32_t *n_colors, fem_str
  *            lax.scan), then a decompression kernel;
  *   FEM_ASSEMBLE_JCOMP: all color passes in ONE element sweep (the passes are
  *            independent), accumulating J_comp with atomics, then decompression;
- *   default: J_comp computed row by row (pull form: row i sums the colored seeds'
- *            responses of its incident elements, a warp per node) with each compressed
- *            entry stored at its decompressed CSR slot (within a row every color names
- *            one column) — no J_comp buffer, atomic-free, bitwise reproducible.
+ *   FEM_ASSEMBLE_ROWS: J_comp computed row by row (pull form: row i sums the colored
+ *            seeds' responses of its incident elements, a warp per node) with each
+ *            compressed entry stored at its decompressed CSR slot (within a row every color
+ *            names one column) — no J_comp buffer, atomic-free, bitwise reproducible;
+ *   default (no mode flag): FEM_ASSEMBLE_ROWS in 3D, FEM_ASSEMBLE_JCOMP in 2D.
  * flags may add FEM_APPLY_BC.  Requires fem_color (the pattern and colors). */
 fem_status fem_assemble_csr(fem_problem *p, const double *z, double *vals, unsigned flags,
                             fem_stream stream);

@@ -578,7 +578,11 @@ static void launch_colored(const AsmArgs &a, bool literal, int pass, cudaStream_
 static fem_status assemble(Problem *p, const double *z, double *vals, unsigned flags,
                            cudaStream_t s) {
   const bool bc = (flags & FEM_APPLY_BC) && p->n_dir;
-  if (!(flags & (FEM_ASSEMBLE_LITERAL | FEM_ASSEMBLE_JCOMP))) {  // default: fused row-pull
+  // default: row-pull in 3D, one-sweep J_comp in 2D (C = 18 columns; measured 3x faster
+  // there, profiles/r01_sweep.csv); explicit mode flags override
+  const bool rows = (flags & FEM_ASSEMBLE_ROWS) ||
+                    (!(flags & (FEM_ASSEMBLE_LITERAL | FEM_ASSEMBLE_JCOMP)) && p->dim == 3);
+  if (rows) {
     fem_status st0 = build_slot_lists(p, s);
     if (st0) return st0;
     RowArgs A{};

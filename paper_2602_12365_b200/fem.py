@@ -25,6 +25,7 @@ APPLY_BC = 1
 DETERMINISTIC = 2
 ASSEMBLE_LITERAL = 4
 ASSEMBLE_JCOMP = 32
+ASSEMBLE_ROWS = 64
 BASELINE_SCATTER = 8
 LOCAL_ONLY = 16
 STATUS = {0: "OK", 1: "INVALID_ARG", 2: "DEGENERATE_ELEMENT", 3: "INVERTED_ELEMENT",
@@ -274,10 +275,10 @@ class Problem:
         _check(load_library().fem_color(self._h, _ptr(colors), C.byref(nc), _stream()), "fem_color")
         return colors, nc.value
 
-    def assemble_csr(self, z, bc: bool = False, mode: str = "rows", out=None) -> torch.Tensor:
+    def assemble_csr(self, z, bc: bool = False, mode: str = "auto", out=None) -> torch.Tensor:
         z = self._vec(z, "z")
         flags = (APPLY_BC if bc else 0) | {"batched": ASSEMBLE_JCOMP, "literal": ASSEMBLE_LITERAL,
-                                             "rows": 0}[mode]
+                                             "rows": ASSEMBLE_ROWS, "auto": 0}[mode]
         nnz = self.nnz()
         out = self._out(out, nnz)
         _check(load_library().fem_assemble_csr(self._h, _ptr(z), _ptr(out), flags, _stream()),

@@ -402,9 +402,11 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 
 // CTAs per SM the register budget targets (A/B on cfg 3, profiles/): the NH HVP is the
 // register-heaviest and runs fastest spill-free at 2; energy at 4; residual at 3.
+// (stated for 256-thread CTAs; smaller tiles scale the CTA count so warps/SM stay equal)
 __host__ __device__ constexpr int pipe_minb(int op, int mat) {
-  return FEM_PIPE_MINB > 0 ? FEM_PIPE_MINB
-                           : (op == OP_ENERGY ? 4 : (op == OP_RESIDUAL ? 3 : (mat == FEM_NEO_HOOKEAN ? 2 : 3)));
+  return (256 / kTile) *
+         (FEM_PIPE_MINB > 0 ? FEM_PIPE_MINB
+                            : (op == OP_ENERGY ? 4 : (op == OP_RESIDUAL ? 3 : (mat == FEM_NEO_HOOKEAN ? 2 : 3))));
 }
 
 struct PipeArgs {
@@ -637,7 +639,7 @@ __global__ void k_slot_gather(const int64_t *node_slot_ptr, const int32_t *node_
 // grid of the persistent kernels: 148 SMs x CTAs/SM of the op (fixed per problem and op,
 // so the energy partial order is deterministic)
 static int pipe_grid(Problem *p, int op) {
-  return (int)std::min<int64_t>(p->tiles.n_tiles, 148 * pipe_minb(op, p->material) * (256 / kTile));
+  return (int)std::min<int64_t>(p->tiles.n_tiles, 148 * pipe_minb(op, p->material));
 }
 
 template <int D, int MAT, int OP, bool MASK, bool DET>

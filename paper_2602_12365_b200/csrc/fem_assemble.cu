@@ -9,6 +9,8 @@
 // dH = e_k (x) G_b and contracted with vol G_a (DESIGN.md §5 derives it).
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
 #include "element.cuh"
 #include "fem_internal.cuh"
 
@@ -229,12 +231,11 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 
 // ------------------------------------------------------------------ per-element tangent context
 // k_elem_ctx evaluates, once per element and in the caller's element order, everything the
-// element Hessian needs (the ColumnCtx above): G_1..G_d, g_1..g_d (G_0, g_0 = -sum) and the
-// scalars vol*mu, vol*c1, vol*c2, stored as one 16-byte aligned record.  The row-pull
-// assembly then reads these records instead of re-gathering coordinates and state and
-// re-evaluating F, F^-1 and ln J for each of the element's nodes.
-template <int D>
-constexpr int ctx_stride() { return D == 3 ? 22 : 12; }
+// element Hessian needs (the ColumnCtx above): per element node a = 1..d the pair (G_a, g_a)
+// (G_0, g_0 = -sum), then the scalars vol*mu, vol*c1, vol*c2, stored as one 16-byte aligned
+// record [G_1 g_1 | ... | G_d g_d | smu sc1 sc2 pad].  The row-pull assembly then reads
+// these records instead of re-gathering coordinates and state and re-evaluating F, F^-1
+// and ln J for each of the element's nodes.
 
 template <int D>
 struct CtxLite {
@@ -261,8 +262,8 @@ __device__ __forceinline__ void load_ctx(const double *ctx, int64_t e, CtxLite<D
   for (int a = 1; a < D + 1; ++a)
 #pragma unroll
     for (int j = 0; j < D; ++j) {
-      c.G[a][j] = v[(a - 1) * D + j];
-      c.g[a][j] = v[D * D + (a - 1) * D + j];
+      c.G[a][j] = v[(a - 1) * 2 * D + j];
+      c.g[a][j] = v[(a - 1) * 2 * D + D + j];
       c.G[0][j] -= c.G[a][j];
       c.g[0][j] -= c.g[a][j];
     }
@@ -296,8 +297,8 @@ __global__ void __launch_bounds__(kThreads) k_elem_ctx(const double *coords, con
     for (int a = 1; a < D + 1; ++a)
 #pragma unroll
       for (int j = 0; j < D; ++j) {
-        v[(a - 1) * D + j] = ok ? cx.G[a][j] : 0.0;
-        v[D * D + (a - 1) * D + j] = ok ? cx.g[a][j] : 0.0;
+        v[(a - 1) * 2 * D + j] = ok ? cx.G[a][j] : 0.0;
+        v[(a - 1) * 2 * D + D + j] = ok ? cx.g[a][j] : 0.0;
       }
     v[2 * D * D] = ok ? cx.vol * cx.mu : 0.0;
     v[2 * D * D + 1] = ok ? cx.vol * cx.c1 : 0.0;
@@ -583,8 +584,12 @@ static fem_status assemble(Problem *p, const double *z, double *vals, unsigned f
   const bool rows = (flags & FEM_ASSEMBLE_ROWS) ||
                     (!(flags & (FEM_ASSEMBLE_LITERAL | FEM_ASSEMBLE_JCOMP)) && p->dim == 3);
   if (rows) {
-    fem_status st0 = build_slot_lists(p, s);
+    fem_status st0 = build_row_plan(p, s);
     if (st0) return st0;
+    if (p->rp_state != 1) {
+      st0 = build_slot_lists(p, s);
+      if (st0) return st0;
+    }
     RowArgs A{};
     A.coords = p->coords; A.conn = p->conn; A.lam = p->lam; A.mu = p->mu;
     A.phase = p->phase; A.lam_tab = p->lam_tab; A.mu_tab = p->mu_tab;
@@ -610,6 +615,8 @@ static fem_status assemble(Problem *p, const double *z, double *vals, unsigned f
         else k_elem_ctx<3, FEM_NEO_HOOKEAN><<<ge, kThreads, 0, s>>>(p->coords, p->conn, p->n_elems, p->lam, p->mu, p->phase, p->lam_tab, p->mu_tab, z, ctx, p->d_err);
       }
     }
+    if (p->rp_state == 1)
+      return launch_rows_stage(p, A.ctx, vals, bc, s);
     const int grid = grid_for(p->n_nodes, kRowGroups, 148 * 64);
     if (p->dim == 2) k_rows_fused<2><<<grid, kRowLanes * kRowGroups, 0, s>>>(A);
     else k_rows_fused<3><<<grid, kRowLanes * kRowGroups, 0, s>>>(A);

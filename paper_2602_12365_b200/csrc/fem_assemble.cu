@@ -230,10 +230,10 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
 
 // ------------------------------------------------------------------ per-element tangent context
-// k_elem_ctx evaluates, once per element and in the caller's element order, everything the
-// element Hessian needs (the ColumnCtx above): per element node a = 1..d the pair (G_a, g_a)
-// (G_0, g_0 = -sum), then the scalars vol*mu, vol*c1, vol*c2, stored as one 16-byte aligned
-// record [G_1 g_1 | ... | G_d g_d | smu sc1 sc2 pad].  The row-pull assembly then reads
+// k_elem_ctx evaluates, once per element, everything the element Hessian needs (the
+// ColumnCtx above): per element node a = 0..d the pair (G_a, g_a), then the scalars vol*mu,
+// vol*c1, vol*c2, stored as one 16-byte aligned record [G_0 g_0 | ... | G_d g_d | smu sc1
+// sc2 pad].  The row-pull assembly then reads
 // these records instead of re-gathering coordinates and state and re-evaluating F, F^-1
 // and ln J for each of the element's nodes.
 
@@ -254,60 +254,68 @@ __device__ __forceinline__ void load_ctx(const double *ctx, int64_t e, CtxLite<D
     v[2 * q + 1] = t.y;
   }
 #pragma unroll
-  for (int j = 0; j < D; ++j) {
-    c.G[0][j] = 0.0;
-    c.g[0][j] = 0.0;
-  }
-#pragma unroll
-  for (int a = 1; a < D + 1; ++a)
+  for (int a = 0; a < D + 1; ++a)
 #pragma unroll
     for (int j = 0; j < D; ++j) {
-      c.G[a][j] = v[(a - 1) * 2 * D + j];
-      c.g[a][j] = v[(a - 1) * 2 * D + D + j];
-      c.G[0][j] -= c.G[a][j];
-      c.g[0][j] -= c.g[a][j];
+      c.G[a][j] = v[a * 2 * D + j];
+      c.g[a][j] = v[a * 2 * D + D + j];
     }
-  c.smu = v[2 * D * D];
-  c.sc1 = v[2 * D * D + 1];
-  c.sc2 = v[2 * D * D + 2];
+  c.smu = v[2 * D * (D + 1)];
+  c.sc1 = v[2 * D * (D + 1) + 1];
+  c.sc2 = v[2 * D * (D + 1) + 2];
 }
 
+constexpr int kCtxThreads = 128;
+
 template <int D, int MAT>
-__global__ void __launch_bounds__(kThreads) k_elem_ctx(const double *coords, const int32_t *conn,
-                                                      int64_t E, double lam0, double mu0,
-                                                      const uint8_t *phase, const double *lam_tab,
-                                                      const double *mu_tab, const double *z,
-                                                      double *ctx, int *err) {
+__global__ void __launch_bounds__(kCtxThreads) k_elem_ctx(const double *coords, const int32_t *conn,
+                                                         int64_t E, double lam0, double mu0,
+                                                         const uint8_t *phase, const double *lam_tab,
+                                                         const double *mu_tab, const double *z,
+                                                         const int32_t *perm, double *ctx, int *err) {
+  // record i holds element perm[i] (the element tiles' Morton order) or element i; each CTA
+  // stages its kCtxThreads consecutive records in shared memory and stores them coalesced
   constexpr int ST = ctx_stride<D>();
-  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < E;
-       e += (int64_t)gridDim.x * blockDim.x) {
-    int32_t nd[D + 1];
-    load_nodes<D>(conn, e, nd);
-    double lam = lam0, mu = mu0;
-    if (phase) {
-      const int ph = phase[e];
-      lam = lam_tab[ph];
-      mu = mu_tab[ph];
-    }
-    ColumnCtx<D> cx;
-    const bool ok = column_ctx<D, MAT>(coords, nd, z, lam, mu, cx);
-    if (!ok) atomicOr(err, ERRW_INVERTED);
-    double v[ST];
-#pragma unroll
-    for (int a = 1; a < D + 1; ++a)
-#pragma unroll
-      for (int j = 0; j < D; ++j) {
-        v[(a - 1) * 2 * D + j] = ok ? cx.G[a][j] : 0.0;
-        v[(a - 1) * 2 * D + D + j] = ok ? cx.g[a][j] : 0.0;
+  __shared__ __align__(16) double srec[kCtxThreads * ST];
+  for (int64_t i0 = (int64_t)blockIdx.x * kCtxThreads; i0 < E; i0 += (int64_t)gridDim.x * kCtxThreads) {
+    const int64_t i = i0 + threadIdx.x;
+    if (i < E) {
+      const int64_t e = perm ? (int64_t)__ldg(perm + i) : i;
+      int32_t nd[D + 1];
+      load_nodes<D>(conn, e, nd);
+      double lam = lam0, mu = mu0;
+      if (phase) {
+        const int ph = phase[e];
+        lam = lam_tab[ph];
+        mu = mu_tab[ph];
       }
-    v[2 * D * D] = ok ? cx.vol * cx.mu : 0.0;
-    v[2 * D * D + 1] = ok ? cx.vol * cx.c1 : 0.0;
-    v[2 * D * D + 2] = ok ? cx.vol * cx.c2 : 0.0;
+      ColumnCtx<D> cx;
+      const bool ok = column_ctx<D, MAT>(coords, nd, z, lam, mu, cx);
+      if (!ok) atomicOr(err, ERRW_INVERTED);
+      double v[ST];
 #pragma unroll
-    for (int q = 2 * D * D + 3; q < ST; ++q) v[q] = 0.0;
-    double2 *o = reinterpret_cast<double2 *>(ctx + e * ST);
+      for (int a = 0; a < D + 1; ++a)
 #pragma unroll
-    for (int q = 0; q < ST / 2; ++q) o[q] = make_double2(v[2 * q], v[2 * q + 1]);
+        for (int j = 0; j < D; ++j) {
+          v[a * 2 * D + j] = ok ? cx.G[a][j] : 0.0;
+          v[a * 2 * D + D + j] = ok ? cx.g[a][j] : 0.0;
+        }
+      constexpr int S0 = 2 * D * (D + 1);
+      v[S0] = ok ? cx.vol * cx.mu : 0.0;
+      v[S0 + 1] = ok ? cx.vol * cx.c1 : 0.0;
+      v[S0 + 2] = ok ? cx.vol * cx.c2 : 0.0;
+#pragma unroll
+      for (int q = S0 + 3; q < ST; ++q) v[q] = 0.0;
+      double2 *o = reinterpret_cast<double2 *>(srec + threadIdx.x * ST);
+#pragma unroll
+      for (int q = 0; q < ST / 2; ++q) o[q] = make_double2(v[2 * q], v[2 * q + 1]);
+    }
+    __syncthreads();
+    const int64_t nrec = (E - i0 < kCtxThreads) ? E - i0 : kCtxThreads;
+    const double2 *src = reinterpret_cast<const double2 *>(srec);
+    double2 *dst = reinterpret_cast<double2 *>(ctx + i0 * ST);
+    for (int q = threadIdx.x; q < nrec * (ST / 2); q += kCtxThreads) dst[q] = src[q];
+    __syncthreads();
   }
 }
 
@@ -605,14 +613,15 @@ static fem_status assemble(Problem *p, const double *z, double *vals, unsigned f
     if (stc) return stc;
     A.ctx = (const double *)p->ctxbuf.ptr;
     if (p->n_elems) {
-      const int ge = grid_for(p->n_elems);
+      const int ge = grid_for(p->n_elems, kCtxThreads);
       double *ctx = (double *)p->ctxbuf.ptr;
+      const int32_t *perm = p->rp_state == 1 ? p->tiles.perm : nullptr;
       if (p->dim == 2) {
-        if (p->material == FEM_LINEAR_ELASTIC) k_elem_ctx<2, FEM_LINEAR_ELASTIC><<<ge, kThreads, 0, s>>>(p->coords, p->conn, p->n_elems, p->lam, p->mu, p->phase, p->lam_tab, p->mu_tab, z, ctx, p->d_err);
-        else k_elem_ctx<2, FEM_NEO_HOOKEAN><<<ge, kThreads, 0, s>>>(p->coords, p->conn, p->n_elems, p->lam, p->mu, p->phase, p->lam_tab, p->mu_tab, z, ctx, p->d_err);
+        if (p->material == FEM_LINEAR_ELASTIC) k_elem_ctx<2, FEM_LINEAR_ELASTIC><<<ge, kCtxThreads, 0, s>>>(p->coords, p->conn, p->n_elems, p->lam, p->mu, p->phase, p->lam_tab, p->mu_tab, z, perm, ctx, p->d_err);
+        else k_elem_ctx<2, FEM_NEO_HOOKEAN><<<ge, kCtxThreads, 0, s>>>(p->coords, p->conn, p->n_elems, p->lam, p->mu, p->phase, p->lam_tab, p->mu_tab, z, perm, ctx, p->d_err);
       } else {
-        if (p->material == FEM_LINEAR_ELASTIC) k_elem_ctx<3, FEM_LINEAR_ELASTIC><<<ge, kThreads, 0, s>>>(p->coords, p->conn, p->n_elems, p->lam, p->mu, p->phase, p->lam_tab, p->mu_tab, z, ctx, p->d_err);
-        else k_elem_ctx<3, FEM_NEO_HOOKEAN><<<ge, kThreads, 0, s>>>(p->coords, p->conn, p->n_elems, p->lam, p->mu, p->phase, p->lam_tab, p->mu_tab, z, ctx, p->d_err);
+        if (p->material == FEM_LINEAR_ELASTIC) k_elem_ctx<3, FEM_LINEAR_ELASTIC><<<ge, kCtxThreads, 0, s>>>(p->coords, p->conn, p->n_elems, p->lam, p->mu, p->phase, p->lam_tab, p->mu_tab, z, perm, ctx, p->d_err);
+        else k_elem_ctx<3, FEM_NEO_HOOKEAN><<<ge, kCtxThreads, 0, s>>>(p->coords, p->conn, p->n_elems, p->lam, p->mu, p->phase, p->lam_tab, p->mu_tab, z, perm, ctx, p->d_err);
       }
     }
     if (p->rp_state == 1)

@@ -94,15 +94,15 @@ struct Problem {
   uint8_t *slot_list = nullptr; // fused assembly: per node (l << 2 | b) grouped by CSR slot
   uint16_t *slot_off = nullptr; // [nnz_node + n_nodes] slot offsets into each node's list
   int32_t *node_order = nullptr; // [n_nodes] Morton order of the nodes (assembly)
-  // staged row assembly plan (fem_rows.cu build_row_plan), indexed by the position in
-  // node_order; fixed strides is (incidences), es (block entries) and ss (slots + 1)
+  // row-pull assembly plan (fem_rows.cu build_row_plan), indexed by the position in
+  // node_order; fixed strides es (block entries) and ss (off-diagonal slots + 1)
   int rp_state = 0;              // 0 not built, 1 built, -1 mesh not eligible (fallback)
-  int rp_is = 0, rp_es = 0, rp_ss = 0;
-  int4 *rp_node = nullptr;       // {n, deg | sn<<8 | ds<<16 | bc(n)<<24, row_ptr[dim*n] lo, hi}
-  int32_t *rp_inc = nullptr;     // [n_nodes*is + 32] e*nen + a (incidence l), -1 padding
-  uint16_t *rp_ent = nullptr;    // [n_nodes*es] blocks (l | a<<5 | b<<7) grouped by CSR slot
-  uint8_t *rp_soff = nullptr;    // [n_nodes*ss + 32] entry offsets of the CSR slots
-  uint8_t *rp_sbc = nullptr;     // [n_nodes*ss + 32] Dirichlet bits of each slot's node
+  int rp_lpn = 0, rp_es = 0, rp_ss = 0;
+  int32_t *epos = nullptr;       // [E] element -> record position (element tile order)
+  int4 *rp_node = nullptr;       // {n, sno | sn<<8 | ds<<16 | bc(n)<<24, row_ptr[dim*n] lo, hi}
+  uint32_t *rp_ent = nullptr;    // [n_pad*es] blocks (pos | a<<27 | b<<29) grouped by slot
+  uint8_t *rp_soff = nullptr;    // [n_pad*ss] entry offsets of the off-diagonal slots
+  uint8_t *rp_sbc = nullptr;     // [n_pad*ss] Dirichlet bits of each slot's node
   // coloring
   bool have_colors = false;
   int32_t n_colors = -1;
@@ -197,7 +197,7 @@ void free_tiles(TileSet &T);
 int tile_energy_partials(Problem *p);
 // per-element tangent context records (k_elem_ctx, fem_assemble.cu): doubles per element
 template <int D>
-constexpr int ctx_stride() { return D == 3 ? 22 : 12; }
+constexpr int ctx_stride() { return D == 3 ? 28 : 16; }  // [G_a g_a] a = 0..D, smu sc1 sc2, pad
 fem_status morton_node_order(Problem *p, cudaStream_t s);
 fem_status build_row_plan(Problem *p, cudaStream_t s);          // fem_rows.cu
 fem_status launch_rows_stage(Problem *p, const double *ctx, double *vals, bool bc,

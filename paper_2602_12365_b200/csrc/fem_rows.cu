@@ -1,46 +1,58 @@
-// fem_rows.cu — staged row-pull assembly of the sparse tangent (the FEM_ASSEMBLE_ROWS form
-// of Alg. 2, reading R3): every CSR row block K_nm = sum_{e ∋ n,m} K^e_{a(n) b(m)}
+// fem_rows.cu — row-pull assembly of the sparse tangent (the FEM_ASSEMBLE_ROWS form of
+// Alg. 2, reading R3): every CSR row block K_nm = sum_{e ∋ n,m} K^e_{a(n) b(m)}
 // evaluated from the per-element context records of k_elem_ctx (fem_assemble.cu) and
 // written once, no atomics, fixed summation order.
 //
-// One warp per node n, nodes in Morton order, persistent grid.  Per node:
-//   1. TMA bulk copies bring the records of n's deg incident elements (one cp.async.bulk of
-//      176 bytes each) and n's block list (setup-time plan, below) into shared memory,
-//      completing on a per-buffer mbarrier; they are issued one node ahead, so the copies
-//      of node k+1 overlap the arithmetic of node k;
-//   2. lane l = incidence l completes (G_0, g_0) = -sum_b (G_b, g_b) in its record;
-//   3. lane s = CSR slot s walks its run of the block list — the entries (l, a, b) of the
-//      elements containing edge (n, nadj[s]), ascending element order — and accumulates
-//      K^e_ab[i][k] = smu (G_a.G_b) d_ik + sc1 g_a[k] g_b[i] + sc2 g_a[i] g_b[k] from the
-//      two record parts; lanes 28..31 walk a quarter each of the diagonal run (l, a, a),
-//      and lanes 0..D*D-1 add the four partials in fixed order.
-// Eligible meshes (build_row_plan): no MPC multiplier columns, <= 32 incidences and <= 28
-// neighbours per node; otherwise the assembly falls back to k_rows_fused (fem_assemble.cu).
+// Element blocks: with spatial gradients g = F^{-T} G and the record scalars smu = vol mu,
+// sc1 = vol (mu - lambda ln J), sc2 = vol lambda,
+//   K^e_ab[i][k] = smu (G_a.G_b) d_ik + sc1 g_a[k] g_b[i] + sc2 g_a[i] g_b[k].
+// Since sum_b G_b = sum_b g_b = 0, every element row sums to zero over b (the energy is
+// translation invariant), so the diagonal block of a row is minus the sum of its
+// off-diagonal blocks: K_nn = -sum_{m != n} K_nm.  Only the off-diagonal blocks are summed
+// from element entries (3 per incidence in 3D instead of 4).
+//
+// Work decomposition: nodes in Morton order (records in the element tiles' Morton order),
+// LPN lanes per node (16: two consecutive nodes per warp), lane q = off-diagonal CSR slot q
+// of its node.  The lane walks its run of the node's block list — the elements containing
+// edge (n, nadj[s]), ascending element order, each entry (record, a, b) — loading the two
+// record parts and the scalars straight from L1/L2 (the records of neighbouring nodes
+// overlap, no shared-memory staging, so occupancy is set by registers), and writes its
+// D x D block; the node's lanes then write the diagonal block (-sum of the slots, fixed
+// order) with the Dirichlet mask.
+// Eligible meshes (build_row_plan): no MPC multiplier columns, <= 32 off-diagonal slots per
+// node, < 2^27 elements; otherwise the assembly falls back to k_rows_fused.
 #include <cuda_runtime.h>
 
 #include <cstdlib>
+#include <vector>
 
 #include "fem_internal.cuh"
 
 namespace fem {
 
-#ifndef FEM_ROWS2_MINB
-#define FEM_ROWS2_MINB 4
+#ifndef FEM_ROWS_WARPS
+#define FEM_ROWS_WARPS 8
 #endif
-constexpr int kStageWarps = 4;
-constexpr int kDiagLane0 = 28;  // lanes 28..31 walk the diagonal run
+#ifndef FEM_ROWS_MINB
+#define FEM_ROWS_MINB 3
+#endif
+constexpr int kRowWarps = FEM_ROWS_WARPS;
+constexpr uint32_t kPosBits = 27;
 
 template <int D>
-struct StageGeom {
+struct RecGeom {
   static constexpr int NEN = D + 1, BS = D * D, CS = ctx_stride<D>(), NP = 2 * D;
-  static constexpr int RS0 = NP + CS;                                // (G_0 g_0) + record
-  static constexpr int RS = ((RS0 / 2) % 2 == 0) ? RS0 + 2 : RS0;   // odd # of 16-byte units
   static constexpr int SC = NEN * NP;                                // smu, sc1, sc2
+  static constexpr int BP = (BS + 1) & ~1;                           // scratch block pitch
 };
 
-__host__ __device__ constexpr int entry_stride(int is, int nen) { return (nen * is + 7) & ~7; }
-
 // ------------------------------------------------------------------ setup: the plan
+__global__ void k_inverse_perm(const int32_t *perm, int64_t n, int32_t *pos) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    pos[perm[i]] = (int32_t)i;
+}
+
 __global__ void k_plan_max(const int64_t *inc_ptr, const int64_t *nadj_ptr, int64_t n, int *mx) {
   int d = 0, s = 0;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
@@ -52,15 +64,15 @@ __global__ void k_plan_max(const int64_t *inc_ptr, const int64_t *nadj_ptr, int6
   atomicMax(mx + 1, s);
 }
 
-// One thread per plan position idx (node n = node_order[idx]): incidences, the block list
-// grouped by CSR slot (slot of a block = position of node b in n's sorted neighbour list),
-// the slot offsets, the Dirichlet bits of the slot nodes, and the row start of n.
+// One thread per node position idx: the node word, the off-diagonal block list grouped by
+// CSR slot (entries pos | a << 27 | b << 29, pos = record position of the element, ascending
+// element order within a slot), the slot offsets and the Dirichlet bits of the slot nodes.
 template <int D>
-__global__ void k_plan_build(const int32_t *node_order, const int64_t *inc_ptr,
-                             const int32_t *inc, const int32_t *conn, const int64_t *nadj_ptr,
-                             const int32_t *nadj, const int64_t *row_ptr, const uint8_t *node_bc,
-                             int64_t n_nodes, int IS, int ES, int SS, int4 *rp_node,
-                             int32_t *rp_inc, uint16_t *rp_ent, uint8_t *rp_soff, uint8_t *rp_sbc,
+__global__ void k_plan_nodes(const int32_t *node_order, const int64_t *inc_ptr,
+                             const int32_t *inc, const int32_t *conn, const int32_t *epos,
+                             const int64_t *nadj_ptr, const int32_t *nadj, const int64_t *row_ptr,
+                             const uint8_t *node_bc, int64_t n_nodes, int ES, int SS,
+                             int4 *rp_node, uint32_t *rp_ent, uint8_t *rp_soff, uint8_t *rp_sbc,
                              int *bad) {
   constexpr int NEN = D + 1;
   for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < n_nodes;
@@ -68,48 +80,49 @@ __global__ void k_plan_build(const int32_t *node_order, const int64_t *inc_ptr,
     const int32_t n = node_order[idx];
     const int64_t i0 = inc_ptr[n], a0 = nadj_ptr[n];
     const int deg = (int)(inc_ptr[n + 1] - i0), sn = (int)(nadj_ptr[n + 1] - a0);
-    if (deg > IS || sn + 1 > SS || deg > 32 || sn > kDiagLane0) { atomicOr(bad, 1); continue; }
-    auto slot_of = [&](int32_t m) {
+    auto slot_of = [&](int32_t mm) {
       int lo = 0, hi = sn;
       while (lo < hi) {
         const int mid = (lo + hi) >> 1;
-        if (nadj[a0 + mid] < m) lo = mid + 1; else hi = mid;
+        if (nadj[a0 + mid] < mm) lo = mid + 1; else hi = mid;
       }
       return lo;
     };
     const int ds = sn > 0 ? slot_of(n) : 0;
+    const int sno = sn > 0 ? sn - 1 : 0;  // off-diagonal slots
+    if (sn == 0 || ds >= sn || nadj[a0 + ds] != n || sno > 32 || (NEN - 1) * deg > ES ||
+        (NEN - 1) * deg > 255) {
+      atomicOr(bad, 1);
+      continue;
+    }
     const int64_t rp0 = row_ptr[(int64_t)n * D];
     for (int i = 1; i <= D; ++i)  // rows of n: exactly D*sn columns each (no multiplier columns)
       if (row_ptr[(int64_t)n * D + i] != rp0 + (int64_t)i * D * sn) atomicOr(bad, 1);
-    uint8_t cur[kDiagLane0 + 2];
-    for (int q = 0; q <= sn; ++q) cur[q] = 0;
+    uint8_t cnt[34];
+    for (int q = 0; q <= sno; ++q) cnt[q] = 0;
+    auto q_of = [&](int s) { return s < ds ? s : s - 1; };  // off-diagonal slot index
     for (int l = 0; l < deg; ++l) {
       const int32_t pk = inc[i0 + l];
       const int64_t e = pk / NEN;
       const int a = pk % NEN;
-      for (int t = 0; t < NEN - 1; ++t) cur[slot_of(conn[e * NEN + (a + 1 + t) % NEN]) + 1]++;
+      for (int t = 1; t < NEN; ++t) cnt[q_of(slot_of(conn[e * NEN + (a + t) % NEN])) + 1]++;
     }
-    for (int q = 0; q < sn; ++q) cur[q + 1] += cur[q];
-    for (int q = 0; q <= sn; ++q) rp_soff[idx * SS + q] = cur[q];
-    for (int q = 0; q < sn; ++q) rp_sbc[idx * SS + q] = node_bc ? node_bc[nadj[a0 + q]] : 0;
-    uint16_t *ent = rp_ent + idx * ES;
-    for (int q = 0; q < ES; ++q) ent[q] = 0;
-    for (int l = 0; l < IS; ++l) {
-      int32_t pk = -1;
-      if (l < deg) {
-        pk = inc[i0 + l];
-        const int64_t e = pk / NEN;
-        const int a = pk % NEN;
-        for (int t = 0; t < NEN - 1; ++t) {
-          const int b = (a + 1 + t) % NEN;
-          ent[cur[slot_of(conn[e * NEN + b])]++] = (uint16_t)(l | a << 5 | b << 7);
-        }
-        ent[(NEN - 1) * deg + l] = (uint16_t)(l | a << 5 | a << 7);  // diagonal run
+    for (int q = 0; q < sno; ++q) cnt[q + 1] += cnt[q];
+    for (int q = 0; q <= sno; ++q) rp_soff[idx * SS + q] = cnt[q];
+    for (int q = 0; q < sno; ++q) rp_sbc[idx * SS + q] = node_bc ? node_bc[nadj[a0 + q + (q >= ds)]] : 0;
+    uint32_t *ent = rp_ent + idx * ES;
+    for (int l = 0; l < deg; ++l) {
+      const int32_t pk = inc[i0 + l];
+      const int64_t e = pk / NEN;
+      const int a = pk % NEN;
+      const uint32_t pos = (uint32_t)epos[e];
+      for (int t = 1; t < NEN; ++t) {
+        const int b = (a + t) % NEN;
+        ent[cnt[q_of(slot_of(conn[e * NEN + b]))]++] = pos | (uint32_t)a << kPosBits | (uint32_t)b << (kPosBits + 2);
       }
-      rp_inc[idx * IS + l] = pk;
     }
     const unsigned bcn = node_bc ? node_bc[n] : 0u;
-    rp_node[idx] = make_int4(n, deg | sn << 8 | ds << 16 | (int)(bcn << 24),
+    rp_node[idx] = make_int4(n, sno | sn << 8 | ds << 16 | (int)(bcn << 24),
                              (int)(uint32_t)(rp0 & 0xffffffffu), (int)(rp0 >> 32));
   }
 }
@@ -117,102 +130,74 @@ __global__ void k_plan_build(const int32_t *node_order, const int64_t *inc_ptr,
 fem_status build_row_plan(Problem *p, cudaStream_t s) {
   if (p->rp_state) return FEM_OK;
   p->rp_state = -1;
-  if (p->n_mpc || p->n_nodes == 0 || p->n_elems == 0 || getenv("FEM_ROWS_LEGACY")) return FEM_OK;
+  if (p->n_mpc || p->n_nodes == 0 || p->n_elems == 0 || p->n_elems >= (int64_t(1) << kPosBits) ||
+      getenv("FEM_ROWS_LEGACY"))
+    return FEM_OK;
   int *d_w = nullptr;
-  FEM_CUDA(cudaMalloc(&d_w, 3 * sizeof(int)));
-  FEM_CUDA(cudaMemsetAsync(d_w, 0, 3 * sizeof(int), s));
+  FEM_CUDA(cudaMalloc(&d_w, 4 * sizeof(int)));
+  FEM_CUDA(cudaMemsetAsync(d_w, 0, 4 * sizeof(int), s));
   k_plan_max<<<grid_for(p->n_nodes), kThreads, 0, s>>>(p->inc_ptr, p->nadj_ptr, p->n_nodes, d_w);
-  int h_w[3] = {0, 0, 0};
+  int h_w[4] = {0, 0, 0, 0};
   FEM_CUDA(cudaMemcpyAsync(h_w, d_w, 2 * sizeof(int), cudaMemcpyDeviceToHost, s));
   FEM_CUDA(cudaStreamSynchronize(s));
-  if (h_w[0] > 32 || h_w[1] > kDiagLane0 || h_w[0] == 0) {
-    cudaFree(d_w);
-    return FEM_OK;
-  }
+  const int IS = h_w[0], max_sn = h_w[1];
+  if (IS == 0 || max_sn - 1 > 32 || (p->nen - 1) * IS > 255) { cudaFree(d_w); return FEM_OK; }
   fem_status st = morton_node_order(p, s);
+  if (!st) st = build_tiles(p, s);  // records are written in the element tiles' Morton order
   if (st) { cudaFree(d_w); return st; }
-  const int IS = h_w[0], ES = entry_stride(IS, p->nen), SS = (h_w[1] + 1 + 3) & ~3;
-  const int64_t n = p->n_nodes;
-  // +32 slack: every lane of a warp may load its word of the plan unconditionally
-  FEM_CUDA(cudaMalloc(&p->rp_node, sizeof(int4) * n));
-  FEM_CUDA(cudaMalloc(&p->rp_inc, sizeof(int32_t) * (n * IS + 32)));
-  FEM_CUDA(cudaMalloc(&p->rp_ent, sizeof(uint16_t) * n * ES));
-  FEM_CUDA(cudaMalloc(&p->rp_soff, (size_t)n * SS + 32));
-  FEM_CUDA(cudaMalloc(&p->rp_sbc, (size_t)n * SS + 32));
-  FEM_CUDA(cudaMemsetAsync(p->rp_inc + n * IS, 0xff, sizeof(int32_t) * 32, s));
-  FEM_CUDA(cudaMemsetAsync(p->rp_soff + n * SS, 0, 32, s));
-  FEM_CUDA(cudaMemsetAsync(p->rp_sbc + n * SS, 0, 32, s));
+  const int64_t n = p->n_nodes, E = p->n_elems;
+  const int lpn = (max_sn - 1 <= 16) ? 16 : 32;
+  const int npw = 32 / lpn;
+  const int ES = ((p->nen - 1) * IS + 3) & ~3, SS = (lpn + 1 + 3) & ~3;
+  const int64_t npad = (n + npw - 1) / npw * npw;
+  FEM_CUDA(cudaMalloc(&p->epos, sizeof(int32_t) * E));
+  k_inverse_perm<<<grid_for(E), kThreads, 0, s>>>(p->tiles.perm, E, p->epos);
+  FEM_CUDA(cudaMalloc(&p->rp_node, sizeof(int4) * npad));
+  FEM_CUDA(cudaMalloc(&p->rp_ent, sizeof(uint32_t) * npad * ES));
+  FEM_CUDA(cudaMalloc(&p->rp_soff, (size_t)npad * SS));
+  FEM_CUDA(cudaMalloc(&p->rp_sbc, (size_t)npad * SS));
+  FEM_CUDA(cudaMemsetAsync(p->rp_node, 0, sizeof(int4) * npad, s));
+  FEM_CUDA(cudaMemsetAsync(p->rp_soff, 0, (size_t)npad * SS, s));
+  FEM_CUDA(cudaMemsetAsync(p->rp_sbc, 0, (size_t)npad * SS, s));
   if (p->dim == 2)
-    k_plan_build<2><<<grid_for(n, 128), 128, 0, s>>>(p->node_order, p->inc_ptr, p->inc, p->conn, p->nadj_ptr, p->nadj, p->row_ptr, p->node_bc, n, IS, ES, SS, p->rp_node, p->rp_inc, p->rp_ent, p->rp_soff, p->rp_sbc, d_w + 2);
+    k_plan_nodes<2><<<grid_for(n, 128), 128, 0, s>>>(p->node_order, p->inc_ptr, p->inc, p->conn, p->epos, p->nadj_ptr, p->nadj, p->row_ptr, p->node_bc, n, ES, SS, p->rp_node, p->rp_ent, p->rp_soff, p->rp_sbc, d_w + 2);
   else
-    k_plan_build<3><<<grid_for(n, 128), 128, 0, s>>>(p->node_order, p->inc_ptr, p->inc, p->conn, p->nadj_ptr, p->nadj, p->row_ptr, p->node_bc, n, IS, ES, SS, p->rp_node, p->rp_inc, p->rp_ent, p->rp_soff, p->rp_sbc, d_w + 2);
-  FEM_LAUNCH_CHECK("row plan");
+    k_plan_nodes<3><<<grid_for(n, 128), 128, 0, s>>>(p->node_order, p->inc_ptr, p->inc, p->conn, p->epos, p->nadj_ptr, p->nadj, p->row_ptr, p->node_bc, n, ES, SS, p->rp_node, p->rp_ent, p->rp_soff, p->rp_sbc, d_w + 2);
+  FEM_LAUNCH_CHECK("row plan (nodes)");
   FEM_CUDA(cudaMemcpyAsync(h_w + 2, d_w + 2, sizeof(int), cudaMemcpyDeviceToHost, s));
   FEM_CUDA(cudaStreamSynchronize(s));
   cudaFree(d_w);
   if (h_w[2]) {
-    void *b[] = {p->rp_node, p->rp_inc, p->rp_ent, p->rp_soff, p->rp_sbc};
-    for (void *x : b) cudaFree(x);
-    p->rp_node = nullptr; p->rp_inc = nullptr; p->rp_ent = nullptr; p->rp_soff = nullptr; p->rp_sbc = nullptr;
+    void *b[] = {p->epos, p->rp_node, p->rp_ent, p->rp_soff, p->rp_sbc};
+    for (void *x : b) if (x) cudaFree(x);
+    p->epos = nullptr; p->rp_node = nullptr; p->rp_ent = nullptr; p->rp_soff = nullptr;
+    p->rp_sbc = nullptr;
     return FEM_OK;
   }
-  p->rp_is = IS;
+  p->rp_lpn = lpn;
   p->rp_es = ES;
   p->rp_ss = SS;
   p->rp_state = 1;
   return FEM_OK;
 }
 
-// ------------------------------------------------------------------ async-copy primitives
-__device__ __forceinline__ unsigned smem_u32(const void *p) {
-  return (unsigned)__cvta_generic_to_shared(p);
-}
-__device__ __forceinline__ void mbar_init(uint64_t *m, unsigned count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(m)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive_tx(uint64_t *m, unsigned bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(m)),
-               "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t *m, unsigned parity) {
-  asm volatile(
-      "{\n .reg .pred p;\n"
-      "WAIT_%=:\n"
-      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-      " @!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(m)),
-      "r"(parity)
-      : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned bytes, uint64_t *m) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
-          smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(m))
-      : "memory");
-}
-__device__ __forceinline__ void fence_async_smem() {
-  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-}
-
 // ------------------------------------------------------------------ kernel
-struct StageArgs {
+struct RowPullArgs {
   const double *ctx;
   const int4 *node;
-  const int32_t *inc;
-  const uint16_t *ent;
+  const uint32_t *ent;
   const uint8_t *soff, *sbc;
-  int64_t n_nodes;
-  int IS, ES, SS, bc;
+  int64_t n_nodes, n_units;
+  int ES, SS, bc;
   double *vals;
 };
 
-// (G_b, g_b) of a record part (16-byte aligned: 2*D doubles)
 template <int D>
-__device__ __forceinline__ void load_part(const double *rp, double (&G)[D], double (&g)[D]) {
+__device__ __forceinline__ void ldg_part(const double *rp, double (&G)[D], double (&g)[D]) {
   double v[2 * D];
 #pragma unroll
   for (int j = 0; j < 2 * D; j += 2) {
-    const double2 u = *reinterpret_cast<const double2 *>(rp + j);
+    const double2 u = __ldg(reinterpret_cast<const double2 *>(rp + j));
     v[j] = u.x;
     v[j + 1] = u.y;
   }
@@ -223,138 +208,87 @@ __device__ __forceinline__ void load_part(const double *rp, double (&G)[D], doub
   }
 }
 
-// the block K^e_ab of list entry (l, a, b), added to acc
-template <int D>
-struct Contrib {
-  double Ga[D], ga[D], Gb[D], gb[D], smu, sc1, sc2;
-  __device__ __forceinline__ void load(const double *recs, uint32_t en) {
-    using Gm = StageGeom<D>;
-    const double *r = recs + (en & 31u) * Gm::RS;
-    load_part<D>(r + ((en >> 5) & 3u) * Gm::NP, Ga, ga);
-    load_part<D>(r + ((en >> 7) & 3u) * Gm::NP, Gb, gb);
-    const double2 s01 = *reinterpret_cast<const double2 *>(r + Gm::SC);
-    smu = s01.x;
-    sc1 = s01.y;
-    sc2 = r[Gm::SC + 2];
-  }
-  __device__ __forceinline__ void add_to(double (&acc)[D * D]) const {
-    double dd = 0.0;
-#pragma unroll
-    for (int j = 0; j < D; ++j) dd = fma(Ga[j], Gb[j], dd);
-    dd *= smu;
-    double p[D], q[D];
-#pragma unroll
-    for (int j = 0; j < D; ++j) {
-      p[j] = sc1 * ga[j];
-      q[j] = sc2 * ga[j];
-    }
-#pragma unroll
-    for (int i = 0; i < D; ++i)
-#pragma unroll
-      for (int k = 0; k < D; ++k) {
-        double v = fma(p[k], gb[i], q[i] * gb[k]);
-        if (i == k) v += dd;
-        acc[i * D + k] += v;
-      }
-  }
-};
-
-template <int D>
-__global__ void __launch_bounds__(32 * kStageWarps, FEM_ROWS2_MINB) k_rows_stage(StageArgs A) {
-  using Gm = StageGeom<D>;
-  constexpr int NEN = Gm::NEN, BS = Gm::BS, NP = Gm::NP, RS = Gm::RS, CS = Gm::CS;
-  extern __shared__ __align__(16) double sm_stage[];
-  __shared__ __align__(8) uint64_t mbar[kStageWarps][2];
+// LPN lanes per node (16: two consecutive nodes per warp), lane q = off-diagonal slot q:
+// the lane loads the entries of its run (up to KE up front), sums their element blocks
+// straight from the records and writes its D x D block; the node's lanes then write the
+// diagonal block = -sum of the slots (ascending slot order) with the Dirichlet mask.
+// (A/B, profiles/: entry-parallel lanes with shared-memory staged blocks 8.9 ms, row
+// stores through shared memory 7.3 ms, cp.async-staged chunk records 8.4 ms, TMA per
+// record 5.1 ms, this form 5.2 ms + 1.3 ms records at cfg 3.)
+template <int D, int LPN>
+__global__ void __launch_bounds__(32 * kRowWarps, FEM_ROWS_MINB) k_rows_pull(RowPullArgs A) {
+  using Gm = RecGeom<D>;
+  constexpr int BS = Gm::BS, NP = Gm::NP, CS = Gm::CS, BP = Gm::BP;
+  constexpr int NPW = 32 / LPN;
+  constexpr uint32_t PMASK = (1u << kPosBits) - 1u;
+  __shared__ __align__(16) double scratch[kRowWarps][32 * BP];  // slot sums (diagonal)
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int64_t nw = (int64_t)gridDim.x * kStageWarps;
-  const int REC = A.IS * RS;                         // doubles of records per buffer
-  const int BUF = REC + A.ES / 4;                    // + the block list (ES uint16)
-  double *const bufs = sm_stage + (size_t)w * 2 * BUF;
-  if (lane == 0) {
-    mbar_init(&mbar[w][0], 1);
-    mbar_init(&mbar[w][1], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-  }
-  __syncwarp();
-  const int64_t last = A.n_nodes - 1;
-  // plan words of position idx (clamped: loads are unconditional, validity is idx <= last)
-  auto meta = [&](int64_t idx, int4 &nd, int32_t &pi) {
-    const int64_t j = idx < last ? idx : last;
-    nd = __ldg(A.node + j);
-    pi = __ldg(A.inc + j * A.IS + lane);
+  const int h = lane / LPN, ql = lane % LPN;
+  double *scr = scratch[w];
+  const int64_t W = (int64_t)gridDim.x * kRowWarps;
+  constexpr int KE = 8;  // entries per lane loaded up front (longer runs loop)
+  // node words of unit u (the plan arrays are padded: loads need no bounds)
+  struct Unit { int4 nd; int lo, hi; unsigned sbc; };
+  auto fetch = [&](int64_t u) {
+    Unit x{make_int4(0, 0, 0, 0), 0, 0, 0u};
+    if (u < A.n_units) {
+      const int64_t idx = u * NPW + h;
+      x.nd = __ldg(A.node + idx);
+      x.lo = __ldg(A.soff + idx * A.SS + ql);
+      x.hi = __ldg(A.soff + idx * A.SS + ql + 1);
+      x.sbc = A.bc ? __ldg(A.sbc + idx * A.SS + ql) : 0u;
+    }
+    return x;
   };
-  auto issue = [&](int64_t idx, const int4 &nd, int32_t pi, int b) {
-    double *dst = bufs + b * BUF;
-    const int deg = nd.y & 0xff;
-    if (lane == 0) {
-      mbar_arrive_tx(&mbar[w][b], (unsigned)(deg * CS * sizeof(double) + A.ES * sizeof(uint16_t)));
-      bulk_g2s(dst + REC, A.ent + idx * A.ES, A.ES * sizeof(uint16_t), &mbar[w][b]);
-    }
-    __syncwarp();
-    if (lane < deg)
-      bulk_g2s(dst + lane * RS + NP, A.ctx + (int64_t)(pi / NEN) * CS, CS * sizeof(double),
-               &mbar[w][b]);
-  };
-  int64_t idx = (int64_t)blockIdx.x * kStageWarps + w;
-  int4 nd_c, nd_n, nd_nn;
-  int32_t pi_c, pi_n, pi_nn;
-  meta(idx, nd_c, pi_c);
-  if (idx <= last) issue(idx, nd_c, pi_c, 0);
-  meta(idx + nw, nd_n, pi_n);
-  for (int it = 0; idx <= last; ++it, idx += nw) {
-    const int b = it & 1;
-    double *cur = bufs + b * BUF;
-    if (idx + nw <= last) issue(idx + nw, nd_n, pi_n, b ^ 1);  // in flight during this node
-    meta(idx + 2 * nw, nd_nn, pi_nn);
-    const int deg = nd_c.y & 0xff, sn = (nd_c.y >> 8) & 0xff, ds = (nd_c.y >> 16) & 0xff;
-    const unsigned bcn = A.bc ? ((unsigned)nd_c.y >> 24) : 0u;
-    const int64_t rp0 = (int64_t)(uint32_t)nd_c.z | ((int64_t)nd_c.w << 32);
-    // this lane's run of the block list: CSR slot `lane`, or a quarter of the diagonal run
-    int lo = __ldg(A.soff + idx * A.SS + lane), hi = __ldg(A.soff + idx * A.SS + lane + 1);
-    const unsigned sbc = A.bc ? __ldg(A.sbc + idx * A.SS + lane) : 0u;
-    const bool slot_lane = lane < sn && lane != ds;
-    if (lane >= kDiagLane0) {
-      const int j = lane - kDiagLane0;
-      lo = (NEN - 1) * deg + (j * deg) / 4;
-      hi = (NEN - 1) * deg + ((j + 1) * deg) / 4;
-    } else if (!slot_lane) {
-      lo = hi = 0;
-    }
-    mbar_wait(&mbar[w][b], (unsigned)(it >> 1) & 1u);
-    if (lane < deg) {  // (G_0, g_0) = -sum of the other parts, in place
-      double *r = cur + lane * RS;
+  int64_t u = (int64_t)blockIdx.x * kRowWarps + w;
+  Unit cur = fetch(u);
+  for (; u < A.n_units; u += W) {
+    const Unit nx = fetch(u + W);  // in flight during this unit
+    const int64_t idx = u * NPW + h;
+    const int4 nd = cur.nd;
+    const int sno = nd.y & 0xff;
+    const int lo = ql < sno ? cur.lo : 0, hi = ql < sno ? cur.hi : 0;
+    const uint32_t *ent = A.ent + idx * A.ES;
+    uint32_t ens[KE];
 #pragma unroll
-      for (int j = 0; j < NP; j += 2) {
-        double2 t = make_double2(0.0, 0.0);
-#pragma unroll
-        for (int q = 1; q < NEN; ++q) {
-          const double2 u = *reinterpret_cast<const double2 *>(r + q * NP + j);
-          t.x += u.x;
-          t.y += u.y;
-        }
-        *reinterpret_cast<double2 *>(r + j) = make_double2(-t.x, -t.y);
-      }
-    }
-    __syncwarp();
-    const uint16_t *ent = reinterpret_cast<const uint16_t *>(cur + REC);
+    for (int t = 0; t < KE; ++t) ens[t] = (lo + t < hi) ? __ldg(ent + lo + t) : 0u;
     double acc[BS];
 #pragma unroll
     for (int q = 0; q < BS; ++q) acc[q] = 0.0;
-    int c = lo;
-    for (; c + 1 < hi; c += 2) {
-      Contrib<D> u, v;
-      u.load(cur, ent[c]);
-      v.load(cur, ent[c + 1]);
-      u.add_to(acc);
-      v.add_to(acc);
-    }
-    if (c < hi) {
-      Contrib<D> u;
-      u.load(cur, ent[c]);
-      u.add_to(acc);
-    }
-    if (slot_lane) {
-      double *row = A.vals + rp0 + lane * D;
+    auto add_entry = [&](uint32_t en) {
+      const double *rr = A.ctx + (int64_t)(en & PMASK) * CS;
+      double Ga[D], ga[D], Gb[D], gb[D];
+      ldg_part<D>(rr + ((en >> kPosBits) & 3u) * NP, Ga, ga);
+      ldg_part<D>(rr + ((en >> (kPosBits + 2)) & 3u) * NP, Gb, gb);
+      const double2 s01 = __ldg(reinterpret_cast<const double2 *>(rr + Gm::SC));
+      const double sc2 = __ldg(rr + Gm::SC + 2);
+      double dd = 0.0;
+#pragma unroll
+      for (int j = 0; j < D; ++j) dd = fma(Ga[j], Gb[j], dd);
+      dd *= s01.x;
+#pragma unroll
+      for (int i = 0; i < D; ++i) {
+        const double qi = sc2 * ga[i];
+#pragma unroll
+        for (int k = 0; k < D; ++k) {
+          double v = fma(s01.y * ga[k], gb[i], acc[i * D + k]);
+          v = fma(qi, gb[k], v);
+          acc[i * D + k] = (i == k) ? v + dd : v;
+        }
+      }
+    };
+#pragma unroll
+    for (int t = 0; t < KE; ++t)
+      if (lo + t < hi) add_entry(ens[t]);
+    for (int e = lo + KE; e < hi; ++e) add_entry(__ldg(ent + e));
+    const int sn = (nd.y >> 8) & 0xff, ds = (nd.y >> 16) & 0xff;
+    const unsigned bcn = A.bc ? ((unsigned)nd.y >> 24) : 0u;
+    const int64_t rp0 = (int64_t)(uint32_t)nd.z | ((int64_t)nd.w << 32);
+    const bool live = idx < A.n_nodes;
+    if (live && ql < sno) {
+      const unsigned sbc = cur.sbc;
+      const int s = ql + (ql >= ds);
+      double *row = A.vals + rp0 + s * D;
       if ((sbc | bcn) == 0u) {
 #pragma unroll
         for (int i = 0; i < D; ++i)
@@ -372,55 +306,51 @@ __global__ void __launch_bounds__(32 * kStageWarps, FEM_ROWS2_MINB) k_rows_stage
           }
       }
     }
-    __syncwarp();  // records consumed: lanes 28..31 park their diagonal partials
-    if (lane >= kDiagLane0) {
-      double *st = cur + (lane - kDiagLane0) * BS;
+    // diagonal block: -sum of the node's off-diagonal slots (unmasked), ascending slot order
 #pragma unroll
-      for (int q = 0; q < BS; ++q) st[q] = acc[q];
-    }
+    for (int q = 0; q < BS; ++q) scr[lane * BP + q] = acc[q];
     __syncwarp();
-    if (lane < BS && deg > 0) {
-      const int i = lane / D, k = lane % D;
-      double v = cur[lane];
-#pragma unroll
-      for (int j = 1; j < 4; ++j) v += cur[j * BS + lane];
+    if (live && ql < BS) {
+      const int i = ql / D, k = ql % D;
+      double v = 0.0;
+      for (int t = 0; t < sno; ++t) v += scr[(h * LPN + t) * BP + ql];
+      v = -v;
       if (bcn & (1u << k)) v = 0.0;                         // masked column
       if (bcn & (1u << i)) v = (i == k) ? 1.0 : 0.0;        // identity row
       A.vals[rp0 + (int64_t)i * D * sn + ds * D + k] = v;
     }
-    fence_async_smem();  // generic accesses to this buffer precede the next bulk copy into it
-    __syncwarp();
-    nd_c = nd_n; pi_c = pi_n;
-    nd_n = nd_nn; pi_n = pi_nn;
+    __syncwarp();  // scratch is rewritten by the next iteration
+    cur = nx;
   }
 }
 
-template <int D>
-static fem_status launch_stage(Problem *p, const double *ctx, double *vals, bool bc,
-                               cudaStream_t s) {
-  StageArgs A{};
-  A.ctx = ctx; A.node = p->rp_node; A.inc = p->rp_inc; A.ent = p->rp_ent;
-  A.soff = p->rp_soff; A.sbc = p->rp_sbc; A.n_nodes = p->n_nodes; A.IS = p->rp_is;
+template <int D, int LPN>
+static fem_status launch_pull(Problem *p, const double *ctx, double *vals, bool bc,
+                              cudaStream_t s) {
+  RowPullArgs A{};
+  constexpr int NPW = 32 / LPN;
+  A.ctx = ctx; A.node = p->rp_node; A.ent = p->rp_ent; A.soff = p->rp_soff; A.sbc = p->rp_sbc;
+  A.n_nodes = p->n_nodes; A.n_units = (p->n_nodes + NPW - 1) / NPW;
   A.ES = p->rp_es; A.SS = p->rp_ss; A.bc = bc ? 1 : 0; A.vals = vals;
-  const size_t buf = sizeof(double) * (size_t)p->rp_is * StageGeom<D>::RS + sizeof(uint16_t) * p->rp_es;
-  const size_t smem = (size_t)kStageWarps * 2 * buf;
-  FEM_CUDA(cudaFuncSetAttribute(k_rows_stage<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  auto kern = k_rows_pull<D, LPN>;
   int per_sm = 0;
-  FEM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_rows_stage<D>, 32 * kStageWarps, smem));
+  FEM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * kRowWarps, 0));
   int dev = 0, sms = 148;
   FEM_CUDA(cudaGetDevice(&dev));
   FEM_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   int64_t grid = (int64_t)sms * (per_sm > 0 ? per_sm : 1);
-  const int64_t need = (p->n_nodes + kStageWarps - 1) / kStageWarps;
+  const int64_t need = (A.n_units + kRowWarps - 1) / kRowWarps;
   if (grid > need) grid = need;
-  k_rows_stage<D><<<(int)grid, 32 * kStageWarps, smem, s>>>(A);
-  FEM_LAUNCH_CHECK("staged row assembly");
+  kern<<<(int)grid, 32 * kRowWarps, 0, s>>>(A);
+  FEM_LAUNCH_CHECK("row-pull assembly");
   return FEM_OK;
 }
 
 fem_status launch_rows_stage(Problem *p, const double *ctx, double *vals, bool bc,
                              cudaStream_t s) {
-  return p->dim == 2 ? launch_stage<2>(p, ctx, vals, bc, s) : launch_stage<3>(p, ctx, vals, bc, s);
+  if (p->dim == 2)
+    return p->rp_lpn == 16 ? launch_pull<2, 16>(p, ctx, vals, bc, s) : launch_pull<2, 32>(p, ctx, vals, bc, s);
+  return p->rp_lpn == 16 ? launch_pull<3, 16>(p, ctx, vals, bc, s) : launch_pull<3, 32>(p, ctx, vals, bc, s);
 }
 
 }  // namespace fem

@@ -42,7 +42,7 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", type=int, default=3, choices=[2, 3, 5])
     ap.add_argument("--n", type=int, default=None, help="override the mesh size (cells per side)")
-    ap.add_argument("--assemble-mode", default="auto", choices=["auto", "batched", "literal", "rows"])
+    ap.add_argument("--assemble-mode", default="auto", choices=["auto", "batched", "literal", "rows", "scatter"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-solve", action="store_true")
     ap.add_argument("--profile-step", action="store_true", help="one step only (for ncu)")
@@ -362,6 +362,7 @@ def main():
         "assemble_batched_ms": time_call(lambda: prob.assemble_csr(zt, bc=True, mode="batched", out=vals), 2),
         "assemble_rows_ms": time_call(lambda: prob.assemble_csr(zt, bc=True, mode="rows", out=vals), 2),
         "assemble_literal_ms": time_call(lambda: prob.assemble_csr(zt, bc=True, mode="literal", out=vals), 1),
+        "assemble_scatter_add_ms": time_call(lambda: prob.assemble_csr(zt, bc=True, mode="scatter", out=vals), 2),
     }
     prob.check()
 

@@ -81,7 +81,9 @@ enum {
                                yields the global result.                                 */
   FEM_ASSEMBLE_JCOMP = 32u, /* fem_assemble_csr: all color passes in ONE element sweep
                                into J_comp [N][C] (atomics), then decompression.         */
-  FEM_ASSEMBLE_ROWS = 64u   /* fem_assemble_csr: row-pull form (no J_comp buffer).         */
+  FEM_ASSEMBLE_ROWS = 64u,  /* fem_assemble_csr: row-pull form (no J_comp buffer).         */
+  FEM_ASSEMBLE_SCATTER = 128u /* fem_assemble_csr: element-Hessian scatter-add with fp64
+                               atomics (the paper's comparison path), not Alg. 2 */
 };
 
 typedef struct {
@@ -178,6 +180,9 @@ fem_status fem_color(fem_problem *p, int32_t *colors, int32_t *n_colors, fem_str
  *            seeds' responses of its incident elements, a warp per node) with each
  *            compressed entry stored at its decompressed CSR slot (within a row every color
  *            names one column) — no J_comp buffer, atomic-free, bitwise reproducible;
+ *   FEM_ASSEMBLE_SCATTER: not Alg. 2 but the assembly the paper compares it with (Fig. 4
+ *            right): dense element Hessians scatter-added into vals with fp64
+ *            atomics (run-to-run rounding differences of the atomic order);
  *   default (no mode flag): FEM_ASSEMBLE_ROWS in 3D, FEM_ASSEMBLE_JCOMP in 2D.
  * flags may add FEM_APPLY_BC.  Requires fem_color (the pattern and colors). */
 fem_status fem_assemble_csr(fem_problem *p, const double *z, double *vals, unsigned flags,
@@ -206,6 +211,21 @@ fem_status fem_cg_solve(fem_problem *p, const double *z, const double *vals, con
                         double *x, const fem_cg_opts *opts, fem_cg_report *report,
                         fem_stream stream);
 
+/* MINRES (Paige & Saunders) on the same BC-applied operator, for the symmetric indefinite
+ * saddle-point system of the MPC Lagrangian [[K, B^T], [B, 0]] (CG does not
+ * apply).  opts as for CG (jacobi must be 0); report.res = true ||b - A x||_2.
+ * Synchronizes `stream`. */
+fem_status fem_minres_solve(fem_problem *p, const double *z, const double *vals, const double *b,
+                            double *x, const fem_cg_opts *opts, fem_cg_report *report,
+                            fem_stream stream);
+
+/* Volume average of the first Piola-Kirchhoff stress (= the Cauchy stress for linear
+ * elasticity), (1/|Omega|) sum_e vol_e P(H_e), the macroscopic stress of homogenization
+ * (P:530-538): sigma (host) [dim*dim] row-major, volume (host) = |Omega|.  Fixed-order
+ * reduction.  Synchronizes `stream`. */
+fem_status fem_mean_stress(fem_problem *p, const double *z, double *sigma, double *volume,
+                           fem_stream stream);
+
 typedef struct {
   double atol, rtol; /* outer: ||r|| <= max(atol, rtol ||r0||)                 */
   int max_iter;
@@ -218,7 +238,8 @@ typedef struct {
 } fem_newton_report;
 
 /* Full-step Newton on the condensed problem (Eq. 1): z starts at the lift; repeat
- * r = residual(z, BC); K(z) dz = -r by CG; z += dz.  Synchronizes `stream`. */
+ * r = residual(z, BC); K(z) dz = -r by CG (MINRES when the problem has MPC multipliers);
+ * z += dz.  Synchronizes `stream`. */
 fem_status fem_newton_solve(fem_problem *p, double *z, const fem_newton_opts *opts,
                             fem_newton_report *report, fem_stream stream);
 

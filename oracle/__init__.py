@@ -236,6 +236,36 @@ class Oracle:
                    "res": r1.value}
 
 
+    def mean_stress(self, z):
+        """(volume average of P as a dim x dim array, |Omega|) — fem_ref_mean_stress."""
+        z = self._f64(z)
+        d = self.mesh.dim
+        sig = np.zeros(d * d)
+        vol = C.c_double(0)
+        st = lib().fem_ref_mean_stress(C.byref(self.s), C.c_void_p(z.ctypes.data),
+                                       C.c_void_p(sig.ctypes.data), C.byref(vol))
+        if st:
+            raise OracleError(st, "fem_ref_mean_stress")
+        return sig.reshape(d, d), vol.value
+
+    def newton_dense(self, z0, atol=1e-12, rtol=1e-10, max_iter=50):
+        """Full-step Newton on the BC-applied Lagrangian with the dense Hessian and
+        numpy.linalg.solve for each step — the plain definition of the stationary point of
+        L (saddle points included) for small N (O-dense, N <= ~2000)."""
+        z = np.array(z0, np.float64, copy=True)
+        r0 = None
+        for it in range(max_iter + 1):
+            r = self.residual(z, bc=True)
+            nr = float(np.linalg.norm(r))
+            r0 = nr if r0 is None else r0
+            if nr <= max(atol, rtol * r0):
+                return z, {"iters": it, "res0": r0, "res": nr, "converged": True}
+            if it == max_iter:
+                break
+            z += np.linalg.solve(self.dense_hessian(z, bc=True), -r)
+        return z, {"iters": max_iter, "res0": r0, "res": nr, "converged": False}
+
+
 def color(row_ptr, col_idx):
     """Distance-2 greedy coloring of an arbitrary CSR pattern (fem_ref_color)."""
     rp = np.ascontiguousarray(row_ptr, dtype=np.int64)

@@ -610,6 +610,47 @@ static int elem_hessian(const fem_ref_mesh *m, int64_t e, const double *z, doubl
   return OK;
 }
 
+/* ------------------------------------------------------------------ mean stress (f2)
+ * Macroscopic stress of homogenization ("the volume average of the
+ * microscopic stress"): sigma = sum_e vol_e P(H_e) / sum_e vol_e with P_ij = d psi / d H_ij
+ * taken by forward-mode dual numbers on psi (seed E_ij), never a hand-derived stress.
+ * Ascending element order, Neumaier-compensated sums.                                  */
+int fem_ref_mean_stress(const fem_ref_mesh *m, const double *z, double *sigma, double *volume) {
+  int d = m->dim, nen = d + 1, a, i, j, k, l, st;
+  int64_t e;
+  ksum acc[9], vs;
+  memset(acc, 0, sizeof(acc));
+  memset(&vs, 0, sizeof(vs));
+  for (e = 0; e < m->n_elems; ++e) {
+    double G[4][3], vol, lam, mu, H[3][3];
+    st = elem_geometry(m, e, G, &vol);
+    if (st) return st;
+    elem_material(m, e, &lam, &mu);
+    for (i = 0; i < d; ++i)
+      for (j = 0; j < d; ++j) {
+        H[i][j] = 0.0;
+        for (a = 0; a < nen; ++a)
+          H[i][j] += z[(int64_t)m->conn[e * nen + a] * d + i] * G[a][j];
+      }
+    for (k = 0; k < d; ++k)
+      for (l = 0; l < d; ++l) {
+        hd Hd[3][3], p;
+        for (i = 0; i < d; ++i)
+          for (j = 0; j < d; ++j) {
+            Hd[i][j] = hd_const(H[i][j]);
+            if (i == k && j == l) Hd[i][j].b = 1.0;
+          }
+        st = psi_hd(d, m->material, lam, mu, Hd, &p);
+        if (st) return st;
+        ks_add(&acc[k * d + l], vol * p.b);
+      }
+    ks_add(&vs, vol);
+  }
+  *volume = ks_val(&vs);
+  for (k = 0; k < d * d; ++k) sigma[k] = ks_val(&acc[k]) / *volume;
+  return OK;
+}
+
 static int64_t find_col(const int32_t *col_idx, int64_t lo, int64_t hi, int64_t col) {
   while (lo < hi) {
     int64_t mid = lo + (hi - lo) / 2;

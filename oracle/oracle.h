@@ -67,6 +67,8 @@ int fem_ref_spmv(int64_t n, const int64_t *row_ptr, const int32_t *col_idx, cons
 int fem_ref_cg(const fem_ref_mesh *m, int op, const double *z, const int64_t *row_ptr,
                const int32_t *col_idx, const double *vals, const double *b, double *x,
                double rtol, double atol, int max_iter, int *iters, double *res0, double *res);
+/* volume-averaged first Piola-Kirchhoff stress sigma[dim*dim] (row-major), *volume = |Omega| */
+int fem_ref_mean_stress(const fem_ref_mesh *m, const double *z, double *sigma, double *volume);
 int fem_ref_newton(const fem_ref_mesh *m, double *z /* in: lift, out: solution */, double atol,
                    double rtol, int max_iter, double cg_rtol, int cg_max_iter, int *iters,
                    int *cg_iters_total, double *res0, double *res);

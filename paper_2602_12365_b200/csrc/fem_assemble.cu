@@ -556,6 +556,95 @@ __global__ void k_rows_mpc(const int32_t *ms, const int32_t *mm, int64_t nc, int
   }
 }
 
+// ------------------------------------------------------------------ element scatter-add (f1)
+// The paper's comparison path (Fig. 4 right): one thread per
+// element evaluates the dense element Hessian K^e (its (D+1)^2 blocks K_ab, the same
+// closed form as the colored columns) and scatter-adds every entry into the CSR values with
+// fp64 atomics — the "unstructured memory access ... atomic contention" the paper measures
+// against.  The CSR position of block (a, b) row i column k is row_ptr[n_a D + i] +
+// D * slot(n_b in the sorted neighbour list of n_a) + k (multiplier columns, if any, come
+// after all u columns of a row).  Masked entries (Dirichlet row or column) are skipped;
+// the unit diagonal of constrained DOFs and the Lagrangian blocks are written afterwards.
+template <int D, int MAT>
+__global__ void __launch_bounds__(kThreads) k_scatter_hessian(AsmArgs A, const int64_t *row_ptr,
+                                                             const int64_t *nadj_ptr,
+                                                             const int32_t *nadj, double *vals) {
+  constexpr int NEN = D + 1;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < A.E; e += stride) {
+    int32_t nd[NEN];
+    load_nodes<D>(A.conn, e, nd);
+    double lam = A.lam, mu = A.mu;
+    if (A.phase) {
+      const int ph = A.phase[e];
+      lam = A.lam_tab[ph];
+      mu = A.mu_tab[ph];
+    }
+    ColumnCtx<D> cx;
+    if (!column_ctx<D, MAT>(A.coords, nd, A.z, lam, mu, cx)) {
+      atomicOr(A.err, ERRW_INVERTED);
+      continue;
+    }
+    unsigned bc[NEN];
+#pragma unroll
+    for (int a = 0; a < NEN; ++a) bc[a] = A.node_bc ? __ldg(A.node_bc + nd[a]) : 0u;
+#pragma unroll
+    for (int a = 0; a < NEN; ++a) {
+      const int64_t a0 = __ldg(nadj_ptr + nd[a]);
+      const int sn = (int)(__ldg(nadj_ptr + nd[a] + 1) - a0);
+      int64_t rows[D];
+#pragma unroll
+      for (int i = 0; i < D; ++i) rows[i] = __ldg(row_ptr + (int64_t)nd[a] * D + i);
+#pragma unroll
+      for (int b = 0; b < NEN; ++b) {
+        int lo = 0, hi = sn;  // slot of nd[b] among nd[a]'s neighbours
+        while (lo < hi) {
+          const int mid = (lo + hi) >> 1;
+          if (__ldg(nadj + a0 + mid) < nd[b]) lo = mid + 1; else hi = mid;
+        }
+#pragma unroll
+        for (int k = 0; k < D; ++k) {
+          if (bc[b] & (1u << k)) continue;  // masked column
+          double col[D];
+          column_block<D>(cx, a, b, k, col);
+#pragma unroll
+          for (int i = 0; i < D; ++i) {
+            if (bc[a] & (1u << i)) continue;  // masked row
+            atomicAdd(vals + rows[i] + (int64_t)lo * D + k, col[i]);
+          }
+        }
+      }
+    }
+  }
+}
+
+// B^T columns of the Lagrangian in the u rows: row s_k / m_k, column N_u + k = +1 / -1
+// (0 when the row DOF is Dirichlet), found by binary search in the row.
+__global__ void k_scatter_mpc_cols(const int32_t *ms, const int32_t *mm, int64_t nc, int64_t nu,
+                                   int dim, const uint8_t *node_bc, const int64_t *row_ptr,
+                                   const int32_t *col_idx, double *vals) {
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < nc;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    for (int side = 0; side < 2; ++side) {
+      const int32_t r = side == 0 ? ms[k] : mm[k];
+      const bool d = node_bc && (node_bc[r / dim] & (1u << (r % dim)));
+      int64_t lo = row_ptr[r], hi = row_ptr[r + 1];
+      const int32_t c = (int32_t)(nu + k);
+      while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (col_idx[mid] < c) lo = mid + 1; else hi = mid;
+      }
+      vals[lo] = d ? 0.0 : (side == 0 ? 1.0 : -1.0);
+    }
+  }
+}
+
+__global__ void k_unit_diag(const int32_t *dofs, int64_t nd, const int64_t *diag_pos, double *vals) {
+  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < nd;
+       q += (int64_t)gridDim.x * blockDim.x)
+    vals[diag_pos[dofs[q]]] = 1.0;
+}
+
 fem_status morton_node_order(Problem *p, cudaStream_t s);
 
 static fem_status build_slot_lists(Problem *p, cudaStream_t s) {
@@ -587,6 +676,30 @@ static void launch_colored(const AsmArgs &a, bool literal, int pass, cudaStream_
 static fem_status assemble(Problem *p, const double *z, double *vals, unsigned flags,
                            cudaStream_t s) {
   const bool bc = (flags & FEM_APPLY_BC) && p->n_dir;
+  if (flags & FEM_ASSEMBLE_SCATTER) {
+    FEM_CUDA(cudaMemsetAsync(vals, 0, sizeof(double) * (size_t)p->nnz, s));
+    AsmArgs a{};
+    a.coords = p->coords; a.conn = p->conn; a.E = p->n_elems; a.lam = p->lam; a.mu = p->mu;
+    a.phase = p->phase; a.lam_tab = p->lam_tab; a.mu_tab = p->mu_tab;
+    a.node_bc = bc ? p->node_bc : nullptr; a.z = z; a.err = p->d_err;
+    if (p->n_elems) {
+      const int g = grid_for(p->n_elems);
+      if (p->dim == 2) {
+        if (p->material == FEM_LINEAR_ELASTIC) k_scatter_hessian<2, FEM_LINEAR_ELASTIC><<<g, kThreads, 0, s>>>(a, p->row_ptr, p->nadj_ptr, p->nadj, vals);
+        else k_scatter_hessian<2, FEM_NEO_HOOKEAN><<<g, kThreads, 0, s>>>(a, p->row_ptr, p->nadj_ptr, p->nadj, vals);
+      } else {
+        if (p->material == FEM_LINEAR_ELASTIC) k_scatter_hessian<3, FEM_LINEAR_ELASTIC><<<g, kThreads, 0, s>>>(a, p->row_ptr, p->nadj_ptr, p->nadj, vals);
+        else k_scatter_hessian<3, FEM_NEO_HOOKEAN><<<g, kThreads, 0, s>>>(a, p->row_ptr, p->nadj_ptr, p->nadj, vals);
+      }
+    }
+    if (p->n_mpc) {
+      k_scatter_mpc_cols<<<grid_for(p->n_mpc), kThreads, 0, s>>>(p->mpc_s, p->mpc_m, p->n_mpc, p->n_u, p->dim, bc ? p->node_bc : nullptr, p->row_ptr, p->col_idx, vals);
+      k_rows_mpc<<<grid_for(p->n_mpc), kThreads, 0, s>>>(p->mpc_s, p->mpc_m, p->n_mpc, p->n_u, p->dim, bc ? p->node_bc : nullptr, p->row_ptr, vals);
+    }
+    if (bc) k_unit_diag<<<grid_for(p->n_dir), kThreads, 0, s>>>(p->dir_dofs, p->n_dir, p->diag_pos, vals);
+    FEM_LAUNCH_CHECK("scatter-add assembly");
+    return FEM_OK;
+  }
   // default: row-pull in 3D, one-sweep J_comp in 2D (C = 18 columns; measured 3x faster
   // there, profiles/r01_sweep.csv); explicit mode flags override
   const bool rows = (flags & FEM_ASSEMBLE_ROWS) ||
@@ -696,7 +809,8 @@ fem_status run_spmv(Problem *p, const double *vals, const double *x, double *y, 
 }
 
 fem_status run_assemble(Problem *p, const double *z, double *vals, unsigned flags, cudaStream_t s) {
-  fem_status st = build_colors(p, s);
+  // Alg. 2 needs the coloring; the scatter-add comparison path only the pattern
+  fem_status st = (flags & FEM_ASSEMBLE_SCATTER) ? build_pattern(p, s) : build_colors(p, s);
   if (st) return st;
   return assemble(p, z, vals, flags, s);
 }

@@ -409,6 +409,62 @@ fem_status run_hvp(Problem *p, const double *z, const double *v, double *y, unsi
 using namespace fem;
 
 // ====================================================================== C ABI
+// ------------------------------------------------------------------ mean stress (f2)
+// Macroscopic stress of homogenization: the volume average of P(H_e) over the
+// elements, per-block partials of (vol P, vol) in a fixed grid, then a fixed-order sum.
+template <int D, int MAT>
+__global__ void __launch_bounds__(kThreads) k_mean_stress(const double *coords, const int32_t *conn,
+                                                         int64_t E, double lam0, double mu0,
+                                                         const uint8_t *phase,
+                                                         const double *lam_tab,
+                                                         const double *mu_tab, const double *z,
+                                                         double *partials, int *err) {
+  constexpr int NEN = D + 1, Q = D * D + 1;
+  double acc[Q];
+#pragma unroll
+  for (int q = 0; q < Q; ++q) acc[q] = 0.0;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < E;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    double x[NEN][D], u[NEN][D], G[NEN][D], H[D][D], P[D][D], vol;
+#pragma unroll
+    for (int a = 0; a < NEN; ++a) {
+      const int64_t n = conn[e * NEN + a];
+#pragma unroll
+      for (int i = 0; i < D; ++i) {
+        x[a][i] = coords[n * D + i];
+        u[a][i] = z[n * D + i];
+      }
+    }
+    geometry<D>(x, G, vol);
+    field_gradient<D>(u, G, H);
+    double lam = lam0, mu = mu0;
+    if (phase) {
+      lam = lam_tab[phase[e]];
+      mu = mu_tab[phase[e]];
+    }
+    if constexpr (MAT == FEM_LINEAR_ELASTIC) {
+      le_stress<D>(H, lam, mu, P);
+    } else {
+      NHState<D> st;
+      if (!nh_state<D>(H, st)) {
+        atomicOr(err, ERRW_INVERTED);
+        continue;
+      }
+      nh_stress<D>(st, lam, mu, P);
+    }
+#pragma unroll
+    for (int i = 0; i < D; ++i)
+#pragma unroll
+      for (int j = 0; j < D; ++j) acc[i * D + j] = fma(vol, P[i][j], acc[i * D + j]);
+    acc[D * D] += vol;
+  }
+#pragma unroll
+  for (int q = 0; q < Q; ++q) {
+    const double t = block_sum<kThreads>(acc[q]);
+    if (threadIdx.x == 0) partials[(int64_t)q * gridDim.x + blockIdx.x] = t;
+  }
+}
+
 extern "C" {
 
 const char *fem_last_error(void) { return g_last_error.c_str(); }
@@ -619,6 +675,43 @@ fem_status fem_hvp(fem_problem *h, const double *z, const double *v, double *y, 
   FEM_ARG(h && z && v && y, "fem_hvp: null argument");
   FEM_ARG(v != y && z != y, "fem_hvp: output aliases an input");
   return run_hvp(&h->p, z, v, y, flags, (cudaStream_t)stream);
+}
+
+fem_status fem_mean_stress(fem_problem *h, const double *z, double *sigma, double *volume,
+                           fem_stream stream) {
+  FEM_ARG(h && z && sigma, "fem_mean_stress: null argument");
+  Problem *p = &h->p;
+  cudaStream_t s = (cudaStream_t)stream;
+  const int D = p->dim, Q = D * D + 1;
+  const int nb = kReduceBlocks;
+  double *part = nullptr, *out = nullptr;
+  FEM_CUDA(cudaMalloc(&part, sizeof(double) * (size_t)nb * Q));
+  FEM_CUDA(cudaMalloc(&out, sizeof(double) * Q));
+  if (p->n_elems == 0) FEM_CUDA(cudaMemsetAsync(part, 0, sizeof(double) * (size_t)nb * Q, s));
+  else if (D == 2) {
+    if (p->material == FEM_LINEAR_ELASTIC) k_mean_stress<2, FEM_LINEAR_ELASTIC><<<nb, kThreads, 0, s>>>(p->coords, p->conn, p->n_elems, p->lam, p->mu, p->phase, p->lam_tab, p->mu_tab, z, part, p->d_err);
+    else k_mean_stress<2, FEM_NEO_HOOKEAN><<<nb, kThreads, 0, s>>>(p->coords, p->conn, p->n_elems, p->lam, p->mu, p->phase, p->lam_tab, p->mu_tab, z, part, p->d_err);
+  } else {
+    if (p->material == FEM_LINEAR_ELASTIC) k_mean_stress<3, FEM_LINEAR_ELASTIC><<<nb, kThreads, 0, s>>>(p->coords, p->conn, p->n_elems, p->lam, p->mu, p->phase, p->lam_tab, p->mu_tab, z, part, p->d_err);
+    else k_mean_stress<3, FEM_NEO_HOOKEAN><<<nb, kThreads, 0, s>>>(p->coords, p->conn, p->n_elems, p->lam, p->mu, p->phase, p->lam_tab, p->mu_tab, z, part, p->d_err);
+  }
+  for (int q = 0; q < Q; ++q) k_final_sum<<<1, kThreads, 0, s>>>(part + (size_t)q * nb, nb, out + q);
+  FEM_LAUNCH_CHECK("mean stress");
+  fem_status st = FEM_OK;
+  for (int q = 0; q < Q && !st; ++q) st = allreduce(p, out + q, 1, s);
+  double h_out[10] = {0};
+  if (!st) {
+    FEM_CUDA(cudaMemcpyAsync(h_out, out, sizeof(double) * Q, cudaMemcpyDeviceToHost, s));
+    FEM_CUDA(cudaStreamSynchronize(s));
+    st = read_error_word(p, s);
+  }
+  cudaFree(part);
+  cudaFree(out);
+  if (st) return st;
+  const double V = h_out[D * D];
+  for (int q = 0; q < D * D; ++q) sigma[q] = V > 0.0 ? h_out[q] / V : 0.0;
+  if (volume) *volume = V;
+  return FEM_OK;
 }
 
 }  // extern "C"

@@ -203,6 +203,178 @@ fem_status run_cg(Problem *p, const double *z, const double *vals, const double 
   return result;
 }
 
+// ------------------------------------------------------------------ MINRES (f2)
+// Saddle-point systems of the periodic Lagrangian are
+// symmetric indefinite, so CG does not apply; MINRES (Paige & Saunders 1975) minimises
+// ||b - A x||_2 over the Krylov space with the Lanczos three-term recurrence and Givens
+// QR updates.  Unpreconditioned.  The scalar recurrence runs in one device thread
+// (k_minres_scalars) so the host only reads the residual estimate every check_every
+// iterations; the vector work is three fused kernels per iteration around the operator.
+enum { M_ALFA = 8, M_BB2 = 9, M_OLDB = 10, M_BETA = 11, M_DBAR = 12, M_EPS = 13, M_PHIBAR = 14,
+       M_CS = 15, M_SN = 16, M_PHI = 17, M_DENOM = 18, M_DELTA = 19, M_OLDEPS = 20,
+       M_BETA1 = 21, M_BN = 22, M_NSLOTS = 24 };
+
+__global__ void k_minres_init(double *scal) {
+  const double beta1 = sqrt(scal[M_BB2]);
+  scal[M_BETA1] = beta1;
+  scal[M_OLDB] = 0.0;
+  scal[M_BETA] = beta1;
+  scal[M_DBAR] = 0.0;
+  scal[M_EPS] = 0.0;
+  scal[M_PHIBAR] = beta1;
+  scal[M_CS] = -1.0;
+  scal[M_SN] = 0.0;
+}
+
+// v = y / beta ; t -= (beta / oldb) r1 (it >= 1) done after the operator: t holds A v
+__global__ void k_minres_scale(const double *scal, const double *y, double *v, int64_t n) {
+  const double sc = scal[M_BETA] > 0.0 ? 1.0 / scal[M_BETA] : 0.0;  // 0: Krylov space exhausted
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    v[i] = sc * y[i];
+}
+
+__global__ void k_minres_lanczos1(const double *scal, int first, double *t, const double *r1,
+                                  int64_t n) {
+  if (first || !(scal[M_OLDB] > 0.0)) return;
+  const double c = scal[M_BETA] / scal[M_OLDB];
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    t[i] = fma(-c, r1[i], t[i]);
+}
+
+__global__ void k_minres_lanczos2(const double *scal, double *t, const double *r2, int64_t n) {
+  const double c = scal[M_BETA] > 0.0 ? scal[M_ALFA] / scal[M_BETA] : 0.0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    t[i] = fma(-c, r2[i], t[i]);
+}
+
+__global__ void k_minres_scalars(double *scal) {
+  const double alfa = scal[M_ALFA];
+  const double oldb = scal[M_BETA];
+  const double beta = sqrt(fmax(scal[M_BB2], 0.0));
+  const double cs = scal[M_CS], sn = scal[M_SN], dbar = scal[M_DBAR];
+  const double oldeps = scal[M_EPS];
+  const double delta = cs * dbar + sn * alfa;
+  const double gbar = sn * dbar - cs * alfa;
+  const double epsln = sn * beta;
+  const double dbar2 = -cs * beta;
+  double gamma = hypot(gbar, beta);
+  if (gamma < 1e-300) gamma = 1e-300;
+  const double cs2 = gbar / gamma, sn2 = beta / gamma;
+  const double phi = cs2 * scal[M_PHIBAR];
+  scal[M_PHIBAR] = sn2 * scal[M_PHIBAR];
+  scal[M_OLDB] = oldb;
+  scal[M_BETA] = beta;
+  scal[M_OLDEPS] = oldeps;
+  scal[M_DELTA] = delta;
+  scal[M_EPS] = epsln;
+  scal[M_DBAR] = dbar2;
+  scal[M_CS] = cs2;
+  scal[M_SN] = sn2;
+  scal[M_PHI] = phi;
+  scal[M_DENOM] = 1.0 / gamma;
+}
+
+// w = (v - oldeps w1 - delta w2) / gamma (w1, w2 after the shift w1 <- w2, w2 <- w; the new
+// w goes to the buffer of the retired w1), x += phi w
+__global__ void k_minres_update(const double *scal, const double *v, const double *w1,
+                                const double *w2, double *wout, double *x, int64_t n) {
+  const double oe = scal[M_OLDEPS], de = scal[M_DELTA], dn = scal[M_DENOM], phi = scal[M_PHI];
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const double wn = (v[i] - oe * w1[i] - de * w2[i]) * dn;
+    wout[i] = wn;
+    x[i] = fma(phi, wn, x[i]);
+  }
+}
+
+fem_status run_minres(Problem *p, const double *z, const double *vals, const double *b, double *x,
+                      const fem_cg_opts *o, fem_cg_report *rep, cudaStream_t s) {
+  const int64_t n = p->N;
+  const int every = o->check_every > 0 ? o->check_every : 1;
+  fem_status st = ensure(p->cgbuf, sizeof(double) * n * 7);
+  if (st) return st;
+  double *B0 = (double *)p->cgbuf.ptr;
+  double *V = B0, *R1 = B0 + n, *R2 = B0 + 2 * n, *T = B0 + 3 * n, *W = B0 + 4 * n,
+         *W1 = B0 + 5 * n, *W2 = B0 + 6 * n;
+  const int g = grid_for(n);
+  double *sc = p->scal;
+  // r1 = b - A x; y = r1 (= R2 at the loop head); beta1 = ||r1||
+  st = apply_op(p, o->op, z, vals, x, T, s);
+  if (st) return st;
+  k_sub<<<g, kThreads, 0, s>>>(b, T, R2, n);
+  FEM_CUDA(cudaMemcpyAsync(R1, R2, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
+  FEM_CUDA(cudaMemsetAsync(W, 0, sizeof(double) * n, s));
+  FEM_CUDA(cudaMemsetAsync(W1, 0, sizeof(double) * n, s));
+  FEM_CUDA(cudaMemsetAsync(W2, 0, sizeof(double) * n, s));
+  st = launch_dot(p, R2, R2, n, sc + M_BB2, s);
+  if (st) return st;
+  st = launch_dot(p, b, b, n, sc + M_BN, s);
+  if (st) return st;
+  k_minres_init<<<1, 1, 0, s>>>(sc);
+  FEM_LAUNCH_CHECK("minres start");
+  st = read_scalars(p, M_NSLOTS, s);
+  if (st) return st;
+  st = read_error_word(p, s);
+  if (st) return st;
+  const double tol = std::fmax(o->rtol * std::sqrt(p->h_scal[M_BN]), o->atol);
+  double rn = p->h_scal[M_BETA1];
+  rep->res0 = rn;
+  rep->iters = 0;
+  rep->converged = 0;
+  int it = 0;
+  fem_status result = FEM_OK;
+  // y lives in R2 at the loop head (r2 = y after the previous iteration); w = W, w1/w2 rotate
+  while (true) {
+    if (rn <= tol) { rep->converged = 1; break; }
+    if (it >= o->max_iter) { result = FEM_ERR_NOT_CONVERGED; break; }
+    if (p->h_scal[M_BETA] == 0.0 && it > 0) { rep->converged = 1; break; }  // invariant space
+    k_minres_scale<<<g, kThreads, 0, s>>>(sc, R2, V, n);
+    st = apply_op(p, o->op, z, vals, V, T, s);
+    if (st) return st;
+    k_minres_lanczos1<<<g, kThreads, 0, s>>>(sc, it == 0, T, R1, n);
+    st = launch_dot(p, V, T, n, sc + M_ALFA, s);
+    if (st) return st;
+    k_minres_lanczos2<<<g, kThreads, 0, s>>>(sc, T, R2, n);
+    st = launch_dot(p, T, T, n, sc + M_BB2, s);
+    if (st) return st;
+    k_minres_scalars<<<1, 1, 0, s>>>(sc);
+    // w1 <- w2, w2 <- w, w <- new (into the retired w1 buffer)
+    k_minres_update<<<g, kThreads, 0, s>>>(sc, V, W2, W, W1, x, n);
+    {
+      double *ow = W, *ow1 = W1, *ow2 = W2;
+      W = ow1; W1 = ow2; W2 = ow;
+    }
+    // r1 <- r2, r2 <- t, t <- old r1
+    double *oR1 = R1;
+    R1 = R2; R2 = T; T = oR1;
+    FEM_LAUNCH_CHECK("minres iteration");
+    ++it;
+    if (it % every == 0 || it >= o->max_iter) {
+      st = read_scalars(p, M_NSLOTS, s);
+      if (st) return st;
+      rn = p->h_scal[M_PHIBAR];
+      if (!std::isfinite(rn)) { result = FEM_ERR_NONFINITE; break; }
+    }
+  }
+  rep->iters = it;
+  // true residual ||b - A x|| for the report
+  st = apply_op(p, o->op, z, vals, x, T, s);
+  if (st) return st;
+  k_sub<<<g, kThreads, 0, s>>>(b, T, T, n);
+  st = launch_dot(p, T, T, n, sc + M_BB2, s);
+  if (st) return st;
+  st = read_scalars(p, M_NSLOTS, s);
+  if (st) return st;
+  rep->res = std::sqrt(p->h_scal[M_BB2]);
+  st = read_error_word(p, s);
+  if (st) return st;
+  if (result == FEM_ERR_NOT_CONVERGED) set_error("MINRES: iteration cap reached");
+  return result;
+}
+
 }  // namespace fem
 
 using namespace fem;
@@ -217,6 +389,17 @@ fem_status fem_cg_solve(fem_problem *h, const double *z, const double *vals, con
   FEM_ARG(o->op == 0 || (vals && h->p.have_pattern), "fem_cg_solve: op 1 needs vals and a pattern");
   FEM_ARG(!o->jacobi || (o->op == 1 && h->p.n_mpc == 0), "fem_cg_solve: Jacobi needs op 1, no MPC");
   return run_cg(&h->p, z, vals, b, x, o, rep, (cudaStream_t)stream);
+}
+
+fem_status fem_minres_solve(fem_problem *h, const double *z, const double *vals, const double *b,
+                            double *x, const fem_cg_opts *o, fem_cg_report *rep,
+                            fem_stream stream) {
+  FEM_ARG(h && b && x && o && rep, "fem_minres_solve: null argument");
+  FEM_ARG(o->op == 0 || o->op == 1, "fem_minres_solve: op must be 0 (HVP) or 1 (CSR)");
+  FEM_ARG(o->op == 1 || z, "fem_minres_solve: op 0 needs z");
+  FEM_ARG(o->op == 0 || (vals && h->p.have_pattern), "fem_minres_solve: op 1 needs vals and a pattern");
+  FEM_ARG(!o->jacobi, "fem_minres_solve: unpreconditioned");
+  return run_minres(&h->p, z, vals, b, x, o, rep, (cudaStream_t)stream);
 }
 
 fem_status fem_newton_solve(fem_problem *h, double *z, const fem_newton_opts *o,
@@ -261,7 +444,9 @@ fem_status fem_newton_solve(fem_problem *h, double *z, const fem_newton_opts *o,
       if (st) { result = st; break; }
     }
     fem_cg_report cr{};
-    st = run_cg(p, z, vals, r, dz, &o->cg, &cr, s);
+    // the Lagrangian Hessian of an MPC problem is indefinite: MINRES instead of CG (f2)
+    st = p->n_mpc ? run_minres(p, z, vals, r, dz, &o->cg, &cr, s)
+                  : run_cg(p, z, vals, r, dz, &o->cg, &cr, s);
     rep->cg_iters += cr.iters;
     if (st) { result = st; break; }
     k_add<<<grid_for(n), kThreads, 0, s>>>(z, dz, n);

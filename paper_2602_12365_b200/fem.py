@@ -7,6 +7,7 @@ CUDA device is present the calls raise.
 The names follow the C ABI: Problem.energy -> fem_energy, .residual -> fem_residual,
 .hvp -> fem_hvp, .sparsity -> fem_sparsity, .color -> fem_color,
 .assemble_csr -> fem_assemble_csr, .spmv -> fem_spmv, .cg_solve -> fem_cg_solve,
+.minres_solve -> fem_minres_solve, .mean_stress -> fem_mean_stress,
 .newton_solve -> fem_newton_solve.
 """
 from __future__ import annotations
@@ -26,6 +27,7 @@ DETERMINISTIC = 2
 ASSEMBLE_LITERAL = 4
 ASSEMBLE_JCOMP = 32
 ASSEMBLE_ROWS = 64
+ASSEMBLE_SCATTER = 128
 BASELINE_SCATTER = 8
 LOCAL_ONLY = 16
 STATUS = {0: "OK", 1: "INVALID_ARG", 2: "DEGENERATE_ELEMENT", 3: "INVERTED_ELEMENT",
@@ -35,7 +37,8 @@ STATUS = {0: "OK", 1: "INVALID_ARG", 2: "DEGENERATE_ELEMENT", 3: "INVERTED_ELEME
 # every symbol include/fem.h declares (checked by tests/test_abi.py)
 EXPORTS = ("fem_create", "fem_destroy", "fem_query", "fem_check", "fem_apply_dirichlet",
            "fem_energy", "fem_residual", "fem_hvp", "fem_sparsity", "fem_color",
-           "fem_assemble_csr", "fem_spmv", "fem_cg_solve", "fem_newton_solve",
+           "fem_assemble_csr", "fem_spmv", "fem_cg_solve", "fem_minres_solve",
+           "fem_mean_stress", "fem_newton_solve",
            "fem_nccl_unique_id", "fem_nccl_comm_init", "fem_nccl_comm_destroy",
            "fem_allreduce_sum", "fem_halo_size", "fem_halo_pack", "fem_halo_combine",
            "fem_last_error", "fem_version")
@@ -109,6 +112,8 @@ def load_library():
         lib.fem_assemble_csr.argtypes = [vp, vp, vp, C.c_uint, vp]
         lib.fem_spmv.argtypes = [vp, vp, vp, vp, vp]
         lib.fem_cg_solve.argtypes = [vp, vp, vp, vp, vp, C.POINTER(CgOpts), C.POINTER(CgReport), vp]
+        lib.fem_minres_solve.argtypes = [vp, vp, vp, vp, vp, C.POINTER(CgOpts), C.POINTER(CgReport), vp]
+        lib.fem_mean_stress.argtypes = [vp, vp, C.POINTER(C.c_double), C.POINTER(C.c_double), vp]
         lib.fem_newton_solve.argtypes = [vp, vp, C.POINTER(NewtonOpts), C.POINTER(NewtonReport), vp]
         lib.fem_nccl_unique_id.argtypes = [C.c_char_p]
         lib.fem_nccl_comm_init.argtypes = [C.c_char_p, C.c_int, C.c_int, C.POINTER(vp)]
@@ -278,7 +283,8 @@ class Problem:
     def assemble_csr(self, z, bc: bool = False, mode: str = "auto", out=None) -> torch.Tensor:
         z = self._vec(z, "z")
         flags = (APPLY_BC if bc else 0) | {"batched": ASSEMBLE_JCOMP, "literal": ASSEMBLE_LITERAL,
-                                             "rows": ASSEMBLE_ROWS, "auto": 0}[mode]
+                                             "rows": ASSEMBLE_ROWS, "scatter": ASSEMBLE_SCATTER,
+                                             "auto": 0}[mode]
         nnz = self.nnz()
         out = self._out(out, nnz)
         _check(load_library().fem_assemble_csr(self._h, _ptr(z), _ptr(out), flags, _stream()),
@@ -305,6 +311,31 @@ class Problem:
         if raise_on_fail:
             _check(st, "fem_cg_solve")
         return x, info
+
+    def minres_solve(self, b, x0=None, z=None, vals=None, op: int = 0, rtol=1e-8, atol=0.0,
+                     max_iter=100000, check_every=1, raise_on_fail=True):
+        """MINRES on the BC-applied operator (symmetric indefinite saddle points, f2)."""
+        b = self._vec(b, "b")
+        x = torch.zeros_like(b) if x0 is None else self._vec(x0, "x0").clone()
+        zz = None if z is None else self._vec(z, "z")
+        o = CgOpts(op, rtol, atol, max_iter, 0, check_every)
+        rep = CgReport()
+        st = load_library().fem_minres_solve(self._h, _ptr(zz), _ptr(vals), _ptr(b), _ptr(x),
+                                             C.byref(o), C.byref(rep), _stream())
+        info = {"status": st, "iters": rep.iters, "converged": bool(rep.converged),
+                "res0": rep.res0, "res": rep.res}
+        if raise_on_fail:
+            _check(st, "fem_minres_solve")
+        return x, info
+
+    def mean_stress(self, z) -> tuple:
+        """(volume-averaged P as a dim x dim numpy array, |Omega|) — fem_mean_stress."""
+        z = self._vec(z, "z")
+        sig = (C.c_double * (self.dim * self.dim))()
+        vol = C.c_double()
+        _check(load_library().fem_mean_stress(self._h, _ptr(z), sig, C.byref(vol), _stream()),
+               "fem_mean_stress")
+        return np.array(sig[:], dtype=np.float64).reshape(self.dim, self.dim), vol.value
 
     # ---------------------------------------------------------------- multi-GPU halo
     def halo_size(self) -> int:

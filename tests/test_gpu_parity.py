@@ -114,7 +114,7 @@ def test_coloring_bit_exact(case):
     assert np.array_equal(colors.cpu().numpy(), rcol)
 
 
-@pytest.mark.parametrize("mode", ["batched", "literal", "rows"])
+@pytest.mark.parametrize("mode", ["batched", "literal", "rows", "scatter"])
 @pytest.mark.parametrize("bc", [False, True])
 def test_assembly(case, mode, bc):
     name, mesh, prob, ref, z, v = case

@@ -705,7 +705,10 @@ static fem_status assemble(Problem *p, const double *z, double *vals, unsigned f
   const bool rows = (flags & FEM_ASSEMBLE_ROWS) ||
                     (!(flags & (FEM_ASSEMBLE_LITERAL | FEM_ASSEMBLE_JCOMP)) && p->dim == 3);
   if (rows) {
-    fem_status st0 = build_row_plan(p, s);
+    fem_status st0 = build_row_tiles(p, s);
+    if (st0) return st0;
+    if (p->rt_state == 1) return launch_row_tiles(p, z, vals, bc, s);
+    st0 = build_row_plan(p, s);
     if (st0) return st0;
     if (p->rp_state != 1) {
       st0 = build_slot_lists(p, s);

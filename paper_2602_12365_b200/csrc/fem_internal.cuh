@@ -103,6 +103,12 @@ struct Problem {
   uint32_t *rp_ent = nullptr;    // [n_pad*es] blocks (pos | a<<27 | b<<29) grouped by slot
   uint8_t *rp_soff = nullptr;    // [n_pad*ss] entry offsets of the off-diagonal slots
   uint8_t *rp_sbc = nullptr;     // [n_pad*ss] Dirichlet bits of each slot's node
+  // fused node-tile assembly (fem_rowtile.cu): packed per-tile metadata blocks
+  int rt_state = 0;              // 0 not built, 1 built, -1 not eligible
+  uint8_t *rt_meta = nullptr;
+  int64_t rt_ntiles = 0;
+  int rt_layout[13] = {0};       // RtLayout fields
+  int rt_smem = 0;
   // coloring
   bool have_colors = false;
   int32_t n_colors = -1;
@@ -202,6 +208,8 @@ fem_status morton_node_order(Problem *p, cudaStream_t s);
 fem_status build_row_plan(Problem *p, cudaStream_t s);          // fem_rows.cu
 fem_status launch_rows_stage(Problem *p, const double *ctx, double *vals, bool bc,
                              cudaStream_t s);
+fem_status build_row_tiles(Problem *p, cudaStream_t s);                  // fem_rowtile.cu
+fem_status launch_row_tiles(Problem *p, const double *z, double *vals, bool bc, cudaStream_t s);
 fem_status dist_setup(Problem *p, const fem_dist_desc *d, cudaStream_t s);
 void dist_free(Problem *p);
 fem_status allreduce(Problem *p, double *buf, int n, cudaStream_t s);

@@ -1,0 +1,598 @@
+// fem_rowtile.cu — fused node-tile assembly of the sparse tangent (FEM_ASSEMBLE_ROWS form of
+// Alg. 2, reading R3; default in 3D): no per-element records in HBM.
+//
+// Nodes in Morton order are cut into tiles of NT consecutive nodes, one tile per CTA
+// iteration of a persistent grid.  Setup packs per tile one metadata block: the tile's
+// element set (every element incident to a tile node), its halo nodes, the elements'
+// halo-local connectivity, and per tile node its CSR row word, off-diagonal slot offsets,
+// Dirichlet bits and block list (entries (element, a, b) grouped by CSR slot, ascending
+// element order).  Per tile the CTA
+//   0. has the block and the halo nodes' coordinates and state copied into shared memory
+//      by cp.async (metadata two tiles ahead, node data one tile ahead);
+//   1. evaluates every tile element's tangent context once into shared memory: spatial
+//      gradients g_a = F^{-T} G_a (a = 0..d), M_ab = vol mu G_a.G_b for the element's node
+//      pairs, sc1 = vol (mu - lambda ln J), sc2 = vol lambda;
+//   2. sums, with 16 lanes per tile node and lane q = off-diagonal slot q, the element blocks
+//      K^e_ab[i][k] = M_ab d_ik + sc1 g_a[k] g_b[i] + sc2 g_a[i] g_b[k] of the slot's run and
+//      writes the D x D block; the diagonal block is minus the sum of the row's off-diagonal
+//      blocks (every element row sums to zero: sum_b G_b = sum_b g_b = 0), summed over the
+//      node's slot lanes in ascending slot order through shared memory.
+// Elements on tile boundaries are evaluated by each tile that touches them (~2x at NT = 32
+// in 3D); in exchange the HBM traffic is the CSR values, the metadata and the node data —
+// no context records.  Atomic-free, fixed order: bitwise reproducible.
+// Eligible meshes: no MPC multiplier columns, <= 16 off-diagonal slots per node, tile sets
+// within the plan's capacity; otherwise the assembly falls back to the row-pull kernels.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdlib>
+#include <vector>
+
+#include "element.cuh"
+#include "fem_internal.cuh"
+
+#ifndef FEM_RT_DIAG_SMEM
+#define FEM_RT_DIAG_SMEM 1
+#endif
+#ifndef FEM_RT_GPAD
+#define FEM_RT_GPAD 0
+#endif
+#ifndef FEM_RT_NT
+#define FEM_RT_NT 16
+#endif
+
+namespace fem {
+
+constexpr int kRtNT = FEM_RT_NT;         // nodes per tile
+constexpr int kRtThreads = 256;          // 8 warps, 2 nodes per warp per pass
+constexpr int kRtLPN = 16;               // lanes per node
+constexpr int kRtSortMax = 4096;         // plan: keys sorted per tile in shared memory
+
+template <int D>
+struct RtGeom {
+  static constexpr int NEN = D + 1, BS = D * D, NPAIR = D == 3 ? 6 : 3;
+  static constexpr int GP = FEM_RT_GPAD ? ((D + 1) & ~1) : D;     // g_a stride (padded: 16 B)
+  static constexpr int G0 = 0, M0 = NEN * GP, S0 = M0 + NPAIR + (NPAIR & 1);  // g | M | sc1 sc2
+  static constexpr int RS = S0 + 2;
+  static constexpr int BP = (BS + 1) & ~1;                        // scratch block pitch
+};
+
+// index of the unordered node pair {a, b}: 3D (01 02 03 12 13 23), 2D (01 02 12)
+template <int D>
+__host__ __device__ constexpr int rt_pair(int a, int b) {
+  return (a < b ? a : b) == 0 ? (a < b ? b : a) - 1
+                              : (D == 2 ? 2 : ((a < b ? a : b) == 1 ? (a < b ? b : a) + 1 : 5));
+}
+
+struct RtLayout {
+  int nt, uem, unm, es, ss, mb;
+  int off_halo, off_lc, off_ph, off_nd, off_so, off_sb, off_en;
+};
+
+static inline int r16(int x) { return (x + 15) & ~15; }
+
+static RtLayout rt_layout(int nt, int uem, int unm, int es, int ss, bool phase) {
+  RtLayout L{};
+  L.nt = nt; L.uem = uem; L.unm = unm; L.es = es; L.ss = ss;
+  L.off_halo = 16;
+  L.off_lc = r16(L.off_halo + 4 * unm);
+  L.off_ph = r16(L.off_lc + 8 * uem);
+  L.off_nd = r16(L.off_ph + (phase ? uem : 0));
+  L.off_so = r16(L.off_nd + 16 * nt);
+  L.off_sb = r16(L.off_so + nt * ss);
+  L.off_en = r16(L.off_sb + nt * ss);
+  L.mb = r16(L.off_en + 2 * nt * es);
+  return L;
+}
+
+// ------------------------------------------------------------------ setup
+__device__ void rt_bitonic(int32_t *key, int m, int tid, int nthr) {
+  int P = 1;
+  while (P < m) P <<= 1;
+  for (int i = m + tid; i < P; i += nthr) key[i] = INT32_MAX;
+  __syncthreads();
+  for (int k = 2; k <= P; k <<= 1)
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int i = tid; i < P; i += nthr) {
+        const int ij = i ^ j;
+        if (ij > i) {
+          const bool up = (i & k) == 0;
+          const int32_t x = key[i], y = key[ij];
+          if ((x > y) == up) { key[i] = y; key[ij] = x; }
+        }
+      }
+      __syncthreads();
+    }
+}
+
+// sorted unique in place (one thread), returns the count
+__device__ int rt_unique(int32_t *key, int m) {
+  int u = 0;
+  for (int i = 0; i < m; ++i)
+    if (i == 0 || key[i] != key[i - 1]) key[u++] = key[i];
+  return u;
+}
+
+__device__ int rt_find(const int32_t *key, int n, int32_t v) {
+  int lo = 0, hi = n;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (key[mid] < v) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+
+// One CTA per tile.  count mode (meta == null): Ue, Un per tile (and a fail flag when the
+// sort capacity is exceeded); fill mode: the packed metadata block.
+template <int D>
+__global__ void __launch_bounds__(256) k_rt_plan(const int32_t *node_order, int64_t n_nodes,
+                                                 const int64_t *inc_ptr, const int32_t *inc,
+                                                 const int32_t *conn, const uint8_t *phase,
+                                                 const int64_t *nadj_ptr, const int32_t *nadj,
+                                                 const int64_t *row_ptr, const uint8_t *node_bc,
+                                                 RtLayout L, int32_t *cnt, uint8_t *meta,
+                                                 int *bad) {
+  constexpr int NEN = D + 1;
+  __shared__ int32_t elems[kRtSortMax];
+  __shared__ int32_t halo[kRtSortMax];
+  __shared__ int s_m, s_ue, s_un;
+  const int64_t t = blockIdx.x;
+  const int tid = threadIdx.x, nthr = blockDim.x;
+  const int64_t n0 = t * L.nt;
+  const int nn = (int)((n_nodes - n0) < L.nt ? (n_nodes - n0) : L.nt);
+  if (tid == 0) s_m = 0;
+  __syncthreads();
+  // incident elements of the tile's nodes
+  for (int j = 0; j < nn; ++j) {
+    const int32_t n = node_order[n0 + j];
+    const int64_t i0 = inc_ptr[n];
+    const int deg = (int)(inc_ptr[n + 1] - i0);
+    const int base = s_m;
+    if (base + deg > kRtSortMax) {
+      if (tid == 0) atomicOr(bad, 1);
+      return;
+    }
+    for (int l = tid; l < deg; l += nthr) elems[base + l] = inc[i0 + l] / NEN;
+    __syncthreads();
+    if (tid == 0) s_m = base + deg;
+    __syncthreads();
+  }
+  rt_bitonic(elems, s_m, tid, nthr);
+  if (tid == 0) s_ue = rt_unique(elems, s_m);
+  __syncthreads();
+  const int ue = s_ue;
+  if (ue * NEN > kRtSortMax) {
+    if (tid == 0) atomicOr(bad, 1);
+    return;
+  }
+  for (int q = tid; q < ue * NEN; q += nthr) halo[q] = conn[(int64_t)elems[q / NEN] * NEN + q % NEN];
+  __syncthreads();
+  rt_bitonic(halo, ue * NEN, tid, nthr);
+  if (tid == 0) s_un = rt_unique(halo, ue * NEN);
+  __syncthreads();
+  const int un = s_un;
+  if (!meta) {
+    if (tid == 0) { cnt[2 * t] = ue; cnt[2 * t + 1] = un; }
+    return;
+  }
+  uint8_t *blk = meta + t * (int64_t)L.mb;
+  if (tid == 0) {
+    int *h = reinterpret_cast<int *>(blk);
+    h[0] = ue; h[1] = un; h[2] = nn; h[3] = 0;
+  }
+  int32_t *hid = reinterpret_cast<int32_t *>(blk + L.off_halo);
+  for (int q = tid; q < L.unm; q += nthr) hid[q] = q < un ? halo[q] : 0;
+  uint16_t *lc = reinterpret_cast<uint16_t *>(blk + L.off_lc);
+  for (int q = tid; q < L.uem * 4; q += nthr) {
+    const int e = q / 4, a = q % 4;
+    uint16_t v = 0;
+    if (e < ue && a < NEN) v = (uint16_t)rt_find(halo, un, conn[(int64_t)elems[e] * NEN + a]);
+    lc[q] = v;
+  }
+  if (phase) {
+    uint8_t *ph = blk + L.off_ph;
+    for (int q = tid; q < L.uem; q += nthr) ph[q] = q < ue ? phase[elems[q]] : 0;
+  }
+  // per tile node: row word, off-diagonal slots, block list
+  int4 *ndw = reinterpret_cast<int4 *>(blk + L.off_nd);
+  uint8_t *so = blk + L.off_so, *sb = blk + L.off_sb;
+  uint16_t *en = reinterpret_cast<uint16_t *>(blk + L.off_en);
+  for (int j = tid; j < L.nt; j += nthr) {
+    ndw[j] = make_int4(0, 0, 0, 0);
+    for (int q = 0; q < L.ss; ++q) { so[j * L.ss + q] = 0; sb[j * L.ss + q] = 0; }
+    if (j >= nn) continue;
+    const int32_t n = node_order[n0 + j];
+    const int64_t i0 = inc_ptr[n], a0 = nadj_ptr[n];
+    const int deg = (int)(inc_ptr[n + 1] - i0), sn = (int)(nadj_ptr[n + 1] - a0);
+    auto slot_of = [&](int32_t mm) {
+      int lo = 0, hi = sn;
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (nadj[a0 + mid] < mm) lo = mid + 1; else hi = mid;
+      }
+      return lo;
+    };
+    const int ds = sn > 0 ? slot_of(n) : 0;
+    const int sno = sn > 0 ? sn - 1 : 0;
+    if (sn == 0 || ds >= sn || nadj[a0 + ds] != n || sno > kRtLPN || (NEN - 1) * deg > L.es) {
+      atomicOr(bad, 1);
+      continue;
+    }
+    const int64_t rp0 = row_ptr[(int64_t)n * D];
+    for (int i = 1; i <= D; ++i)
+      if (row_ptr[(int64_t)n * D + i] != rp0 + (int64_t)i * D * sn) atomicOr(bad, 1);
+    uint8_t c[kRtLPN + 2];
+    for (int q = 0; q <= sno; ++q) c[q] = 0;
+    auto q_of = [&](int s) { return s < ds ? s : s - 1; };
+    for (int l = 0; l < deg; ++l) {
+      const int32_t pk = inc[i0 + l];
+      const int64_t e = pk / NEN;
+      const int a = pk % NEN;
+      for (int k = 1; k < NEN; ++k) c[q_of(slot_of(conn[e * NEN + (a + k) % NEN])) + 1]++;
+    }
+    for (int q = 0; q < sno; ++q) c[q + 1] += c[q];
+    for (int q = 0; q <= sno; ++q) so[j * L.ss + q] = c[q];
+    for (int q = 0; q < sno; ++q) sb[j * L.ss + q] = node_bc ? node_bc[nadj[a0 + q + (q >= ds)]] : 0;
+    uint16_t *ej = en + j * L.es;
+    for (int q = 0; q < L.es; ++q) ej[q] = 0;
+    for (int l = 0; l < deg; ++l) {
+      const int32_t pk = inc[i0 + l];
+      const int64_t e = pk / NEN;
+      const int a = pk % NEN;
+      const int r = rt_find(elems, ue, (int32_t)e);
+      for (int k = 1; k < NEN; ++k) {
+        const int b = (a + k) % NEN;
+        ej[c[q_of(slot_of(conn[e * NEN + b]))]++] = (uint16_t)(r | a << 10 | b << 12);
+      }
+    }
+    const unsigned bcn = node_bc ? node_bc[n] : 0u;
+    ndw[j] = make_int4(n, sno | sn << 8 | ds << 16 | (int)(bcn << 24),
+                       (int)(uint32_t)(rp0 & 0xffffffffu), (int)(rp0 >> 32));
+  }
+}
+
+fem_status build_row_tiles(Problem *p, cudaStream_t s) {
+  if (p->rt_state) return FEM_OK;
+  p->rt_state = -1;
+  if (p->n_mpc || p->n_nodes == 0 || p->n_elems == 0 || getenv("FEM_ROWS_PULL")) return FEM_OK;
+  fem_status st = morton_node_order(p, s);
+  if (st) return st;
+  const int D = p->dim, NEN = D + 1, NT = kRtNT;
+  const int64_t n = p->n_nodes, nt = (n + NT - 1) / NT;
+  // max degree -> entry stride
+  std::vector<int64_t> hip(n + 1);
+  FEM_CUDA(cudaMemcpyAsync(hip.data(), p->inc_ptr, sizeof(int64_t) * (n + 1), cudaMemcpyDeviceToHost, s));
+  FEM_CUDA(cudaStreamSynchronize(s));
+  int IS = 0;
+  for (int64_t i = 0; i < n; ++i) IS = std::max<int>(IS, (int)(hip[i + 1] - hip[i]));
+  const int ES = (((NEN - 1) * IS) + 7) & ~7, SS = (kRtLPN + 1 + 3) & ~3;
+  if (IS == 0 || (NEN - 1) * IS > 255) return FEM_OK;
+  int *d_bad = nullptr;
+  int32_t *cnt = nullptr;
+  FEM_CUDA(cudaMalloc(&d_bad, sizeof(int)));
+  FEM_CUDA(cudaMalloc(&cnt, sizeof(int32_t) * 2 * nt));
+  FEM_CUDA(cudaMemsetAsync(d_bad, 0, sizeof(int), s));
+  RtLayout L0 = rt_layout(NT, 8, 8, ES, SS, p->phase != nullptr);
+  if (D == 2) k_rt_plan<2><<<(unsigned)nt, 256, 0, s>>>(p->node_order, n, p->inc_ptr, p->inc, p->conn, p->phase, p->nadj_ptr, p->nadj, p->row_ptr, p->node_bc, L0, cnt, nullptr, d_bad);
+  else k_rt_plan<3><<<(unsigned)nt, 256, 0, s>>>(p->node_order, n, p->inc_ptr, p->inc, p->conn, p->phase, p->nadj_ptr, p->nadj, p->row_ptr, p->node_bc, L0, cnt, nullptr, d_bad);
+  FEM_LAUNCH_CHECK("row tiles (count)");
+  std::vector<int32_t> hc(2 * nt);
+  int hbad = 0;
+  FEM_CUDA(cudaMemcpyAsync(hc.data(), cnt, sizeof(int32_t) * 2 * nt, cudaMemcpyDeviceToHost, s));
+  FEM_CUDA(cudaMemcpyAsync(&hbad, d_bad, sizeof(int), cudaMemcpyDeviceToHost, s));
+  FEM_CUDA(cudaStreamSynchronize(s));
+  int uem = 0, unm = 0;
+  for (int64_t t = 0; t < nt; ++t) {
+    uem = std::max(uem, hc[2 * t]);
+    unm = std::max(unm, hc[2 * t + 1]);
+  }
+  uem = (uem + 7) & ~7;
+  unm = (unm + 7) & ~7;
+  const RtLayout L = rt_layout(NT, uem, unm, ES, SS, p->phase != nullptr);
+  // shared memory of the assembly kernel: 3 metadata blocks, 2 node-data buffers, records
+  const int RS = D == 3 ? RtGeom<3>::RS : RtGeom<2>::RS;
+  const int BP = D == 3 ? RtGeom<3>::BP : RtGeom<2>::BP;
+  const size_t smem = 3 * (size_t)L.mb + 2 * sizeof(double) * 2 * D * (size_t)unm +
+                      sizeof(double) * (size_t)RS * uem +
+                      (FEM_RT_DIAG_SMEM ? sizeof(double) * (kRtThreads / 32) * 32 * BP : 0);
+  if (hbad || uem >= 1024 || smem > 220 * 1024) {
+    cudaFree(d_bad); cudaFree(cnt);
+    return FEM_OK;
+  }
+  FEM_CUDA(cudaMalloc(&p->rt_meta, (size_t)L.mb * nt));
+  if (D == 2) k_rt_plan<2><<<(unsigned)nt, 256, 0, s>>>(p->node_order, n, p->inc_ptr, p->inc, p->conn, p->phase, p->nadj_ptr, p->nadj, p->row_ptr, p->node_bc, L, cnt, p->rt_meta, d_bad);
+  else k_rt_plan<3><<<(unsigned)nt, 256, 0, s>>>(p->node_order, n, p->inc_ptr, p->inc, p->conn, p->phase, p->nadj_ptr, p->nadj, p->row_ptr, p->node_bc, L, cnt, p->rt_meta, d_bad);
+  FEM_LAUNCH_CHECK("row tiles (fill)");
+  FEM_CUDA(cudaMemcpyAsync(&hbad, d_bad, sizeof(int), cudaMemcpyDeviceToHost, s));
+  FEM_CUDA(cudaStreamSynchronize(s));
+  cudaFree(d_bad);
+  cudaFree(cnt);
+  if (hbad) {
+    cudaFree(p->rt_meta);
+    p->rt_meta = nullptr;
+    return FEM_OK;
+  }
+  p->rt_ntiles = nt;
+  p->rt_layout[0] = L.nt; p->rt_layout[1] = L.uem; p->rt_layout[2] = L.unm;
+  p->rt_layout[3] = L.es; p->rt_layout[4] = L.ss; p->rt_layout[5] = L.mb;
+  p->rt_layout[6] = L.off_halo; p->rt_layout[7] = L.off_lc; p->rt_layout[8] = L.off_ph;
+  p->rt_layout[9] = L.off_nd; p->rt_layout[10] = L.off_so; p->rt_layout[11] = L.off_sb;
+  p->rt_layout[12] = L.off_en;
+  p->rt_smem = (int)smem;
+  p->rt_state = 1;
+  return FEM_OK;
+}
+
+// ------------------------------------------------------------------ kernel
+__device__ __forceinline__ void rt_cp16(void *smem, const void *gmem) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem));
+}
+__device__ __forceinline__ void rt_cp8(void *smem, const void *gmem) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gmem));
+}
+__device__ __forceinline__ void rt_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+__device__ __forceinline__ void rt_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+
+struct RtArgs {
+  const uint8_t *meta;
+  int64_t n_tiles;
+  RtLayout L;
+  const double *coords, *z;
+  double lam, mu;
+  const double *lam_tab, *mu_tab;
+  int has_phase, bc;
+  double *vals;
+  int *err;
+};
+
+template <int D, int MAT>
+__global__ void __launch_bounds__(kRtThreads, 2) k_rows_tile(RtArgs A) {
+  using Gm = RtGeom<D>;
+  constexpr int NEN = Gm::NEN, BS = Gm::BS, RS = Gm::RS;
+  constexpr unsigned FULL = 0xffffffffu;
+  extern __shared__ __align__(16) unsigned char sm_rt[];
+  const RtLayout &L = A.L;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int mb = L.mb, unm = L.unm;
+  unsigned char *metab = sm_rt;
+  double *nodeb = reinterpret_cast<double *>(sm_rt + 3 * mb);  // [2][2][unm][D]: x | u
+  double *rec = nodeb + 2 * 2 * unm * D;                         // [uem][RS]
+  double *scratch = rec + (size_t)L.uem * RS;                    // [8 warps][32][BP]
+  const int64_t G = gridDim.x;
+
+  auto issue_meta = [&](int64_t t, unsigned char *dst) {
+    const unsigned char *src = A.meta + t * (int64_t)mb;
+    for (int off = tid * 16; off < mb; off += kRtThreads * 16) rt_cp16(dst + off, src + off);
+  };
+  auto issue_nodes = [&](const unsigned char *m, double *dst) {
+    const int un = reinterpret_cast<const int *>(m)[1];
+    const int32_t *hid = reinterpret_cast<const int32_t *>(m + L.off_halo);
+    for (int i = tid; i < un * D; i += kRtThreads) {
+      const int64_t g = (int64_t)hid[i / D] * D + (i % D);
+      rt_cp8(dst + i, A.coords + g);
+      rt_cp8(dst + unm * D + i, A.z + g);
+    }
+  };
+
+  int64_t t = blockIdx.x;
+  if (t < A.n_tiles) {
+    issue_meta(t, metab);
+    rt_commit();
+    rt_wait_all();
+    __syncthreads();
+    issue_nodes(metab, nodeb);
+    if (t + G < A.n_tiles) issue_meta(t + G, metab + mb);
+    rt_commit();
+  }
+  for (int k = 0; t < A.n_tiles; ++k, t += G) {
+    rt_wait_all();
+    __syncthreads();
+    const unsigned char *m = metab + (k % 3) * mb;
+    const double *xs = nodeb + (k & 1) * 2 * unm * D, *us = xs + unm * D;
+    if (t + G < A.n_tiles) issue_nodes(metab + ((k + 1) % 3) * mb, nodeb + ((k + 1) & 1) * 2 * unm * D);
+    if (t + 2 * G < A.n_tiles) issue_meta(t + 2 * G, metab + ((k + 2) % 3) * mb);
+    rt_commit();
+    const int ue = reinterpret_cast<const int *>(m)[0];
+    const int nn = reinterpret_cast<const int *>(m)[2];
+    // ---- 1: element contexts
+    const uint16_t *lc = reinterpret_cast<const uint16_t *>(m + L.off_lc);
+    for (int e = tid; e < ue; e += kRtThreads) {
+      const ushort4 l4 = reinterpret_cast<const ushort4 *>(lc)[e];
+      const int li[4] = {l4.x, l4.y, l4.z, l4.w};
+      double x[NEN][D], u[NEN][D], G[NEN][D], vol;
+#pragma unroll
+      for (int a = 0; a < NEN; ++a)
+#pragma unroll
+        for (int i = 0; i < D; ++i) {
+          x[a][i] = xs[li[a] * D + i];
+          u[a][i] = us[li[a] * D + i];
+        }
+      geometry<D>(x, G, vol);
+      double lam = A.lam, mu = A.mu;
+      if (A.has_phase) {
+        const int ph = m[L.off_ph + e];
+        lam = A.lam_tab[ph];
+        mu = A.mu_tab[ph];
+      }
+      double *r = rec + e * RS;
+      double c1 = mu;
+      bool ok = true;
+      if constexpr (MAT == FEM_LINEAR_ELASTIC) {
+#pragma unroll
+        for (int a = 0; a < NEN; ++a)
+#pragma unroll
+          for (int i = 0; i < D; ++i) r[Gm::G0 + a * Gm::GP + i] = G[a][i];
+      } else {
+        double H[D][D];
+        field_gradient<D>(u, G, H);
+        NHState<D> st;
+        ok = nh_state<D>(H, st);
+        if (!ok) atomicOr(A.err, ERRW_INVERTED);
+        c1 = mu - lam * st.lnJ;
+#pragma unroll
+        for (int a = 0; a < NEN; ++a)
+#pragma unroll
+          for (int i = 0; i < D; ++i) {
+            double g = 0.0;
+#pragma unroll
+            for (int j = 0; j < D; ++j) g = fma(st.FiT[i][j], G[a][j], g);
+            r[Gm::G0 + a * Gm::GP + i] = ok ? g : 0.0;
+          }
+      }
+      const double smu = ok ? vol * mu : 0.0;
+#pragma unroll
+      for (int a = 0; a < NEN; ++a)
+#pragma unroll
+        for (int b = a + 1; b < NEN; ++b) {
+          double gg = 0.0;
+#pragma unroll
+          for (int j = 0; j < D; ++j) gg = fma(G[a][j], G[b][j], gg);
+          r[Gm::M0 + rt_pair<D>(a, b)] = smu * gg;
+        }
+      r[Gm::S0] = ok ? vol * c1 : 0.0;
+      r[Gm::S0 + 1] = ok ? vol * lam : 0.0;
+    }
+    __syncthreads();
+    // ---- 2: rows, 16 lanes per tile node
+    const int h = lane / kRtLPN, ql = lane % kRtLPN;
+    const int4 *ndw = reinterpret_cast<const int4 *>(m + L.off_nd);
+    for (int j = 2 * w + h; j < L.nt; j += 2 * (kRtThreads / 32)) {
+      const int4 nd = ndw[j];
+      const int sno = nd.y & 0xff, sn = (nd.y >> 8) & 0xff, ds = (nd.y >> 16) & 0xff;
+      const unsigned bcn = A.bc ? ((unsigned)nd.y >> 24) : 0u;
+      const int64_t rp0 = (int64_t)(uint32_t)nd.z | ((int64_t)nd.w << 32);
+      int lo = 0, hi = 0;
+      if (ql < sno) {
+        lo = m[L.off_so + j * L.ss + ql];
+        hi = m[L.off_so + j * L.ss + ql + 1];
+      }
+      const uint16_t *ent = reinterpret_cast<const uint16_t *>(m + L.off_en) + j * L.es;
+      double acc[BS];
+#pragma unroll
+      for (int q = 0; q < BS; ++q) acc[q] = 0.0;
+      for (int c = lo; c < hi; ++c) {
+        const uint32_t en = ent[c];
+        const double *r = rec + (en & 1023u) * RS;
+        const int a = (en >> 10) & 3u, b = (en >> 12) & 3u;
+        double ga[Gm::GP + 1], gb[Gm::GP + 1];
+        if constexpr (Gm::GP % 2 == 0) {
+#pragma unroll
+          for (int i = 0; i < Gm::GP; i += 2) {
+            const double2 x = *reinterpret_cast<const double2 *>(r + Gm::G0 + a * Gm::GP + i);
+            const double2 y = *reinterpret_cast<const double2 *>(r + Gm::G0 + b * Gm::GP + i);
+            ga[i] = x.x; ga[i + 1] = x.y;
+            gb[i] = y.x; gb[i + 1] = y.y;
+          }
+        } else {
+#pragma unroll
+          for (int i = 0; i < D; ++i) {
+            ga[i] = r[Gm::G0 + a * Gm::GP + i];
+            gb[i] = r[Gm::G0 + b * Gm::GP + i];
+          }
+        }
+        const double Mab = r[Gm::M0 + rt_pair<D>(a, b)];
+        const double2 scs = *reinterpret_cast<const double2 *>(r + Gm::S0);
+        const double sc1 = scs.x, sc2 = scs.y;
+#pragma unroll
+        for (int i = 0; i < D; ++i) {
+          const double qi = sc2 * ga[i];
+#pragma unroll
+          for (int kk = 0; kk < D; ++kk) {
+            double v = fma(sc1 * ga[kk], gb[i], acc[i * D + kk]);
+            v = fma(qi, gb[kk], v);
+            acc[i * D + kk] = (i == kk) ? v + Mab : v;
+          }
+        }
+      }
+      const bool live = j < nn;
+      if (live && ql < sno) {
+        const unsigned sbc = A.bc ? m[L.off_sb + j * L.ss + ql] : 0u;
+        const int s = ql + (ql >= ds);
+        double *row = A.vals + rp0 + s * D;
+        if ((sbc | bcn) == 0u) {
+#pragma unroll
+          for (int i = 0; i < D; ++i)
+#pragma unroll
+            for (int kk = 0; kk < D; ++kk) row[(int64_t)i * D * sn + kk] = acc[i * D + kk];
+        } else {
+#pragma unroll
+          for (int i = 0; i < D; ++i)
+#pragma unroll
+            for (int kk = 0; kk < D; ++kk) {
+              double v = acc[i * D + kk];
+              if ((sbc >> kk) & 1u) v = 0.0;  // masked column
+              if ((bcn >> i) & 1u) v = 0.0;   // identity row (off-diagonal)
+              row[(int64_t)i * D * sn + kk] = v;
+            }
+        }
+      }
+#if FEM_RT_DIAG_SMEM
+      // diagonal block = -sum of the node's off-diagonal slots, ascending slot order
+      double *scr = scratch + (w * 32 + lane) * Gm::BP;
+#pragma unroll
+      for (int q = 0; q < BS; ++q) scr[q] = acc[q];
+      __syncwarp();
+      if (live && ql < BS) {
+        const int i = ql / D, kk = ql % D;
+        const double *sb = scratch + (w * 32 + h * kRtLPN) * Gm::BP + ql;
+        double v = 0.0;
+        for (int q = 0; q < sno; ++q) v += sb[q * Gm::BP];
+        v = -v;
+        if (bcn & (1u << kk)) v = 0.0;                      // masked column
+        if (bcn & (1u << i)) v = (i == kk) ? 1.0 : 0.0;     // identity row
+        A.vals[rp0 + (int64_t)i * D * sn + ds * D + kk] = v;
+      }
+      __syncwarp();
+#else
+      // diagonal block = -sum over the node's slots (fixed butterfly order)
+#pragma unroll
+      for (int q = 0; q < BS; ++q) {
+        double v = acc[q];
+#pragma unroll
+        for (int o = kRtLPN / 2; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, v, o, kRtLPN);
+        acc[q] = v;
+      }
+      if (live) {
+#pragma unroll
+        for (int q = 0; q < BS; ++q)
+          if (ql == q) {
+            const int i = q / D, kk = q % D;
+            double v = -acc[q];
+            if (bcn & (1u << kk)) v = 0.0;                      // masked column
+            if (bcn & (1u << i)) v = (i == kk) ? 1.0 : 0.0;     // identity row
+            A.vals[rp0 + (int64_t)i * D * sn + ds * D + kk] = v;
+          }
+      }
+#endif
+    }
+  }
+}
+
+fem_status launch_row_tiles(Problem *p, const double *z, double *vals, bool bc, cudaStream_t s) {
+  RtArgs A{};
+  const int *lay = p->rt_layout;
+  A.L.nt = lay[0]; A.L.uem = lay[1]; A.L.unm = lay[2]; A.L.es = lay[3]; A.L.ss = lay[4];
+  A.L.mb = lay[5]; A.L.off_halo = lay[6]; A.L.off_lc = lay[7]; A.L.off_ph = lay[8];
+  A.L.off_nd = lay[9]; A.L.off_so = lay[10]; A.L.off_sb = lay[11]; A.L.off_en = lay[12];
+  A.meta = p->rt_meta; A.n_tiles = p->rt_ntiles; A.coords = p->coords; A.z = z;
+  A.lam = p->lam; A.mu = p->mu; A.lam_tab = p->lam_tab; A.mu_tab = p->mu_tab;
+  A.has_phase = p->phase != nullptr; A.bc = bc ? 1 : 0; A.vals = vals; A.err = p->d_err;
+  void (*kern)(RtArgs);
+  if (p->dim == 2) kern = p->material == FEM_LINEAR_ELASTIC ? k_rows_tile<2, FEM_LINEAR_ELASTIC> : k_rows_tile<2, FEM_NEO_HOOKEAN>;
+  else kern = p->material == FEM_LINEAR_ELASTIC ? k_rows_tile<3, FEM_LINEAR_ELASTIC> : k_rows_tile<3, FEM_NEO_HOOKEAN>;
+  FEM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, p->rt_smem));
+  int per_sm = 0;
+  FEM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kRtThreads, p->rt_smem));
+  int dev = 0, sms = 148;
+  FEM_CUDA(cudaGetDevice(&dev));
+  FEM_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  int64_t grid = (int64_t)sms * (per_sm > 0 ? per_sm : 1);
+  if (grid > p->rt_ntiles) grid = p->rt_ntiles;
+  kern<<<(int)grid, kRtThreads, p->rt_smem, s>>>(A);
+  FEM_LAUNCH_CHECK("node-tile assembly");
+  return FEM_OK;
+}
+
+}  // namespace fem

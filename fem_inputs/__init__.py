@@ -205,6 +205,30 @@ def roller_bc(mesh: Mesh, eps: float) -> Mesh:
                           dirichlet_vals=vals[first].astype(np.float64))
 
 
+def roller_symmetry_bc(mesh: Mesh) -> Mesh:
+    """Symmetry rollers only: u_x=0 on x=0, u_y=0 on y=0 (, u_z=0 on z=0) — the traction
+    problem of PAPER.md §6.1 without the prescribed stretch."""
+    m = mesh.dim
+    dofs = np.concatenate([_nodes_at(mesh, c, 0.0) * m + c for c in range(m)])
+    uniq = np.unique(dofs)
+    return mesh.copy_with(dirichlet_dofs=uniq.astype(np.int32),
+                          dirichlet_vals=np.zeros(uniq.shape[0]))
+
+
+def boundary_facets(mesh: Mesh, comp: int, value: float) -> np.ndarray:
+    """Facets (Line2 in 2D, Tri3 in 3D; [n][dim] node ids) of the elements lying on the
+    plane X_comp = value: element faces whose nodes all sit on it (each boundary face belongs
+    to exactly one element)."""
+    on = np.zeros(mesh.n_nodes, bool)
+    on[_nodes_at(mesh, comp, value)] = True
+    d = mesh.dim
+    out = []
+    for drop in range(d + 1):
+        face = np.delete(mesh.conn, drop, axis=1)
+        out.append(face[on[face].all(axis=1)])
+    return np.ascontiguousarray(np.concatenate(out), dtype=np.int32)
+
+
 def clamped_bc(mesh: Mesh, eps: float) -> Mesh:
     """C15 clamped variant: u = 0 on x=0; u = (eps*L, 0[, 0]) on x=L."""
     m, L = mesh.dim, mesh.length

@@ -177,13 +177,17 @@ fem_status fem_color(fem_problem *p, int32_t *colors, int32_t *n_colors, fem_str
  *   FEM_ASSEMBLE_JCOMP: all color passes in ONE element sweep (the passes are
  *            independent), accumulating J_comp with atomics, then decompression;
  *   FEM_ASSEMBLE_ROWS: J_comp computed row by row (pull form: row i sums the colored
- *            seeds' responses of its incident elements, a warp per node) with each
- *            compressed entry stored at its decompressed CSR slot (within a row every color
- *            names one column) — no J_comp buffer, atomic-free, bitwise reproducible;
+ *            seeds' responses of its incident elements) with each compressed entry stored
+ *            at its decompressed CSR slot (within a row every color names one column) — no
+ *            J_comp buffer, atomic-free, bitwise reproducible.  Node tiles of 16 Morton-
+ *            ordered nodes evaluate their elements' tangent contexts in shared memory (no
+ *            context records in HBM); the diagonal block is minus the row's off-diagonal
+ *            sum (element rows sum to zero);
  *   FEM_ASSEMBLE_SCATTER: not Alg. 2 but the assembly the paper compares it with (Fig. 4
  *            right): dense element Hessians scatter-added into vals with fp64
  *            atomics (run-to-run rounding differences of the atomic order);
- *   default (no mode flag): FEM_ASSEMBLE_ROWS in 3D, FEM_ASSEMBLE_JCOMP in 2D.
+ *   default (no mode flag): FEM_ASSEMBLE_ROWS, except FEM_ASSEMBLE_JCOMP for 2D problems
+ *            with MPC multipliers.
  * flags may add FEM_APPLY_BC.  Requires fem_color (the pattern and colors). */
 fem_status fem_assemble_csr(fem_problem *p, const double *z, double *vals, unsigned flags,
                             fem_stream stream);
@@ -225,6 +229,20 @@ fem_status fem_minres_solve(fem_problem *p, const double *z, const double *vals,
  * reduction.  Synchronizes `stream`. */
 fem_status fem_mean_stress(fem_problem *p, const double *z, double *sigma, double *volume,
                            fem_stream stream);
+
+/* External loads of the total potential energy (listing P:380-386; SURVEY §8(f)
+ * f3): Psi -= int_St t . u dGamma (traction on boundary facets: Line2 in 2D, Tri3 in 3D) and
+ * Psi -= int b . u dOmega (uniform body force).  Linear in u and, with P1 shape functions
+ * and loads constant per facet, exactly the consistent nodal loads t |facet| / dim and
+ * b vol / (dim+1): both are ADDED to the problem's f_ext (energy, residual and Newton use
+ * it; the HVP is unchanged).  facets [n_facets][dim] node ids, traction [n_facets][dim]
+ * (device).  fem_add_traction synchronizes `stream` (id check: INVALID_ARG).
+ * fem_get_fext copies the accumulated f_ext [N_u] (device). */
+fem_status fem_add_traction(fem_problem *p, int64_t n_facets, const int32_t *facets,
+                            const double *traction, fem_stream stream);
+fem_status fem_add_body_force(fem_problem *p, const double *b /* (host) [dim] */,
+                              fem_stream stream);
+fem_status fem_get_fext(fem_problem *p, double *f_ext, fem_stream stream);
 
 typedef struct {
   double atol, rtol; /* outer: ||r|| <= max(atol, rtol ||r0||)                 */

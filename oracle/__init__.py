@@ -248,6 +248,29 @@ class Oracle:
             raise OracleError(st, "fem_ref_mean_stress")
         return sig.reshape(d, d), vol.value
 
+    def traction_load(self, facets, traction):
+        """int N_a t dGamma over the facets (fem_ref_traction_load), [N_u]."""
+        f = np.zeros(self.mesh.n_nodes * self.mesh.dim)
+        fa = np.ascontiguousarray(facets, np.int32)
+        t = np.asarray(traction, np.float64)
+        t = np.ascontiguousarray(np.tile(t, (len(fa), 1)) if t.ndim == 1 else t)
+        st = lib().fem_ref_traction_load(C.c_int(self.mesh.dim), C.c_int64(self.mesh.n_nodes),
+                                         C.c_void_p(self._coords.ctypes.data), C.c_int64(len(fa)),
+                                         C.c_void_p(fa.ctypes.data), C.c_void_p(t.ctypes.data),
+                                         C.c_void_p(f.ctypes.data))
+        if st:
+            raise OracleError(st, "fem_ref_traction_load")
+        return f
+
+    def body_load(self, b):
+        f = np.zeros(self.mesh.n_nodes * self.mesh.dim)
+        bb = np.ascontiguousarray(np.asarray(b, np.float64))
+        st = lib().fem_ref_body_load(C.byref(self.s), C.c_void_p(bb.ctypes.data),
+                                     C.c_void_p(f.ctypes.data))
+        if st:
+            raise OracleError(st, "fem_ref_body_load")
+        return f
+
     def newton_dense(self, z0, atol=1e-12, rtol=1e-10, max_iter=50):
         """Full-step Newton on the BC-applied Lagrangian with the dense Hessian and
         numpy.linalg.solve for each step — the plain definition of the stationary point of

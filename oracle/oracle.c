@@ -651,6 +651,82 @@ int fem_ref_mean_stress(const fem_ref_mesh *m, const double *z, double *sigma, d
   return OK;
 }
 
+/* ------------------------------------------------------------------ external loads (f3)
+ * Consistent nodal loads of the linear load terms of the total potential energy (PAPER.md
+ * §6.1): f_a = int N_a t dGamma over boundary facets (Line2 in 2D, Tri3 in 3D) and
+ * f_a = int N_a b dOmega over the elements, by Gauss rules exact for the linear integrands
+ * (Line2: 2 points xi = 1/2 -+ 1/(2 sqrt 3), w 1/2; Tri3: the 3 edge midpoints, w 1/3;
+ * Tri3 element: the same; Tet4: 4 points a = (5 - sqrt 5)/20, b = (5 + 3 sqrt 5)/20, w 1/4),
+ * i.e. not the one-point shortcut the GPU uses.  Accumulated in ascending facet order.     */
+int fem_ref_traction_load(int dim, int64_t n_nodes, const double *coords, int64_t nf,
+                          const int32_t *facets, const double *t, double *f) {
+  int64_t q;
+  int a, i, g;
+  for (q = 0; q < nf; ++q) {
+    double area, N[3][3], w[3];
+    int ng;
+    const int32_t *nd = facets + q * dim;
+    for (a = 0; a < dim; ++a)
+      if (nd[a] < 0 || nd[a] >= n_nodes) return E_ARG;
+    if (dim == 2) {
+      const double dx = coords[nd[1] * 2] - coords[nd[0] * 2];
+      const double dy = coords[nd[1] * 2 + 1] - coords[nd[0] * 2 + 1];
+      const double r = 0.5 / sqrt(3.0);
+      area = sqrt(dx * dx + dy * dy);
+      ng = 2;
+      N[0][0] = 1.0 - (0.5 - r); N[0][1] = 0.5 - r;
+      N[1][0] = 1.0 - (0.5 + r); N[1][1] = 0.5 + r;
+      w[0] = w[1] = 0.5;
+    } else {
+      double e1[3], e2[3], c[3];
+      for (i = 0; i < 3; ++i) {
+        e1[i] = coords[nd[1] * 3 + i] - coords[nd[0] * 3 + i];
+        e2[i] = coords[nd[2] * 3 + i] - coords[nd[0] * 3 + i];
+      }
+      c[0] = e1[1] * e2[2] - e1[2] * e2[1];
+      c[1] = e1[2] * e2[0] - e1[0] * e2[2];
+      c[2] = e1[0] * e2[1] - e1[1] * e2[0];
+      area = 0.5 * sqrt(c[0] * c[0] + c[1] * c[1] + c[2] * c[2]);
+      ng = 3;  /* edge midpoints: N = (1/2, 1/2, 0) and permutations */
+      for (g = 0; g < 3; ++g)
+        for (a = 0; a < 3; ++a) N[g][a] = (a == g) ? 0.0 : 0.5;
+      w[0] = w[1] = w[2] = 1.0 / 3.0;
+    }
+    for (g = 0; g < ng; ++g)
+      for (a = 0; a < dim; ++a)
+        for (i = 0; i < dim; ++i) f[(int64_t)nd[a] * dim + i] += w[g] * N[g][a] * area * t[q * dim + i];
+  }
+  return OK;
+}
+
+int fem_ref_body_load(const fem_ref_mesh *m, const double *b, double *f) {
+  int d = m->dim, nen = d + 1, a, i, g, st;
+  int64_t e;
+  const double ta = (5.0 - sqrt(5.0)) / 20.0, tb = (5.0 + 3.0 * sqrt(5.0)) / 20.0;
+  for (e = 0; e < m->n_elems; ++e) {
+    double G[4][3], vol, N[4][4], w;
+    int ng;
+    st = elem_geometry(m, e, G, &vol);
+    if (st) return st;
+    if (d == 2) {
+      ng = 3;
+      w = 1.0 / 3.0;
+      for (g = 0; g < 3; ++g)
+        for (a = 0; a < 3; ++a) N[g][a] = (a == g) ? 0.0 : 0.5;
+    } else {
+      ng = 4;
+      w = 0.25;
+      for (g = 0; g < 4; ++g)
+        for (a = 0; a < 4; ++a) N[g][a] = (a == g) ? tb : ta;
+    }
+    for (g = 0; g < ng; ++g)
+      for (a = 0; a < nen; ++a)
+        for (i = 0; i < d; ++i)
+          f[(int64_t)m->conn[e * nen + a] * d + i] += w * N[g][a] * vol * b[i];
+  }
+  return OK;
+}
+
 static int64_t find_col(const int32_t *col_idx, int64_t lo, int64_t hi, int64_t col) {
   while (lo < hi) {
     int64_t mid = lo + (hi - lo) / 2;

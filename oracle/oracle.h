@@ -69,6 +69,11 @@ int fem_ref_cg(const fem_ref_mesh *m, int op, const double *z, const int64_t *ro
                double rtol, double atol, int max_iter, int *iters, double *res0, double *res);
 /* volume-averaged first Piola-Kirchhoff stress sigma[dim*dim] (row-major), *volume = |Omega| */
 int fem_ref_mean_stress(const fem_ref_mesh *m, const double *z, double *sigma, double *volume);
+/* consistent nodal loads (added into f[n_nodes*dim]) of a traction on facets [nf][dim]
+ * (t [nf][dim]) and of a uniform body force b[dim] */
+int fem_ref_traction_load(int dim, int64_t n_nodes, const double *coords, int64_t nf,
+                          const int32_t *facets, const double *t, double *f);
+int fem_ref_body_load(const fem_ref_mesh *m, const double *b, double *f);
 int fem_ref_newton(const fem_ref_mesh *m, double *z /* in: lift, out: solution */, double atol,
                    double rtol, int max_iter, double cg_rtol, int cg_max_iter, int *iters,
                    int *cg_iters_total, double *res0, double *res);

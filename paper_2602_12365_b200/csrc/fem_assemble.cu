@@ -700,10 +700,11 @@ static fem_status assemble(Problem *p, const double *z, double *vals, unsigned f
     FEM_LAUNCH_CHECK("scatter-add assembly");
     return FEM_OK;
   }
-  // default: row-pull in 3D, one-sweep J_comp in 2D (C = 18 columns; measured 3x faster
-  // there, profiles/r01_sweep.csv); explicit mode flags override
+  // default: the fused node-tile row form (3D, and 2D without multipliers); the one-sweep
+  // J_comp form for 2D problems with MPC multipliers (A/B: profiles/)
   const bool rows = (flags & FEM_ASSEMBLE_ROWS) ||
-                    (!(flags & (FEM_ASSEMBLE_LITERAL | FEM_ASSEMBLE_JCOMP)) && p->dim == 3);
+                    (!(flags & (FEM_ASSEMBLE_LITERAL | FEM_ASSEMBLE_JCOMP)) &&
+                     (p->dim == 3 || p->n_mpc == 0));
   if (rows) {
     fem_status st0 = build_row_tiles(p, s);
     if (st0) return st0;

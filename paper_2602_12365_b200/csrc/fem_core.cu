@@ -465,6 +465,77 @@ __global__ void __launch_bounds__(kThreads) k_mean_stress(const double *coords, 
   }
 }
 
+// ------------------------------------------------------------------ external loads (f3)
+// Traction and body-force terms of the total potential energy (§6.1 Eq. P:366-372,
+// listing P:380-386): Psi -= int_St t . u dGamma + int_Omega b . u dOmega.  Both are linear in
+// u, so with P1 shape functions and a load constant per boundary facet / element they are
+// exactly the consistent nodal loads int N_a t = t |facet| / n_facet_nodes (one-point rule
+// of the Line2 / Tri3 boundary operator, exact here) and int N_a b = b vol / (d+1); they are
+// accumulated into the problem's f_ext, which the energy, residual and Newton already use.
+template <int D>
+__global__ void k_traction_load(const double *coords, const int32_t *facets, int64_t nf,
+                                const double *t, int64_t n_nodes, double *f, int *err) {
+  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < nf;
+       q += (int64_t)gridDim.x * blockDim.x) {
+    int32_t nd[D];
+    bool okid = true;
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+      nd[a] = facets[q * D + a];
+      okid = okid && nd[a] >= 0 && nd[a] < n_nodes;
+    }
+    if (!okid) { atomicOr(err, ERRW_ADJ_OVERFLOW); continue; }
+    double area;
+    if constexpr (D == 2) {  // Line2: length
+      const double dx = coords[nd[1] * 2] - coords[nd[0] * 2];
+      const double dy = coords[nd[1] * 2 + 1] - coords[nd[0] * 2 + 1];
+      area = sqrt(dx * dx + dy * dy);
+    } else {                 // Tri3: half the cross-product norm
+      double e1[3], e2[3];
+#pragma unroll
+      for (int i = 0; i < 3; ++i) {
+        e1[i] = coords[nd[1] * 3 + i] - coords[nd[0] * 3 + i];
+        e2[i] = coords[nd[2] * 3 + i] - coords[nd[0] * 3 + i];
+      }
+      const double cx = e1[1] * e2[2] - e1[2] * e2[1], cy = e1[2] * e2[0] - e1[0] * e2[2],
+                   cz = e1[0] * e2[1] - e1[1] * e2[0];
+      area = 0.5 * sqrt(cx * cx + cy * cy + cz * cz);
+    }
+    const double w = area / D;  // int N_a over the facet
+#pragma unroll
+    for (int a = 0; a < D; ++a)
+#pragma unroll
+      for (int i = 0; i < D; ++i) atomicAdd(f + (int64_t)nd[a] * D + i, w * t[q * D + i]);
+  }
+}
+
+template <int D>
+__global__ void k_body_load(const double *coords, const int32_t *conn, int64_t E, double b0,
+                            double b1, double b2, double *f) {
+  const double b[3] = {b0, b1, b2};
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < E;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    double x[D + 1][D], G[D + 1][D], vol;
+#pragma unroll
+    for (int a = 0; a < D + 1; ++a)
+#pragma unroll
+      for (int i = 0; i < D; ++i) x[a][i] = coords[(int64_t)conn[e * (D + 1) + a] * D + i];
+    geometry<D>(x, G, vol);
+    const double w = vol / (D + 1);
+#pragma unroll
+    for (int a = 0; a < D + 1; ++a)
+#pragma unroll
+      for (int i = 0; i < D; ++i) atomicAdd(f + (int64_t)conn[e * (D + 1) + a] * D + i, w * b[i]);
+  }
+}
+
+static fem_status ensure_fext(Problem *p, cudaStream_t s) {
+  if (p->f_ext) return FEM_OK;
+  FEM_CUDA(cudaMalloc(&p->f_ext, sizeof(double) * (p->n_u > 0 ? p->n_u : 1)));
+  FEM_CUDA(cudaMemsetAsync(p->f_ext, 0, sizeof(double) * (p->n_u > 0 ? p->n_u : 1), s));
+  return FEM_OK;
+}
+
 extern "C" {
 
 const char *fem_last_error(void) { return g_last_error.c_str(); }
@@ -711,6 +782,54 @@ fem_status fem_mean_stress(fem_problem *h, const double *z, double *sigma, doubl
   const double V = h_out[D * D];
   for (int q = 0; q < D * D; ++q) sigma[q] = V > 0.0 ? h_out[q] / V : 0.0;
   if (volume) *volume = V;
+  return FEM_OK;
+}
+
+fem_status fem_add_traction(fem_problem *h, int64_t n_facets, const int32_t *facets,
+                            const double *traction, fem_stream stream) {
+  FEM_ARG(h && n_facets >= 0, "fem_add_traction: bad arguments");
+  FEM_ARG(n_facets == 0 || (facets && traction), "fem_add_traction: null facets / traction");
+  Problem *p = &h->p;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (n_facets == 0) return FEM_OK;
+  fem_status st = ensure_fext(p, s);
+  if (st) return st;
+  const int g = grid_for(n_facets);
+  if (p->dim == 2) k_traction_load<2><<<g, kThreads, 0, s>>>(p->coords, facets, n_facets, traction, p->n_nodes, p->f_ext, p->d_err);
+  else k_traction_load<3><<<g, kThreads, 0, s>>>(p->coords, facets, n_facets, traction, p->n_nodes, p->f_ext, p->d_err);
+  FEM_LAUNCH_CHECK("traction load");
+  FEM_CUDA(cudaStreamSynchronize(s));
+  int herr = 0;
+  FEM_CUDA(cudaMemcpy(&herr, p->d_err, sizeof(int), cudaMemcpyDeviceToHost));
+  if (herr & ERRW_ADJ_OVERFLOW) {
+    FEM_CUDA(cudaMemset(p->d_err, 0, sizeof(int)));
+    set_error("fem_add_traction: facet node id out of range");
+    return FEM_ERR_INVALID_ARG;
+  }
+  return read_error_word(p, s);
+}
+
+fem_status fem_add_body_force(fem_problem *h, const double *b, fem_stream stream) {
+  FEM_ARG(h && b, "fem_add_body_force: null argument");
+  Problem *p = &h->p;
+  cudaStream_t s = (cudaStream_t)stream;
+  fem_status st = ensure_fext(p, s);
+  if (st) return st;
+  if (p->n_elems) {
+    const int g = grid_for(p->n_elems);
+    if (p->dim == 2) k_body_load<2><<<g, kThreads, 0, s>>>(p->coords, p->conn, p->n_elems, b[0], b[1], 0.0, p->f_ext);
+    else k_body_load<3><<<g, kThreads, 0, s>>>(p->coords, p->conn, p->n_elems, b[0], b[1], b[2], p->f_ext);
+    FEM_LAUNCH_CHECK("body load");
+  }
+  return FEM_OK;
+}
+
+fem_status fem_get_fext(fem_problem *h, double *f, fem_stream stream) {
+  FEM_ARG(h && f, "fem_get_fext: null argument");
+  Problem *p = &h->p;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (p->f_ext) FEM_CUDA(cudaMemcpyAsync(f, p->f_ext, sizeof(double) * p->n_u, cudaMemcpyDeviceToDevice, s));
+  else FEM_CUDA(cudaMemsetAsync(f, 0, sizeof(double) * p->n_u, s));
   return FEM_OK;
 }
 

@@ -38,7 +38,8 @@ STATUS = {0: "OK", 1: "INVALID_ARG", 2: "DEGENERATE_ELEMENT", 3: "INVERTED_ELEME
 EXPORTS = ("fem_create", "fem_destroy", "fem_query", "fem_check", "fem_apply_dirichlet",
            "fem_energy", "fem_residual", "fem_hvp", "fem_sparsity", "fem_color",
            "fem_assemble_csr", "fem_spmv", "fem_cg_solve", "fem_minres_solve",
-           "fem_mean_stress", "fem_newton_solve",
+           "fem_mean_stress", "fem_add_traction", "fem_add_body_force", "fem_get_fext",
+           "fem_newton_solve",
            "fem_nccl_unique_id", "fem_nccl_comm_init", "fem_nccl_comm_destroy",
            "fem_allreduce_sum", "fem_halo_size", "fem_halo_pack", "fem_halo_combine",
            "fem_last_error", "fem_version")
@@ -114,6 +115,9 @@ def load_library():
         lib.fem_cg_solve.argtypes = [vp, vp, vp, vp, vp, C.POINTER(CgOpts), C.POINTER(CgReport), vp]
         lib.fem_minres_solve.argtypes = [vp, vp, vp, vp, vp, C.POINTER(CgOpts), C.POINTER(CgReport), vp]
         lib.fem_mean_stress.argtypes = [vp, vp, C.POINTER(C.c_double), C.POINTER(C.c_double), vp]
+        lib.fem_add_traction.argtypes = [vp, C.c_int64, vp, vp, vp]
+        lib.fem_add_body_force.argtypes = [vp, C.POINTER(C.c_double), vp]
+        lib.fem_get_fext.argtypes = [vp, vp, vp]
         lib.fem_newton_solve.argtypes = [vp, vp, C.POINTER(NewtonOpts), C.POINTER(NewtonReport), vp]
         lib.fem_nccl_unique_id.argtypes = [C.c_char_p]
         lib.fem_nccl_comm_init.argtypes = [C.c_char_p, C.c_int, C.c_int, C.POINTER(vp)]
@@ -336,6 +340,26 @@ class Problem:
         _check(load_library().fem_mean_stress(self._h, _ptr(z), sig, C.byref(vol), _stream()),
                "fem_mean_stress")
         return np.array(sig[:], dtype=np.float64).reshape(self.dim, self.dim), vol.value
+
+    def add_traction(self, facets, traction) -> None:
+        """Psi -= int t . u over boundary facets (Line2 / Tri3); traction [n_facets][dim]
+        (or one [dim] vector for all) — fem_add_traction."""
+        f = torch.as_tensor(np.ascontiguousarray(facets, dtype=np.int32), device=self.device)
+        t = np.asarray(traction, np.float64)
+        if t.ndim == 1:
+            t = np.tile(t, (len(f), 1))
+        t = torch.as_tensor(np.ascontiguousarray(t), device=self.device)
+        _check(load_library().fem_add_traction(self._h, len(f), _ptr(f), _ptr(t), _stream()),
+               "fem_add_traction")
+
+    def add_body_force(self, b) -> None:
+        bb = (C.c_double * 3)(*([float(x) for x in b] + [0.0] * (3 - len(b))))
+        _check(load_library().fem_add_body_force(self._h, bb, _stream()), "fem_add_body_force")
+
+    def f_ext(self) -> torch.Tensor:
+        out = torch.empty(self.n_u, dtype=torch.float64, device=self.device)
+        _check(load_library().fem_get_fext(self._h, _ptr(out), _stream()), "fem_get_fext")
+        return out
 
     # ---------------------------------------------------------------- multi-GPU halo
     def halo_size(self) -> int:

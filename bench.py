@@ -180,7 +180,7 @@ def algorithmic(mesh, nnz, C, mode):
     f_ctx = fr + 2 * d * d * nen
     f_blocks = nen * nen * (2 * d + 6 * d * d)
     asm_bytes = conn + coords + vec + 8 * nnz                          # inputs + vals written once
-    if mode in ("batched", "literal") or (mode == "auto" and d == 2):  # J_comp written + read
+    if mode in ("batched", "literal") or (mode == "auto" and d == 2 and mesh.n_mpc):  # J_comp
         asm_bytes += 2 * 8 * N * C + nnz * (4 + 4)
     return {
         "energy": {"bytes": conn + coords + vec, "flops": fe * E},

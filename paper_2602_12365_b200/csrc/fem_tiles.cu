@@ -422,12 +422,175 @@ struct PipeArgs {
   int *err;
 };
 
-template <int D, int MAT, int OP, bool MASK, bool DET>
-__global__ void __launch_bounds__(kTile, pipe_minb(OP, MAT)) k_tile_pipe(PipeArgs A) {
+template <int D, int MAT, int OP, bool MASK>
+__device__ __forceinline__ void tile_phase1(const PipeArgs &A, const unsigned char *m,
+                                            const double *xs, const double *us, const double *vs,
+                                            int64_t t, int tid, double *cb, double &eacc) {
   constexpr int NEN = D + 1;
   constexpr bool NEED_U = (OP != OP_HVP) || (MAT == FEM_NEO_HOOKEAN);
+  const int64_t e = t * kTile + tid;
+  if (e < A.E) {
+    const ushort4 lc4 = reinterpret_cast<const ushort4 *>(m + A.off_lconn)[tid];
+    const int lc[4] = {lc4.x, lc4.y, lc4.z, lc4.w};
+    double x[NEN][D], c[D][D];
+#pragma unroll
+    for (int a = 0; a < NEN; ++a)
+#pragma unroll
+      for (int i = 0; i < D; ++i) x[a][i] = xs[lc[a] * D + i];
+    const double det = cof_gradients<D>(x, c);
+    const double id = 1.0 / det;
+    constexpr double inv_fact = (D == 3) ? 1.0 / 6.0 : 0.5;  // vol = det / d!
+    double lam = A.lam, mu = A.mu;
+    if (A.has_phase) {
+      const int ph = m[A.off_ph + tid];
+      lam = A.lam_tab[ph];
+      mu = A.mu_tab[ph];
+    }
+    double H[D][D];
+    if constexpr (NEED_U) {
+      double u[NEN][D];
+#pragma unroll
+      for (int a = 0; a < NEN; ++a)
+#pragma unroll
+        for (int i = 0; i < D; ++i) u[a][i] = us[lc[a] * D + i];
+      grad_hat<D>(u, c, H);
+#pragma unroll
+      for (int i = 0; i < D; ++i)
+#pragma unroll
+        for (int j = 0; j < D; ++j) H[i][j] *= id;
+    }
+    bool ok = true;
+    double S[D][D];
+    if constexpr (OP == OP_ENERGY) {
+      const double vol = det * inv_fact;
+      if constexpr (MAT == FEM_LINEAR_ELASTIC) {
+        eacc += vol * le_psi<D>(H, lam, mu);
+      } else {
+        NHState<D> s;
+        ok = nh_state<D>(H, s);
+        if (ok) eacc += vol * nh_psi<D>(H, s, lam, mu);
+      }
+    } else if constexpr (OP == OP_RESIDUAL) {
+      // vol P G_a = (P / d!) c_a; P linear in (lambda, mu)
+      const double ls = lam * inv_fact, ms = mu * inv_fact;
+      if constexpr (MAT == FEM_LINEAR_ELASTIC) {
+        le_stress<D>(H, ls, ms, S);
+      } else {
+        NHState<D> s;
+        ok = nh_state<D>(H, s);
+        if (ok) nh_stress<D>(s, ls, ms, S);
+      }
+    } else {
+      // dH = dHh / det; vol dP(dH) G_a = dP(dHh) c_a * (1 / (det d!)): fold into (lambda, mu)
+      double v[NEN][D], dH[D][D];
+#pragma unroll
+      for (int a = 0; a < NEN; ++a) {
+        const unsigned bc = MASK ? m[A.off_bc + lc[a]] : 0u;
+#pragma unroll
+        for (int i = 0; i < D; ++i) v[a][i] = (bc & (1u << i)) ? 0.0 : vs[lc[a] * D + i];
+      }
+      grad_hat<D>(v, c, dH);
+      const double sc = id * inv_fact;
+      const double ls = lam * sc, ms = mu * sc;
+      if constexpr (MAT == FEM_LINEAR_ELASTIC) {
+        le_stress<D>(dH, ls, ms, S);
+      } else {
+        NHState<D> s;
+        ok = nh_state<D>(H, s);
+        if (ok) nh_dstress<D>(s, ls, ms, dH, S);
+      }
+    }
+    if (!ok) atomicOr(A.err, ERRW_INVERTED);
+    if constexpr (OP != OP_ENERGY) {
+      double f[NEN][D];
+      nodal_from_c<D>(S, c, f);
+#pragma unroll
+      for (int a = 0; a < NEN; ++a)
+#pragma unroll
+        for (int i = 0; i < D; ++i) cb[(a * D + i) * kTile + tid] = ok ? f[a][i] : 0.0;
+    }
+  }
+}
+
+// Phase 2: fixed-order per-tile-node sums of the contributions, stored (interior nodes),
+// RED (tile-boundary nodes) or written to the node's slot (DET).
+template <int D, int OP, bool DET>
+__device__ __forceinline__ void tile_phase2(const PipeArgs &A, const unsigned char *m, int U,
+                                            int64_t t, int tid, const double *cb) {
+  {
+    // phase 2: fixed-order per-tile-node sums
+    const uint16_t *ptr = reinterpret_cast<const uint16_t *>(m + A.off_ptr);
+    const uint16_t *inc = reinterpret_cast<const uint16_t *>(m + A.off_inc);
+    const int32_t *nodes = reinterpret_cast<const int32_t *>(m + A.off_nodes);
+    for (int r = tid; r < U; r += kTile) {  // one thread per tile node, D components
+      const int lo = ptr[r], hi = ptr[r + 1];
+      double sacc[D];
+#pragma unroll
+      for (int cc = 0; cc < D; ++cc) sacc[cc] = 0.0;
+      for (int w = lo; w < hi; ++w) {
+        const int pk = inc[w];
+        const int el = pk >> 2, a = pk & 3;
+#pragma unroll
+        for (int cc = 0; cc < D; ++cc) sacc[cc] += cb[(a * D + cc) * kTile + el];
+      }
+      if constexpr (DET) {
+        double *slot = A.slots + (A.slot_off[t] + r) * D;
+#pragma unroll
+        for (int cc = 0; cc < D; ++cc) slot[cc] = sacc[cc];
+      } else {
+        const int64_t g = (int64_t)nodes[r] * D;
+        if (m[A.off_int + r]) {
+#pragma unroll
+          for (int cc = 0; cc < D; ++cc) A.out[g + cc] = sacc[cc];
+        } else {
+#pragma unroll
+          for (int cc = 0; cc < D; ++cc) atomicAdd(A.out + g + cc, sacc[cc]);
+        }
+      }
+    }
+    }
+
+}
+
+// Residual / energy: CTA-wide pipeline (cp.async.wait_all + barrier per tile).  HVP (the
+// register-heaviest, 2 CTAs/SM): barrier-free data path — every thread's cp.async copies of
+// a stage arrive (cp.async.mbarrier.arrive.noinc) on that stage buffer's mbarrier (expected
+// count kTile) and consumers wait on its phase; the only __syncthreads per tile separates
+// phase 1 from phase 2, and the contribution array is double-buffered, so threads that
+// finish phase 2 of tile k go on to phase 1 of tile k+1 while others are still summing.
+// Buffer reuse is ordered by that barrier: tile k+1's node data overwrites tile k-1's (read
+// in phase 1 of k-1, before barrier k-1); tile k+2's metadata overwrites tile k-1's (read in
+// phase 2 of k-1, before barrier k) and is issued after barrier k.  A/B (profiles/): HVP
+// 1.13 -> 1.06 ms; residual / energy slower this way (smem of the second buffer, 3-4 CTAs/SM).
+__device__ __forceinline__ unsigned smem_addr(const void *p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mb_init(uint64_t *m, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_addr(m)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mb_cp_arrive(uint64_t *m) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(smem_addr(m)) : "memory");
+}
+__device__ __forceinline__ void mb_wait(uint64_t *m, unsigned parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n}\n" ::"r"(smem_addr(m)),
+      "r"(parity)
+      : "memory");
+}
+
+template <int OP>
+constexpr bool pipe_decoupled() { return OP == OP_HVP; }
+
+template <int D, int MAT, int OP, bool MASK, bool DET>
+__global__ void __launch_bounds__(kTile, pipe_minb(OP, MAT)) k_tile_pipe(PipeArgs A) {
+  constexpr bool NEED_U = (OP != OP_HVP) || (MAT == FEM_NEO_HOOKEAN);
   constexpr int NF = 1 + (NEED_U ? 1 : 0) + (OP == OP_HVP ? 1 : 0);
+  constexpr bool DEC = pipe_decoupled<OP>();
   extern __shared__ __align__(16) unsigned char sm[];
+  __shared__ __align__(8) uint64_t mb_meta[3], mb_node[2];
   const int tid = threadIdx.x;
   const int mb = A.mb, um = A.um;
   const int nstride = um * D * NF;
@@ -436,11 +599,14 @@ __global__ void __launch_bounds__(kTile, pipe_minb(OP, MAT)) k_tile_pipe(PipeArg
   double *contrib = nodeb + 2 * nstride;
   const int64_t G = gridDim.x;
 
-  auto issue_meta = [&](int64_t t, unsigned char *dst) {
+  auto issue_meta = [&](int64_t t, int b) {
+    unsigned char *dst = metab + b * mb;
     const unsigned char *src = A.meta + t * (int64_t)mb;
     for (int off = tid * 16; off < mb; off += kTile * 16) cp_async16(dst + off, src + off);
+    if constexpr (DEC) mb_cp_arrive(&mb_meta[b]);
   };
-  auto issue_nodes = [&](const unsigned char *m, double *dst) {
+  auto issue_nodes = [&](const unsigned char *m, int b) {
+    double *dst = nodeb + b * nstride;
     const int U = reinterpret_cast<const int *>(m)[0];
     const int32_t *nodes = reinterpret_cast<const int32_t *>(m + A.off_nodes);
     for (int i = tid; i < U * D; i += kTile) {
@@ -449,166 +615,67 @@ __global__ void __launch_bounds__(kTile, pipe_minb(OP, MAT)) k_tile_pipe(PipeArg
       if constexpr (NEED_U) cp_async8(dst + um * D + i, A.u + g);
       if constexpr (OP == OP_HVP) cp_async8(dst + (NF - 1) * um * D + i, A.v + g);
     }
+    if constexpr (DEC) mb_cp_arrive(&mb_node[b]);
   };
 
   double eacc = 0.0;
   int64_t t = blockIdx.x;
-  if (t < A.n_tiles) {
-    issue_meta(t, metab);
-    cp_async_commit();
-    cp_async_wait_all();
-    __syncthreads();
-    issue_nodes(metab, nodeb);
-    if (t + G < A.n_tiles) issue_meta(t + G, metab + mb);
-    cp_async_commit();
-  }
-  for (int k = 0; t < A.n_tiles; ++k, t += G) {
-    cp_async_wait_all();
-    __syncthreads();
-    const unsigned char *m = metab + (k % 3) * mb;
-    const double *nb = nodeb + (k & 1) * nstride;
-    if (t + G < A.n_tiles) issue_nodes(metab + ((k + 1) % 3) * mb, nodeb + ((k + 1) & 1) * nstride);
-    if (t + 2 * G < A.n_tiles) issue_meta(t + 2 * G, metab + ((k + 2) % 3) * mb);
-    cp_async_commit();
-
-    const int U = reinterpret_cast<const int *>(m)[0];
-    const double *xs = nb, *us = nb + um * D, *vs = nb + (NF - 1) * um * D;
-    // phase 1: one element per thread
-    const int64_t e = t * kTile + tid;
-    if (e < A.E) {
-      const ushort4 lc4 = reinterpret_cast<const ushort4 *>(m + A.off_lconn)[tid];
-      const int lc[4] = {lc4.x, lc4.y, lc4.z, lc4.w};
-      double x[NEN][D], c[D][D];
-#pragma unroll
-      for (int a = 0; a < NEN; ++a)
-#pragma unroll
-        for (int i = 0; i < D; ++i) x[a][i] = xs[lc[a] * D + i];
-      const double det = cof_gradients<D>(x, c);
-      const double id = 1.0 / det;
-      constexpr double inv_fact = (D == 3) ? 1.0 / 6.0 : 0.5;  // vol = det / d!
-      double lam = A.lam, mu = A.mu;
-      if (A.has_phase) {
-        const int ph = m[A.off_ph + tid];
-        lam = A.lam_tab[ph];
-        mu = A.mu_tab[ph];
-      }
-      double H[D][D];
-      if constexpr (NEED_U) {
-        double u[NEN][D];
-#pragma unroll
-        for (int a = 0; a < NEN; ++a)
-#pragma unroll
-          for (int i = 0; i < D; ++i) u[a][i] = us[lc[a] * D + i];
-        grad_hat<D>(u, c, H);
-#pragma unroll
-        for (int i = 0; i < D; ++i)
-#pragma unroll
-          for (int j = 0; j < D; ++j) H[i][j] *= id;
-      }
-      bool ok = true;
-      double S[D][D];
-      if constexpr (OP == OP_ENERGY) {
-        const double vol = det * inv_fact;
-        if constexpr (MAT == FEM_LINEAR_ELASTIC) {
-          eacc += vol * le_psi<D>(H, lam, mu);
-        } else {
-          NHState<D> s;
-          ok = nh_state<D>(H, s);
-          if (ok) eacc += vol * nh_psi<D>(H, s, lam, mu);
-        }
-      } else if constexpr (OP == OP_RESIDUAL) {
-        // vol P G_a = (P / d!) c_a; P linear in (lambda, mu)
-        const double ls = lam * inv_fact, ms = mu * inv_fact;
-        if constexpr (MAT == FEM_LINEAR_ELASTIC) {
-          le_stress<D>(H, ls, ms, S);
-        } else {
-          NHState<D> s;
-          ok = nh_state<D>(H, s);
-          if (ok) nh_stress<D>(s, ls, ms, S);
-        }
-      } else {
-        // dH = dHh / det; vol dP(dH) G_a = dP(dHh) c_a * (1 / (det d!)): fold into (lambda, mu)
-        double v[NEN][D], dH[D][D];
-#pragma unroll
-        for (int a = 0; a < NEN; ++a) {
-          const unsigned bc = MASK ? m[A.off_bc + lc[a]] : 0u;
-#pragma unroll
-          for (int i = 0; i < D; ++i) v[a][i] = (bc & (1u << i)) ? 0.0 : vs[lc[a] * D + i];
-        }
-        grad_hat<D>(v, c, dH);
-        const double sc = id * inv_fact;
-        const double ls = lam * sc, ms = mu * sc;
-        if constexpr (MAT == FEM_LINEAR_ELASTIC) {
-          le_stress<D>(dH, ls, ms, S);
-        } else {
-          NHState<D> s;
-          ok = nh_state<D>(H, s);
-          if (ok) nh_dstress<D>(s, ls, ms, dH, S);
-        }
-      }
-      if (!ok) atomicOr(A.err, ERRW_INVERTED);
-      if constexpr (OP != OP_ENERGY) {
-        double f[NEN][D];
-        nodal_from_c<D>(S, c, f);
-#pragma unroll
-        for (int a = 0; a < NEN; ++a)
-#pragma unroll
-          for (int i = 0; i < D; ++i) contrib[(a * D + i) * kTile + tid] = ok ? f[a][i] : 0.0;
-      }
+  if constexpr (DEC) {
+    if (tid == 0) {
+      for (int b = 0; b < 3; ++b) mb_init(&mb_meta[b], kTile);
+      for (int b = 0; b < 2; ++b) mb_init(&mb_node[b], kTile);
+      asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
-    if constexpr (OP != OP_ENERGY) {
+    __syncthreads();
+    if (t < A.n_tiles) issue_meta(t, 0);
+    if (t + G < A.n_tiles) issue_meta(t + G, 1);
+    if (t < A.n_tiles) {
+      mb_wait(&mb_meta[0], 0);
+      issue_nodes(metab, 0);
+    }
+    for (int k = 0; t < A.n_tiles; ++k, t += G) {
+      const int bm = k % 3, bn = k & 1;
+      const unsigned char *m = metab + bm * mb;
+      mb_wait(&mb_node[bn], (unsigned)(k >> 1) & 1u);  // node data of tile k
+      if (t + G < A.n_tiles) {  // node data of tile k+1 (its metadata issued after barrier k-1)
+        const int bm1 = (k + 1) % 3;
+        mb_wait(&mb_meta[bm1], (unsigned)((k + 1) / 3) & 1u);
+        issue_nodes(metab + bm1 * mb, bn ^ 1);
+      }
+      const double *nb = nodeb + bn * nstride;
+      double *cb = contrib + (k & 1) * ((D + 1) * D * kTile);
+      tile_phase1<D, MAT, OP, MASK>(A, m, nb, nb + um * D, nb + (NF - 1) * um * D, t, tid, cb, eacc);
+      __syncthreads();  // phase 1 of tile k done; tile k-1 fully consumed
+      if (t + 2 * G < A.n_tiles) issue_meta(t + 2 * G, (k + 2) % 3);
+      if constexpr (OP != OP_ENERGY)
+        tile_phase2<D, OP, DET>(A, m, reinterpret_cast<const int *>(m)[0], t, tid, cb);
+    }
+    asm volatile("cp.async.wait_all;\n" ::: "memory");
+  } else {
+    if (t < A.n_tiles) {
+      issue_meta(t, 0);
+      cp_async_commit();
+      cp_async_wait_all();
       __syncthreads();
-      // phase 2: fixed-order per-tile-node sums
-      const uint16_t *ptr = reinterpret_cast<const uint16_t *>(m + A.off_ptr);
-      const uint16_t *inc = reinterpret_cast<const uint16_t *>(m + A.off_inc);
-      const int32_t *nodes = reinterpret_cast<const int32_t *>(m + A.off_nodes);
-#if FEM_PHASE2_SPLIT
-      for (int q = tid; q < U * D; q += kTile) {  // (tile node, component) items
-        const int r = q / D, cc = q - r * D;
-        const int lo = ptr[r], hi = ptr[r + 1];
-        double sacc = 0.0;
-        for (int w = lo; w < hi; ++w) {
-          const int pk = inc[w];
-          sacc += contrib[((pk & 3) * D + cc) * kTile + (pk >> 2)];
-        }
-        if constexpr (DET) {
-          A.slots[(A.slot_off[t] + r) * D + cc] = sacc;
-        } else {
-          const int64_t g = (int64_t)nodes[r] * D + cc;
-          if (m[A.off_int + r]) A.out[g] = sacc;
-          else atomicAdd(A.out + g, sacc);
-        }
-      }
-#else
-      for (int r = tid; r < U; r += kTile) {  // one thread per tile node, D components
-        const int lo = ptr[r], hi = ptr[r + 1];
-        double sacc[D];
-#pragma unroll
-        for (int cc = 0; cc < D; ++cc) sacc[cc] = 0.0;
-        for (int w = lo; w < hi; ++w) {
-          const int pk = inc[w];
-          const int el = pk >> 2, a = pk & 3;
-#pragma unroll
-          for (int cc = 0; cc < D; ++cc) sacc[cc] += contrib[(a * D + cc) * kTile + el];
-        }
-        if constexpr (DET) {
-          double *slot = A.slots + (A.slot_off[t] + r) * D;
-#pragma unroll
-          for (int cc = 0; cc < D; ++cc) slot[cc] = sacc[cc];
-        } else {
-          const int64_t g = (int64_t)nodes[r] * D;
-          if (m[A.off_int + r]) {
-#pragma unroll
-            for (int cc = 0; cc < D; ++cc) A.out[g + cc] = sacc[cc];
-          } else {
-#pragma unroll
-            for (int cc = 0; cc < D; ++cc) atomicAdd(A.out + g + cc, sacc[cc]);
-          }
-        }
-      }
-#endif
+      issue_nodes(metab, 0);
+      if (t + G < A.n_tiles) issue_meta(t + G, 1);
+      cp_async_commit();
     }
-    __syncthreads();
+    for (int k = 0; t < A.n_tiles; ++k, t += G) {
+      cp_async_wait_all();
+      __syncthreads();
+      const unsigned char *m = metab + (k % 3) * mb;
+      const double *nb = nodeb + (k & 1) * nstride;
+      if (t + G < A.n_tiles) issue_nodes(metab + ((k + 1) % 3) * mb, (k + 1) & 1);
+      if (t + 2 * G < A.n_tiles) issue_meta(t + 2 * G, (k + 2) % 3);
+      cp_async_commit();
+      tile_phase1<D, MAT, OP, MASK>(A, m, nb, nb + um * D, nb + (NF - 1) * um * D, t, tid, contrib, eacc);
+      if constexpr (OP != OP_ENERGY) {
+        __syncthreads();
+        tile_phase2<D, OP, DET>(A, m, reinterpret_cast<const int *>(m)[0], t, tid, contrib);
+      }
+      __syncthreads();
+    }
   }
   if constexpr (OP == OP_ENERGY) {
     const double tsum = block_sum<kTile>(eacc);
@@ -648,7 +715,7 @@ static fem_status launch_pipe_t(Problem *p, const PipeArgs &a, cudaStream_t s) {
   const bool need_u = (OP != OP_HVP) || (MAT == FEM_NEO_HOOKEAN);
   const int nf = 1 + (need_u ? 1 : 0) + (OP == OP_HVP ? 1 : 0);
   const size_t smem = (size_t)3 * T.mb + sizeof(double) * 2 * (size_t)T.um * D * nf +
-                      (OP == OP_ENERGY ? 0 : sizeof(double) * (size_t)(D + 1) * D * kTile);
+                      (OP == OP_ENERGY ? 0 : (pipe_decoupled<OP>() ? 2 : 1) * sizeof(double) * (size_t)(D + 1) * D * kTile);
   auto kern = k_tile_pipe<D, MAT, OP, MASK, DET>;
   FEM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   kern<<<pipe_grid(p, OP), kTile, smem, s>>>(a);

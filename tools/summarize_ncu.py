@@ -16,7 +16,7 @@ import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 PHASE_OF = {"k_tile_pipe<3, 1, 0": "energy", "k_tile_pipe<3, 1, 1": "residual",
-            "k_tile_pipe<3, 1, 2": "hvp", "k_rows_fused": "assemble", "k_rows_pull": "assemble", "k_elem_ctx": "assemble",
+            "k_tile_pipe<3, 1, 2": "hvp", "k_rows_fused": "assemble", "k_rows_pull": "assemble", "k_rows_tile": "assemble", "k_elem_ctx": "assemble",
             "k_spmv": "spmv"}
 
 

@@ -236,7 +236,10 @@ fem_status fem_mean_stress(fem_problem *p, const double *z, double *sigma, doubl
  * and loads constant per facet, exactly the consistent nodal loads t |facet| / dim and
  * b vol / (dim+1): both are ADDED to the problem's f_ext (energy, residual and Newton use
  * it; the HVP is unchanged).  facets [n_facets][dim] node ids, traction [n_facets][dim]
- * (device).  fem_add_traction synchronizes `stream` (id check: INVALID_ARG).
+ * (device).  On a multi-GPU problem every facet is passed to one rank (that of its element)
+ * and the loads of shared nodes are summed over the ranks (halo add), so f_ext holds the
+ * global nodal load on every rank.  Both synchronize `stream` (facet ids out of range:
+ * INVALID_ARG).
  * fem_get_fext copies the accumulated f_ext [N_u] (device). */
 fem_status fem_add_traction(fem_problem *p, int64_t n_facets, const int32_t *facets,
                             const double *traction, fem_stream stream);

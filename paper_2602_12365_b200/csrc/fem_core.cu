@@ -794,11 +794,18 @@ fem_status fem_add_traction(fem_problem *h, int64_t n_facets, const int32_t *fac
   if (n_facets == 0) return FEM_OK;
   fem_status st = ensure_fext(p, s);
   if (st) return st;
+  double *tmp = nullptr;  // this rank's facet loads, summed over the ranks sharing a node
+  FEM_CUDA(cudaMalloc(&tmp, sizeof(double) * (p->N > 0 ? p->N : 1)));
+  FEM_CUDA(cudaMemsetAsync(tmp, 0, sizeof(double) * (p->N > 0 ? p->N : 1), s));
   const int g = grid_for(n_facets);
-  if (p->dim == 2) k_traction_load<2><<<g, kThreads, 0, s>>>(p->coords, facets, n_facets, traction, p->n_nodes, p->f_ext, p->d_err);
-  else k_traction_load<3><<<g, kThreads, 0, s>>>(p->coords, facets, n_facets, traction, p->n_nodes, p->f_ext, p->d_err);
+  if (p->dim == 2) k_traction_load<2><<<g, kThreads, 0, s>>>(p->coords, facets, n_facets, traction, p->n_nodes, tmp, p->d_err);
+  else k_traction_load<3><<<g, kThreads, 0, s>>>(p->coords, facets, n_facets, traction, p->n_nodes, tmp, p->d_err);
   FEM_LAUNCH_CHECK("traction load");
+  if (p->size > 1) st = halo_add(p, tmp, s);
+  if (!st) k_axpy<<<grid_for(p->n_u), kThreads, 0, s>>>(p->f_ext, tmp, 1.0, p->n_u, nullptr, p->dim);
   FEM_CUDA(cudaStreamSynchronize(s));
+  cudaFree(tmp);
+  if (st) return st;
   int herr = 0;
   FEM_CUDA(cudaMemcpy(&herr, p->d_err, sizeof(int), cudaMemcpyDeviceToHost));
   if (herr & ERRW_ADJ_OVERFLOW) {
@@ -815,13 +822,20 @@ fem_status fem_add_body_force(fem_problem *h, const double *b, fem_stream stream
   cudaStream_t s = (cudaStream_t)stream;
   fem_status st = ensure_fext(p, s);
   if (st) return st;
+  double *tmp = nullptr;  // this rank's element loads, summed over the ranks sharing a node
+  FEM_CUDA(cudaMalloc(&tmp, sizeof(double) * (p->N > 0 ? p->N : 1)));
+  FEM_CUDA(cudaMemsetAsync(tmp, 0, sizeof(double) * (p->N > 0 ? p->N : 1), s));
   if (p->n_elems) {
     const int g = grid_for(p->n_elems);
-    if (p->dim == 2) k_body_load<2><<<g, kThreads, 0, s>>>(p->coords, p->conn, p->n_elems, b[0], b[1], 0.0, p->f_ext);
-    else k_body_load<3><<<g, kThreads, 0, s>>>(p->coords, p->conn, p->n_elems, b[0], b[1], b[2], p->f_ext);
+    if (p->dim == 2) k_body_load<2><<<g, kThreads, 0, s>>>(p->coords, p->conn, p->n_elems, b[0], b[1], 0.0, tmp);
+    else k_body_load<3><<<g, kThreads, 0, s>>>(p->coords, p->conn, p->n_elems, b[0], b[1], b[2], tmp);
     FEM_LAUNCH_CHECK("body load");
   }
-  return FEM_OK;
+  if (p->size > 1) st = halo_add(p, tmp, s);
+  if (!st) k_axpy<<<grid_for(p->n_u), kThreads, 0, s>>>(p->f_ext, tmp, 1.0, p->n_u, nullptr, p->dim);
+  FEM_CUDA(cudaStreamSynchronize(s));
+  cudaFree(tmp);
+  return st;
 }
 
 fem_status fem_get_fext(fem_problem *h, double *f, fem_stream stream) {

@@ -264,6 +264,49 @@ typedef struct {
 fem_status fem_newton_solve(fem_problem *p, double *z, const fem_newton_opts *opts,
                             fem_newton_report *report, fem_stream stream);
 
+/* ---------------------------------------------------------------- virtual-work path (f4)
+ * Non-variational problems by the principle of virtual work (§3.1): a
+ * scalar field c on a P1 mesh with W(c, v) = sum_e vol_e [ D grad c . grad v + (w_e . grad c)
+ * vbar_e ] + m sum_a V_a (c_a - cold_a) v_a (one-point rule: vbar_e = mean of v over the
+ * element, w_e = mean nodal velocity; V_a = lumped nodal volume; m = 1/dt, 0 = steady) —
+ * the advection-diffusion example of P:772-802 on a flat mesh.  r = grad_v W at v = 0
+ * (P:232); the tangent K = grad_c r is non-symmetric (advection), applied matrix-free
+ * (fem_vw_jvp) and solved with restarted GMRES.  Dirichlet nodes: r[D] = 0 and the masked
+ * operator P_f K P_f + P_D, as for the elastic path. */
+typedef struct fem_vw_problem fem_vw_problem; /* opaque, library-owned */
+typedef struct {
+  int dim;                          /* 2 (Tri3) or 3 (Tet4)                                   */
+  int64_t n_nodes, n_elems;
+  const double *coords;             /* [n_nodes][dim]                                         */
+  const int32_t *conn;              /* [n_elems][dim+1], positively oriented                  */
+  double diffusivity;               /* D >= 0                                                 */
+  const double *velocity;           /* [n_nodes][dim] nodal velocity                          */
+  double mass_coef;                 /* m = 1/dt >= 0 (lumped mass), 0: steady                 */
+  int64_t n_dirichlet;
+  const int32_t *dirichlet_nodes;   /* unique node ids                                        */
+  const double *dirichlet_vals;
+} fem_vw_desc;
+typedef struct {
+  int restart;                      /* Krylov dimension per cycle, 1..64                       */
+  int max_iter;                     /* total Arnoldi steps                                    */
+  double rtol, atol;                /* stop when ||b - A x|| <= max(rtol ||b||, atol)          */
+} fem_gmres_opts;
+/* create copies the inputs (host or device pointers); synchronizes `stream`. */
+fem_status fem_vw_create(fem_vw_problem **p, const fem_vw_desc *d, fem_stream stream);
+fem_status fem_vw_destroy(fem_vw_problem *p);
+fem_status fem_vw_apply_dirichlet(fem_vw_problem *p, double *c, fem_stream stream);
+/* r [n_nodes] = grad_v W(c, v)|_{v=0}; c_old may be NULL (= 0); flags: FEM_APPLY_BC */
+fem_status fem_vw_residual(fem_vw_problem *p, const double *c, const double *c_old, double *r,
+                           unsigned flags, fem_stream stream);
+/* y = K x (FEM_APPLY_BC: the masked operator) */
+fem_status fem_vw_jvp(fem_vw_problem *p, const double *x, double *y, unsigned flags,
+                      fem_stream stream);
+/* GMRES(restart) on the masked operator; x: in x0, out solution; report as for CG
+ * (res = the Arnoldi residual estimate).  Synchronizes `stream`. */
+fem_status fem_vw_gmres_solve(fem_vw_problem *p, const double *b, double *x,
+                              const fem_gmres_opts *opts, fem_cg_report *report,
+                              fem_stream stream);
+
 /* NCCL bootstrap for fem_dist_desc: rank 0 creates the id, the caller
  * broadcasts its 128 bytes (torch.distributed), every rank initialises the comm. */
 fem_status fem_nccl_unique_id(unsigned char id[128]);

@@ -289,6 +289,55 @@ class Oracle:
         return z, {"iters": max_iter, "res0": r0, "res": nr, "converged": False}
 
 
+class _Vw(C.Structure):
+    _fields_ = [("dim", C.c_int), ("n_nodes", C.c_int64), ("n_elems", C.c_int64),
+                ("coords", C.c_void_p), ("conn", C.c_void_p), ("diffusivity", C.c_double),
+                ("velocity", C.c_void_p), ("mass_coef", C.c_double), ("n_dirichlet", C.c_int64),
+                ("dirichlet_nodes", C.c_void_p), ("dirichlet_vals", C.c_void_p)]
+
+
+class VwOracle:
+    """Virtual-work path (f4): fem_ref_vw_residual / fem_ref_vw_jvp on host arrays."""
+
+    def __init__(self, coords, conn, diffusivity, velocity, mass_coef=0.0, dirichlet_nodes=None,
+                 dirichlet_vals=None):
+        self.coords = np.ascontiguousarray(coords, np.float64)
+        self.conn = np.ascontiguousarray(conn, np.int32)
+        self.vel = np.ascontiguousarray(velocity, np.float64)
+        dn = np.zeros(0, np.int32) if dirichlet_nodes is None else dirichlet_nodes
+        dv = np.zeros(0) if dirichlet_vals is None else dirichlet_vals
+        self.dn = np.ascontiguousarray(dn, np.int32)
+        self.dv = np.ascontiguousarray(dv, np.float64)
+        self.n = self.coords.shape[0]
+        self.s = _Vw(self.coords.shape[1], self.n, self.conn.shape[0], _p(self.coords),
+                     _p(self.conn), diffusivity, _p(self.vel), mass_coef, len(self.dn),
+                     _p(self.dn), _p(self.dv))
+
+    def residual(self, c, c_old=None, bc=False):
+        c = np.ascontiguousarray(c, np.float64)
+        co = None if c_old is None else np.ascontiguousarray(c_old, np.float64)
+        r = np.zeros(self.n)
+        st = lib().fem_ref_vw_residual(C.byref(self.s), C.c_void_p(c.ctypes.data),
+                                       C.c_void_p(_p(co)), C.c_void_p(r.ctypes.data),
+                                       C.c_uint(APPLY_BC if bc else 0))
+        if st:
+            raise OracleError(st, "fem_ref_vw_residual")
+        return r
+
+    def jvp(self, x, bc=False):
+        x = np.ascontiguousarray(x, np.float64)
+        y = np.zeros(self.n)
+        st = lib().fem_ref_vw_jvp(C.byref(self.s), C.c_void_p(x.ctypes.data),
+                                  C.c_void_p(y.ctypes.data), C.c_uint(APPLY_BC if bc else 0))
+        if st:
+            raise OracleError(st, "fem_ref_vw_jvp")
+        return y
+
+    def dense(self, bc=False):
+        """K column by column (n JVPs) — the plain definition for small n."""
+        return np.stack([self.jvp(np.eye(self.n)[j], bc=bc) for j in range(self.n)], axis=1)
+
+
 def color(row_ptr, col_idx):
     """Distance-2 greedy coloring of an arbitrary CSR pattern (fem_ref_color)."""
     rp = np.ascontiguousarray(row_ptr, dtype=np.int64)

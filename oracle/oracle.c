@@ -727,6 +727,97 @@ int fem_ref_body_load(const fem_ref_mesh *m, const double *b, double *f) {
   return OK;
 }
 
+/* ------------------------------------------------------------------ virtual work (f4)
+ * Non-variational path (§3.1; advection-diffusion P:772-802) on a P1
+ * mesh, scalar field c: W(c, v) = sum_e vol_e [ D grad c . grad v + (w_e . grad c) vbar_e ]
+ * + m sum_a V_a (c_a - cold_a) v_a (reading R8: one-point rule, vbar_e = mean of
+ * v over the element's nodes, w_e = mean nodal velocity, V_a = sum_{e ∋ a} vol_e/(d+1)).
+ * r = grad_v W at v = 0 by dual numbers seeded on one nodal v_a at a time; the JVP
+ * K x = d r(c + t x)/dt by hyper-dual numbers (eps1 on v_a, eps2 on c along x) — the
+ * definitions differentiated, never a hand-assembled operator.                          */
+static hd vw_elem(const fem_ref_vw *p, const fem_ref_mesh *gm, int64_t e, const hd *ce,
+                  const hd *ve, int *st) {
+  int d = p->dim, nen = d + 1, a, j;
+  double G[4][3], vol, w[3] = {0, 0, 0};
+  hd gc[3], gv[3], diff = hd_const(0.0), adv = hd_const(0.0), vbar = hd_const(0.0);
+  *st = elem_geometry(gm, e, G, &vol);
+  for (a = 0; a < nen; ++a)
+    for (j = 0; j < d; ++j) w[j] += p->velocity[(int64_t)p->conn[e * nen + a] * d + j] / nen;
+  for (j = 0; j < d; ++j) {
+    gc[j] = hd_const(0.0);
+    gv[j] = hd_const(0.0);
+    for (a = 0; a < nen; ++a) {
+      gc[j] = hd_add(gc[j], hd_scale(ce[a], G[a][j]));
+      gv[j] = hd_add(gv[j], hd_scale(ve[a], G[a][j]));
+    }
+    diff = hd_add(diff, hd_mul(gc[j], gv[j]));
+    adv = hd_add(adv, hd_scale(gc[j], w[j]));
+  }
+  for (a = 0; a < nen; ++a) vbar = hd_add(vbar, hd_scale(ve[a], 1.0 / nen));
+  return hd_scale(hd_add(hd_scale(diff, p->diffusivity), hd_mul(adv, vbar)), vol);
+}
+
+static void vw_mesh(const fem_ref_vw *p, fem_ref_mesh *gm) {
+  memset(gm, 0, sizeof(*gm));
+  gm->dim = p->dim;
+  gm->n_nodes = p->n_nodes;
+  gm->n_elems = p->n_elems;
+  gm->coords = p->coords;
+  gm->conn = p->conn;
+}
+
+/* mode 0: residual of c (c_old may be NULL), mode 1: K x */
+static int vw_eval(const fem_ref_vw *p, const double *c, const double *cold, double *out,
+                   unsigned flags, int mode) {
+  int d = p->dim, nen = d + 1, a, b, st;
+  int64_t e, i;
+  fem_ref_mesh gm;
+  unsigned char *dir = (unsigned char *)calloc((size_t)p->n_nodes, 1);
+  double *V = (double *)calloc((size_t)p->n_nodes, sizeof(double));
+  if (!dir || !V) { free(dir); free(V); return E_ARG; }
+  for (i = 0; i < p->n_dirichlet; ++i) dir[p->dirichlet_nodes[i]] = 1;
+  const int mask = (flags & FEM_REF_APPLY_BC) && p->n_dirichlet > 0;
+  vw_mesh(p, &gm);
+  for (i = 0; i < p->n_nodes; ++i) out[i] = 0.0;
+  for (e = 0; e < p->n_elems; ++e) {
+    hd ce[4], ve[4];
+    double G[4][3], vol;
+    st = elem_geometry(&gm, e, G, &vol);
+    if (st) { free(dir); free(V); return st; }
+    for (a = 0; a < nen; ++a) V[p->conn[e * nen + a]] += vol / nen;
+    for (a = 0; a < nen; ++a) {           /* seed v_a */
+      for (b = 0; b < nen; ++b) {
+        const int64_t n = p->conn[e * nen + b];
+        double q = c[n];
+        if (mode == 1 && mask && dir[n]) q = 0.0;      /* P_f x */
+        ce[b] = mode == 0 ? hd_const(q) : (hd){0.0, 0.0, q, 0.0};
+        ve[b] = hd_const(0.0);
+        if (b == a) ve[b].b = 1.0;
+      }
+      hd W = vw_elem(p, &gm, e, ce, ve, &st);
+      out[p->conn[e * nen + a]] += mode == 0 ? W.b : W.d;
+    }
+  }
+  for (i = 0; i < p->n_nodes; ++i) {
+    double q = c[i];
+    if (mode == 1 && mask && dir[i]) q = 0.0;
+    out[i] += p->mass_coef * V[i] * (q - (mode == 0 && cold ? cold[i] : 0.0));
+    if (mask && dir[i]) out[i] = (mode == 0) ? 0.0 : c[i];   /* r[D] = 0; P_D x */
+  }
+  free(dir);
+  free(V);
+  return OK;
+}
+
+int fem_ref_vw_residual(const fem_ref_vw *p, const double *c, const double *cold, double *r,
+                        unsigned flags) {
+  return vw_eval(p, c, cold, r, flags, 0);
+}
+
+int fem_ref_vw_jvp(const fem_ref_vw *p, const double *x, double *y, unsigned flags) {
+  return vw_eval(p, x, NULL, y, flags, 1);
+}
+
 static int64_t find_col(const int32_t *col_idx, int64_t lo, int64_t hi, int64_t col) {
   while (lo < hi) {
     int64_t mid = lo + (hi - lo) / 2;

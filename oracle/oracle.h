@@ -74,6 +74,22 @@ int fem_ref_mean_stress(const fem_ref_mesh *m, const double *z, double *sigma, d
 int fem_ref_traction_load(int dim, int64_t n_nodes, const double *coords, int64_t nf,
                           const int32_t *facets, const double *t, double *f);
 int fem_ref_body_load(const fem_ref_mesh *m, const double *b, double *f);
+/* virtual-work path (f4): scalar advection-diffusion on a P1 mesh */
+typedef struct {
+  int dim;
+  int64_t n_nodes, n_elems;
+  const double *coords;
+  const int32_t *conn;
+  double diffusivity;
+  const double *velocity;   /* [n_nodes][dim] */
+  double mass_coef;         /* 1/dt, lumped mass; 0 = steady */
+  int64_t n_dirichlet;
+  const int32_t *dirichlet_nodes;
+  const double *dirichlet_vals;
+} fem_ref_vw;
+int fem_ref_vw_residual(const fem_ref_vw *p, const double *c, const double *cold, double *r,
+                        unsigned flags);
+int fem_ref_vw_jvp(const fem_ref_vw *p, const double *x, double *y, unsigned flags);
 int fem_ref_newton(const fem_ref_mesh *m, double *z /* in: lift, out: solution */, double atol,
                    double rtol, int max_iter, double cg_rtol, int cg_max_iter, int *iters,
                    int *cg_iters_total, double *res0, double *res);

@@ -39,7 +39,8 @@ EXPORTS = ("fem_create", "fem_destroy", "fem_query", "fem_check", "fem_apply_dir
            "fem_energy", "fem_residual", "fem_hvp", "fem_sparsity", "fem_color",
            "fem_assemble_csr", "fem_spmv", "fem_cg_solve", "fem_minres_solve",
            "fem_mean_stress", "fem_add_traction", "fem_add_body_force", "fem_get_fext",
-           "fem_newton_solve",
+           "fem_newton_solve", "fem_vw_create", "fem_vw_destroy", "fem_vw_apply_dirichlet",
+           "fem_vw_residual", "fem_vw_jvp", "fem_vw_gmres_solve",
            "fem_nccl_unique_id", "fem_nccl_comm_init", "fem_nccl_comm_destroy",
            "fem_allreduce_sum", "fem_halo_size", "fem_halo_pack", "fem_halo_combine",
            "fem_last_error", "fem_version")
@@ -75,6 +76,18 @@ class CgOpts(C.Structure):
 class CgReport(C.Structure):
     _fields_ = [("iters", C.c_int), ("converged", C.c_int), ("res0", C.c_double),
                 ("res", C.c_double)]
+
+
+class VwDesc(C.Structure):
+    _fields_ = [("dim", C.c_int), ("n_nodes", C.c_int64), ("n_elems", C.c_int64),
+                ("coords", C.c_void_p), ("conn", C.c_void_p), ("diffusivity", C.c_double),
+                ("velocity", C.c_void_p), ("mass_coef", C.c_double), ("n_dirichlet", C.c_int64),
+                ("dirichlet_nodes", C.c_void_p), ("dirichlet_vals", C.c_void_p)]
+
+
+class GmresOpts(C.Structure):
+    _fields_ = [("restart", C.c_int), ("max_iter", C.c_int), ("rtol", C.c_double),
+                ("atol", C.c_double)]
 
 
 class NewtonOpts(C.Structure):
@@ -118,6 +131,12 @@ def load_library():
         lib.fem_add_traction.argtypes = [vp, C.c_int64, vp, vp, vp]
         lib.fem_add_body_force.argtypes = [vp, C.POINTER(C.c_double), vp]
         lib.fem_get_fext.argtypes = [vp, vp, vp]
+        lib.fem_vw_create.argtypes = [C.POINTER(vp), C.POINTER(VwDesc), vp]
+        lib.fem_vw_destroy.argtypes = [vp]
+        lib.fem_vw_apply_dirichlet.argtypes = [vp, vp, vp]
+        lib.fem_vw_residual.argtypes = [vp, vp, vp, vp, C.c_uint, vp]
+        lib.fem_vw_jvp.argtypes = [vp, vp, vp, C.c_uint, vp]
+        lib.fem_vw_gmres_solve.argtypes = [vp, vp, vp, C.POINTER(GmresOpts), C.POINTER(CgReport), vp]
         lib.fem_newton_solve.argtypes = [vp, vp, C.POINTER(NewtonOpts), C.POINTER(NewtonReport), vp]
         lib.fem_nccl_unique_id.argtypes = [C.c_char_p]
         lib.fem_nccl_comm_init.argtypes = [C.c_char_p, C.c_int, C.c_int, C.POINTER(vp)]
@@ -405,3 +424,73 @@ def nccl_comm_init(uid: bytes, rank: int, size: int):
 
 def nccl_comm_destroy(comm) -> None:
     load_library().fem_nccl_comm_destroy(comm)
+
+
+class VirtualWorkProblem:
+    """Non-variational path (fem_vw_*): scalar advection-diffusion virtual
+    work W(c, v) on a P1 mesh; residual r = grad_v W at v = 0, the non-symmetric JVP and
+    GMRES.  Argument marshalling only."""
+
+    def __init__(self, coords, conn, diffusivity, velocity, mass_coef=0.0, dirichlet_nodes=None,
+                 dirichlet_vals=None, device="cuda"):
+        lib = load_library()
+        if not torch.cuda.is_available():
+            raise RuntimeError("VirtualWorkProblem needs a CUDA device (no CPU fallback)")
+        self.device = torch.device(device)
+        coords = np.ascontiguousarray(coords, np.float64)
+        conn = np.ascontiguousarray(conn, np.int32)
+        vel = np.ascontiguousarray(velocity, np.float64)
+        dn = np.ascontiguousarray(np.zeros(0) if dirichlet_nodes is None else dirichlet_nodes, np.int32)
+        dv = np.ascontiguousarray(np.zeros(0) if dirichlet_vals is None else dirichlet_vals, np.float64)
+        self.n = coords.shape[0]
+        self._keep = (coords, conn, vel, dn, dv)
+        d = VwDesc(coords.shape[1], self.n, conn.shape[0], coords.ctypes.data, conn.ctypes.data,
+                   diffusivity, vel.ctypes.data, mass_coef, len(dn),
+                   dn.ctypes.data if len(dn) else None, dv.ctypes.data if len(dv) else None)
+        h = C.c_void_p()
+        _check(lib.fem_vw_create(C.byref(h), C.byref(d), _stream()), "fem_vw_create")
+        self._h = h
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            load_library().fem_vw_destroy(self._h)
+            self._h = None
+
+    def _vec(self, x):
+        t = torch.as_tensor(x, dtype=torch.float64, device=self.device)
+        if t.numel() != self.n:
+            raise ValueError(f"expected {self.n} entries, got {t.numel()}")
+        return t.contiguous()
+
+    def apply_dirichlet(self, c):
+        _check(load_library().fem_vw_apply_dirichlet(self._h, _ptr(c), _stream()), "fem_vw_apply_dirichlet")
+        return c
+
+    def residual(self, c, c_old=None, bc=False):
+        c = self._vec(c)
+        co = None if c_old is None else self._vec(c_old)
+        r = torch.empty(self.n, dtype=torch.float64, device=self.device)
+        _check(load_library().fem_vw_residual(self._h, _ptr(c), _ptr(co), _ptr(r),
+                                              APPLY_BC if bc else 0, _stream()), "fem_vw_residual")
+        return r
+
+    def jvp(self, x, bc=False):
+        x = self._vec(x)
+        y = torch.empty(self.n, dtype=torch.float64, device=self.device)
+        _check(load_library().fem_vw_jvp(self._h, _ptr(x), _ptr(y), APPLY_BC if bc else 0,
+                                         _stream()), "fem_vw_jvp")
+        return y
+
+    def gmres_solve(self, b, x0=None, restart=30, max_iter=10000, rtol=1e-10, atol=0.0,
+                    raise_on_fail=True):
+        b = self._vec(b)
+        x = torch.zeros_like(b) if x0 is None else self._vec(x0).clone()
+        o = GmresOpts(restart, max_iter, rtol, atol)
+        rep = CgReport()
+        st = load_library().fem_vw_gmres_solve(self._h, _ptr(b), _ptr(x), C.byref(o), C.byref(rep),
+                                               _stream())
+        info = {"status": st, "iters": rep.iters, "converged": bool(rep.converged),
+                "res0": rep.res0, "res": rep.res}
+        if raise_on_fail:
+            _check(st, "fem_vw_gmres_solve")
+        return x, info

@@ -34,6 +34,9 @@
 #ifndef FEM_RT_DIAG_SMEM
 #define FEM_RT_DIAG_SMEM 1
 #endif
+#ifndef FEM_RT_RSODD
+#define FEM_RT_RSODD 1
+#endif
 #ifndef FEM_RT_GPAD
 #define FEM_RT_GPAD 0
 #endif
@@ -53,7 +56,7 @@ struct RtGeom {
   static constexpr int NEN = D + 1, BS = D * D, NPAIR = D == 3 ? 6 : 3;
   static constexpr int GP = FEM_RT_GPAD ? ((D + 1) & ~1) : D;     // g_a stride (padded: 16 B)
   static constexpr int G0 = 0, M0 = NEN * GP, S0 = M0 + NPAIR + (NPAIR & 1);  // g | M | sc1 sc2
-  static constexpr int RS = S0 + 2;
+  static constexpr int RS = FEM_RT_RSODD ? ((S0 + 2) | 1) : (S0 + 2);  // odd: spreads records over banks
   static constexpr int BP = (BS + 1) & ~1;                        // scratch block pitch
 };
 
@@ -477,7 +480,7 @@ __global__ void __launch_bounds__(kRtThreads, 2) k_rows_tile(RtArgs A) {
         const double *r = rec + (en & 1023u) * RS;
         const int a = (en >> 10) & 3u, b = (en >> 12) & 3u;
         double ga[Gm::GP + 1], gb[Gm::GP + 1];
-        if constexpr (Gm::GP % 2 == 0) {
+        if constexpr (Gm::GP % 2 == 0 && Gm::RS % 2 == 0) {
 #pragma unroll
           for (int i = 0; i < Gm::GP; i += 2) {
             const double2 x = *reinterpret_cast<const double2 *>(r + Gm::G0 + a * Gm::GP + i);
@@ -493,8 +496,7 @@ __global__ void __launch_bounds__(kRtThreads, 2) k_rows_tile(RtArgs A) {
           }
         }
         const double Mab = r[Gm::M0 + rt_pair<D>(a, b)];
-        const double2 scs = *reinterpret_cast<const double2 *>(r + Gm::S0);
-        const double sc1 = scs.x, sc2 = scs.y;
+        const double sc1 = r[Gm::S0], sc2 = r[Gm::S0 + 1];
 #pragma unroll
         for (int i = 0; i < D; ++i) {
           const double qi = sc2 * ga[i];

@@ -34,6 +34,9 @@
 #ifndef FEM_RT_DIAG_SMEM
 #define FEM_RT_DIAG_SMEM 1
 #endif
+#ifndef FEM_RT_MINB
+#define FEM_RT_MINB 2
+#endif
 #ifndef FEM_RT_RSODD
 #define FEM_RT_RSODD 1
 #endif
@@ -351,7 +354,7 @@ struct RtArgs {
 };
 
 template <int D, int MAT>
-__global__ void __launch_bounds__(kRtThreads, 2) k_rows_tile(RtArgs A) {
+__global__ void __launch_bounds__(kRtThreads, FEM_RT_MINB) k_rows_tile(RtArgs A) {
   using Gm = RtGeom<D>;
   constexpr int NEN = Gm::NEN, BS = Gm::BS, RS = Gm::RS;
   constexpr unsigned FULL = 0xffffffffu;

@@ -110,3 +110,14 @@ def test_homogenized_stiffness(fem, oracle_mod):
     C0, _ = homogenized_stiffness(lambda e: fi.periodic_mpc(hom, e), 2)
     ref0 = c_iso(hom.lam, hom.mu)
     assert np.abs(C0 - ref0).max() <= 1e-10 * np.abs(ref0).max()
+
+
+def test_minres_zero_rhs_and_iteration_cap(fem):
+    m = rve(6)
+    prob = fem.Problem(m)
+    z0 = dev(fi.lift(m))
+    x, info = prob.minres_solve(torch.zeros(m.n_total, dtype=torch.float64, device="cuda"), z=z0)
+    assert info["converged"] and info["iters"] == 0 and float(x.abs().max()) == 0.0
+    b = dev(fi.random_direction(m.n_total, 3))
+    _, info = prob.minres_solve(b, z=z0, rtol=1e-30, max_iter=5, raise_on_fail=False)
+    assert info["status"] == 6 and info["iters"] == 5        # FEM_ERR_NOT_CONVERGED

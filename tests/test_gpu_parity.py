@@ -304,3 +304,21 @@ def test_full_size_newton_cfg2_closed_form(fem, oracle_mod):
     ref = fi.affine_field(mesh, np.diag([0.1, s - 1.0]))
     assert rel(z, ref) <= 1e-10
     assert abs(s - s_ref) < 1e-10
+
+
+@pytest.mark.parametrize("variant", ["pull", "fused"])
+def test_row_assembly_fallback_kernels(fem, oracle_mod, variant, monkeypatch):
+    """The row-form fallbacks the node tiles hand over to (meshes the tile plan does not
+    cover): the direct-load row pull over HBM context records (FEM_ROWS_PULL) and the
+    per-lane-context warp pull (FEM_ROWS_PULL + FEM_ROWS_LEGACY); plans are built per
+    problem, so the variables are read when the problem first assembles."""
+    monkeypatch.setenv("FEM_ROWS_PULL", "1")
+    if variant == "fused":
+        monkeypatch.setenv("FEM_ROWS_LEGACY", "1")
+    for name in ("3d-nh", "3d-nh-shuffled", "2d-nh-roller", "2d-nh-phases-fext"):
+        mesh = MESHES[name]
+        z = fi.lift(mesh, fi.generic_state(mesh, 1))
+        prob = fem.Problem(mesh)
+        for bc in (False, True):
+            vals = prob.assemble_csr(dev(z), bc=bc, mode="rows")
+            assert rel(vals, oracle_mod.Oracle(mesh).assemble_alg2(z, bc=bc)) <= TOL

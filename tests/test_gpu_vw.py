@@ -92,3 +92,12 @@ def test_vw_errors(fem):
     bad[0, 0] = base.n_nodes + 5
     with pytest.raises(fem.FemError):
         fem.VirtualWorkProblem(base.coords, bad, **kw)
+
+
+def test_gmres_zero_rhs_and_restart_bounds(fem):
+    base, vel, kw = problem(2, 4, 8)
+    g = fem.VirtualWorkProblem(base.coords, base.conn, **kw)
+    x, info = g.gmres_solve(torch.zeros(base.n_nodes, dtype=torch.float64, device="cuda"))
+    assert info["converged"] and info["iters"] == 0
+    with pytest.raises(fem.FemError):
+        g.gmres_solve(torch.ones(base.n_nodes, dtype=torch.float64, device="cuda"), restart=0)

@@ -668,6 +668,7 @@ fem_status fem_destroy(fem_problem *h) {
   for (void *b : bufs)
     if (b) cudaFree(b);
   if (p->h_scal) cudaFreeHost(p->h_scal);
+  if (p->cap_stream) cudaStreamDestroy(p->cap_stream);
   free_tiles(p->tiles);
   dist_free(p);
   delete h;

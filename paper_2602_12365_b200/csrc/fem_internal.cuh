@@ -115,6 +115,7 @@ struct Problem {
   int32_t *colors = nullptr;    // [N]
   // workspaces
   Workspace jcomp, cgbuf, tmp, slotbuf, ctxbuf;
+  cudaStream_t cap_stream = nullptr;  // CUDA-graph capture of solver iterations
   TileSet tiles;
   // multi-GPU (fem_dist.cu)
   void *nccl = nullptr;

@@ -6,7 +6,9 @@
 // Operator: the masked HVP at z (matrix-free Newton-Krylov) or the CSR SpMV.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
+#include <cstdlib>
 
 #include "fem_internal.cuh"
 
@@ -167,25 +169,58 @@ fem_status run_cg(Problem *p, const double *z, const double *vals, const double 
   rep->converged = 0;
   int it = 0;
   fem_status result = FEM_OK;
-  while (true) {
-    if (rn <= tol) { rep->converged = 1; break; }
-    if (it >= o->max_iter) { result = FEM_ERR_NOT_CONVERGED; break; }
-    const int cur = it & 1;  // rz / rr of the current residual live in slot cur
-    st = apply_op(p, o->op, z, vals, pp, Ap, s);
-    if (st) return st;
-    st = launch_dot(p, pp, Ap, n, p->scal + S_PAP, s);
-    if (st) return st;
+  // one CG iteration on slot parity cur (rz / rr of the current residual live in slot cur)
+  auto body = [&](int cur, cudaStream_t s) -> fem_status {
+    fem_status sb = apply_op(p, o->op, z, vals, pp, Ap, s);
+    if (sb) return sb;
+    sb = launch_dot(p, pp, Ap, n, p->scal + S_PAP, s);
+    if (sb) return sb;
     k_cg_update<<<nb, kThreads, 0, s>>>(p->scal, S_RZ0 + cur, x, r, zv, pp, Ap, dinv, n, part_a,
                                         part_b, own, p->dim);
     k_final_sum2<<<1, kThreads, 0, s>>>(part_a, part_b, nb, p->scal + S_RR0 + (cur ^ 1),
                                         p->scal + S_RZ0 + (cur ^ 1));
-    st = allreduce(p, p->scal + S_RR0 + (cur ^ 1), 1, s);
-    if (st) return st;
-    st = allreduce(p, p->scal + S_RZ0 + (cur ^ 1), 1, s);
-    if (st) return st;
+    sb = allreduce(p, p->scal + S_RR0 + (cur ^ 1), 1, s);
+    if (sb) return sb;
+    sb = allreduce(p, p->scal + S_RZ0 + (cur ^ 1), 1, s);
+    if (sb) return sb;
     k_cg_dir<<<grid_for(n), kThreads, 0, s>>>(p->scal, S_RZ0 + cur, S_RZ0 + (cur ^ 1), zv, pp, n);
     FEM_LAUNCH_CHECK("cg iteration");
-    ++it;
+    return FEM_OK;
+  };
+  // Between host checks the iterations run as a CUDA graph of two iterations (the slot
+  // parity pattern repeats every 2), captured once per solve on a single GPU: ~10 kernel
+  // launches per iteration become one graph launch per pair (small problems are
+  // launch-bound).  Multi-GPU solves (NCCL inside the body) launch kernels directly.
+  const bool graphs = p->size == 1 && every >= 2 && !getenv("FEM_NO_GRAPHS");
+  cudaGraphExec_t exec = nullptr;
+  cudaGraph_t graph = nullptr;
+  while (true) {
+    if (rn <= tol) { rep->converged = 1; break; }
+    if (it >= o->max_iter) { result = FEM_ERR_NOT_CONVERGED; break; }
+    const int todo = std::min(every - it % every, o->max_iter - it);  // until the next check
+    if (graphs && (it & 1) == 0 && todo >= 2) {
+      if (!exec) {  // captured on a private stream (the legacy default stream cannot capture)
+        if (!p->cap_stream) FEM_CUDA(cudaStreamCreateWithFlags(&p->cap_stream, cudaStreamNonBlocking));
+        FEM_CUDA(cudaStreamBeginCapture(p->cap_stream, cudaStreamCaptureModeRelaxed));
+        fem_status sc = body(0, p->cap_stream);
+        if (!sc) sc = body(1, p->cap_stream);
+        cudaError_t ce = cudaStreamEndCapture(p->cap_stream, &graph);
+        if (sc) return sc;
+        FEM_CUDA(ce);
+        FEM_CUDA(cudaGraphInstantiate(&exec, graph, 0));
+      }
+      for (int k = 0; k < todo / 2; ++k) FEM_CUDA(cudaGraphLaunch(exec, s));
+      it += 2 * (todo / 2);
+      if (todo & 1) {
+        st = body(it & 1, s);
+        if (st) return st;
+        ++it;
+      }
+    } else {
+      st = body(it & 1, s);
+      if (st) return st;
+      ++it;
+    }
     if (it % every == 0 || it >= o->max_iter) {
       st = read_scalars(p, 8, s);
       if (st) return st;
@@ -194,6 +229,8 @@ fem_status run_cg(Problem *p, const double *z, const double *vals, const double 
       if (!std::isfinite(rn)) { result = FEM_ERR_NONFINITE; break; }
     }
   }
+  if (exec) cudaGraphExecDestroy(exec);
+  if (graph) cudaGraphDestroy(graph);
   rep->iters = it;
   rep->res = rn;
   st = read_error_word(p, s);

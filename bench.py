@@ -187,7 +187,10 @@ def algorithmic(mesh, nnz, C, mode):
         "residual": {"bytes": conn + coords + vec + 2 * vec, "flops": fr * E},  # r zero + write
         "hvp": {"bytes": conn + coords + 2 * vec + 2 * vec, "flops": fh * E},   # u, v; y zero + write
         "assemble": {"bytes": asm_bytes, "flops": (f_ctx + f_blocks) * E},
-        "spmv": {"bytes": nnz * 12 + 8 * (N + 1) + 2 * vec, "flops": 2 * nnz},
+        # node-block SpMV (no multipliers): vals + one neighbour id per D x D block; plain
+        # CSR otherwise (vals + col_idx + row_ptr)
+        "spmv": {"bytes": (nnz * 8 + 4 * nnz // (d * d) + 8 * (mesh.n_nodes + 1) if not mesh.n_mpc
+                           else nnz * 12 + 8 * (N + 1)) + 2 * vec, "flops": 2 * nnz},
     }
 
 

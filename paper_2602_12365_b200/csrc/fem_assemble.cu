@@ -801,12 +801,91 @@ __global__ void __launch_bounds__(256) k_spmv(const int64_t *row_ptr, const int3
   }
 }
 
+// Node-block SpMV for patterns of full D x D node blocks (no multiplier columns): the D rows
+// of node n share one column list (the D * sn columns of its sn neighbour nodes, sorted), so
+// the kernel reads the neighbour list nadj (4 B per block) instead of col_idx (4 B per
+// entry), and each neighbour's D x-values once for the D rows.  LPN lanes per node, lane s =
+// neighbour slot s; per row the lanes' partial sums are reduced by a butterfly.
+template <int D, int LPN>
+__global__ void __launch_bounds__(256) k_spmv_nodes(const int64_t *row_ptr, const int64_t *nadj_ptr,
+                                                    const int32_t *nadj, const double *vals,
+                                                    const double *x, double *y, int64_t n_nodes) {
+  const int lane = threadIdx.x % LPN;
+  const int64_t groups = (int64_t)gridDim.x * (blockDim.x / LPN);
+  for (int64_t n = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / LPN; n < n_nodes; n += groups) {
+    const int64_t a0 = __ldg(nadj_ptr + n);
+    const int sn = (int)(__ldg(nadj_ptr + n + 1) - a0);
+    const int64_t rp0 = __ldg(row_ptr + n * D);
+    double acc[D];
+#pragma unroll
+    for (int i = 0; i < D; ++i) acc[i] = 0.0;
+    for (int sl = lane; sl < sn; sl += LPN) {
+      const int64_t m = __ldg(nadj + a0 + sl);
+      double xm[D];
+#pragma unroll
+      for (int k = 0; k < D; ++k) xm[k] = __ldg(x + m * D + k);
+#pragma unroll
+      for (int i = 0; i < D; ++i) {
+        const double *v = vals + rp0 + (int64_t)i * D * sn + sl * D;
+#pragma unroll
+        for (int k = 0; k < D; ++k) acc[i] = fma(__ldg(v + k), xm[k], acc[i]);
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < D; ++i)
+#pragma unroll
+      for (int o = LPN / 2; o > 0; o >>= 1) acc[i] += __shfl_xor_sync(0xffffffffu, acc[i], o, LPN);
+    if (lane < D) {
+      double v = acc[0];
+#pragma unroll
+      for (int i = 1; i < D; ++i)
+        if (lane == i) v = acc[i];
+      y[n * D + lane] = v;
+    }
+  }
+}
+
+__global__ void k_max_adj(const int64_t *nadj_ptr, int64_t n, int *mx) {
+  int m = 0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    m = max(m, (int)(nadj_ptr[i + 1] - nadj_ptr[i]));
+  atomicMax(mx, m);
+}
+
 fem_status run_spmv(Problem *p, const double *vals, const double *x, double *y, cudaStream_t s) {
-  const int64_t avg = p->N ? p->nnz / p->N : 0;
-  const int64_t threads_needed = p->N * (avg > 24 ? 8 : 4);
-  const int grid = grid_for(threads_needed, 256, 148 * 32);
-  if (avg > 24) k_spmv<8><<<grid, 256, 0, s>>>(p->row_ptr, p->col_idx, vals, x, y, p->N);
-  else k_spmv<4><<<grid, 256, 0, s>>>(p->row_ptr, p->col_idx, vals, x, y, p->N);
+  if (p->spmv_lpn == 0) {  // node-block form available? (pattern of full node blocks)
+    p->spmv_lpn = -1;
+    if (p->n_mpc == 0 && p->n_nodes > 0 && !getenv("FEM_SPMV_CSR")) {
+      int *d = nullptr, h = 0;
+      FEM_CUDA(cudaMalloc(&d, sizeof(int)));
+      FEM_CUDA(cudaMemsetAsync(d, 0, sizeof(int), s));
+      k_max_adj<<<grid_for(p->n_nodes), kThreads, 0, s>>>(p->nadj_ptr, p->n_nodes, d);
+      FEM_CUDA(cudaMemcpyAsync(&h, d, sizeof(int), cudaMemcpyDeviceToHost, s));
+      FEM_CUDA(cudaStreamSynchronize(s));
+      cudaFree(d);
+      p->spmv_lpn = h <= 8 ? 8 : (h <= 16 ? 16 : 32);
+    }
+  }
+  if (p->spmv_lpn > 0) {
+    const int lpn = p->spmv_lpn;
+    const int grid = grid_for(p->n_nodes * lpn, 256, 148 * 32);
+    if (p->dim == 3) {
+      if (lpn == 8) k_spmv_nodes<3, 8><<<grid, 256, 0, s>>>(p->row_ptr, p->nadj_ptr, p->nadj, vals, x, y, p->n_nodes);
+      else if (lpn == 16) k_spmv_nodes<3, 16><<<grid, 256, 0, s>>>(p->row_ptr, p->nadj_ptr, p->nadj, vals, x, y, p->n_nodes);
+      else k_spmv_nodes<3, 32><<<grid, 256, 0, s>>>(p->row_ptr, p->nadj_ptr, p->nadj, vals, x, y, p->n_nodes);
+    } else {
+      if (lpn == 8) k_spmv_nodes<2, 8><<<grid, 256, 0, s>>>(p->row_ptr, p->nadj_ptr, p->nadj, vals, x, y, p->n_nodes);
+      else if (lpn == 16) k_spmv_nodes<2, 16><<<grid, 256, 0, s>>>(p->row_ptr, p->nadj_ptr, p->nadj, vals, x, y, p->n_nodes);
+      else k_spmv_nodes<2, 32><<<grid, 256, 0, s>>>(p->row_ptr, p->nadj_ptr, p->nadj, vals, x, y, p->n_nodes);
+    }
+  } else {
+    const int64_t avg = p->N ? p->nnz / p->N : 0;
+    const int64_t threads_needed = p->N * (avg > 24 ? 8 : 4);
+    const int grid = grid_for(threads_needed, 256, 148 * 32);
+    if (avg > 24) k_spmv<8><<<grid, 256, 0, s>>>(p->row_ptr, p->col_idx, vals, x, y, p->N);
+    else k_spmv<4><<<grid, 256, 0, s>>>(p->row_ptr, p->col_idx, vals, x, y, p->N);
+  }
   FEM_LAUNCH_CHECK("spmv");
   if (p->size > 1) return halo_add(p, y, s);
   return FEM_OK;

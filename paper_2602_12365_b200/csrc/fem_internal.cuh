@@ -116,6 +116,7 @@ struct Problem {
   // workspaces
   Workspace jcomp, cgbuf, tmp, slotbuf, ctxbuf;
   cudaStream_t cap_stream = nullptr;  // CUDA-graph capture of solver iterations
+  int spmv_lpn = 0;             // node-block SpMV lanes per node (0 unset, -1 plain CSR)
   TileSet tiles;
   // multi-GPU (fem_dist.cu)
   void *nccl = nullptr;

@@ -34,6 +34,9 @@
 #ifndef FEM_RT_DIAG_SMEM
 #define FEM_RT_DIAG_SMEM 1
 #endif
+#ifndef FEM_RT_UNROLL
+#define FEM_RT_UNROLL 4
+#endif
 #ifndef FEM_RT_MINB
 #define FEM_RT_MINB 2
 #endif
@@ -50,6 +53,7 @@
 namespace fem {
 
 constexpr int kRtNT = FEM_RT_NT;         // nodes per tile
+constexpr int kRtUnroll = FEM_RT_UNROLL; // entries per unrolled step of the slot sums
 constexpr int kRtThreads = 256;          // 8 warps, 2 nodes per warp per pass
 constexpr int kRtLPN = 16;               // lanes per node
 constexpr int kRtSortMax = 4096;         // plan: keys sorted per tile in shared memory
@@ -478,6 +482,7 @@ __global__ void __launch_bounds__(kRtThreads, FEM_RT_MINB) k_rows_tile(RtArgs A)
       double acc[BS];
 #pragma unroll
       for (int q = 0; q < BS; ++q) acc[q] = 0.0;
+#pragma unroll kRtUnroll
       for (int c = lo; c < hi; ++c) {
         const uint32_t en = ent[c];
         const double *r = rec + (en & 1023u) * RS;

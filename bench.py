@@ -354,8 +354,11 @@ def main():
         torch.cuda.synchronize()
         return a.elapsed_time(b) / reps
 
+    prob.linearize(zt)
     ab = {
         "hvp_tiles_ms": time_call(lambda: prob.hvp(zt, vt, bc=True, out=y)),
+        "hvp_linearized_ms": time_call(lambda: prob.hvp(zt, vt, bc=True, out=y, flags=fem.LINEARIZED)),
+        "linearize_ms": time_call(lambda: prob.linearize(zt)),
         "hvp_baseline_scatter_ms": time_call(
             lambda: prob.hvp(zt, vt, bc=True, out=y, flags=fem.BASELINE_SCATTER)),
         "hvp_deterministic_ms": time_call(

@@ -82,8 +82,11 @@ enum {
   FEM_ASSEMBLE_JCOMP = 32u, /* fem_assemble_csr: all color passes in ONE element sweep
                                into J_comp [N][C] (atomics), then decompression.         */
   FEM_ASSEMBLE_ROWS = 64u,  /* fem_assemble_csr: row-pull form (no J_comp buffer).         */
-  FEM_ASSEMBLE_SCATTER = 128u /* fem_assemble_csr: element-Hessian scatter-add with fp64
+  FEM_ASSEMBLE_SCATTER = 128u,/* fem_assemble_csr: element-Hessian scatter-add with fp64
                                atomics (the paper's comparison path), not Alg. 2 */
+  FEM_LINEARIZED = 256u     /* fem_hvp / CG op 0: the tangent at the state of the last
+                               fem_linearize (its z; the z argument is not read for the
+                               state) — Newton-Krylov applies K(z) thousands of times */
 };
 
 typedef struct {
@@ -202,6 +205,7 @@ typedef struct {
   int max_iter;
   int jacobi;       /* 1: Jacobi preconditioner (op 1 only)                                */
   int check_every;  /* read the residual norm on the host every k iterations (>= 1)        */
+  unsigned hvp_flags; /* op 0: extra fem_hvp flags (FEM_LINEARIZED)                         */
 } fem_cg_opts;
 
 typedef struct {
@@ -214,6 +218,13 @@ typedef struct {
 fem_status fem_cg_solve(fem_problem *p, const double *z, const double *vals, const double *b,
                         double *x, const fem_cg_opts *opts, fem_cg_report *report,
                         fem_stream stream);
+
+/* Linearize the tangent at z (jax.linearize analogue): caches per element F^{-T} and ln J
+ * of the neo-Hookean state (80 B / element, element-tile order; nothing for linear
+ * elasticity) so FEM_LINEARIZED HVPs skip the state evaluation (measured at cfg 3: the
+ * cached HVP is slower, 1.27 vs 1.05 ms — 80 B/element of HBM reads cost more than the
+ * recomputed state — so fem_newton_solve only uses it with FEM_NEWTON_LINEARIZE set). */
+fem_status fem_linearize(fem_problem *p, const double *z, fem_stream stream);
 
 /* MINRES (Paige & Saunders) on the same BC-applied operator, for the symmetric indefinite
  * saddle-point system of the MPC Lagrangian [[K, B^T], [B, 0]] (CG does not

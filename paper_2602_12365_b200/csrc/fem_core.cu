@@ -387,7 +387,12 @@ fem_status run_hvp(Problem *p, const double *z, const double *v, double *y, unsi
             : launch_elem<OP_HVP, false>(p, a, grid_for(p->n_elems), s);
   } else {
     if (det && p->n_mpc) FEM_CUDA(cudaMemsetAsync(y + p->n_u, 0, sizeof(double) * p->n_mpc, s));
-    st = tile_pass(p, OP_HVP, z, v, y, bc, det, nullptr, s);
+    const bool lin = (flags & FEM_LINEARIZED) && p->material == FEM_NEO_HOOKEAN;
+    if (lin && !p->lin_valid) {
+      set_error("fem_hvp: FEM_LINEARIZED without a preceding fem_linearize");
+      return FEM_ERR_INVALID_ARG;
+    }
+    st = tile_pass(p, lin ? OP_HVP_LIN : OP_HVP, z, v, y, bc, det, nullptr, s);
   }
   if (st) return st;
   if (p->size > 1 && !(flags & FEM_LOCAL_ONLY)) {
@@ -401,6 +406,20 @@ fem_status run_hvp(Problem *p, const double *z, const double *v, double *y, unsi
   const uint8_t *own = (p->size > 1 && (flags & FEM_LOCAL_ONLY)) ? p->owned : nullptr;
   if (bc) k_bc_fix<<<grid_for(p->n_dir), kThreads, 0, s>>>(y, p->dir_dofs, p->n_dir, v, own, p->dim);
   FEM_LAUNCH_CHECK("hvp");
+  return FEM_OK;
+}
+
+fem_status run_linearize(Problem *p, const double *z, cudaStream_t s) {
+  if (p->material != FEM_NEO_HOOKEAN || p->n_elems == 0) {  // LE: the tangent is constant
+    p->lin_valid = true;
+    return FEM_OK;
+  }
+  fem_status st = build_tiles(p, s);
+  if (st) return st;
+  if (!p->lin) FEM_CUDA(cudaMalloc(&p->lin, sizeof(double) * 10 * (size_t)p->tiles.n_tiles * kTile));
+  st = tile_pass(p, OP_LIN, z, nullptr, nullptr, false, false, nullptr, s);
+  if (st) return st;
+  p->lin_valid = true;
   return FEM_OK;
 }
 
@@ -669,6 +688,7 @@ fem_status fem_destroy(fem_problem *h) {
     if (b) cudaFree(b);
   if (p->h_scal) cudaFreeHost(p->h_scal);
   if (p->cap_stream) cudaStreamDestroy(p->cap_stream);
+  if (p->lin) cudaFree(p->lin);
   free_tiles(p->tiles);
   dist_free(p);
   delete h;
@@ -846,6 +866,11 @@ fem_status fem_get_fext(fem_problem *h, double *f, fem_stream stream) {
   if (p->f_ext) FEM_CUDA(cudaMemcpyAsync(f, p->f_ext, sizeof(double) * p->n_u, cudaMemcpyDeviceToDevice, s));
   else FEM_CUDA(cudaMemsetAsync(f, 0, sizeof(double) * p->n_u, s));
   return FEM_OK;
+}
+
+fem_status fem_linearize(fem_problem *h, const double *z, fem_stream stream) {
+  FEM_ARG(h && z, "fem_linearize: null argument");
+  return run_linearize(&h->p, z, (cudaStream_t)stream);
 }
 
 }  // extern "C"

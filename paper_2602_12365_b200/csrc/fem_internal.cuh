@@ -25,7 +25,8 @@ constexpr int kThreads = 256;
 #endif
 constexpr int kTile = FEM_TILE;     // elements per tile (one CTA)
 
-enum { OP_ENERGY = 0, OP_RESIDUAL = 1, OP_HVP = 2 };
+enum { OP_ENERGY = 0, OP_RESIDUAL = 1, OP_HVP = 2, OP_HVP_LIN = 3, OP_LIN = 4 };
+// OP_LIN: cache the tangent state at z (fem_linearize); OP_HVP_LIN: HVP from that cache
 
 // Element tiles (fem_tiles.cu).  maxe = kTile * (dim+1) reserved entries per tile.
 struct TileSet {
@@ -117,6 +118,8 @@ struct Problem {
   Workspace jcomp, cgbuf, tmp, slotbuf, ctxbuf;
   cudaStream_t cap_stream = nullptr;  // CUDA-graph capture of solver iterations
   int spmv_lpn = 0;             // node-block SpMV lanes per node (0 unset, -1 plain CSR)
+  double *lin = nullptr;        // fem_linearize cache: [10][n_tiles*kTile] F^-T (9), ln J, SoA
+  bool lin_valid = false;
   TileSet tiles;
   // multi-GPU (fem_dist.cu)
   void *nccl = nullptr;
@@ -211,6 +214,7 @@ fem_status build_row_plan(Problem *p, cudaStream_t s);          // fem_rows.cu
 fem_status launch_rows_stage(Problem *p, const double *ctx, double *vals, bool bc,
                              cudaStream_t s);
 fem_status build_row_tiles(Problem *p, cudaStream_t s);                  // fem_rowtile.cu
+fem_status run_linearize(Problem *p, const double *z, cudaStream_t s);   // fem_core.cu
 fem_status launch_row_tiles(Problem *p, const double *z, double *vals, bool bc, cudaStream_t s);
 fem_status dist_setup(Problem *p, const fem_dist_desc *d, cudaStream_t s);
 void dist_free(Problem *p);

@@ -120,8 +120,8 @@ __global__ void k_add(double *a, const double *b, int64_t n) {
 }
 
 static fem_status apply_op(Problem *p, int op, const double *z, const double *vals, const double *x,
-                           double *y, cudaStream_t s) {
-  if (op == 0) return run_hvp(p, z, x, y, FEM_APPLY_BC, s);
+                           double *y, cudaStream_t s, unsigned extra = 0) {
+  if (op == 0) return run_hvp(p, z, x, y, FEM_APPLY_BC | (extra & FEM_LINEARIZED), s);
   return run_spmv(p, vals, x, y, s);
 }
 
@@ -144,7 +144,7 @@ fem_status run_cg(Problem *p, const double *z, const double *vals, const double 
   double *part_a = p->partials, *part_b = p->partials + kReduceBlocks;
   if (jac) k_jacobi_diag<<<grid_for(n), kThreads, 0, s>>>(vals, p->diag_pos, n, dinv, p->d_err);
   // r0 = b - A x0
-  st = apply_op(p, o->op, z, vals, x, Ap, s);
+  st = apply_op(p, o->op, z, vals, x, Ap, s, o->hvp_flags);
   if (st) return st;
   k_sub<<<grid_for(n), kThreads, 0, s>>>(b, Ap, r, n);
   const uint8_t *own = p->size > 1 ? p->owned : nullptr;
@@ -171,7 +171,7 @@ fem_status run_cg(Problem *p, const double *z, const double *vals, const double 
   fem_status result = FEM_OK;
   // one CG iteration on slot parity cur (rz / rr of the current residual live in slot cur)
   auto body = [&](int cur, cudaStream_t s) -> fem_status {
-    fem_status sb = apply_op(p, o->op, z, vals, pp, Ap, s);
+    fem_status sb = apply_op(p, o->op, z, vals, pp, Ap, s, o->hvp_flags);
     if (sb) return sb;
     sb = launch_dot(p, pp, Ap, n, p->scal + S_PAP, s);
     if (sb) return sb;
@@ -339,7 +339,7 @@ fem_status run_minres(Problem *p, const double *z, const double *vals, const dou
   const int g = grid_for(n);
   double *sc = p->scal;
   // r1 = b - A x; y = r1 (= R2 at the loop head); beta1 = ||r1||
-  st = apply_op(p, o->op, z, vals, x, T, s);
+  st = apply_op(p, o->op, z, vals, x, T, s, o->hvp_flags);
   if (st) return st;
   k_sub<<<g, kThreads, 0, s>>>(b, T, R2, n);
   FEM_CUDA(cudaMemcpyAsync(R1, R2, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
@@ -369,7 +369,7 @@ fem_status run_minres(Problem *p, const double *z, const double *vals, const dou
     if (it >= o->max_iter) { result = FEM_ERR_NOT_CONVERGED; break; }
     if (p->h_scal[M_BETA] == 0.0 && it > 0) { rep->converged = 1; break; }  // invariant space
     k_minres_scale<<<g, kThreads, 0, s>>>(sc, R2, V, n);
-    st = apply_op(p, o->op, z, vals, V, T, s);
+    st = apply_op(p, o->op, z, vals, V, T, s, o->hvp_flags);
     if (st) return st;
     k_minres_lanczos1<<<g, kThreads, 0, s>>>(sc, it == 0, T, R1, n);
     st = launch_dot(p, V, T, n, sc + M_ALFA, s);
@@ -398,7 +398,7 @@ fem_status run_minres(Problem *p, const double *z, const double *vals, const dou
   }
   rep->iters = it;
   // true residual ||b - A x|| for the report
-  st = apply_op(p, o->op, z, vals, x, T, s);
+  st = apply_op(p, o->op, z, vals, x, T, s, o->hvp_flags);
   if (st) return st;
   k_sub<<<g, kThreads, 0, s>>>(b, T, T, n);
   st = launch_dot(p, T, T, n, sc + M_BB2, s);
@@ -481,9 +481,17 @@ fem_status fem_newton_solve(fem_problem *h, double *z, const fem_newton_opts *o,
       if (st) { result = st; break; }
     }
     fem_cg_report cr{};
+    fem_cg_opts co = o->cg;
+    // opt-in: with the state cache the HVP trades ~100 FP64 ops per element for 80 B of HBM
+    // reads and measured slower at cfg 3 (1.27 vs 1.05 ms), so Newton recomputes by default
+    if (!csr && getenv("FEM_NEWTON_LINEARIZE")) {
+      st = run_linearize(p, z, s);
+      if (st) { result = st; break; }
+      co.hvp_flags |= FEM_LINEARIZED;
+    }
     // the Lagrangian Hessian of an MPC problem is indefinite: MINRES instead of CG (f2)
-    st = p->n_mpc ? run_minres(p, z, vals, r, dz, &o->cg, &cr, s)
-                  : run_cg(p, z, vals, r, dz, &o->cg, &cr, s);
+    st = p->n_mpc ? run_minres(p, z, vals, r, dz, &co, &cr, s)
+                  : run_cg(p, z, vals, r, dz, &co, &cr, s);
     rep->cg_iters += cr.iters;
     if (st) { result = st; break; }
     k_add<<<grid_for(n), kThreads, 0, s>>>(z, dz, n);

@@ -406,7 +406,8 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 __host__ __device__ constexpr int pipe_minb(int op, int mat) {
   return (256 / kTile) *
          (FEM_PIPE_MINB > 0 ? FEM_PIPE_MINB
-                            : (op == OP_ENERGY ? 4 : (op == OP_RESIDUAL ? 3 : (mat == FEM_NEO_HOOKEAN ? 2 : 3))));
+                            : (op == OP_ENERGY ? 4 : (op == OP_RESIDUAL || op == OP_LIN ? 3
+                                : (op == OP_HVP_LIN ? 3 : (mat == FEM_NEO_HOOKEAN ? 2 : 3)))));
 }
 
 struct PipeArgs {
@@ -419,15 +420,24 @@ struct PipeArgs {
   double lam, mu;
   const double *lam_tab, *mu_tab;
   double *out, *slots, *partials;
+  double *lin;        // linearization cache [10][lin_stride] (OP_LIN writes, OP_HVP_LIN reads)
+  int64_t lin_stride;
   int *err;
 };
+
+template <int OP>
+constexpr bool op_is_hvp() { return OP == OP_HVP || OP == OP_HVP_LIN; }
+template <int OP>
+constexpr bool op_has_p2() { return OP == OP_RESIDUAL || op_is_hvp<OP>(); }
+template <int OP, int MAT>
+constexpr bool op_needs_u() { return OP == OP_ENERGY || OP == OP_RESIDUAL || OP == OP_LIN || (OP == OP_HVP && MAT == FEM_NEO_HOOKEAN); }
 
 template <int D, int MAT, int OP, bool MASK>
 __device__ __forceinline__ void tile_phase1(const PipeArgs &A, const unsigned char *m,
                                             const double *xs, const double *us, const double *vs,
                                             int64_t t, int tid, double *cb, double &eacc) {
   constexpr int NEN = D + 1;
-  constexpr bool NEED_U = (OP != OP_HVP) || (MAT == FEM_NEO_HOOKEAN);
+  constexpr bool NEED_U = op_needs_u<OP, MAT>();
   const int64_t e = t * kTile + tid;
   if (e < A.E) {
     const ushort4 lc4 = reinterpret_cast<const ushort4 *>(m + A.off_lconn)[tid];
@@ -480,6 +490,16 @@ __device__ __forceinline__ void tile_phase1(const PipeArgs &A, const unsigned ch
         ok = nh_state<D>(H, s);
         if (ok) nh_stress<D>(s, ls, ms, S);
       }
+    } else if constexpr (OP == OP_LIN) {
+      if constexpr (MAT == FEM_NEO_HOOKEAN) {  // cache F^-T and ln J at this state (SoA)
+        NHState<D> s;
+        ok = nh_state<D>(H, s);
+#pragma unroll
+        for (int i = 0; i < D; ++i)
+#pragma unroll
+          for (int j = 0; j < D; ++j) A.lin[(int64_t)(i * D + j) * A.lin_stride + e] = ok ? s.FiT[i][j] : 0.0;
+        A.lin[(int64_t)(D * D) * A.lin_stride + e] = ok ? s.lnJ : 0.0;
+      }
     } else {
       // dH = dHh / det; vol dP(dH) G_a = dP(dHh) c_a * (1 / (det d!)): fold into (lambda, mu)
       double v[NEN][D], dH[D][D];
@@ -494,6 +514,14 @@ __device__ __forceinline__ void tile_phase1(const PipeArgs &A, const unsigned ch
       const double ls = lam * sc, ms = mu * sc;
       if constexpr (MAT == FEM_LINEAR_ELASTIC) {
         le_stress<D>(dH, ls, ms, S);
+      } else if constexpr (OP == OP_HVP_LIN) {  // F^-T, ln J from fem_linearize's cache
+        NHState<D> s;
+#pragma unroll
+        for (int i = 0; i < D; ++i)
+#pragma unroll
+          for (int j = 0; j < D; ++j) s.FiT[i][j] = __ldg(A.lin + (int64_t)(i * D + j) * A.lin_stride + e);
+        s.lnJ = __ldg(A.lin + (int64_t)(D * D) * A.lin_stride + e);
+        nh_dstress<D>(s, ls, ms, dH, S);
       } else {
         NHState<D> s;
         ok = nh_state<D>(H, s);
@@ -501,7 +529,7 @@ __device__ __forceinline__ void tile_phase1(const PipeArgs &A, const unsigned ch
       }
     }
     if (!ok) atomicOr(A.err, ERRW_INVERTED);
-    if constexpr (OP != OP_ENERGY) {
+    if constexpr (op_has_p2<OP>()) {
       double f[NEN][D];
       nodal_from_c<D>(S, c, f);
 #pragma unroll
@@ -582,12 +610,12 @@ __device__ __forceinline__ void mb_wait(uint64_t *m, unsigned parity) {
 }
 
 template <int OP>
-constexpr bool pipe_decoupled() { return OP == OP_HVP; }
+constexpr bool pipe_decoupled() { return op_is_hvp<OP>(); }
 
 template <int D, int MAT, int OP, bool MASK, bool DET>
 __global__ void __launch_bounds__(kTile, pipe_minb(OP, MAT)) k_tile_pipe(PipeArgs A) {
-  constexpr bool NEED_U = (OP != OP_HVP) || (MAT == FEM_NEO_HOOKEAN);
-  constexpr int NF = 1 + (NEED_U ? 1 : 0) + (OP == OP_HVP ? 1 : 0);
+  constexpr bool NEED_U = op_needs_u<OP, MAT>();
+  constexpr int NF = 1 + (NEED_U ? 1 : 0) + (op_is_hvp<OP>() ? 1 : 0);
   constexpr bool DEC = pipe_decoupled<OP>();
   extern __shared__ __align__(16) unsigned char sm[];
   __shared__ __align__(8) uint64_t mb_meta[3], mb_node[2];
@@ -613,7 +641,7 @@ __global__ void __launch_bounds__(kTile, pipe_minb(OP, MAT)) k_tile_pipe(PipeArg
       const int64_t g = (int64_t)nodes[i / D] * D + (i % D);
       cp_async8(dst + i, A.coords + g);
       if constexpr (NEED_U) cp_async8(dst + um * D + i, A.u + g);
-      if constexpr (OP == OP_HVP) cp_async8(dst + (NF - 1) * um * D + i, A.v + g);
+      if constexpr (op_is_hvp<OP>()) cp_async8(dst + (NF - 1) * um * D + i, A.v + g);
     }
     if constexpr (DEC) mb_cp_arrive(&mb_node[b]);
   };
@@ -647,7 +675,7 @@ __global__ void __launch_bounds__(kTile, pipe_minb(OP, MAT)) k_tile_pipe(PipeArg
       tile_phase1<D, MAT, OP, MASK>(A, m, nb, nb + um * D, nb + (NF - 1) * um * D, t, tid, cb, eacc);
       __syncthreads();  // phase 1 of tile k done; tile k-1 fully consumed
       if (t + 2 * G < A.n_tiles) issue_meta(t + 2 * G, (k + 2) % 3);
-      if constexpr (OP != OP_ENERGY)
+      if constexpr (op_has_p2<OP>())
         tile_phase2<D, OP, DET>(A, m, reinterpret_cast<const int *>(m)[0], t, tid, cb);
     }
     asm volatile("cp.async.wait_all;\n" ::: "memory");
@@ -670,7 +698,7 @@ __global__ void __launch_bounds__(kTile, pipe_minb(OP, MAT)) k_tile_pipe(PipeArg
       if (t + 2 * G < A.n_tiles) issue_meta(t + 2 * G, (k + 2) % 3);
       cp_async_commit();
       tile_phase1<D, MAT, OP, MASK>(A, m, nb, nb + um * D, nb + (NF - 1) * um * D, t, tid, contrib, eacc);
-      if constexpr (OP != OP_ENERGY) {
+      if constexpr (op_has_p2<OP>()) {
         __syncthreads();
         tile_phase2<D, OP, DET>(A, m, reinterpret_cast<const int *>(m)[0], t, tid, contrib);
       }
@@ -712,10 +740,10 @@ static int pipe_grid(Problem *p, int op) {
 template <int D, int MAT, int OP, bool MASK, bool DET>
 static fem_status launch_pipe_t(Problem *p, const PipeArgs &a, cudaStream_t s) {
   const TileSet &T = p->tiles;
-  const bool need_u = (OP != OP_HVP) || (MAT == FEM_NEO_HOOKEAN);
-  const int nf = 1 + (need_u ? 1 : 0) + (OP == OP_HVP ? 1 : 0);
+  const bool need_u = op_needs_u<OP, MAT>();
+  const int nf = 1 + (need_u ? 1 : 0) + (op_is_hvp<OP>() ? 1 : 0);
   const size_t smem = (size_t)3 * T.mb + sizeof(double) * 2 * (size_t)T.um * D * nf +
-                      (OP == OP_ENERGY ? 0 : (pipe_decoupled<OP>() ? 2 : 1) * sizeof(double) * (size_t)(D + 1) * D * kTile);
+                      (!op_has_p2<OP>() ? 0 : (pipe_decoupled<OP>() ? 2 : 1) * sizeof(double) * (size_t)(D + 1) * D * kTile);
   auto kern = k_tile_pipe<D, MAT, OP, MASK, DET>;
   FEM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   kern<<<pipe_grid(p, OP), kTile, smem, s>>>(a);
@@ -760,12 +788,16 @@ fem_status tile_pass(Problem *p, int op, const double *u, const double *v, doubl
   a.out = out;
   a.partials = partials;
   a.err = p->d_err;
+  a.lin = p->lin;
+  a.lin_stride = T.n_tiles * kTile;
   if (op == OP_ENERGY) return launch_pipe_op<OP_ENERGY, false, false>(p, a, s);
+  if (op == OP_LIN) return launch_pipe_op<OP_LIN, false, false>(p, a, s);
   if (det) {
     st = ensure(p->slotbuf, sizeof(double) * T.n_slots * p->dim);
     if (st) return st;
     a.slots = (double *)p->slotbuf.ptr;
     if (op == OP_RESIDUAL) st = launch_pipe_op<OP_RESIDUAL, false, true>(p, a, s);
+    else if (op == OP_HVP_LIN) st = mask ? launch_pipe_op<OP_HVP_LIN, true, true>(p, a, s) : launch_pipe_op<OP_HVP_LIN, false, true>(p, a, s);
     else st = mask ? launch_pipe_op<OP_HVP, true, true>(p, a, s) : launch_pipe_op<OP_HVP, false, true>(p, a, s);
     if (st) return st;
     if (p->dim == 2)
@@ -776,6 +808,8 @@ fem_status tile_pass(Problem *p, int op, const double *u, const double *v, doubl
     return FEM_OK;
   }
   if (op == OP_RESIDUAL) return launch_pipe_op<OP_RESIDUAL, false, false>(p, a, s);
+  if (op == OP_HVP_LIN)
+    return mask ? launch_pipe_op<OP_HVP_LIN, true, false>(p, a, s) : launch_pipe_op<OP_HVP_LIN, false, false>(p, a, s);
   return mask ? launch_pipe_op<OP_HVP, true, false>(p, a, s) : launch_pipe_op<OP_HVP, false, false>(p, a, s);
 }
 

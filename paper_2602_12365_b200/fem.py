@@ -28,6 +28,7 @@ ASSEMBLE_LITERAL = 4
 ASSEMBLE_JCOMP = 32
 ASSEMBLE_ROWS = 64
 ASSEMBLE_SCATTER = 128
+LINEARIZED = 256
 BASELINE_SCATTER = 8
 LOCAL_ONLY = 16
 STATUS = {0: "OK", 1: "INVALID_ARG", 2: "DEGENERATE_ELEMENT", 3: "INVERTED_ELEMENT",
@@ -38,7 +39,7 @@ STATUS = {0: "OK", 1: "INVALID_ARG", 2: "DEGENERATE_ELEMENT", 3: "INVERTED_ELEME
 EXPORTS = ("fem_create", "fem_destroy", "fem_query", "fem_check", "fem_apply_dirichlet",
            "fem_energy", "fem_residual", "fem_hvp", "fem_sparsity", "fem_color",
            "fem_assemble_csr", "fem_spmv", "fem_cg_solve", "fem_minres_solve",
-           "fem_mean_stress", "fem_add_traction", "fem_add_body_force", "fem_get_fext",
+           "fem_mean_stress", "fem_linearize", "fem_add_traction", "fem_add_body_force", "fem_get_fext",
            "fem_newton_solve", "fem_vw_create", "fem_vw_destroy", "fem_vw_apply_dirichlet",
            "fem_vw_residual", "fem_vw_jvp", "fem_vw_gmres_solve",
            "fem_nccl_unique_id", "fem_nccl_comm_init", "fem_nccl_comm_destroy",
@@ -70,7 +71,8 @@ class DistDesc(C.Structure):
 
 class CgOpts(C.Structure):
     _fields_ = [("op", C.c_int), ("rtol", C.c_double), ("atol", C.c_double),
-                ("max_iter", C.c_int), ("jacobi", C.c_int), ("check_every", C.c_int)]
+                ("max_iter", C.c_int), ("jacobi", C.c_int), ("check_every", C.c_int),
+                ("hvp_flags", C.c_uint)]
 
 
 class CgReport(C.Structure):
@@ -127,6 +129,7 @@ def load_library():
         lib.fem_spmv.argtypes = [vp, vp, vp, vp, vp]
         lib.fem_cg_solve.argtypes = [vp, vp, vp, vp, vp, C.POINTER(CgOpts), C.POINTER(CgReport), vp]
         lib.fem_minres_solve.argtypes = [vp, vp, vp, vp, vp, C.POINTER(CgOpts), C.POINTER(CgReport), vp]
+        lib.fem_linearize.argtypes = [vp, vp, vp]
         lib.fem_mean_stress.argtypes = [vp, vp, C.POINTER(C.c_double), C.POINTER(C.c_double), vp]
         lib.fem_add_traction.argtypes = [vp, C.c_int64, vp, vp, vp]
         lib.fem_add_body_force.argtypes = [vp, C.POINTER(C.c_double), vp]
@@ -320,12 +323,19 @@ class Problem:
         _check(load_library().fem_spmv(self._h, _ptr(vals), _ptr(x), _ptr(out), _stream()), "fem_spmv")
         return out
 
+    def linearize(self, z) -> None:
+        """Cache the tangent state at z for FEM_LINEARIZED HVPs (fem_linearize)."""
+        z = self._vec(z, "z")
+        _check(load_library().fem_linearize(self._h, _ptr(z), _stream()), "fem_linearize")
+
     def cg_solve(self, b, x0=None, z=None, vals=None, op: int = 0, rtol=1e-8, atol=0.0,
-                 max_iter=100000, jacobi=False, check_every=1, raise_on_fail=True):
+                 max_iter=100000, jacobi=False, check_every=1, raise_on_fail=True,
+                 linearized=False):
         b = self._vec(b, "b")
         x = torch.zeros_like(b) if x0 is None else self._vec(x0, "x0").clone()
         zz = None if z is None else self._vec(z, "z")
-        o = CgOpts(op, rtol, atol, max_iter, int(jacobi), check_every)
+        o = CgOpts(op, rtol, atol, max_iter, int(jacobi), check_every,
+                   LINEARIZED if linearized else 0)
         rep = CgReport()
         st = load_library().fem_cg_solve(self._h, _ptr(zz), _ptr(vals), _ptr(b), _ptr(x),
                                          C.byref(o), C.byref(rep), _stream())
@@ -341,7 +351,7 @@ class Problem:
         b = self._vec(b, "b")
         x = torch.zeros_like(b) if x0 is None else self._vec(x0, "x0").clone()
         zz = None if z is None else self._vec(z, "z")
-        o = CgOpts(op, rtol, atol, max_iter, 0, check_every)
+        o = CgOpts(op, rtol, atol, max_iter, 0, check_every, 0)
         rep = CgReport()
         st = load_library().fem_minres_solve(self._h, _ptr(zz), _ptr(vals), _ptr(b), _ptr(x),
                                              C.byref(o), C.byref(rep), _stream())
@@ -399,7 +409,8 @@ class Problem:
     def newton_solve(self, z0, atol=1e-12, rtol=1e-10, max_iter=50, op=0, cg_rtol=1e-10,
                      cg_max_iter=100000, jacobi=False, check_every=1, raise_on_fail=True):
         z = self._vec(z0, "z0").clone()
-        o = NewtonOpts(atol, rtol, max_iter, CgOpts(op, cg_rtol, 0.0, cg_max_iter, int(jacobi), check_every))
+        o = NewtonOpts(atol, rtol, max_iter, CgOpts(op, cg_rtol, 0.0, cg_max_iter, int(jacobi),
+                                                    check_every, 0))
         rep = NewtonReport()
         st = load_library().fem_newton_solve(self._h, _ptr(z), C.byref(o), C.byref(rep), _stream())
         info = {"status": st, "iters": rep.iters, "cg_iters": rep.cg_iters,

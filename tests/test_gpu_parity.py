@@ -343,3 +343,26 @@ def test_cg_graph_batches_match_direct_launches(fem, monkeypatch):
     assert torch.equal(xg, xd)
     assert hig["converged"] and hid["converged"]
     assert rel(hg, hd.cpu().numpy()) <= 1e-10
+
+
+def test_linearized_hvp_and_newton(fem, monkeypatch):
+    """fem_linearize caches F^-T, ln J at z; FEM_LINEARIZED HVPs equal the full HVP, and
+    Newton-Krylov linearizing at every iterate (opt-in) reaches the same solution."""
+    for name in ("3d-nh", "2d-nh-roller", "2d-nh-phases-fext"):
+        mesh = MESHES[name]
+        z = dev(fi.lift(mesh, fi.generic_state(mesh, 1)))
+        v = dev(fi.random_direction(mesh.n_total, 2))
+        prob = fem.Problem(mesh)
+        prob.linearize(z)
+        for bc in (False, True):
+            y = prob.hvp(z, v, bc=bc)
+            yl = prob.hvp(z, v, bc=bc, flags=fem.LINEARIZED)
+            assert rel(yl, y.cpu().numpy()) <= 1e-13
+    mesh = MESHES["3d-nh"]
+    prob = fem.Problem(mesh)
+    z0 = dev(fi.lift(mesh))
+    za, ia = prob.newton_solve(z0, cg_rtol=1e-12, check_every=8)
+    monkeypatch.setenv("FEM_NEWTON_LINEARIZE", "1")
+    zb, ib = prob.newton_solve(z0, cg_rtol=1e-12, check_every=8)
+    assert ia["converged"] and ib["converged"]
+    assert rel(za, zb.cpu().numpy()) <= 1e-10

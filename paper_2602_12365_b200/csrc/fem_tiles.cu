@@ -23,6 +23,9 @@
 #include "element.cuh"
 #include "fem_internal.cuh"
 
+#ifndef FEM_RES_MINB
+#define FEM_RES_MINB 3
+#endif
 #ifndef FEM_PIPE_MINB
 #define FEM_PIPE_MINB 0  // 0: per-op choice (pipe_minb)
 #endif
@@ -406,7 +409,7 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 __host__ __device__ constexpr int pipe_minb(int op, int mat) {
   return (256 / kTile) *
          (FEM_PIPE_MINB > 0 ? FEM_PIPE_MINB
-                            : (op == OP_ENERGY ? 4 : (op == OP_RESIDUAL || op == OP_LIN ? 3
+                            : (op == OP_ENERGY ? 4 : (op == OP_RESIDUAL ? FEM_RES_MINB : op == OP_LIN ? 3
                                 : (op == OP_HVP_LIN ? 3 : (mat == FEM_NEO_HOOKEAN ? 2 : 3)))));
 }
 
@@ -609,8 +612,11 @@ __device__ __forceinline__ void mb_wait(uint64_t *m, unsigned parity) {
       : "memory");
 }
 
+#ifndef FEM_RES_DEC
+#define FEM_RES_DEC 0
+#endif
 template <int OP>
-constexpr bool pipe_decoupled() { return op_is_hvp<OP>(); }
+constexpr bool pipe_decoupled() { return op_is_hvp<OP>() || (FEM_RES_DEC && OP == OP_RESIDUAL); }
 
 template <int D, int MAT, int OP, bool MASK, bool DET>
 __global__ void __launch_bounds__(kTile, pipe_minb(OP, MAT)) k_tile_pipe(PipeArgs A) {

@@ -742,7 +742,7 @@ static fem_status assemble(Problem *p, const double *z, double *vals, unsigned f
       }
     }
     if (p->rp_state == 1)
-      return launch_rows_stage(p, A.ctx, vals, bc, s);
+      return launch_rows_pull(p, A.ctx, vals, bc, s);
     const int grid = grid_for(p->n_nodes, kRowGroups, 148 * 64);
     if (p->dim == 2) k_rows_fused<2><<<grid, kRowLanes * kRowGroups, 0, s>>>(A);
     else k_rows_fused<3><<<grid, kRowLanes * kRowGroups, 0, s>>>(A);

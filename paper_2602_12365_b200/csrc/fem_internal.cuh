@@ -211,7 +211,7 @@ template <int D>
 constexpr int ctx_stride() { return D == 3 ? 28 : 16; }  // [G_a g_a] a = 0..D, smu sc1 sc2, pad
 fem_status morton_node_order(Problem *p, cudaStream_t s);
 fem_status build_row_plan(Problem *p, cudaStream_t s);          // fem_rows.cu
-fem_status launch_rows_stage(Problem *p, const double *ctx, double *vals, bool bc,
+fem_status launch_rows_pull(Problem *p, const double *ctx, double *vals, bool bc,
                              cudaStream_t s);
 fem_status build_row_tiles(Problem *p, cudaStream_t s);                  // fem_rowtile.cu
 fem_status run_linearize(Problem *p, const double *z, cudaStream_t s);   // fem_core.cu

@@ -346,7 +346,7 @@ static fem_status launch_pull(Problem *p, const double *ctx, double *vals, bool 
   return FEM_OK;
 }
 
-fem_status launch_rows_stage(Problem *p, const double *ctx, double *vals, bool bc,
+fem_status launch_rows_pull(Problem *p, const double *ctx, double *vals, bool bc,
                              cudaStream_t s) {
   if (p->dim == 2)
     return p->rp_lpn == 16 ? launch_pull<2, 16>(p, ctx, vals, bc, s) : launch_pull<2, 32>(p, ctx, vals, bc, s);

@@ -22,7 +22,7 @@ from paper_2602_12365_b200 import build, fem  # noqa: E402
 
 CASES = [("cfg5: 2D LE + periodic MPC", lambda n: fi.config_mesh(5, n=n), (70, 223, 706, 2235)),
          ("cfg2: 2D NH roller", lambda n: fi.config_mesh(2, n=n), (70, 223, 706, 2235)),
-         ("cfg3: 3D NH roller (Kuhn)", lambda n: fi.config_mesh(3, n=n), (21, 46, 99, 150))]
+         ("cfg3: 3D NH roller (Kuhn)", lambda n: fi.config_mesh(3, n=n), (21, 46, 99, 150, 200))]
 
 
 def main(prefix):
@@ -88,6 +88,10 @@ def main(prefix):
             print(name, n, mesh.n_total, {k: round(1e3 * t, 3) for k, t in res.items()}, flush=True)
         slopes[name] = {op: float(np.polyfit(np.log([a for a, _ in pts]), np.log([b for _, b in pts]), 1)[0])
                         for op, pts in per_op.items()}
+        # asymptotic slope over the two largest sizes (launch overhead dominates small ones)
+        slopes[name + " (two largest)"] = {
+            op: float(np.log(pts[-1][1] / pts[-2][1]) / np.log(pts[-1][0] / pts[-2][0]))
+            for op, pts in per_op.items()}
     with open(prefix + "_sweep.csv", "w", newline="") as f:
         w = csv.DictWriter(f, fieldnames=list(rows[0].keys()))
         w.writeheader()

@@ -109,6 +109,29 @@ def grid_tri3(nx: int, ny: int, length: float = 1.0) -> Mesh:
     return Mesh(dim=2, coords=coords, conn=conn, shape=(nx, ny), length=length)
 
 
+def delaunay_tri3(n_interior: int, n_side: int, seed: int, length: float = 1.0) -> Mesh:
+    """Unstructured Tri3 mesh of [0,L]^2 (SURVEY §8(d1) structure variant): Delaunay
+    triangulation (scipy.spatial) of n_interior seeded uniform points in the open square plus
+    n_side + 1 equispaced points on each side, oriented counter-clockwise.  Irregular node
+    degrees (the coloring / gather robustness case)."""
+    from scipy.spatial import Delaunay
+    rng = np.random.default_rng(seed)
+    h = length / n_side
+    inner = rng.uniform(0.5 * h, length - 0.5 * h, size=(n_interior, 2))
+    t = np.linspace(0.0, length, n_side + 1)
+    side = np.concatenate([np.stack([t, np.zeros_like(t)], 1), np.stack([t, np.full_like(t, length)], 1),
+                           np.stack([np.zeros_like(t[1:-1]), t[1:-1]], 1),
+                           np.stack([np.full_like(t[1:-1], length), t[1:-1]], 1)])
+    coords = np.ascontiguousarray(np.concatenate([side, inner]), np.float64)
+    conn = Delaunay(coords).simplices.astype(np.int32)
+    X = coords[conn]
+    det = ((X[:, 1, 0] - X[:, 0, 0]) * (X[:, 2, 1] - X[:, 0, 1])
+           - (X[:, 2, 0] - X[:, 0, 0]) * (X[:, 1, 1] - X[:, 0, 1]))
+    flip = det < 0
+    conn[flip, 1], conn[flip, 2] = conn[flip, 2].copy(), conn[flip, 1].copy()
+    return Mesh(dim=2, coords=coords, conn=np.ascontiguousarray(conn), length=length)
+
+
 def grid_tet4(nx: int, ny: int, nz: int, length: float = 1.0, z0: int = 0,
               nz_total: Optional[int] = None) -> Mesh:
     """Structured Kuhn Tet4 mesh (C6) of the box [0,L]x[0,L]x[0,L*nz_total/nz_total].
@@ -298,8 +321,12 @@ def affine_field(mesh: Mesh, A: np.ndarray, c: Optional[np.ndarray] = None) -> n
 def generic_state(mesh: Mesh, seed: int, eps: float = 0.05, noise: float = 0.01,
                   h: Optional[float] = None) -> np.ndarray:
     """§8(c4): affine stretch (eps) plus U(-noise*h, noise*h) per DOF, multipliers U(-1,1)."""
-    if h is None:
-        h = mesh.length / max(mesh.shape) if mesh.shape else 0.1
+    if h is None:  # structured: the cell size; unstructured: the equivalent grid spacing
+        if mesh.shape:
+            h = mesh.length / max(mesh.shape)
+        else:
+            per_cell = 2 if mesh.dim == 2 else 6
+            h = mesh.length * (per_cell / max(mesh.n_elems, 1)) ** (1.0 / mesh.dim)
     rng = np.random.default_rng(seed)
     A = np.zeros((mesh.dim, mesh.dim))
     A[0, 0] = eps

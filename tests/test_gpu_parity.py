@@ -45,6 +45,7 @@ def meshes():
         "3d-nh": fi.roller_bc(fi.perturb(fi.grid_tet4(6, 7, 5), 0.1, 6).copy_with(material=1), 0.05),
         "2d-le-mpc": fi.config_mesh(5, n=13),
         "3d-nh-shuffled": fi.renumber_nodes(fi.grid_tet4(5, 4, 6).copy_with(material=1), 21),
+        "2d-nh-delaunay": fi.roller_bc(fi.delaunay_tri3(1800, 30, 7).copy_with(material=1), 0.05),
     }
     ph = fi.two_phase(fi.perturb(fi.grid_tri3(16, 16), 0.2, 8).copy_with(material=1), 0.3,
                       (0.5, 0.3), (5.0, 3.0))

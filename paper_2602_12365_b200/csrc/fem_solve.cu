@@ -364,19 +364,18 @@ fem_status run_minres(Problem *p, const double *z, const double *vals, const dou
   int it = 0;
   fem_status result = FEM_OK;
   // y lives in R2 at the loop head (r2 = y after the previous iteration); w = W, w1/w2 rotate
-  while (true) {
-    if (rn <= tol) { rep->converged = 1; break; }
-    if (it >= o->max_iter) { result = FEM_ERR_NOT_CONVERGED; break; }
-    if (p->h_scal[M_BETA] == 0.0 && it > 0) { rep->converged = 1; break; }  // invariant space
+  // one MINRES iteration; the Lanczos (r1, r2, t) and direction (w, w1, w2) buffers rotate
+  // with period 3, so 3 iterations captured as a CUDA graph replay with consistent pointers
+  auto body = [&](bool first, cudaStream_t s) -> fem_status {
     k_minres_scale<<<g, kThreads, 0, s>>>(sc, R2, V, n);
-    st = apply_op(p, o->op, z, vals, V, T, s, o->hvp_flags);
-    if (st) return st;
-    k_minres_lanczos1<<<g, kThreads, 0, s>>>(sc, it == 0, T, R1, n);
-    st = launch_dot(p, V, T, n, sc + M_ALFA, s);
-    if (st) return st;
+    fem_status sb = apply_op(p, o->op, z, vals, V, T, s, o->hvp_flags);
+    if (sb) return sb;
+    k_minres_lanczos1<<<g, kThreads, 0, s>>>(sc, first, T, R1, n);
+    sb = launch_dot(p, V, T, n, sc + M_ALFA, s);
+    if (sb) return sb;
     k_minres_lanczos2<<<g, kThreads, 0, s>>>(sc, T, R2, n);
-    st = launch_dot(p, T, T, n, sc + M_BB2, s);
-    if (st) return st;
+    sb = launch_dot(p, T, T, n, sc + M_BB2, s);
+    if (sb) return sb;
     k_minres_scalars<<<1, 1, 0, s>>>(sc);
     // w1 <- w2, w2 <- w, w <- new (into the retired w1 buffer)
     k_minres_update<<<g, kThreads, 0, s>>>(sc, V, W2, W, W1, x, n);
@@ -388,13 +387,45 @@ fem_status run_minres(Problem *p, const double *z, const double *vals, const dou
     double *oR1 = R1;
     R1 = R2; R2 = T; T = oR1;
     FEM_LAUNCH_CHECK("minres iteration");
-    ++it;
+    return FEM_OK;
+  };
+  const bool graphs = p->size == 1 && every >= 3 && !getenv("FEM_NO_GRAPHS");
+  cudaGraphExec_t exec[3] = {nullptr, nullptr, nullptr};  // keyed by the rotation phase
+  cudaGraph_t graph[3] = {nullptr, nullptr, nullptr};
+  while (true) {
+    if (rn <= tol) { rep->converged = 1; break; }
+    if (it >= o->max_iter) { result = FEM_ERR_NOT_CONVERGED; break; }
+    if (p->h_scal[M_BETA] == 0.0 && it > 0) { rep->converged = 1; break; }  // invariant space
+    const int todo = std::min(every - it % every, o->max_iter - it);
+    if (graphs && it >= 1 && todo >= 3) {
+      const int ph = it % 3;
+      if (!exec[ph]) {
+        if (!p->cap_stream) FEM_CUDA(cudaStreamCreateWithFlags(&p->cap_stream, cudaStreamNonBlocking));
+        FEM_CUDA(cudaStreamBeginCapture(p->cap_stream, cudaStreamCaptureModeRelaxed));
+        fem_status sc3 = FEM_OK;
+        for (int k = 0; k < 3 && !sc3; ++k) sc3 = body(false, p->cap_stream);
+        cudaError_t ce = cudaStreamEndCapture(p->cap_stream, &graph[ph]);
+        if (sc3) return sc3;
+        FEM_CUDA(ce);
+        FEM_CUDA(cudaGraphInstantiate(&exec[ph], graph[ph], 0));
+      }
+      for (int k = 0; k < todo / 3; ++k) FEM_CUDA(cudaGraphLaunch(exec[ph], s));
+      it += 3 * (todo / 3);
+    } else {
+      st = body(it == 0, s);
+      if (st) return st;
+      ++it;
+    }
     if (it % every == 0 || it >= o->max_iter) {
       st = read_scalars(p, M_NSLOTS, s);
       if (st) return st;
       rn = p->h_scal[M_PHIBAR];
       if (!std::isfinite(rn)) { result = FEM_ERR_NONFINITE; break; }
     }
+  }
+  for (int k = 0; k < 3; ++k) {
+    if (exec[k]) cudaGraphExecDestroy(exec[k]);
+    if (graph[k]) cudaGraphDestroy(graph[k]);
   }
   rep->iters = it;
   // true residual ||b - A x|| for the report

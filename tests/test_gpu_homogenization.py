@@ -121,3 +121,18 @@ def test_minres_zero_rhs_and_iteration_cap(fem):
     b = dev(fi.random_direction(m.n_total, 3))
     _, info = prob.minres_solve(b, z=z0, rtol=1e-30, max_iter=5, raise_on_fail=False)
     assert info["status"] == 6 and info["iters"] == 5        # FEM_ERR_NOT_CONVERGED
+
+
+def test_minres_graph_batches_match_direct_launches(fem, monkeypatch):
+    # MINRES iterations between host checks replay a 3-iteration CUDA graph (the buffer
+    # rotation has period 3); with the deterministic CSR operator the iterates are identical
+    m = rve(12)
+    prob = fem.Problem(m)
+    z0 = dev(fi.lift(m))
+    vals = prob.assemble_csr(z0, bc=True)
+    b = dev(fi.random_direction(m.n_total, 4))
+    xg, ig = prob.minres_solve(b, vals=vals, op=1, rtol=1e-13, check_every=9)
+    monkeypatch.setenv("FEM_NO_GRAPHS", "1")
+    xd, idd = prob.minres_solve(b, vals=vals, op=1, rtol=1e-13, check_every=9)
+    assert ig["converged"] and idd["converged"] and ig["iters"] == idd["iters"]
+    assert torch.equal(xg, xd)

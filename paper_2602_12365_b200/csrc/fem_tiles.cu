@@ -548,39 +548,49 @@ __device__ __forceinline__ void tile_phase1(const PipeArgs &A, const unsigned ch
 template <int D, int OP, bool DET>
 __device__ __forceinline__ void tile_phase2(const PipeArgs &A, const unsigned char *m, int U,
                                             int64_t t, int tid, const double *cb) {
-  {
-    // phase 2: fixed-order per-tile-node sums
-    const uint16_t *ptr = reinterpret_cast<const uint16_t *>(m + A.off_ptr);
-    const uint16_t *inc = reinterpret_cast<const uint16_t *>(m + A.off_inc);
-    const int32_t *nodes = reinterpret_cast<const int32_t *>(m + A.off_nodes);
-    for (int r = tid; r < U; r += kTile) {  // one thread per tile node, D components
-      const int lo = ptr[r], hi = ptr[r + 1];
-      double sacc[D];
+  const uint16_t *ptr = reinterpret_cast<const uint16_t *>(m + A.off_ptr);
+  const uint16_t *inc = reinterpret_cast<const uint16_t *>(m + A.off_inc);
+  const int32_t *nodes = reinterpret_cast<const int32_t *>(m + A.off_nodes);
+  for (int r = tid; r < U; r += kTile) {  // one thread per tile node, D components
+    const int lo = ptr[r], hi = ptr[r + 1];
+    // two interleaved partial sums (even / odd incidences, combined in a fixed order):
+    // halves the dependent shared-memory-load -> add chain of the node's sum (A/B at cfg 3:
+    // residual 0.86 -> 0.83 ms, HVP 1.056 -> 1.042 ms; 3- and 4-way splits were slower)
+    double s0[D], s1[D];
 #pragma unroll
-      for (int cc = 0; cc < D; ++cc) sacc[cc] = 0.0;
-      for (int w = lo; w < hi; ++w) {
-        const int pk = inc[w];
-        const int el = pk >> 2, a = pk & 3;
+    for (int cc = 0; cc < D; ++cc) s0[cc] = s1[cc] = 0.0;
+    int w = lo;
+    for (; w + 1 < hi; w += 2) {
+      const int p0 = inc[w], p1 = inc[w + 1];
 #pragma unroll
-        for (int cc = 0; cc < D; ++cc) sacc[cc] += cb[(a * D + cc) * kTile + el];
+      for (int cc = 0; cc < D; ++cc) {
+        s0[cc] += cb[((p0 & 3) * D + cc) * kTile + (p0 >> 2)];
+        s1[cc] += cb[((p1 & 3) * D + cc) * kTile + (p1 >> 2)];
       }
-      if constexpr (DET) {
-        double *slot = A.slots + (A.slot_off[t] + r) * D;
+    }
+    if (w < hi) {
+      const int pk = inc[w];
 #pragma unroll
-        for (int cc = 0; cc < D; ++cc) slot[cc] = sacc[cc];
+      for (int cc = 0; cc < D; ++cc) s0[cc] += cb[((pk & 3) * D + cc) * kTile + (pk >> 2)];
+    }
+    double sacc[D];
+#pragma unroll
+    for (int cc = 0; cc < D; ++cc) sacc[cc] = s0[cc] + s1[cc];
+    if constexpr (DET) {
+      double *slot = A.slots + (A.slot_off[t] + r) * D;
+#pragma unroll
+      for (int cc = 0; cc < D; ++cc) slot[cc] = sacc[cc];
+    } else {
+      const int64_t g = (int64_t)nodes[r] * D;
+      if (m[A.off_int + r]) {
+#pragma unroll
+        for (int cc = 0; cc < D; ++cc) A.out[g + cc] = sacc[cc];
       } else {
-        const int64_t g = (int64_t)nodes[r] * D;
-        if (m[A.off_int + r]) {
 #pragma unroll
-          for (int cc = 0; cc < D; ++cc) A.out[g + cc] = sacc[cc];
-        } else {
-#pragma unroll
-          for (int cc = 0; cc < D; ++cc) atomicAdd(A.out + g + cc, sacc[cc]);
-        }
+        for (int cc = 0; cc < D; ++cc) atomicAdd(A.out + g + cc, sacc[cc]);
       }
     }
-    }
-
+  }
 }
 
 // Residual / energy: CTA-wide pipeline (cp.async.wait_all + barrier per tile).  HVP (the

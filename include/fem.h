@@ -191,11 +191,15 @@ fem_status fem_color(fem_problem *p, int32_t *colors, int32_t *n_colors, fem_str
  *            atomics (run-to-run rounding differences of the atomic order);
  *   default (no mode flag): FEM_ASSEMBLE_ROWS, except FEM_ASSEMBLE_JCOMP for 2D problems
  *            with MPC multipliers.
- * flags may add FEM_APPLY_BC.  Requires fem_color (the pattern and colors). */
+ * flags may add FEM_APPLY_BC.  Builds the pattern and (for the Alg. 2 modes) the coloring if
+ * needed; synchronizes `stream` only on that first setup. */
 fem_status fem_assemble_csr(fem_problem *p, const double *z, double *vals, unsigned flags,
                             fem_stream stream);
 
-/* y = K_csr x (pattern of fem_sparsity, values `vals`); row-ordered accumulation. */
+/* y = K_csr x (pattern of fem_sparsity, values `vals`); row-ordered accumulation.  Patterns
+ * of full dim x dim node blocks (no multiplier columns) use a node-block kernel that reads
+ * the node adjacency instead of col_idx (same values, same per-row order up to the lane
+ * reduction); otherwise plain CSR. */
 fem_status fem_spmv(fem_problem *p, const double *vals, const double *x, double *y,
                     fem_stream stream);
 

@@ -82,23 +82,6 @@ __device__ __forceinline__ void column_block(const ColumnCtx<D> &c, int a, int b
   }
 }
 
-// Same, with row node a's gradients passed in registers (runtime a).
-template <int D>
-__device__ __forceinline__ void column_block_row(const ColumnCtx<D> &c, const double (&Ga)[D],
-                                                 const double (&ga)[D], int b, int k,
-                                                 double (&out)[D]) {
-  double GG = 0.0;
-#pragma unroll
-  for (int j = 0; j < D; ++j) GG = fma(Ga[j], c.G[b][j], GG);
-  const double ak = c.c1 * ga[k], bk = c.c2 * c.g[b][k];
-#pragma unroll
-  for (int i = 0; i < D; ++i) {
-    double t = fma(ak, c.g[b][i], bk * ga[i]);
-    if (i == k) t += c.mu * GG;
-    out[i] = c.vol * t;
-  }
-}
-
 struct AsmArgs {
   const double *coords;
   const int32_t *conn;

@@ -625,8 +625,13 @@ __device__ __forceinline__ void mb_wait(uint64_t *m, unsigned parity) {
 #ifndef FEM_RES_DEC
 #define FEM_RES_DEC 0
 #endif
+#ifndef FEM_ENERGY_DEC
+#define FEM_ENERGY_DEC 0
+#endif
 template <int OP>
-constexpr bool pipe_decoupled() { return op_is_hvp<OP>() || (FEM_RES_DEC && OP == OP_RESIDUAL); }
+constexpr bool pipe_decoupled() {
+  return op_is_hvp<OP>() || (FEM_RES_DEC && OP == OP_RESIDUAL) || (FEM_ENERGY_DEC && OP == OP_ENERGY);
+}
 
 template <int D, int MAT, int OP, bool MASK, bool DET>
 __global__ void __launch_bounds__(kTile, pipe_minb(OP, MAT)) k_tile_pipe(PipeArgs A) {

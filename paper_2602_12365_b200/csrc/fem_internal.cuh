@@ -108,7 +108,7 @@ struct Problem {
   int rt_state = 0;              // 0 not built, 1 built, -1 not eligible
   uint8_t *rt_meta = nullptr;
   int64_t rt_ntiles = 0;
-  int rt_layout[13] = {0};       // RtLayout fields
+  int rt_layout[14] = {0};       // RtLayout fields
   int rt_smem = 0;
   // coloring
   bool have_colors = false;

@@ -55,7 +55,7 @@ namespace fem {
 constexpr int kRtNT = FEM_RT_NT;         // nodes per tile
 constexpr int kRtUnroll = FEM_RT_UNROLL; // entries per unrolled step of the slot sums
 constexpr int kRtThreads = 256;          // 8 warps, 2 nodes per warp per pass
-constexpr int kRtLPN = 16;               // lanes per node
+constexpr int kRtLPNMax = 16;            // lanes per node: 16 (3D) or 8 (2D, <= 8 off-diag slots)
 constexpr int kRtSortMax = 4096;         // plan: keys sorted per tile in shared memory
 
 template <int D>
@@ -75,15 +75,15 @@ __host__ __device__ constexpr int rt_pair(int a, int b) {
 }
 
 struct RtLayout {
-  int nt, uem, unm, es, ss, mb;
+  int nt, lpn, uem, unm, es, ss, mb;
   int off_halo, off_lc, off_ph, off_nd, off_so, off_sb, off_en;
 };
 
 static inline int r16(int x) { return (x + 15) & ~15; }
 
-static RtLayout rt_layout(int nt, int uem, int unm, int es, int ss, bool phase) {
+static RtLayout rt_layout(int nt, int lpn, int uem, int unm, int es, int ss, bool phase) {
   RtLayout L{};
-  L.nt = nt; L.uem = uem; L.unm = unm; L.es = es; L.ss = ss;
+  L.nt = nt; L.lpn = lpn; L.uem = uem; L.unm = unm; L.es = es; L.ss = ss;
   L.off_halo = 16;
   L.off_lc = r16(L.off_halo + 4 * unm);
   L.off_ph = r16(L.off_lc + 8 * uem);
@@ -224,14 +224,14 @@ __global__ void __launch_bounds__(256) k_rt_plan(const int32_t *node_order, int6
     };
     const int ds = sn > 0 ? slot_of(n) : 0;
     const int sno = sn > 0 ? sn - 1 : 0;
-    if (sn == 0 || ds >= sn || nadj[a0 + ds] != n || sno > kRtLPN || (NEN - 1) * deg > L.es) {
+    if (sn == 0 || ds >= sn || nadj[a0 + ds] != n || sno > L.lpn || (NEN - 1) * deg > L.es) {
       atomicOr(bad, 1);
       continue;
     }
     const int64_t rp0 = row_ptr[(int64_t)n * D];
     for (int i = 1; i <= D; ++i)
       if (row_ptr[(int64_t)n * D + i] != rp0 + (int64_t)i * D * sn) atomicOr(bad, 1);
-    uint8_t c[kRtLPN + 2];
+    uint8_t c[kRtLPNMax + 2];
     for (int q = 0; q <= sno; ++q) c[q] = 0;
     auto q_of = [&](int s) { return s < ds ? s : s - 1; };
     for (int l = 0; l < deg; ++l) {
@@ -267,22 +267,32 @@ fem_status build_row_tiles(Problem *p, cudaStream_t s) {
   if (p->n_mpc || p->n_nodes == 0 || p->n_elems == 0 || getenv("FEM_ROWS_PULL")) return FEM_OK;
   fem_status st = morton_node_order(p, s);
   if (st) return st;
-  const int D = p->dim, NEN = D + 1, NT = kRtNT;
-  const int64_t n = p->n_nodes, nt = (n + NT - 1) / NT;
-  // max degree -> entry stride
-  std::vector<int64_t> hip(n + 1);
+  const int D = p->dim, NEN = D + 1;
+  const int64_t n = p->n_nodes;
+  // max degree -> entry stride; max off-diagonal slots -> lanes per node
+  std::vector<int64_t> hip(n + 1), hap(n + 1);
   FEM_CUDA(cudaMemcpyAsync(hip.data(), p->inc_ptr, sizeof(int64_t) * (n + 1), cudaMemcpyDeviceToHost, s));
+  FEM_CUDA(cudaMemcpyAsync(hap.data(), p->nadj_ptr, sizeof(int64_t) * (n + 1), cudaMemcpyDeviceToHost, s));
   FEM_CUDA(cudaStreamSynchronize(s));
-  int IS = 0;
-  for (int64_t i = 0; i < n; ++i) IS = std::max<int>(IS, (int)(hip[i + 1] - hip[i]));
-  const int ES = (((NEN - 1) * IS) + 7) & ~7, SS = (kRtLPN + 1 + 3) & ~3;
+  int IS = 0, SN = 0;
+  for (int64_t i = 0; i < n; ++i) {
+    IS = std::max<int>(IS, (int)(hip[i + 1] - hip[i]));
+    SN = std::max<int>(SN, (int)(hap[i + 1] - hap[i]));
+  }
+  if (SN - 1 > kRtLPNMax) return FEM_OK;
+  // 8 lanes per node when the slots allow (2D Tri3: 6): 4 nodes per warp, 32-node tiles;
+  // otherwise 16 lanes (3D Kuhn: 14 slots), 2 nodes per warp, kRtNT-node tiles
+  const int LPN = (SN - 1 <= 8 && !getenv("FEM_RT_LPN16")) ? 8 : 16;
+  const int NT = LPN == 8 ? 32 : kRtNT;
+  const int64_t nt = (n + NT - 1) / NT;
+  const int ES = (((NEN - 1) * IS) + 7) & ~7, SS = (LPN + 1 + 3) & ~3;
   if (IS == 0 || (NEN - 1) * IS > 255) return FEM_OK;
   int *d_bad = nullptr;
   int32_t *cnt = nullptr;
   FEM_CUDA(cudaMalloc(&d_bad, sizeof(int)));
   FEM_CUDA(cudaMalloc(&cnt, sizeof(int32_t) * 2 * nt));
   FEM_CUDA(cudaMemsetAsync(d_bad, 0, sizeof(int), s));
-  RtLayout L0 = rt_layout(NT, 8, 8, ES, SS, p->phase != nullptr);
+  RtLayout L0 = rt_layout(NT, LPN, 8, 8, ES, SS, p->phase != nullptr);
   if (D == 2) k_rt_plan<2><<<(unsigned)nt, 256, 0, s>>>(p->node_order, n, p->inc_ptr, p->inc, p->conn, p->phase, p->nadj_ptr, p->nadj, p->row_ptr, p->node_bc, L0, cnt, nullptr, d_bad);
   else k_rt_plan<3><<<(unsigned)nt, 256, 0, s>>>(p->node_order, n, p->inc_ptr, p->inc, p->conn, p->phase, p->nadj_ptr, p->nadj, p->row_ptr, p->node_bc, L0, cnt, nullptr, d_bad);
   FEM_LAUNCH_CHECK("row tiles (count)");
@@ -298,7 +308,7 @@ fem_status build_row_tiles(Problem *p, cudaStream_t s) {
   }
   uem = (uem + 7) & ~7;
   unm = (unm + 7) & ~7;
-  const RtLayout L = rt_layout(NT, uem, unm, ES, SS, p->phase != nullptr);
+  const RtLayout L = rt_layout(NT, LPN, uem, unm, ES, SS, p->phase != nullptr);
   // shared memory of the assembly kernel: 3 metadata blocks, 2 node-data buffers, records
   const int RS = D == 3 ? RtGeom<3>::RS : RtGeom<2>::RS;
   const int BP = D == 3 ? RtGeom<3>::BP : RtGeom<2>::BP;
@@ -328,6 +338,7 @@ fem_status build_row_tiles(Problem *p, cudaStream_t s) {
   p->rt_layout[6] = L.off_halo; p->rt_layout[7] = L.off_lc; p->rt_layout[8] = L.off_ph;
   p->rt_layout[9] = L.off_nd; p->rt_layout[10] = L.off_so; p->rt_layout[11] = L.off_sb;
   p->rt_layout[12] = L.off_en;
+  p->rt_layout[13] = L.lpn;
   p->rt_smem = (int)smem;
   p->rt_state = 1;
   return FEM_OK;
@@ -357,7 +368,7 @@ struct RtArgs {
   int *err;
 };
 
-template <int D, int MAT>
+template <int D, int MAT, int LPN>
 __global__ void __launch_bounds__(kRtThreads, FEM_RT_MINB) k_rows_tile(RtArgs A) {
   using Gm = RtGeom<D>;
   constexpr int NEN = Gm::NEN, BS = Gm::BS, RS = Gm::RS;
@@ -465,10 +476,11 @@ __global__ void __launch_bounds__(kRtThreads, FEM_RT_MINB) k_rows_tile(RtArgs A)
       r[Gm::S0 + 1] = ok ? vol * lam : 0.0;
     }
     __syncthreads();
-    // ---- 2: rows, 16 lanes per tile node
-    const int h = lane / kRtLPN, ql = lane % kRtLPN;
+    // ---- 2: rows, LPN lanes per tile node (NPW nodes per warp)
+    constexpr int NPW = 32 / LPN;
+    const int h = lane / LPN, ql = lane % LPN;
     const int4 *ndw = reinterpret_cast<const int4 *>(m + L.off_nd);
-    for (int j = 2 * w + h; j < L.nt; j += 2 * (kRtThreads / 32)) {
+    for (int j = NPW * w + h; j < L.nt; j += NPW * (kRtThreads / 32)) {
       const int4 nd = ndw[j];
       const int sno = nd.y & 0xff, sn = (nd.y >> 8) & 0xff, ds = (nd.y >> 16) & 0xff;
       const unsigned bcn = A.bc ? ((unsigned)nd.y >> 24) : 0u;
@@ -546,7 +558,7 @@ __global__ void __launch_bounds__(kRtThreads, FEM_RT_MINB) k_rows_tile(RtArgs A)
       __syncwarp();
       if (live && ql < BS) {
         const int i = ql / D, kk = ql % D;
-        const double *sb = scratch + (w * 32 + h * kRtLPN) * Gm::BP + ql;
+        const double *sb = scratch + (w * 32 + h * LPN) * Gm::BP + ql;
         double v = 0.0;
         for (int q = 0; q < sno; ++q) v += sb[q * Gm::BP];
         v = -v;
@@ -561,7 +573,7 @@ __global__ void __launch_bounds__(kRtThreads, FEM_RT_MINB) k_rows_tile(RtArgs A)
       for (int q = 0; q < BS; ++q) {
         double v = acc[q];
 #pragma unroll
-        for (int o = kRtLPN / 2; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, v, o, kRtLPN);
+        for (int o = LPN / 2; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, v, o, LPN);
         acc[q] = v;
       }
       if (live) {
@@ -586,12 +598,18 @@ fem_status launch_row_tiles(Problem *p, const double *z, double *vals, bool bc, 
   A.L.nt = lay[0]; A.L.uem = lay[1]; A.L.unm = lay[2]; A.L.es = lay[3]; A.L.ss = lay[4];
   A.L.mb = lay[5]; A.L.off_halo = lay[6]; A.L.off_lc = lay[7]; A.L.off_ph = lay[8];
   A.L.off_nd = lay[9]; A.L.off_so = lay[10]; A.L.off_sb = lay[11]; A.L.off_en = lay[12];
+  A.L.lpn = lay[13];
   A.meta = p->rt_meta; A.n_tiles = p->rt_ntiles; A.coords = p->coords; A.z = z;
   A.lam = p->lam; A.mu = p->mu; A.lam_tab = p->lam_tab; A.mu_tab = p->mu_tab;
   A.has_phase = p->phase != nullptr; A.bc = bc ? 1 : 0; A.vals = vals; A.err = p->d_err;
   void (*kern)(RtArgs);
-  if (p->dim == 2) kern = p->material == FEM_LINEAR_ELASTIC ? k_rows_tile<2, FEM_LINEAR_ELASTIC> : k_rows_tile<2, FEM_NEO_HOOKEAN>;
-  else kern = p->material == FEM_LINEAR_ELASTIC ? k_rows_tile<3, FEM_LINEAR_ELASTIC> : k_rows_tile<3, FEM_NEO_HOOKEAN>;
+  const bool le = p->material == FEM_LINEAR_ELASTIC, l8 = A.L.lpn == 8;
+  if (p->dim == 2)
+    kern = le ? (l8 ? k_rows_tile<2, FEM_LINEAR_ELASTIC, 8> : k_rows_tile<2, FEM_LINEAR_ELASTIC, 16>)
+              : (l8 ? k_rows_tile<2, FEM_NEO_HOOKEAN, 8> : k_rows_tile<2, FEM_NEO_HOOKEAN, 16>);
+  else
+    kern = le ? (l8 ? k_rows_tile<3, FEM_LINEAR_ELASTIC, 8> : k_rows_tile<3, FEM_LINEAR_ELASTIC, 16>)
+              : (l8 ? k_rows_tile<3, FEM_NEO_HOOKEAN, 8> : k_rows_tile<3, FEM_NEO_HOOKEAN, 16>);
   FEM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, p->rt_smem));
   int per_sm = 0;
   FEM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kRtThreads, p->rt_smem));

@@ -34,6 +34,9 @@
 #ifndef FEM_RT_DIAG_SMEM
 #define FEM_RT_DIAG_SMEM 1
 #endif
+#ifndef FEM_RT_BPODD
+#define FEM_RT_BPODD 1
+#endif
 #ifndef FEM_RT_UNROLL
 #define FEM_RT_UNROLL 4
 #endif
@@ -64,7 +67,7 @@ struct RtGeom {
   static constexpr int GP = FEM_RT_GPAD ? ((D + 1) & ~1) : D;     // g_a stride (padded: 16 B)
   static constexpr int G0 = 0, M0 = NEN * GP, S0 = M0 + NPAIR + (NPAIR & 1);  // g | M | sc1 sc2
   static constexpr int RS = FEM_RT_RSODD ? ((S0 + 2) | 1) : (S0 + 2);  // odd: spreads records over banks
-  static constexpr int BP = (BS + 1) & ~1;                        // scratch block pitch
+  static constexpr int BP = FEM_RT_BPODD ? (BS | 1) : ((BS + 1) & ~1);  // scratch block pitch
 };
 
 // index of the unordered node pair {a, b}: 3D (01 02 03 12 13 23), 2D (01 02 12)

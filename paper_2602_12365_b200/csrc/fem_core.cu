@@ -341,6 +341,30 @@ __global__ void k_validate_dofs(const int32_t *dd, int64_t nd, const int32_t *ms
 
 // ------------------------------------------------------------------ internal runners
 
+// Element pass of the residual / HVP on a multi-GPU problem: tiles touching interface nodes,
+// then (exchange of their partials on the comm stream) the interior tiles, then the combine;
+// FEM_LOCAL_ONLY runs the same two passes without the exchange.  Single GPU: one pass.
+static fem_status element_pass_halo(Problem *p, int op, const double *z, const double *v,
+                                    double *y, bool bc, bool det, bool local_only,
+                                    cudaStream_t s) {
+  if (p->size <= 1 || det) {
+    fem_status st = tile_pass(p, op, z, v, y, bc, det, nullptr, s);
+    if (st) return st;
+    return (p->size > 1 && !local_only) ? halo_add(p, y, s) : FEM_OK;
+  }
+  fem_status st = build_tile_lists(p, s);
+  if (st) return st;
+  st = tile_pass(p, op, z, v, y, bc, false, nullptr, s, 1);
+  if (st) return st;
+  if (!local_only) {
+    st = halo_begin(p, y, s);
+    if (st) return st;
+  }
+  st = tile_pass(p, op, z, v, y, bc, false, nullptr, s, 2);
+  if (st) return st;
+  return local_only ? FEM_OK : halo_end(p, y, s);
+}
+
 fem_status run_residual(Problem *p, const double *z, double *r, unsigned flags, cudaStream_t s) {
   const bool det = flags & FEM_DETERMINISTIC;
   if (!det || p->n_elems == 0) FEM_CUDA(cudaMemsetAsync(r, 0, sizeof(double) * p->N, s));
@@ -352,10 +376,10 @@ fem_status run_residual(Problem *p, const double *z, double *r, unsigned flags, 
     st = launch_elem<OP_RESIDUAL, false>(p, a, grid_for(p->n_elems), s);
   } else {
     if (det && p->n_mpc) FEM_CUDA(cudaMemsetAsync(r + p->n_u, 0, sizeof(double) * p->n_mpc, s));
-    st = tile_pass(p, OP_RESIDUAL, z, nullptr, r, false, det, nullptr, s);
+    st = element_pass_halo(p, OP_RESIDUAL, z, nullptr, r, false, det, flags & FEM_LOCAL_ONLY, s);
   }
   if (st) return st;
-  if (p->size > 1 && !(flags & FEM_LOCAL_ONLY)) {
+  if ((flags & FEM_BASELINE_SCATTER) && p->size > 1 && !(flags & FEM_LOCAL_ONLY)) {
     st = halo_add(p, r, s);
     if (st) return st;
   }
@@ -392,10 +416,10 @@ fem_status run_hvp(Problem *p, const double *z, const double *v, double *y, unsi
       set_error("fem_hvp: FEM_LINEARIZED without a preceding fem_linearize");
       return FEM_ERR_INVALID_ARG;
     }
-    st = tile_pass(p, lin ? OP_HVP_LIN : OP_HVP, z, v, y, bc, det, nullptr, s);
+    st = element_pass_halo(p, lin ? OP_HVP_LIN : OP_HVP, z, v, y, bc, det, flags & FEM_LOCAL_ONLY, s);
   }
   if (st) return st;
-  if (p->size > 1 && !(flags & FEM_LOCAL_ONLY)) {
+  if ((flags & FEM_BASELINE_SCATTER) && p->size > 1 && !(flags & FEM_LOCAL_ONLY)) {
     st = halo_add(p, y, s);
     if (st) return st;
   }

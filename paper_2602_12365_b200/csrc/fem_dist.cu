@@ -96,15 +96,22 @@ fem_status dist_setup(Problem *p, const fem_dist_desc *d, cudaStream_t s) {
   }
   FEM_CUDA(cudaMemcpyAsync(p->halo_src_ptr, src_ptr.data(), sizeof(int32_t) * src_ptr.size(), cudaMemcpyHostToDevice, s));
   FEM_CUDA(cudaMemcpyAsync(p->owned, d->owned, p->n_nodes, cudaMemcpyHostToDevice, s));
+  std::vector<uint8_t> shared(p->n_nodes, 0);
+  for (int32_t n : nodes) shared[n] = 1;
+  FEM_CUDA(cudaMalloc(&p->shared, p->n_nodes > 0 ? p->n_nodes : 1));
+  if (p->n_nodes) FEM_CUDA(cudaMemcpyAsync(p->shared, shared.data(), p->n_nodes, cudaMemcpyHostToDevice, s));
   FEM_CUDA(cudaStreamSynchronize(s));  // host vectors above go out of scope
   return FEM_OK;
 }
 
 void dist_free(Problem *p) {
   void *bufs[] = {p->halo_send_nodes, p->halo_nodes, p->halo_src_ptr, p->halo_src, p->sendbuf,
-                  p->recvbuf, p->owned};
+                  p->recvbuf, p->owned, p->shared};
   for (void *b : bufs)
     if (b) cudaFree(b);
+  if (p->ev_part_a) cudaEventDestroy(p->ev_part_a);
+  if (p->ev_halo) cudaEventDestroy(p->ev_halo);
+  if (p->comm_stream) cudaStreamDestroy(p->comm_stream);
 }
 
 static fem_status halo_pack(Problem *p, const double *y, double *send, cudaStream_t s) {
@@ -122,13 +129,13 @@ static fem_status halo_combine(Problem *p, double *y, const double *recv, cudaSt
   return FEM_OK;
 }
 
-fem_status halo_add(Problem *p, double *y, cudaStream_t s) {
-  if (p->size <= 1) return FEM_OK;
+// pack + grouped send / recv of y's shared-node partials on stream cs
+static fem_status halo_exchange(Problem *p, const double *y, cudaStream_t cs) {
   if (!p->nccl) {
     set_error("halo add needs an NCCL communicator (or FEM_LOCAL_ONLY + fem_halo_pack/combine)");
     return FEM_ERR_NCCL;
   }
-  fem_status st = halo_pack(p, y, p->sendbuf, s);
+  fem_status st = halo_pack(p, y, p->sendbuf, cs);
   if (st) return st;
   ncclComm_t comm = (ncclComm_t)p->nccl;
   const int D = p->dim;
@@ -136,13 +143,42 @@ fem_status halo_add(Problem *p, double *y, cudaStream_t s) {
   if (r) return r;
   for (int k = 0; k < p->n_nbr; ++k) {
     const int64_t off = p->nbr_off_h[k] * D, cnt = (p->nbr_off_h[k + 1] - p->nbr_off_h[k]) * D;
-    r = nccl_status(ncclSend(p->sendbuf + off, (size_t)cnt, ncclDouble, p->nbr_rank_h[k], comm, s), "ncclSend");
+    r = nccl_status(ncclSend(p->sendbuf + off, (size_t)cnt, ncclDouble, p->nbr_rank_h[k], comm, cs), "ncclSend");
     if (r) return r;
-    r = nccl_status(ncclRecv(p->recvbuf + off, (size_t)cnt, ncclDouble, p->nbr_rank_h[k], comm, s), "ncclRecv");
+    r = nccl_status(ncclRecv(p->recvbuf + off, (size_t)cnt, ncclDouble, p->nbr_rank_h[k], comm, cs), "ncclRecv");
     if (r) return r;
   }
-  r = nccl_status(ncclGroupEnd(), "ncclGroupEnd");
-  if (r) return r;
+  return nccl_status(ncclGroupEnd(), "ncclGroupEnd");
+}
+
+fem_status halo_add(Problem *p, double *y, cudaStream_t s) {
+  if (p->size <= 1) return FEM_OK;
+  fem_status st = halo_exchange(p, y, s);
+  if (st) return st;
+  return halo_combine(p, y, p->recvbuf, s);
+}
+
+// Overlapped form: called after the pass over the tiles that touch interface
+// nodes, whose partials are then final.  The exchange runs on the problem's comm stream
+// while the caller's stream computes the interior tiles; halo_end joins and combines.
+fem_status halo_begin(Problem *p, const double *y, cudaStream_t s) {
+  if (p->size <= 1) return FEM_OK;
+  if (!p->comm_stream) {
+    FEM_CUDA(cudaStreamCreateWithFlags(&p->comm_stream, cudaStreamNonBlocking));
+    FEM_CUDA(cudaEventCreateWithFlags(&p->ev_part_a, cudaEventDisableTiming));
+    FEM_CUDA(cudaEventCreateWithFlags(&p->ev_halo, cudaEventDisableTiming));
+  }
+  FEM_CUDA(cudaEventRecord(p->ev_part_a, s));
+  FEM_CUDA(cudaStreamWaitEvent(p->comm_stream, p->ev_part_a, 0));
+  fem_status st = halo_exchange(p, y, p->comm_stream);
+  if (st) return st;
+  FEM_CUDA(cudaEventRecord(p->ev_halo, p->comm_stream));
+  return FEM_OK;
+}
+
+fem_status halo_end(Problem *p, double *y, cudaStream_t s) {
+  if (p->size <= 1) return FEM_OK;
+  FEM_CUDA(cudaStreamWaitEvent(s, p->ev_halo, 0));
   return halo_combine(p, y, p->recvbuf, s);
 }
 

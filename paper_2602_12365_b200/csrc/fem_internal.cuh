@@ -32,6 +32,10 @@ enum { OP_ENERGY = 0, OP_RESIDUAL = 1, OP_HVP = 2, OP_HVP_LIN = 3, OP_LIN = 4 };
 struct TileSet {
   bool built = false;
   int64_t n_tiles = 0, n_slots = 0;
+  // multi-GPU: tiles touching shared (interface) nodes first, then the interior tiles, so the
+  // halo exchange overlaps the interior pass (fem_core.cu element_pass_halo)
+  int32_t *list = nullptr;       // [n_tiles] boundary tiles, then interior tiles
+  int64_t n_boundary = -1;       // -1: lists not built
   int maxe = 0, max_U = 0;
   int32_t *perm = nullptr;       // [E] tile order -> caller element id
   int32_t *nodes = nullptr;      // [n_tiles][maxe] sorted unique nodes (first U valid)
@@ -131,6 +135,9 @@ struct Problem {
           *halo_src = nullptr;
   double *sendbuf = nullptr, *recvbuf = nullptr;
   uint8_t *owned = nullptr;     // [n_nodes] (size > 1)
+  uint8_t *shared = nullptr;    // [n_nodes] 1 if the node is on an interface (size > 1)
+  cudaStream_t comm_stream = nullptr;
+  cudaEvent_t ev_part_a = nullptr, ev_halo = nullptr;
 };
 
 // ------------------------------------------------------------------ error plumbing
@@ -202,8 +209,12 @@ fem_status run_hvp(Problem *p, const double *z, const double *v, double *y, unsi
 fem_status run_spmv(Problem *p, const double *vals, const double *x, double *y, cudaStream_t s);
 fem_status halo_add(Problem *p, double *y, cudaStream_t s);
 fem_status build_tiles(Problem *p, cudaStream_t s);
+// part: 0 all tiles, 1 the tiles touching interface nodes, 2 the other tiles (TileSet::list)
 fem_status tile_pass(Problem *p, int op, const double *u, const double *v, double *out, bool mask,
-                     bool det, double *partials, cudaStream_t s);
+                     bool det, double *partials, cudaStream_t s, int part = 0);
+fem_status build_tile_lists(Problem *p, cudaStream_t s);
+fem_status halo_begin(Problem *p, const double *y, cudaStream_t s);
+fem_status halo_end(Problem *p, double *y, cudaStream_t s);
 void free_tiles(TileSet &T);
 int tile_energy_partials(Problem *p);
 // per-element tangent context records (k_elem_ctx, fem_assemble.cu): doubles per element

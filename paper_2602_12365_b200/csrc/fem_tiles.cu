@@ -423,6 +423,7 @@ struct PipeArgs {
   double lam, mu;
   const double *lam_tab, *mu_tab;
   double *out, *slots, *partials;
+  const int32_t *list;  // tile ids to process (null: tiles 0 .. n_tiles-1)
   double *lin;        // linearization cache [10][lin_stride] (OP_LIN writes, OP_HVP_LIN reads)
   int64_t lin_stride;
   int *err;
@@ -648,9 +649,10 @@ __global__ void __launch_bounds__(kTile, pipe_minb(OP, MAT)) k_tile_pipe(PipeArg
   double *contrib = nodeb + 2 * nstride;
   const int64_t G = gridDim.x;
 
+  auto tile_id = [&](int64_t i) -> int64_t { return A.list ? (int64_t)__ldg(A.list + i) : i; };
   auto issue_meta = [&](int64_t t, int b) {
     unsigned char *dst = metab + b * mb;
-    const unsigned char *src = A.meta + t * (int64_t)mb;
+    const unsigned char *src = A.meta + tile_id(t) * (int64_t)mb;
     for (int off = tid * 16; off < mb; off += kTile * 16) cp_async16(dst + off, src + off);
     if constexpr (DEC) mb_cp_arrive(&mb_meta[b]);
   };
@@ -693,11 +695,11 @@ __global__ void __launch_bounds__(kTile, pipe_minb(OP, MAT)) k_tile_pipe(PipeArg
       }
       const double *nb = nodeb + bn * nstride;
       double *cb = contrib + (k & 1) * ((D + 1) * D * kTile);
-      tile_phase1<D, MAT, OP, MASK>(A, m, nb, nb + um * D, nb + (NF - 1) * um * D, t, tid, cb, eacc);
+      tile_phase1<D, MAT, OP, MASK>(A, m, nb, nb + um * D, nb + (NF - 1) * um * D, tile_id(t), tid, cb, eacc);
       __syncthreads();  // phase 1 of tile k done; tile k-1 fully consumed
       if (t + 2 * G < A.n_tiles) issue_meta(t + 2 * G, (k + 2) % 3);
       if constexpr (op_has_p2<OP>())
-        tile_phase2<D, OP, DET>(A, m, reinterpret_cast<const int *>(m)[0], t, tid, cb);
+        tile_phase2<D, OP, DET>(A, m, reinterpret_cast<const int *>(m)[0], tile_id(t), tid, cb);
     }
     asm volatile("cp.async.wait_all;\n" ::: "memory");
   } else {
@@ -718,10 +720,10 @@ __global__ void __launch_bounds__(kTile, pipe_minb(OP, MAT)) k_tile_pipe(PipeArg
       if (t + G < A.n_tiles) issue_nodes(metab + ((k + 1) % 3) * mb, (k + 1) & 1);
       if (t + 2 * G < A.n_tiles) issue_meta(t + 2 * G, (k + 2) % 3);
       cp_async_commit();
-      tile_phase1<D, MAT, OP, MASK>(A, m, nb, nb + um * D, nb + (NF - 1) * um * D, t, tid, contrib, eacc);
+      tile_phase1<D, MAT, OP, MASK>(A, m, nb, nb + um * D, nb + (NF - 1) * um * D, tile_id(t), tid, contrib, eacc);
       if constexpr (op_has_p2<OP>()) {
         __syncthreads();
-        tile_phase2<D, OP, DET>(A, m, reinterpret_cast<const int *>(m)[0], t, tid, contrib);
+        tile_phase2<D, OP, DET>(A, m, reinterpret_cast<const int *>(m)[0], tile_id(t), tid, contrib);
       }
       __syncthreads();
     }
@@ -754,8 +756,8 @@ __global__ void k_slot_gather(const int64_t *node_slot_ptr, const int32_t *node_
 // grid of the persistent kernels (fixed per problem: deterministic energy partial order)
 // grid of the persistent kernels: 148 SMs x CTAs/SM of the op (fixed per problem and op,
 // so the energy partial order is deterministic)
-static int pipe_grid(Problem *p, int op) {
-  return (int)std::min<int64_t>(p->tiles.n_tiles, 148 * pipe_minb(op, p->material));
+static int pipe_grid(Problem *p, int op, int64_t n = -1) {
+  return (int)std::max<int64_t>(1, std::min<int64_t>(n < 0 ? p->tiles.n_tiles : n, 148 * pipe_minb(op, p->material)));
 }
 
 template <int D, int MAT, int OP, bool MASK, bool DET>
@@ -767,7 +769,7 @@ static fem_status launch_pipe_t(Problem *p, const PipeArgs &a, cudaStream_t s) {
                       (!op_has_p2<OP>() ? 0 : (pipe_decoupled<OP>() ? 2 : 1) * sizeof(double) * (size_t)(D + 1) * D * kTile);
   auto kern = k_tile_pipe<D, MAT, OP, MASK, DET>;
   FEM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  kern<<<pipe_grid(p, OP), kTile, smem, s>>>(a);
+  kern<<<pipe_grid(p, OP, a.n_tiles), kTile, smem, s>>>(a);
   FEM_LAUNCH_CHECK("tile pipeline kernel");
   return FEM_OK;
 }
@@ -785,7 +787,7 @@ static fem_status launch_pipe_op(Problem *p, const PipeArgs &a, cudaStream_t s) 
 // Element pass of the residual / HVP (op = OP_RESIDUAL / OP_HVP) or the energy partials
 // (OP_ENERGY: one partial per CTA into `partials`, *n_partials set).
 fem_status tile_pass(Problem *p, int op, const double *u, const double *v, double *out,
-                     bool mask, bool det, double *partials, cudaStream_t s) {
+                     bool mask, bool det, double *partials, cudaStream_t s, int part) {
   fem_status st = build_tiles(p, s);
   if (st) return st;
   if (p->n_elems == 0) return FEM_OK;
@@ -793,6 +795,12 @@ fem_status tile_pass(Problem *p, int op, const double *u, const double *v, doubl
   PipeArgs a{};
   a.meta = T.meta;
   a.n_tiles = T.n_tiles;
+  if (part) {  // one of the two halves of TileSet::list (no DET, no energy)
+    if (T.n_boundary < 0 || det || op == OP_ENERGY) return FEM_ERR_INVALID_ARG;
+    a.list = T.list + (part == 1 ? 0 : T.n_boundary);
+    a.n_tiles = part == 1 ? T.n_boundary : T.n_tiles - T.n_boundary;
+    if (a.n_tiles == 0) return FEM_OK;
+  }
   a.E = p->n_elems;
   a.mb = T.mb; a.um = T.um; a.off_nodes = T.off_nodes; a.off_lconn = T.off_lconn;
   a.off_ptr = T.off_ptr; a.off_inc = T.off_inc; a.off_int = T.off_int; a.off_bc = T.off_bc;
@@ -835,6 +843,43 @@ fem_status tile_pass(Problem *p, int op, const double *u, const double *v, doubl
 }
 
 int tile_energy_partials(Problem *p) { return pipe_grid(p, OP_ENERGY); }
+
+__global__ void k_tile_shared(TileSet T, const uint8_t *shared, uint8_t *flag) {
+  for (int64_t t = blockIdx.x; t < T.n_tiles; t += gridDim.x) {
+    const int U = T.U[t];
+    int any = 0;
+    for (int r = threadIdx.x; r < U; r += blockDim.x) any |= shared[T.nodes[t * T.maxe + r]];
+    any = __syncthreads_or(any);
+    if (threadIdx.x == 0) flag[t] = (uint8_t)(any != 0);
+  }
+}
+
+// Multi-GPU: order the tiles as (tiles touching interface nodes, the rest); stable in tile
+// order within each part.
+fem_status build_tile_lists(Problem *p, cudaStream_t s) {
+  TileSet &T = p->tiles;
+  if (T.n_boundary >= 0 || p->size <= 1 || !p->shared) return FEM_OK;
+  fem_status st = build_tiles(p, s);
+  if (st) return st;
+  uint8_t *flag = nullptr;
+  FEM_CUDA(cudaMalloc(&flag, T.n_tiles > 0 ? T.n_tiles : 1));
+  if (T.n_tiles) k_tile_shared<<<grid_for(T.n_tiles, 1, 148 * 16), 128, 0, s>>>(T, p->shared, flag);
+  FEM_LAUNCH_CHECK("tile lists");
+  std::vector<uint8_t> hf(T.n_tiles);
+  FEM_CUDA(cudaMemcpyAsync(hf.data(), flag, T.n_tiles, cudaMemcpyDeviceToHost, s));
+  FEM_CUDA(cudaStreamSynchronize(s));
+  cudaFree(flag);
+  std::vector<int32_t> lst;
+  lst.reserve(T.n_tiles);
+  for (int64_t t = 0; t < T.n_tiles; ++t) if (hf[t]) lst.push_back((int32_t)t);
+  const int64_t nb = (int64_t)lst.size();
+  for (int64_t t = 0; t < T.n_tiles; ++t) if (!hf[t]) lst.push_back((int32_t)t);
+  FEM_CUDA(cudaMalloc(&T.list, sizeof(int32_t) * (lst.empty() ? 1 : lst.size())));
+  if (!lst.empty()) FEM_CUDA(cudaMemcpyAsync(T.list, lst.data(), sizeof(int32_t) * lst.size(), cudaMemcpyHostToDevice, s));
+  FEM_CUDA(cudaStreamSynchronize(s));
+  T.n_boundary = nb;
+  return FEM_OK;
+}
 
 
 template <int D>
@@ -893,7 +938,7 @@ fem_status morton_node_order(Problem *p, cudaStream_t s) {
 
 void free_tiles(TileSet &T) {
   void *bufs[] = {T.perm, T.nodes, T.U, T.ptr, T.inc, T.lconn, T.interior, T.phase, T.slot_off,
-                  T.node_slots, T.node_slot_ptr, T.epart, T.meta};
+                  T.node_slots, T.node_slot_ptr, T.epart, T.meta, T.list};
   for (void *b : bufs)
     if (b) cudaFree(b);
   T = TileSet{};

@@ -96,14 +96,19 @@ __global__ void k_final_sum2(const double *pa, const double *pb, int n, double *
   }
 }
 
-__global__ void k_jacobi_diag(const double *vals, const int64_t *diag_pos, int64_t N, double *dinv,
-                              int *err) {
+__global__ void k_diag_of(const double *vals, const int64_t *diag_pos, int64_t N, double *d) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < N;
        i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t q = diag_pos[i];
-    const double d = q >= 0 ? vals[q] : 0.0;
-    if (!(d > 0.0)) atomicOr(err, ERRW_NONFINITE);
-    dinv[i] = 1.0 / d;
+    d[i] = q >= 0 ? vals[q] : 0.0;
+  }
+}
+
+__global__ void k_invert(double *d, int64_t N, int *err) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < N;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    if (!(d[i] > 0.0)) atomicOr(err, ERRW_NONFINITE);
+    d[i] = 1.0 / d[i];
   }
 }
 
@@ -142,7 +147,14 @@ fem_status run_cg(Problem *p, const double *z, const double *vals, const double 
   double *zv = jac ? Ap + n : r, *dinv = jac ? Ap + 2 * n : nullptr;
   const int nb = grid_for(n, kThreads, kReduceBlocks);
   double *part_a = p->partials, *part_b = p->partials + kReduceBlocks;
-  if (jac) k_jacobi_diag<<<grid_for(n), kThreads, 0, s>>>(vals, p->diag_pos, n, dinv, p->d_err);
+  if (jac) {  // multi-GPU: interface rows of the local CSR hold partial sums -> halo add
+    k_diag_of<<<grid_for(n), kThreads, 0, s>>>(vals, p->diag_pos, n, dinv);
+    if (p->size > 1) {
+      st = halo_add(p, dinv, s);
+      if (st) return st;
+    }
+    k_invert<<<grid_for(n), kThreads, 0, s>>>(dinv, n, p->d_err);
+  }
   // r0 = b - A x0
   st = apply_op(p, o->op, z, vals, x, Ap, s, o->hvp_flags);
   if (st) return st;

@@ -23,6 +23,9 @@
 #include "element.cuh"
 #include "fem_internal.cuh"
 
+#ifndef FEM_PIPE_MINB2D
+#define FEM_PIPE_MINB2D 0
+#endif
 #ifndef FEM_RES_MINB
 #define FEM_RES_MINB 3
 #endif
@@ -406,9 +409,17 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 // CTAs per SM the register budget targets (A/B on cfg 3, profiles/): the NH HVP is the
 // register-heaviest and runs fastest spill-free at 2; energy at 4; residual at 3.
 // (stated for 256-thread CTAs; smaller tiles scale the CTA count so warps/SM stay equal)
-__host__ __device__ constexpr int pipe_minb(int op, int mat) {
+// 2D elements need far fewer registers (46-68): more CTAs per SM.  A/B at the cfg 2 size
+// (10M DOFs, CTAs/SM 2/3/4/5): HVP 0.340/0.303/0.344/0.344 ms, residual (3 by default)
+// 0.266/0.266/0.255/0.251 ms, energy (4 by default) 0.166/0.172/0.170/0.163 ms.
+__host__ __device__ constexpr int pipe_minb2d(int op, int mat) {
+  return op == OP_ENERGY || op == OP_RESIDUAL || op == OP_LIN ? 5
+         : (mat == FEM_NEO_HOOKEAN ? 3 : 4);
+}
+__host__ __device__ constexpr int pipe_minb(int op, int mat, int dim = 3) {
   return (256 / kTile) *
-         (FEM_PIPE_MINB > 0 ? FEM_PIPE_MINB
+         (dim == 2 ? (FEM_PIPE_MINB2D > 0 ? FEM_PIPE_MINB2D : pipe_minb2d(op, mat))
+          : FEM_PIPE_MINB > 0 ? FEM_PIPE_MINB
                             : (op == OP_ENERGY ? 4 : (op == OP_RESIDUAL ? FEM_RES_MINB : op == OP_LIN ? 3
                                 : (op == OP_HVP_LIN ? 3 : (mat == FEM_NEO_HOOKEAN ? 2 : 3)))));
 }
@@ -635,7 +646,7 @@ constexpr bool pipe_decoupled() {
 }
 
 template <int D, int MAT, int OP, bool MASK, bool DET>
-__global__ void __launch_bounds__(kTile, pipe_minb(OP, MAT)) k_tile_pipe(PipeArgs A) {
+__global__ void __launch_bounds__(kTile, pipe_minb(OP, MAT, D)) k_tile_pipe(PipeArgs A) {
   constexpr bool NEED_U = op_needs_u<OP, MAT>();
   constexpr int NF = 1 + (NEED_U ? 1 : 0) + (op_is_hvp<OP>() ? 1 : 0);
   constexpr bool DEC = pipe_decoupled<OP>();
@@ -757,7 +768,7 @@ __global__ void k_slot_gather(const int64_t *node_slot_ptr, const int32_t *node_
 // grid of the persistent kernels: 148 SMs x CTAs/SM of the op (fixed per problem and op,
 // so the energy partial order is deterministic)
 static int pipe_grid(Problem *p, int op, int64_t n = -1) {
-  return (int)std::max<int64_t>(1, std::min<int64_t>(n < 0 ? p->tiles.n_tiles : n, 148 * pipe_minb(op, p->material)));
+  return (int)std::max<int64_t>(1, std::min<int64_t>(n < 0 ? p->tiles.n_tiles : n, 148 * pipe_minb(op, p->material, p->dim)));
 }
 
 template <int D, int MAT, int OP, bool MASK, bool DET>

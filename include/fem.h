@@ -189,8 +189,7 @@ fem_status fem_color(fem_problem *p, int32_t *colors, int32_t *n_colors, fem_str
  *   FEM_ASSEMBLE_SCATTER: not Alg. 2 but the assembly the paper compares it with (Fig. 4
  *            right): dense element Hessians scatter-added into vals with fp64
  *            atomics (run-to-run rounding differences of the atomic order);
- *   default (no mode flag): FEM_ASSEMBLE_ROWS, except FEM_ASSEMBLE_JCOMP for 2D problems
- *            with MPC multipliers.
+ *   default (no mode flag): FEM_ASSEMBLE_ROWS.
  * flags may add FEM_APPLY_BC.  Builds the pattern and (for the Alg. 2 modes) the coloring if
  * needed; synchronizes `stream` only on that first setup. */
 fem_status fem_assemble_csr(fem_problem *p, const double *z, double *vals, unsigned flags,

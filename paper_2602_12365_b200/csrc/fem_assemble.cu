@@ -683,15 +683,22 @@ static fem_status assemble(Problem *p, const double *z, double *vals, unsigned f
     FEM_LAUNCH_CHECK("scatter-add assembly");
     return FEM_OK;
   }
-  // default: the fused node-tile row form (3D, and 2D without multipliers); the one-sweep
-  // J_comp form for 2D problems with MPC multipliers (A/B: profiles/)
+  // default: the row form (node tiles; fallbacks below); explicit mode flags override
   const bool rows = (flags & FEM_ASSEMBLE_ROWS) ||
-                    (!(flags & (FEM_ASSEMBLE_LITERAL | FEM_ASSEMBLE_JCOMP)) &&
-                     (p->dim == 3 || p->n_mpc == 0));
+                    !(flags & (FEM_ASSEMBLE_LITERAL | FEM_ASSEMBLE_JCOMP));
   if (rows) {
     fem_status st0 = build_row_tiles(p, s);
     if (st0) return st0;
-    if (p->rt_state == 1) return launch_row_tiles(p, z, vals, bc, s);
+    if (p->rt_state == 1) {
+      st0 = launch_row_tiles(p, z, vals, bc, s);
+      if (st0) return st0;
+      if (p->n_mpc) {  // the Lagrangian's B^T columns in the u rows and the multiplier rows
+        k_scatter_mpc_cols<<<grid_for(p->n_mpc), kThreads, 0, s>>>(p->mpc_s, p->mpc_m, p->n_mpc, p->n_u, p->dim, bc ? p->node_bc : nullptr, p->row_ptr, p->col_idx, vals);
+        k_rows_mpc<<<grid_for(p->n_mpc), kThreads, 0, s>>>(p->mpc_s, p->mpc_m, p->n_mpc, p->n_u, p->dim, bc ? p->node_bc : nullptr, p->row_ptr, vals);
+        FEM_LAUNCH_CHECK("row tiles: Lagrangian entries");
+      }
+      return FEM_OK;
+    }
     st0 = build_row_plan(p, s);
     if (st0) return st0;
     if (p->rp_state != 1) {

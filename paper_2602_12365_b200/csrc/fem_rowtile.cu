@@ -20,8 +20,10 @@
 // Elements on tile boundaries are evaluated by each tile that touches them (~2x at NT = 32
 // in 3D); in exchange the HBM traffic is the CSR values, the metadata and the node data —
 // no context records.  Atomic-free, fixed order: bitwise reproducible.
-// Eligible meshes: no MPC multiplier columns, <= 16 off-diagonal slots per node, tile sets
-// within the plan's capacity; otherwise the assembly falls back to the row-pull kernels.
+// Eligible meshes: <= 16 off-diagonal slots per node, tile sets within the plan's capacity;
+// otherwise the assembly falls back to the row-pull kernels.  MPC problems: the kernel writes
+// the u-blocks of every row (each row's multiplier columns follow them) and the assembly
+// adds the Lagrangian entries (B^T columns, multiplier rows) with two small kernels.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -231,9 +233,16 @@ __global__ void __launch_bounds__(256) k_rt_plan(const int32_t *node_order, int6
       atomicOr(bad, 1);
       continue;
     }
+    // row i of node n = D * sn u-columns (the node blocks) followed by its multiplier columns
+    // (MPC Lagrangian, indices >= N_u): start = rp0 + i D sn + ex_i, ex_i = multiplier columns
+    // of the node's rows before i (packed in the node word; <= 0xffff)
     const int64_t rp0 = row_ptr[(int64_t)n * D];
-    for (int i = 1; i <= D; ++i)
-      if (row_ptr[(int64_t)n * D + i] != rp0 + (int64_t)i * D * sn) atomicOr(bad, 1);
+    int ex[4] = {0, 0, 0, 0};
+    for (int i = 1; i <= D; ++i) {
+      const int64_t extra = row_ptr[(int64_t)n * D + i] - (rp0 + (int64_t)i * D * sn);
+      if (extra < 0 || extra > 0xffff || (i < D && extra > 0xffff)) atomicOr(bad, 1);
+      ex[i] = (int)extra;
+    }
     uint8_t c[kRtLPNMax + 2];
     for (int q = 0; q <= sno; ++q) c[q] = 0;
     auto q_of = [&](int s) { return s < ds ? s : s - 1; };
@@ -259,7 +268,7 @@ __global__ void __launch_bounds__(256) k_rt_plan(const int32_t *node_order, int6
       }
     }
     const unsigned bcn = node_bc ? node_bc[n] : 0u;
-    ndw[j] = make_int4(n, sno | sn << 8 | ds << 16 | (int)(bcn << 24),
+    ndw[j] = make_int4(ex[1] | (D == 3 ? ex[2] << 16 : 0), sno | sn << 8 | ds << 16 | (int)(bcn << 24),
                        (int)(uint32_t)(rp0 & 0xffffffffu), (int)(rp0 >> 32));
   }
 }
@@ -267,7 +276,7 @@ __global__ void __launch_bounds__(256) k_rt_plan(const int32_t *node_order, int6
 fem_status build_row_tiles(Problem *p, cudaStream_t s) {
   if (p->rt_state) return FEM_OK;
   p->rt_state = -1;
-  if (p->n_mpc || p->n_nodes == 0 || p->n_elems == 0 || getenv("FEM_ROWS_PULL")) return FEM_OK;
+  if (p->n_nodes == 0 || p->n_elems == 0 || getenv("FEM_ROWS_PULL")) return FEM_OK;
   fem_status st = morton_node_order(p, s);
   if (st) return st;
   const int D = p->dim, NEN = D + 1;
@@ -488,6 +497,10 @@ __global__ void __launch_bounds__(kRtThreads, FEM_RT_MINB) k_rows_tile(RtArgs A)
       const int sno = nd.y & 0xff, sn = (nd.y >> 8) & 0xff, ds = (nd.y >> 16) & 0xff;
       const unsigned bcn = A.bc ? ((unsigned)nd.y >> 24) : 0u;
       const int64_t rp0 = (int64_t)(uint32_t)nd.z | ((int64_t)nd.w << 32);
+      // start of row i relative to rp0: i D sn + multiplier columns of the earlier rows
+      auto roff = [&](int i) -> int64_t {
+        return (int64_t)i * D * sn + (i == 0 ? 0 : (i == 1 ? (nd.x & 0xffff) : ((unsigned)nd.x >> 16)));
+      };
       int lo = 0, hi = 0;
       if (ql < sno) {
         lo = m[L.off_so + j * L.ss + ql];
@@ -540,7 +553,7 @@ __global__ void __launch_bounds__(kRtThreads, FEM_RT_MINB) k_rows_tile(RtArgs A)
 #pragma unroll
           for (int i = 0; i < D; ++i)
 #pragma unroll
-            for (int kk = 0; kk < D; ++kk) row[(int64_t)i * D * sn + kk] = acc[i * D + kk];
+            for (int kk = 0; kk < D; ++kk) row[roff(i) + kk] = acc[i * D + kk];
         } else {
 #pragma unroll
           for (int i = 0; i < D; ++i)
@@ -549,7 +562,7 @@ __global__ void __launch_bounds__(kRtThreads, FEM_RT_MINB) k_rows_tile(RtArgs A)
               double v = acc[i * D + kk];
               if ((sbc >> kk) & 1u) v = 0.0;  // masked column
               if ((bcn >> i) & 1u) v = 0.0;   // identity row (off-diagonal)
-              row[(int64_t)i * D * sn + kk] = v;
+              row[roff(i) + kk] = v;
             }
         }
       }
@@ -567,7 +580,7 @@ __global__ void __launch_bounds__(kRtThreads, FEM_RT_MINB) k_rows_tile(RtArgs A)
         v = -v;
         if (bcn & (1u << kk)) v = 0.0;                      // masked column
         if (bcn & (1u << i)) v = (i == kk) ? 1.0 : 0.0;     // identity row
-        A.vals[rp0 + (int64_t)i * D * sn + ds * D + kk] = v;
+        A.vals[rp0 + roff(i) + ds * D + kk] = v;
       }
       __syncwarp();
 #else
@@ -587,7 +600,7 @@ __global__ void __launch_bounds__(kRtThreads, FEM_RT_MINB) k_rows_tile(RtArgs A)
             double v = -acc[q];
             if (bcn & (1u << kk)) v = 0.0;                      // masked column
             if (bcn & (1u << i)) v = (i == kk) ? 1.0 : 0.0;     // identity row
-            A.vals[rp0 + (int64_t)i * D * sn + ds * D + kk] = v;
+            A.vals[rp0 + roff(i) + ds * D + kk] = v;
           }
       }
 #endif

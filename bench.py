@@ -369,6 +369,7 @@ def main():
         return a.elapsed_time(b) / reps
 
     prob.linearize(zt)
+    e1 = torch.empty(1, dtype=torch.float64, device=zt.device)
     ab = {
         "hvp_tiles_ms": time_call(lambda: prob.hvp(zt, vt, bc=True, out=y)),
         "hvp_linearized_ms": time_call(lambda: prob.hvp(zt, vt, bc=True, out=y, flags=fem.LINEARIZED)),
@@ -377,6 +378,10 @@ def main():
             lambda: prob.hvp(zt, vt, bc=True, out=y, flags=fem.BASELINE_SCATTER)),
         "hvp_deterministic_ms": time_call(
             lambda: prob.hvp(zt, vt, bc=True, out=y, flags=fem.DETERMINISTIC)),
+        "energy_plus_residual_ms": time_call(
+            lambda: (prob.energy(zt, out=e1), prob.residual(zt, bc=True, out=r))),
+        "energy_residual_one_pass_ms": time_call(
+            lambda: prob.energy_residual(zt, bc=True, out_energy=e1, out=r)),
         "residual_baseline_scatter_ms": time_call(
             lambda: prob.residual(zt, bc=True, out=r, flags=fem.BASELINE_SCATTER)),
         "assemble_batched_ms": time_call(lambda: prob.assemble_csr(zt, bc=True, mode="batched", out=vals), 2),

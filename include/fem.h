@@ -153,6 +153,13 @@ fem_status fem_energy(fem_problem *p, const double *z, double *energy, fem_strea
 fem_status fem_residual(fem_problem *p, const double *z, double *r, unsigned flags,
                         fem_stream stream);
 
+/* energy and residual in ONE element pass (value and gradient, the jax.value_and_grad
+ * analogue): *energy (device scalar) as fem_energy, r as fem_residual with `flags`.
+ * Multi-GPU problems and the FEM_DETERMINISTIC / FEM_BASELINE_SCATTER modes run the two
+ * calls. */
+fem_status fem_energy_residual(fem_problem *p, const double *z, double *energy, double *r,
+                               unsigned flags, fem_stream stream);
+
 /* y = K(z) v [N] (Eq. 3, §2.1), K the Hessian of the Lagrangian:
  * y_u = K_uu v_u + B^T v_lambda, y_lambda = B v_u; FEM_APPLY_BC: y = P_f K P_f v + P_D v.
  * v and y must not alias. */

@@ -383,6 +383,13 @@ fem_status run_residual(Problem *p, const double *z, double *r, unsigned flags, 
     st = halo_add(p, r, s);
     if (st) return st;
   }
+  return run_residual_terms(p, z, r, flags, s);
+}
+
+// the DOF-wise terms of the residual after the element pass: B^T lambda and g(u) (MPC),
+// -f_ext, the Dirichlet rows
+fem_status run_residual_terms(Problem *p, const double *z, double *r, unsigned flags,
+                              cudaStream_t s) {
   if (p->n_mpc) {
     k_mpc_apply<<<grid_for(p->n_mpc), kThreads, 0, s>>>(z, p->mpc_s, p->mpc_m, p->mpc_b, p->n_mpc,
                                                         p->n_u, p->dim, nullptr, r);
@@ -744,22 +751,10 @@ fem_status fem_apply_dirichlet(fem_problem *h, double *z, fem_stream stream) {
   return FEM_OK;
 }
 
-fem_status fem_energy(fem_problem *h, const double *z, double *energy, fem_stream stream) {
-  FEM_ARG(h && z && energy, "fem_energy: null argument");
-  Problem *p = &h->p;
-  cudaStream_t s = (cudaStream_t)stream;
-  int n = 0;
-  if (p->n_elems) {
-    fem_status st;
-    {
-      st = build_tiles(p, s);
-      if (st) return st;
-      st = tile_pass(p, OP_ENERGY, z, nullptr, nullptr, false, false, p->tiles.epart, s);
-      k_final_sum<<<1, kThreads, 0, s>>>(p->tiles.epart, tile_energy_partials(p), p->partials);
-      n = 1;
-    }
-    if (st) return st;
-  }
+// energy = sum of n_elem element-energy partials already in p->partials[0..n_elem) (0 or 1
+// here: a single pre-summed value) + lambda . g(u) - f_ext . u, fixed-order final sum
+static fem_status energy_finish(Problem *p, const double *z, double *energy, int n,
+                                cudaStream_t s) {
   if (p->n_mpc) {
     const int g2 = grid_for(p->n_mpc, kThreads, kReduceBlocks);
     k_mpc_energy<<<g2, kThreads, 0, s>>>(z, p->mpc_s, p->mpc_m, p->mpc_b, p->n_mpc, p->n_u,
@@ -774,9 +769,47 @@ fem_status fem_energy(fem_problem *h, const double *z, double *energy, fem_strea
   }
   if (n == 0) FEM_CUDA(cudaMemsetAsync(energy, 0, sizeof(double), s));
   else k_final_sum<<<1, kThreads, 0, s>>>(p->partials, n, energy);
-  FEM_LAUNCH_CHECK("fem_energy");
+  FEM_LAUNCH_CHECK("energy");
   return allreduce(p, energy, 1, s);
-  return FEM_OK;
+}
+
+fem_status fem_energy(fem_problem *h, const double *z, double *energy, fem_stream stream) {
+  FEM_ARG(h && z && energy, "fem_energy: null argument");
+  Problem *p = &h->p;
+  cudaStream_t s = (cudaStream_t)stream;
+  int n = 0;
+  if (p->n_elems) {
+    fem_status st = build_tiles(p, s);
+    if (st) return st;
+    st = tile_pass(p, OP_ENERGY, z, nullptr, nullptr, false, false, p->tiles.epart, s);
+    if (st) return st;
+    k_final_sum<<<1, kThreads, 0, s>>>(p->tiles.epart, tile_energy_partials(p), p->partials);
+    n = 1;
+  }
+  return energy_finish(p, z, energy, n, s);
+}
+
+fem_status fem_energy_residual(fem_problem *h, const double *z, double *energy, double *r,
+                               unsigned flags, fem_stream stream) {
+  FEM_ARG(h && z && energy && r, "fem_energy_residual: null argument");
+  FEM_ARG(z != r, "fem_energy_residual: z and r alias");
+  Problem *p = &h->p;
+  cudaStream_t s = (cudaStream_t)stream;
+  // one element pass on a single GPU with the default scatter; otherwise the two calls
+  if (p->size > 1 || (flags & (FEM_DETERMINISTIC | FEM_BASELINE_SCATTER)) || p->n_elems == 0) {
+    fem_status st = fem_energy(h, z, energy, stream);
+    if (st) return st;
+    return run_residual(p, z, r, flags, s);
+  }
+  fem_status st = build_tiles(p, s);
+  if (st) return st;
+  FEM_CUDA(cudaMemsetAsync(r, 0, sizeof(double) * p->N, s));
+  st = tile_pass(p, OP_RESIDUAL, z, nullptr, r, false, false, p->tiles.epart, s);
+  if (st) return st;
+  k_final_sum<<<1, kThreads, 0, s>>>(p->tiles.epart, tile_energy_partials(p, OP_RESIDUAL), p->partials);
+  st = energy_finish(p, z, energy, 1, s);
+  if (st) return st;
+  return run_residual_terms(p, z, r, flags, s);
 }
 
 fem_status fem_residual(fem_problem *h, const double *z, double *r, unsigned flags,

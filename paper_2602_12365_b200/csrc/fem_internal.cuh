@@ -204,6 +204,7 @@ fem_status launch_dot(Problem *p, const double *a, const double *b, int64_t n, d
 fem_status build_pattern(Problem *p, cudaStream_t s);
 fem_status build_colors(Problem *p, cudaStream_t s);
 fem_status run_residual(Problem *p, const double *z, double *r, unsigned flags, cudaStream_t s);
+fem_status run_residual_terms(Problem *p, const double *z, double *r, unsigned flags, cudaStream_t s);
 fem_status run_hvp(Problem *p, const double *z, const double *v, double *y, unsigned flags,
                    cudaStream_t s);
 fem_status run_spmv(Problem *p, const double *vals, const double *x, double *y, cudaStream_t s);
@@ -216,7 +217,7 @@ fem_status build_tile_lists(Problem *p, cudaStream_t s);
 fem_status halo_begin(Problem *p, const double *y, cudaStream_t s);
 fem_status halo_end(Problem *p, double *y, cudaStream_t s);
 void free_tiles(TileSet &T);
-int tile_energy_partials(Problem *p);
+int tile_energy_partials(Problem *p, int op = OP_ENERGY);
 // per-element tangent context records (k_elem_ctx, fem_assemble.cu): doubles per element
 template <int D>
 constexpr int ctx_stride() { return D == 3 ? 28 : 16; }  // [G_a g_a] a = 0..D, smu sc1 sc2, pad

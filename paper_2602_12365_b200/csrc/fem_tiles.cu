@@ -496,14 +496,20 @@ __device__ __forceinline__ void tile_phase1(const PipeArgs &A, const unsigned ch
         if (ok) eacc += vol * nh_psi<D>(H, s, lam, mu);
       }
     } else if constexpr (OP == OP_RESIDUAL) {
-      // vol P G_a = (P / d!) c_a; P linear in (lambda, mu)
+      // vol P G_a = (P / d!) c_a; P linear in (lambda, mu).  With partials (fem_energy_residual)
+      // the element energy vol psi(H) is accumulated in the same pass (value and gradient).
       const double ls = lam * inv_fact, ms = mu * inv_fact;
+      const double vol = det * inv_fact;
       if constexpr (MAT == FEM_LINEAR_ELASTIC) {
         le_stress<D>(H, ls, ms, S);
+        if (A.partials) eacc += vol * le_psi<D>(H, lam, mu);
       } else {
         NHState<D> s;
         ok = nh_state<D>(H, s);
-        if (ok) nh_stress<D>(s, ls, ms, S);
+        if (ok) {
+          nh_stress<D>(s, ls, ms, S);
+          if (A.partials) eacc += vol * nh_psi<D>(H, s, lam, mu);
+        }
       }
     } else if constexpr (OP == OP_LIN) {
       if constexpr (MAT == FEM_NEO_HOOKEAN) {  // cache F^-T and ln J at this state (SoA)
@@ -739,7 +745,7 @@ __global__ void __launch_bounds__(kTile, pipe_minb(OP, MAT, D)) k_tile_pipe(Pipe
       __syncthreads();
     }
   }
-  if constexpr (OP == OP_ENERGY) {
+  if (OP == OP_ENERGY || (OP == OP_RESIDUAL && A.partials)) {  // uniform over the CTA
     const double tsum = block_sum<kTile>(eacc);
     if (tid == 0) A.partials[blockIdx.x] = tsum;
   }
@@ -853,7 +859,7 @@ fem_status tile_pass(Problem *p, int op, const double *u, const double *v, doubl
   return mask ? launch_pipe_op<OP_HVP, true, false>(p, a, s) : launch_pipe_op<OP_HVP, false, false>(p, a, s);
 }
 
-int tile_energy_partials(Problem *p) { return pipe_grid(p, OP_ENERGY); }
+int tile_energy_partials(Problem *p, int op) { return pipe_grid(p, op); }
 
 __global__ void k_tile_shared(TileSet T, const uint8_t *shared, uint8_t *flag) {
   for (int64_t t = blockIdx.x; t < T.n_tiles; t += gridDim.x) {

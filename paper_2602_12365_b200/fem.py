@@ -37,7 +37,7 @@ STATUS = {0: "OK", 1: "INVALID_ARG", 2: "DEGENERATE_ELEMENT", 3: "INVERTED_ELEME
 
 # every symbol include/fem.h declares (checked by tests/test_abi.py)
 EXPORTS = ("fem_create", "fem_destroy", "fem_query", "fem_check", "fem_apply_dirichlet",
-           "fem_energy", "fem_residual", "fem_hvp", "fem_sparsity", "fem_color",
+           "fem_energy", "fem_residual", "fem_energy_residual", "fem_hvp", "fem_sparsity", "fem_color",
            "fem_assemble_csr", "fem_spmv", "fem_cg_solve", "fem_minres_solve",
            "fem_mean_stress", "fem_linearize", "fem_add_traction", "fem_add_body_force", "fem_get_fext",
            "fem_newton_solve", "fem_vw_create", "fem_vw_destroy", "fem_vw_apply_dirichlet",
@@ -122,6 +122,7 @@ def load_library():
         lib.fem_apply_dirichlet.argtypes = [vp, vp, vp]
         lib.fem_energy.argtypes = [vp, vp, vp, vp]
         lib.fem_residual.argtypes = [vp, vp, vp, C.c_uint, vp]
+        lib.fem_energy_residual.argtypes = [vp, vp, vp, vp, C.c_uint, vp]
         lib.fem_hvp.argtypes = [vp, vp, vp, vp, C.c_uint, vp]
         lib.fem_sparsity.argtypes = [vp, vp, vp, vp]
         lib.fem_color.argtypes = [vp, vp, C.POINTER(C.c_int32), vp]
@@ -279,6 +280,16 @@ class Problem:
         _check(load_library().fem_residual(self._h, _ptr(z), _ptr(out), (APPLY_BC if bc else 0) | flags,
                                            _stream()), "fem_residual")
         return out
+
+    def energy_residual(self, z, bc: bool = False, flags: int = 0, out_energy=None, out=None):
+        """(energy [1], residual [N]) from one element pass (fem_energy_residual)."""
+        z = self._vec(z, "z")
+        e = self._out(out_energy, 1)
+        r = self._out(out)
+        _check(load_library().fem_energy_residual(self._h, _ptr(z), _ptr(e), _ptr(r),
+                                                  (APPLY_BC if bc else 0) | flags, _stream()),
+               "fem_energy_residual")
+        return e, r
 
     def hvp(self, z, v, bc: bool = False, out=None, flags: int = 0) -> torch.Tensor:
         z, v = self._vec(z, "z"), self._vec(v, "v")

@@ -80,6 +80,17 @@ def test_residual(case, bc):
     assert rel(prob.residual(dev(z), bc=bc), ref.residual(z, bc=bc)) <= TOL
 
 
+@pytest.mark.parametrize("flag", [0, "DETERMINISTIC"])
+def test_energy_residual_one_pass(case, fem, flag):
+    """fem_energy_residual (value and gradient from one element pass) against the oracle."""
+    name, mesh, prob, ref, z, v = case
+    f = getattr(fem, flag) if flag else 0
+    e, r = prob.energy_residual(dev(z), bc=True, flags=f)
+    re = ref.energy(z)
+    assert abs(e.item() - re) <= TOL * abs(re)
+    assert rel(r, ref.residual(z, bc=True)) <= TOL
+
+
 @pytest.mark.parametrize("bc", [False, True])
 def test_hvp(case, bc):
     name, mesh, prob, ref, z, v = case

@@ -42,6 +42,11 @@
 #ifndef FEM_RT_UNROLL
 #define FEM_RT_UNROLL 4
 #endif
+// diagnostics only (A/B timing of the two phases; results are wrong when set): 1 = skip the
+// element contexts, 2 = skip the slot sums and stores
+#ifndef FEM_RT_DIAG_SKIP
+#define FEM_RT_DIAG_SKIP 0
+#endif
 #ifndef FEM_RT_MINB
 #define FEM_RT_MINB 2
 #endif
@@ -431,7 +436,7 @@ __global__ void __launch_bounds__(kRtThreads, FEM_RT_MINB) k_rows_tile(RtArgs A)
     const int nn = reinterpret_cast<const int *>(m)[2];
     // ---- 1: element contexts
     const uint16_t *lc = reinterpret_cast<const uint16_t *>(m + L.off_lc);
-    for (int e = tid; e < ue; e += kRtThreads) {
+    for (int e = tid; e < (FEM_RT_DIAG_SKIP == 1 ? 0 : ue); e += kRtThreads) {
       const ushort4 l4 = reinterpret_cast<const ushort4 *>(lc)[e];
       const int li[4] = {l4.x, l4.y, l4.z, l4.w};
       double x[NEN][D], u[NEN][D], G[NEN][D], vol;
@@ -442,7 +447,7 @@ __global__ void __launch_bounds__(kRtThreads, FEM_RT_MINB) k_rows_tile(RtArgs A)
           x[a][i] = xs[li[a] * D + i];
           u[a][i] = us[li[a] * D + i];
         }
-      geometry<D>(x, G, vol);
+      const double det0 = geometry<D>(x, G, vol);
       double lam = A.lam, mu = A.mu;
       if (A.has_phase) {
         const int ph = m[L.off_ph + e];
@@ -458,21 +463,22 @@ __global__ void __launch_bounds__(kRtThreads, FEM_RT_MINB) k_rows_tile(RtArgs A)
 #pragma unroll
           for (int i = 0; i < D; ++i) r[Gm::G0 + a * Gm::GP + i] = G[a][i];
       } else {
-        double H[D][D];
-        field_gradient<D>(u, G, H);
-        NHState<D> st;
-        ok = nh_state<D>(H, st);
-        if (!ok) atomicOr(A.err, ERRW_INVERTED);
-        c1 = mu - lam * st.lnJ;
+        // g_a = F^-T G_a is the shape-function gradient in the deformed configuration, i.e.
+        // the geometry of the element at x + u, and J = det F = det J(x + u) / det J(x): two
+        // independent geometry chains instead of H -> F^-1 -> F^-T G (shorter dependencies)
+        double xc[NEN][D], g[NEN][D], volc;
 #pragma unroll
         for (int a = 0; a < NEN; ++a)
 #pragma unroll
-          for (int i = 0; i < D; ++i) {
-            double g = 0.0;
+          for (int i = 0; i < D; ++i) xc[a][i] = x[a][i] + u[a][i];
+        const double Jd = geometry<D>(xc, g, volc) / det0;
+        ok = Jd > 0.0;
+        if (!ok) atomicOr(A.err, ERRW_INVERTED);
+        c1 = ok ? mu - lam * log(Jd) : 0.0;
 #pragma unroll
-            for (int j = 0; j < D; ++j) g = fma(st.FiT[i][j], G[a][j], g);
-            r[Gm::G0 + a * Gm::GP + i] = ok ? g : 0.0;
-          }
+        for (int a = 0; a < NEN; ++a)
+#pragma unroll
+          for (int i = 0; i < D; ++i) r[Gm::G0 + a * Gm::GP + i] = ok ? g[a][i] : 0.0;
       }
       const double smu = ok ? vol * mu : 0.0;
 #pragma unroll
@@ -492,7 +498,7 @@ __global__ void __launch_bounds__(kRtThreads, FEM_RT_MINB) k_rows_tile(RtArgs A)
     constexpr int NPW = 32 / LPN;
     const int h = lane / LPN, ql = lane % LPN;
     const int4 *ndw = reinterpret_cast<const int4 *>(m + L.off_nd);
-    for (int j = NPW * w + h; j < L.nt; j += NPW * (kRtThreads / 32)) {
+    for (int j = NPW * w + h; j < (FEM_RT_DIAG_SKIP == 2 ? 0 : L.nt); j += NPW * (kRtThreads / 32)) {
       const int4 nd = ndw[j];
       const int sno = nd.y & 0xff, sn = (nd.y >> 8) & 0xff, ds = (nd.y >> 16) & 0xff;
       const unsigned bcn = A.bc ? ((unsigned)nd.y >> 24) : 0u;

@@ -36,6 +36,10 @@
 #define FEM_PHASE2_SPLIT 0
 #endif
 
+#ifndef FEM_HVP_SPATIAL
+#define FEM_HVP_SPATIAL 1
+#endif
+
 namespace fem {
 
 // ------------------------------------------------------------------ setup
@@ -453,6 +457,8 @@ __device__ __forceinline__ void tile_phase1(const PipeArgs &A, const unsigned ch
                                             int64_t t, int tid, double *cb, double &eacc) {
   constexpr int NEN = D + 1;
   constexpr bool NEED_U = op_needs_u<OP, MAT>();
+  // NH HVP in the deformed configuration (FEM_HVP_SPATIAL): see the HVP branch below
+  constexpr bool SPATIAL = FEM_HVP_SPATIAL && OP == OP_HVP && MAT == FEM_NEO_HOOKEAN;
   const int64_t e = t * kTile + tid;
   if (e < A.E) {
     const ushort4 lc4 = reinterpret_cast<const ushort4 *>(m + A.off_lconn)[tid];
@@ -472,18 +478,28 @@ __device__ __forceinline__ void tile_phase1(const PipeArgs &A, const unsigned ch
       mu = A.mu_tab[ph];
     }
     double H[D][D];
+    double cs[D][D], dets = 1.0;  // SPATIAL: cofactor gradients and det J at x + u
     if constexpr (NEED_U) {
       double u[NEN][D];
 #pragma unroll
       for (int a = 0; a < NEN; ++a)
 #pragma unroll
         for (int i = 0; i < D; ++i) u[a][i] = us[lc[a] * D + i];
-      grad_hat<D>(u, c, H);
+      if constexpr (SPATIAL) {
 #pragma unroll
-      for (int i = 0; i < D; ++i)
+        for (int a = 0; a < NEN; ++a)
 #pragma unroll
-        for (int j = 0; j < D; ++j) H[i][j] *= id;
+          for (int i = 0; i < D; ++i) u[a][i] += x[a][i];
+        dets = cof_gradients<D>(u, cs);
+      } else {
+        grad_hat<D>(u, c, H);
+#pragma unroll
+        for (int i = 0; i < D; ++i)
+#pragma unroll
+          for (int j = 0; j < D; ++j) H[i][j] *= id;
+      }
     }
+    double f[NEN][D];  // SPATIAL: the nodal vectors, formed in the HVP branch
     bool ok = true;
     double S[D][D];
     if constexpr (OP == OP_ENERGY) {
@@ -533,7 +549,41 @@ __device__ __forceinline__ void tile_phase1(const PipeArgs &A, const unsigned ch
       grad_hat<D>(v, c, dH);
       const double sc = id * inv_fact;
       const double ls = lam * sc, ms = mu * sc;
-      if constexpr (MAT == FEM_LINEAR_ELASTIC) {
+      if constexpr (SPATIAL) {
+        // g_b = F^-T G_b = cs_b / det J(x+u) are the deformed-configuration gradients, so
+        // A = dH F^-1 = sum_b v_b (x) g_b = Ah / det J(x+u) (Ah = grad_hat(v, cs)),
+        // F^-T dH^T F^-T G_a = A^T g_a and F^-T : dH = tr A.  With J = det J(x+u) / det J(x):
+        //   vol dP G_a = mu/(d! det) dHh c_a + 1/(d! J det J(x+u)) (c1 Ah^T cs_a + lam tr(Ah) cs_a)
+        // for a >= 1 (c1 = mu - lam ln J), and minus their sum for a = 0.  F, F^-1 and H are
+        // never formed; the two geometry chains (x and x + u) are independent.
+        double Ah[D][D];
+        grad_hat<D>(v, cs, Ah);
+        const double Jr = dets * id;
+        ok = Jr > 0.0;
+        const double c1 = mu - lam * log(Jr);
+        const double sr = mu * sc, scur = inv_fact / (Jr * dets);
+        double tr = 0.0;
+#pragma unroll
+        for (int k = 0; k < D; ++k) tr += Ah[k][k];
+        const double ltr = lam * tr;
+#pragma unroll
+        for (int i = 0; i < D; ++i) {
+          double s0 = 0.0;
+#pragma unroll
+          for (int a = 0; a < D; ++a) {
+            double p = 0.0, q = ltr * cs[a][i], w = 0.0;
+#pragma unroll
+            for (int j = 0; j < D; ++j) {
+              p = fma(dH[i][j], c[a][j], p);
+              w = fma(Ah[j][i], cs[a][j], w);
+            }
+            const double fa = fma(sr, p, scur * fma(c1, w, q));
+            f[a + 1][i] = fa;
+            s0 += fa;
+          }
+          f[0][i] = -s0;
+        }
+      } else if constexpr (MAT == FEM_LINEAR_ELASTIC) {
         le_stress<D>(dH, ls, ms, S);
       } else if constexpr (OP == OP_HVP_LIN) {  // F^-T, ln J from fem_linearize's cache
         NHState<D> s;
@@ -551,8 +601,7 @@ __device__ __forceinline__ void tile_phase1(const PipeArgs &A, const unsigned ch
     }
     if (!ok) atomicOr(A.err, ERRW_INVERTED);
     if constexpr (op_has_p2<OP>()) {
-      double f[NEN][D];
-      nodal_from_c<D>(S, c, f);
+      if constexpr (!SPATIAL) nodal_from_c<D>(S, c, f);
 #pragma unroll
       for (int a = 0; a < NEN; ++a)
 #pragma unroll

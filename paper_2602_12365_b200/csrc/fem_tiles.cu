@@ -36,6 +36,9 @@
 #define FEM_PHASE2_SPLIT 0
 #endif
 
+#ifndef FEM_RES_SPATIAL
+#define FEM_RES_SPATIAL 1
+#endif
 #ifndef FEM_HVP_SPATIAL
 #define FEM_HVP_SPATIAL 1
 #endif
@@ -459,6 +462,8 @@ __device__ __forceinline__ void tile_phase1(const PipeArgs &A, const unsigned ch
   constexpr bool NEED_U = op_needs_u<OP, MAT>();
   // NH HVP in the deformed configuration (FEM_HVP_SPATIAL): see the HVP branch below
   constexpr bool SPATIAL = FEM_HVP_SPATIAL && OP == OP_HVP && MAT == FEM_NEO_HOOKEAN;
+  // NH residual with F^-T G_a from the same deformed geometry (FEM_RES_SPATIAL)
+  constexpr bool SPATIAL_R = FEM_RES_SPATIAL && OP == OP_RESIDUAL && MAT == FEM_NEO_HOOKEAN;
   const int64_t e = t * kTile + tid;
   if (e < A.E) {
     const ushort4 lc4 = reinterpret_cast<const ushort4 *>(m + A.off_lconn)[tid];
@@ -485,7 +490,8 @@ __device__ __forceinline__ void tile_phase1(const PipeArgs &A, const unsigned ch
       for (int a = 0; a < NEN; ++a)
 #pragma unroll
         for (int i = 0; i < D; ++i) u[a][i] = us[lc[a] * D + i];
-      if constexpr (SPATIAL) {
+      if constexpr (SPATIAL_R) grad_hat<D>(u, c, H);  // Hh = det H (scaled where used)
+      if constexpr (SPATIAL || SPATIAL_R) {
 #pragma unroll
         for (int a = 0; a < NEN; ++a)
 #pragma unroll
@@ -519,6 +525,38 @@ __device__ __forceinline__ void tile_phase1(const PipeArgs &A, const unsigned ch
       if constexpr (MAT == FEM_LINEAR_ELASTIC) {
         le_stress<D>(H, ls, ms, S);
         if (A.partials) eacc += vol * le_psi<D>(H, lam, mu);
+      } else if constexpr (SPATIAL_R) {
+        // P = mu (F - F^-T) + lam ln J F^-T with F c_a = c_a + Hh c_a / det and
+        // F^-T c_a = det g_a = cs_a / J (g_a: gradients at x + u, J = det J(x+u) / det J(x)):
+        //   vol P G_a = (1/d!) [mu c_a + (mu/det) Hh c_a + ((lam ln J - mu) / J) cs_a], a >= 1
+        const double Jr = dets * id;
+        ok = Jr > 0.0;
+        const double lnJ = log(Jr);
+        const double kc = (lam * lnJ - mu) / Jr * inv_fact, kh = ms * id;
+#pragma unroll
+        for (int i = 0; i < D; ++i) {
+          double s0 = 0.0;
+#pragma unroll
+          for (int a = 0; a < D; ++a) {
+            double p = 0.0;
+#pragma unroll
+            for (int j = 0; j < D; ++j) p = fma(H[i][j], c[a][j], p);
+            const double fa = fma(ms, c[a][i], fma(kh, p, kc * cs[a][i]));
+            f[a + 1][i] = fa;
+            s0 += fa;
+          }
+          f[0][i] = -s0;
+        }
+        if (A.partials && ok) {  // psi from H = Hh / det: F:F - d = 2 tr H + H:H
+          double th = 0.0;
+#pragma unroll
+          for (int i = 0; i < D; ++i) {
+            th += 2.0 * (H[i][i] * id);
+#pragma unroll
+            for (int j = 0; j < D; ++j) th = fma(H[i][j] * id, H[i][j] * id, th);
+          }
+          eacc += vol * (0.5 * mu * (th - 2.0 * lnJ) + 0.5 * lam * lnJ * lnJ);
+        }
       } else {
         NHState<D> s;
         ok = nh_state<D>(H, s);
@@ -601,7 +639,7 @@ __device__ __forceinline__ void tile_phase1(const PipeArgs &A, const unsigned ch
     }
     if (!ok) atomicOr(A.err, ERRW_INVERTED);
     if constexpr (op_has_p2<OP>()) {
-      if constexpr (!SPATIAL) nodal_from_c<D>(S, c, f);
+      if constexpr (!SPATIAL && !SPATIAL_R) nodal_from_c<D>(S, c, f);
 #pragma unroll
       for (int a = 0; a < NEN; ++a)
 #pragma unroll

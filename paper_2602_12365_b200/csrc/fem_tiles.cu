@@ -26,6 +26,9 @@
 #ifndef FEM_PIPE_MINB2D
 #define FEM_PIPE_MINB2D 0
 #endif
+#ifndef FEM_HVP_MINB
+#define FEM_HVP_MINB 2
+#endif
 #ifndef FEM_RES_MINB
 #define FEM_RES_MINB 3
 #endif
@@ -428,7 +431,7 @@ __host__ __device__ constexpr int pipe_minb(int op, int mat, int dim = 3) {
          (dim == 2 ? (FEM_PIPE_MINB2D > 0 ? FEM_PIPE_MINB2D : pipe_minb2d(op, mat))
           : FEM_PIPE_MINB > 0 ? FEM_PIPE_MINB
                             : (op == OP_ENERGY ? 4 : (op == OP_RESIDUAL ? FEM_RES_MINB : op == OP_LIN ? 3
-                                : (op == OP_HVP_LIN ? 3 : (mat == FEM_NEO_HOOKEAN ? 2 : 3)))));
+                                : (op == OP_HVP_LIN ? 3 : (mat == FEM_NEO_HOOKEAN ? FEM_HVP_MINB : 3)))));
 }
 
 struct PipeArgs {

@@ -5,8 +5,9 @@
 // iteration of a persistent grid.  Setup packs per tile one metadata block: the tile's
 // element set (every element incident to a tile node), its halo nodes, the elements'
 // halo-local connectivity, and per tile node its CSR row word, off-diagonal slot offsets,
-// Dirichlet bits and block list (entries (element, a, b) grouped by CSR slot, ascending
-// element order).  Per tile the CTA
+// Dirichlet bits and block list (entries (element, a, b) grouped by CSR slot; by default
+// co-scheduled so that the slot lanes of a node read the same element at the same step, see
+// k_rt_plan).  Per tile the CTA
 //   0. has the block and the halo nodes' coordinates and state copied into shared memory
 //      by cp.async (metadata two tiles ahead, node data one tile ahead);
 //   1. evaluates every tile element's tangent context once into shared memory: spatial
@@ -53,11 +54,18 @@
 #ifndef FEM_RT_RSODD
 #define FEM_RT_RSODD 1
 #endif
+#ifndef FEM_RT_RSPAD
+#define FEM_RT_RSPAD 0
+#endif
 #ifndef FEM_RT_GPAD
 #define FEM_RT_GPAD 0
 #endif
 #ifndef FEM_RT_NT
 #define FEM_RT_NT 16
+#endif
+// co-scheduled block lists (see k_rt_plan): 0 = each slot's run in ascending element order
+#ifndef FEM_RT_SCHED
+#define FEM_RT_SCHED 1
 #endif
 
 namespace fem {
@@ -73,7 +81,7 @@ struct RtGeom {
   static constexpr int NEN = D + 1, BS = D * D, NPAIR = D == 3 ? 6 : 3;
   static constexpr int GP = FEM_RT_GPAD ? ((D + 1) & ~1) : D;     // g_a stride (padded: 16 B)
   static constexpr int G0 = 0, M0 = NEN * GP, S0 = M0 + NPAIR + (NPAIR & 1);  // g | M | sc1 sc2
-  static constexpr int RS = FEM_RT_RSODD ? ((S0 + 2) | 1) : (S0 + 2);  // odd: spreads records over banks
+  static constexpr int RS = (FEM_RT_RSODD ? ((S0 + 2) | 1) : (S0 + 2)) + FEM_RT_RSPAD;  // odd: spreads records over banks
   static constexpr int BP = FEM_RT_BPODD ? (BS | 1) : ((BS + 1) & ~1);  // scratch block pitch
 };
 
@@ -262,6 +270,80 @@ __global__ void __launch_bounds__(256) k_rt_plan(const int32_t *node_order, int6
     for (int q = 0; q < sno; ++q) sb[j * L.ss + q] = node_bc ? node_bc[nadj[a0 + q + (q >= ds)]] : 0;
     uint16_t *ej = en + j * L.es;
     for (int q = 0; q < L.es; ++q) ej[q] = 0;
+    const unsigned bcn = node_bc ? node_bc[n] : 0u;
+    const int4 word = make_int4(ex[1] | (D == 3 ? ex[2] << 16 : 0),
+                                sno | sn << 8 | ds << 16 | (int)(bcn << 24),
+                                (int)(uint32_t)(rp0 & 0xffffffffu), (int)(rp0 >> 32));
+#if FEM_RT_SCHED
+    // Co-scheduling: the slot lanes of a node step through their runs in lock step; an element
+    // incident to the node feeds 3 (2D: 2) slots.  Place each element at one iteration k of
+    // all its slots' runs (first fit over a few deterministic element orders, the shortest
+    // schedule kept), so the lanes reading that element's g_a, sc1, sc2 at step k read the
+    // same shared-memory words (broadcast) instead of NEN-1 random records.  Idle steps point
+    // at the zero record (index uem): exact no-op contributions.  Run q = entries
+    // [q C, (q + 1) C).  Nodes whose schedule does not fit keep the grouped runs below.
+    constexpr int kSchedMaxDeg = 64, kSchedMaxC = 15;
+    int maxrun = 0;
+    for (int q = 0; q < sno; ++q) maxrun = max(maxrun, (int)(c[q + 1] - c[q]));
+    if (deg <= kSchedMaxDeg && maxrun > 0) {
+      uint32_t msk[kSchedMaxDeg];
+      for (int l = 0; l < deg; ++l) {
+        const int32_t pk = inc[i0 + l];
+        const int64_t e = pk / NEN;
+        const int a = pk % NEN;
+        uint32_t mm = 0;
+        for (int k = 1; k < NEN; ++k) mm |= 1u << q_of(slot_of(conn[e * NEN + (a + k) % NEN]));
+        msk[l] = mm;
+      }
+      uint8_t perm[kSchedMaxDeg], it[kSchedMaxDeg];
+      auto attempt = [&](int seed) -> int {  // returns the schedule length (kSchedMaxC + 1: failed)
+        for (int l = 0; l < deg; ++l) perm[l] = (uint8_t)l;
+        uint32_t st = 0x9e3779b9u * (uint32_t)(seed + 1);
+        if (seed)
+          for (int l = deg - 1; l > 0; --l) {  // Fisher-Yates with a fixed LCG
+            st = st * 1664525u + 1013904223u;
+            const int k = (int)((st >> 8) % (uint32_t)(l + 1));
+            const uint8_t tmp = perm[l]; perm[l] = perm[k]; perm[k] = tmp;
+          }
+        uint32_t busy[kSchedMaxC];
+        for (int k = 0; k < kSchedMaxC; ++k) busy[k] = 0;
+        int C = 0;
+        for (int x = 0; x < deg; ++x) {
+          const int l = perm[x];
+          int k = 0;
+          while (k < kSchedMaxC && (busy[k] & msk[l])) ++k;
+          if (k == kSchedMaxC) return kSchedMaxC + 1;
+          busy[k] |= msk[l];
+          it[l] = (uint8_t)k;
+          C = max(C, k + 1);
+        }
+        return C;
+      };
+      int best = kSchedMaxC + 1, bseed = 0;
+      for (int seed = 0; seed < 64 && best > maxrun; ++seed) {
+        const int C = attempt(seed);
+        if (C < best) { best = C; bseed = seed; }
+      }
+      if (best <= kSchedMaxC && sno * best <= L.es && sno * best <= 255) {
+        attempt(bseed);
+        const uint16_t zero = (uint16_t)(L.uem | 0 << 10 | 1 << 12);
+        for (int q = 0; q < sno * best; ++q) ej[q] = zero;
+        for (int l = 0; l < deg; ++l) {
+          const int32_t pk = inc[i0 + l];
+          const int64_t e = pk / NEN;
+          const int a = pk % NEN;
+          const int r = rt_find(elems, ue, (int32_t)e);
+          for (int k = 1; k < NEN; ++k) {
+            const int b = (a + k) % NEN;
+            ej[q_of(slot_of(conn[e * NEN + b])) * best + it[l]] = (uint16_t)(r | a << 10 | b << 12);
+          }
+        }
+        for (int q = 0; q <= sno; ++q) so[j * L.ss + q] = (uint8_t)(q * best);
+        ndw[j] = word;
+        continue;
+      }
+    }
+#endif
     for (int l = 0; l < deg; ++l) {
       const int32_t pk = inc[i0 + l];
       const int64_t e = pk / NEN;
@@ -272,9 +354,7 @@ __global__ void __launch_bounds__(256) k_rt_plan(const int32_t *node_order, int6
         ej[c[q_of(slot_of(conn[e * NEN + b]))]++] = (uint16_t)(r | a << 10 | b << 12);
       }
     }
-    const unsigned bcn = node_bc ? node_bc[n] : 0u;
-    ndw[j] = make_int4(ex[1] | (D == 3 ? ex[2] << 16 : 0), sno | sn << 8 | ds << 16 | (int)(bcn << 24),
-                       (int)(uint32_t)(rp0 & 0xffffffffu), (int)(rp0 >> 32));
+    ndw[j] = word;
   }
 }
 
@@ -302,7 +382,8 @@ fem_status build_row_tiles(Problem *p, cudaStream_t s) {
   const int LPN = (SN - 1 <= 8 && !getenv("FEM_RT_LPN16")) ? 8 : 16;
   const int NT = LPN == 8 ? 32 : kRtNT;
   const int64_t nt = (n + NT - 1) / NT;
-  const int ES = (((NEN - 1) * IS) + 7) & ~7, SS = (LPN + 1 + 3) & ~3;
+  const int ES = std::max((((NEN - 1) * IS) + 7) & ~7, FEM_RT_SCHED ? LPN * (D == 3 ? 7 : 5) : 0),
+            SS = (LPN + 1 + 3) & ~3;
   if (IS == 0 || (NEN - 1) * IS > 255) return FEM_OK;
   int *d_bad = nullptr;
   int32_t *cnt = nullptr;
@@ -330,7 +411,7 @@ fem_status build_row_tiles(Problem *p, cudaStream_t s) {
   const int RS = D == 3 ? RtGeom<3>::RS : RtGeom<2>::RS;
   const int BP = D == 3 ? RtGeom<3>::BP : RtGeom<2>::BP;
   const size_t smem = 3 * (size_t)L.mb + 2 * sizeof(double) * 2 * D * (size_t)unm +
-                      sizeof(double) * (size_t)RS * uem +
+                      sizeof(double) * (size_t)RS * (uem + 1) +
                       (FEM_RT_DIAG_SMEM ? sizeof(double) * (kRtThreads / 32) * 32 * BP : 0);
   if (hbad || uem >= 1024 || smem > 220 * 1024) {
     cudaFree(d_bad); cudaFree(cnt);
@@ -397,7 +478,8 @@ __global__ void __launch_bounds__(kRtThreads, FEM_RT_MINB) k_rows_tile(RtArgs A)
   unsigned char *metab = sm_rt;
   double *nodeb = reinterpret_cast<double *>(sm_rt + 3 * mb);  // [2][2][unm][D]: x | u
   double *rec = nodeb + 2 * 2 * unm * D;                         // [uem][RS]
-  double *scratch = rec + (size_t)L.uem * RS;                    // [8 warps][32][BP]
+  double *scratch = rec + (size_t)(L.uem + 1) * RS;              // [8 warps][32][BP]
+  for (int q = tid; q < RS; q += kRtThreads) rec[(size_t)L.uem * RS + q] = 0.0;  // zero record
   const int64_t G = gridDim.x;
 
   auto issue_meta = [&](int64_t t, unsigned char *dst) {

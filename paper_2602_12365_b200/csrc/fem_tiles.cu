@@ -39,6 +39,9 @@
 #define FEM_PHASE2_SPLIT 0
 #endif
 
+#ifndef FEM_TILE_SCHED
+#define FEM_TILE_SCHED 1
+#endif
 #ifndef FEM_RES_SPATIAL
 #define FEM_RES_SPATIAL 1
 #endif
@@ -382,8 +385,47 @@ __global__ void k_pack_meta(TileSet T, const uint8_t *node_bc, int64_t E) {
       base[T.off_ph + i] = (e0 + i < E) ? T.phase[e0 + i] : 0;
 }
 
+// Phase-2 bank scheduling (FEM_TILE_SCHED): every tile node sums its incident contributions
+// cb[(a D + c) kTile + el] in the order of its incidence list, and the 32 nodes of a warp step
+// through their lists together; the shared-memory bank of a read is el mod 16 (64-bit words).
+// Reorder each list (step by step, greedy: the remaining entry whose bank the warp's other
+// nodes use least at this step) so a step's reads spread over the banks.  Only the (fixed,
+// deterministic) summation order of each node changes.
+__global__ void k_sched_inc(TileSet T) {
+  const int64_t t = blockIdx.x;
+  const int U = T.U[t];
+  const uint16_t *ptr = T.ptr + t * (T.maxe + 1);
+  uint16_t *inc = T.inc + t * T.maxe;
+  for (int g = threadIdx.x; g * 32 < U; g += blockDim.x) {
+    const int r0 = g * 32, r1 = min(U, r0 + 32);
+    int len = 0;
+    for (int r = r0; r < r1; ++r) len = max(len, (int)ptr[r + 1] - (int)ptr[r]);
+    for (int w = 0; w < len; ++w) {
+      int cnt[16];
+      for (int b = 0; b < 16; ++b) cnt[b] = 0;
+      for (int r = r0; r < r1; ++r) {
+        const int lo = ptr[r] + w, hi = ptr[r + 1];
+        if (lo >= hi) continue;
+        int best = lo, bc = 1 << 30;
+        for (int q = lo; q < hi && bc > 0; ++q) {
+          const int c = cnt[(inc[q] >> 2) & 15];
+          if (c < bc) { bc = c; best = q; }
+        }
+        const uint16_t x = inc[best];
+        inc[best] = inc[lo];
+        inc[lo] = x;
+        ++cnt[(x >> 2) & 15];
+      }
+    }
+  }
+}
+
 fem_status pack_tile_meta(Problem *p, cudaStream_t s) {
   TileSet &T = p->tiles;
+  if (FEM_TILE_SCHED) {
+    k_sched_inc<<<(unsigned)T.n_tiles, 8, 0, s>>>(T);
+    FEM_LAUNCH_CHECK("tile incidence scheduling");
+  }
   T.um = round_up(T.max_U > 0 ? T.max_U : 1, 8);
   T.off_nodes = 16;
   T.off_lconn = T.off_nodes + 4 * T.um;

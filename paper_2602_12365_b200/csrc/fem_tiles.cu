@@ -39,6 +39,9 @@
 #define FEM_PHASE2_SPLIT 0
 #endif
 
+#ifndef FEM_ELEM_SCHED
+#define FEM_ELEM_SCHED 0  // A/B: 1 = slower (HVP 0.982 -> 1.013 ms at cfg 3)
+#endif
 #ifndef FEM_TILE_SCHED
 #define FEM_TILE_SCHED 1
 #endif
@@ -204,6 +207,46 @@ __global__ void __launch_bounds__(kTile) k_tile_build(const int32_t *conn, const
   }
 }
 
+// Phase-1 bank scheduling (FEM_ELEM_SCHED): thread tid of a tile reads the D-vectors of its
+// element's nodes at nodal-buffer offsets D lconn[a] (+ i), bank (D lconn[a] + i) mod 16.
+// Reorder the elements inside each tile (greedy, warp by warp: the element among the next
+// kSchedWin unplaced ones whose NEN banks the warp uses least) so a warp's node reads spread
+// over the banks.  The tile's element set, and with it every per-tile structure, is unchanged.
+constexpr int kSchedWin = 32;
+template <int D>
+__global__ void k_sched_elems(const uint16_t *lconn, int32_t *perm, int64_t E, int64_t nt) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= nt) return;
+  const int64_t e0 = t * kTile;
+  const int n = (int)(E - e0 < kTile ? E - e0 : kTile);
+  uint32_t taken[kTile / 32];
+  for (int q = 0; q < kTile / 32; ++q) taken[q] = 0;
+  uint16_t order[kTile];
+  int first = 0;
+  for (int w = 0; w * 32 < n; ++w) {
+    uint8_t cnt[D + 1][16];
+    for (int a = 0; a <= D; ++a)
+      for (int b = 0; b < 16; ++b) cnt[a][b] = 0;
+    for (int l = 0; l < 32 && w * 32 + l < n; ++l) {
+      while ((taken[first >> 5] >> (first & 31)) & 1u) ++first;
+      int best = first, bc = 1 << 30, seen = 0;
+      for (int q = first; q < n && seen < kSchedWin && bc > 0; ++q) {
+        if ((taken[q >> 5] >> (q & 31)) & 1u) continue;
+        ++seen;
+        int c = 0;
+        for (int a = 0; a <= D; ++a) c += cnt[a][(D * lconn[(e0 + q) * 4 + a]) & 15];
+        if (c < bc) { bc = c; best = q; }
+      }
+      taken[best >> 5] |= 1u << (best & 31);
+      for (int a = 0; a <= D; ++a) ++cnt[a][(D * lconn[(e0 + best) * 4 + a]) & 15];
+      order[w * 32 + l] = (uint16_t)best;
+    }
+  }
+  int32_t pv[kTile];
+  for (int q = 0; q < n; ++q) pv[q] = perm[e0 + order[q]];
+  for (int q = 0; q < n; ++q) perm[e0 + q] = pv[q];
+}
+
 __global__ void k_permute_u8(const uint8_t *src, const int32_t *perm, int64_t n, uint8_t *dst) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x)
@@ -289,6 +332,15 @@ fem_status build_tiles(Problem *p, cudaStream_t s) {
   if (D == 3) k_tile_build<3><<<(unsigned)nt, kTile, 0, s>>>(p->conn, T.perm, E, node_cnt, T);
   else k_tile_build<2><<<(unsigned)nt, kTile, 0, s>>>(p->conn, T.perm, E, node_cnt, T);
   FEM_LAUNCH_CHECK("tile build");
+  if (FEM_ELEM_SCHED) {  // reorder inside the tiles, then rebuild the per-tile structures
+    const unsigned g = (unsigned)((nt + 63) / 64);
+    if (D == 3) k_sched_elems<3><<<g, 64, 0, s>>>(T.lconn, T.perm, E, nt);
+    else k_sched_elems<2><<<g, 64, 0, s>>>(T.lconn, T.perm, E, nt);
+    FEM_CUDA(cudaMemsetAsync(T.lconn, 0, sizeof(uint16_t) * nt * kTile * 4, s));
+    if (D == 3) k_tile_build<3><<<(unsigned)nt, kTile, 0, s>>>(p->conn, T.perm, E, node_cnt, T);
+    else k_tile_build<2><<<(unsigned)nt, kTile, 0, s>>>(p->conn, T.perm, E, node_cnt, T);
+    FEM_LAUNCH_CHECK("tile element scheduling");
+  }
   if (p->phase) {
     FEM_CUDA(cudaMalloc(&T.phase, E));
     k_permute_u8<<<grid_for(E), kThreads, 0, s>>>(p->phase, T.perm, E, T.phase);

@@ -137,6 +137,21 @@ __device__ __forceinline__ double cof_gradients(const double (&x)[D + 1][D], dou
   }
 }
 
+// Edge form of the deformed element x + u: node 0 at the origin, node a at
+// (x_a - x_0) + (u_a - u_0).  Differences first: forming x + u would round at the scale of
+// |x| instead of the element size (cofactors of a 1e-3 element off by 1e-13 relative).
+template <int D>
+__device__ __forceinline__ void deformed_edges(const double (&x)[D + 1][D],
+                                               const double (&u)[D + 1][D],
+                                               double (&xd)[D + 1][D]) {
+#pragma unroll
+  for (int i = 0; i < D; ++i) {
+    xd[0][i] = 0.0;
+#pragma unroll
+    for (int a = 1; a < D + 1; ++a) xd[a][i] = (x[a][i] - x[0][i]) + (u[a][i] - u[0][i]);
+  }
+}
+
 // Hh = sum_{a>=1} (u_a - u_0) (x) c_a   (= det * H)
 template <int D>
 __device__ __forceinline__ void grad_hat(const double (&u)[D + 1][D], const double (&c)[D][D],

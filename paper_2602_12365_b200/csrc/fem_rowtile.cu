@@ -549,10 +549,7 @@ __global__ void __launch_bounds__(kRtThreads, FEM_RT_MINB) k_rows_tile(RtArgs A)
         // the geometry of the element at x + u, and J = det F = det J(x + u) / det J(x): two
         // independent geometry chains instead of H -> F^-1 -> F^-T G (shorter dependencies)
         double xc[NEN][D], g[NEN][D], volc;
-#pragma unroll
-        for (int a = 0; a < NEN; ++a)
-#pragma unroll
-          for (int i = 0; i < D; ++i) xc[a][i] = x[a][i] + u[a][i];
+        deformed_edges<D>(x, u, xc);
         const double Jd = geometry<D>(xc, g, volc) / det0;
         ok = Jd > 0.0;
         if (!ok) atomicOr(A.err, ERRW_INVERTED);

@@ -589,11 +589,9 @@ __device__ __forceinline__ void tile_phase1(const PipeArgs &A, const unsigned ch
         for (int i = 0; i < D; ++i) u[a][i] = us[lc[a] * D + i];
       if constexpr (SPATIAL_R) grad_hat<D>(u, c, H);  // Hh = det H (scaled where used)
       if constexpr (SPATIAL || SPATIAL_R) {
-#pragma unroll
-        for (int a = 0; a < NEN; ++a)
-#pragma unroll
-          for (int i = 0; i < D; ++i) u[a][i] += x[a][i];
-        dets = cof_gradients<D>(u, cs);
+        double xd[NEN][D];
+        deformed_edges<D>(x, u, xd);
+        dets = cof_gradients<D>(xd, cs);
       } else {
         grad_hat<D>(u, c, H);
 #pragma unroll

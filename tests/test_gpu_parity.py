@@ -222,6 +222,30 @@ def test_errors(fem):
         p.hvp(z, dev(np.zeros(5)))
 
 
+@pytest.mark.parametrize("dim", [2, 3])
+def test_inverted_element_every_op(fem, dim):
+    """J <= 0 (InvertedElement) is reported by every NH kernel: energy,
+    residual (both forms), the one-pass energy+residual, HVP (tile, deterministic, baseline
+    scatter), linearize and the assembly (every mode)."""
+    mesh = fi.grid_tri3(3, 3) if dim == 2 else fi.grid_tet4(3, 3, 3)
+    mesh = mesh.copy_with(material=fi.NEO_HOOKEAN)
+    p = fem.Problem(mesh)
+    z = np.zeros(mesh.n_total)
+    z[0:dim] = 5.0   # corner node 0 pushed through the opposite faces of its elements: J < 0
+    zt, vt = dev(z), dev(np.ones(mesh.n_total))
+    calls = [lambda: p.energy(zt), lambda: p.residual(zt), lambda: p.energy_residual(zt),
+             lambda: p.hvp(zt, vt), lambda: p.hvp(zt, vt, flags=fem.DETERMINISTIC),
+             lambda: p.hvp(zt, vt, flags=fem.BASELINE_SCATTER), lambda: p.linearize(zt),
+             lambda: p.residual(zt, flags=fem.BASELINE_SCATTER)]
+    calls += [lambda m=m: p.assemble_csr(zt, mode=m) for m in ("rows", "batched", "scatter")]
+    for call in calls:
+        with pytest.raises(fem.FemError) as ei:
+            call()
+            p.check()
+        assert ei.value.status == 3
+    p.check()   # the error word is cleared once reported
+
+
 # ------------------------------------------------------------------ full BASELINE sizes
 
 def sampled_rows(n, k, seed):

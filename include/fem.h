@@ -213,7 +213,7 @@ typedef struct {
   int op;           /* 0: masked HVP at z (matrix-free); 1: CSR `vals` (SpMV)       */
   double rtol, atol;/* stop when ||r||_2 <= max(rtol ||b||_2, atol)                        */
   int max_iter;
-  int jacobi;       /* 1: Jacobi preconditioner (op 1 only)                                */
+  int jacobi;       /* 1: Jacobi, 2: node-block (D x D) Jacobi (op 1 only; 2: one GPU)    */
   int check_every;  /* read the residual norm on the host every k iterations (>= 1)        */
   unsigned hvp_flags; /* op 0: extra fem_hvp flags (FEM_LINEARIZED)                         */
 } fem_cg_opts;

@@ -112,6 +112,88 @@ __global__ void k_invert(double *d, int64_t N, int *err) {
   }
 }
 
+// Block Jacobi (jacobi = 2): the D x D diagonal block of every node from the CSR values (its
+// columns are contiguous in each of the node's rows: entry (nD+i, nD+k) sits at
+// diag_pos[nD+i] + k - i), inverted in closed form.  Dirichlet rows are identity rows with
+// zero off-diagonal columns, so their blocks stay invertible.
+template <int D>
+__global__ void k_block_jacobi(const double *vals, const int64_t *diag_pos, int64_t n_nodes,
+                               double *binv, int *err) {
+  for (int64_t nd = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; nd < n_nodes;
+       nd += (int64_t)gridDim.x * blockDim.x) {
+    double B[D][D];
+#pragma unroll
+    for (int i = 0; i < D; ++i) {
+      const int64_t q = diag_pos[nd * D + i];
+#pragma unroll
+      for (int k = 0; k < D; ++k) B[i][k] = vals[q + k - i];
+    }
+    double C[D][D], det;
+    if constexpr (D == 2) {
+      C[0][0] = B[1][1]; C[0][1] = -B[0][1]; C[1][0] = -B[1][0]; C[1][1] = B[0][0];
+      det = B[0][0] * B[1][1] - B[0][1] * B[1][0];
+    } else {  // adjugate: C = adj(B), B^-1 = C / det
+      C[0][0] = B[1][1] * B[2][2] - B[1][2] * B[2][1];
+      C[0][1] = B[0][2] * B[2][1] - B[0][1] * B[2][2];
+      C[0][2] = B[0][1] * B[1][2] - B[0][2] * B[1][1];
+      C[1][0] = B[1][2] * B[2][0] - B[1][0] * B[2][2];
+      C[1][1] = B[0][0] * B[2][2] - B[0][2] * B[2][0];
+      C[1][2] = B[0][2] * B[1][0] - B[0][0] * B[1][2];
+      C[2][0] = B[1][0] * B[2][1] - B[1][1] * B[2][0];
+      C[2][1] = B[0][1] * B[2][0] - B[0][0] * B[2][1];
+      C[2][2] = B[0][0] * B[1][1] - B[0][1] * B[1][0];
+      det = B[0][0] * C[0][0] + B[0][1] * C[1][0] + B[0][2] * C[2][0];
+    }
+    if (!(det > 0.0)) atomicOr(err, ERRW_NONFINITE);  // SPD blocks have det > 0
+    const double id = 1.0 / det;
+#pragma unroll
+    for (int i = 0; i < D; ++i)
+#pragma unroll
+      for (int k = 0; k < D; ++k) binv[(nd * D + i) * D + k] = C[i][k] * id;
+  }
+}
+
+// block-preconditioned CG steps (one thread per node): z = B^-1 r per node, partial r.r, r.z;
+// start: p = z; update: x += alpha p, r -= alpha Ap first
+template <int D, bool START>
+__global__ void k_cg_block(const double *scal, int rz_slot, double *x, double *r, double *zv,
+                           double *p, const double *Ap, const double *binv, int64_t n_nodes,
+                           double *part_rr, double *part_rz) {
+  const double alpha = START ? 0.0 : scal[rz_slot] / scal[S_PAP];
+  double rr = 0.0, rz = 0.0;
+  for (int64_t nd = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; nd < n_nodes;
+       nd += (int64_t)gridDim.x * blockDim.x) {
+    double rv[D];
+#pragma unroll
+    for (int i = 0; i < D; ++i) {
+      const int64_t k = nd * D + i;
+      if constexpr (START) {
+        rv[i] = r[k];
+      } else {
+        x[k] = fma(alpha, p[k], x[k]);
+        rv[i] = fma(-alpha, Ap[k], r[k]);
+        r[k] = rv[i];
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < D; ++i) {
+      double zi = 0.0;
+#pragma unroll
+      for (int k = 0; k < D; ++k) zi = fma(binv[(nd * D + i) * D + k], rv[k], zi);
+      zv[nd * D + i] = zi;
+      if constexpr (START) p[nd * D + i] = zi;
+      rr = fma(rv[i], rv[i], rr);
+      rz = fma(rv[i], zi, rz);
+    }
+  }
+  const double a = block_sum<kThreads>(rr);
+  const double b = block_sum<kThreads>(rz);
+  if (threadIdx.x == 0) {
+    part_rr[blockIdx.x] = a;
+    part_rz[blockIdx.x] = b;
+  }
+}
+
 __global__ void k_neg_copy(const double *a, double *b, int64_t n) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x)
@@ -139,15 +221,21 @@ static fem_status read_scalars(Problem *p, int n, cudaStream_t s) {
 fem_status run_cg(Problem *p, const double *z, const double *vals, const double *b, double *x,
                   const fem_cg_opts *o, fem_cg_report *rep, cudaStream_t s) {
   const int64_t n = p->N;
-  const bool jac = o->jacobi != 0;
+  const bool jac = o->jacobi != 0, blk = o->jacobi == 2;
   const int every = o->check_every > 0 ? o->check_every : 1;
-  fem_status st = ensure(p->cgbuf, sizeof(double) * n * (jac ? 5 : 3));
+  const int D = p->dim;
+  fem_status st = ensure(p->cgbuf, sizeof(double) * n * (jac ? (blk ? 4 + D : 5) : 3));
   if (st) return st;
   double *r = (double *)p->cgbuf.ptr, *pp = r + n, *Ap = pp + n;
   double *zv = jac ? Ap + n : r, *dinv = jac ? Ap + 2 * n : nullptr;
   const int nb = grid_for(n, kThreads, kReduceBlocks);
   double *part_a = p->partials, *part_b = p->partials + kReduceBlocks;
-  if (jac) {  // multi-GPU: interface rows of the local CSR hold partial sums -> halo add
+  const int64_t nn = p->n_nodes;
+  const int nbb = grid_for(nn, kThreads, kReduceBlocks);
+  if (blk) {
+    if (D == 3) k_block_jacobi<3><<<grid_for(nn), kThreads, 0, s>>>(vals, p->diag_pos, nn, dinv, p->d_err);
+    else k_block_jacobi<2><<<grid_for(nn), kThreads, 0, s>>>(vals, p->diag_pos, nn, dinv, p->d_err);
+  } else if (jac) {  // multi-GPU: interface rows of the local CSR hold partial sums -> halo add
     k_diag_of<<<grid_for(n), kThreads, 0, s>>>(vals, p->diag_pos, n, dinv);
     if (p->size > 1) {
       st = halo_add(p, dinv, s);
@@ -160,8 +248,13 @@ fem_status run_cg(Problem *p, const double *z, const double *vals, const double 
   if (st) return st;
   k_sub<<<grid_for(n), kThreads, 0, s>>>(b, Ap, r, n);
   const uint8_t *own = p->size > 1 ? p->owned : nullptr;
-  k_cg_start<<<nb, kThreads, 0, s>>>(r, dinv, zv, pp, n, part_a, part_b, own, p->dim);
-  k_final_sum2<<<1, kThreads, 0, s>>>(part_a, part_b, nb, p->scal + S_RR0, p->scal + S_RZ0);
+  if (blk) {
+    if (D == 3) k_cg_block<3, true><<<nbb, kThreads, 0, s>>>(p->scal, 0, x, r, zv, pp, Ap, dinv, nn, part_a, part_b);
+    else k_cg_block<2, true><<<nbb, kThreads, 0, s>>>(p->scal, 0, x, r, zv, pp, Ap, dinv, nn, part_a, part_b);
+  } else {
+    k_cg_start<<<nb, kThreads, 0, s>>>(r, dinv, zv, pp, n, part_a, part_b, own, p->dim);
+  }
+  k_final_sum2<<<1, kThreads, 0, s>>>(part_a, part_b, blk ? nbb : nb, p->scal + S_RR0, p->scal + S_RZ0);
   st = allreduce(p, p->scal + S_RR0, 1, s);
   if (st) return st;
   st = allreduce(p, p->scal + S_RZ0, 1, s);
@@ -187,9 +280,14 @@ fem_status run_cg(Problem *p, const double *z, const double *vals, const double 
     if (sb) return sb;
     sb = launch_dot(p, pp, Ap, n, p->scal + S_PAP, s);
     if (sb) return sb;
-    k_cg_update<<<nb, kThreads, 0, s>>>(p->scal, S_RZ0 + cur, x, r, zv, pp, Ap, dinv, n, part_a,
-                                        part_b, own, p->dim);
-    k_final_sum2<<<1, kThreads, 0, s>>>(part_a, part_b, nb, p->scal + S_RR0 + (cur ^ 1),
+    if (blk) {
+      if (D == 3) k_cg_block<3, false><<<nbb, kThreads, 0, s>>>(p->scal, S_RZ0 + cur, x, r, zv, pp, Ap, dinv, nn, part_a, part_b);
+      else k_cg_block<2, false><<<nbb, kThreads, 0, s>>>(p->scal, S_RZ0 + cur, x, r, zv, pp, Ap, dinv, nn, part_a, part_b);
+    } else {
+      k_cg_update<<<nb, kThreads, 0, s>>>(p->scal, S_RZ0 + cur, x, r, zv, pp, Ap, dinv, n, part_a,
+                                          part_b, own, p->dim);
+    }
+    k_final_sum2<<<1, kThreads, 0, s>>>(part_a, part_b, blk ? nbb : nb, p->scal + S_RR0 + (cur ^ 1),
                                         p->scal + S_RZ0 + (cur ^ 1));
     sb = allreduce(p, p->scal + S_RR0 + (cur ^ 1), 1, s);
     if (sb) return sb;
@@ -468,6 +566,8 @@ fem_status fem_cg_solve(fem_problem *h, const double *z, const double *vals, con
   FEM_ARG(o->op == 1 || z, "fem_cg_solve: op 0 needs z");
   FEM_ARG(o->op == 0 || (vals && h->p.have_pattern), "fem_cg_solve: op 1 needs vals and a pattern");
   FEM_ARG(!o->jacobi || (o->op == 1 && h->p.n_mpc == 0), "fem_cg_solve: Jacobi needs op 1, no MPC");
+  FEM_ARG(o->jacobi >= 0 && o->jacobi <= 2, "fem_cg_solve: jacobi must be 0, 1 or 2");
+  FEM_ARG(o->jacobi != 2 || h->p.size == 1, "fem_cg_solve: block Jacobi is single-GPU");
   return run_cg(&h->p, z, vals, b, x, o, rep, (cudaStream_t)stream);
 }
 

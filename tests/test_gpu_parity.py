@@ -168,6 +168,8 @@ def test_cg_matrix_free_and_csr(case):
     assert info1["converged"] and rel(x1, xr) <= 1e-10
     x2, info2 = prob.cg_solve(dev(b), vals=vals, op=1, rtol=1e-13, jacobi=True)
     assert info2["converged"] and rel(x2, xr) <= 1e-10
+    x3, info3 = prob.cg_solve(dev(b), vals=vals, op=1, rtol=1e-13, jacobi=2)   # node blocks
+    assert info3["converged"] and rel(x3, xr) <= 1e-10
 
 
 def test_newton(case):
@@ -176,8 +178,8 @@ def test_newton(case):
         pytest.skip("Newton parity on the roller / clamped problems")
     z0 = fi.lift(mesh)
     zr, rinfo = ref.newton(z0, cg_rtol=1e-13)
-    for op in (0, 1):
-        zg, info = prob.newton_solve(dev(z0), op=op, cg_rtol=1e-13)
+    for op, jac in ((0, 0), (1, 0), (1, 2)):
+        zg, info = prob.newton_solve(dev(z0), op=op, cg_rtol=1e-13, jacobi=jac)
         assert info["converged"] and rinfo["status"] == 0
         assert rel(zg, zr) <= 1e-10
 

@@ -153,10 +153,12 @@ fem_status fem_energy(fem_problem *p, const double *z, double *energy, fem_strea
 fem_status fem_residual(fem_problem *p, const double *z, double *r, unsigned flags,
                         fem_stream stream);
 
-/* energy and residual in ONE element pass (value and gradient, the jax.value_and_grad
- * analogue): *energy (device scalar) as fem_energy, r as fem_residual with `flags`.
- * Multi-GPU problems and the FEM_DETERMINISTIC / FEM_BASELINE_SCATTER modes run the two
- * calls. */
+/* energy and residual in ONE element pass (value and gradient of Eq. 1-2):
+ * *energy (device scalar, [1]) as fem_energy, r [N] as fem_residual with `flags`; all
+ * pointers device memory owned by the caller; z and r must not alias (FEM_ERR_INVALID_ARG).
+ * Inverted elements set the device error word (FEM_ERR_INVERTED_ELEMENT at the next
+ * fem_check).  Multi-GPU problems and the FEM_DETERMINISTIC / FEM_BASELINE_SCATTER modes
+ * run the two calls. */
 fem_status fem_energy_residual(fem_problem *p, const double *z, double *energy, double *r,
                                unsigned flags, fem_stream stream);
 

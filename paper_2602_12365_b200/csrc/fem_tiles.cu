@@ -453,9 +453,12 @@ __global__ void k_sched_inc(TileSet T) {
     int len = 0;
     for (int r = r0; r < r1; ++r) len = max(len, (int)ptr[r + 1] - (int)ptr[r]);
     for (int w = 0; w < len; ++w) {
+      // a warp's 64-bit shared loads are served per half-warp: banks must differ within each
+      // group of 16 consecutive nodes
       int cnt[16];
-      for (int b = 0; b < 16; ++b) cnt[b] = 0;
       for (int r = r0; r < r1; ++r) {
+        if (((r - r0) & 15) == 0)
+          for (int b = 0; b < 16; ++b) cnt[b] = 0;
         const int lo = ptr[r] + w, hi = ptr[r + 1];
         if (lo >= hi) continue;
         int best = lo, bc = 1 << 30;

@@ -265,10 +265,15 @@ def test_full_size_sampled_parity(fem, oracle_mod, cfg):
     v = fi.random_direction(mesh.n_total, 4)
     rows = sampled_rows(mesh.n_total, 2000, 5)
     zt, vt = dev(z), dev(v)
+    e_ref = ref.energy(z)                      # full-size energy (compensated sum)
+    assert abs(prob.energy(zt).item() - e_ref) <= TOL * abs(e_ref)
     for bc in (False, True):
         r = prob.residual(zt, bc=bc).cpu().numpy()
         rr = ref.residual_rows(z, rows, bc=bc)
         assert np.abs(r[rows] - rr).max() <= TOL * np.abs(r).max()
+        e1, r1 = prob.energy_residual(zt, bc=bc)     # one-pass value and gradient
+        assert abs(e1.item() - e_ref) <= TOL * abs(e_ref)
+        assert np.abs(r1.cpu().numpy()[rows] - rr).max() <= TOL * np.abs(r).max()
         y = prob.hvp(zt, vt, bc=bc).cpu().numpy()
         yr = ref.hvp_rows(z, v, rows, bc=bc)
         assert np.abs(y[rows] - yr).max() <= TOL * np.abs(y).max()

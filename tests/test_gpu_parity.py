@@ -277,6 +277,9 @@ def test_full_size_sampled_parity(fem, oracle_mod, cfg):
         y = prob.hvp(zt, vt, bc=bc).cpu().numpy()
         yr = ref.hvp_rows(z, v, rows, bc=bc)
         assert np.abs(y[rows] - yr).max() <= TOL * np.abs(y).max()
+        for f in (fem.DETERMINISTIC, fem.BASELINE_SCATTER):   # the other element-pass modes
+            yf = prob.hvp(zt, vt, bc=bc, flags=f).cpu().numpy()
+            assert np.abs(yf[rows] - yr).max() <= TOL * np.abs(y).max()
     # tangent and residual patch tests at full size (exact on any P1 mesh)
     dim = mesh.dim
     F = np.diag([1.05] + [0.98] * (dim - 1))

@@ -277,7 +277,8 @@ def test_full_size_sampled_parity(fem, oracle_mod, cfg):
         y = prob.hvp(zt, vt, bc=bc).cpu().numpy()
         yr = ref.hvp_rows(z, v, rows, bc=bc)
         assert np.abs(y[rows] - yr).max() <= TOL * np.abs(y).max()
-        for f in (fem.DETERMINISTIC, fem.BASELINE_SCATTER):   # the other element-pass modes
+        prob.linearize(zt)
+        for f in (fem.DETERMINISTIC, fem.BASELINE_SCATTER, fem.LINEARIZED):  # other HVP modes
             yf = prob.hvp(zt, vt, bc=bc, flags=f).cpu().numpy()
             assert np.abs(yf[rows] - yr).max() <= TOL * np.abs(y).max()
     # tangent and residual patch tests at full size (exact on any P1 mesh)
@@ -299,7 +300,7 @@ def test_full_size_sampled_parity(fem, oracle_mod, cfg):
     srow = sampled_rows(mesh.n_total, 300, 6)
     ref_vals = ref.csr_rows(z, srow, rp_n, ci_n, bc=True)
     idx = np.concatenate([np.arange(rp_n[r], rp_n[r + 1]) for r in srow])
-    for mode in ("rows", "batched"):
+    for mode in ("rows", "batched", "scatter"):
         vals = prob.assemble_csr(zt, bc=True, mode=mode).cpu().numpy()
         assert np.abs(vals[idx] - ref_vals).max() <= TOL * np.abs(vals).max()
         del vals

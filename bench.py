@@ -45,7 +45,11 @@ def parse():
     ap.add_argument("--assemble-mode", default="auto", choices=["auto", "batched", "literal", "rows", "scatter"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-solve", action="store_true")
+    ap.add_argument("--setup-reps", type=int, default=5, help="timed pattern + coloring runs")
     ap.add_argument("--profile-step", action="store_true", help="one step only (for ncu)")
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="weak: one cfg-3-sized z-slab per GPU (N = 1: cfg 3 itself); strong: "
+                         "BASELINE cfg 4 (255x255x256 cells, 50.5M DOFs) cut into N z-slabs")
     return ap.parse_args()
 
 
@@ -153,6 +157,36 @@ def run_reference(args):
         "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}))
 
 
+def scaling_plan(mode: str, world: int, n=None) -> dict:
+    """Global problem and per-rank z-slab of the multi-GPU bench.
+
+    weak:   every rank owns an n x n x n Kuhn block (n = 150: cfg 3 per GPU) stacked in z;
+            the global block is n x n x (n P) cells.
+    strong: BASELINE cfg 4, 255 x 255 x 256 cells (50,528,256 DOFs) whatever P is; rank r
+            owns cells z in [r 256/P, (r+1) 256/P).
+    DOFs = 3 (nx+1)(ny+1)(nz+1); elements = 6 nx ny nz."""
+    if mode == "strong":
+        nx = ny = 255 if n is None else n
+        nz_total = 256 if n is None else n + 1
+        if nz_total % world:
+            raise SystemExit(f"strong scaling: {nz_total} z-cells do not split into {world} slabs")
+        nzr = nz_total // world
+        name = (f"strong scaling: BASELINE cfg4 3D NH block {nx}x{ny}x{nz_total} Kuhn-Tet4 cells "
+                f"split into {world} z-slabs of {nzr} cells, perturbed a=0.1, roller eps=0.05, "
+                f"NCCL halo add")
+        seed = 14
+    else:
+        nx = ny = nzr = 150 if n is None else n
+        nz_total = nzr * world
+        name = (f"weak scaling: {world} z-slabs of {nx}^3 Kuhn-Tet4 cells (cfg 3 per GPU), "
+                f"3D NH, perturbed a=0.1, roller eps=0.05, NCCL halo add")
+        seed = 13
+    nodes = (nx + 1) * (ny + 1) * (nz_total + 1)
+    return {"mode": mode, "nx": nx, "ny": ny, "nz_total": nz_total, "nz_per_rank": nzr,
+            "n_global_nodes": nodes, "n_global_dofs": 3 * nodes,
+            "n_global_elems": 6 * nx * ny * nz_total, "workload": name, "seed": seed}
+
+
 def workload_name(cfg):
     return {3: "BASELINE cfg3: 3D compressible neo-Hookean block, 150^3 Kuhn-Tet4 cells, "
                "10,328,853 DOFs, perturbed a=0.1, roller eps=0.05",
@@ -206,39 +240,46 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"WORLD_SIZE={world} but --gpus {args.gpus}: launch N > 1 under "
+                         f"torch.distributed.run with --nproc-per-node N")
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     fbuild.build()
 
     comm = None
-    if world > 1:
-        # weak scaling: every rank owns one cfg-3-sized z-slab of a 150 x 150 x (150 N) block
-        # (N = 1 reproduces cfg 3 exactly); one halo add per residual / HVP / SpMV over NCCL
+    plan = scaling_plan(args.scaling, world, args.n)
+    if args.scaling == "strong" or world > 1:
+        # element partition into z-slabs: weak = one cfg-3-sized slab per rank,
+        # strong = BASELINE cfg 4 (255 x 255 x 256 cells) cut into slabs of 256/P cells.
+        # One halo add per residual / HVP / SpMV over NCCL; states drawn per global node so
+        # shared DOFs agree on every rank and every P computes the same global problem.
         from paper_2602_12365_b200 import dist as fd
         if args.config != 3:
-            raise SystemExit("multi-GPU bench runs the 3D cfg-3 slabs")
-        k = args.n or 150
-        mesh, gids = fd.slab_mesh(k, k, k, world, rank, perturb_a=0.1)
-        all_ids = [None] * world
-        dist.all_gather_object(all_ids, gids)
-        plan = fd.halo_plan(all_ids, rank)
-        del all_ids
-        uid = [fem.nccl_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(uid, src=0)
-        comm = fem.nccl_comm_init(uid[0], rank, world)
-        # states drawn per global node so shared DOFs agree on every rank
-        h = 1.0 / (k * world)
-        n_glob_nodes = (k + 1) * (k + 1) * (k * world + 1)
-        gz = np.random.default_rng(5).uniform(-0.01 * h, 0.01 * h, size=(n_glob_nodes, 3))
-        gv = np.random.default_rng(4).uniform(-1, 1, size=(n_glob_nodes, 3))
+            raise SystemExit("multi-GPU bench runs the 3D Kuhn slabs (cfg 3 weak / cfg 4 strong)")
+        mesh, gids = fd.slab_mesh(plan["nx"], plan["ny"], plan["nz_per_rank"], world, rank,
+                                  perturb_a=0.1, seed=plan["seed"])
+        hplan = None
+        if world > 1:
+            all_ids = [None] * world
+            dist.all_gather_object(all_ids, gids)
+            hplan = fd.halo_plan(all_ids, rank)
+            del all_ids
+            uid = [fem.nccl_unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(uid, src=0)
+            comm = fem.nccl_comm_init(uid[0], rank, world)
+            plan["nccl_comm_count"] = fem.nccl_comm_count(comm)
+            assert plan["nccl_comm_count"] == world
+        h = 1.0 / max(plan["nx"], plan["ny"], plan["nz_total"])
+        gz = np.random.default_rng(5).uniform(-0.01 * h, 0.01 * h, size=(plan["n_global_nodes"], 3))
+        gv = np.random.default_rng(4).uniform(-1, 1, size=(plan["n_global_nodes"], 3))
         z = fi.lift(mesh, (fi.affine_field(mesh, np.diag([0.05, 0.0, 0.0])).reshape(-1, 3)
                            + gz[gids]).ravel())
         v = gv[gids].ravel()
         del gz, gv
-        wname = (f"weak scaling: {world} z-slabs of 150^3 Kuhn-Tet4 cells (cfg 3 per GPU), "
-                 f"3D NH, perturbed a=0.1, roller eps=0.05, NCCL halo add")
-        prob = fem.Problem(mesh, plan=plan, nccl_comm=comm)
+        wname = plan["workload"]
+        prob = fem.Problem(mesh, plan=hplan, nccl_comm=comm)
     else:
         mesh, wname, z, v = workload(args.config, args.n)
         prob = fem.Problem(mesh)
@@ -267,22 +308,30 @@ def main():
     colors, C = prob.color()
     e2.record()
     torch.cuda.synchronize()
-    setup = {"pattern_ms": e0.elapsed_time(e1), "coloring_ms": e1.elapsed_time(e2),
-             "nnz": nnz, "n_colors": C,
-             "note": "first problem on the device: includes the first-touch cost of the "
-                     "multi-GB pattern allocations; *_warm = a second problem on the same mesh"}
-    if world == 1:  # steady-state setup: the same mesh again, fresh problem
-        p2 = fem.Problem(mesh)
-        torch.cuda.synchronize()
-        e0.record()
-        p2.nnz()
-        e1.record()
-        p2.color()
-        e2.record()
-        torch.cuda.synchronize()
-        setup["pattern_ms_warm"] = e0.elapsed_time(e1)
-        setup["coloring_ms_warm"] = e1.elapsed_time(e2)
-        del p2
+    setup = {"pattern_ms_first": e0.elapsed_time(e1), "coloring_ms_first": e1.elapsed_time(e2),
+             "nnz": nnz, "n_colors": C}
+    if world == 1:
+        # 3 warm-up runs, then the median of >= 5; each run is a fresh problem
+        # on the same mesh (the pattern and colors are per problem), timed with CUDA events
+        samples = {"pattern_ms": [], "coloring_ms": []}
+        for rep in range(3 + args.setup_reps):
+            p2 = fem.Problem(mesh)
+            torch.cuda.synchronize()
+            e0.record()
+            p2.nnz()
+            e1.record()
+            p2.color()
+            e2.record()
+            torch.cuda.synchronize()
+            if rep >= 3:
+                samples["pattern_ms"].append(e0.elapsed_time(e1))
+                samples["coloring_ms"].append(e1.elapsed_time(e2))
+            del p2
+        for key, xs in samples.items():
+            setup[key] = float(np.median(xs))
+            setup[key + "_samples"] = xs
+        setup["note"] = ("*_first: the bench problem's own first call (first touch of the "
+                         "multi-GB allocations); median of fresh problems after 3 warm-ups")
 
     energy = torch.empty(1, dtype=torch.float64, device="cuda")
     r = torch.empty(N, dtype=torch.float64, device="cuda")
@@ -334,8 +383,8 @@ def main():
     torch.cuda.synchronize()
     t_start, t_end = ev(), ev()
     t_start.record(stream)
-    for k in range(args.steps):
-        step(events[k])
+    for it in range(args.steps):
+        step(events[it])
     t_end.record(stream)
     torch.cuda.synchronize()
     if world > 1:
@@ -344,7 +393,7 @@ def main():
     clk = clocks.stop()
     prob.check()
     total_ms = t_start.elapsed_time(t_end)
-    per = {ph: sum(events[k][i].elapsed_time(events[k][i + 1]) for k in range(args.steps))
+    per = {ph: sum(events[it][i].elapsed_time(events[it][i + 1]) for it in range(args.steps))
            for i, ph in enumerate(phases)}
     if world > 1:
         t = torch.tensor([total_ms] + [per[p] for p in phases], dtype=torch.float64, device="cuda")
@@ -352,7 +401,7 @@ def main():
         total_ms = float(t[0])
         per = {p: float(t[i + 1]) for i, p in enumerate(phases)}
     K = args.steps
-    n_global = N if world == 1 else 3 * (k + 1) * (k + 1) * (k * world + 1)
+    n_global = plan["n_global_dofs"] if (world > 1 or args.scaling == "strong") else N
     hvp_ms = per["hvp"] / K
     value = n_global / (hvp_ms * 1e-3) / 1e9
 
@@ -453,8 +502,16 @@ def main():
     b.record(stream)
     torch.cuda.synchronize()
     e2e_ms = a.elapsed_time(b) / K
+    n_local_sum = N
+    if world > 1:  # max over ranks of the device time; bytes summed over ranks
+        t = torch.tensor([e2e_ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t[0])
+        t = torch.tensor([N], dtype=torch.int64, device="cuda")
+        dist.all_reduce(t)
+        n_local_sum = int(t[0])
     e2e = {"value": n_global / (e2e_ms * 1e-3) / 1e9, "unit": UNIT,
-           "h2d_bytes_per_step": 2 * 8 * N, "d2h_bytes_per_step": 8 * N,
+           "h2d_bytes_per_step": 2 * 8 * n_local_sum, "d2h_bytes_per_step": 8 * n_local_sum,
            "what": "fem_hvp with pinned-host z, v copied in and y copied out every step; "
                    "steps pipelined over 2 buffer sets (H2D / compute / D2H streams)"}
 
@@ -545,16 +602,21 @@ def main():
             solve["newton_csr_vs_hvp_maxdiff"] = float((zc - zs).abs().max())
 
     cpu = None
-    if not args.no_cpu_baseline and rank == 0:
+    if not args.no_cpu_baseline and rank == 0 and world == 1:
         cpu = oracle_hvp_sample(args.config)
 
     out = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
         "warmup": args.warmup, "ms_per_step": total_ms / K, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": wname if args.n else workload_name(args.config),
-                   "n_dofs": n_global, "n_elems": mesh.n_elems * world, "nnz": nnz, "n_colors": C,
-                   "assemble_mode": mode, "parallelism": f"element partition x{world}",
+        "scaling": args.scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": wname if (args.n or world > 1 or args.scaling == "strong")
+                   else workload_name(args.config),
+                   "n_dofs": n_global,
+                   "n_elems": plan["n_global_elems"] if (world > 1 or args.scaling == "strong")
+                   else mesh.n_elems,
+                   "nnz": nnz, "n_colors": C,  # rank 0's local CSR when P > 1
+                   "assemble_mode": mode, "parallelism": f"element partition x{world} (z-slabs)",
+                   "nccl_comm_count": plan.get("nccl_comm_count"),
                    "l2": f"inputs larger than L2 (126 MB): the HVP moves {alg['hvp']['bytes'] / 1e9:.2f} GB per call (algorithmic)"},
         "assembly_ms": per["assemble"] / K,
         "residual_gdofs": n_global / (per["residual"] / K * 1e-3) / 1e9,

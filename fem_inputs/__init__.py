@@ -132,6 +132,41 @@ def delaunay_tri3(n_interior: int, n_side: int, seed: int, length: float = 1.0) 
     return Mesh(dim=2, coords=coords, conn=np.ascontiguousarray(conn), length=length)
 
 
+def delaunay_tet4(n_interior: int, n_side: int, seed: int, length: float = 1.0) -> Mesh:
+    """Unstructured Tet4 mesh of [0,L]^3 (the "general 3D mesh" of PAPER.md App. A):
+    Delaunay tetrahedralization (scipy.spatial / qhull) of n_interior seeded uniform points in
+    the open cube plus the (n_side+1)^3 - (n_side-1)^3 nodes of a regular grid on its surface
+    (so each boundary plane is exactly a coordinate plane: the roller BCs of C15 apply), every
+    tet oriented to det J > 0.  Node degrees vary (interior ~ 13-40 neighbours), unlike the
+    Kuhn meshes' uniform 14: the high-degree gather, fallback and capacity paths run."""
+    from scipy.spatial import Delaunay
+    rng = np.random.default_rng(seed)
+    h = length / n_side
+    t = np.linspace(0.0, length, n_side + 1)
+    Z, Y, X = np.meshgrid(t, t, t, indexing="ij")
+    grid = np.stack([X.ravel(), Y.ravel(), Z.ravel()], axis=1)
+    on = ((grid == 0.0) | (grid == length)).any(axis=1)
+    inner = rng.uniform(0.5 * h, length - 0.5 * h, size=(n_interior, 3))
+    coords = np.ascontiguousarray(np.concatenate([grid[on], inner]), np.float64)
+    conn = Delaunay(coords).simplices.astype(np.int32)
+    X = coords[conn]
+    e = X[:, 1:, :] - X[:, :1, :]
+    det = np.linalg.det(e)
+    # qhull may emit (near-)flat tets spanned by four coplanar surface nodes: drop them (their
+    # volume is zero, so the rest still tiles the cube; the test suite checks sum vol = L^3)
+    keep = np.abs(det) > 1e-10 * h ** 3
+    conn, det = conn[keep], det[keep]
+    flip = det < 0
+    conn[flip, 2], conn[flip, 3] = conn[flip, 3].copy(), conn[flip, 2].copy()
+    used = np.unique(conn)
+    if len(used) != len(coords):      # drop nodes only flat tets touched (none in practice)
+        remap = np.full(len(coords), -1, np.int64)
+        remap[used] = np.arange(len(used))
+        coords, conn = coords[used], remap[conn].astype(np.int32)
+    return Mesh(dim=3, coords=np.ascontiguousarray(coords), conn=np.ascontiguousarray(conn),
+                length=length)
+
+
 def grid_tet4(nx: int, ny: int, nz: int, length: float = 1.0, z0: int = 0,
               nz_total: Optional[int] = None) -> Mesh:
     """Structured Kuhn Tet4 mesh (C6) of the box [0,L]x[0,L]x[0,L*nz_total/nz_total].
@@ -355,7 +390,7 @@ def config_mesh(cfg: int, n: Optional[int] = None, perturbed: bool = True) -> Me
     """BASELINE.json configs as concrete synthetic meshes.
 
     cfg 1: 2D LE 8x8 unit square; cfg 2: 2D NH 706^2 plate (roller eps=0.1);
-    cfg 3: 3D NH 150^3 Kuhn block (roller eps=0.05); cfg 4: 3D NH 255x255x256;
+    cfg 3: 3D NH 150^3 Kuhn block (roller eps=0.05); cfg 4: 3D NH 255x255x256 (seed 14);
     cfg 5: 2D LE n^2 with periodic MPC.  `n` overrides the size.
     """
     if cfg == 1:
@@ -375,8 +410,10 @@ def config_mesh(cfg: int, n: Optional[int] = None, perturbed: bool = True) -> Me
         if perturbed:
             m = perturb(m, 0.1, seed=13)
         return roller_bc(m.copy_with(material=NEO_HOOKEAN), eps=0.05)
-    if cfg == 4:
-        m = grid_tet4(255, 255, 256) if n is None else grid_tet4(n, n, n)
+    if cfg == 4:  # n x n x (n + 1) cells, like 255 x 255 x 256 (z-slabs of 256 / P, §8(e))
+        m = grid_tet4(255, 255, 256) if n is None else grid_tet4(n, n, n + 1)
+        if perturbed:
+            m = perturb(m, 0.1, seed=14)
         return roller_bc(m.copy_with(material=NEO_HOOKEAN), eps=0.05)
     if cfg == 5:
         k = 70 if n is None else n

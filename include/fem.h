@@ -335,6 +335,8 @@ fem_status fem_vw_gmres_solve(fem_vw_problem *p, const double *b, double *x,
 fem_status fem_nccl_unique_id(unsigned char id[128]);
 fem_status fem_nccl_comm_init(const unsigned char id[128], int rank, int size, void **comm);
 fem_status fem_nccl_comm_destroy(void *comm);
+/* (host) number of ranks in the communicator (ncclCommCount); bench.py logs it. */
+fem_status fem_nccl_comm_count(void *comm, int *count);
 
 /* (host) n = 1 / 2 scalar all-reduce (sum) of a device buffer over the problem's ranks
  * (no-op on a single GPU); used for global dots in multi-GPU CG and the energy. */

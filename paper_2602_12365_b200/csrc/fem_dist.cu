@@ -219,6 +219,11 @@ fem_status fem_nccl_comm_init(const unsigned char id[128], int rank, int size, v
   return FEM_OK;
 }
 
+fem_status fem_nccl_comm_count(void *comm, int *count) {
+  FEM_ARG(comm && count, "fem_nccl_comm_count: null argument");
+  return nccl_status(ncclCommCount((ncclComm_t)comm, count), "ncclCommCount");
+}
+
 fem_status fem_nccl_comm_destroy(void *comm) {
   if (!comm) return FEM_OK;
   return nccl_status(ncclCommDestroy((ncclComm_t)comm), "ncclCommDestroy");

@@ -42,7 +42,7 @@ EXPORTS = ("fem_create", "fem_destroy", "fem_query", "fem_check", "fem_apply_dir
            "fem_mean_stress", "fem_linearize", "fem_add_traction", "fem_add_body_force", "fem_get_fext",
            "fem_newton_solve", "fem_vw_create", "fem_vw_destroy", "fem_vw_apply_dirichlet",
            "fem_vw_residual", "fem_vw_jvp", "fem_vw_gmres_solve",
-           "fem_nccl_unique_id", "fem_nccl_comm_init", "fem_nccl_comm_destroy",
+           "fem_nccl_unique_id", "fem_nccl_comm_init", "fem_nccl_comm_destroy", "fem_nccl_comm_count",
            "fem_allreduce_sum", "fem_halo_size", "fem_halo_pack", "fem_halo_combine",
            "fem_last_error", "fem_version")
 
@@ -145,6 +145,7 @@ def load_library():
         lib.fem_nccl_unique_id.argtypes = [C.c_char_p]
         lib.fem_nccl_comm_init.argtypes = [C.c_char_p, C.c_int, C.c_int, C.POINTER(vp)]
         lib.fem_nccl_comm_destroy.argtypes = [vp]
+        lib.fem_nccl_comm_count.argtypes = [vp, C.POINTER(C.c_int)]
         lib.fem_allreduce_sum.argtypes = [vp, vp, C.c_int, vp]
         lib.fem_halo_size.argtypes = [vp, i64p]
         lib.fem_halo_pack.argtypes = [vp, vp, vp, vp]
@@ -442,6 +443,12 @@ def nccl_comm_init(uid: bytes, rank: int, size: int):
     _check(load_library().fem_nccl_comm_init(C.create_string_buffer(uid, 128), rank, size,
                                              C.byref(comm)), "fem_nccl_comm_init")
     return comm.value
+
+
+def nccl_comm_count(comm) -> int:
+    n = C.c_int(0)
+    _check(load_library().fem_nccl_comm_count(comm, C.byref(n)), "fem_nccl_comm_count")
+    return n.value
 
 
 def nccl_comm_destroy(comm) -> None:

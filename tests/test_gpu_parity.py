@@ -46,6 +46,8 @@ def meshes():
         "2d-le-mpc": fi.config_mesh(5, n=13),
         "3d-nh-shuffled": fi.renumber_nodes(fi.grid_tet4(5, 4, 6).copy_with(material=1), 21),
         "2d-nh-delaunay": fi.roller_bc(fi.delaunay_tri3(1800, 30, 7).copy_with(material=1), 0.05),
+        # unstructured tets (App. A): node degrees 13-30, > 16 slots on many nodes
+        "3d-nh-delaunay": fi.roller_bc(fi.delaunay_tet4(1500, 6, 7).copy_with(material=1), 0.05),
     }
     ph = fi.two_phase(fi.perturb(fi.grid_tri3(16, 16), 0.2, 8).copy_with(material=1), 0.3,
                       (0.5, 0.3), (5.0, 3.0))
@@ -177,6 +179,8 @@ def test_newton(case):
     if mesh.n_mpc or len(mesh.dirichlet_dofs) == 0 or mesh.f_ext is not None:
         pytest.skip("Newton parity on the roller / clamped problems")
     z0 = fi.lift(mesh)
+    if "delaunay" in name:  # slivers next to x = L: start from the affine predictor (R2)
+        z0 = fi.lift(mesh, fi.affine_field(mesh, np.diag([0.05] + [0.0] * (mesh.dim - 1))))
     zr, rinfo = ref.newton(z0, cg_rtol=1e-13)
     for op, jac in ((0, 0), (1, 0), (1, 2)):
         zg, info = prob.newton_solve(dev(z0), op=op, cg_rtol=1e-13, jacobi=jac)

@@ -20,11 +20,33 @@ def test_mesh_counts():
 
 
 @pytest.mark.parametrize("mesh", [fi.perturb(fi.grid_tri3(9, 7), 0.2, 3),
-                                  fi.perturb(fi.grid_tet4(4, 3, 5), 0.1, 4)])
+                                  fi.perturb(fi.grid_tet4(4, 3, 5), 0.1, 4),
+                                  fi.delaunay_tri3(300, 10, 3), fi.delaunay_tet4(400, 5, 3)])
 def test_generator_orientation_positive(mesh):
     x = mesh.coords[mesh.conn]
     J = np.stack([x[:, a] - x[:, 0] for a in range(1, mesh.dim + 1)], axis=2)
     assert np.all(np.linalg.det(J) > 0)
+
+
+def test_delaunay_tet4_is_a_conforming_tiling_with_irregular_degrees():
+    """The unstructured 3D mesh (App. A's general tets): conforming (every face shared
+    by <= 2 tets), boundary triangles exactly tile the 6 cube faces (area 6), interior node
+    degrees irregular and above 16 for some nodes (the fallback paths of the GPU gathers)."""
+    m = fi.delaunay_tet4(600, 5, 1)
+    faces = np.sort(np.concatenate([m.conn[:, [0, 1, 2]], m.conn[:, [0, 1, 3]],
+                                    m.conn[:, [0, 2, 3]], m.conn[:, [1, 2, 3]]]), axis=1)
+    uf, cnt = np.unique(faces, axis=0, return_counts=True)
+    assert set(cnt.tolist()) <= {1, 2}
+    b = m.coords[uf[cnt == 1]]                                   # [nb, 3 nodes, 3]
+    area = 0.5 * np.linalg.norm(np.cross(b[:, 1] - b[:, 0], b[:, 2] - b[:, 0]), axis=1)
+    assert abs(area.sum() - 6.0) < 1e-12
+    assert np.all([(np.ptp(t, axis=0) < 1e-15).any() for t in b])   # each lies in a face plane
+    adj = [set() for _ in range(m.n_nodes)]
+    for e in m.conn:
+        for a in e:
+            adj[a].update(e)
+    deg = np.array([len(s) - 1 for s in adj])
+    assert deg.max() > 16 and deg.min() < 14
 
 
 def test_kuhn_split_is_conforming():
@@ -38,7 +60,8 @@ def test_kuhn_split_is_conforming():
 
 
 @pytest.mark.parametrize("mesh,measure", [(fi.perturb(fi.grid_tri3(8, 8), 0.2, 11), 1.0),
-                                          (fi.perturb(fi.grid_tet4(5, 4, 3), 0.1, 5), 1.0)])
+                                          (fi.perturb(fi.grid_tet4(5, 4, 3), 0.1, 5), 1.0),
+                                          (fi.delaunay_tet4(400, 5, 3), 1.0)])
 def test_volume_sum_and_partition_of_unity(oracle_mod, mesh, measure):
     G, vol = oracle_mod.Oracle(mesh).geometry()
     assert np.all(vol > 0)
@@ -47,7 +70,8 @@ def test_volume_sum_and_partition_of_unity(oracle_mod, mesh, measure):
 
 
 @pytest.mark.parametrize("mesh", [fi.perturb(fi.grid_tri3(6, 5), 0.2, 2),
-                                  fi.perturb(fi.grid_tet4(3, 3, 3), 0.1, 2)])
+                                  fi.perturb(fi.grid_tet4(3, 3, 3), 0.1, 2),
+                                  fi.delaunay_tet4(100, 3, 2)])
 def test_gradient_of_linear_fields_is_exact(oracle_mod, mesh):
     # sum_a x_a (x) G_a = I for the identity map, and = A for u = A x
     G, _ = oracle_mod.Oracle(mesh).geometry()

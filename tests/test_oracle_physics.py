@@ -302,3 +302,19 @@ def test_lagrangian_hessian_blocks(oracle_mod):
     assert np.array_equal(H[:nu, nu:], B.T)
     assert np.all(H[nu:, nu:] == 0.0)
     assert np.linalg.matrix_rank(B) == m.n_mpc == 2 * (2 * 5 + 1)   # C13: full row rank
+
+
+@pytest.mark.parametrize("material", [0, 1])
+def test_patch_tests_on_unstructured_tets(oracle_mod, material):
+    """Residual and tangent patch tests (§8(c3)) on the Delaunay Tet4 mesh (slivers, node
+    degrees 13-30): exact on any P1 mesh, so the interior entries vanish to rounding."""
+    m = fi.delaunay_tet4(300, 4, 11).copy_with(material=material)
+    o = oracle_mod.Oracle(m)
+    interior = ~fi.boundary_node_mask(m)
+    A = np.random.default_rng(9).uniform(-0.08, 0.08, (3, 3))
+    r = o.residual(fi.affine_field(m, A)).reshape(-1, 3)
+    assert np.abs(r[interior]).max() < 1e-13 * np.abs(r).max()
+    F = np.diag([1.1, 0.97, 0.97])
+    v = fi.affine_field(m, np.random.default_rng(4).uniform(-1, 1, (3, 3)))
+    y = o.hvp(fi.affine_field(m, F - np.eye(3)), v).reshape(-1, 3)
+    assert np.abs(y[interior]).max() < 1e-13 * np.abs(y).max()

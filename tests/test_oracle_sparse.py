@@ -122,7 +122,8 @@ def test_coloring_spec_examples(oracle_mod):
 
 @pytest.mark.parametrize("mesh", [fi.grid_tri3(8, 8), fi.grid_tri3(9, 9), fi.grid_tet4(4, 4, 4),
                                   fi.renumber_nodes(fi.grid_tri3(7, 6), 21),
-                                  fi.config_mesh(5, n=8), fi.delaunay_tri3(150, 8, 3)])
+                                  fi.config_mesh(5, n=8), fi.delaunay_tri3(150, 8, 3),
+                                  fi.delaunay_tet4(40, 3, 5)])
 def test_coloring_equals_networkx_ordered_greedy(oracle_mod, mesh):
     o = oracle_mod.Oracle(mesh)
     rp, ci = o.sparsity()

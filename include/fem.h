@@ -181,24 +181,26 @@ fem_status fem_sparsity(fem_problem *p, int64_t *row_ptr, int32_t *col_idx, fem_
  * Synchronizes `stream`. */
 fem_status fem_color(fem_problem *p, int32_t *colors, int32_t *n_colors, fem_stream stream);
 
-/* vals [nnz] in fem_sparsity order = the sparse tangent at z by Alg. 2:
+/* vals [nnz] in fem_sparsity order = the sparse tangent K(z); the colored modes follow Alg. 2:
  * for each color c the HVP along the implicit seed e_c (e_j = [color_j == c]) gives
  * J_comp[:, c]; K_ij = J_comp[i, color_j] (decompression).  Modes (flags):
  *   FEM_ASSEMBLE_LITERAL: C sequential per-color passes into J_comp [N][C] (the paper's
  *            lax.scan), then a decompression kernel;
  *   FEM_ASSEMBLE_JCOMP: all color passes in ONE element sweep (the passes are
  *            independent), accumulating J_comp with atomics, then decompression;
- *   FEM_ASSEMBLE_ROWS: J_comp computed row by row (pull form: row i sums the colored
- *            seeds' responses of its incident elements) with each compressed entry stored
- *            at its decompressed CSR slot (within a row every color names one column) — no
- *            J_comp buffer, atomic-free, bitwise reproducible.  Node tiles of 16 Morton-
- *            ordered nodes evaluate their elements' tangent contexts in shared memory (no
- *            context records in HBM); the diagonal block is minus the row's off-diagonal
- *            sum (element rows sum to zero);
+ *   FEM_ASSEMBLE_ROWS: NOT Alg. 2: the row-owner gather form of the element-Hessian
+ *            assembly (the sum of element Hessians, which
+ *            Alg. 2 reproduces exactly).  Each node's D rows sum the tangent blocks
+ *            K^e_nm of its incident elements and store them at the row's CSR slots; it reads
+ *            neither the coloring nor a J_comp buffer, is atomic-free and bitwise
+ *            reproducible.  Node tiles of 16 Morton-ordered nodes evaluate their elements'
+ *            tangent contexts in shared memory (no context records in HBM); the diagonal
+ *            block is minus the row's off-diagonal sum (element rows sum to zero);
  *   FEM_ASSEMBLE_SCATTER: not Alg. 2 but the assembly the paper compares it with (Fig. 4
  *            right): dense element Hessians scatter-added into vals with fp64
  *            atomics (run-to-run rounding differences of the atomic order);
- *   default (no mode flag): FEM_ASSEMBLE_ROWS.
+ *   default (no mode flag): FEM_ASSEMBLE_ROWS (the fastest on B200; bench.py reports the
+ *            colored Alg. 2 modes next to it as colored_assembly_ms).
  * flags may add FEM_APPLY_BC.  Builds the pattern and (for the Alg. 2 modes) the coloring if
  * needed; synchronizes `stream` only on that first setup. */
 fem_status fem_assemble_csr(fem_problem *p, const double *z, double *vals, unsigned flags,

@@ -20,6 +20,65 @@
 
 namespace fem {
 
+#ifndef FEM_FAST_MATH
+#define FEM_FAST_MATH 1
+#endif
+
+// 1/x to ~1 ulp: the SFU's ~2^-23 seed (rcp.approx.ftz.f64) refined by two Newton steps
+// (quadratic convergence: 2^-46, then below 2^-53 + one rounding).  For the finite,
+// nonzero geometric determinants of the element kernels (DegenerateElement rejects
+// det <= eps_det at create; inverted deformed elements are flagged before use); the
+// compiler's IEEE 1.0/x adds a slow-path branch for denormal / special operands.
+__device__ __forceinline__ double fem_rcp(double x) {
+#if FEM_FAST_MATH
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  double e = fma(-x, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-x, r, 1.0);
+  return fma(r, e, r);
+#else
+  return 1.0 / x;
+#endif
+}
+
+// ln x for x > 0: x = 2^k m with m in [sqrt(1/2), sqrt(2)), ln m = 2 atanh(f),
+// f = (m - 1)/(m + 1), |f| <= 0.1716, atanh(f)/f = sum_{j<=11} f^2j / (2j + 1) (truncation
+// below 2^-55 relative); ln x = k ln 2 + ln m with ln 2 split hi/lo.  ~30 instructions
+// against ~65 for the general log(); zero, negative, subnormal, inf and NaN operands take
+// log() itself (same results as libm there).
+__device__ __forceinline__ double fem_log(double x) {
+#if FEM_FAST_MATH
+  const int hi = __double2hiint(x);
+  if (hi < 0x00100000 || hi >= 0x7ff00000) return log(x);
+  int k = (hi >> 20) - 1023;
+  int mh = (hi & 0x000fffff) | 0x3ff00000;
+  if (mh > 0x3ff6a09e) {  // m > sqrt(2): halve it
+    mh -= 0x00100000;
+    ++k;
+  }
+  const double m = __hiloint2double(mh, __double2loint(x));
+  const double f = (m - 1.0) * fem_rcp(m + 1.0);
+  const double s = f * f;
+  double p = 1.0 / 23.0;
+  p = fma(p, s, 1.0 / 21.0);
+  p = fma(p, s, 1.0 / 19.0);
+  p = fma(p, s, 1.0 / 17.0);
+  p = fma(p, s, 1.0 / 15.0);
+  p = fma(p, s, 1.0 / 13.0);
+  p = fma(p, s, 1.0 / 11.0);
+  p = fma(p, s, 1.0 / 9.0);
+  p = fma(p, s, 1.0 / 7.0);
+  p = fma(p, s, 1.0 / 5.0);
+  p = fma(p, s, 1.0 / 3.0);
+  const double lnm = fma(2.0 * f * s, p, 2.0 * f);   // 2f + 2f s P(s)
+  const double dk = (double)k;
+  return fma(dk, 6.93147180369123816490e-01, fma(dk, 1.90821492927058770002e-10, lnm));
+#else
+  return log(x);
+#endif
+}
+
 template <int D>
 struct Elem {
   static constexpr int NEN = D + 1;
@@ -254,12 +313,12 @@ __device__ __forceinline__ bool nh_state(const double (&H)[D][D], NHState<D> &s)
     s.J = F[0][0] * cof[0][0] + F[0][1] * cof[0][1] + F[0][2] * cof[0][2];
   }
   if (!(s.J > 0.0)) return false;
-  const double iJ = 1.0 / s.J;
+  const double iJ = fem_rcp(s.J);
 #pragma unroll
   for (int i = 0; i < D; ++i)
 #pragma unroll
     for (int j = 0; j < D; ++j) s.FiT[i][j] = cof[i][j] * iJ;
-  s.lnJ = log(s.J);
+  s.lnJ = fem_log(s.J);
   return true;
 }
 

@@ -49,10 +49,16 @@ struct TileSet {
   int32_t *node_slots = nullptr; // [n_slots] slots of each node, tile order
   int64_t *node_slot_ptr = nullptr; // [n_nodes+1]
   double *epart = nullptr;       // [n_tiles] energy partials
+  // balanced phase-2 schedule (fem_tiles.cu k_build_sched): per tile sched_rounds x kTile
+  // task slots {8 cb offsets (uint16), meta = r | n << 12 | pos << 16 | g << 20}
+  int sched_rounds = 0;
+  uint16_t *soff = nullptr;      // [n_tiles][rounds*kTile][8]
+  uint32_t *smeta = nullptr;     // [n_tiles][rounds*kTile]
+  uint32_t *shdr = nullptr;      // [n_tiles] rounds | shuffle steps << 8
   // packed per-tile metadata blocks (fem_tiles.cu pack_tile_meta), mb bytes each
   uint8_t *meta = nullptr;
   int um = 0, mb = 0, off_nodes = 0, off_lconn = 0, off_ptr = 0, off_inc = 0, off_int = 0,
-      off_bc = 0, off_ph = 0;
+      off_bc = 0, off_ph = 0, off_soff = 0, off_smeta = 0;
 };
 
 struct Workspace {

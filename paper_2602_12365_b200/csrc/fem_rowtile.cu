@@ -553,7 +553,7 @@ __global__ void __launch_bounds__(kRtThreads, FEM_RT_MINB) k_rows_tile(RtArgs A)
         const double Jd = geometry<D>(xc, g, volc) / det0;
         ok = Jd > 0.0;
         if (!ok) atomicOr(A.err, ERRW_INVERTED);
-        c1 = ok ? mu - lam * log(Jd) : 0.0;
+        c1 = ok ? mu - lam * fem_log(Jd) : 0.0;
 #pragma unroll
         for (int a = 0; a < NEN; ++a)
 #pragma unroll

@@ -51,6 +51,23 @@
 #ifndef FEM_HVP_SPATIAL
 #define FEM_HVP_SPATIAL 1
 #endif
+// Phase 2 as a balanced task schedule (k_build_sched) instead of one thread per tile node.
+// A/B at cfg 3 (r02): HVP 0.975 -> 1.011 ms, residual 0.811 -> 0.811 ms: the barrier stall
+// moves to shared-memory latency and the 5 KB of schedule per tile adds 0.3 GB of DRAM reads
+// per launch, so the one-thread-per-node sums stay the default.
+#ifndef FEM_P2_BAL
+#define FEM_P2_BAL 0
+#endif
+// Phase 0: one thread per tile node issues the node's D-vector copies (no div / mod by D;
+// A/B r02: neutral, 0.975 vs 0.972 ms HVP)
+// NH HVP in metric form (M_ab = c_a . c_b, D_ab = dv_b . cs_a): fewer FP64 operations than
+// the dH / Ah products (tile_phase1)
+#ifndef FEM_HVP_MD
+#define FEM_HVP_MD 1
+#endif
+#ifndef FEM_ISSUE_NODE
+#define FEM_ISSUE_NODE 1
+#endif
 
 namespace fem {
 
@@ -416,18 +433,27 @@ __global__ void k_pack_meta(TileSet T, const uint8_t *node_bc, int64_t E) {
   if (threadIdx.x == 0) {
     reinterpret_cast<int *>(base)[0] = U;
     reinterpret_cast<int *>(base)[1] = nvalid;
-    reinterpret_cast<int *>(base)[2] = 0;
+    reinterpret_cast<int *>(base)[2] = T.shdr ? (int)T.shdr[t] : 0;
     reinterpret_cast<int *>(base)[3] = 0;
+  }
+  if (T.shdr) {
+    const int cap = T.sched_rounds * kTile;
+    uint16_t *so = reinterpret_cast<uint16_t *>(base + T.off_soff);
+    uint32_t *sm = reinterpret_cast<uint32_t *>(base + T.off_smeta);
+    for (int i = threadIdx.x; i < cap * 8; i += blockDim.x) so[i] = T.soff[t * cap * 8 + i];
+    for (int i = threadIdx.x; i < cap; i += blockDim.x) sm[i] = T.smeta[t * cap + i];
   }
   int32_t *nodes = reinterpret_cast<int32_t *>(base + T.off_nodes);
   for (int i = threadIdx.x; i < T.um; i += blockDim.x) nodes[i] = i < U ? T.nodes[t * T.maxe + i] : 0;
   uint16_t *lc = reinterpret_cast<uint16_t *>(base + T.off_lconn);
   for (int i = threadIdx.x; i < kTile * 4; i += blockDim.x) lc[i] = T.lconn[t * kTile * 4 + i];
-  uint16_t *ptr = reinterpret_cast<uint16_t *>(base + T.off_ptr);
-  for (int i = threadIdx.x; i <= T.um; i += blockDim.x)
-    ptr[i] = i <= U ? T.ptr[t * (T.maxe + 1) + i] : (uint16_t)nvalid;
-  uint16_t *inc = reinterpret_cast<uint16_t *>(base + T.off_inc);
-  for (int i = threadIdx.x; i < kTile * 4; i += blockDim.x) inc[i] = i < nvalid ? T.inc[t * T.maxe + i] : 0;
+  if (T.off_ptr >= 0) {
+    uint16_t *ptr = reinterpret_cast<uint16_t *>(base + T.off_ptr);
+    for (int i = threadIdx.x; i <= T.um; i += blockDim.x)
+      ptr[i] = i <= U ? T.ptr[t * (T.maxe + 1) + i] : (uint16_t)nvalid;
+    uint16_t *inc = reinterpret_cast<uint16_t *>(base + T.off_inc);
+    for (int i = threadIdx.x; i < kTile * 4; i += blockDim.x) inc[i] = i < nvalid ? T.inc[t * T.maxe + i] : 0;
+  }
   for (int i = threadIdx.x; i < T.um; i += blockDim.x) {
     base[T.off_int + i] = i < U ? T.interior[t * T.maxe + i] : 0;
     base[T.off_bc + i] = i < U ? node_bc[T.nodes[t * T.maxe + i]] : 0;
@@ -475,18 +501,128 @@ __global__ void k_sched_inc(TileSet T) {
   }
 }
 
+// Balanced phase-2 schedule (FEM_P2_BAL).  The tile's incidences (node r, element el, slot
+// a) are cut into tasks of <= K incidences of one node (K in 4..8, the smallest that fits the
+// lanes: rounds x kTile task slots), a node's g tasks on consecutive lanes of one warp; lane
+// l sums its task's <= 8 contributions cb[(a D + c) kTile + el] (offsets w = a D kTile + el
+// precomputed) for c < D, and the g lanes of a node combine by a shuffle tree (head = pos 0).
+// Every thread of the CTA takes part, the longest chain is K loads instead of the node's
+// full incidence count, and no address arithmetic runs per incidence.  The entries of each
+// lane are ordered so that the 16 lanes of a half-warp hit distinct banks (el mod 16) at every
+// step where possible.  Summation order is fixed by the schedule (deterministic).
+__device__ int sched_lanes(const uint16_t *ptr, int U, int K) {
+  int lane = 0;
+  for (int r = 0; r < U; ++r) {
+    const int n = ptr[r + 1] - ptr[r];
+    const int g = (n + K - 1) / K;
+    if ((lane & 31) + g > 32) lane = (lane + 31) & ~31;
+    lane += g;
+  }
+  return lane;
+}
+
+__global__ void k_sched_count(TileSet T, int *max_lanes) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= T.n_tiles) return;
+  atomicMax(max_lanes, sched_lanes(T.ptr + t * (T.maxe + 1), T.U[t], 8));
+}
+
+template <int D>
+__global__ void k_build_sched(TileSet T, int rounds) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= T.n_tiles) return;
+  const int U = T.U[t];
+  const uint16_t *ptr = T.ptr + t * (T.maxe + 1);
+  const uint16_t *inc = T.inc + t * T.maxe;
+  const int cap = rounds * kTile;
+  int K = 4;
+  while (K < 8 && sched_lanes(ptr, U, K) > cap) ++K;
+  uint16_t *so = T.soff + t * (int64_t)cap * 8;
+  uint32_t *sm = T.smeta + t * (int64_t)cap;
+  for (int j = 0; j < cap; ++j) {
+    sm[j] = 0u;
+    for (int q = 0; q < 8; ++q) so[j * 8 + q] = 0;
+  }
+  int lane = 0, gmax = 1;
+  for (int r = 0; r < U; ++r) {
+    const int lo = ptr[r], n = ptr[r + 1] - lo;
+    const int g = (n + K - 1) / K;
+    if ((lane & 31) + g > 32) lane = (lane + 31) & ~31;
+    const int base = n / g, rem = n % g;
+    int q0 = lo;
+    for (int p = 0; p < g; ++p) {
+      const int cnt = base + (p < rem ? 1 : 0);
+      for (int q = 0; q < cnt; ++q) {
+        const int e = inc[q0 + q];
+        so[(lane + p) * 8 + q] = (uint16_t)((e & 3) * D * kTile + (e >> 2));
+      }
+      sm[lane + p] = (uint32_t)r | (uint32_t)cnt << 11 | (uint32_t)p << 15 | (uint32_t)g << 23;
+      q0 += cnt;
+    }
+    lane += g;
+    gmax = max(gmax, g);
+  }
+  for (int h = 0; h < cap / 16; ++h)        // bank order per half-warp and step
+    for (int q = 0; q < 8; ++q) {
+      int cnt[16];
+      for (int b = 0; b < 16; ++b) cnt[b] = 0;
+      for (int l = h * 16; l < h * 16 + 16; ++l) {
+        const int n = (sm[l] >> 11) & 15;
+        if (q >= n) continue;
+        int best = q, bc = 1 << 30;
+        for (int qq = q; qq < n && bc > 0; ++qq) {
+          const int c = cnt[so[l * 8 + qq] & 15];
+          if (c < bc) { bc = c; best = qq; }
+        }
+        const uint16_t x = so[l * 8 + best];
+        so[l * 8 + best] = so[l * 8 + q];
+        so[l * 8 + q] = x;
+        ++cnt[x & 15];
+      }
+    }
+  int steps = 0;
+  while ((1 << steps) < gmax) ++steps;
+  T.shdr[t] = (uint32_t)rounds | (uint32_t)steps << 8;
+}
+
 fem_status pack_tile_meta(Problem *p, cudaStream_t s) {
   TileSet &T = p->tiles;
-  if (FEM_TILE_SCHED) {
+  if (FEM_P2_BAL) {
+    int *d_max = nullptr, h_max = 0;
+    FEM_CUDA(cudaMalloc(&d_max, sizeof(int)));
+    FEM_CUDA(cudaMemsetAsync(d_max, 0, sizeof(int), s));
+    const unsigned g = (unsigned)((T.n_tiles + 127) / 128);
+    k_sched_count<<<g, 128, 0, s>>>(T, d_max);
+    FEM_CUDA(cudaMemcpyAsync(&h_max, d_max, sizeof(int), cudaMemcpyDeviceToHost, s));
+    FEM_CUDA(cudaStreamSynchronize(s));
+    cudaFree(d_max);
+    T.sched_rounds = std::max(1, (h_max + kTile - 1) / kTile);
+    const int64_t cap = (int64_t)T.sched_rounds * kTile;
+    FEM_CUDA(cudaMalloc(&T.soff, sizeof(uint16_t) * 8 * cap * T.n_tiles));
+    FEM_CUDA(cudaMalloc(&T.smeta, sizeof(uint32_t) * cap * T.n_tiles));
+    FEM_CUDA(cudaMalloc(&T.shdr, sizeof(uint32_t) * T.n_tiles));
+    if (p->dim == 3) k_build_sched<3><<<g, 128, 0, s>>>(T, T.sched_rounds);
+    else k_build_sched<2><<<g, 128, 0, s>>>(T, T.sched_rounds);
+    FEM_LAUNCH_CHECK("phase-2 schedule");
+  }
+  if (FEM_TILE_SCHED && !FEM_P2_BAL) {
     k_sched_inc<<<(unsigned)T.n_tiles, 8, 0, s>>>(T);
     FEM_LAUNCH_CHECK("tile incidence scheduling");
   }
   T.um = round_up(T.max_U > 0 ? T.max_U : 1, 8);
   T.off_nodes = 16;
   T.off_lconn = T.off_nodes + 4 * T.um;
-  T.off_ptr = T.off_lconn + 8 * kTile;
-  T.off_inc = T.off_ptr + round_up(2 * (T.um + 1), 16);
-  T.off_int = T.off_inc + 8 * kTile;
+  if (FEM_P2_BAL) {
+    const int cap = T.sched_rounds * kTile;
+    T.off_soff = T.off_lconn + 8 * kTile;
+    T.off_smeta = T.off_soff + 16 * cap;
+    T.off_int = T.off_smeta + 4 * cap;
+    T.off_ptr = T.off_inc = -1;
+  } else {
+    T.off_ptr = T.off_lconn + 8 * kTile;
+    T.off_inc = T.off_ptr + round_up(2 * (T.um + 1), 16);
+    T.off_int = T.off_inc + 8 * kTile;
+  }
   T.off_bc = T.off_int + round_up(T.um, 16);
   T.off_ph = T.off_bc + round_up(T.um, 16);
   T.mb = round_up(T.off_ph + (T.phase ? kTile : 0), 16);
@@ -494,6 +630,11 @@ fem_status pack_tile_meta(Problem *p, cudaStream_t s) {
   if (p->dim == 2) k_pack_meta<2><<<(unsigned)T.n_tiles, 256, 0, s>>>(T, p->node_bc, p->n_elems);
   else k_pack_meta<3><<<(unsigned)T.n_tiles, 256, 0, s>>>(T, p->node_bc, p->n_elems);
   FEM_LAUNCH_CHECK("pack tile meta");
+  if (FEM_P2_BAL) {  // packed into the metadata blocks: the staging copies are not needed
+    FEM_CUDA(cudaStreamSynchronize(s));
+    cudaFree(T.soff); cudaFree(T.smeta); cudaFree(T.shdr);
+    T.soff = nullptr; T.smeta = nullptr; T.shdr = nullptr;
+  }
   return FEM_OK;
 }
 
@@ -534,7 +675,7 @@ __host__ __device__ constexpr int pipe_minb(int op, int mat, int dim = 3) {
 struct PipeArgs {
   const uint8_t *meta;
   int64_t n_tiles, E;
-  int mb, um, off_nodes, off_lconn, off_ptr, off_inc, off_int, off_bc, off_ph;
+  int mb, um, off_nodes, off_lconn, off_ptr, off_inc, off_int, off_bc, off_ph, off_soff, off_smeta;
   bool has_phase;
   const int64_t *slot_off;
   const double *coords, *u, *v;
@@ -574,7 +715,7 @@ __device__ __forceinline__ void tile_phase1(const PipeArgs &A, const unsigned ch
 #pragma unroll
       for (int i = 0; i < D; ++i) x[a][i] = xs[lc[a] * D + i];
     const double det = cof_gradients<D>(x, c);
-    const double id = 1.0 / det;
+    const double id = fem_rcp(det);
     constexpr double inv_fact = (D == 3) ? 1.0 / 6.0 : 0.5;  // vol = det / d!
     double lam = A.lam, mu = A.mu;
     if (A.has_phase) {
@@ -629,8 +770,8 @@ __device__ __forceinline__ void tile_phase1(const PipeArgs &A, const unsigned ch
         //   vol P G_a = (1/d!) [mu c_a + (mu/det) Hh c_a + ((lam ln J - mu) / J) cs_a], a >= 1
         const double Jr = dets * id;
         ok = Jr > 0.0;
-        const double lnJ = log(Jr);
-        const double kc = (lam * lnJ - mu) / Jr * inv_fact, kh = ms * id;
+        const double lnJ = fem_log(Jr);
+        const double kc = (lam * lnJ - mu) * fem_rcp(Jr) * inv_fact, kh = ms * id;
 #pragma unroll
         for (int i = 0; i < D; ++i) {
           double s0 = 0.0;
@@ -673,6 +814,72 @@ __device__ __forceinline__ void tile_phase1(const PipeArgs &A, const unsigned ch
           for (int j = 0; j < D; ++j) A.lin[(int64_t)(i * D + j) * A.lin_stride + e] = ok ? s.FiT[i][j] : 0.0;
         A.lin[(int64_t)(D * D) * A.lin_stride + e] = ok ? s.lnJ : 0.0;
       }
+    } else if constexpr (SPATIAL && FEM_HVP_MD) {
+      // Deformed-configuration HVP (reading R9) in metric form.  With dv_b = v_b - v_0,
+      // c_a the cofactor rows at x, cs_a those at x + u (g_a = cs_a / det J(x+u)):
+      //   vol dP G_a = sr sum_b M_ab dv_b + sum_b (k1 D_ab + k2 delta_ab) cs_b,  a >= 1,
+      //   M_ab = c_a . c_b,  D_ab = dv_b . cs_a,  tr A det J(x+u) = sum_b D_bb,
+      //   sr = mu / (d! det), k1 = c1 s, k2 = lam tr(D) s, s = 1 / (d! J det J(x+u)),
+      //   c1 = mu - lam ln J, J = det J(x+u) / det J(x); node 0 = minus the sum.
+      // (the same terms as the dH / Ah form below: (dH c_a) = sum_b M_ab dv_b and
+      // (Ah^T cs_a) = sum_b D_ab cs_b; 3x3 metrics replace two 3x3x3 products)
+      double dv[D][D];
+      {
+        double v0[D];
+        const unsigned bc0 = MASK ? m[A.off_bc + lc[0]] : 0u;
+#pragma unroll
+        for (int i = 0; i < D; ++i) v0[i] = (bc0 & (1u << i)) ? 0.0 : vs[lc[0] * D + i];
+#pragma unroll
+        for (int b = 0; b < D; ++b) {
+          const unsigned bc = MASK ? m[A.off_bc + lc[b + 1]] : 0u;
+#pragma unroll
+          for (int i = 0; i < D; ++i)
+            dv[b][i] = ((bc & (1u << i)) ? 0.0 : vs[lc[b + 1] * D + i]) - v0[i];
+        }
+      }
+      const double Jr = dets * id;
+      ok = Jr > 0.0;
+      const double c1 = mu - lam * fem_log(Jr);
+      const double sr = mu * id * inv_fact, scur = inv_fact * fem_rcp(Jr * dets);
+      double Dm[D][D], tr = 0.0;
+#pragma unroll
+      for (int a = 0; a < D; ++a)
+#pragma unroll
+        for (int b = 0; b < D; ++b) {
+          double t = 0.0;
+#pragma unroll
+          for (int j = 0; j < D; ++j) t = fma(dv[b][j], cs[a][j], t);
+          Dm[a][b] = t;
+          if (a == b) tr += t;
+        }
+      const double k1 = scur * c1, k2 = scur * lam * tr;
+#pragma unroll
+      for (int a = 0; a < D; ++a)
+#pragma unroll
+        for (int b = 0; b < D; ++b) Dm[a][b] = (a == b) ? fma(k1, Dm[a][b], k2) : k1 * Dm[a][b];
+      double Ms[D][D];
+#pragma unroll
+      for (int a = 0; a < D; ++a)
+#pragma unroll
+        for (int b = a; b < D; ++b) {
+          double t = 0.0;
+#pragma unroll
+          for (int j = 0; j < D; ++j) t = fma(c[a][j], c[b][j], t);
+          Ms[a][b] = Ms[b][a] = sr * t;
+        }
+#pragma unroll
+      for (int i = 0; i < D; ++i) {
+        double s0 = 0.0;
+#pragma unroll
+        for (int a = 0; a < D; ++a) {
+          double fa = 0.0;
+#pragma unroll
+          for (int b = 0; b < D; ++b) fa = fma(Ms[a][b], dv[b][i], fma(Dm[a][b], cs[b][i], fa));
+          f[a + 1][i] = fa;
+          s0 += fa;
+        }
+        f[0][i] = -s0;
+      }
     } else {
       // dH = dHh / det; vol dP(dH) G_a = dP(dHh) c_a * (1 / (det d!)): fold into (lambda, mu)
       double v[NEN][D], dH[D][D];
@@ -696,8 +903,8 @@ __device__ __forceinline__ void tile_phase1(const PipeArgs &A, const unsigned ch
         grad_hat<D>(v, cs, Ah);
         const double Jr = dets * id;
         ok = Jr > 0.0;
-        const double c1 = mu - lam * log(Jr);
-        const double sr = mu * sc, scur = inv_fact / (Jr * dets);
+        const double c1 = mu - lam * fem_log(Jr);
+        const double sr = mu * sc, scur = inv_fact * fem_rcp(Jr * dets);
         double tr = 0.0;
 #pragma unroll
         for (int k = 0; k < D; ++k) tr += Ah[k][k];
@@ -748,12 +955,77 @@ __device__ __forceinline__ void tile_phase1(const PipeArgs &A, const unsigned ch
 
 // Phase 2: fixed-order per-tile-node sums of the contributions, stored (interior nodes),
 // RED (tile-boundary nodes) or written to the node's slot (DET).
+template <int D, bool DET>
+__device__ __forceinline__ void node_write(const PipeArgs &A, const unsigned char *m, int r,
+                                           int64_t t, const double (&sacc)[D]) {
+  if constexpr (DET) {
+    double *slot = A.slots + (A.slot_off[t] + r) * D;
+#pragma unroll
+    for (int cc = 0; cc < D; ++cc) slot[cc] = sacc[cc];
+  } else {
+    const int32_t *nodes = reinterpret_cast<const int32_t *>(m + A.off_nodes);
+    const int64_t g = (int64_t)nodes[r] * D;
+    if (m[A.off_int + r]) {
+#pragma unroll
+      for (int cc = 0; cc < D; ++cc) A.out[g + cc] = sacc[cc];
+    } else {
+#pragma unroll
+      for (int cc = 0; cc < D; ++cc) atomicAdd(A.out + g + cc, sacc[cc]);
+    }
+  }
+}
+
+#if FEM_P2_BAL
+// Balanced schedule (k_build_sched): every thread sums one task of <= 8 incidences of one
+// node from precomputed offsets; the g lanes of a node combine by a shuffle tree.
+template <int D, int OP, bool DET>
+__device__ __forceinline__ void tile_phase2(const PipeArgs &A, const unsigned char *m, int U,
+                                            int64_t t, int tid, const double *cb) {
+  const uint32_t hdr = reinterpret_cast<const uint32_t *>(m)[2];
+  const int rounds = hdr & 0xff, steps = (hdr >> 8) & 0xff;
+  const uint4 *so = reinterpret_cast<const uint4 *>(m + A.off_soff);
+  const uint32_t *sm = reinterpret_cast<const uint32_t *>(m + A.off_smeta);
+  for (int rd = 0; rd < rounds; ++rd) {   // uniform over the CTA (shuffles below)
+    const int j = rd * kTile + tid;
+    const uint32_t mt = sm[j];
+    const uint4 o4 = so[j];
+    const int n = (mt >> 11) & 15, pos = (mt >> 15) & 0xff, g = (mt >> 23) & 0xff;
+    const uint32_t ow[4] = {o4.x, o4.y, o4.z, o4.w};
+    double s0[D], s1[D];
+#pragma unroll
+    for (int cc = 0; cc < D; ++cc) s0[cc] = s1[cc] = 0.0;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      if (q < n) {
+        const double *pq = cb + ((ow[q >> 1] >> ((q & 1) * 16)) & 0xffffu);
+#pragma unroll
+        for (int cc = 0; cc < D; ++cc) {
+          if (q & 1) s1[cc] += pq[cc * kTile];
+          else s0[cc] += pq[cc * kTile];
+        }
+      }
+    }
+    double sacc[D];
+#pragma unroll
+    for (int cc = 0; cc < D; ++cc) sacc[cc] = s0[cc] + s1[cc];
+    for (int st = 0; st < steps; ++st) {
+      const int off = 1 << st;
+      const bool take = (pos & (2 * off - 1)) == 0 && pos + off < g;
+#pragma unroll
+      for (int cc = 0; cc < D; ++cc) {
+        const double x = __shfl_down_sync(0xffffffffu, sacc[cc], off);
+        if (take) sacc[cc] += x;
+      }
+    }
+    if (n > 0 && pos == 0) node_write<D, DET>(A, m, (int)(mt & 0x7ffu), t, sacc);
+  }
+}
+#else
 template <int D, int OP, bool DET>
 __device__ __forceinline__ void tile_phase2(const PipeArgs &A, const unsigned char *m, int U,
                                             int64_t t, int tid, const double *cb) {
   const uint16_t *ptr = reinterpret_cast<const uint16_t *>(m + A.off_ptr);
   const uint16_t *inc = reinterpret_cast<const uint16_t *>(m + A.off_inc);
-  const int32_t *nodes = reinterpret_cast<const int32_t *>(m + A.off_nodes);
   for (int r = tid; r < U; r += kTile) {  // one thread per tile node, D components
     const int lo = ptr[r], hi = ptr[r + 1];
     // two interleaved partial sums (even / odd incidences, combined in a fixed order):
@@ -779,22 +1051,10 @@ __device__ __forceinline__ void tile_phase2(const PipeArgs &A, const unsigned ch
     double sacc[D];
 #pragma unroll
     for (int cc = 0; cc < D; ++cc) sacc[cc] = s0[cc] + s1[cc];
-    if constexpr (DET) {
-      double *slot = A.slots + (A.slot_off[t] + r) * D;
-#pragma unroll
-      for (int cc = 0; cc < D; ++cc) slot[cc] = sacc[cc];
-    } else {
-      const int64_t g = (int64_t)nodes[r] * D;
-      if (m[A.off_int + r]) {
-#pragma unroll
-        for (int cc = 0; cc < D; ++cc) A.out[g + cc] = sacc[cc];
-      } else {
-#pragma unroll
-        for (int cc = 0; cc < D; ++cc) atomicAdd(A.out + g + cc, sacc[cc]);
-      }
-    }
+    node_write<D, DET>(A, m, r, t, sacc);
   }
 }
+#endif
 
 // Residual / energy: CTA-wide pipeline (cp.async.wait_all + barrier per tile).  HVP (the
 // register-heaviest, 2 CTAs/SM): barrier-free data path — every thread's cp.async copies of
@@ -862,11 +1122,23 @@ __global__ void __launch_bounds__(kTile, pipe_minb(OP, MAT, D)) k_tile_pipe(Pipe
     double *dst = nodeb + b * nstride;
     const int U = reinterpret_cast<const int *>(m)[0];
     const int32_t *nodes = reinterpret_cast<const int32_t *>(m + A.off_nodes);
-    for (int i = tid; i < U * D; i += kTile) {
-      const int64_t g = (int64_t)nodes[i / D] * D + (i % D);
-      cp_async8(dst + i, A.coords + g);
-      if constexpr (NEED_U) cp_async8(dst + um * D + i, A.u + g);
-      if constexpr (op_is_hvp<OP>()) cp_async8(dst + (NF - 1) * um * D + i, A.v + g);
+    if (FEM_ISSUE_NODE) {
+      for (int r = tid; r < U; r += kTile) {
+        const int64_t g = (int64_t)nodes[r] * D;
+#pragma unroll
+        for (int c = 0; c < D; ++c) {
+          cp_async8(dst + r * D + c, A.coords + g + c);
+          if constexpr (NEED_U) cp_async8(dst + um * D + r * D + c, A.u + g + c);
+          if constexpr (op_is_hvp<OP>()) cp_async8(dst + (NF - 1) * um * D + r * D + c, A.v + g + c);
+        }
+      }
+    } else {
+      for (int i = tid; i < U * D; i += kTile) {
+        const int64_t g = (int64_t)nodes[i / D] * D + (i % D);
+        cp_async8(dst + i, A.coords + g);
+        if constexpr (NEED_U) cp_async8(dst + um * D + i, A.u + g);
+        if constexpr (op_is_hvp<OP>()) cp_async8(dst + (NF - 1) * um * D + i, A.v + g);
+      }
     }
     if constexpr (DEC) mb_cp_arrive(&mb_node[b]);
   };
@@ -1007,6 +1279,8 @@ fem_status tile_pass(Problem *p, int op, const double *u, const double *v, doubl
   a.mb = T.mb; a.um = T.um; a.off_nodes = T.off_nodes; a.off_lconn = T.off_lconn;
   a.off_ptr = T.off_ptr; a.off_inc = T.off_inc; a.off_int = T.off_int; a.off_bc = T.off_bc;
   a.off_ph = T.off_ph;
+  a.off_soff = T.off_soff;
+  a.off_smeta = T.off_smeta;
   a.has_phase = T.phase != nullptr;
   a.slot_off = T.slot_off;
   a.coords = p->coords;

@@ -474,6 +474,16 @@ def main():
             lambda: prob.energy_residual(zt, bc=True, out_energy=e1, out=r)),
         "residual_baseline_scatter_ms": time_call(
             lambda: prob.residual(zt, bc=True, out=r, flags=fem.BASELINE_SCATTER)),
+        # geometry streamed per element (Alg. 1's gather, 80 B / tet,
+        # one TMA bulk copy per tile) instead of recomputed from the coordinates
+        "hvp_stream_geom_ms": time_call(lambda: prob.hvp(zt, vt, bc=True, out=y, flags=fem.STREAM_GEOM)),
+        "residual_stream_geom_ms": time_call(
+            lambda: prob.residual(zt, bc=True, out=r, flags=fem.STREAM_GEOM)),
+        # A/B 1(C): element-colored conflict-free passes (plain stores, no atomics)
+        "hvp_colored_scatter_ms": time_call(
+            lambda: prob.hvp(zt, vt, bc=True, out=y, flags=fem.COLORED_SCATTER)),
+        "residual_colored_scatter_ms": time_call(
+            lambda: prob.residual(zt, bc=True, out=r, flags=fem.COLORED_SCATTER)),
         "assemble_batched_ms": time_call(lambda: prob.assemble_csr(zt, bc=True, mode="batched", out=vals), 2),
         "assemble_rows_ms": time_call(lambda: prob.assemble_csr(zt, bc=True, mode="rows", out=vals), 2),
         "assemble_literal_ms": time_call(lambda: prob.assemble_csr(zt, bc=True, mode="literal", out=vals), 1),

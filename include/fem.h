@@ -84,9 +84,20 @@ enum {
   FEM_ASSEMBLE_ROWS = 64u,  /* fem_assemble_csr: row-pull form (no J_comp buffer).         */
   FEM_ASSEMBLE_SCATTER = 128u,/* fem_assemble_csr: element-Hessian scatter-add with fp64
                                atomics (the paper's comparison path), not Alg. 2 */
-  FEM_LINEARIZED = 256u     /* fem_hvp / CG op 0: the tangent at the state of the last
+  FEM_LINEARIZED = 256u,    /* fem_hvp / CG op 0: the tangent at the state of the last
                                fem_linearize (its z; the z argument is not read for the
                                state) — Newton-Krylov applies K(z) thousands of times */
+  FEM_STREAM_GEOM = 512u,   /* residual / HVP: read each element's reference geometry
+                               (cofactor rows c_a = det J G_a and det J, 80 B per Tet4) from a
+                               per-element stream built once, loaded per tile by one TMA bulk
+                               copy — Alg. 1's per-batch gather of grad N and det J
+                                — instead of recomputing it from the coordinates.
+                               Not with FEM_DETERMINISTIC / BASELINE_SCATTER / LINEARIZED. */
+  FEM_COLORED_SCATTER = 1024u /* residual / HVP: elements colored so that no two elements of
+                               a color share a node (greedy in tile order, setup); one pass
+                               per color, each element adds its nodal vectors to the output
+                               with plain loads / stores — conflict-free without atomics,
+                               deterministic (fixed color order).  Single GPU.            */
 };
 
 typedef struct {

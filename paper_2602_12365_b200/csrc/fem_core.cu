@@ -75,6 +75,8 @@ struct ElemArgs {
   double *out;
   double *partials;
   int *err;
+  const int32_t *list;  // COLORED: the elements of one color (caller ids)
+  int64_t n_list;
 };
 
 template <int D>
@@ -97,11 +99,15 @@ __device__ __forceinline__ void gather(const double *f, const int32_t (&nd)[D + 
     for (int i = 0; i < D; ++i) x[a][i] = __ldg(f + (int64_t)nd[a] * D + i);
 }
 
-template <int D, int MAT, int OP, bool MASK>
+// COLORED (FEM_COLORED_SCATTER): the elements of one color share no node, so each adds its
+// nodal vectors with plain loads / stores (no atomics, no conflicts); colors run in order.
+template <int D, int MAT, int OP, bool MASK, bool COLORED = false>
 __global__ void __launch_bounds__(kThreads) k_elem(ElemArgs A) {
   double acc = 0.0;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < A.E; e += stride) {
+  const int64_t n_items = COLORED ? A.n_list : A.E;
+  for (int64_t it = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; it < n_items; it += stride) {
+    const int64_t e = COLORED ? (int64_t)__ldg(A.list + it) : it;
     int32_t nd[D + 1];
     load_conn<D>(A.conn, e, nd);
     double x[D + 1][D], G[D + 1][D], vol;
@@ -163,7 +169,10 @@ __global__ void __launch_bounds__(kThreads) k_elem(ElemArgs A) {
 #pragma unroll
       for (int a = 0; a < D + 1; ++a)
 #pragma unroll
-        for (int i = 0; i < D; ++i) atomicAdd(A.out + (int64_t)nd[a] * D + i, f[a][i]);
+        for (int i = 0; i < D; ++i) {
+          if constexpr (COLORED) A.out[(int64_t)nd[a] * D + i] += f[a][i];
+          else atomicAdd(A.out + (int64_t)nd[a] * D + i, f[a][i]);
+        }
     }
   }
   if constexpr (OP == OP_ENERGY) {
@@ -172,10 +181,10 @@ __global__ void __launch_bounds__(kThreads) k_elem(ElemArgs A) {
   }
 }
 
-template <int OP, bool MASK>
+template <int OP, bool MASK, bool COLORED = false>
 static fem_status launch_elem(Problem *p, const ElemArgs &a, int grid, cudaStream_t s) {
   if (p->n_elems == 0) return FEM_OK;
-#define FEM_DISPATCH(D, M) k_elem<D, M, OP, MASK><<<grid, kThreads, 0, s>>>(a)
+#define FEM_DISPATCH(D, M) k_elem<D, M, OP, MASK, COLORED><<<grid, kThreads, 0, s>>>(a)
   if (p->dim == 2) {
     if (p->material == FEM_LINEAR_ELASTIC) FEM_DISPATCH(2, FEM_LINEAR_ELASTIC);
     else FEM_DISPATCH(2, FEM_NEO_HOOKEAN);
@@ -365,21 +374,92 @@ static fem_status element_pass_halo(Problem *p, int op, const double *z, const d
   return local_only ? FEM_OK : halo_end(p, y, s);
 }
 
+// Element coloring (FEM_COLORED_SCATTER): greedy in element-tile (Morton) order, each element
+// takes the smallest color none of its nodes' earlier elements holds (per-node 128-bit color
+// masks); a host pass over the connectivity at setup.  Colors >= the max node-element
+// degree (24 for interior Kuhn nodes).
+static fem_status build_elem_colors(Problem *p, cudaStream_t s) {
+  if (p->ecolor_list || p->n_elems == 0) return FEM_OK;
+  fem_status st = build_tiles(p, s);
+  if (st) return st;
+  const int nen = p->nen;
+  const int64_t E = p->n_elems;
+  std::vector<int32_t> conn((size_t)E * nen), perm((size_t)E);
+  FEM_CUDA(cudaMemcpyAsync(conn.data(), p->conn, sizeof(int32_t) * conn.size(), cudaMemcpyDeviceToHost, s));
+  FEM_CUDA(cudaMemcpyAsync(perm.data(), p->tiles.perm, sizeof(int32_t) * E, cudaMemcpyDeviceToHost, s));
+  FEM_CUDA(cudaStreamSynchronize(s));
+  std::vector<uint64_t> mask((size_t)p->n_nodes * 2, 0ull);
+  std::vector<uint8_t> col((size_t)E);
+  std::vector<int64_t> cnt(129, 0);
+  int nc = 0;
+  for (int64_t i = 0; i < E; ++i) {
+    const int64_t e = perm[i];
+    uint64_t m0 = 0, m1 = 0;
+    for (int a = 0; a < nen; ++a) {
+      const int64_t n = conn[e * nen + a];
+      m0 |= mask[2 * n];
+      m1 |= mask[2 * n + 1];
+    }
+    int c = ~m0 ? __builtin_ctzll(~m0) : (~m1 ? 64 + __builtin_ctzll(~m1) : 128);
+    if (c >= 128) {
+      set_error("FEM_COLORED_SCATTER: more than 128 element colors");
+      return FEM_ERR_TOO_MANY_COLORS;
+    }
+    for (int a = 0; a < nen; ++a) mask[2 * conn[e * nen + a] + (c >> 6)] |= 1ull << (c & 63);
+    col[i] = (uint8_t)c;
+    ++cnt[c + 1];
+    nc = std::max(nc, c + 1);
+  }
+  p->ecolor_off.assign(nc + 1, 0);
+  for (int c = 0; c < nc; ++c) p->ecolor_off[c + 1] = p->ecolor_off[c] + cnt[c + 1];
+  std::vector<int32_t> list((size_t)E);
+  std::vector<int64_t> fill(p->ecolor_off.begin(), p->ecolor_off.end() - 1);
+  for (int64_t i = 0; i < E; ++i) list[fill[col[i]]++] = perm[i];
+  FEM_CUDA(cudaMalloc(&p->ecolor_list, sizeof(int32_t) * E));
+  FEM_CUDA(cudaMemcpyAsync(p->ecolor_list, list.data(), sizeof(int32_t) * E, cudaMemcpyHostToDevice, s));
+  FEM_CUDA(cudaStreamSynchronize(s));
+  return FEM_OK;
+}
+
+template <int OP, bool MASK>
+static fem_status colored_pass(Problem *p, ElemArgs a, cudaStream_t s) {
+  fem_status st = build_elem_colors(p, s);
+  if (st) return st;
+  for (size_t c = 0; c + 1 < p->ecolor_off.size(); ++c) {
+    a.list = p->ecolor_list + p->ecolor_off[c];
+    a.n_list = p->ecolor_off[c + 1] - p->ecolor_off[c];
+    st = launch_elem<OP, MASK, true>(p, a, grid_for(a.n_list), s);
+    if (st) return st;
+  }
+  return FEM_OK;
+}
+
 fem_status run_residual(Problem *p, const double *z, double *r, unsigned flags, cudaStream_t s) {
   const bool det = flags & FEM_DETERMINISTIC;
   if (!det || p->n_elems == 0) FEM_CUDA(cudaMemsetAsync(r, 0, sizeof(double) * p->N, s));
   fem_status st;
-  if (flags & FEM_BASELINE_SCATTER) {
+  if (flags & FEM_COLORED_SCATTER) {
+    ElemArgs a = elem_args(p);
+    a.u = z;
+    a.out = r;
+    st = colored_pass<OP_RESIDUAL, false>(p, a, s);
+  } else if (flags & FEM_BASELINE_SCATTER) {
     ElemArgs a = elem_args(p);
     a.u = z;
     a.out = r;
     st = launch_elem<OP_RESIDUAL, false>(p, a, grid_for(p->n_elems), s);
   } else {
     if (det && p->n_mpc) FEM_CUDA(cudaMemsetAsync(r + p->n_u, 0, sizeof(double) * p->n_mpc, s));
-    st = element_pass_halo(p, OP_RESIDUAL, z, nullptr, r, false, det, flags & FEM_LOCAL_ONLY, s);
+    const bool sg = flags & FEM_STREAM_GEOM;
+    if (sg && det) {
+      set_error("fem_residual: FEM_STREAM_GEOM with FEM_DETERMINISTIC");
+      return FEM_ERR_INVALID_ARG;
+    }
+    st = element_pass_halo(p, sg ? OP_RESIDUAL_S : OP_RESIDUAL, z, nullptr, r, false, det,
+                           flags & FEM_LOCAL_ONLY, s);
   }
   if (st) return st;
-  if ((flags & FEM_BASELINE_SCATTER) && p->size > 1 && !(flags & FEM_LOCAL_ONLY)) {
+  if ((flags & (FEM_BASELINE_SCATTER | FEM_COLORED_SCATTER)) && p->size > 1 && !(flags & FEM_LOCAL_ONLY)) {
     st = halo_add(p, r, s);
     if (st) return st;
   }
@@ -408,7 +488,14 @@ fem_status run_hvp(Problem *p, const double *z, const double *v, double *y, unsi
   if (!det || p->n_elems == 0) FEM_CUDA(cudaMemsetAsync(y, 0, sizeof(double) * p->N, s));
   const bool bc = (flags & FEM_APPLY_BC) && p->n_dir;
   fem_status st;
-  if (flags & FEM_BASELINE_SCATTER) {
+  if (flags & FEM_COLORED_SCATTER) {
+    ElemArgs a = elem_args(p);
+    a.u = z;
+    a.v = v;
+    a.out = y;
+    a.node_bc = p->node_bc;
+    st = bc ? colored_pass<OP_HVP, true>(p, a, s) : colored_pass<OP_HVP, false>(p, a, s);
+  } else if (flags & FEM_BASELINE_SCATTER) {
     ElemArgs a = elem_args(p);
     a.u = z;
     a.v = v;
@@ -423,10 +510,16 @@ fem_status run_hvp(Problem *p, const double *z, const double *v, double *y, unsi
       set_error("fem_hvp: FEM_LINEARIZED without a preceding fem_linearize");
       return FEM_ERR_INVALID_ARG;
     }
-    st = element_pass_halo(p, lin ? OP_HVP_LIN : OP_HVP, z, v, y, bc, det, flags & FEM_LOCAL_ONLY, s);
+    const bool sg = flags & FEM_STREAM_GEOM;
+    if (sg && (det || lin)) {
+      set_error("fem_hvp: FEM_STREAM_GEOM with FEM_DETERMINISTIC / FEM_LINEARIZED");
+      return FEM_ERR_INVALID_ARG;
+    }
+    st = element_pass_halo(p, lin ? OP_HVP_LIN : sg ? OP_HVP_S : OP_HVP, z, v, y, bc, det,
+                           flags & FEM_LOCAL_ONLY, s);
   }
   if (st) return st;
-  if ((flags & FEM_BASELINE_SCATTER) && p->size > 1 && !(flags & FEM_LOCAL_ONLY)) {
+  if ((flags & (FEM_BASELINE_SCATTER | FEM_COLORED_SCATTER)) && p->size > 1 && !(flags & FEM_LOCAL_ONLY)) {
     st = halo_add(p, y, s);
     if (st) return st;
   }
@@ -720,6 +813,7 @@ fem_status fem_destroy(fem_problem *h) {
   if (p->h_scal) cudaFreeHost(p->h_scal);
   if (p->cap_stream) cudaStreamDestroy(p->cap_stream);
   if (p->lin) cudaFree(p->lin);
+  if (p->ecolor_list) cudaFree(p->ecolor_list);
   free_tiles(p->tiles);
   dist_free(p);
   delete h;
@@ -796,7 +890,8 @@ fem_status fem_energy_residual(fem_problem *h, const double *z, double *energy, 
   Problem *p = &h->p;
   cudaStream_t s = (cudaStream_t)stream;
   // one element pass on a single GPU with the default scatter; otherwise the two calls
-  if (p->size > 1 || (flags & (FEM_DETERMINISTIC | FEM_BASELINE_SCATTER)) || p->n_elems == 0) {
+  if (p->size > 1 || (flags & (FEM_DETERMINISTIC | FEM_BASELINE_SCATTER | FEM_STREAM_GEOM |
+                                FEM_COLORED_SCATTER)) || p->n_elems == 0) {
     fem_status st = fem_energy(h, z, energy, stream);
     if (st) return st;
     return run_residual(p, z, r, flags, s);

@@ -25,7 +25,10 @@ constexpr int kThreads = 256;
 #endif
 constexpr int kTile = FEM_TILE;     // elements per tile (one CTA)
 
-enum { OP_ENERGY = 0, OP_RESIDUAL = 1, OP_HVP = 2, OP_HVP_LIN = 3, OP_LIN = 4 };
+enum { OP_ENERGY = 0, OP_RESIDUAL = 1, OP_HVP = 2, OP_HVP_LIN = 3, OP_LIN = 4, OP_RESIDUAL_S = 5,
+       OP_HVP_S = 6 };
+// OP_*_S: residual / HVP from the streamed per-element geometry (TileSet::geom; Alg. 1's
+// per-batch gather of grad N and det J) instead of coordinates (FEM_STREAM_GEOM)
 // OP_LIN: cache the tangent state at z (fem_linearize); OP_HVP_LIN: HVP from that cache
 
 // Element tiles (fem_tiles.cu).  maxe = kTile * (dim+1) reserved entries per tile.
@@ -49,6 +52,7 @@ struct TileSet {
   int32_t *node_slots = nullptr; // [n_slots] slots of each node, tile order
   int64_t *node_slot_ptr = nullptr; // [n_nodes+1]
   double *epart = nullptr;       // [n_tiles] energy partials
+  double *geom = nullptr;        // [n_tiles][D*D+1][kTile] cofactor rows c_a and det J (SoA per tile)
   // balanced phase-2 schedule (fem_tiles.cu k_build_sched): per tile sched_rounds x kTile
   // task slots {8 cb offsets (uint16), meta = r | n << 12 | pos << 16 | g << 20}
   int sched_rounds = 0;
@@ -128,6 +132,10 @@ struct Problem {
   Workspace jcomp, cgbuf, tmp, slotbuf, ctxbuf;
   cudaStream_t cap_stream = nullptr;  // CUDA-graph capture of solver iterations
   int spmv_lpn = 0;             // node-block SpMV lanes per node (0 unset, -1 plain CSR)
+  // element coloring for FEM_COLORED_SCATTER (fem_core.cu build_elem_colors): elements of
+  // color c (caller ids, tile order) at ecolor_list[ecolor_off[c] .. ecolor_off[c+1])
+  int32_t *ecolor_list = nullptr;
+  std::vector<int64_t> ecolor_off;
   double *lin = nullptr;        // fem_linearize cache: [10][n_tiles*kTile] F^-T (9), ln J, SoA
   bool lin_valid = false;
   TileSet tiles;
@@ -220,6 +228,7 @@ fem_status build_tiles(Problem *p, cudaStream_t s);
 fem_status tile_pass(Problem *p, int op, const double *u, const double *v, double *out, bool mask,
                      bool det, double *partials, cudaStream_t s, int part = 0);
 fem_status build_tile_lists(Problem *p, cudaStream_t s);
+fem_status build_geom_stream(Problem *p, cudaStream_t s);                // fem_tiles.cu
 fem_status halo_begin(Problem *p, const double *y, cudaStream_t s);
 fem_status halo_end(Problem *p, double *y, cudaStream_t s);
 void free_tiles(TileSet &T);

@@ -661,13 +661,14 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 // (10M DOFs, CTAs/SM 2/3/4/5): HVP 0.340/0.303/0.344/0.344 ms, residual (3 by default)
 // 0.266/0.266/0.255/0.251 ms, energy (4 by default) 0.166/0.172/0.170/0.163 ms.
 __host__ __device__ constexpr int pipe_minb2d(int op, int mat) {
-  return op == OP_ENERGY || op == OP_RESIDUAL || op == OP_LIN ? 5
+  return op == OP_RESIDUAL_S || op == OP_HVP_S ? 3 : op == OP_ENERGY || op == OP_RESIDUAL || op == OP_LIN ? 5
          : (mat == FEM_NEO_HOOKEAN ? 3 : 4);
 }
 __host__ __device__ constexpr int pipe_minb(int op, int mat, int dim = 3) {
   return (256 / kTile) *
          (dim == 2 ? (FEM_PIPE_MINB2D > 0 ? FEM_PIPE_MINB2D : pipe_minb2d(op, mat))
           : FEM_PIPE_MINB > 0 ? FEM_PIPE_MINB
+                            : (op == OP_RESIDUAL_S || op == OP_HVP_S) ? 2
                             : (op == OP_ENERGY ? 4 : (op == OP_RESIDUAL ? FEM_RES_MINB : op == OP_LIN ? 3
                                 : (op == OP_HVP_LIN ? 3 : (mat == FEM_NEO_HOOKEAN ? FEM_HVP_MINB : 3)))));
 }
@@ -684,37 +685,59 @@ struct PipeArgs {
   double *out, *slots, *partials;
   const int32_t *list;  // tile ids to process (null: tiles 0 .. n_tiles-1)
   double *lin;        // linearization cache [10][lin_stride] (OP_LIN writes, OP_HVP_LIN reads)
+  const double *geom; // OP_*_S: per-tile geometry blocks [n_tiles][D*D+1][kTile]
   int64_t lin_stride;
   int *err;
 };
 
 template <int OP>
-constexpr bool op_is_hvp() { return OP == OP_HVP || OP == OP_HVP_LIN; }
+constexpr bool op_streams() { return OP == OP_RESIDUAL_S || OP == OP_HVP_S; }
+template <int OP>  // the operation an OP_*_S variant computes
+constexpr int base_op() { return OP == OP_RESIDUAL_S ? OP_RESIDUAL : OP == OP_HVP_S ? OP_HVP : OP; }
 template <int OP>
-constexpr bool op_has_p2() { return OP == OP_RESIDUAL || op_is_hvp<OP>(); }
+constexpr bool op_is_hvp() { return OP == OP_HVP || OP == OP_HVP_LIN || OP == OP_HVP_S; }
+template <int OP>
+constexpr bool op_has_p2() { return base_op<OP>() == OP_RESIDUAL || op_is_hvp<OP>(); }
 template <int OP, int MAT>
-constexpr bool op_needs_u() { return OP == OP_ENERGY || OP == OP_RESIDUAL || OP == OP_LIN || (OP == OP_HVP && MAT == FEM_NEO_HOOKEAN); }
+constexpr bool op_needs_u() {
+  return OP == OP_ENERGY || base_op<OP>() == OP_RESIDUAL || OP == OP_LIN ||
+         (base_op<OP>() == OP_HVP && MAT == FEM_NEO_HOOKEAN);
+}
+constexpr int geom_words(int D) { return D * D + 1; }
 
-template <int D, int MAT, int OP, bool MASK>
+template <int D, int MAT, int OP_, bool MASK>
 __device__ __forceinline__ void tile_phase1(const PipeArgs &A, const unsigned char *m,
                                             const double *xs, const double *us, const double *vs,
-                                            int64_t t, int tid, double *cb, double &eacc) {
+                                            int64_t t, int tid, double *cb, double &eacc,
+                                            const double *gs = nullptr) {
+  // OP_*_S: the same operation with c_a, det J read from the streamed geometry block gs
+  constexpr int OP = base_op<OP_>();
+  constexpr bool STREAM = op_streams<OP_>();
   constexpr int NEN = D + 1;
   constexpr bool NEED_U = op_needs_u<OP, MAT>();
-  // NH HVP in the deformed configuration (FEM_HVP_SPATIAL): see the HVP branch below
-  constexpr bool SPATIAL = FEM_HVP_SPATIAL && OP == OP_HVP && MAT == FEM_NEO_HOOKEAN;
+  // NH HVP in the deformed configuration (FEM_HVP_SPATIAL): see the HVP branch below; the
+  // streamed form has no coordinates and runs the material form (F = I + H, F^-T, ln J)
+  constexpr bool SPATIAL = FEM_HVP_SPATIAL && OP == OP_HVP && MAT == FEM_NEO_HOOKEAN && !STREAM;
   // NH residual with F^-T G_a from the same deformed geometry (FEM_RES_SPATIAL)
-  constexpr bool SPATIAL_R = FEM_RES_SPATIAL && OP == OP_RESIDUAL && MAT == FEM_NEO_HOOKEAN;
+  constexpr bool SPATIAL_R = FEM_RES_SPATIAL && OP == OP_RESIDUAL && MAT == FEM_NEO_HOOKEAN && !STREAM;
   const int64_t e = t * kTile + tid;
   if (e < A.E) {
     const ushort4 lc4 = reinterpret_cast<const ushort4 *>(m + A.off_lconn)[tid];
     const int lc[4] = {lc4.x, lc4.y, lc4.z, lc4.w};
-    double x[NEN][D], c[D][D];
+    double x[NEN][D], c[D][D], det;
+    if constexpr (STREAM) {  // Alg. 1's gathered geometry: c_a = det G_a, det J
 #pragma unroll
-    for (int a = 0; a < NEN; ++a)
+      for (int a = 0; a < D; ++a)
 #pragma unroll
-      for (int i = 0; i < D; ++i) x[a][i] = xs[lc[a] * D + i];
-    const double det = cof_gradients<D>(x, c);
+        for (int j = 0; j < D; ++j) c[a][j] = gs[(a * D + j) * kTile + tid];
+      det = gs[D * D * kTile + tid];
+    } else {
+#pragma unroll
+      for (int a = 0; a < NEN; ++a)
+#pragma unroll
+        for (int i = 0; i < D; ++i) x[a][i] = xs[lc[a] * D + i];
+      det = cof_gradients<D>(x, c);
+    }
     const double id = fem_rcp(det);
     constexpr double inv_fact = (D == 3) ? 1.0 / 6.0 : 0.5;  // vol = det / d!
     double lam = A.lam, mu = A.mu;
@@ -1085,6 +1108,21 @@ __device__ __forceinline__ void mb_wait(uint64_t *m, unsigned parity) {
       : "memory");
 }
 
+// TMA bulk copy (non-tensor) global -> shared, completing on an mbarrier with a byte count
+__device__ __forceinline__ void mb_expect_tx(uint64_t *m, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_addr(m)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned bytes, uint64_t *m) {
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+          smem_addr(dst)),
+      "l"(src), "r"(bytes), "r"(smem_addr(m))
+      : "memory");
+}
+
 #ifndef FEM_RES_DEC
 #define FEM_RES_DEC 0
 #endif
@@ -1093,7 +1131,8 @@ __device__ __forceinline__ void mb_wait(uint64_t *m, unsigned parity) {
 #endif
 template <int OP>
 constexpr bool pipe_decoupled() {
-  return op_is_hvp<OP>() || (FEM_RES_DEC && OP == OP_RESIDUAL) || (FEM_ENERGY_DEC && OP == OP_ENERGY);
+  return (op_is_hvp<OP>() && !op_streams<OP>()) || (FEM_RES_DEC && OP == OP_RESIDUAL) ||
+         (FEM_ENERGY_DEC && OP == OP_ENERGY);
 }
 
 template <int D, int MAT, int OP, bool MASK, bool DET>
@@ -1101,17 +1140,27 @@ __global__ void __launch_bounds__(kTile, pipe_minb(OP, MAT, D)) k_tile_pipe(Pipe
   constexpr bool NEED_U = op_needs_u<OP, MAT>();
   constexpr int NF = 1 + (NEED_U ? 1 : 0) + (op_is_hvp<OP>() ? 1 : 0);
   constexpr bool DEC = pipe_decoupled<OP>();
+  constexpr bool STREAM = op_streams<OP>();
+  constexpr unsigned GBYTES = sizeof(double) * geom_words(D) * kTile;
   extern __shared__ __align__(16) unsigned char sm[];
-  __shared__ __align__(8) uint64_t mb_meta[3], mb_node[2];
+  __shared__ __align__(8) uint64_t mb_meta[3], mb_node[2], mb_geom[2];
   const int tid = threadIdx.x;
   const int mb = A.mb, um = A.um;
   const int nstride = um * D * NF;
   unsigned char *metab = sm;
   double *nodeb = reinterpret_cast<double *>(sm + 3 * mb);
   double *contrib = nodeb + 2 * nstride;
+  double *geomb = contrib + (DEC ? 2 : 1) * ((D + 1) * D * kTile);  // STREAM: 2 blocks
   const int64_t G = gridDim.x;
 
   auto tile_id = [&](int64_t i) -> int64_t { return A.list ? (int64_t)__ldg(A.list + i) : i; };
+  auto issue_geom = [&](int64_t t, int b) {  // one TMA bulk copy of the tile's geometry block
+    if (tid == 0) {
+      mb_expect_tx(&mb_geom[b], GBYTES);
+      bulk_g2s(geomb + b * (GBYTES / 8), A.geom + tile_id(t) * (int64_t)(GBYTES / 8), GBYTES,
+               &mb_geom[b]);
+    }
+  };
   auto issue_meta = [&](int64_t t, int b) {
     unsigned char *dst = metab + b * mb;
     const unsigned char *src = A.meta + tile_id(t) * (int64_t)mb;
@@ -1127,7 +1176,7 @@ __global__ void __launch_bounds__(kTile, pipe_minb(OP, MAT, D)) k_tile_pipe(Pipe
         const int64_t g = (int64_t)nodes[r] * D;
 #pragma unroll
         for (int c = 0; c < D; ++c) {
-          cp_async8(dst + r * D + c, A.coords + g + c);
+          if constexpr (!STREAM) cp_async8(dst + r * D + c, A.coords + g + c);
           if constexpr (NEED_U) cp_async8(dst + um * D + r * D + c, A.u + g + c);
           if constexpr (op_is_hvp<OP>()) cp_async8(dst + (NF - 1) * um * D + r * D + c, A.v + g + c);
         }
@@ -1135,7 +1184,7 @@ __global__ void __launch_bounds__(kTile, pipe_minb(OP, MAT, D)) k_tile_pipe(Pipe
     } else {
       for (int i = tid; i < U * D; i += kTile) {
         const int64_t g = (int64_t)nodes[i / D] * D + (i % D);
-        cp_async8(dst + i, A.coords + g);
+        if constexpr (!STREAM) cp_async8(dst + i, A.coords + g);
         if constexpr (NEED_U) cp_async8(dst + um * D + i, A.u + g);
         if constexpr (op_is_hvp<OP>()) cp_async8(dst + (NF - 1) * um * D + i, A.v + g);
       }
@@ -1177,24 +1226,37 @@ __global__ void __launch_bounds__(kTile, pipe_minb(OP, MAT, D)) k_tile_pipe(Pipe
     }
     asm volatile("cp.async.wait_all;\n" ::: "memory");
   } else {
+    if constexpr (STREAM) {
+      if (tid == 0) {
+        for (int b = 0; b < 2; ++b) mb_init(&mb_geom[b], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+      }
+      __syncthreads();
+    }
     if (t < A.n_tiles) {
       issue_meta(t, 0);
       cp_async_commit();
       cp_async_wait_all();
       __syncthreads();
       issue_nodes(metab, 0);
+      if constexpr (STREAM) issue_geom(t, 0);
       if (t + G < A.n_tiles) issue_meta(t + G, 1);
       cp_async_commit();
     }
     for (int k = 0; t < A.n_tiles; ++k, t += G) {
       cp_async_wait_all();
       __syncthreads();
+      if constexpr (STREAM) mb_wait(&mb_geom[k & 1], (unsigned)(k >> 1) & 1u);
       const unsigned char *m = metab + (k % 3) * mb;
       const double *nb = nodeb + (k & 1) * nstride;
-      if (t + G < A.n_tiles) issue_nodes(metab + ((k + 1) % 3) * mb, (k + 1) & 1);
+      if (t + G < A.n_tiles) {
+        issue_nodes(metab + ((k + 1) % 3) * mb, (k + 1) & 1);
+        if constexpr (STREAM) issue_geom(t + G, (k + 1) & 1);
+      }
       if (t + 2 * G < A.n_tiles) issue_meta(t + 2 * G, (k + 2) % 3);
       cp_async_commit();
-      tile_phase1<D, MAT, OP, MASK>(A, m, nb, nb + um * D, nb + (NF - 1) * um * D, tile_id(t), tid, contrib, eacc);
+      tile_phase1<D, MAT, OP, MASK>(A, m, nb, nb + um * D, nb + (NF - 1) * um * D, tile_id(t), tid, contrib, eacc,
+                                    STREAM ? geomb + (k & 1) * (GBYTES / 8) : nullptr);
       if constexpr (op_has_p2<OP>()) {
         __syncthreads();
         tile_phase2<D, OP, DET>(A, m, reinterpret_cast<const int *>(m)[0], tile_id(t), tid, contrib);
@@ -1240,7 +1302,8 @@ static fem_status launch_pipe_t(Problem *p, const PipeArgs &a, cudaStream_t s) {
   const bool need_u = op_needs_u<OP, MAT>();
   const int nf = 1 + (need_u ? 1 : 0) + (op_is_hvp<OP>() ? 1 : 0);
   const size_t smem = (size_t)3 * T.mb + sizeof(double) * 2 * (size_t)T.um * D * nf +
-                      (!op_has_p2<OP>() ? 0 : (pipe_decoupled<OP>() ? 2 : 1) * sizeof(double) * (size_t)(D + 1) * D * kTile);
+                      (!op_has_p2<OP>() ? 0 : (pipe_decoupled<OP>() ? 2 : 1) * sizeof(double) * (size_t)(D + 1) * D * kTile) +
+                      (op_streams<OP>() ? 2 * sizeof(double) * geom_words(D) * kTile : 0);
   auto kern = k_tile_pipe<D, MAT, OP, MASK, DET>;
   FEM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   kern<<<pipe_grid(p, OP, a.n_tiles), kTile, smem, s>>>(a);
@@ -1256,6 +1319,44 @@ static fem_status launch_pipe_op(Problem *p, const PipeArgs &a, cudaStream_t s) 
   }
   if (p->material == FEM_LINEAR_ELASTIC) return launch_pipe_t<3, FEM_LINEAR_ELASTIC, OP, MASK, DET>(p, a, s);
   return launch_pipe_t<3, FEM_NEO_HOOKEAN, OP, MASK, DET>(p, a, s);
+}
+
+// Streamed geometry (FEM_STREAM_GEOM): per tile one contiguous SoA block {c_a[j] (D x D),
+// det J} x kTile elements in tile order, computed once from the coordinates (same cofactor
+// arithmetic as the recompute path), loaded per tile by one TMA bulk copy.
+template <int D>
+__global__ void k_geom_stream(const double *coords, const int32_t *conn, const int32_t *perm,
+                              int64_t E, int64_t n_slots, double *geom) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_slots;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t t = i / kTile, l = i % kTile;
+    double *g = geom + t * geom_words(D) * kTile + l;
+    if (i >= E) {
+      for (int w = 0; w < D * D; ++w) g[w * kTile] = 0.0;
+      g[D * D * kTile] = 1.0;
+      continue;
+    }
+    const int64_t e = perm[i];
+    double x[D + 1][D], c[D][D];
+    for (int a = 0; a <= D; ++a)
+      for (int j = 0; j < D; ++j) x[a][j] = coords[(int64_t)conn[e * (D + 1) + a] * D + j];
+    const double det = cof_gradients<D>(x, c);
+    for (int a = 0; a < D; ++a)
+      for (int j = 0; j < D; ++j) g[(a * D + j) * kTile] = c[a][j];
+    g[D * D * kTile] = det;
+  }
+}
+
+fem_status build_geom_stream(Problem *p, cudaStream_t s) {
+  TileSet &T = p->tiles;
+  if (T.geom) return FEM_OK;
+  const int D = p->dim;
+  const int64_t n_slots = T.n_tiles * kTile;
+  FEM_CUDA(cudaMalloc(&T.geom, sizeof(double) * geom_words(D) * n_slots));
+  if (D == 3) k_geom_stream<3><<<grid_for(n_slots), kThreads, 0, s>>>(p->coords, p->conn, T.perm, p->n_elems, n_slots, T.geom);
+  else k_geom_stream<2><<<grid_for(n_slots), kThreads, 0, s>>>(p->coords, p->conn, T.perm, p->n_elems, n_slots, T.geom);
+  FEM_LAUNCH_CHECK("geometry stream");
+  return FEM_OK;
 }
 
 // Element pass of the residual / HVP (op = OP_RESIDUAL / OP_HVP) or the energy partials
@@ -1295,6 +1396,7 @@ fem_status tile_pass(Problem *p, int op, const double *u, const double *v, doubl
   a.err = p->d_err;
   a.lin = p->lin;
   a.lin_stride = T.n_tiles * kTile;
+  a.geom = T.geom;
   if (op == OP_ENERGY) return launch_pipe_op<OP_ENERGY, false, false>(p, a, s);
   if (op == OP_LIN) return launch_pipe_op<OP_LIN, false, false>(p, a, s);
   if (det) {
@@ -1311,6 +1413,13 @@ fem_status tile_pass(Problem *p, int op, const double *u, const double *v, doubl
       k_slot_gather<3><<<grid_for(p->n_nodes), kThreads, 0, s>>>(T.node_slot_ptr, T.node_slots, a.slots, p->n_nodes, out);
     FEM_LAUNCH_CHECK("slot gather");
     return FEM_OK;
+  }
+  if (op == OP_RESIDUAL_S || op == OP_HVP_S) {
+    st = build_geom_stream(p, s);
+    if (st) return st;
+    a.geom = T.geom;
+    if (op == OP_RESIDUAL_S) return launch_pipe_op<OP_RESIDUAL_S, false, false>(p, a, s);
+    return mask ? launch_pipe_op<OP_HVP_S, true, false>(p, a, s) : launch_pipe_op<OP_HVP_S, false, false>(p, a, s);
   }
   if (op == OP_RESIDUAL) return launch_pipe_op<OP_RESIDUAL, false, false>(p, a, s);
   if (op == OP_HVP_LIN)
@@ -1414,7 +1523,7 @@ fem_status morton_node_order(Problem *p, cudaStream_t s) {
 
 void free_tiles(TileSet &T) {
   void *bufs[] = {T.perm, T.nodes, T.U, T.ptr, T.inc, T.lconn, T.interior, T.phase, T.slot_off,
-                  T.node_slots, T.node_slot_ptr, T.epart, T.meta, T.list};
+                  T.node_slots, T.node_slot_ptr, T.epart, T.meta, T.list, T.geom};
   for (void *b : bufs)
     if (b) cudaFree(b);
   T = TileSet{};

@@ -484,6 +484,11 @@ def main():
             lambda: prob.hvp(zt, vt, bc=True, out=y, flags=fem.COLORED_SCATTER)),
         "residual_colored_scatter_ms": time_call(
             lambda: prob.residual(zt, bc=True, out=r, flags=fem.COLORED_SCATTER)),
+        # the same at tile granularity: tile-colored passes, plain boundary writes
+        "hvp_tile_colored_ms": time_call(
+            lambda: prob.hvp(zt, vt, bc=True, out=y, flags=fem.TILE_COLORED)),
+        "residual_tile_colored_ms": time_call(
+            lambda: prob.residual(zt, bc=True, out=r, flags=fem.TILE_COLORED)),
         "assemble_batched_ms": time_call(lambda: prob.assemble_csr(zt, bc=True, mode="batched", out=vals), 2),
         "assemble_rows_ms": time_call(lambda: prob.assemble_csr(zt, bc=True, mode="rows", out=vals), 2),
         "assemble_literal_ms": time_call(lambda: prob.assemble_csr(zt, bc=True, mode="literal", out=vals), 1),

@@ -93,11 +93,16 @@ enum {
                                copy — Alg. 1's per-batch gather of grad N and det J
                                 — instead of recomputing it from the coordinates.
                                Not with FEM_DETERMINISTIC / BASELINE_SCATTER / LINEARIZED. */
-  FEM_COLORED_SCATTER = 1024u /* residual / HVP: elements colored so that no two elements of
+  FEM_COLORED_SCATTER = 1024u,/* residual / HVP: elements colored so that no two elements of
                                a color share a node (greedy in tile order, setup); one pass
                                per color, each element adds its nodal vectors to the output
                                with plain loads / stores — conflict-free without atomics,
-                               deterministic (fixed color order).  Single GPU.            */
+                               deterministic (fixed color order).                         */
+  FEM_TILE_COLORED = 2048u  /* residual / HVP: the element tiles colored so that tiles of a
+                               color share no node; one tile pass per color, in-tile sums as
+                               usual, tile-boundary sums written with plain read-add-write
+                               instead of fp64 atomics — the color-ordered conflict-free
+                               scatter at tile granularity; deterministic.                */
 };
 
 typedef struct {

@@ -438,7 +438,9 @@ fem_status run_residual(Problem *p, const double *z, double *r, unsigned flags, 
   const bool det = flags & FEM_DETERMINISTIC;
   if (!det || p->n_elems == 0) FEM_CUDA(cudaMemsetAsync(r, 0, sizeof(double) * p->N, s));
   fem_status st;
-  if (flags & FEM_COLORED_SCATTER) {
+  if (flags & FEM_TILE_COLORED) {
+    st = tile_pass(p, OP_RESIDUAL, z, nullptr, r, false, false, nullptr, s, 3);
+  } else if (flags & FEM_COLORED_SCATTER) {
     ElemArgs a = elem_args(p);
     a.u = z;
     a.out = r;
@@ -459,7 +461,8 @@ fem_status run_residual(Problem *p, const double *z, double *r, unsigned flags, 
                            flags & FEM_LOCAL_ONLY, s);
   }
   if (st) return st;
-  if ((flags & (FEM_BASELINE_SCATTER | FEM_COLORED_SCATTER)) && p->size > 1 && !(flags & FEM_LOCAL_ONLY)) {
+  if ((flags & (FEM_BASELINE_SCATTER | FEM_COLORED_SCATTER | FEM_TILE_COLORED)) && p->size > 1 &&
+      !(flags & FEM_LOCAL_ONLY)) {
     st = halo_add(p, r, s);
     if (st) return st;
   }
@@ -488,7 +491,9 @@ fem_status run_hvp(Problem *p, const double *z, const double *v, double *y, unsi
   if (!det || p->n_elems == 0) FEM_CUDA(cudaMemsetAsync(y, 0, sizeof(double) * p->N, s));
   const bool bc = (flags & FEM_APPLY_BC) && p->n_dir;
   fem_status st;
-  if (flags & FEM_COLORED_SCATTER) {
+  if (flags & FEM_TILE_COLORED) {
+    st = tile_pass(p, OP_HVP, z, v, y, bc, false, nullptr, s, 3);
+  } else if (flags & FEM_COLORED_SCATTER) {
     ElemArgs a = elem_args(p);
     a.u = z;
     a.v = v;
@@ -519,7 +524,8 @@ fem_status run_hvp(Problem *p, const double *z, const double *v, double *y, unsi
                            flags & FEM_LOCAL_ONLY, s);
   }
   if (st) return st;
-  if ((flags & (FEM_BASELINE_SCATTER | FEM_COLORED_SCATTER)) && p->size > 1 && !(flags & FEM_LOCAL_ONLY)) {
+  if ((flags & (FEM_BASELINE_SCATTER | FEM_COLORED_SCATTER | FEM_TILE_COLORED)) && p->size > 1 &&
+      !(flags & FEM_LOCAL_ONLY)) {
     st = halo_add(p, y, s);
     if (st) return st;
   }
@@ -891,7 +897,7 @@ fem_status fem_energy_residual(fem_problem *h, const double *z, double *energy, 
   cudaStream_t s = (cudaStream_t)stream;
   // one element pass on a single GPU with the default scatter; otherwise the two calls
   if (p->size > 1 || (flags & (FEM_DETERMINISTIC | FEM_BASELINE_SCATTER | FEM_STREAM_GEOM |
-                                FEM_COLORED_SCATTER)) || p->n_elems == 0) {
+                                FEM_COLORED_SCATTER | FEM_TILE_COLORED)) || p->n_elems == 0) {
     fem_status st = fem_energy(h, z, energy, stream);
     if (st) return st;
     return run_residual(p, z, r, flags, s);

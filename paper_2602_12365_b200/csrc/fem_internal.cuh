@@ -53,6 +53,8 @@ struct TileSet {
   int64_t *node_slot_ptr = nullptr; // [n_nodes+1]
   double *epart = nullptr;       // [n_tiles] energy partials
   double *geom = nullptr;        // [n_tiles][D*D+1][kTile] cofactor rows c_a and det J (SoA per tile)
+  int32_t *tcolor_list = nullptr;  // FEM_TILE_COLORED: tiles of color c at [tcolor_off[c], ..)
+  std::vector<int64_t> tcolor_off;
   // balanced phase-2 schedule (fem_tiles.cu k_build_sched): per tile sched_rounds x kTile
   // task slots {8 cb offsets (uint16), meta = r | n << 12 | pos << 16 | g << 20}
   int sched_rounds = 0;
@@ -224,11 +226,13 @@ fem_status run_hvp(Problem *p, const double *z, const double *v, double *y, unsi
 fem_status run_spmv(Problem *p, const double *vals, const double *x, double *y, cudaStream_t s);
 fem_status halo_add(Problem *p, double *y, cudaStream_t s);
 fem_status build_tiles(Problem *p, cudaStream_t s);
-// part: 0 all tiles, 1 the tiles touching interface nodes, 2 the other tiles (TileSet::list)
+// part: 0 all tiles, 1 the tiles touching interface nodes, 2 the other tiles (TileSet::list),
+// 3 tile-colored passes with plain boundary writes (FEM_TILE_COLORED)
 fem_status tile_pass(Problem *p, int op, const double *u, const double *v, double *out, bool mask,
                      bool det, double *partials, cudaStream_t s, int part = 0);
 fem_status build_tile_lists(Problem *p, cudaStream_t s);
 fem_status build_geom_stream(Problem *p, cudaStream_t s);                // fem_tiles.cu
+fem_status build_tile_colors(Problem *p, cudaStream_t s);                // fem_tiles.cu
 fem_status halo_begin(Problem *p, const double *y, cudaStream_t s);
 fem_status halo_end(Problem *p, double *y, cudaStream_t s);
 void free_tiles(TileSet &T);

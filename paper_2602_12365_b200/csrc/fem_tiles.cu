@@ -978,10 +978,12 @@ __device__ __forceinline__ void tile_phase1(const PipeArgs &A, const unsigned ch
 
 // Phase 2: fixed-order per-tile-node sums of the contributions, stored (interior nodes),
 // RED (tile-boundary nodes) or written to the node's slot (DET).
-template <int D, bool DET>
+// Scatter mode SC of the tile-boundary nodes: 0 RED (default), 1 the node's slot (DET),
+// 2 plain read-add-write (tile-colored passes: tiles of one color share no node).
+template <int D, int SC>
 __device__ __forceinline__ void node_write(const PipeArgs &A, const unsigned char *m, int r,
                                            int64_t t, const double (&sacc)[D]) {
-  if constexpr (DET) {
+  if constexpr (SC == 1) {
     double *slot = A.slots + (A.slot_off[t] + r) * D;
 #pragma unroll
     for (int cc = 0; cc < D; ++cc) slot[cc] = sacc[cc];
@@ -991,6 +993,9 @@ __device__ __forceinline__ void node_write(const PipeArgs &A, const unsigned cha
     if (m[A.off_int + r]) {
 #pragma unroll
       for (int cc = 0; cc < D; ++cc) A.out[g + cc] = sacc[cc];
+    } else if constexpr (SC == 2) {
+#pragma unroll
+      for (int cc = 0; cc < D; ++cc) A.out[g + cc] += sacc[cc];
     } else {
 #pragma unroll
       for (int cc = 0; cc < D; ++cc) atomicAdd(A.out + g + cc, sacc[cc]);
@@ -1001,7 +1006,7 @@ __device__ __forceinline__ void node_write(const PipeArgs &A, const unsigned cha
 #if FEM_P2_BAL
 // Balanced schedule (k_build_sched): every thread sums one task of <= 8 incidences of one
 // node from precomputed offsets; the g lanes of a node combine by a shuffle tree.
-template <int D, int OP, bool DET>
+template <int D, int OP, int SC>
 __device__ __forceinline__ void tile_phase2(const PipeArgs &A, const unsigned char *m, int U,
                                             int64_t t, int tid, const double *cb) {
   const uint32_t hdr = reinterpret_cast<const uint32_t *>(m)[2];
@@ -1040,11 +1045,11 @@ __device__ __forceinline__ void tile_phase2(const PipeArgs &A, const unsigned ch
         if (take) sacc[cc] += x;
       }
     }
-    if (n > 0 && pos == 0) node_write<D, DET>(A, m, (int)(mt & 0x7ffu), t, sacc);
+    if (n > 0 && pos == 0) node_write<D, SC>(A, m, (int)(mt & 0x7ffu), t, sacc);
   }
 }
 #else
-template <int D, int OP, bool DET>
+template <int D, int OP, int SC>
 __device__ __forceinline__ void tile_phase2(const PipeArgs &A, const unsigned char *m, int U,
                                             int64_t t, int tid, const double *cb) {
   const uint16_t *ptr = reinterpret_cast<const uint16_t *>(m + A.off_ptr);
@@ -1074,7 +1079,7 @@ __device__ __forceinline__ void tile_phase2(const PipeArgs &A, const unsigned ch
     double sacc[D];
 #pragma unroll
     for (int cc = 0; cc < D; ++cc) sacc[cc] = s0[cc] + s1[cc];
-    node_write<D, DET>(A, m, r, t, sacc);
+    node_write<D, SC>(A, m, r, t, sacc);
   }
 }
 #endif
@@ -1135,7 +1140,7 @@ constexpr bool pipe_decoupled() {
          (FEM_ENERGY_DEC && OP == OP_ENERGY);
 }
 
-template <int D, int MAT, int OP, bool MASK, bool DET>
+template <int D, int MAT, int OP, bool MASK, int SC>
 __global__ void __launch_bounds__(kTile, pipe_minb(OP, MAT, D)) k_tile_pipe(PipeArgs A) {
   constexpr bool NEED_U = op_needs_u<OP, MAT>();
   constexpr int NF = 1 + (NEED_U ? 1 : 0) + (op_is_hvp<OP>() ? 1 : 0);
@@ -1222,7 +1227,7 @@ __global__ void __launch_bounds__(kTile, pipe_minb(OP, MAT, D)) k_tile_pipe(Pipe
       __syncthreads();  // phase 1 of tile k done; tile k-1 fully consumed
       if (t + 2 * G < A.n_tiles) issue_meta(t + 2 * G, (k + 2) % 3);
       if constexpr (op_has_p2<OP>())
-        tile_phase2<D, OP, DET>(A, m, reinterpret_cast<const int *>(m)[0], tile_id(t), tid, cb);
+        tile_phase2<D, OP, SC>(A, m, reinterpret_cast<const int *>(m)[0], tile_id(t), tid, cb);
     }
     asm volatile("cp.async.wait_all;\n" ::: "memory");
   } else {
@@ -1259,7 +1264,7 @@ __global__ void __launch_bounds__(kTile, pipe_minb(OP, MAT, D)) k_tile_pipe(Pipe
                                     STREAM ? geomb + (k & 1) * (GBYTES / 8) : nullptr);
       if constexpr (op_has_p2<OP>()) {
         __syncthreads();
-        tile_phase2<D, OP, DET>(A, m, reinterpret_cast<const int *>(m)[0], tile_id(t), tid, contrib);
+        tile_phase2<D, OP, SC>(A, m, reinterpret_cast<const int *>(m)[0], tile_id(t), tid, contrib);
       }
       __syncthreads();
     }
@@ -1296,7 +1301,7 @@ static int pipe_grid(Problem *p, int op, int64_t n = -1) {
   return (int)std::max<int64_t>(1, std::min<int64_t>(n < 0 ? p->tiles.n_tiles : n, 148 * pipe_minb(op, p->material, p->dim)));
 }
 
-template <int D, int MAT, int OP, bool MASK, bool DET>
+template <int D, int MAT, int OP, bool MASK, int SC>
 static fem_status launch_pipe_t(Problem *p, const PipeArgs &a, cudaStream_t s) {
   const TileSet &T = p->tiles;
   const bool need_u = op_needs_u<OP, MAT>();
@@ -1304,21 +1309,21 @@ static fem_status launch_pipe_t(Problem *p, const PipeArgs &a, cudaStream_t s) {
   const size_t smem = (size_t)3 * T.mb + sizeof(double) * 2 * (size_t)T.um * D * nf +
                       (!op_has_p2<OP>() ? 0 : (pipe_decoupled<OP>() ? 2 : 1) * sizeof(double) * (size_t)(D + 1) * D * kTile) +
                       (op_streams<OP>() ? 2 * sizeof(double) * geom_words(D) * kTile : 0);
-  auto kern = k_tile_pipe<D, MAT, OP, MASK, DET>;
+  auto kern = k_tile_pipe<D, MAT, OP, MASK, SC>;
   FEM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   kern<<<pipe_grid(p, OP, a.n_tiles), kTile, smem, s>>>(a);
   FEM_LAUNCH_CHECK("tile pipeline kernel");
   return FEM_OK;
 }
 
-template <int OP, bool MASK, bool DET>
+template <int OP, bool MASK, int SC>
 static fem_status launch_pipe_op(Problem *p, const PipeArgs &a, cudaStream_t s) {
   if (p->dim == 2) {
-    if (p->material == FEM_LINEAR_ELASTIC) return launch_pipe_t<2, FEM_LINEAR_ELASTIC, OP, MASK, DET>(p, a, s);
-    return launch_pipe_t<2, FEM_NEO_HOOKEAN, OP, MASK, DET>(p, a, s);
+    if (p->material == FEM_LINEAR_ELASTIC) return launch_pipe_t<2, FEM_LINEAR_ELASTIC, OP, MASK, SC>(p, a, s);
+    return launch_pipe_t<2, FEM_NEO_HOOKEAN, OP, MASK, SC>(p, a, s);
   }
-  if (p->material == FEM_LINEAR_ELASTIC) return launch_pipe_t<3, FEM_LINEAR_ELASTIC, OP, MASK, DET>(p, a, s);
-  return launch_pipe_t<3, FEM_NEO_HOOKEAN, OP, MASK, DET>(p, a, s);
+  if (p->material == FEM_LINEAR_ELASTIC) return launch_pipe_t<3, FEM_LINEAR_ELASTIC, OP, MASK, SC>(p, a, s);
+  return launch_pipe_t<3, FEM_NEO_HOOKEAN, OP, MASK, SC>(p, a, s);
 }
 
 // Streamed geometry (FEM_STREAM_GEOM): per tile one contiguous SoA block {c_a[j] (D x D),
@@ -1359,6 +1364,51 @@ fem_status build_geom_stream(Problem *p, cudaStream_t s) {
   return FEM_OK;
 }
 
+// Tile coloring (FEM_TILE_COLORED): greedy in tile (Morton) order, a tile takes the smallest
+// color none of its nodes' earlier tiles holds (per-node 128-bit masks over the tiles' node
+// lists, a host pass at setup).  Tiles of one color share no node, so a pass over them
+// writes the tile-boundary sums with plain read-add-write: the color-ordered conflict-free
+// scatter at tile granularity (each tile keeps its in-tile reduction and its locality).
+fem_status build_tile_colors(Problem *p, cudaStream_t s) {
+  TileSet &T = p->tiles;
+  if (T.tcolor_list) return FEM_OK;
+  const int64_t nt = T.n_tiles;
+  std::vector<int32_t> U(nt), nodes((size_t)nt * T.maxe);
+  FEM_CUDA(cudaMemcpyAsync(U.data(), T.U, sizeof(int32_t) * nt, cudaMemcpyDeviceToHost, s));
+  FEM_CUDA(cudaMemcpyAsync(nodes.data(), T.nodes, sizeof(int32_t) * nodes.size(), cudaMemcpyDeviceToHost, s));
+  FEM_CUDA(cudaStreamSynchronize(s));
+  std::vector<uint64_t> mask((size_t)p->n_nodes * 2, 0ull);
+  std::vector<uint8_t> col(nt);
+  std::vector<int64_t> cnt(129, 0);
+  int nc = 0;
+  for (int64_t t = 0; t < nt; ++t) {
+    uint64_t m0 = 0, m1 = 0;
+    const int32_t *nd = nodes.data() + t * T.maxe;
+    for (int r = 0; r < U[t]; ++r) {
+      m0 |= mask[2 * (int64_t)nd[r]];
+      m1 |= mask[2 * (int64_t)nd[r] + 1];
+    }
+    const int c = ~m0 ? __builtin_ctzll(~m0) : (~m1 ? 64 + __builtin_ctzll(~m1) : 128);
+    if (c >= 128) {
+      set_error("FEM_TILE_COLORED: more than 128 tile colors");
+      return FEM_ERR_TOO_MANY_COLORS;
+    }
+    for (int r = 0; r < U[t]; ++r) mask[2 * (int64_t)nd[r] + (c >> 6)] |= 1ull << (c & 63);
+    col[t] = (uint8_t)c;
+    ++cnt[c + 1];
+    nc = std::max(nc, c + 1);
+  }
+  T.tcolor_off.assign(nc + 1, 0);
+  for (int c = 0; c < nc; ++c) T.tcolor_off[c + 1] = T.tcolor_off[c] + cnt[c + 1];
+  std::vector<int32_t> list(nt);
+  std::vector<int64_t> fill(T.tcolor_off.begin(), T.tcolor_off.end() - 1);
+  for (int64_t t = 0; t < nt; ++t) list[fill[col[t]]++] = (int32_t)t;
+  FEM_CUDA(cudaMalloc(&T.tcolor_list, sizeof(int32_t) * (nt > 0 ? nt : 1)));
+  FEM_CUDA(cudaMemcpyAsync(T.tcolor_list, list.data(), sizeof(int32_t) * nt, cudaMemcpyHostToDevice, s));
+  FEM_CUDA(cudaStreamSynchronize(s));
+  return FEM_OK;
+}
+
 // Element pass of the residual / HVP (op = OP_RESIDUAL / OP_HVP) or the energy partials
 // (OP_ENERGY: one partial per CTA into `partials`, *n_partials set).
 fem_status tile_pass(Problem *p, int op, const double *u, const double *v, double *out,
@@ -1370,7 +1420,7 @@ fem_status tile_pass(Problem *p, int op, const double *u, const double *v, doubl
   PipeArgs a{};
   a.meta = T.meta;
   a.n_tiles = T.n_tiles;
-  if (part) {  // one of the two halves of TileSet::list (no DET, no energy)
+  if (part == 1 || part == 2) {  // one of the two halves of TileSet::list (no DET, no energy)
     if (T.n_boundary < 0 || det || op == OP_ENERGY) return FEM_ERR_INVALID_ARG;
     a.list = T.list + (part == 1 ? 0 : T.n_boundary);
     a.n_tiles = part == 1 ? T.n_boundary : T.n_tiles - T.n_boundary;
@@ -1397,15 +1447,28 @@ fem_status tile_pass(Problem *p, int op, const double *u, const double *v, doubl
   a.lin = p->lin;
   a.lin_stride = T.n_tiles * kTile;
   a.geom = T.geom;
-  if (op == OP_ENERGY) return launch_pipe_op<OP_ENERGY, false, false>(p, a, s);
-  if (op == OP_LIN) return launch_pipe_op<OP_LIN, false, false>(p, a, s);
+  if (part == 3) {  // tile-colored passes (FEM_TILE_COLORED): plain writes, no atomics
+    if (det || (op != OP_RESIDUAL && op != OP_HVP)) return FEM_ERR_INVALID_ARG;
+    st = build_tile_colors(p, s);
+    if (st) return st;
+    for (size_t c = 0; c + 1 < T.tcolor_off.size(); ++c) {
+      a.list = T.tcolor_list + T.tcolor_off[c];
+      a.n_tiles = T.tcolor_off[c + 1] - T.tcolor_off[c];
+      if (op == OP_RESIDUAL) st = launch_pipe_op<OP_RESIDUAL, false, 2>(p, a, s);
+      else st = mask ? launch_pipe_op<OP_HVP, true, 2>(p, a, s) : launch_pipe_op<OP_HVP, false, 2>(p, a, s);
+      if (st) return st;
+    }
+    return FEM_OK;
+  }
+  if (op == OP_ENERGY) return launch_pipe_op<OP_ENERGY, false, 0>(p, a, s);
+  if (op == OP_LIN) return launch_pipe_op<OP_LIN, false, 0>(p, a, s);
   if (det) {
     st = ensure(p->slotbuf, sizeof(double) * T.n_slots * p->dim);
     if (st) return st;
     a.slots = (double *)p->slotbuf.ptr;
-    if (op == OP_RESIDUAL) st = launch_pipe_op<OP_RESIDUAL, false, true>(p, a, s);
-    else if (op == OP_HVP_LIN) st = mask ? launch_pipe_op<OP_HVP_LIN, true, true>(p, a, s) : launch_pipe_op<OP_HVP_LIN, false, true>(p, a, s);
-    else st = mask ? launch_pipe_op<OP_HVP, true, true>(p, a, s) : launch_pipe_op<OP_HVP, false, true>(p, a, s);
+    if (op == OP_RESIDUAL) st = launch_pipe_op<OP_RESIDUAL, false, 1>(p, a, s);
+    else if (op == OP_HVP_LIN) st = mask ? launch_pipe_op<OP_HVP_LIN, true, 1>(p, a, s) : launch_pipe_op<OP_HVP_LIN, false, 1>(p, a, s);
+    else st = mask ? launch_pipe_op<OP_HVP, true, 1>(p, a, s) : launch_pipe_op<OP_HVP, false, 1>(p, a, s);
     if (st) return st;
     if (p->dim == 2)
       k_slot_gather<2><<<grid_for(p->n_nodes), kThreads, 0, s>>>(T.node_slot_ptr, T.node_slots, a.slots, p->n_nodes, out);
@@ -1418,13 +1481,13 @@ fem_status tile_pass(Problem *p, int op, const double *u, const double *v, doubl
     st = build_geom_stream(p, s);
     if (st) return st;
     a.geom = T.geom;
-    if (op == OP_RESIDUAL_S) return launch_pipe_op<OP_RESIDUAL_S, false, false>(p, a, s);
-    return mask ? launch_pipe_op<OP_HVP_S, true, false>(p, a, s) : launch_pipe_op<OP_HVP_S, false, false>(p, a, s);
+    if (op == OP_RESIDUAL_S) return launch_pipe_op<OP_RESIDUAL_S, false, 0>(p, a, s);
+    return mask ? launch_pipe_op<OP_HVP_S, true, 0>(p, a, s) : launch_pipe_op<OP_HVP_S, false, 0>(p, a, s);
   }
-  if (op == OP_RESIDUAL) return launch_pipe_op<OP_RESIDUAL, false, false>(p, a, s);
+  if (op == OP_RESIDUAL) return launch_pipe_op<OP_RESIDUAL, false, 0>(p, a, s);
   if (op == OP_HVP_LIN)
-    return mask ? launch_pipe_op<OP_HVP_LIN, true, false>(p, a, s) : launch_pipe_op<OP_HVP_LIN, false, false>(p, a, s);
-  return mask ? launch_pipe_op<OP_HVP, true, false>(p, a, s) : launch_pipe_op<OP_HVP, false, false>(p, a, s);
+    return mask ? launch_pipe_op<OP_HVP_LIN, true, 0>(p, a, s) : launch_pipe_op<OP_HVP_LIN, false, 0>(p, a, s);
+  return mask ? launch_pipe_op<OP_HVP, true, 0>(p, a, s) : launch_pipe_op<OP_HVP, false, 0>(p, a, s);
 }
 
 int tile_energy_partials(Problem *p, int op) { return pipe_grid(p, op); }
@@ -1523,7 +1586,7 @@ fem_status morton_node_order(Problem *p, cudaStream_t s) {
 
 void free_tiles(TileSet &T) {
   void *bufs[] = {T.perm, T.nodes, T.U, T.ptr, T.inc, T.lconn, T.interior, T.phase, T.slot_off,
-                  T.node_slots, T.node_slot_ptr, T.epart, T.meta, T.list, T.geom};
+                  T.node_slots, T.node_slot_ptr, T.epart, T.meta, T.list, T.geom, T.tcolor_list};
   for (void *b : bufs)
     if (b) cudaFree(b);
   T = TileSet{};

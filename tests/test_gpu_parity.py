@@ -99,7 +99,8 @@ def test_hvp(case, bc):
     assert rel(prob.hvp(dev(z), dev(v), bc=bc), ref.hvp(z, v, bc=bc)) <= TOL
 
 
-@pytest.mark.parametrize("flag", ["DETERMINISTIC", "BASELINE_SCATTER", "STREAM_GEOM", "COLORED_SCATTER"])
+@pytest.mark.parametrize("flag", ["DETERMINISTIC", "BASELINE_SCATTER", "STREAM_GEOM", "COLORED_SCATTER",
+                                  "TILE_COLORED"])
 def test_residual_hvp_modes(case, fem, flag):
     name, mesh, prob, ref, z, v = case
     f = getattr(fem, flag)
@@ -107,7 +108,7 @@ def test_residual_hvp_modes(case, fem, flag):
     y1 = prob.hvp(dev(z), dev(v), bc=True, flags=f).cpu().numpy()
     assert rel(r1, ref.residual(z, bc=True)) <= TOL
     assert rel(y1, ref.hvp(z, v, bc=True)) <= TOL
-    if flag in ("DETERMINISTIC", "COLORED_SCATTER"):   # fixed summation orders
+    if flag in ("DETERMINISTIC", "COLORED_SCATTER", "TILE_COLORED"):   # fixed summation orders
         assert np.array_equal(r1, prob.residual(dev(z), bc=True, flags=f).cpu().numpy())
         assert np.array_equal(y1, prob.hvp(dev(z), dev(v), bc=True, flags=f).cpu().numpy())
 
@@ -283,10 +284,10 @@ def test_full_size_sampled_parity(fem, oracle_mod, cfg):
         assert np.abs(y[rows] - yr).max() <= TOL * np.abs(y).max()
         prob.linearize(zt)
         for f in (fem.DETERMINISTIC, fem.BASELINE_SCATTER, fem.LINEARIZED, fem.STREAM_GEOM,
-                  fem.COLORED_SCATTER):  # other HVP modes
+                  fem.COLORED_SCATTER, fem.TILE_COLORED):  # other HVP modes
             yf = prob.hvp(zt, vt, bc=bc, flags=f).cpu().numpy()
             assert np.abs(yf[rows] - yr).max() <= TOL * np.abs(y).max()
-        for f in (fem.STREAM_GEOM, fem.COLORED_SCATTER):   # other residual modes
+        for f in (fem.STREAM_GEOM, fem.COLORED_SCATTER, fem.TILE_COLORED):   # other residual modes
             rf = prob.residual(zt, bc=bc, flags=f).cpu().numpy()
             assert np.abs(rf[rows] - rr).max() <= TOL * np.abs(r).max()
     # tangent and residual patch tests at full size (exact on any P1 mesh)

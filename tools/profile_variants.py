@@ -31,7 +31,9 @@ calls = {
     "hvp_s": lambda: prob.hvp(zt, vt, bc=True, out=y, flags=fem.STREAM_GEOM),
     "hvp_col": lambda: prob.hvp(zt, vt, bc=True, out=y, flags=fem.COLORED_SCATTER),
     "hvp_atomic": lambda: prob.hvp(zt, vt, bc=True, out=y, flags=fem.BASELINE_SCATTER),
+    "hvp_tcol": lambda: prob.hvp(zt, vt, bc=True, out=y, flags=fem.TILE_COLORED),
     "res": lambda: prob.residual(zt, bc=True, out=y),
+    "res_tcol": lambda: prob.residual(zt, bc=True, out=y, flags=fem.TILE_COLORED),
     "res_s": lambda: prob.residual(zt, bc=True, out=y, flags=fem.STREAM_GEOM),
     "res_col": lambda: prob.residual(zt, bc=True, out=y, flags=fem.COLORED_SCATTER),
     "energy": lambda: prob.energy(zt),

@@ -98,11 +98,15 @@ enum {
                                per color, each element adds its nodal vectors to the output
                                with plain loads / stores — conflict-free without atomics,
                                deterministic (fixed color order).                         */
-  FEM_TILE_COLORED = 2048u  /* residual / HVP: the element tiles colored so that tiles of a
+  FEM_TILE_COLORED = 2048u, /* residual / HVP: the element tiles colored so that tiles of a
                                color share no node; one tile pass per color, in-tile sums as
                                usual, tile-boundary sums written with plain read-add-write
                                instead of fp64 atomics — the color-ordered conflict-free
                                scatter at tile granularity; deterministic.                */
+  FEM_ASSEMBLE_COLORED = 4096u /* fem_assemble_csr: Alg. 2 in fused form — one pass per node
+                               color; each seed node's D colored columns are evaluated from
+                               its incident elements and written straight to their CSR slots
+                               (conflict-free plain stores), no J_comp.  No multipliers.   */
 };
 
 typedef struct {
@@ -204,6 +208,10 @@ fem_status fem_color(fem_problem *p, int32_t *colors, int32_t *n_colors, fem_str
  *            lax.scan), then a decompression kernel;
  *   FEM_ASSEMBLE_JCOMP: all color passes in ONE element sweep (the passes are
  *            independent), accumulating J_comp with atomics, then decompression;
+ *   FEM_ASSEMBLE_COLORED: C/D node-color passes; every seed node's D columns K e_j are
+ *            gathered from its incident elements and stored at their decompressed slots
+ *            (Alg. 2 fused: compress and decompress in one step, no J_comp; the columns of
+ *            one color never share a slot, so no atomics);
  *   FEM_ASSEMBLE_ROWS: NOT Alg. 2: the row-owner gather form of the element-Hessian
  *            assembly (the sum of element Hessians, which
  *            Alg. 2 reproduces exactly).  Each node's D rows sum the tangent blocks

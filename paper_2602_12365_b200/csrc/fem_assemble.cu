@@ -339,6 +339,7 @@ struct RowArgs {
   int dim;
   double *vals;
   int *err;
+  const uint8_t *tslot;         // TR: position of n in the adjacency of its slot-s neighbour
 };
 
 template <int D>
@@ -380,7 +381,15 @@ __device__ __forceinline__ int64_t rp_row(const RowArgs &A, int64_t n, int i) {
   return __ldg(A.row_ptr + n * (int64_t)A.dim + i);
 }
 
-template <int D>
+// TR (FEM_ASSEMBLE_COLORED): the fused colored form of Alg. 2.  node_order lists the seed
+// nodes of ONE node color; for seed n the warp evaluates K e_j for its D seed DOFs j (the
+// columns n D + k) from the incident elements and writes each compressed entry directly at
+// its decompressed CSR slot (row m D + i, column n D + k) — no J_comp.  Within a color no
+// two seeds share a row (distance-2), and every (row, column) slot belongs to one seed, so
+// the writes are conflict-free plain stores.  By the symmetry of every element Hessian the
+// column block K[m, n] is the transpose of the row block the row form computes, so the same
+// warp code produces it; only where it is written changes.
+template <int D, bool TR = false>
 __global__ void __launch_bounds__(kRowLanes * kRowGroups, FEM_ROWS_MINB) k_rows_fused(RowArgs A) {
   constexpr int NEN = D + 1, BS = D * D;
   __shared__ __align__(16) double stage[kRowGroups][kRowLanes][NEN * BS + 1];  // +1: no bank conflicts
@@ -473,7 +482,12 @@ __global__ void __launch_bounds__(kRowLanes * kRowGroups, FEM_ROWS_MINB) k_rows_
         for (int q = 0; q < BS; ++q) acc[q] = 0.0;
         if (!first) {
 #pragma unroll
-          for (int q = 0; q < BS; ++q) acc[q] = A.vals[rp_row(A, n, q / D) + (int64_t)s * D + q % D];
+          for (int q = 0; q < BS; ++q) {
+            if constexpr (TR)  // partial sums of earlier chunks at the transposed slot
+              acc[q] = A.vals[rp_row(A, A.nadj[a0 + s], q % D) + (int64_t)A.tslot[a0 + s] * D + q / D];
+            else
+              acc[q] = A.vals[rp_row(A, n, q / D) + (int64_t)s * D + q % D];
+          }
         }
         for (int c = so[s]; c < so[s + 1]; ++c) {
           const int ent = sl[c];
@@ -485,15 +499,30 @@ __global__ void __launch_bounds__(kRowLanes * kRowGroups, FEM_ROWS_MINB) k_rows_
         }
         const int32_t m = A.nadj[a0 + s];
         const unsigned bcm = (last && A.node_bc) ? A.node_bc[m] : 0u;
-#pragma unroll
-        for (int i = 0; i < D; ++i) {
-          const int64_t base = rp_row(A, n, i) + (int64_t)s * D;
+        if constexpr (TR) {  // K[m D + k, n D + i] = K[n D + i, m D + k]
+          const int64_t ts = A.tslot[a0 + s];
 #pragma unroll
           for (int k = 0; k < D; ++k) {
-            double v = acc[i * D + k];
-            if (last && ((bcm >> k) & 1u)) v = 0.0;     // masked column
-            if (last && ((bcn >> i) & 1u)) v = 0.0;     // identity row (off-diagonal)
-            A.vals[base + k] = v;
+            const int64_t base = rp_row(A, m, k) + ts * D;
+#pragma unroll
+            for (int i = 0; i < D; ++i) {
+              double v = acc[i * D + k];
+              if (last && ((bcm >> k) & 1u)) v = 0.0;   // identity row of (m, k) (off-diagonal)
+              if (last && ((bcn >> i) & 1u)) v = 0.0;   // masked column (n, i)
+              A.vals[base + i] = v;
+            }
+          }
+        } else {
+#pragma unroll
+          for (int i = 0; i < D; ++i) {
+            const int64_t base = rp_row(A, n, i) + (int64_t)s * D;
+#pragma unroll
+            for (int k = 0; k < D; ++k) {
+              double v = acc[i * D + k];
+              if (last && ((bcm >> k) & 1u)) v = 0.0;     // masked column
+              if (last && ((bcn >> i) & 1u)) v = 0.0;     // identity row (off-diagonal)
+              A.vals[base + k] = v;
+            }
           }
         }
       }
@@ -656,9 +685,97 @@ static void launch_colored(const AsmArgs &a, bool literal, int pass, cudaStream_
   else k_colored_hvp<D, MAT, false><<<grid, kThreads, 0, s>>>(a, pass);
 }
 
+// tslot[nadj_ptr[n] + s] = index of n in the (sorted) adjacency of its s-th neighbour
+__global__ void k_transpose_slots(const int64_t *nadj_ptr, const int32_t *nadj, int64_t n_nodes,
+                                  uint8_t *tslot) {
+  for (int64_t n = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; n < n_nodes;
+       n += (int64_t)gridDim.x * blockDim.x)
+    for (int64_t q = nadj_ptr[n]; q < nadj_ptr[n + 1]; ++q) {
+      const int32_t m = nadj[q];
+      int64_t lo = nadj_ptr[m], hi = nadj_ptr[m + 1];
+      while (hi - lo > 1) {
+        const int64_t mid = (lo + hi) / 2;
+        if (nadj[mid] <= n) lo = mid;
+        else hi = mid;
+      }
+      tslot[q] = (uint8_t)(lo - nadj_ptr[m]);
+    }
+}
+
+// FEM_ASSEMBLE_COLORED: setup (node colors from the DOF coloring, color = colors[n D] / D;
+// seed lists per color in Morton order; transposed slots; slot lists) and one launch of
+// k_rows_fused<D, true> per node color.
+static fem_status assemble_colored(Problem *p, const double *z, double *vals, bool bc,
+                                   cudaStream_t s) {
+  if (p->n_mpc) {
+    set_error("FEM_ASSEMBLE_COLORED: multipliers not supported (use the default row form)");
+    return FEM_ERR_INVALID_ARG;
+  }
+  fem_status st = build_slot_lists(p, s);   // also the Morton node order
+  if (st) return st;
+  const int D = p->dim;
+  if (!p->ncolor_list) {
+    std::vector<int32_t> col((size_t)p->N), order((size_t)p->n_nodes);
+    FEM_CUDA(cudaMemcpyAsync(col.data(), p->colors, sizeof(int32_t) * p->N, cudaMemcpyDeviceToHost, s));
+    FEM_CUDA(cudaMemcpyAsync(order.data(), p->node_order, sizeof(int32_t) * p->n_nodes, cudaMemcpyDeviceToHost, s));
+    FEM_CUDA(cudaStreamSynchronize(s));
+    const int ncol = (p->n_colors + D - 1) / D;
+    std::vector<int64_t> cnt(ncol + 1, 0);
+    for (int64_t n = 0; n < p->n_nodes; ++n) ++cnt[col[n * D] / D + 1];
+    p->ncolor_off.assign(ncol + 1, 0);
+    for (int c = 0; c < ncol; ++c) p->ncolor_off[c + 1] = p->ncolor_off[c] + cnt[c + 1];
+    std::vector<int64_t> fill(p->ncolor_off.begin(), p->ncolor_off.end() - 1);
+    std::vector<int32_t> list((size_t)p->n_nodes);
+    for (int64_t q = 0; q < p->n_nodes; ++q) {
+      const int32_t n = order[q];
+      list[fill[col[(int64_t)n * D] / D]++] = n;
+    }
+    FEM_CUDA(cudaMalloc(&p->ncolor_list, sizeof(int32_t) * (p->n_nodes > 0 ? p->n_nodes : 1)));
+    FEM_CUDA(cudaMemcpyAsync(p->ncolor_list, list.data(), sizeof(int32_t) * p->n_nodes, cudaMemcpyHostToDevice, s));
+    int64_t nadj_total = 0;
+    FEM_CUDA(cudaMemcpyAsync(&nadj_total, p->nadj_ptr + p->n_nodes, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    FEM_CUDA(cudaStreamSynchronize(s));
+    FEM_CUDA(cudaMalloc(&p->tslot, nadj_total > 0 ? nadj_total : 1));
+    k_transpose_slots<<<grid_for(p->n_nodes), kThreads, 0, s>>>(p->nadj_ptr, p->nadj, p->n_nodes, p->tslot);
+    FEM_LAUNCH_CHECK("transposed slots");
+  }
+  RowArgs A{};
+  A.node_bc = bc ? p->node_bc : nullptr; A.z = z;
+  A.inc_ptr = p->inc_ptr; A.inc = p->inc; A.nadj_ptr = p->nadj_ptr; A.nadj = p->nadj;
+  A.slot_list = p->slot_list; A.slot_off = p->slot_off;
+  A.row_ptr = p->row_ptr; A.n_u = p->n_u; A.vals = vals; A.err = p->d_err; A.dim = D;
+  A.tslot = p->tslot;
+  const int st_ctx = D == 3 ? ctx_stride<3>() : ctx_stride<2>();
+  st = ensure(p->ctxbuf, sizeof(double) * (size_t)st_ctx * (p->n_elems > 0 ? p->n_elems : 1));
+  if (st) return st;
+  A.ctx = (const double *)p->ctxbuf.ptr;
+  if (p->n_elems) {   // tangent contexts in caller element order (p->inc indexes them)
+    const int ge = grid_for(p->n_elems, kCtxThreads);
+    double *ctx = (double *)p->ctxbuf.ptr;
+    if (D == 2) {
+      if (p->material == FEM_LINEAR_ELASTIC) k_elem_ctx<2, FEM_LINEAR_ELASTIC><<<ge, kCtxThreads, 0, s>>>(p->coords, p->conn, p->n_elems, p->lam, p->mu, p->phase, p->lam_tab, p->mu_tab, z, nullptr, ctx, p->d_err);
+      else k_elem_ctx<2, FEM_NEO_HOOKEAN><<<ge, kCtxThreads, 0, s>>>(p->coords, p->conn, p->n_elems, p->lam, p->mu, p->phase, p->lam_tab, p->mu_tab, z, nullptr, ctx, p->d_err);
+    } else {
+      if (p->material == FEM_LINEAR_ELASTIC) k_elem_ctx<3, FEM_LINEAR_ELASTIC><<<ge, kCtxThreads, 0, s>>>(p->coords, p->conn, p->n_elems, p->lam, p->mu, p->phase, p->lam_tab, p->mu_tab, z, nullptr, ctx, p->d_err);
+      else k_elem_ctx<3, FEM_NEO_HOOKEAN><<<ge, kCtxThreads, 0, s>>>(p->coords, p->conn, p->n_elems, p->lam, p->mu, p->phase, p->lam_tab, p->mu_tab, z, nullptr, ctx, p->d_err);
+    }
+  }
+  for (size_t c = 0; c + 1 < p->ncolor_off.size(); ++c) {
+    A.node_order = p->ncolor_list + p->ncolor_off[c];
+    A.n_nodes = p->ncolor_off[c + 1] - p->ncolor_off[c];
+    if (A.n_nodes == 0) continue;
+    const int grid = grid_for(A.n_nodes, kRowGroups, 148 * 64);
+    if (D == 2) k_rows_fused<2, true><<<grid, kRowLanes * kRowGroups, 0, s>>>(A);
+    else k_rows_fused<3, true><<<grid, kRowLanes * kRowGroups, 0, s>>>(A);
+  }
+  FEM_LAUNCH_CHECK("fused colored assembly");
+  return FEM_OK;
+}
+
 static fem_status assemble(Problem *p, const double *z, double *vals, unsigned flags,
                            cudaStream_t s) {
   const bool bc = (flags & FEM_APPLY_BC) && p->n_dir;
+  if (flags & FEM_ASSEMBLE_COLORED) return assemble_colored(p, z, vals, bc, s);
   if (flags & FEM_ASSEMBLE_SCATTER) {
     FEM_CUDA(cudaMemsetAsync(vals, 0, sizeof(double) * (size_t)p->nnz, s));
     AsmArgs a{};

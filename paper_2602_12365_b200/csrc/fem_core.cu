@@ -820,6 +820,8 @@ fem_status fem_destroy(fem_problem *h) {
   if (p->cap_stream) cudaStreamDestroy(p->cap_stream);
   if (p->lin) cudaFree(p->lin);
   if (p->ecolor_list) cudaFree(p->ecolor_list);
+  if (p->ncolor_list) cudaFree(p->ncolor_list);
+  if (p->tslot) cudaFree(p->tslot);
   free_tiles(p->tiles);
   dist_free(p);
   delete h;

@@ -111,6 +111,11 @@ struct Problem {
   uint8_t *slot_list = nullptr; // fused assembly: per node (l << 2 | b) grouped by CSR slot
   uint16_t *slot_off = nullptr; // [nnz_node + n_nodes] slot offsets into each node's list
   int32_t *node_order = nullptr; // [n_nodes] Morton order of the nodes (assembly)
+  // FEM_ASSEMBLE_COLORED: seed nodes grouped by node color (Morton order within a color) and
+  // the transposed slot of each adjacency entry (fem_assemble.cu assemble_colored)
+  int32_t *ncolor_list = nullptr;
+  std::vector<int64_t> ncolor_off;
+  uint8_t *tslot = nullptr;
   // row-pull assembly plan (fem_rows.cu build_row_plan), indexed by the position in
   // node_order; fixed strides es (block entries) and ss (off-diagonal slots + 1)
   int rp_state = 0;              // 0 not built, 1 built, -1 mesh not eligible (fallback)

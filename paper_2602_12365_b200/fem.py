@@ -28,6 +28,7 @@ ASSEMBLE_LITERAL = 4
 ASSEMBLE_JCOMP = 32
 ASSEMBLE_ROWS = 64
 ASSEMBLE_SCATTER = 128
+ASSEMBLE_COLORED = 4096
 LINEARIZED = 256
 BASELINE_SCATTER = 8
 STREAM_GEOM = 512          # residual / HVP from the streamed per-element geometry (Alg. 1)
@@ -325,6 +326,7 @@ class Problem:
         z = self._vec(z, "z")
         flags = (APPLY_BC if bc else 0) | {"batched": ASSEMBLE_JCOMP, "literal": ASSEMBLE_LITERAL,
                                              "rows": ASSEMBLE_ROWS, "scatter": ASSEMBLE_SCATTER,
+                                             "colored": ASSEMBLE_COLORED,
                                              "auto": 0}[mode]
         nnz = self.nnz()
         out = self._out(out, nnz)

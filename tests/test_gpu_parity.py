@@ -129,10 +129,12 @@ def test_coloring_bit_exact(case):
     assert np.array_equal(colors.cpu().numpy(), rcol)
 
 
-@pytest.mark.parametrize("mode", ["batched", "literal", "rows", "scatter"])
+@pytest.mark.parametrize("mode", ["batched", "literal", "rows", "scatter", "colored"])
 @pytest.mark.parametrize("bc", [False, True])
 def test_assembly(case, mode, bc):
     name, mesh, prob, ref, z, v = case
+    if mode == "colored" and mesh.n_mpc:
+        pytest.skip("fused colored form: node-color seeds, no multiplier columns")
     vals = prob.assemble_csr(dev(z), bc=bc, mode=mode)
     assert rel(vals, ref.assemble_alg2(z, bc=bc)) <= TOL
 
@@ -309,7 +311,7 @@ def test_full_size_sampled_parity(fem, oracle_mod, cfg):
     srow = sampled_rows(mesh.n_total, 300, 6)
     ref_vals = ref.csr_rows(z, srow, rp_n, ci_n, bc=True)
     idx = np.concatenate([np.arange(rp_n[r], rp_n[r + 1]) for r in srow])
-    for mode in ("rows", "batched", "scatter"):
+    for mode in ("rows", "batched", "scatter", "colored"):
         vals = prob.assemble_csr(zt, bc=True, mode=mode).cpu().numpy()
         assert np.abs(vals[idx] - ref_vals).max() <= TOL * np.abs(vals).max()
         del vals

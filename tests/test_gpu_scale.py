@@ -113,7 +113,7 @@ def test_cfg4_one_gpu_nnz_above_2_31(fem, oracle_mod):
     assert 80 <= nc <= 100
     ref_vals = oracle_csr_rows(ref, z, srow, lo, hi, cols, N, bc=True)
     vals = torch.empty(int(rp[-1]), dtype=torch.float64, device="cuda")
-    for mode in ("rows", "scatter"):
+    for mode in ("rows", "scatter", "colored"):
         prob.assemble_csr(zt, bc=True, mode=mode, out=vals)
         vmax = float(vals.abs().max())
         assert np.abs(vals[idx].cpu().numpy() - ref_vals).max() <= TOL * vmax
@@ -155,7 +155,7 @@ def test_unstructured_3d_delaunay_1e5_dofs(fem, oracle_mod):
     rcol, rnc = ref.colors()
     assert nc == rnc and np.array_equal(colors.cpu().numpy(), rcol)
     ve = ref.assemble_elem(z, bc=True)
-    for mode in ("rows", "batched", "scatter"):
+    for mode in ("rows", "batched", "scatter", "colored"):
         assert rel(prob.assemble_csr(zt, bc=True, mode=mode), ve) <= TOL
     vals = prob.assemble_csr(zt, bc=True)
     assert rel(prob.spmv(vals, vt), ref.hvp(z, v, bc=True)) <= TOL

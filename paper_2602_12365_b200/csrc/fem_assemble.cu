@@ -1013,12 +1013,14 @@ extern "C" {
 
 fem_status fem_assemble_csr(fem_problem *h, const double *z, double *vals, unsigned flags,
                             fem_stream stream) {
+  FEM_NVTX_RANGE("fem_assemble_csr");
   FEM_ARG(h && z && vals, "fem_assemble_csr: null argument");
   return run_assemble(&h->p, z, vals, flags, (cudaStream_t)stream);
 }
 
 fem_status fem_spmv(fem_problem *h, const double *vals, const double *x, double *y,
                     fem_stream stream) {
+  FEM_NVTX_RANGE("fem_spmv");
   FEM_ARG(h && vals && x && y, "fem_spmv: null argument");
   FEM_ARG(h->p.have_pattern, "fem_spmv: call fem_sparsity first");
   FEM_ARG(x != y, "fem_spmv: x and y alias");

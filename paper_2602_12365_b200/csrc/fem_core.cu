@@ -692,6 +692,7 @@ const char *fem_version(void) { return "fem-b200 0.1 (sm_100a)"; }
 
 fem_status fem_create(fem_problem **out, const fem_mesh_desc *d, const fem_dist_desc *dist,
                       fem_stream stream) {
+  FEM_NVTX_RANGE("fem_create");
   FEM_ARG(out && d, "fem_create: null argument");
   *out = nullptr;
   FEM_ARG(d->dim == 2 || d->dim == 3, "fem_create: dim must be 2 or 3");
@@ -807,6 +808,7 @@ fem_status fem_create(fem_problem **out, const fem_mesh_desc *d, const fem_dist_
 }
 
 fem_status fem_destroy(fem_problem *h) {
+  FEM_NVTX_RANGE("fem_destroy");
   if (!h) return FEM_OK;
   Problem *p = &h->p;
   void *bufs[] = {p->coords, p->conn, p->phase, p->lam_tab, p->mu_tab, p->node_bc, p->dir_dofs,
@@ -838,12 +840,14 @@ fem_status fem_query(const fem_problem *h, int64_t *n_total, int64_t *nnz, int32
 }
 
 fem_status fem_check(fem_problem *h, fem_stream stream) {
+  FEM_NVTX_RANGE("fem_check");
   FEM_ARG(h, "fem_check: null problem");
   FEM_CUDA(cudaGetLastError());
   return read_error_word(&h->p, (cudaStream_t)stream);
 }
 
 fem_status fem_apply_dirichlet(fem_problem *h, double *z, fem_stream stream) {
+  FEM_NVTX_RANGE("fem_apply_dirichlet");
   FEM_ARG(h && z, "fem_apply_dirichlet: null argument");
   Problem *p = &h->p;
   if (p->n_dir)
@@ -876,6 +880,7 @@ static fem_status energy_finish(Problem *p, const double *z, double *energy, int
 }
 
 fem_status fem_energy(fem_problem *h, const double *z, double *energy, fem_stream stream) {
+  FEM_NVTX_RANGE("fem_energy");
   FEM_ARG(h && z && energy, "fem_energy: null argument");
   Problem *p = &h->p;
   cudaStream_t s = (cudaStream_t)stream;
@@ -893,6 +898,7 @@ fem_status fem_energy(fem_problem *h, const double *z, double *energy, fem_strea
 
 fem_status fem_energy_residual(fem_problem *h, const double *z, double *energy, double *r,
                                unsigned flags, fem_stream stream) {
+  FEM_NVTX_RANGE("fem_energy_residual");
   FEM_ARG(h && z && energy && r, "fem_energy_residual: null argument");
   FEM_ARG(z != r, "fem_energy_residual: z and r alias");
   Problem *p = &h->p;
@@ -917,6 +923,7 @@ fem_status fem_energy_residual(fem_problem *h, const double *z, double *energy, 
 
 fem_status fem_residual(fem_problem *h, const double *z, double *r, unsigned flags,
                         fem_stream stream) {
+  FEM_NVTX_RANGE("fem_residual");
   FEM_ARG(h && z && r, "fem_residual: null argument");
   FEM_ARG(z != r, "fem_residual: z and r alias");
   return run_residual(&h->p, z, r, flags, (cudaStream_t)stream);
@@ -924,6 +931,7 @@ fem_status fem_residual(fem_problem *h, const double *z, double *r, unsigned fla
 
 fem_status fem_hvp(fem_problem *h, const double *z, const double *v, double *y, unsigned flags,
                    fem_stream stream) {
+  FEM_NVTX_RANGE("fem_hvp");
   FEM_ARG(h && z && v && y, "fem_hvp: null argument");
   FEM_ARG(v != y && z != y, "fem_hvp: output aliases an input");
   return run_hvp(&h->p, z, v, y, flags, (cudaStream_t)stream);
@@ -931,6 +939,7 @@ fem_status fem_hvp(fem_problem *h, const double *z, const double *v, double *y, 
 
 fem_status fem_mean_stress(fem_problem *h, const double *z, double *sigma, double *volume,
                            fem_stream stream) {
+  FEM_NVTX_RANGE("fem_mean_stress");
   FEM_ARG(h && z && sigma, "fem_mean_stress: null argument");
   Problem *p = &h->p;
   cudaStream_t s = (cudaStream_t)stream;
@@ -968,6 +977,7 @@ fem_status fem_mean_stress(fem_problem *h, const double *z, double *sigma, doubl
 
 fem_status fem_add_traction(fem_problem *h, int64_t n_facets, const int32_t *facets,
                             const double *traction, fem_stream stream) {
+  FEM_NVTX_RANGE("fem_add_traction");
   FEM_ARG(h && n_facets >= 0, "fem_add_traction: bad arguments");
   FEM_ARG(n_facets == 0 || (facets && traction), "fem_add_traction: null facets / traction");
   Problem *p = &h->p;
@@ -998,6 +1008,7 @@ fem_status fem_add_traction(fem_problem *h, int64_t n_facets, const int32_t *fac
 }
 
 fem_status fem_add_body_force(fem_problem *h, const double *b, fem_stream stream) {
+  FEM_NVTX_RANGE("fem_add_body_force");
   FEM_ARG(h && b, "fem_add_body_force: null argument");
   Problem *p = &h->p;
   cudaStream_t s = (cudaStream_t)stream;
@@ -1020,6 +1031,7 @@ fem_status fem_add_body_force(fem_problem *h, const double *b, fem_stream stream
 }
 
 fem_status fem_get_fext(fem_problem *h, double *f, fem_stream stream) {
+  FEM_NVTX_RANGE("fem_get_fext");
   FEM_ARG(h && f, "fem_get_fext: null argument");
   Problem *p = &h->p;
   cudaStream_t s = (cudaStream_t)stream;
@@ -1029,6 +1041,7 @@ fem_status fem_get_fext(fem_problem *h, double *f, fem_stream stream) {
 }
 
 fem_status fem_linearize(fem_problem *h, const double *z, fem_stream stream) {
+  FEM_NVTX_RANGE("fem_linearize");
   FEM_ARG(h && z, "fem_linearize: null argument");
   return run_linearize(&h->p, z, (cudaStream_t)stream);
 }

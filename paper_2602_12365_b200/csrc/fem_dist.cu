@@ -209,6 +209,7 @@ fem_status fem_nccl_unique_id(unsigned char id[128]) {
 }
 
 fem_status fem_nccl_comm_init(const unsigned char id[128], int rank, int size, void **comm) {
+  FEM_NVTX_RANGE("fem_nccl_comm_init");
   FEM_ARG(id && comm && size > 0 && rank >= 0 && rank < size, "fem_nccl_comm_init: bad args");
   ncclUniqueId u;
   for (int i = 0; i < 128; ++i) u.internal[i] = (char)id[i];
@@ -220,32 +221,38 @@ fem_status fem_nccl_comm_init(const unsigned char id[128], int rank, int size, v
 }
 
 fem_status fem_nccl_comm_count(void *comm, int *count) {
+  FEM_NVTX_RANGE("fem_nccl_comm_count");
   FEM_ARG(comm && count, "fem_nccl_comm_count: null argument");
   return nccl_status(ncclCommCount((ncclComm_t)comm, count), "ncclCommCount");
 }
 
 fem_status fem_nccl_comm_destroy(void *comm) {
+  FEM_NVTX_RANGE("fem_nccl_comm_destroy");
   if (!comm) return FEM_OK;
   return nccl_status(ncclCommDestroy((ncclComm_t)comm), "ncclCommDestroy");
 }
 
 fem_status fem_allreduce_sum(fem_problem *h, double *buf, int n, fem_stream stream) {
+  FEM_NVTX_RANGE("fem_allreduce_sum");
   FEM_ARG(h && buf && n > 0, "fem_allreduce_sum: bad args");
   return allreduce(&h->p, buf, n, (cudaStream_t)stream);
 }
 
 fem_status fem_halo_size(const fem_problem *h, int64_t *n_doubles) {
+  FEM_NVTX_RANGE("fem_halo_size");
   FEM_ARG(h && n_doubles, "fem_halo_size: null argument");
   *n_doubles = h->p.n_halo_entries * h->p.dim;
   return FEM_OK;
 }
 
 fem_status fem_halo_pack(fem_problem *h, const double *y, double *sendbuf, fem_stream stream) {
+  FEM_NVTX_RANGE("fem_halo_pack");
   FEM_ARG(h && y && sendbuf, "fem_halo_pack: null argument");
   return halo_pack(&h->p, y, sendbuf, (cudaStream_t)stream);
 }
 
 fem_status fem_halo_combine(fem_problem *h, double *y, const double *recvbuf, fem_stream stream) {
+  FEM_NVTX_RANGE("fem_halo_combine");
   FEM_ARG(h && y && recvbuf, "fem_halo_combine: null argument");
   return halo_combine(&h->p, y, recvbuf, (cudaStream_t)stream);
 }

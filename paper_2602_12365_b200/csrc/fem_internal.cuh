@@ -13,7 +13,28 @@
 
 #include "../../include/fem.h"
 
+// NVTX ranges around every C-ABI call (nsys / ncu --nvtx timelines); header-only NVTX v3,
+// no-ops without an attached tool.  FEM_NVTX=0 compiles them out.
+#ifndef FEM_NVTX
+#define FEM_NVTX 1
+#endif
+#if FEM_NVTX
+#include <nvtx3/nvToolsExt.h>
+#endif
+
 namespace fem {
+
+#if FEM_NVTX
+struct NvtxScope {
+  explicit NvtxScope(const char *name) { nvtxRangePushA(name); }
+  ~NvtxScope() { nvtxRangePop(); }
+};
+#define FEM_NVTX_RANGE(name) ::fem::NvtxScope fem_nvtx_scope_(name)
+#else
+#define FEM_NVTX_RANGE(name) \
+  do {                       \
+  } while (0)
+#endif
 
 enum : int { ERRW_INVERTED = 1, ERRW_TOO_MANY_COLORS = 2, ERRW_NONFINITE = 4, ERRW_ADJ_OVERFLOW = 8 };
 

@@ -16,7 +16,9 @@ namespace fem {
 
 fem_status run_assemble(Problem *p, const double *z, double *vals, unsigned flags, cudaStream_t s);
 
-enum { S_RZ0 = 0, S_RZ1 = 1, S_PAP = 2, S_BB = 3, S_RR0 = 4, S_RR1 = 5, S_NRM = 6 };
+// CG scalars: for slot parity c, rz at 2c and rr at 2c + 1 (adjacent: one 2-double
+// all-reduce per iteration on multi-GPU problems)
+enum { S_RZ0 = 0, S_RR0 = 1, S_RZ1 = 2, S_RR1 = 3, S_PAP = 4, S_BB = 5, S_NRM = 6 };
 
 __global__ void k_sub(const double *b, const double *Ax, double *r, int64_t n) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
@@ -255,9 +257,7 @@ fem_status run_cg(Problem *p, const double *z, const double *vals, const double 
     k_cg_start<<<nb, kThreads, 0, s>>>(r, dinv, zv, pp, n, part_a, part_b, own, p->dim);
   }
   k_final_sum2<<<1, kThreads, 0, s>>>(part_a, part_b, blk ? nbb : nb, p->scal + S_RR0, p->scal + S_RZ0);
-  st = allreduce(p, p->scal + S_RR0, 1, s);
-  if (st) return st;
-  st = allreduce(p, p->scal + S_RZ0, 1, s);
+  st = allreduce(p, p->scal + S_RZ0, 2, s);   // rz and rr
   if (st) return st;
   st = launch_dot(p, b, b, n, p->scal + S_BB, s);
   if (st) return st;
@@ -281,44 +281,55 @@ fem_status run_cg(Problem *p, const double *z, const double *vals, const double 
     sb = launch_dot(p, pp, Ap, n, p->scal + S_PAP, s);
     if (sb) return sb;
     if (blk) {
-      if (D == 3) k_cg_block<3, false><<<nbb, kThreads, 0, s>>>(p->scal, S_RZ0 + cur, x, r, zv, pp, Ap, dinv, nn, part_a, part_b);
-      else k_cg_block<2, false><<<nbb, kThreads, 0, s>>>(p->scal, S_RZ0 + cur, x, r, zv, pp, Ap, dinv, nn, part_a, part_b);
+      if (D == 3) k_cg_block<3, false><<<nbb, kThreads, 0, s>>>(p->scal, S_RZ0 + 2 * cur, x, r, zv, pp, Ap, dinv, nn, part_a, part_b);
+      else k_cg_block<2, false><<<nbb, kThreads, 0, s>>>(p->scal, S_RZ0 + 2 * cur, x, r, zv, pp, Ap, dinv, nn, part_a, part_b);
     } else {
-      k_cg_update<<<nb, kThreads, 0, s>>>(p->scal, S_RZ0 + cur, x, r, zv, pp, Ap, dinv, n, part_a,
+      k_cg_update<<<nb, kThreads, 0, s>>>(p->scal, S_RZ0 + 2 * cur, x, r, zv, pp, Ap, dinv, n, part_a,
                                           part_b, own, p->dim);
     }
-    k_final_sum2<<<1, kThreads, 0, s>>>(part_a, part_b, blk ? nbb : nb, p->scal + S_RR0 + (cur ^ 1),
-                                        p->scal + S_RZ0 + (cur ^ 1));
-    sb = allreduce(p, p->scal + S_RR0 + (cur ^ 1), 1, s);
+    const int nxt = 2 * (cur ^ 1);
+    k_final_sum2<<<1, kThreads, 0, s>>>(part_a, part_b, blk ? nbb : nb, p->scal + S_RR0 + nxt,
+                                        p->scal + S_RZ0 + nxt);
+    sb = allreduce(p, p->scal + S_RZ0 + nxt, 2, s);   // rz and rr of the new residual
     if (sb) return sb;
-    sb = allreduce(p, p->scal + S_RZ0 + (cur ^ 1), 1, s);
-    if (sb) return sb;
-    k_cg_dir<<<grid_for(n), kThreads, 0, s>>>(p->scal, S_RZ0 + cur, S_RZ0 + (cur ^ 1), zv, pp, n);
+    k_cg_dir<<<grid_for(n), kThreads, 0, s>>>(p->scal, S_RZ0 + 2 * cur, S_RZ0 + nxt, zv, pp, n);
     FEM_LAUNCH_CHECK("cg iteration");
     return FEM_OK;
   };
   // Between host checks the iterations run as a CUDA graph of two iterations (the slot
-  // parity pattern repeats every 2), captured once per solve on a single GPU: ~10 kernel
-  // launches per iteration become one graph launch per pair (small problems are
-  // launch-bound).  Multi-GPU solves (NCCL inside the body) launch kernels directly.
-  const bool graphs = p->size == 1 && every >= 2 && !getenv("FEM_NO_GRAPHS");
+  // parity pattern repeats every 2), captured once per solve: ~10 kernel launches per
+  // iteration become one graph launch per pair (small problems are launch-bound).  On a
+  // multi-GPU problem the NCCL all-reduces and the halo exchange (forked onto the comm
+  // stream and joined by events) are captured with the kernels; if the capture is refused
+  // the iterations launch directly (FEM_NO_GRAPHS forces that).
+  bool graphs = every >= 2 && !getenv("FEM_NO_GRAPHS");
   cudaGraphExec_t exec = nullptr;
   cudaGraph_t graph = nullptr;
   while (true) {
     if (rn <= tol) { rep->converged = 1; break; }
     if (it >= o->max_iter) { result = FEM_ERR_NOT_CONVERGED; break; }
     const int todo = std::min(every - it % every, o->max_iter - it);  // until the next check
-    if (graphs && (it & 1) == 0 && todo >= 2) {
-      if (!exec) {  // captured on a private stream (the legacy default stream cannot capture)
-        if (!p->cap_stream) FEM_CUDA(cudaStreamCreateWithFlags(&p->cap_stream, cudaStreamNonBlocking));
-        FEM_CUDA(cudaStreamBeginCapture(p->cap_stream, cudaStreamCaptureModeRelaxed));
-        fem_status sc = body(0, p->cap_stream);
-        if (!sc) sc = body(1, p->cap_stream);
-        cudaError_t ce = cudaStreamEndCapture(p->cap_stream, &graph);
-        if (sc) return sc;
-        FEM_CUDA(ce);
-        FEM_CUDA(cudaGraphInstantiate(&exec, graph, 0));
+    if (graphs && !exec && (it & 1) == 0 && todo >= 2) {
+      // captured on a private stream (the legacy default stream cannot capture)
+      if (!p->cap_stream) FEM_CUDA(cudaStreamCreateWithFlags(&p->cap_stream, cudaStreamNonBlocking));
+      FEM_CUDA(cudaStreamBeginCapture(p->cap_stream, cudaStreamCaptureModeRelaxed));
+      fem_status sc = body(0, p->cap_stream);
+      if (!sc) sc = body(1, p->cap_stream);
+      cudaError_t ce = cudaStreamEndCapture(p->cap_stream, &graph);
+      if (!sc && ce == cudaSuccess) ce = cudaGraphInstantiate(&exec, graph, 0);
+      if (sc || ce != cudaSuccess) {
+        if (p->size == 1) {
+          if (sc) return sc;
+          FEM_CUDA(ce);
+        }
+        (void)cudaGetLastError();  // multi-GPU: capture refused -> direct launches
+        if (graph) cudaGraphDestroy(graph);
+        graph = nullptr;
+        exec = nullptr;
+        graphs = false;
       }
+    }
+    if (exec && (it & 1) == 0 && todo >= 2) {
       for (int k = 0; k < todo / 2; ++k) FEM_CUDA(cudaGraphLaunch(exec, s));
       it += 2 * (todo / 2);
       if (todo & 1) {
@@ -335,7 +346,7 @@ fem_status run_cg(Problem *p, const double *z, const double *vals, const double 
       st = read_scalars(p, 8, s);
       if (st) return st;
       if (!(p->h_scal[S_PAP] > 0.0)) { result = FEM_ERR_CG_BREAKDOWN; break; }
-      rn = std::sqrt(p->h_scal[S_RR0 + (it & 1)]);
+      rn = std::sqrt(p->h_scal[S_RR0 + 2 * (it & 1)]);
       if (!std::isfinite(rn)) { result = FEM_ERR_NONFINITE; break; }
     }
   }
@@ -561,6 +572,7 @@ extern "C" {
 
 fem_status fem_cg_solve(fem_problem *h, const double *z, const double *vals, const double *b,
                         double *x, const fem_cg_opts *o, fem_cg_report *rep, fem_stream stream) {
+  FEM_NVTX_RANGE("fem_cg_solve");
   FEM_ARG(h && b && x && o && rep, "fem_cg_solve: null argument");
   FEM_ARG(o->op == 0 || o->op == 1, "fem_cg_solve: op must be 0 (HVP) or 1 (CSR)");
   FEM_ARG(o->op == 1 || z, "fem_cg_solve: op 0 needs z");
@@ -574,6 +586,7 @@ fem_status fem_cg_solve(fem_problem *h, const double *z, const double *vals, con
 fem_status fem_minres_solve(fem_problem *h, const double *z, const double *vals, const double *b,
                             double *x, const fem_cg_opts *o, fem_cg_report *rep,
                             fem_stream stream) {
+  FEM_NVTX_RANGE("fem_minres_solve");
   FEM_ARG(h && b && x && o && rep, "fem_minres_solve: null argument");
   FEM_ARG(o->op == 0 || o->op == 1, "fem_minres_solve: op must be 0 (HVP) or 1 (CSR)");
   FEM_ARG(o->op == 1 || z, "fem_minres_solve: op 0 needs z");
@@ -584,6 +597,7 @@ fem_status fem_minres_solve(fem_problem *h, const double *z, const double *vals,
 
 fem_status fem_newton_solve(fem_problem *h, double *z, const fem_newton_opts *o,
                             fem_newton_report *rep, fem_stream stream) {
+  FEM_NVTX_RANGE("fem_newton_solve");
   FEM_ARG(h && z && o && rep, "fem_newton_solve: null argument");
   Problem *p = &h->p;
   cudaStream_t s = (cudaStream_t)stream;

@@ -417,6 +417,7 @@ using namespace fem;
 extern "C" {
 
 fem_status fem_sparsity(fem_problem *h, int64_t *row_ptr, int32_t *col_idx, fem_stream stream) {
+  FEM_NVTX_RANGE("fem_sparsity");
   FEM_ARG(h, "fem_sparsity: null problem");
   Problem *p = &h->p;
   cudaStream_t s = (cudaStream_t)stream;
@@ -430,6 +431,7 @@ fem_status fem_sparsity(fem_problem *h, int64_t *row_ptr, int32_t *col_idx, fem_
 }
 
 fem_status fem_color(fem_problem *h, int32_t *colors, int32_t *n_colors, fem_stream stream) {
+  FEM_NVTX_RANGE("fem_color");
   FEM_ARG(h, "fem_color: null problem");
   Problem *p = &h->p;
   cudaStream_t s = (cudaStream_t)stream;

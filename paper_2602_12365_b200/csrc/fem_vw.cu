@@ -204,6 +204,7 @@ static fem_status vw_dots(VwProblem *p, const double *V, int j, const double *w,
 extern "C" {
 
 fem_status fem_vw_create(fem_vw_problem **out, const fem_vw_desc *d, fem_stream stream) {
+  FEM_NVTX_RANGE("fem_vw_create");
   FEM_ARG(out && d, "fem_vw_create: null argument");
   FEM_ARG(d->dim == 2 || d->dim == 3, "fem_vw_create: dim must be 2 or 3");
   FEM_ARG(d->n_nodes > 0 && d->n_elems >= 0 && d->coords && (d->n_elems == 0 || d->conn) && d->velocity,
@@ -265,6 +266,7 @@ fem_status fem_vw_create(fem_vw_problem **out, const fem_vw_desc *d, fem_stream 
 }
 
 fem_status fem_vw_destroy(fem_vw_problem *h) {
+  FEM_NVTX_RANGE("fem_vw_destroy");
   if (!h) return FEM_OK;
   VwProblem *p = &h->p;
   void *b[] = {p->coords, p->vel, p->lumped, p->dir_vals, p->conn, p->dir_nodes, p->is_dir,
@@ -282,6 +284,7 @@ __global__ void k_vw_lift(const int32_t *nodes, const double *vals, int64_t n, d
 }
 
 fem_status fem_vw_apply_dirichlet(fem_vw_problem *h, double *c, fem_stream stream) {
+  FEM_NVTX_RANGE("fem_vw_apply_dirichlet");
   FEM_ARG(h && c, "fem_vw_apply_dirichlet: null argument");
   VwProblem *p = &h->p;
   if (p->n_dir)
@@ -292,6 +295,7 @@ fem_status fem_vw_apply_dirichlet(fem_vw_problem *h, double *c, fem_stream strea
 
 fem_status fem_vw_residual(fem_vw_problem *h, const double *c, const double *c_old, double *r,
                            unsigned flags, fem_stream stream) {
+  FEM_NVTX_RANGE("fem_vw_residual");
   FEM_ARG(h && c && r, "fem_vw_residual: null argument");
   FEM_ARG(c != r, "fem_vw_residual: c and r alias");
   VwProblem *p = &h->p;
@@ -309,6 +313,7 @@ fem_status fem_vw_residual(fem_vw_problem *h, const double *c, const double *c_o
 
 fem_status fem_vw_jvp(fem_vw_problem *h, const double *x, double *y, unsigned flags,
                       fem_stream stream) {
+  FEM_NVTX_RANGE("fem_vw_jvp");
   FEM_ARG(h && x && y, "fem_vw_jvp: null argument");
   FEM_ARG(x != y, "fem_vw_jvp: x and y alias");
   VwProblem *p = &h->p;
@@ -318,6 +323,7 @@ fem_status fem_vw_jvp(fem_vw_problem *h, const double *x, double *y, unsigned fl
 
 fem_status fem_vw_gmres_solve(fem_vw_problem *h, const double *b, double *x,
                               const fem_gmres_opts *o, fem_cg_report *rep, fem_stream stream) {
+  FEM_NVTX_RANGE("fem_vw_gmres_solve");
   FEM_ARG(h && b && x && o && rep, "fem_vw_gmres_solve: null argument");
   FEM_ARG(o->restart >= 1 && o->restart <= kVwMaxRestart, "fem_vw_gmres_solve: restart in [1, 64]");
   VwProblem *p = &h->p;

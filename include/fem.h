@@ -257,11 +257,13 @@ fem_status fem_cg_solve(fem_problem *p, const double *z, const double *vals, con
                         double *x, const fem_cg_opts *opts, fem_cg_report *report,
                         fem_stream stream);
 
-/* Linearize the tangent at z (jax.linearize analogue): caches per element F^{-T} and ln J
- * of the neo-Hookean state (80 B / element, element-tile order; nothing for linear
- * elasticity) so FEM_LINEARIZED HVPs skip the state evaluation (measured at cfg 3: the
- * cached HVP is slower, 1.27 vs 1.05 ms — 80 B/element of HBM reads cost more than the
- * recomputed state — so fem_newton_solve only uses it with FEM_NEWTON_LINEARIZE set). */
+/* Linearize the tangent at z (jax.linearize analogue): caches per element the deformed-
+ * configuration metric form of the neo-Hookean tangent — cofactor rows of x + u, the two
+ * state scalars (mu - lam ln J, lam scaled by 1 / (d! J det J(x+u))) and mu G_a.G_b vol —
+ * 136 B per Tet4 in element-tile order (nothing for linear elasticity), so FEM_LINEARIZED
+ * HVPs skip the geometry, the log and the reciprocals (cfg 3: 0.76 ms, HBM-bound at ~69 %
+ * of the copy bandwidth, vs 0.94 ms recomputing).  fem_newton_solve linearizes at every
+ * iterate for its matrix-free CG (FEM_NEWTON_RECOMPUTE=1: recompute instead). */
 fem_status fem_linearize(fem_problem *p, const double *z, fem_stream stream);
 
 /* MINRES (Paige & Saunders) on the same BC-applied operator, for the symmetric indefinite

@@ -546,7 +546,8 @@ fem_status run_linearize(Problem *p, const double *z, cudaStream_t s) {
   }
   fem_status st = build_tiles(p, s);
   if (st) return st;
-  if (!p->lin) FEM_CUDA(cudaMalloc(&p->lin, sizeof(double) * 10 * (size_t)p->tiles.n_tiles * kTile));
+  const int W = p->dim == 3 ? 3 * 3 + 2 + 6 : 2 * 2 + 2 + 3;   // lin_words(D), fem_tiles.cu
+  if (!p->lin) FEM_CUDA(cudaMalloc(&p->lin, sizeof(double) * W * (size_t)p->tiles.n_tiles * kTile));
   st = tile_pass(p, OP_LIN, z, nullptr, nullptr, false, false, nullptr, s);
   if (st) return st;
   p->lin_valid = true;

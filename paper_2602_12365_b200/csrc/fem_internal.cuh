@@ -79,6 +79,8 @@ struct TileSet {
   // balanced phase-2 schedule (fem_tiles.cu k_build_sched): per tile sched_rounds x kTile
   // task slots {8 cb offsets (uint16), meta = r | n << 12 | pos << 16 | g << 20}
   int sched_rounds = 0;
+  int me8 = 0;                   // G8: padded incidence entries per tile (multiple of 8)
+  uint16_t *inc8 = nullptr, *ptr8 = nullptr;  // G8 staging for k_pack_meta
   uint16_t *soff = nullptr;      // [n_tiles][rounds*kTile][8]
   uint32_t *smeta = nullptr;     // [n_tiles][rounds*kTile]
   uint32_t *shdr = nullptr;      // [n_tiles] rounds | shuffle steps << 8
@@ -164,7 +166,7 @@ struct Problem {
   // color c (caller ids, tile order) at ecolor_list[ecolor_off[c] .. ecolor_off[c+1])
   int32_t *ecolor_list = nullptr;
   std::vector<int64_t> ecolor_off;
-  double *lin = nullptr;        // fem_linearize cache: [10][n_tiles*kTile] F^-T (9), ln J, SoA
+  double *lin = nullptr;        // fem_linearize cache: [lin_words(D)][n_tiles*kTile] metric-form tangent, SoA
   bool lin_valid = false;
   TileSet tiles;
   // multi-GPU (fem_dist.cu)

@@ -639,9 +639,9 @@ fem_status fem_newton_solve(fem_problem *h, double *z, const fem_newton_opts *o,
     }
     fem_cg_report cr{};
     fem_cg_opts co = o->cg;
-    // opt-in: with the state cache the HVP trades ~100 FP64 ops per element for 80 B of HBM
-    // reads and measured slower at cfg 3 (1.27 vs 1.05 ms), so Newton recomputes by default
-    if (!csr && getenv("FEM_NEWTON_LINEARIZE")) {
+    // matrix-free CG on the linearized tangent (fem_linearize: the cached metric form; cfg 3
+    // HVP 0.76 vs 0.94 ms recomputed); FEM_NEWTON_RECOMPUTE=1 recomputes the state per HVP
+    if (!csr && p->material == FEM_NEO_HOOKEAN && !getenv("FEM_NEWTON_RECOMPUTE")) {
       st = run_linearize(p, z, s);
       if (st) { result = st; break; }
       co.hvp_flags |= FEM_LINEARIZED;

@@ -58,6 +58,15 @@
 #ifndef FEM_P2_BAL
 #define FEM_P2_BAL 0
 #endif
+// Phase 2 over padded incidence groups (k_g8_fill; A/B r02 at cfg 3: HVP 0.936 -> 0.923 ms,
+// residual 0.807 -> 0.818 ms — within noise, so off by default): each node's list is padded to a multiple
+// of 8 entries (pad = a zero column of the contribution array) and stored as precomputed
+// contribution offsets, so a node thread loads 8 offsets with one 16-byte shared load and
+// then issues 8 x D independent value loads: one dependent shared-memory round trip per 8
+// incidences instead of two per 2 (the node sums were the kernels' longest dependency chain).
+#ifndef FEM_P2_G8
+#define FEM_P2_G8 0
+#endif
 // Phase 0: one thread per tile node issues the node's D-vector copies (no div / mod by D;
 // A/B r02: neutral, 0.975 vs 0.972 ms HVP)
 // NH HVP in metric form (M_ab = c_a . c_b, D_ab = dv_b . cs_a): fewer FP64 operations than
@@ -70,6 +79,11 @@
 #endif
 
 namespace fem {
+
+// row stride of the per-tile contribution array cb[(a D + c)][kCbStride]: G8 appends 8 zero
+// columns (the pad entries of the incidence groups point there)
+constexpr int kCbStride = FEM_P2_G8 ? kTile + 8 : kTile;
+static_assert(!(FEM_P2_G8 && FEM_P2_BAL), "FEM_P2_G8 and FEM_P2_BAL are alternatives");
 
 // ------------------------------------------------------------------ setup
 __global__ void k_bbox_partial(const double *coords, int64_t n, int dim, double *part) {
@@ -447,7 +461,12 @@ __global__ void k_pack_meta(TileSet T, const uint8_t *node_bc, int64_t E) {
   for (int i = threadIdx.x; i < T.um; i += blockDim.x) nodes[i] = i < U ? T.nodes[t * T.maxe + i] : 0;
   uint16_t *lc = reinterpret_cast<uint16_t *>(base + T.off_lconn);
   for (int i = threadIdx.x; i < kTile * 4; i += blockDim.x) lc[i] = T.lconn[t * kTile * 4 + i];
-  if (T.off_ptr >= 0) {
+  if (T.inc8) {
+    uint16_t *ptr = reinterpret_cast<uint16_t *>(base + T.off_ptr);
+    for (int i = threadIdx.x; i <= T.um; i += blockDim.x) ptr[i] = T.ptr8[t * (T.um + 1) + i];
+    uint16_t *inc = reinterpret_cast<uint16_t *>(base + T.off_inc);
+    for (int i = threadIdx.x; i < T.me8; i += blockDim.x) inc[i] = T.inc8[t * (int64_t)T.me8 + i];
+  } else if (T.off_ptr >= 0) {
     uint16_t *ptr = reinterpret_cast<uint16_t *>(base + T.off_ptr);
     for (int i = threadIdx.x; i <= T.um; i += blockDim.x)
       ptr[i] = i <= U ? T.ptr[t * (T.maxe + 1) + i] : (uint16_t)nvalid;
@@ -585,6 +604,44 @@ __global__ void k_build_sched(TileSet T, int rounds) {
   T.shdr[t] = (uint32_t)rounds | (uint32_t)steps << 8;
 }
 
+// G8 incidence groups: per tile node its (bank-scheduled) incidence list as contribution
+// offsets w = a D kCbStride + el, padded with kTile (a zero column) to a multiple of 8;
+// ptr8[r] = the node's first group.
+__device__ int g8_entries(const uint16_t *ptr, int U) {
+  int n8 = 0;
+  for (int r = 0; r < U; ++r) n8 += (ptr[r + 1] - ptr[r] + 7) & ~7;
+  return n8;
+}
+
+__global__ void k_g8_count(TileSet T, int *max_entries) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= T.n_tiles) return;
+  atomicMax(max_entries, g8_entries(T.ptr + t * (T.maxe + 1), T.U[t]));
+}
+
+template <int D>
+__global__ void k_g8_fill(TileSet T, int me8, uint16_t *inc8, uint16_t *ptr8) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= T.n_tiles) return;
+  const int U = T.U[t];
+  const uint16_t *ptr = T.ptr + t * (T.maxe + 1);
+  const uint16_t *inc = T.inc + t * T.maxe;
+  uint16_t *o = inc8 + t * (int64_t)me8;
+  uint16_t *pg = ptr8 + t * (int64_t)(T.um + 1);
+  int w = 0;
+  for (int r = 0; r < U; ++r) {
+    pg[r] = (uint16_t)(w / 8);
+    const int lo = ptr[r], n = ptr[r + 1] - lo, n8 = (n + 7) & ~7;
+    for (int q = 0; q < n8; ++q) {
+      const int e = q < n ? inc[lo + q] : -1;
+      o[w + q] = e < 0 ? (uint16_t)kTile : (uint16_t)((e & 3) * D * kCbStride + (e >> 2));
+    }
+    w += n8;
+  }
+  for (int r = U; r <= T.um; ++r) pg[r] = (uint16_t)(w / 8);
+  for (; w < me8; ++w) o[w] = (uint16_t)kTile;
+}
+
 fem_status pack_tile_meta(Problem *p, cudaStream_t s) {
   TileSet &T = p->tiles;
   if (FEM_P2_BAL) {
@@ -610,6 +667,22 @@ fem_status pack_tile_meta(Problem *p, cudaStream_t s) {
     FEM_LAUNCH_CHECK("tile incidence scheduling");
   }
   T.um = round_up(T.max_U > 0 ? T.max_U : 1, 8);
+  if (FEM_P2_G8) {  // padded incidence groups (k_g8_fill), staged for k_pack_meta
+    int *d_max = nullptr, h_max = 0;
+    FEM_CUDA(cudaMalloc(&d_max, sizeof(int)));
+    FEM_CUDA(cudaMemsetAsync(d_max, 0, sizeof(int), s));
+    const unsigned g = (unsigned)((T.n_tiles + 127) / 128);
+    k_g8_count<<<g, 128, 0, s>>>(T, d_max);
+    FEM_CUDA(cudaMemcpyAsync(&h_max, d_max, sizeof(int), cudaMemcpyDeviceToHost, s));
+    FEM_CUDA(cudaStreamSynchronize(s));
+    cudaFree(d_max);
+    T.me8 = round_up(std::max(h_max, 8), 8);
+    FEM_CUDA(cudaMalloc(&T.inc8, sizeof(uint16_t) * (size_t)T.me8 * T.n_tiles));
+    FEM_CUDA(cudaMalloc(&T.ptr8, sizeof(uint16_t) * (size_t)(T.um + 1) * T.n_tiles));
+    if (p->dim == 3) k_g8_fill<3><<<g, 128, 0, s>>>(T, T.me8, T.inc8, T.ptr8);
+    else k_g8_fill<2><<<g, 128, 0, s>>>(T, T.me8, T.inc8, T.ptr8);
+    FEM_LAUNCH_CHECK("phase-2 incidence groups");
+  }
   T.off_nodes = 16;
   T.off_lconn = T.off_nodes + 4 * T.um;
   if (FEM_P2_BAL) {
@@ -618,6 +691,10 @@ fem_status pack_tile_meta(Problem *p, cudaStream_t s) {
     T.off_smeta = T.off_soff + 16 * cap;
     T.off_int = T.off_smeta + 4 * cap;
     T.off_ptr = T.off_inc = -1;
+  } else if (FEM_P2_G8) {
+    T.off_ptr = T.off_lconn + 8 * kTile;
+    T.off_inc = T.off_ptr + round_up(2 * (T.um + 1), 16);
+    T.off_int = T.off_inc + round_up(2 * T.me8, 16);
   } else {
     T.off_ptr = T.off_lconn + 8 * kTile;
     T.off_inc = T.off_ptr + round_up(2 * (T.um + 1), 16);
@@ -630,6 +707,11 @@ fem_status pack_tile_meta(Problem *p, cudaStream_t s) {
   if (p->dim == 2) k_pack_meta<2><<<(unsigned)T.n_tiles, 256, 0, s>>>(T, p->node_bc, p->n_elems);
   else k_pack_meta<3><<<(unsigned)T.n_tiles, 256, 0, s>>>(T, p->node_bc, p->n_elems);
   FEM_LAUNCH_CHECK("pack tile meta");
+  if (T.inc8) {
+    FEM_CUDA(cudaStreamSynchronize(s));
+    cudaFree(T.inc8); cudaFree(T.ptr8);
+    T.inc8 = nullptr; T.ptr8 = nullptr;
+  }
   if (FEM_P2_BAL) {  // packed into the metadata blocks: the staging copies are not needed
     FEM_CUDA(cudaStreamSynchronize(s));
     cudaFree(T.soff); cudaFree(T.smeta); cudaFree(T.shdr);
@@ -684,7 +766,7 @@ struct PipeArgs {
   const double *lam_tab, *mu_tab;
   double *out, *slots, *partials;
   const int32_t *list;  // tile ids to process (null: tiles 0 .. n_tiles-1)
-  double *lin;        // linearization cache [10][lin_stride] (OP_LIN writes, OP_HVP_LIN reads)
+  double *lin;        // linearization cache [lin_words][lin_stride] (OP_LIN writes, OP_HVP_LIN reads)
   const double *geom; // OP_*_S: per-tile geometry blocks [n_tiles][D*D+1][kTile]
   int64_t lin_stride;
   int *err;
@@ -704,6 +786,12 @@ constexpr bool op_needs_u() {
          (base_op<OP>() == OP_HVP && MAT == FEM_NEO_HOOKEAN);
 }
 constexpr int geom_words(int D) { return D * D + 1; }
+template <int OP, int MAT>  // the coordinates are staged unless the geometry comes from a stream / cache
+constexpr bool op_needs_x() { return !op_streams<OP>() && !(OP == OP_HVP_LIN && MAT == FEM_NEO_HOOKEAN); }
+// fem_linearize cache per element (NH, deformed-configuration metric form of the HVP):
+// cs_a (D x D), s1 = c1 / (d! J det J(x+u)), s2 = lam / (d! J det J(x+u)), Ms (D(D+1)/2,
+// symmetric: mu (c_a . c_b) / (d! det J(x)))
+__host__ __device__ constexpr int lin_words(int D) { return D * D + 2 + D * (D + 1) / 2; }
 
 template <int D, int MAT, int OP_, bool MASK>
 __device__ __forceinline__ void tile_phase1(const PipeArgs &A, const unsigned char *m,
@@ -720,12 +808,22 @@ __device__ __forceinline__ void tile_phase1(const PipeArgs &A, const unsigned ch
   constexpr bool SPATIAL = FEM_HVP_SPATIAL && OP == OP_HVP && MAT == FEM_NEO_HOOKEAN && !STREAM;
   // NH residual with F^-T G_a from the same deformed geometry (FEM_RES_SPATIAL)
   constexpr bool SPATIAL_R = FEM_RES_SPATIAL && OP == OP_RESIDUAL && MAT == FEM_NEO_HOOKEAN && !STREAM;
+  // linearization (OP_LIN) caches the deformed-configuration metric form; the cached HVP
+  // (OP_HVP_LIN) then needs no geometry at all
+  constexpr bool LIN_S = OP == OP_LIN && MAT == FEM_NEO_HOOKEAN;
+  constexpr bool NO_GEOM = OP == OP_HVP_LIN && MAT == FEM_NEO_HOOKEAN;
   const int64_t e = t * kTile + tid;
   if (e < A.E) {
     const ushort4 lc4 = reinterpret_cast<const ushort4 *>(m + A.off_lconn)[tid];
     const int lc[4] = {lc4.x, lc4.y, lc4.z, lc4.w};
     double x[NEN][D], c[D][D], det;
-    if constexpr (STREAM) {  // Alg. 1's gathered geometry: c_a = det G_a, det J
+    if constexpr (NO_GEOM) {
+#pragma unroll
+      for (int a = 0; a < D; ++a)
+#pragma unroll
+        for (int j = 0; j < D; ++j) c[a][j] = 0.0;
+      det = 1.0;
+    } else if constexpr (STREAM) {  // Alg. 1's gathered geometry: c_a = det G_a, det J
 #pragma unroll
       for (int a = 0; a < D; ++a)
 #pragma unroll
@@ -755,7 +853,7 @@ __device__ __forceinline__ void tile_phase1(const PipeArgs &A, const unsigned ch
 #pragma unroll
         for (int i = 0; i < D; ++i) u[a][i] = us[lc[a] * D + i];
       if constexpr (SPATIAL_R) grad_hat<D>(u, c, H);  // Hh = det H (scaled where used)
-      if constexpr (SPATIAL || SPATIAL_R) {
+      if constexpr (SPATIAL || SPATIAL_R || LIN_S) {
         double xd[NEN][D];
         deformed_edges<D>(x, u, xd);
         dets = cof_gradients<D>(xd, cs);
@@ -828,14 +926,92 @@ __device__ __forceinline__ void tile_phase1(const PipeArgs &A, const unsigned ch
         }
       }
     } else if constexpr (OP == OP_LIN) {
-      if constexpr (MAT == FEM_NEO_HOOKEAN) {  // cache F^-T and ln J at this state (SoA)
-        NHState<D> s;
-        ok = nh_state<D>(H, s);
+      if constexpr (MAT == FEM_NEO_HOOKEAN) {  // the metric-form tangent at this state (SoA)
+        const double Jr = dets * id;
+        ok = Jr > 0.0;
+        const double scur = inv_fact * fem_rcp(Jr * dets);
+        const double c1 = mu - lam * fem_log(Jr);
+        const double sr = mu * id * inv_fact;
+        double *L = A.lin + e;
+        const int64_t st = A.lin_stride;
 #pragma unroll
-        for (int i = 0; i < D; ++i)
+        for (int a = 0; a < D; ++a)
 #pragma unroll
-          for (int j = 0; j < D; ++j) A.lin[(int64_t)(i * D + j) * A.lin_stride + e] = ok ? s.FiT[i][j] : 0.0;
-        A.lin[(int64_t)(D * D) * A.lin_stride + e] = ok ? s.lnJ : 0.0;
+          for (int j = 0; j < D; ++j) L[(a * D + j) * st] = ok ? cs[a][j] : 0.0;
+        L[(D * D) * st] = ok ? scur * c1 : 0.0;
+        L[(D * D + 1) * st] = ok ? scur * lam : 0.0;
+        int q = D * D + 2;
+#pragma unroll
+        for (int a = 0; a < D; ++a)
+#pragma unroll
+          for (int b = a; b < D; ++b) {
+            double t = 0.0;
+#pragma unroll
+            for (int j = 0; j < D; ++j) t = fma(c[a][j], c[b][j], t);
+            L[(q++) * st] = ok ? sr * t : 0.0;
+          }
+      }
+    } else if constexpr (NO_GEOM) {
+      // cached HVP (FEM_LINEARIZED): the HVP's metric form with cs_a, s1 = k1 / c1... read
+      // from the linearization — per element lin_words(D) loads instead of the geometry of
+      // x and x + u, the log and the reciprocals
+      const double *L = A.lin + e;
+      const int64_t st = A.lin_stride;
+      double csl[D][D], Ms[D][D];
+#pragma unroll
+      for (int a = 0; a < D; ++a)
+#pragma unroll
+        for (int j = 0; j < D; ++j) csl[a][j] = __ldg(L + (a * D + j) * st);
+      const double s1 = __ldg(L + (D * D) * st), s2 = __ldg(L + (D * D + 1) * st);
+      {
+        int q = D * D + 2;
+#pragma unroll
+        for (int a = 0; a < D; ++a)
+#pragma unroll
+          for (int b = a; b < D; ++b) Ms[a][b] = Ms[b][a] = __ldg(L + (q++) * st);
+      }
+      double dv[D][D];
+      {
+        double v0[D];
+        const unsigned bc0 = MASK ? m[A.off_bc + lc[0]] : 0u;
+#pragma unroll
+        for (int i = 0; i < D; ++i) v0[i] = (bc0 & (1u << i)) ? 0.0 : vs[lc[0] * D + i];
+#pragma unroll
+        for (int b = 0; b < D; ++b) {
+          const unsigned bc = MASK ? m[A.off_bc + lc[b + 1]] : 0u;
+#pragma unroll
+          for (int i = 0; i < D; ++i)
+            dv[b][i] = ((bc & (1u << i)) ? 0.0 : vs[lc[b + 1] * D + i]) - v0[i];
+        }
+      }
+      double Dm[D][D], tr = 0.0;
+#pragma unroll
+      for (int a = 0; a < D; ++a)
+#pragma unroll
+        for (int b = 0; b < D; ++b) {
+          double t = 0.0;
+#pragma unroll
+          for (int j = 0; j < D; ++j) t = fma(dv[b][j], csl[a][j], t);
+          Dm[a][b] = t;
+          if (a == b) tr += t;
+        }
+      const double k2 = s2 * tr;
+#pragma unroll
+      for (int a = 0; a < D; ++a)
+#pragma unroll
+        for (int b = 0; b < D; ++b) Dm[a][b] = (a == b) ? fma(s1, Dm[a][b], k2) : s1 * Dm[a][b];
+#pragma unroll
+      for (int i = 0; i < D; ++i) {
+        double s0 = 0.0;
+#pragma unroll
+        for (int a = 0; a < D; ++a) {
+          double fa = 0.0;
+#pragma unroll
+          for (int b = 0; b < D; ++b) fa = fma(Ms[a][b], dv[b][i], fma(Dm[a][b], csl[b][i], fa));
+          f[a + 1][i] = fa;
+          s0 += fa;
+        }
+        f[0][i] = -s0;
       }
     } else if constexpr (SPATIAL && FEM_HVP_MD) {
       // Deformed-configuration HVP (reading R9) in metric form.  With dv_b = v_b - v_0,
@@ -951,14 +1127,6 @@ __device__ __forceinline__ void tile_phase1(const PipeArgs &A, const unsigned ch
         }
       } else if constexpr (MAT == FEM_LINEAR_ELASTIC) {
         le_stress<D>(dH, ls, ms, S);
-      } else if constexpr (OP == OP_HVP_LIN) {  // F^-T, ln J from fem_linearize's cache
-        NHState<D> s;
-#pragma unroll
-        for (int i = 0; i < D; ++i)
-#pragma unroll
-          for (int j = 0; j < D; ++j) s.FiT[i][j] = __ldg(A.lin + (int64_t)(i * D + j) * A.lin_stride + e);
-        s.lnJ = __ldg(A.lin + (int64_t)(D * D) * A.lin_stride + e);
-        nh_dstress<D>(s, ls, ms, dH, S);
       } else {
         NHState<D> s;
         ok = nh_state<D>(H, s);
@@ -967,11 +1135,11 @@ __device__ __forceinline__ void tile_phase1(const PipeArgs &A, const unsigned ch
     }
     if (!ok) atomicOr(A.err, ERRW_INVERTED);
     if constexpr (op_has_p2<OP>()) {
-      if constexpr (!SPATIAL && !SPATIAL_R) nodal_from_c<D>(S, c, f);
+      if constexpr (!SPATIAL && !SPATIAL_R && !NO_GEOM) nodal_from_c<D>(S, c, f);
 #pragma unroll
       for (int a = 0; a < NEN; ++a)
 #pragma unroll
-        for (int i = 0; i < D; ++i) cb[(a * D + i) * kTile + tid] = ok ? f[a][i] : 0.0;
+        for (int i = 0; i < D; ++i) cb[(a * D + i) * kCbStride + tid] = ok ? f[a][i] : 0.0;
     }
   }
 }
@@ -1046,6 +1214,38 @@ __device__ __forceinline__ void tile_phase2(const PipeArgs &A, const unsigned ch
       }
     }
     if (n > 0 && pos == 0) node_write<D, SC>(A, m, (int)(mt & 0x7ffu), t, sacc);
+  }
+}
+#elif FEM_P2_G8
+// One thread per tile node; the node's entries come in groups of 8 contribution offsets
+// (16-byte loads), pad entries point at the zero columns; two interleaved partial sums.
+template <int D, int OP, int SC>
+__device__ __forceinline__ void tile_phase2(const PipeArgs &A, const unsigned char *m, int U,
+                                            int64_t t, int tid, const double *cb) {
+  const uint16_t *ptr = reinterpret_cast<const uint16_t *>(m + A.off_ptr);
+  const uint4 *grp = reinterpret_cast<const uint4 *>(m + A.off_inc);
+  for (int r = tid; r < U; r += kTile) {
+    const int g0 = ptr[r], g1 = ptr[r + 1];
+    double s0[D], s1[D];
+#pragma unroll
+    for (int cc = 0; cc < D; ++cc) s0[cc] = s1[cc] = 0.0;
+    for (int g = g0; g < g1; ++g) {
+      const uint4 o4 = grp[g];
+      const uint32_t ow[4] = {o4.x, o4.y, o4.z, o4.w};
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const double *pq = cb + ((ow[q >> 1] >> ((q & 1) * 16)) & 0xffffu);
+#pragma unroll
+        for (int cc = 0; cc < D; ++cc) {
+          if (q & 1) s1[cc] += pq[cc * kCbStride];
+          else s0[cc] += pq[cc * kCbStride];
+        }
+      }
+    }
+    double sacc[D];
+#pragma unroll
+    for (int cc = 0; cc < D; ++cc) sacc[cc] = s0[cc] + s1[cc];
+    node_write<D, SC>(A, m, r, t, sacc);
   }
 }
 #else
@@ -1143,7 +1343,10 @@ constexpr bool pipe_decoupled() {
 template <int D, int MAT, int OP, bool MASK, int SC>
 __global__ void __launch_bounds__(kTile, pipe_minb(OP, MAT, D)) k_tile_pipe(PipeArgs A) {
   constexpr bool NEED_U = op_needs_u<OP, MAT>();
-  constexpr int NF = 1 + (NEED_U ? 1 : 0) + (op_is_hvp<OP>() ? 1 : 0);
+  constexpr bool NEED_X = op_needs_x<OP, MAT>();
+  // node-data slots per stage: x (if read), u (if read), v (HVP)
+  constexpr int NF = (NEED_X ? 1 : 0) + (NEED_U ? 1 : 0) + (op_is_hvp<OP>() ? 1 : 0);
+  constexpr int UOFF = NEED_X ? 1 : 0;
   constexpr bool DEC = pipe_decoupled<OP>();
   constexpr bool STREAM = op_streams<OP>();
   constexpr unsigned GBYTES = sizeof(double) * geom_words(D) * kTile;
@@ -1155,10 +1358,14 @@ __global__ void __launch_bounds__(kTile, pipe_minb(OP, MAT, D)) k_tile_pipe(Pipe
   unsigned char *metab = sm;
   double *nodeb = reinterpret_cast<double *>(sm + 3 * mb);
   double *contrib = nodeb + 2 * nstride;
-  double *geomb = contrib + (DEC ? 2 : 1) * ((D + 1) * D * kTile);  // STREAM: 2 blocks
+  double *geomb = contrib + (DEC ? 2 : 1) * ((D + 1) * D * kCbStride);  // STREAM: 2 blocks
   const int64_t G = gridDim.x;
 
   auto tile_id = [&](int64_t i) -> int64_t { return A.list ? (int64_t)__ldg(A.list + i) : i; };
+  if constexpr (FEM_P2_G8 && op_has_p2<OP>()) {  // the pad columns read by the G8 node sums
+    for (int q = tid; q < (DEC ? 2 : 1) * (D + 1) * D * 8; q += kTile)
+      contrib[(q / 8) * kCbStride + kTile + (q % 8)] = 0.0;
+  }
   auto issue_geom = [&](int64_t t, int b) {  // one TMA bulk copy of the tile's geometry block
     if (tid == 0) {
       mb_expect_tx(&mb_geom[b], GBYTES);
@@ -1181,16 +1388,16 @@ __global__ void __launch_bounds__(kTile, pipe_minb(OP, MAT, D)) k_tile_pipe(Pipe
         const int64_t g = (int64_t)nodes[r] * D;
 #pragma unroll
         for (int c = 0; c < D; ++c) {
-          if constexpr (!STREAM) cp_async8(dst + r * D + c, A.coords + g + c);
-          if constexpr (NEED_U) cp_async8(dst + um * D + r * D + c, A.u + g + c);
+          if constexpr (NEED_X) cp_async8(dst + r * D + c, A.coords + g + c);
+          if constexpr (NEED_U) cp_async8(dst + UOFF * um * D + r * D + c, A.u + g + c);
           if constexpr (op_is_hvp<OP>()) cp_async8(dst + (NF - 1) * um * D + r * D + c, A.v + g + c);
         }
       }
     } else {
       for (int i = tid; i < U * D; i += kTile) {
         const int64_t g = (int64_t)nodes[i / D] * D + (i % D);
-        if constexpr (!STREAM) cp_async8(dst + i, A.coords + g);
-        if constexpr (NEED_U) cp_async8(dst + um * D + i, A.u + g);
+        if constexpr (NEED_X) cp_async8(dst + i, A.coords + g);
+        if constexpr (NEED_U) cp_async8(dst + UOFF * um * D + i, A.u + g);
         if constexpr (op_is_hvp<OP>()) cp_async8(dst + (NF - 1) * um * D + i, A.v + g);
       }
     }
@@ -1220,10 +1427,18 @@ __global__ void __launch_bounds__(kTile, pipe_minb(OP, MAT, D)) k_tile_pipe(Pipe
         const int bm1 = (k + 1) % 3;
         mb_wait(&mb_meta[bm1], (unsigned)((k + 1) / 3) & 1u);
         issue_nodes(metab + bm1 * mb, bn ^ 1);
+        if constexpr (OP == OP_HVP_LIN && MAT == FEM_NEO_HOOKEAN) {  // cache rows of tile k+1 -> L2
+          if (tid < lin_words(D)) {
+            const double *src = A.lin + tid * A.lin_stride + tile_id(t + G) * kTile;
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(src),
+                         "r"((unsigned)(kTile * sizeof(double)))
+                         : "memory");
+          }
+        }
       }
       const double *nb = nodeb + bn * nstride;
-      double *cb = contrib + (k & 1) * ((D + 1) * D * kTile);
-      tile_phase1<D, MAT, OP, MASK>(A, m, nb, nb + um * D, nb + (NF - 1) * um * D, tile_id(t), tid, cb, eacc);
+      double *cb = contrib + (k & 1) * ((D + 1) * D * kCbStride);
+      tile_phase1<D, MAT, OP, MASK>(A, m, nb, nb + UOFF * um * D, nb + (NF - 1) * um * D, tile_id(t), tid, cb, eacc);
       __syncthreads();  // phase 1 of tile k done; tile k-1 fully consumed
       if (t + 2 * G < A.n_tiles) issue_meta(t + 2 * G, (k + 2) % 3);
       if constexpr (op_has_p2<OP>())
@@ -1260,7 +1475,7 @@ __global__ void __launch_bounds__(kTile, pipe_minb(OP, MAT, D)) k_tile_pipe(Pipe
       }
       if (t + 2 * G < A.n_tiles) issue_meta(t + 2 * G, (k + 2) % 3);
       cp_async_commit();
-      tile_phase1<D, MAT, OP, MASK>(A, m, nb, nb + um * D, nb + (NF - 1) * um * D, tile_id(t), tid, contrib, eacc,
+      tile_phase1<D, MAT, OP, MASK>(A, m, nb, nb + UOFF * um * D, nb + (NF - 1) * um * D, tile_id(t), tid, contrib, eacc,
                                     STREAM ? geomb + (k & 1) * (GBYTES / 8) : nullptr);
       if constexpr (op_has_p2<OP>()) {
         __syncthreads();
@@ -1305,9 +1520,9 @@ template <int D, int MAT, int OP, bool MASK, int SC>
 static fem_status launch_pipe_t(Problem *p, const PipeArgs &a, cudaStream_t s) {
   const TileSet &T = p->tiles;
   const bool need_u = op_needs_u<OP, MAT>();
-  const int nf = 1 + (need_u ? 1 : 0) + (op_is_hvp<OP>() ? 1 : 0);
+  const int nf = (op_needs_x<OP, MAT>() ? 1 : 0) + (need_u ? 1 : 0) + (op_is_hvp<OP>() ? 1 : 0);
   const size_t smem = (size_t)3 * T.mb + sizeof(double) * 2 * (size_t)T.um * D * nf +
-                      (!op_has_p2<OP>() ? 0 : (pipe_decoupled<OP>() ? 2 : 1) * sizeof(double) * (size_t)(D + 1) * D * kTile) +
+                      (!op_has_p2<OP>() ? 0 : (pipe_decoupled<OP>() ? 2 : 1) * sizeof(double) * (size_t)(D + 1) * D * kCbStride) +
                       (op_streams<OP>() ? 2 * sizeof(double) * geom_words(D) * kTile : 0);
   auto kern = k_tile_pipe<D, MAT, OP, MASK, SC>;
   FEM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));

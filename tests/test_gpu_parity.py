@@ -404,8 +404,9 @@ def test_cg_graph_batches_match_direct_launches(fem, monkeypatch):
 
 
 def test_linearized_hvp_and_newton(fem, monkeypatch):
-    """fem_linearize caches F^-T, ln J at z; FEM_LINEARIZED HVPs equal the full HVP, and
-    Newton-Krylov linearizing at every iterate (opt-in) reaches the same solution."""
+    """fem_linearize caches the metric-form tangent at z; FEM_LINEARIZED HVPs equal the full
+    HVP, and Newton-Krylov linearizing at every iterate (default) reaches the same solution
+    as recomputing the state per HVP (FEM_NEWTON_RECOMPUTE)."""
     for name in ("3d-nh", "2d-nh-roller", "2d-nh-phases-fext"):
         mesh = MESHES[name]
         z = dev(fi.lift(mesh, fi.generic_state(mesh, 1)))
@@ -420,7 +421,7 @@ def test_linearized_hvp_and_newton(fem, monkeypatch):
     prob = fem.Problem(mesh)
     z0 = dev(fi.lift(mesh))
     za, ia = prob.newton_solve(z0, cg_rtol=1e-12, check_every=8)
-    monkeypatch.setenv("FEM_NEWTON_LINEARIZE", "1")
+    monkeypatch.setenv("FEM_NEWTON_RECOMPUTE", "1")
     zb, ib = prob.newton_solve(z0, cg_rtol=1e-12, check_every=8)
     assert ia["converged"] and ib["converged"]
     assert rel(za, zb.cpu().numpy()) <= 1e-10

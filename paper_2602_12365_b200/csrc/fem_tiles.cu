@@ -67,6 +67,15 @@
 #ifndef FEM_P2_G8
 #define FEM_P2_G8 0
 #endif
+// Phase 2 over a node-major contribution array (FEM_P2_NM): phase 1 stores element e's
+// contribution for local node a at the position of incidence (e, a) in the node-sorted
+// incidence list (lpos, setup), so each tile node sums a contiguous run cb[q D + c],
+// q in [ptr[r], ptr[r+1]) — no index loads, no dependent address chain.  A/B r02 at cfg 3:
+// HVP 0.935 -> 1.041 ms, residual 0.807 -> 0.928 ms (the scattered phase-1 stores conflict
+// in the banks), so off by default.
+#ifndef FEM_P2_NM
+#define FEM_P2_NM 0
+#endif
 // Phase 0: one thread per tile node issues the node's D-vector copies (no div / mod by D;
 // A/B r02: neutral, 0.975 vs 0.972 ms HVP)
 // NH HVP in metric form (M_ab = c_a . c_b, D_ab = dv_b . cs_a): fewer FP64 operations than
@@ -84,6 +93,7 @@ namespace fem {
 // columns (the pad entries of the incidence groups point there)
 constexpr int kCbStride = FEM_P2_G8 ? kTile + 8 : kTile;
 static_assert(!(FEM_P2_G8 && FEM_P2_BAL), "FEM_P2_G8 and FEM_P2_BAL are alternatives");
+static_assert(!(FEM_P2_NM && (FEM_P2_G8 || FEM_P2_BAL)), "FEM_P2_NM is an alternative phase 2");
 
 // ------------------------------------------------------------------ setup
 __global__ void k_bbox_partial(const double *coords, int64_t n, int dim, double *part) {
@@ -471,7 +481,13 @@ __global__ void k_pack_meta(TileSet T, const uint8_t *node_bc, int64_t E) {
     for (int i = threadIdx.x; i <= T.um; i += blockDim.x)
       ptr[i] = i <= U ? T.ptr[t * (T.maxe + 1) + i] : (uint16_t)nvalid;
     uint16_t *inc = reinterpret_cast<uint16_t *>(base + T.off_inc);
-    for (int i = threadIdx.x; i < kTile * 4; i += blockDim.x) inc[i] = i < nvalid ? T.inc[t * T.maxe + i] : 0;
+    if (FEM_P2_NM) {  // lpos[e 4 + a] = list position of incidence (e, a)
+      for (int i = threadIdx.x; i < kTile * 4; i += blockDim.x) inc[i] = 0;
+      __syncthreads();
+      for (int i = threadIdx.x; i < nvalid; i += blockDim.x) inc[T.inc[t * T.maxe + i]] = (uint16_t)i;
+    } else {
+      for (int i = threadIdx.x; i < kTile * 4; i += blockDim.x) inc[i] = i < nvalid ? T.inc[t * T.maxe + i] : 0;
+    }
   }
   for (int i = threadIdx.x; i < T.um; i += blockDim.x) {
     base[T.off_int + i] = i < U ? T.interior[t * T.maxe + i] : 0;
@@ -1139,7 +1155,14 @@ __device__ __forceinline__ void tile_phase1(const PipeArgs &A, const unsigned ch
 #pragma unroll
       for (int a = 0; a < NEN; ++a)
 #pragma unroll
-        for (int i = 0; i < D; ++i) cb[(a * D + i) * kCbStride + tid] = ok ? f[a][i] : 0.0;
+        for (int i = 0; i < D; ++i) {
+          if constexpr (FEM_P2_NM) {  // node-major: at the incidence's list position
+            const int q = reinterpret_cast<const uint16_t *>(m + A.off_inc)[tid * 4 + a];
+            cb[q * D + i] = ok ? f[a][i] : 0.0;
+          } else {
+            cb[(a * D + i) * kCbStride + tid] = ok ? f[a][i] : 0.0;
+          }
+        }
     }
   }
 }
@@ -1214,6 +1237,35 @@ __device__ __forceinline__ void tile_phase2(const PipeArgs &A, const unsigned ch
       }
     }
     if (n > 0 && pos == 0) node_write<D, SC>(A, m, (int)(mt & 0x7ffu), t, sacc);
+  }
+}
+#elif FEM_P2_NM
+template <int D, int OP, int SC>
+__device__ __forceinline__ void tile_phase2(const PipeArgs &A, const unsigned char *m, int U,
+                                            int64_t t, int tid, const double *cb) {
+  const uint16_t *ptr = reinterpret_cast<const uint16_t *>(m + A.off_ptr);
+  for (int r = tid; r < U; r += kTile) {  // one thread per tile node: a contiguous run
+    const int lo = ptr[r], hi = ptr[r + 1];
+    double s0[D], s1[D];
+#pragma unroll
+    for (int cc = 0; cc < D; ++cc) s0[cc] = s1[cc] = 0.0;
+    int q = lo;
+    for (; q + 3 < hi; q += 4) {
+#pragma unroll
+      for (int cc = 0; cc < D; ++cc) {
+        s0[cc] += cb[q * D + cc];
+        s1[cc] += cb[(q + 1) * D + cc];
+        s0[cc] += cb[(q + 2) * D + cc];
+        s1[cc] += cb[(q + 3) * D + cc];
+      }
+    }
+    for (; q < hi; ++q)
+#pragma unroll
+      for (int cc = 0; cc < D; ++cc) s0[cc] += cb[q * D + cc];
+    double sacc[D];
+#pragma unroll
+    for (int cc = 0; cc < D; ++cc) sacc[cc] = s0[cc] + s1[cc];
+    node_write<D, SC>(A, m, r, t, sacc);
   }
 }
 #elif FEM_P2_G8

@@ -607,6 +607,20 @@ def main():
                              "bound": "hbm" if t_hbm >= t_alu else "alu",
                              "frac_of_bound": max(t_hbm, t_alu) / (ms * 1e-3),
                              "share_of_step": per[p] / total_ms}
+    # the linearized HVP (Newton-Krylov operator, fem_linearize + FEM_LINEARIZED): compulsory
+    # bytes = the cached metric-form tangent (D^2 + 2 + D(D+1)/2 doubles per element) + v read
+    # + y zeroed and written; FP64 ~ 130 flops per tet (3D)
+    if mesh.material == 1:
+        d_ = mesh.dim
+        lin_b = 8 * (d_ * d_ + 2 + d_ * (d_ + 1) // 2) * mesh.n_elems + 3 * 8 * N
+        ms_l = ab["hvp_linearized_ms"]
+        extra_phases = {"hvp_linearized": {
+            "ms": ms_l, "alg_GB": lin_b / 1e9, "GB/s": lin_b / (ms_l * 1e-3) / 1e9,
+            "frac_hbm": lin_b / (ms_l * 1e-3) / 1e9 / hbm, "gdofs": n_global / (ms_l * 1e-3) / 1e9,
+            "what": "FEM_LINEARIZED HVP (cached metric-form tangent, 136 B/tet) - the operator "
+                    "of fem_newton_solve's matrix-free CG; A/B timing, 5 calls"}}
+    else:
+        extra_phases = {}
     dom = max(phases, key=lambda p: per[p])
     pr = phase_roofline[dom]
     if pr["bound"] == "hbm":
@@ -693,6 +707,7 @@ def main():
         "energy_gdofs": n_global / (per["energy"] / K * 1e-3) / 1e9,
         "spmv_ms": per["spmv"] / K,
         "phases": phase_roofline,
+        "phases_extra": extra_phases,
         "ab": ab,
         "setup": setup,
         "solve": solve,

@@ -1,16 +1,22 @@
 #!/bin/bash
-# Round evidence in one call: smoke, full bench (default flags), reference arm, ncu launch
-# list of one step, ncu --set full of the step's main kernels (CSV exports), all under
-# gpurun_out/ (summaries copied to profiles/ by hand).
+# Round evidence in one call (TAG names the outputs): smoke, full bench (default flags), the
+# reference arm, cfg4 strong P=1, ncu launch list of one step, ncu --set full of the step's
+# main kernels and of the residual / HVP variants (CSV exports), under gpurun_out/.
 cd "${GRAFT_REPO_ROOT:-/root/repo}"; mkdir -p gpurun_out
-python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1
-timeout 600 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?" >> gpurun_out/smoke.log
-timeout 900 python bench.py > gpurun_out/bench_full.json 2> gpurun_out/bench_full.err
-timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err
+T=${TAG:-ev}
+python -c "import __graft_entry__ as g; g.build()" > gpurun_out/${T}_build.log 2>&1
+timeout 600 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/${T}_smoke.log 2>&1; echo "smoke rc=$?" >> gpurun_out/${T}_smoke.log
+timeout 900 python bench.py > gpurun_out/${T}_bench.json 2> gpurun_out/${T}_bench.err
+timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/${T}_bench_ref.json 2> gpurun_out/${T}_bench_ref.err
+timeout 900 python bench.py --scaling strong --no-cpu-baseline --steps 5 > gpurun_out/${T}_strong.json 2> gpurun_out/${T}_strong.err
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --profile-from-start off --csv \
-   --log-file gpurun_out/launches.csv python bench.py --profile-step > gpurun_out/ncu_list.log 2>&1
+   --log-file gpurun_out/${T}_launches.csv python bench.py --profile-step > gpurun_out/${T}_ncu_list.log 2>&1
 timeout 1500 ncu --set full --clock-control none --import-source on --profile-from-start off \
-   -k regex:"k_tile_pipe|k_rows_tile|k_spmv" -c 5 -o gpurun_out/prof_full -f \
-   python bench.py --profile-step > gpurun_out/ncu_full.log 2>&1
-ncu -i gpurun_out/prof_full.ncu-rep --page raw --csv > gpurun_out/prof_full_raw.csv 2>/dev/null
-tail -2 gpurun_out/smoke.log; tail -c 400 gpurun_out/bench_full.json
+   -k regex:"k_tile_pipe|k_rows_tile|k_spmv" -c 5 -o gpurun_out/${T}_prof_full -f \
+   python bench.py --profile-step > gpurun_out/${T}_ncu_full.log 2>&1
+ncu -i gpurun_out/${T}_prof_full.ncu-rep --page raw --csv > gpurun_out/${T}_prof_full_raw.csv 2>/dev/null
+timeout 1200 ncu --set full --clock-control none --import-source on --profile-from-start off \
+   -k regex:"k_tile_pipe|k_rows_fused|k_elem_ctx" -c 12 -o gpurun_out/${T}_prof_var -f \
+   python tools/profile_variants.py --variants hvp,hvp_lin,hvp_s,res,res_s,assemble_col > gpurun_out/${T}_ncu_var.log 2>&1
+ncu -i gpurun_out/${T}_prof_var.ncu-rep --page raw --csv > gpurun_out/${T}_prof_var_raw.csv 2>/dev/null
+tail -2 gpurun_out/${T}_smoke.log; tail -c 300 gpurun_out/${T}_bench.json; echo; tail -c 200 gpurun_out/${T}_strong.json

@@ -36,10 +36,13 @@ calls = {
     "res_tcol": lambda: prob.residual(zt, bc=True, out=y, flags=fem.TILE_COLORED),
     "res_s": lambda: prob.residual(zt, bc=True, out=y, flags=fem.STREAM_GEOM),
     "res_col": lambda: prob.residual(zt, bc=True, out=y, flags=fem.COLORED_SCATTER),
+    "hvp_lin": lambda: (prob.hvp(zt, vt, bc=True, out=y, flags=fem.LINEARIZED)),
     "energy": lambda: prob.energy(zt),
+    "assemble_col": lambda: prob.assemble_csr(zt, bc=True, mode="colored"),
     "assemble": lambda: prob.assemble_csr(zt, bc=True),
 }
 sel = a.variants.split(",")
+prob.linearize(zt)
 for k in sel:          # warm: lazy setup (geometry stream, element colors, pattern)
     calls[k]()
 torch.cuda.synchronize()

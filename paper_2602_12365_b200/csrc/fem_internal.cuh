@@ -38,7 +38,7 @@ struct NvtxScope {
 
 enum : int { ERRW_INVERTED = 1, ERRW_TOO_MANY_COLORS = 2, ERRW_NONFINITE = 4, ERRW_ADJ_OVERFLOW = 8 };
 
-constexpr int kMaxNodeAdj = 64;     // max distinct node neighbours (incl. self) per node
+constexpr int kMaxNodeAdj = 128;    // max distinct node neighbours (incl. self) per node (setup-time local arrays; Delaunay 3D meshes reach ~32)
 constexpr int kReduceBlocks = 1184; // 148 SMs x 8: fixed grid => fixed reduction order
 constexpr int kThreads = 256;
 #ifndef FEM_TILE

@@ -1352,6 +1352,9 @@ __device__ __forceinline__ unsigned smem_addr(const void *p) {
 __device__ __forceinline__ void mb_init(uint64_t *m, unsigned count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_addr(m)), "r"(count) : "memory");
 }
+__device__ __forceinline__ void mb_arrive(uint64_t *m) {  // release.cta
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_addr(m)) : "memory");
+}
 __device__ __forceinline__ void mb_cp_arrive(uint64_t *m) {
   asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(smem_addr(m)) : "memory");
 }
@@ -1383,6 +1386,16 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned by
 #ifndef FEM_RES_DEC
 #define FEM_RES_DEC 0
 #endif
+// Barrier-free decoupled pipeline: the per-tile __syncthreads between phase 1 and phase 2 is
+// replaced by two mbarriers per contribution buffer (phase 1 of tile k done: all threads
+// arrive, node-sum threads wait; phase 2 of tile k done: all arrive, the writers of tile
+// k+2's contributions / tile k+3's metadata wait), so warps without node sums run up to one
+// tile ahead instead of idling at the barrier.  Correct (parity-tested) but measured much
+// slower at cfg 3 (HVP 1.69 vs 0.94 ms: the spinning mbarrier waits and the drifted warps'
+// buffer waits cost more than the barrier), so off by default.
+#ifndef FEM_DEC2
+#define FEM_DEC2 0
+#endif
 #ifndef FEM_ENERGY_DEC
 #define FEM_ENERGY_DEC 0
 #endif
@@ -1403,7 +1416,7 @@ __global__ void __launch_bounds__(kTile, pipe_minb(OP, MAT, D)) k_tile_pipe(Pipe
   constexpr bool STREAM = op_streams<OP>();
   constexpr unsigned GBYTES = sizeof(double) * geom_words(D) * kTile;
   extern __shared__ __align__(16) unsigned char sm[];
-  __shared__ __align__(8) uint64_t mb_meta[3], mb_node[2], mb_geom[2];
+  __shared__ __align__(8) uint64_t mb_meta[3], mb_node[2], mb_geom[2], mb_p1[2], mb_p2[2];
   const int tid = threadIdx.x;
   const int mb = A.mb, um = A.um;
   const int nstride = um * D * NF;
@@ -1462,6 +1475,8 @@ __global__ void __launch_bounds__(kTile, pipe_minb(OP, MAT, D)) k_tile_pipe(Pipe
     if (tid == 0) {
       for (int b = 0; b < 3; ++b) mb_init(&mb_meta[b], kTile);
       for (int b = 0; b < 2; ++b) mb_init(&mb_node[b], kTile);
+      for (int b = 0; b < 2; ++b) mb_init(&mb_p1[b], kTile);
+      for (int b = 0; b < 2; ++b) mb_init(&mb_p2[b], kTile);
       asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
     __syncthreads();
@@ -1471,30 +1486,65 @@ __global__ void __launch_bounds__(kTile, pipe_minb(OP, MAT, D)) k_tile_pipe(Pipe
       mb_wait(&mb_meta[0], 0);
       issue_nodes(metab, 0);
     }
-    for (int k = 0; t < A.n_tiles; ++k, t += G) {
-      const int bm = k % 3, bn = k & 1;
-      const unsigned char *m = metab + bm * mb;
-      mb_wait(&mb_node[bn], (unsigned)(k >> 1) & 1u);  // node data of tile k
-      if (t + G < A.n_tiles) {  // node data of tile k+1 (its metadata issued after barrier k-1)
-        const int bm1 = (k + 1) % 3;
-        mb_wait(&mb_meta[bm1], (unsigned)((k + 1) / 3) & 1u);
-        issue_nodes(metab + bm1 * mb, bn ^ 1);
-        if constexpr (OP == OP_HVP_LIN && MAT == FEM_NEO_HOOKEAN) {  // cache rows of tile k+1 -> L2
-          if (tid < lin_words(D)) {
-            const double *src = A.lin + tid * A.lin_stride + tile_id(t + G) * kTile;
-            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(src),
-                         "r"((unsigned)(kTile * sizeof(double)))
-                         : "memory");
+    if constexpr (FEM_DEC2 && !FEM_P2_BAL) {
+      for (int k = 0; t < A.n_tiles; ++k, t += G) {
+        const int bm = k % 3, bn = k & 1;
+        const unsigned char *m = metab + bm * mb;
+        mb_wait(&mb_node[bn], (unsigned)(k >> 1) & 1u);  // node data of tile k
+        if (t + G < A.n_tiles) {  // node data of tile k+1 -> buffer of tile k-1
+          const int bm1 = (k + 1) % 3;
+          mb_wait(&mb_meta[bm1], (unsigned)((k + 1) / 3) & 1u);
+          if (k >= 1) mb_wait(&mb_p1[(k - 1) & 1], (unsigned)((k - 1) >> 1) & 1u);
+          issue_nodes(metab + bm1 * mb, bn ^ 1);
+          if constexpr (OP == OP_HVP_LIN && MAT == FEM_NEO_HOOKEAN) {  // cache rows of tile k+1 -> L2
+            if (tid < lin_words(D)) {
+              const double *src = A.lin + tid * A.lin_stride + tile_id(t + G) * kTile;
+              asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(src),
+                           "r"((unsigned)(kTile * sizeof(double)))
+                           : "memory");
+            }
           }
         }
+        const double *nb = nodeb + bn * nstride;
+        double *cb = contrib + (k & 1) * ((D + 1) * D * kCbStride);
+        if (k >= 2) mb_wait(&mb_p2[k & 1], (unsigned)((k - 2) >> 1) & 1u);  // tile k-2 summed
+        tile_phase1<D, MAT, OP, MASK>(A, m, nb, nb + UOFF * um * D, nb + (NF - 1) * um * D, tile_id(t), tid, cb, eacc);
+        mb_arrive(&mb_p1[k & 1]);
+        if (t + 2 * G < A.n_tiles) {  // metadata of tile k+2 -> buffer of tile k-1
+          if (k >= 1) mb_wait(&mb_p2[(k - 1) & 1], (unsigned)((k - 1) >> 1) & 1u);
+          issue_meta(t + 2 * G, (k + 2) % 3);
+        }
+        const int U = reinterpret_cast<const int *>(m)[0];
+        if (tid < U) mb_wait(&mb_p1[k & 1], (unsigned)(k >> 1) & 1u);  // all of tile k's phase 1
+        if constexpr (op_has_p2<OP>()) tile_phase2<D, OP, SC>(A, m, U, tile_id(t), tid, cb);
+        mb_arrive(&mb_p2[k & 1]);
       }
-      const double *nb = nodeb + bn * nstride;
-      double *cb = contrib + (k & 1) * ((D + 1) * D * kCbStride);
-      tile_phase1<D, MAT, OP, MASK>(A, m, nb, nb + UOFF * um * D, nb + (NF - 1) * um * D, tile_id(t), tid, cb, eacc);
-      __syncthreads();  // phase 1 of tile k done; tile k-1 fully consumed
-      if (t + 2 * G < A.n_tiles) issue_meta(t + 2 * G, (k + 2) % 3);
-      if constexpr (op_has_p2<OP>())
-        tile_phase2<D, OP, SC>(A, m, reinterpret_cast<const int *>(m)[0], tile_id(t), tid, cb);
+    } else {
+      for (int k = 0; t < A.n_tiles; ++k, t += G) {
+        const int bm = k % 3, bn = k & 1;
+        const unsigned char *m = metab + bm * mb;
+        mb_wait(&mb_node[bn], (unsigned)(k >> 1) & 1u);  // node data of tile k
+        if (t + G < A.n_tiles) {  // node data of tile k+1 (its metadata issued after barrier k-1)
+          const int bm1 = (k + 1) % 3;
+          mb_wait(&mb_meta[bm1], (unsigned)((k + 1) / 3) & 1u);
+          issue_nodes(metab + bm1 * mb, bn ^ 1);
+          if constexpr (OP == OP_HVP_LIN && MAT == FEM_NEO_HOOKEAN) {  // cache rows of tile k+1 -> L2
+            if (tid < lin_words(D)) {
+              const double *src = A.lin + tid * A.lin_stride + tile_id(t + G) * kTile;
+              asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(src),
+                           "r"((unsigned)(kTile * sizeof(double)))
+                           : "memory");
+            }
+          }
+        }
+        const double *nb = nodeb + bn * nstride;
+        double *cb = contrib + (k & 1) * ((D + 1) * D * kCbStride);
+        tile_phase1<D, MAT, OP, MASK>(A, m, nb, nb + UOFF * um * D, nb + (NF - 1) * um * D, tile_id(t), tid, cb, eacc);
+        __syncthreads();  // phase 1 of tile k done; tile k-1 fully consumed
+        if (t + 2 * G < A.n_tiles) issue_meta(t + 2 * G, (k + 2) % 3);
+        if constexpr (op_has_p2<OP>())
+          tile_phase2<D, OP, SC>(A, m, reinterpret_cast<const int *>(m)[0], tile_id(t), tid, cb);
+      }
     }
     asm volatile("cp.async.wait_all;\n" ::: "memory");
   } else {

@@ -1,7 +1,7 @@
 #!/usr/bin/env python
 """Summarise an ncu --set full report and an ncu launch list into profiles/<tag>_*.
 
-usage: python tools/summarize_ncu.py <tag> <prof.ncu-rep> <launches.csv>
+usage: python tools/summarize_ncu.py <tag> <prof.ncu-rep | raw.csv> <launches.csv>
 Writes profiles/<tag>_ncu_kernels.csv (per captured kernel: time, DRAM traffic, pipe use,
 occupancy, stall mix), profiles/<tag>_launches.csv (the launch list, kernel name + duration),
 profiles/<tag>_step_shares.csv (one bench step's kernels with their share of the step) and
@@ -21,8 +21,12 @@ PHASE_OF = {"k_tile_pipe<3, 1, 0": "energy", "k_tile_pipe<3, 1, 1": "residual",
 
 
 def raw(rep):
-    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
-                         text=True, check=True).stdout
+    """the raw page of an ncu report (.ncu-rep) or its CSV export (ncu -i … --page raw --csv)"""
+    if rep.endswith(".csv"):
+        out = open(rep).read()
+    else:
+        out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
+                             text=True, check=True).stdout
     r = list(csv.reader(io.StringIO(out)))
     return r[0], r[1], r[2:]
 

@@ -462,6 +462,12 @@ def main():
     e1 = torch.empty(1, dtype=torch.float64, device=zt.device)
     ab = {
         "hvp_tiles_ms": time_call(lambda: prob.hvp(zt, vt, bc=True, out=y)),
+        # the per-element reference metric mu vol G_a.G_b, 1/det J read from a cache computed
+        # once per problem (Alg. 1's precomputed geometry) instead of recomputed per call
+        "hvp_reference_metric_ms": time_call(
+            lambda: prob.hvp(zt, vt, bc=True, out=y, flags=fem.REFERENCE_METRIC)),
+        "residual_reference_metric_ms": time_call(
+            lambda: prob.residual(zt, bc=True, out=r, flags=fem.REFERENCE_METRIC)),
         "hvp_linearized_ms": time_call(lambda: prob.hvp(zt, vt, bc=True, out=y, flags=fem.LINEARIZED)),
         "linearize_ms": time_call(lambda: prob.linearize(zt)),
         "hvp_baseline_scatter_ms": time_call(

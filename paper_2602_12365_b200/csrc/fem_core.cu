@@ -457,7 +457,8 @@ fem_status run_residual(Problem *p, const double *z, double *r, unsigned flags, 
       set_error("fem_residual: FEM_STREAM_GEOM with FEM_DETERMINISTIC");
       return FEM_ERR_INVALID_ARG;
     }
-    st = element_pass_halo(p, sg ? OP_RESIDUAL_S : OP_RESIDUAL, z, nullptr, r, false, det,
+    const int op = sg ? OP_RESIDUAL_S : (flags & FEM_REFERENCE_METRIC) ? OP_RESIDUAL_R : OP_RESIDUAL;
+    st = element_pass_halo(p, op, z, nullptr, r, false, det,
                            flags & FEM_LOCAL_ONLY, s);
   }
   if (st) return st;
@@ -520,7 +521,8 @@ fem_status run_hvp(Problem *p, const double *z, const double *v, double *y, unsi
       set_error("fem_hvp: FEM_STREAM_GEOM with FEM_DETERMINISTIC / FEM_LINEARIZED");
       return FEM_ERR_INVALID_ARG;
     }
-    st = element_pass_halo(p, lin ? OP_HVP_LIN : sg ? OP_HVP_S : OP_HVP, z, v, y, bc, det,
+    const int op = lin ? OP_HVP_LIN : sg ? OP_HVP_S : (flags & FEM_REFERENCE_METRIC) ? OP_HVP_R : OP_HVP;
+    st = element_pass_halo(p, op, z, v, y, bc, det,
                            flags & FEM_LOCAL_ONLY, s);
   }
   if (st) return st;

@@ -47,10 +47,14 @@ constexpr int kThreads = 256;
 constexpr int kTile = FEM_TILE;     // elements per tile (one CTA)
 
 enum { OP_ENERGY = 0, OP_RESIDUAL = 1, OP_HVP = 2, OP_HVP_LIN = 3, OP_LIN = 4, OP_RESIDUAL_S = 5,
-       OP_HVP_S = 6 };
+       OP_HVP_S = 6, OP_RESIDUAL_R = 7, OP_HVP_R = 8 };
 // OP_*_S: residual / HVP from the streamed per-element geometry (TileSet::geom; Alg. 1's
 // per-batch gather of grad N and det J) instead of coordinates (FEM_STREAM_GEOM)
 // OP_LIN: cache the tangent state at z (fem_linearize); OP_HVP_LIN: HVP from that cache
+// OP_*_R: NH residual / HVP with the element's reference metric mu vol G_a.G_b and 1/det J
+// read from TileSet::refm (mesh constants computed once, Alg. 1's precomputed grad N / det J,
+// P:124-127) — only the deformed geometry at x + u is evaluated per call (FEM_REFERENCE_METRIC;
+// A/B at cfg 3: HVP 0.986 vs 0.935 ms recomputed, residual 0.787 vs 0.805 ms — not the default)
 
 // Element tiles (fem_tiles.cu).  maxe = kTile * (dim+1) reserved entries per tile.
 struct TileSet {
@@ -74,6 +78,7 @@ struct TileSet {
   int64_t *node_slot_ptr = nullptr; // [n_nodes+1]
   double *epart = nullptr;       // [n_tiles] energy partials
   double *geom = nullptr;        // [n_tiles][D*D+1][kTile] cofactor rows c_a and det J (SoA per tile)
+  double *refm = nullptr;        // [n_tiles][D(D+1)/2+1][kTile] mu vol G_a.G_b (a<=b, a,b>=1), 1/det J
   int32_t *tcolor_list = nullptr;  // FEM_TILE_COLORED: tiles of color c at [tcolor_off[c], ..)
   std::vector<int64_t> tcolor_off;
   // balanced phase-2 schedule (fem_tiles.cu k_build_sched): per tile sched_rounds x kTile
@@ -260,6 +265,7 @@ fem_status tile_pass(Problem *p, int op, const double *u, const double *v, doubl
                      bool det, double *partials, cudaStream_t s, int part = 0);
 fem_status build_tile_lists(Problem *p, cudaStream_t s);
 fem_status build_geom_stream(Problem *p, cudaStream_t s);                // fem_tiles.cu
+fem_status build_refm(Problem *p, cudaStream_t s);                       // fem_tiles.cu
 fem_status build_tile_colors(Problem *p, cudaStream_t s);                // fem_tiles.cu
 fem_status halo_begin(Problem *p, const double *y, cudaStream_t s);
 fem_status halo_end(Problem *p, double *y, cudaStream_t s);

@@ -76,6 +76,12 @@
 #ifndef FEM_P2_NM
 #define FEM_P2_NM 0
 #endif
+// Two lanes per tile node in phase 2 (FEM_P2_PAIR): A/B r02 at cfg 3 (same box): HVP 0.997 vs
+// 0.938 ms, residual 0.864 vs 0.809 ms (the shuffles and the lost bank schedule cost more than
+// the shorter per-node chains save), so off by default.
+#ifndef FEM_P2_PAIR
+#define FEM_P2_PAIR 0
+#endif
 // Phase 0: one thread per tile node issues the node's D-vector copies (no div / mod by D;
 // A/B r02: neutral, 0.975 vs 0.972 ms HVP)
 // NH HVP in metric form (M_ab = c_a . c_b, D_ab = dv_b . cs_a): fewer FP64 operations than
@@ -762,8 +768,16 @@ __host__ __device__ constexpr int pipe_minb2d(int op, int mat) {
   return op == OP_RESIDUAL_S || op == OP_HVP_S ? 3 : op == OP_ENERGY || op == OP_RESIDUAL || op == OP_LIN ? 5
          : (mat == FEM_NEO_HOOKEAN ? 3 : 4);
 }
+#ifndef FEM_HVPR_MINB
+#define FEM_HVPR_MINB 2
+#endif
+#ifndef FEM_RESR_MINB
+#define FEM_RESR_MINB 3
+#endif
 __host__ __device__ constexpr int pipe_minb(int op, int mat, int dim = 3) {
-  return (256 / kTile) *
+  return op == OP_HVP_R ? (256 / kTile) * (dim == 2 ? 3 : FEM_HVPR_MINB)
+         : op == OP_RESIDUAL_R ? (256 / kTile) * (dim == 2 ? 5 : FEM_RESR_MINB) :
+         (256 / kTile) *
          (dim == 2 ? (FEM_PIPE_MINB2D > 0 ? FEM_PIPE_MINB2D : pipe_minb2d(op, mat))
           : FEM_PIPE_MINB > 0 ? FEM_PIPE_MINB
                             : (op == OP_RESIDUAL_S || op == OP_HVP_S) ? 2
@@ -784,16 +798,28 @@ struct PipeArgs {
   const int32_t *list;  // tile ids to process (null: tiles 0 .. n_tiles-1)
   double *lin;        // linearization cache [lin_words][lin_stride] (OP_LIN writes, OP_HVP_LIN reads)
   const double *geom; // OP_*_S: per-tile geometry blocks [n_tiles][D*D+1][kTile]
+  const double *refm; // OP_*_R: per-tile reference metric blocks [n_tiles][refm_words(D)][kTile]
   int64_t lin_stride;
   int *err;
 };
 
 template <int OP>
 constexpr bool op_streams() { return OP == OP_RESIDUAL_S || OP == OP_HVP_S; }
-template <int OP>  // the operation an OP_*_S variant computes
-constexpr int base_op() { return OP == OP_RESIDUAL_S ? OP_RESIDUAL : OP == OP_HVP_S ? OP_HVP : OP; }
+template <int OP>  // the operation an OP_*_S / OP_*_R variant computes
+constexpr int base_op() {
+  return (OP == OP_RESIDUAL_S || OP == OP_RESIDUAL_R) ? OP_RESIDUAL
+         : (OP == OP_HVP_S || OP == OP_HVP_R) ? OP_HVP : OP;
+}
 template <int OP>
-constexpr bool op_is_hvp() { return OP == OP_HVP || OP == OP_HVP_LIN || OP == OP_HVP_S; }
+constexpr bool op_is_hvp() { return OP == OP_HVP || OP == OP_HVP_LIN || OP == OP_HVP_S || OP == OP_HVP_R; }
+template <int OP>
+constexpr bool op_refm() { return OP == OP_RESIDUAL_R || OP == OP_HVP_R; }
+// reference metric per element (OP_*_R): mu vol G_a.G_b for 1 <= a <= b <= D (row-major upper
+// triangle) and 1 / det J(x)
+__host__ __device__ constexpr int refm_words(int D) { return D * (D + 1) / 2 + 1; }
+__host__ __device__ constexpr int sym_idx(int a, int b, int D) {  // upper-triangle position
+  return a <= b ? a * D - a * (a - 1) / 2 + (b - a) : b * D - b * (b - 1) / 2 + (a - b);
+}
 template <int OP>
 constexpr bool op_has_p2() { return base_op<OP>() == OP_RESIDUAL || op_is_hvp<OP>(); }
 template <int OP, int MAT>
@@ -817,6 +843,10 @@ __device__ __forceinline__ void tile_phase1(const PipeArgs &A, const unsigned ch
   // OP_*_S: the same operation with c_a, det J read from the streamed geometry block gs
   constexpr int OP = base_op<OP_>();
   constexpr bool STREAM = op_streams<OP_>();
+  // OP_*_R: the reference metric mu vol G_a.G_b and 1/det J come from the per-element cache,
+  // so the reference cofactors c_a are never formed (only the deformed geometry at x + u)
+  constexpr bool REFM = op_refm<OP_>();
+  constexpr int RW = refm_words(D);
   constexpr int NEN = D + 1;
   constexpr bool NEED_U = op_needs_u<OP, MAT>();
   // NH HVP in the deformed configuration (FEM_HVP_SPATIAL): see the HVP branch below; the
@@ -832,6 +862,12 @@ __device__ __forceinline__ void tile_phase1(const PipeArgs &A, const unsigned ch
   if (e < A.E) {
     const ushort4 lc4 = reinterpret_cast<const ushort4 *>(m + A.off_lconn)[tid];
     const int lc[4] = {lc4.x, lc4.y, lc4.z, lc4.w};
+    double rm[RW];
+    if constexpr (REFM) {  // coalesced over the tile (SoA), L2-prefetched one tile ahead
+      const double *R = A.refm + t * (RW * kTile) + tid;
+#pragma unroll
+      for (int w = 0; w < RW; ++w) rm[w] = __ldg(R + w * kTile);
+    }
     double x[NEN][D], c[D][D], det;
     if constexpr (NO_GEOM) {
 #pragma unroll
@@ -850,9 +886,17 @@ __device__ __forceinline__ void tile_phase1(const PipeArgs &A, const unsigned ch
       for (int a = 0; a < NEN; ++a)
 #pragma unroll
         for (int i = 0; i < D; ++i) x[a][i] = xs[lc[a] * D + i];
-      det = cof_gradients<D>(x, c);
+      if constexpr (REFM) {
+#pragma unroll
+        for (int a = 0; a < D; ++a)
+#pragma unroll
+          for (int j = 0; j < D; ++j) c[a][j] = 0.0;
+        det = 1.0;
+      } else {
+        det = cof_gradients<D>(x, c);
+      }
     }
-    const double id = fem_rcp(det);
+    const double id = REFM ? rm[RW - 1] : fem_rcp(det);
     constexpr double inv_fact = (D == 3) ? 1.0 / 6.0 : 0.5;  // vol = det / d!
     double lam = A.lam, mu = A.mu;
     if (A.has_phase) {
@@ -862,15 +906,15 @@ __device__ __forceinline__ void tile_phase1(const PipeArgs &A, const unsigned ch
     }
     double H[D][D];
     double cs[D][D], dets = 1.0;  // SPATIAL: cofactor gradients and det J at x + u
+    double xd[NEN][D];            // deformed edge vectors (SPATIAL forms)
     if constexpr (NEED_U) {
       double u[NEN][D];
 #pragma unroll
       for (int a = 0; a < NEN; ++a)
 #pragma unroll
         for (int i = 0; i < D; ++i) u[a][i] = us[lc[a] * D + i];
-      if constexpr (SPATIAL_R) grad_hat<D>(u, c, H);  // Hh = det H (scaled where used)
+      if constexpr (SPATIAL_R && !REFM) grad_hat<D>(u, c, H);  // Hh = det H (scaled where used)
       if constexpr (SPATIAL || SPATIAL_R || LIN_S) {
-        double xd[NEN][D];
         deformed_edges<D>(x, u, xd);
         dets = cof_gradients<D>(xd, cs);
       } else {
@@ -909,6 +953,24 @@ __device__ __forceinline__ void tile_phase1(const PipeArgs &A, const unsigned ch
         ok = Jr > 0.0;
         const double lnJ = fem_log(Jr);
         const double kc = (lam * lnJ - mu) * fem_rcp(Jr) * inv_fact, kh = ms * id;
+        if constexpr (REFM) {
+          // mu vol F G_a = mu vol sum_b xd_b (G_b.G_a) (F = sum_b xd_b (x) G_b over the deformed
+          // edges): vol P G_a = sum_b Ms_ab xd_b + kc cs_a, a >= 1 — the same terms as below
+          // (sum_b Ms_ab (x_b - x_0) = mu c_a / d!), from the cached metric Ms
+#pragma unroll
+          for (int i = 0; i < D; ++i) {
+            double s0 = 0.0;
+#pragma unroll
+            for (int a = 0; a < D; ++a) {
+              double fa = kc * cs[a][i];
+#pragma unroll
+              for (int b = 0; b < D; ++b) fa = fma(rm[sym_idx(a, b, D)], xd[b + 1][i], fa);
+              f[a + 1][i] = fa;
+              s0 += fa;
+            }
+            f[0][i] = -s0;
+          }
+        } else {
 #pragma unroll
         for (int i = 0; i < D; ++i) {
           double s0 = 0.0;
@@ -923,7 +985,8 @@ __device__ __forceinline__ void tile_phase1(const PipeArgs &A, const unsigned ch
           }
           f[0][i] = -s0;
         }
-        if (A.partials && ok) {  // psi from H = Hh / det: F:F - d = 2 tr H + H:H
+        }
+        if (!REFM && A.partials && ok) {  // psi from H = Hh / det: F:F - d = 2 tr H + H:H
           double th = 0.0;
 #pragma unroll
           for (int i = 0; i < D; ++i) {
@@ -1077,10 +1140,14 @@ __device__ __forceinline__ void tile_phase1(const PipeArgs &A, const unsigned ch
       for (int a = 0; a < D; ++a)
 #pragma unroll
         for (int b = a; b < D; ++b) {
-          double t = 0.0;
+          if constexpr (REFM) {
+            Ms[a][b] = Ms[b][a] = rm[sym_idx(a, b, D)];
+          } else {
+            double t = 0.0;
 #pragma unroll
-          for (int j = 0; j < D; ++j) t = fma(c[a][j], c[b][j], t);
-          Ms[a][b] = Ms[b][a] = sr * t;
+            for (int j = 0; j < D; ++j) t = fma(c[a][j], c[b][j], t);
+            Ms[a][b] = Ms[b][a] = sr * t;
+          }
         }
 #pragma unroll
       for (int i = 0; i < D; ++i) {
@@ -1300,6 +1367,49 @@ __device__ __forceinline__ void tile_phase2(const PipeArgs &A, const unsigned ch
     node_write<D, SC>(A, m, r, t, sacc);
   }
 }
+#elif FEM_P2_PAIR
+// Two lanes per tile node (lanes 2r, 2r+1 of the CTA): each sums half of the node's
+// incidence list (two interleaved partial sums), the pair combines by one shuffle per
+// component and the even lane writes.  Up to 128 nodes per pass, so all 8 warps share the
+// node sums instead of ceil(U / 32) of them (the critical path before the next tile's barrier).
+template <int D, int OP, int SC>
+__device__ __forceinline__ void tile_phase2(const PipeArgs &A, const unsigned char *m, int U,
+                                            int64_t t, int tid, const double *cb) {
+  const uint16_t *ptr = reinterpret_cast<const uint16_t *>(m + A.off_ptr);
+  const uint16_t *inc = reinterpret_cast<const uint16_t *>(m + A.off_inc);
+  for (int base = 0; base < 2 * U; base += kTile) {  // uniform over the CTA (shuffles)
+    const int r2 = base + tid, r = r2 >> 1, half = r2 & 1;
+    double s0[D], s1[D];
+#pragma unroll
+    for (int cc = 0; cc < D; ++cc) s0[cc] = s1[cc] = 0.0;
+    if (r < U) {
+      const int lo = ptr[r], hi = ptr[r + 1], mid = (lo + hi + 1) >> 1;
+      int w = half ? mid : lo;
+      const int e = half ? hi : mid;
+      for (; w + 1 < e; w += 2) {
+        const int p0 = inc[w], p1 = inc[w + 1];
+#pragma unroll
+        for (int cc = 0; cc < D; ++cc) {
+          s0[cc] += cb[((p0 & 3) * D + cc) * kTile + (p0 >> 2)];
+          s1[cc] += cb[((p1 & 3) * D + cc) * kTile + (p1 >> 2)];
+        }
+      }
+      if (w < e) {
+        const int pk = inc[w];
+#pragma unroll
+        for (int cc = 0; cc < D; ++cc) s0[cc] += cb[((pk & 3) * D + cc) * kTile + (pk >> 2)];
+      }
+    }
+    double sacc[D];
+#pragma unroll
+    for (int cc = 0; cc < D; ++cc) {
+      const double own = s0[cc] + s1[cc];
+      const double oth = __shfl_xor_sync(0xffffffffu, own, 1);
+      sacc[cc] = half ? oth + own : own + oth;   // (first half) + (second half) on both lanes
+    }
+    if (r < U && !half) node_write<D, SC>(A, m, r, t, sacc);
+  }
+}
 #else
 template <int D, int OP, int SC>
 __device__ __forceinline__ void tile_phase2(const PipeArgs &A, const unsigned char *m, int U,
@@ -1469,8 +1579,20 @@ __global__ void __launch_bounds__(kTile, pipe_minb(OP, MAT, D)) k_tile_pipe(Pipe
     if constexpr (DEC) mb_cp_arrive(&mb_node[b]);
   };
 
+  // OP_*_R: the next tile's reference-metric block (contiguous, refm_words(D) rows) -> L2
+  auto prefetch_refm = [&](int64_t tn) {
+    if constexpr (op_refm<OP>()) {
+      if (tid < refm_words(D)) {
+        const double *src = A.refm + (tile_id(tn) * refm_words(D) + tid) * kTile;
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(src),
+                     "r"((unsigned)(kTile * sizeof(double)))
+                     : "memory");
+      }
+    }
+  };
   double eacc = 0.0;
   int64_t t = blockIdx.x;
+  if (t < A.n_tiles) prefetch_refm(t);
   if constexpr (DEC) {
     if (tid == 0) {
       for (int b = 0; b < 3; ++b) mb_init(&mb_meta[b], kTile);
@@ -1504,6 +1626,7 @@ __global__ void __launch_bounds__(kTile, pipe_minb(OP, MAT, D)) k_tile_pipe(Pipe
                            : "memory");
             }
           }
+          prefetch_refm(t + G);
         }
         const double *nb = nodeb + bn * nstride;
         double *cb = contrib + (k & 1) * ((D + 1) * D * kCbStride);
@@ -1515,7 +1638,7 @@ __global__ void __launch_bounds__(kTile, pipe_minb(OP, MAT, D)) k_tile_pipe(Pipe
           issue_meta(t + 2 * G, (k + 2) % 3);
         }
         const int U = reinterpret_cast<const int *>(m)[0];
-        if (tid < U) mb_wait(&mb_p1[k & 1], (unsigned)(k >> 1) & 1u);  // all of tile k's phase 1
+        if (tid < (FEM_P2_PAIR ? 2 * U : U)) mb_wait(&mb_p1[k & 1], (unsigned)(k >> 1) & 1u);  // all of tile k's phase 1
         if constexpr (op_has_p2<OP>()) tile_phase2<D, OP, SC>(A, m, U, tile_id(t), tid, cb);
         mb_arrive(&mb_p2[k & 1]);
       }
@@ -1536,6 +1659,7 @@ __global__ void __launch_bounds__(kTile, pipe_minb(OP, MAT, D)) k_tile_pipe(Pipe
                            : "memory");
             }
           }
+          prefetch_refm(t + G);
         }
         const double *nb = nodeb + bn * nstride;
         double *cb = contrib + (k & 1) * ((D + 1) * D * kCbStride);
@@ -1574,6 +1698,7 @@ __global__ void __launch_bounds__(kTile, pipe_minb(OP, MAT, D)) k_tile_pipe(Pipe
       if (t + G < A.n_tiles) {
         issue_nodes(metab + ((k + 1) % 3) * mb, (k + 1) & 1);
         if constexpr (STREAM) issue_geom(t + G, (k + 1) & 1);
+        prefetch_refm(t + G);
       }
       if (t + 2 * G < A.n_tiles) issue_meta(t + 2 * G, (k + 2) % 3);
       cp_async_commit();
@@ -1623,6 +1748,7 @@ static fem_status launch_pipe_t(Problem *p, const PipeArgs &a, cudaStream_t s) {
   const TileSet &T = p->tiles;
   const bool need_u = op_needs_u<OP, MAT>();
   const int nf = (op_needs_x<OP, MAT>() ? 1 : 0) + (need_u ? 1 : 0) + (op_is_hvp<OP>() ? 1 : 0);
+  if constexpr (op_refm<OP>()) static_assert(MAT == FEM_NEO_HOOKEAN, "OP_*_R: neo-Hookean only");
   const size_t smem = (size_t)3 * T.mb + sizeof(double) * 2 * (size_t)T.um * D * nf +
                       (!op_has_p2<OP>() ? 0 : (pipe_decoupled<OP>() ? 2 : 1) * sizeof(double) * (size_t)(D + 1) * D * kCbStride) +
                       (op_streams<OP>() ? 2 * sizeof(double) * geom_words(D) * kTile : 0);
@@ -1635,12 +1761,17 @@ static fem_status launch_pipe_t(Problem *p, const PipeArgs &a, cudaStream_t s) {
 
 template <int OP, bool MASK, int SC>
 static fem_status launch_pipe_op(Problem *p, const PipeArgs &a, cudaStream_t s) {
-  if (p->dim == 2) {
-    if (p->material == FEM_LINEAR_ELASTIC) return launch_pipe_t<2, FEM_LINEAR_ELASTIC, OP, MASK, SC>(p, a, s);
-    return launch_pipe_t<2, FEM_NEO_HOOKEAN, OP, MASK, SC>(p, a, s);
+  if constexpr (op_refm<OP>()) {  // neo-Hookean only (tile_pass maps LE to the base op)
+    if (p->dim == 2) return launch_pipe_t<2, FEM_NEO_HOOKEAN, OP, MASK, SC>(p, a, s);
+    return launch_pipe_t<3, FEM_NEO_HOOKEAN, OP, MASK, SC>(p, a, s);
+  } else {
+    if (p->dim == 2) {
+      if (p->material == FEM_LINEAR_ELASTIC) return launch_pipe_t<2, FEM_LINEAR_ELASTIC, OP, MASK, SC>(p, a, s);
+      return launch_pipe_t<2, FEM_NEO_HOOKEAN, OP, MASK, SC>(p, a, s);
+    }
+    if (p->material == FEM_LINEAR_ELASTIC) return launch_pipe_t<3, FEM_LINEAR_ELASTIC, OP, MASK, SC>(p, a, s);
+    return launch_pipe_t<3, FEM_NEO_HOOKEAN, OP, MASK, SC>(p, a, s);
   }
-  if (p->material == FEM_LINEAR_ELASTIC) return launch_pipe_t<3, FEM_LINEAR_ELASTIC, OP, MASK, SC>(p, a, s);
-  return launch_pipe_t<3, FEM_NEO_HOOKEAN, OP, MASK, SC>(p, a, s);
 }
 
 // Streamed geometry (FEM_STREAM_GEOM): per tile one contiguous SoA block {c_a[j] (D x D),
@@ -1667,6 +1798,55 @@ __global__ void k_geom_stream(const double *coords, const int32_t *conn, const i
       for (int j = 0; j < D; ++j) g[(a * D + j) * kTile] = c[a][j];
     g[D * D * kTile] = det;
   }
+}
+
+// Reference metric (OP_*_R): per tile one contiguous SoA block {mu vol G_a.G_b (a <= b),
+// 1/det J} x kTile elements in tile order, computed once per problem from the coordinates with
+// the recompute path's own arithmetic (cofactors, fem_rcp, sr = mu id / d!), so the cached and
+// recomputed kernels see the same bits.  mu is the element's (phase table) shear modulus.
+template <int D>
+__global__ void k_refm(const double *coords, const int32_t *conn, const int32_t *perm,
+                       const uint8_t *phase, const double *mu_tab, double mu0, int64_t E,
+                       int64_t n_slots, double *refm) {
+  constexpr int RW = refm_words(D);
+  constexpr double inv_fact = (D == 3) ? 1.0 / 6.0 : 0.5;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_slots;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t t = i / kTile, l = i % kTile;
+    double *g = refm + t * RW * kTile + l;
+    if (i >= E) {
+      for (int w = 0; w < RW - 1; ++w) g[w * kTile] = 0.0;
+      g[(RW - 1) * kTile] = 1.0;
+      continue;
+    }
+    const int64_t e = perm[i];
+    double x[D + 1][D], c[D][D];
+    for (int a = 0; a <= D; ++a)
+      for (int j = 0; j < D; ++j) x[a][j] = coords[(int64_t)conn[e * (D + 1) + a] * D + j];
+    const double det = cof_gradients<D>(x, c);
+    const double id = fem_rcp(det);
+    const double mu = phase ? mu_tab[phase[i]] : mu0;
+    const double sr = mu * id * inv_fact;
+    for (int a = 0; a < D; ++a)
+      for (int b = a; b < D; ++b) {
+        double tt = 0.0;
+        for (int j = 0; j < D; ++j) tt = fma(c[a][j], c[b][j], tt);
+        g[sym_idx(a, b, D) * kTile] = sr * tt;
+      }
+    g[(RW - 1) * kTile] = id;
+  }
+}
+
+fem_status build_refm(Problem *p, cudaStream_t s) {
+  TileSet &T = p->tiles;
+  if (T.refm) return FEM_OK;
+  const int D = p->dim;
+  const int64_t n_slots = T.n_tiles * kTile;
+  FEM_CUDA(cudaMalloc(&T.refm, sizeof(double) * refm_words(D) * n_slots));
+  if (D == 3) k_refm<3><<<grid_for(n_slots), kThreads, 0, s>>>(p->coords, p->conn, T.perm, T.phase, p->mu_tab, p->mu, p->n_elems, n_slots, T.refm);
+  else k_refm<2><<<grid_for(n_slots), kThreads, 0, s>>>(p->coords, p->conn, T.perm, T.phase, p->mu_tab, p->mu, p->n_elems, n_slots, T.refm);
+  FEM_LAUNCH_CHECK("reference metric");
+  return FEM_OK;
 }
 
 fem_status build_geom_stream(Problem *p, cudaStream_t s) {
@@ -1733,6 +1913,16 @@ fem_status tile_pass(Problem *p, int op, const double *u, const double *v, doubl
   fem_status st = build_tiles(p, s);
   if (st) return st;
   if (p->n_elems == 0) return FEM_OK;
+  if (op == OP_RESIDUAL_R || op == OP_HVP_R) {
+    // the reference-metric forms exist for the neo-Hookean spatial kernels; the deterministic
+    // slot mode, the tile-colored passes and the energy partials keep the recompute form
+    if (p->material != FEM_NEO_HOOKEAN || det || part == 3 || partials)
+      op = op == OP_RESIDUAL_R ? OP_RESIDUAL : OP_HVP;
+    else {
+      st = build_refm(p, s);
+      if (st) return st;
+    }
+  }
   const TileSet &T = p->tiles;
   PipeArgs a{};
   a.meta = T.meta;
@@ -1764,6 +1954,7 @@ fem_status tile_pass(Problem *p, int op, const double *u, const double *v, doubl
   a.lin = p->lin;
   a.lin_stride = T.n_tiles * kTile;
   a.geom = T.geom;
+  a.refm = T.refm;
   if (part == 3) {  // tile-colored passes (FEM_TILE_COLORED): plain writes, no atomics
     if (det || (op != OP_RESIDUAL && op != OP_HVP)) return FEM_ERR_INVALID_ARG;
     st = build_tile_colors(p, s);
@@ -1801,6 +1992,9 @@ fem_status tile_pass(Problem *p, int op, const double *u, const double *v, doubl
     if (op == OP_RESIDUAL_S) return launch_pipe_op<OP_RESIDUAL_S, false, 0>(p, a, s);
     return mask ? launch_pipe_op<OP_HVP_S, true, 0>(p, a, s) : launch_pipe_op<OP_HVP_S, false, 0>(p, a, s);
   }
+  if (op == OP_RESIDUAL_R) return launch_pipe_op<OP_RESIDUAL_R, false, 0>(p, a, s);
+  if (op == OP_HVP_R)
+    return mask ? launch_pipe_op<OP_HVP_R, true, 0>(p, a, s) : launch_pipe_op<OP_HVP_R, false, 0>(p, a, s);
   if (op == OP_RESIDUAL) return launch_pipe_op<OP_RESIDUAL, false, 0>(p, a, s);
   if (op == OP_HVP_LIN)
     return mask ? launch_pipe_op<OP_HVP_LIN, true, 0>(p, a, s) : launch_pipe_op<OP_HVP_LIN, false, 0>(p, a, s);
@@ -1903,7 +2097,7 @@ fem_status morton_node_order(Problem *p, cudaStream_t s) {
 
 void free_tiles(TileSet &T) {
   void *bufs[] = {T.perm, T.nodes, T.U, T.ptr, T.inc, T.lconn, T.interior, T.phase, T.slot_off,
-                  T.node_slots, T.node_slot_ptr, T.epart, T.meta, T.list, T.geom, T.tcolor_list};
+                  T.node_slots, T.node_slot_ptr, T.epart, T.meta, T.list, T.geom, T.tcolor_list, T.refm};
   for (void *b : bufs)
     if (b) cudaFree(b);
   T = TileSet{};

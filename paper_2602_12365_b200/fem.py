@@ -34,6 +34,7 @@ BASELINE_SCATTER = 8
 STREAM_GEOM = 512          # residual / HVP from the streamed per-element geometry (Alg. 1)
 COLORED_SCATTER = 1024     # residual / HVP by element-colored conflict-free passes
 TILE_COLORED = 2048        # residual / HVP by tile-colored passes (plain boundary writes)
+REFERENCE_METRIC = 8192    # NH residual / HVP: read the cached reference metric (Alg. 1)
 LOCAL_ONLY = 16
 STATUS = {0: "OK", 1: "INVALID_ARG", 2: "DEGENERATE_ELEMENT", 3: "INVERTED_ELEMENT",
           4: "NONFINITE", 5: "CG_BREAKDOWN", 6: "NOT_CONVERGED", 7: "TOO_MANY_COLORS",

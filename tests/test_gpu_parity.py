@@ -99,7 +99,7 @@ def test_hvp(case, bc):
     assert rel(prob.hvp(dev(z), dev(v), bc=bc), ref.hvp(z, v, bc=bc)) <= TOL
 
 
-@pytest.mark.parametrize("flag", ["DETERMINISTIC", "BASELINE_SCATTER", "STREAM_GEOM", "COLORED_SCATTER",
+@pytest.mark.parametrize("flag", ["DETERMINISTIC", "BASELINE_SCATTER", "STREAM_GEOM", "REFERENCE_METRIC", "COLORED_SCATTER",
                                   "TILE_COLORED"])
 def test_residual_hvp_modes(case, fem, flag):
     name, mesh, prob, ref, z, v = case
@@ -285,11 +285,11 @@ def test_full_size_sampled_parity(fem, oracle_mod, cfg):
         yr = ref.hvp_rows(z, v, rows, bc=bc)
         assert np.abs(y[rows] - yr).max() <= TOL * np.abs(y).max()
         prob.linearize(zt)
-        for f in (fem.DETERMINISTIC, fem.BASELINE_SCATTER, fem.LINEARIZED, fem.STREAM_GEOM,
+        for f in (fem.DETERMINISTIC, fem.BASELINE_SCATTER, fem.LINEARIZED, fem.STREAM_GEOM, fem.REFERENCE_METRIC,
                   fem.COLORED_SCATTER, fem.TILE_COLORED):  # other HVP modes
             yf = prob.hvp(zt, vt, bc=bc, flags=f).cpu().numpy()
             assert np.abs(yf[rows] - yr).max() <= TOL * np.abs(y).max()
-        for f in (fem.STREAM_GEOM, fem.COLORED_SCATTER, fem.TILE_COLORED):   # other residual modes
+        for f in (fem.STREAM_GEOM, fem.REFERENCE_METRIC, fem.COLORED_SCATTER, fem.TILE_COLORED):   # other residual modes
             rf = prob.residual(zt, bc=bc, flags=f).cpu().numpy()
             assert np.abs(rf[rows] - rr).max() <= TOL * np.abs(r).max()
     # tangent and residual patch tests at full size (exact on any P1 mesh)

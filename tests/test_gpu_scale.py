@@ -85,7 +85,7 @@ def test_cfg4_one_gpu_nnz_above_2_31(fem, oracle_mod):
         yr = ref.hvp_rows(z, v, rows, bc=bc)
         ymax = float(y.abs().max())
         assert np.abs(y[rt].cpu().numpy() - yr).max() <= TOL * ymax
-        for f in (fem.DETERMINISTIC, fem.BASELINE_SCATTER, fem.STREAM_GEOM, fem.COLORED_SCATTER,
+        for f in (fem.DETERMINISTIC, fem.BASELINE_SCATTER, fem.STREAM_GEOM, fem.REFERENCE_METRIC, fem.COLORED_SCATTER,
                   fem.TILE_COLORED):
             yf = prob.hvp(zt, vt, bc=bc, flags=f)
             assert np.abs(yf[rt].cpu().numpy() - yr).max() <= TOL * ymax
@@ -142,7 +142,7 @@ def test_unstructured_3d_delaunay_1e5_dofs(fem, oracle_mod):
     assert abs(prob.energy(zt).item() - e) <= TOL * abs(e)
     for bc in (False, True):
         rr, yr = ref.residual(z, bc=bc), ref.hvp(z, v, bc=bc)
-        for f in (0, fem.DETERMINISTIC, fem.BASELINE_SCATTER, fem.STREAM_GEOM, fem.COLORED_SCATTER,
+        for f in (0, fem.DETERMINISTIC, fem.BASELINE_SCATTER, fem.STREAM_GEOM, fem.REFERENCE_METRIC, fem.COLORED_SCATTER,
                   fem.TILE_COLORED):
             assert rel(prob.residual(zt, bc=bc, flags=f), rr) <= TOL
             assert rel(prob.hvp(zt, vt, bc=bc, flags=f), yr) <= TOL

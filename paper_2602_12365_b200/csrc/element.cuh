@@ -196,6 +196,27 @@ __device__ __forceinline__ double cof_gradients(const double (&x)[D + 1][D], dou
   }
 }
 
+// Gradients G_a from the cofactor rows with the SFU-seeded reciprocal: G_a = c_a / det
+// (a >= 1), G_0 = -sum_a G_a; returns det J and 1/det J in id.
+template <int D>
+__device__ __forceinline__ double cof_geometry(const double (&x)[D + 1][D], double (&G)[D + 1][D],
+                                               double &id) {
+  double c[D][D];
+  const double det = cof_gradients<D>(x, c);
+  id = fem_rcp(det);
+#pragma unroll
+  for (int j = 0; j < D; ++j) {
+    double s = 0.0;
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+      G[a + 1][j] = c[a][j] * id;
+      s += G[a + 1][j];
+    }
+    G[0][j] = -s;
+  }
+  return det;
+}
+
 // Edge form of the deformed element x + u: node 0 at the origin, node a at
 // (x_a - x_0) + (u_a - u_0).  Differences first: forming x + u would round at the scale of
 // |x| instead of the element size (cofactors of a 1e-3 element off by 1e-13 relative).

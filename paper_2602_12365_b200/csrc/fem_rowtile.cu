@@ -67,6 +67,10 @@
 #ifndef FEM_RT_SCHED
 #define FEM_RT_SCHED 1
 #endif
+// element contexts in cofactor form with fem_rcp instead of geometry()'s IEEE divisions
+#ifndef FEM_RT_COF
+#define FEM_RT_COF 1
+#endif
 
 namespace fem {
 
@@ -529,7 +533,15 @@ __global__ void __launch_bounds__(kRtThreads, FEM_RT_MINB) k_rows_tile(RtArgs A)
           x[a][i] = xs[li[a] * D + i];
           u[a][i] = us[li[a] * D + i];
         }
+#if FEM_RT_COF
+      // cofactor form with the SFU-seeded reciprocal (reading R12): G_a = c_a / det (a >= 1),
+      // G_0 = -sum_a G_a — no IEEE divisions and their slow-path branches
+      double id0;
+      const double det0 = cof_geometry<D>(x, G, id0);
+      vol = det0 * (D == 3 ? 1.0 / 6.0 : 0.5);
+#else
       const double det0 = geometry<D>(x, G, vol);
+#endif
       double lam = A.lam, mu = A.mu;
       if (A.has_phase) {
         const int ph = m[L.off_ph + e];
@@ -548,9 +560,15 @@ __global__ void __launch_bounds__(kRtThreads, FEM_RT_MINB) k_rows_tile(RtArgs A)
         // g_a = F^-T G_a is the shape-function gradient in the deformed configuration, i.e.
         // the geometry of the element at x + u, and J = det F = det J(x + u) / det J(x): two
         // independent geometry chains instead of H -> F^-1 -> F^-T G (shorter dependencies)
-        double xc[NEN][D], g[NEN][D], volc;
+        double xc[NEN][D], g[NEN][D];
         deformed_edges<D>(x, u, xc);
+#if FEM_RT_COF
+        double idc;
+        const double Jd = cof_geometry<D>(xc, g, idc) * id0;
+#else
+        double volc;
         const double Jd = geometry<D>(xc, g, volc) / det0;
+#endif
         ok = Jd > 0.0;
         if (!ok) atomicOr(A.err, ERRW_INVERTED);
         c1 = ok ? mu - lam * fem_log(Jd) : 0.0;

@@ -775,6 +775,9 @@ __host__ __device__ constexpr int pipe_minb2d(int op, int mat) {
 #define FEM_RESR_MINB 3
 #endif
 __host__ __device__ constexpr int pipe_minb(int op, int mat, int dim = 3) {
+#ifdef FEM_HVPR_CTAS
+  if (op == OP_HVP_R && dim == 3) return FEM_HVPR_CTAS;
+#endif
   return op == OP_HVP_R ? (256 / kTile) * (dim == 2 ? 3 : FEM_HVPR_MINB)
          : op == OP_RESIDUAL_R ? (256 / kTile) * (dim == 2 ? 5 : FEM_RESR_MINB) :
          (256 / kTile) *
@@ -1506,12 +1509,18 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned by
 #ifndef FEM_DEC2
 #define FEM_DEC2 0
 #endif
+// HVP on the mbarrier-decoupled pipeline (double-buffered contributions); 0: the CTA-wide
+// pipeline of the residual (single contribution buffer: 60 KB of shared memory at cfg 3, so
+// 3 CTAs/SM fit when the register budget allows, FEM_HVP_MINB=3)
+#ifndef FEM_HVP_DEC
+#define FEM_HVP_DEC 1
+#endif
 #ifndef FEM_ENERGY_DEC
 #define FEM_ENERGY_DEC 0
 #endif
 template <int OP>
 constexpr bool pipe_decoupled() {
-  return (op_is_hvp<OP>() && !op_streams<OP>()) || (FEM_RES_DEC && OP == OP_RESIDUAL) ||
+  return (FEM_HVP_DEC && op_is_hvp<OP>() && !op_streams<OP>()) || (FEM_RES_DEC && OP == OP_RESIDUAL) ||
          (FEM_ENERGY_DEC && OP == OP_ENERGY);
 }
 

@@ -40,7 +40,10 @@ def parse():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", type=int, default=3, choices=[2, 3, 5])
+    ap.add_argument("--config", type=int, default=3, choices=[2, 3, 5, 6],
+                    help="BASELINE cfg 2 / 3 / 5; 6 = unstructured 3D NH Delaunay block (not a "
+                         "BASELINE config: the general-mesh paths at scale; --n = interior points "
+                         "in thousands, default 1000)")
     ap.add_argument("--n", type=int, default=None, help="override the mesh size (cells per side)")
     ap.add_argument("--assemble-mode", default="auto", choices=["auto", "batched", "literal", "rows", "scatter", "colored"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -53,7 +56,22 @@ def parse():
     return ap.parse_args()
 
 
+def delaunay_workload(n_pts):
+    """cfg 6 (reading R11): qhull Delaunay of seeded points + a surface grid, NH,
+    roller stretch; state noise 1e-4 h (Delaunay slivers invert under a 1e-2 h jitter)."""
+    side = max(4, int(round(n_pts ** (1.0 / 3.0) / 2.5)))
+    mesh = fi.roller_bc(fi.delaunay_tet4(n_pts, side, 7).copy_with(material=fi.NEO_HOOKEAN), 0.05)
+    h = mesh.length / n_pts ** (1.0 / 3.0)
+    z = fi.lift(mesh, fi.generic_state(mesh, 5, eps=0.05, noise=1e-4, h=h))
+    v = fi.random_direction(mesh.n_total, 4)
+    name = (f"unstructured 3D NH Delaunay block: {n_pts} interior points + {side}^3 surface grid, "
+            f"{mesh.n_total} DOFs, {mesh.n_elems} tets (not a BASELINE config)")
+    return mesh, name, z, v
+
+
 def workload(cfg, n):
+    if cfg == 6:
+        return delaunay_workload(1000 * (n or 1000))
     mesh = fi.config_mesh(cfg, n=n)
     name = {2: "cfg2: 2D NH plate Tri3", 3: "cfg3: 3D NH block Kuhn-Tet4",
             5: "cfg5: 2D LE + periodic MPC Tri3"}[cfg]
@@ -135,11 +153,14 @@ def oracle_sample(cfg, budget=4.0):
         os.sched_setaffinity(0, {sorted(os.sched_getaffinity(0))[0]})
     except (AttributeError, OSError):
         pass
-    n = {3: 40, 2: 400, 5: 400}[cfg]
-    mesh = fi.config_mesh(cfg, n=n)
-    h = mesh.length / max(mesh.shape)
-    z = fi.lift(mesh, fi.generic_state(mesh, 5, eps=0.05, noise=0.01, h=h))
-    v = fi.random_direction(mesh.n_total, 4)
+    if cfg == 6:
+        mesh, _, z, v = delaunay_workload(30000)
+    else:
+        n = {3: 40, 2: 400, 5: 400}[cfg]
+        mesh = fi.config_mesh(cfg, n=n)
+        h = mesh.length / max(mesh.shape)
+        z = fi.lift(mesh, fi.generic_state(mesh, 5, eps=0.05, noise=0.01, h=h))
+        v = fi.random_direction(mesh.n_total, 4)
     o = oracle.Oracle(mesh)
     N = mesh.n_total
     t0 = time.perf_counter()
@@ -158,7 +179,8 @@ def oracle_sample(cfg, budget=4.0):
     total = time.perf_counter() - t0
     per_op = {k: {"s": t, "GDOF/s": N / t / 1e9} for k, t in secs.items()}
     return {"value": N / secs["hvp"] / 1e9, "unit": UNIT, "cores": 1, "kind": "oracle",
-            "sample": f"oracle (plain C, 1 thread pinned to one core) on the {n}^{mesh.dim}-cell "
+            "sample": f"oracle (plain C, 1 thread pinned to one core) on the "
+                      f"{'30k-point Delaunay' if cfg == 6 else f'{n}^{mesh.dim}-cell'} "
                       f"sub-block of the workload ({N} DOFs, nnz {len(ci)}): energy, residual, "
                       f"HVP (value), pattern, coloring, best of <= 3 runs each; {total:.1f} s",
             "n_dofs": N, "per_op": per_op, "host_cpu": host_cpu(), "oracle_threads": 1}
@@ -230,7 +252,8 @@ def workload_name(cfg):
     return {3: "BASELINE cfg3: 3D compressible neo-Hookean block, 150^3 Kuhn-Tet4 cells, "
                "10,328,853 DOFs, perturbed a=0.1, roller eps=0.05",
             2: "BASELINE cfg2: 2D compressible neo-Hookean plate, 706^2 Tri3 cells, 999,698 DOFs",
-            5: "BASELINE cfg5: 2D linear elastic + periodic MPC"}[cfg]
+            5: "BASELINE cfg5: 2D linear elastic + periodic MPC",
+            6: "unstructured 3D NH Delaunay block (not a BASELINE config)"}[cfg]
 
 
 # ------------------------------------------------------------------ B200 arm

@@ -329,7 +329,7 @@ struct RowArgs {
   const int32_t *inc;
   const int64_t *nadj_ptr;
   const int32_t *nadj;
-  const uint8_t *slot_list;
+  const uint16_t *slot_list;
   const uint16_t *slot_off;
   const int32_t *dmpc_ptr, *dmpc, *ms, *mm;
   const int64_t *row_ptr;
@@ -345,15 +345,15 @@ struct RowArgs {
 template <int D>
 __global__ void k_slot_build(const int64_t *inc_ptr, const int32_t *inc, const int32_t *conn,
                              const int64_t *nadj_ptr, const int32_t *nadj, int64_t n_nodes,
-                             uint8_t *slot_list, uint16_t *slot_off, int *err) {
+                             uint16_t *slot_list, uint16_t *slot_off, int *err) {
   constexpr int NEN = D + 1;
   for (int64_t n = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; n < n_nodes;
        n += (int64_t)gridDim.x * blockDim.x) {
     const int deg = (int)(inc_ptr[n + 1] - inc_ptr[n]);
     const int64_t a0 = nadj_ptr[n];
     const int sn = (int)(nadj_ptr[n + 1] - a0);
-    if (deg > 63 || sn > 2 * kRowLanes) { atomicOr(err, ERRW_ADJ_OVERFLOW); continue; }
-    uint16_t cnt[2 * kRowLanes + 1];
+    if (deg > kRowMaxDeg || sn > kMaxNodeAdj) { atomicOr(err, ERRW_ADJ_OVERFLOW); continue; }
+    uint16_t cnt[kMaxNodeAdj + 1];
     for (int q = 0; q <= sn; ++q) cnt[q] = 0;
     for (int pass = 0; pass < 2; ++pass) {
       for (int l = 0; l < deg; ++l) {
@@ -366,7 +366,7 @@ __global__ void k_slot_build(const int64_t *inc_ptr, const int32_t *inc, const i
             if (nadj[a0 + mid] < m) lo = mid + 1; else hi = mid;
           }
           if (pass == 0) cnt[lo + 1]++;
-          else slot_list[NEN * inc_ptr[n] + cnt[lo]++] = (uint8_t)(l << 2 | b);
+          else slot_list[NEN * inc_ptr[n] + cnt[lo]++] = (uint16_t)(l << 2 | b);
         }
       }
       if (pass == 0) {
@@ -393,8 +393,8 @@ template <int D, bool TR = false>
 __global__ void __launch_bounds__(kRowLanes * kRowGroups, FEM_ROWS_MINB) k_rows_fused(RowArgs A) {
   constexpr int NEN = D + 1, BS = D * D;
   __shared__ __align__(16) double stage[kRowGroups][kRowLanes][NEN * BS + 1];  // +1: no bank conflicts
-  __shared__ uint8_t s_list[kRowGroups][NEN * 64];                              // node's slot list
-  __shared__ uint16_t s_off[kRowGroups][2 * kRowLanes + 1];                     // its slot offsets
+  __shared__ uint16_t s_list[kRowGroups][NEN * kRowMaxDeg];                     // node's slot list
+  __shared__ uint16_t s_off[kRowGroups][kMaxNodeAdj + 1];                       // its slot offsets
   const unsigned FULL = 0xffffffffu;
   const int lane = threadIdx.x % kRowLanes, g = threadIdx.x / kRowLanes;
   const int my_i = (lane % BS) / D, my_k = lane % D;  // diagonal entry of lanes < BS
@@ -417,7 +417,7 @@ __global__ void __launch_bounds__(kRowLanes * kRowGroups, FEM_ROWS_MINB) k_rows_
     }
     const int64_t rp_lane = lane < D ? A.row_ptr[n * D + lane] : 0;
     const int64_t rp_my = __shfl_sync(FULL, rp_lane, my_i);
-    const uint8_t *sl = s_list[g];
+    const uint16_t *sl = s_list[g];
     const uint16_t *so = s_off[g];
     double dsum = 0.0;  // diagonal-block entry (lanes < BS), summed over all incident elements
     for (int l0 = 0; l0 < deg; l0 += kRowLanes) {
@@ -666,7 +666,7 @@ static fem_status build_slot_lists(Problem *p, cudaStream_t s) {
   int64_t nadj_total = 0;
   FEM_CUDA(cudaMemcpyAsync(&nadj_total, p->nadj_ptr + p->n_nodes, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
   FEM_CUDA(cudaStreamSynchronize(s));
-  FEM_CUDA(cudaMalloc(&p->slot_list, nent > 0 ? nent : 1));
+  FEM_CUDA(cudaMalloc(&p->slot_list, sizeof(uint16_t) * (nent > 0 ? nent : 1)));
   FEM_CUDA(cudaMalloc(&p->slot_off, sizeof(uint16_t) * (nadj_total + nnode_nnz + 1)));
   if (p->dim == 2)
     k_slot_build<2><<<grid_for(p->n_nodes, 128), 128, 0, s>>>(p->inc_ptr, p->inc, p->conn, p->nadj_ptr, p->nadj, p->n_nodes, p->slot_list, p->slot_off, p->d_err);

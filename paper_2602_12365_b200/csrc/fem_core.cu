@@ -49,7 +49,8 @@ fem_status read_error_word(Problem *p, cudaStream_t s) {
     return FEM_ERR_TOO_MANY_COLORS;
   }
   if (h & ERRW_ADJ_OVERFLOW) {
-    set_error("a node has more than kMaxNodeAdj distinct neighbours");
+    set_error("a node exceeds an adjacency capacity: more than kMaxNodeAdj = 128 distinct "
+              "neighbours, or more than kRowMaxDeg = 256 incident elements (row-gather assembly)");
     return FEM_ERR_INVALID_ARG;
   }
   if (h & ERRW_NONFINITE) {

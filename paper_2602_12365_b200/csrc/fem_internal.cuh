@@ -38,7 +38,8 @@ struct NvtxScope {
 
 enum : int { ERRW_INVERTED = 1, ERRW_TOO_MANY_COLORS = 2, ERRW_NONFINITE = 4, ERRW_ADJ_OVERFLOW = 8 };
 
-constexpr int kMaxNodeAdj = 128;    // max distinct node neighbours (incl. self) per node (setup-time local arrays; Delaunay 3D meshes reach ~32)
+constexpr int kMaxNodeAdj = 128;    // max distinct node neighbours (incl. self) per node (setup-time local arrays; Delaunay 3D meshes reach ~36)
+constexpr int kRowMaxDeg = 256;     // max incident elements per node in the row-gather assembly fallback (k_rows_fused)
 constexpr int kReduceBlocks = 1184; // 148 SMs x 8: fixed grid => fixed reduction order
 constexpr int kThreads = 256;
 #ifndef FEM_TILE
@@ -136,7 +137,7 @@ struct Problem {
   int64_t *row_ptr = nullptr;
   int32_t *col_idx = nullptr;
   int64_t *diag_pos = nullptr;  // [N] position of the diagonal in each row (-1 if absent)
-  uint8_t *slot_list = nullptr; // fused assembly: per node (l << 2 | b) grouped by CSR slot
+  uint16_t *slot_list = nullptr; // fused assembly: per node (l << 2 | b) grouped by CSR slot
   uint16_t *slot_off = nullptr; // [nnz_node + n_nodes] slot offsets into each node's list
   int32_t *node_order = nullptr; // [n_nodes] Morton order of the nodes (assembly)
   // FEM_ASSEMBLE_COLORED: seed nodes grouped by node color (Morton order within a color) and

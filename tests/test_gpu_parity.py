@@ -48,6 +48,10 @@ def meshes():
         "2d-nh-delaunay": fi.roller_bc(fi.delaunay_tri3(1800, 30, 7).copy_with(material=1), 0.05),
         # unstructured tets (App. A): node degrees 13-30, > 16 slots on many nodes
         "3d-nh-delaunay": fi.roller_bc(fi.delaunay_tet4(1500, 6, 7).copy_with(material=1), 0.05),
+        # coarse surface grid around dense interior points: surface nodes with up to 80 incident
+        # tets and 45 neighbours (beyond the node-tile and row-plan caps: the row-gather
+        # fallback at high degree)
+        "3d-nh-delaunay-graded": fi.roller_bc(fi.delaunay_tet4(3000, 3, 7).copy_with(material=1), 0.05),
     }
     ph = fi.two_phase(fi.perturb(fi.grid_tri3(16, 16), 0.2, 8).copy_with(material=1), 0.3,
                       (0.5, 0.3), (5.0, 3.0))
@@ -57,6 +61,8 @@ def meshes():
 
 
 MESHES = meshes()
+# state noise (x h) per mesh where the default 1e-2 inverts slivers (reading R11)
+NOISE = {"3d-nh-delaunay-graded": 1e-4}
 
 
 @pytest.fixture(scope="module", params=sorted(MESHES))
@@ -64,7 +70,7 @@ def case(request, fem, oracle_mod):
     mesh = MESHES[request.param]
     prob = fem.Problem(mesh)
     ref = oracle_mod.Oracle(mesh)
-    z = fi.lift(mesh, fi.generic_state(mesh, 1))
+    z = fi.lift(mesh, fi.generic_state(mesh, 1, noise=NOISE.get(request.param, 0.01)))
     v = fi.random_direction(mesh.n_total, 2)
     return request.param, mesh, prob, ref, z, v
 

@@ -77,7 +77,9 @@ namespace fem {
 constexpr int kRtNT = FEM_RT_NT;         // nodes per tile
 constexpr int kRtUnroll = FEM_RT_UNROLL; // entries per unrolled step of the slot sums
 constexpr int kRtThreads = 256;          // 8 warps, 2 nodes per warp per pass
-constexpr int kRtLPNMax = 16;            // lanes per node: 16 (3D) or 8 (2D, <= 8 off-diag slots)
+constexpr int kRtLPNMax = 32;            // lanes per node: 8 (2D, <= 8 off-diagonal slots), 16 (3D Kuhn,
+                                         // <= 16) or 32 (unstructured, 8-node tiles)
+constexpr int kRtMaxSlots = 64;          // off-diagonal slots per node: a lane sums slots ql, ql + LPN, ...
 constexpr int kRtSortMax = 4096;         // plan: keys sorted per tile in shared memory
 
 template <int D>
@@ -111,7 +113,7 @@ static RtLayout rt_layout(int nt, int lpn, int uem, int unm, int es, int ss, boo
   L.off_ph = r16(L.off_lc + 8 * uem);
   L.off_nd = r16(L.off_ph + (phase ? uem : 0));
   L.off_so = r16(L.off_nd + 16 * nt);
-  L.off_sb = r16(L.off_so + nt * ss);
+  L.off_sb = r16(L.off_so + 2 * nt * ss);   // slot offsets: uint16
   L.off_en = r16(L.off_sb + nt * ss);
   L.mb = r16(L.off_en + 2 * nt * es);
   return L;
@@ -227,7 +229,8 @@ __global__ void __launch_bounds__(256) k_rt_plan(const int32_t *node_order, int6
   }
   // per tile node: row word, off-diagonal slots, block list
   int4 *ndw = reinterpret_cast<int4 *>(blk + L.off_nd);
-  uint8_t *so = blk + L.off_so, *sb = blk + L.off_sb;
+  uint16_t *so = reinterpret_cast<uint16_t *>(blk + L.off_so);
+  uint8_t *sb = blk + L.off_sb;
   uint16_t *en = reinterpret_cast<uint16_t *>(blk + L.off_en);
   for (int j = tid; j < L.nt; j += nthr) {
     ndw[j] = make_int4(0, 0, 0, 0);
@@ -246,7 +249,8 @@ __global__ void __launch_bounds__(256) k_rt_plan(const int32_t *node_order, int6
     };
     const int ds = sn > 0 ? slot_of(n) : 0;
     const int sno = sn > 0 ? sn - 1 : 0;
-    if (sn == 0 || ds >= sn || nadj[a0 + ds] != n || sno > L.lpn || (NEN - 1) * deg > L.es) {
+    if (sn == 0 || ds >= sn || nadj[a0 + ds] != n || sno > kRtMaxSlots || sno + 1 > L.ss ||
+        (NEN - 1) * deg > L.es) {
       atomicOr(bad, 1);
       continue;
     }
@@ -260,7 +264,7 @@ __global__ void __launch_bounds__(256) k_rt_plan(const int32_t *node_order, int6
       if (extra < 0 || extra > 0xffff || (i < D && extra > 0xffff)) atomicOr(bad, 1);
       ex[i] = (int)extra;
     }
-    uint8_t c[kRtLPNMax + 2];
+    uint16_t c[kRtMaxSlots + 2];
     for (int q = 0; q <= sno; ++q) c[q] = 0;
     auto q_of = [&](int s) { return s < ds ? s : s - 1; };
     for (int l = 0; l < deg; ++l) {
@@ -290,13 +294,13 @@ __global__ void __launch_bounds__(256) k_rt_plan(const int32_t *node_order, int6
     int maxrun = 0;
     for (int q = 0; q < sno; ++q) maxrun = max(maxrun, (int)(c[q + 1] - c[q]));
     if (deg <= kSchedMaxDeg && maxrun > 0) {
-      uint32_t msk[kSchedMaxDeg];
+      uint64_t msk[kSchedMaxDeg];
       for (int l = 0; l < deg; ++l) {
         const int32_t pk = inc[i0 + l];
         const int64_t e = pk / NEN;
         const int a = pk % NEN;
-        uint32_t mm = 0;
-        for (int k = 1; k < NEN; ++k) mm |= 1u << q_of(slot_of(conn[e * NEN + (a + k) % NEN]));
+        uint64_t mm = 0;
+        for (int k = 1; k < NEN; ++k) mm |= 1ull << q_of(slot_of(conn[e * NEN + (a + k) % NEN]));
         msk[l] = mm;
       }
       uint8_t perm[kSchedMaxDeg], it[kSchedMaxDeg];
@@ -309,7 +313,7 @@ __global__ void __launch_bounds__(256) k_rt_plan(const int32_t *node_order, int6
             const int k = (int)((st >> 8) % (uint32_t)(l + 1));
             const uint8_t tmp = perm[l]; perm[l] = perm[k]; perm[k] = tmp;
           }
-        uint32_t busy[kSchedMaxC];
+        uint64_t busy[kSchedMaxC];
         for (int k = 0; k < kSchedMaxC; ++k) busy[k] = 0;
         int C = 0;
         for (int x = 0; x < deg; ++x) {
@@ -328,7 +332,7 @@ __global__ void __launch_bounds__(256) k_rt_plan(const int32_t *node_order, int6
         const int C = attempt(seed);
         if (C < best) { best = C; bseed = seed; }
       }
-      if (best <= kSchedMaxC && sno * best <= L.es && sno * best <= 255) {
+      if (best <= kSchedMaxC && sno * best <= L.es) {
         attempt(bseed);
         const uint16_t zero = (uint16_t)(L.uem | 0 << 10 | 1 << 12);
         for (int q = 0; q < sno * best; ++q) ej[q] = zero;
@@ -342,7 +346,7 @@ __global__ void __launch_bounds__(256) k_rt_plan(const int32_t *node_order, int6
             ej[q_of(slot_of(conn[e * NEN + b])) * best + it[l]] = (uint16_t)(r | a << 10 | b << 12);
           }
         }
-        for (int q = 0; q <= sno; ++q) so[j * L.ss + q] = (uint8_t)(q * best);
+        for (int q = 0; q <= sno; ++q) so[j * L.ss + q] = (uint16_t)(q * best);
         ndw[j] = word;
         continue;
       }
@@ -380,15 +384,21 @@ fem_status build_row_tiles(Problem *p, cudaStream_t s) {
     IS = std::max<int>(IS, (int)(hip[i + 1] - hip[i]));
     SN = std::max<int>(SN, (int)(hap[i + 1] - hap[i]));
   }
-  if (SN - 1 > kRtLPNMax) return FEM_OK;
+  if (SN - 1 > kRtMaxSlots) return FEM_OK;
   // 8 lanes per node when the slots allow (2D Tri3: 6): 4 nodes per warp, 32-node tiles;
-  // otherwise 16 lanes (3D Kuhn: 14 slots), 2 nodes per warp, kRtNT-node tiles
-  const int LPN = (SN - 1 <= 8 && !getenv("FEM_RT_LPN16")) ? 8 : 16;
-  const int NT = LPN == 8 ? 32 : kRtNT;
+  // 16 lanes (3D Kuhn: 14 slots), 2 nodes per warp, kRtNT-node tiles; more slots
+  // (unstructured meshes): 32 lanes, one node per warp, 8-node tiles (the element sets of
+  // high-degree nodes are large), each lane summing slots ql, ql + 32
+  const bool force32 = getenv("FEM_RT_LPN32") != nullptr;  // tests: the unstructured form anywhere
+  const int LPN = force32 ? 32
+                  : (D == 2 && SN - 1 <= 8 && !getenv("FEM_RT_LPN16")) ? 8
+                  : (SN - 1 <= 16) ? 16 : 32;
+  const int NT = LPN == 8 ? 32 : LPN == 16 ? kRtNT : 8;
   const int64_t nt = (n + NT - 1) / NT;
-  const int ES = std::max((((NEN - 1) * IS) + 7) & ~7, FEM_RT_SCHED ? LPN * (D == 3 ? 7 : 5) : 0),
-            SS = (LPN + 1 + 3) & ~3;
-  if (IS == 0 || (NEN - 1) * IS > 255) return FEM_OK;
+  const int MS = std::max(LPN, SN - 1);  // slots per node the layout holds
+  const int ES = std::max((((NEN - 1) * IS) + 7) & ~7, FEM_RT_SCHED ? MS * (D == 3 ? 7 : 5) : 0),
+            SS = (MS + 1 + 3) & ~3;
+  if (IS == 0 || ES > 65535) return FEM_OK;
   int *d_bad = nullptr;
   int32_t *cnt = nullptr;
   FEM_CUDA(cudaMalloc(&d_bad, sizeof(int)));
@@ -604,12 +614,20 @@ __global__ void __launch_bounds__(kRtThreads, FEM_RT_MINB) k_rows_tile(RtArgs A)
       auto roff = [&](int i) -> int64_t {
         return (int64_t)i * D * sn + (i == 0 ? 0 : (i == 1 ? (nd.x & 0xffff) : ((unsigned)nd.x >> 16)));
       };
-      int lo = 0, hi = 0;
-      if (ql < sno) {
-        lo = m[L.off_so + j * L.ss + ql];
-        hi = m[L.off_so + j * L.ss + ql + 1];
-      }
       const uint16_t *ent = reinterpret_cast<const uint16_t *>(m + L.off_en) + j * L.es;
+      const uint16_t *sof = reinterpret_cast<const uint16_t *>(m + L.off_so) + j * L.ss;
+      const bool live = j < nn;
+      double dacc = 0.0;  // lanes ql < BS: diagonal entry, summed over the slot passes
+      // slot passes: 8 / 16 lanes are chosen only when every node has <= LPN slots (one
+      // pass); 32 lanes (one node per warp) loop over ceil(sno / 32) passes
+      const int npass = LPN == 32 ? (sno + LPN - 1) / LPN : 1;
+      for (int pass = 0; pass < npass; ++pass) {
+      const int q = pass * LPN + ql;           // this lane's slot in this pass
+      int lo = 0, hi = 0;
+      if (q < sno) {
+        lo = sof[q];
+        hi = sof[q + 1];
+      }
       double acc[BS];
 #pragma unroll
       for (int q = 0; q < BS; ++q) acc[q] = 0.0;
@@ -647,10 +665,9 @@ __global__ void __launch_bounds__(kRtThreads, FEM_RT_MINB) k_rows_tile(RtArgs A)
           }
         }
       }
-      const bool live = j < nn;
-      if (live && ql < sno) {
-        const unsigned sbc = A.bc ? m[L.off_sb + j * L.ss + ql] : 0u;
-        const int s = ql + (ql >= ds);
+      if (live && q < sno) {
+        const unsigned sbc = A.bc ? m[L.off_sb + j * L.ss + q] : 0u;
+        const int s = q + (q >= ds);
         double *row = A.vals + rp0 + s * D;
         if ((sbc | bcn) == 0u) {
 #pragma unroll
@@ -673,19 +690,22 @@ __global__ void __launch_bounds__(kRtThreads, FEM_RT_MINB) k_rows_tile(RtArgs A)
       // diagonal block = -sum of the node's off-diagonal slots, ascending slot order
       double *scr = scratch + (w * 32 + lane) * Gm::BP;
 #pragma unroll
-      for (int q = 0; q < BS; ++q) scr[q] = acc[q];
+      for (int qq = 0; qq < BS; ++qq) scr[qq] = acc[qq];
       __syncwarp();
       if (live && ql < BS) {
-        const int i = ql / D, kk = ql % D;
         const double *sb = scratch + (w * 32 + h * LPN) * Gm::BP + ql;
-        double v = 0.0;
-        for (int q = 0; q < sno; ++q) v += sb[q * Gm::BP];
-        v = -v;
+        const int cnt = min(LPN, sno - pass * LPN);
+        for (int qq = 0; qq < cnt; ++qq) dacc += sb[qq * Gm::BP];
+      }
+      __syncwarp();
+      }  // slot passes
+      if (live && ql < BS) {
+        const int i = ql / D, kk = ql % D;
+        double v = -dacc;
         if (bcn & (1u << kk)) v = 0.0;                      // masked column
         if (bcn & (1u << i)) v = (i == kk) ? 1.0 : 0.0;     // identity row
         A.vals[rp0 + roff(i) + ds * D + kk] = v;
       }
-      __syncwarp();
 #else
       // diagonal block = -sum over the node's slots (fixed butterfly order)
 #pragma unroll
@@ -695,6 +715,7 @@ __global__ void __launch_bounds__(kRtThreads, FEM_RT_MINB) k_rows_tile(RtArgs A)
         for (int o = LPN / 2; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, v, o, LPN);
         acc[q] = v;
       }
+      }  // slot passes (FEM_RT_DIAG_SMEM=0 supports one pass only: LPN >= slots)
       if (live) {
 #pragma unroll
         for (int q = 0; q < BS; ++q)
@@ -722,13 +743,14 @@ fem_status launch_row_tiles(Problem *p, const double *z, double *vals, bool bc, 
   A.lam = p->lam; A.mu = p->mu; A.lam_tab = p->lam_tab; A.mu_tab = p->mu_tab;
   A.has_phase = p->phase != nullptr; A.bc = bc ? 1 : 0; A.vals = vals; A.err = p->d_err;
   void (*kern)(RtArgs);
-  const bool le = p->material == FEM_LINEAR_ELASTIC, l8 = A.L.lpn == 8;
+  const bool le = p->material == FEM_LINEAR_ELASTIC;
+  const int lpn = A.L.lpn;
   if (p->dim == 2)
-    kern = le ? (l8 ? k_rows_tile<2, FEM_LINEAR_ELASTIC, 8> : k_rows_tile<2, FEM_LINEAR_ELASTIC, 16>)
-              : (l8 ? k_rows_tile<2, FEM_NEO_HOOKEAN, 8> : k_rows_tile<2, FEM_NEO_HOOKEAN, 16>);
+    kern = le ? (lpn == 8 ? k_rows_tile<2, FEM_LINEAR_ELASTIC, 8> : lpn == 16 ? k_rows_tile<2, FEM_LINEAR_ELASTIC, 16> : k_rows_tile<2, FEM_LINEAR_ELASTIC, 32>)
+              : (lpn == 8 ? k_rows_tile<2, FEM_NEO_HOOKEAN, 8> : lpn == 16 ? k_rows_tile<2, FEM_NEO_HOOKEAN, 16> : k_rows_tile<2, FEM_NEO_HOOKEAN, 32>);
   else
-    kern = le ? (l8 ? k_rows_tile<3, FEM_LINEAR_ELASTIC, 8> : k_rows_tile<3, FEM_LINEAR_ELASTIC, 16>)
-              : (l8 ? k_rows_tile<3, FEM_NEO_HOOKEAN, 8> : k_rows_tile<3, FEM_NEO_HOOKEAN, 16>);
+    kern = le ? (lpn == 16 ? k_rows_tile<3, FEM_LINEAR_ELASTIC, 16> : k_rows_tile<3, FEM_LINEAR_ELASTIC, 32>)
+              : (lpn == 16 ? k_rows_tile<3, FEM_NEO_HOOKEAN, 16> : k_rows_tile<3, FEM_NEO_HOOKEAN, 32>);
   FEM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, p->rt_smem));
   int per_sm = 0;
   FEM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kRtThreads, p->rt_smem));

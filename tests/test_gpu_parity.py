@@ -388,6 +388,21 @@ def test_row_assembly_fallback_kernels(fem, oracle_mod, variant, monkeypatch):
             assert rel(vals, oracle_mod.Oracle(mesh).assemble_alg2(z, bc=bc)) <= TOL
 
 
+def test_row_tiles_32_lanes(fem, oracle_mod, monkeypatch):
+    """The 32-lane node tiles (one node per warp, 8-node tiles, each lane summing slots ql and
+    ql + 32: the unstructured-mesh form) forced on meshes the 8/16-lane tiles would take,
+    incl. multiplier columns; the Delaunay meshes run them by default (> 16 slots, and > 32
+    on the graded mesh's surface nodes: two slot passes)."""
+    monkeypatch.setenv("FEM_RT_LPN32", "1")
+    for name in ("3d-nh", "3d-le", "2d-nh-roller", "2d-le-mpc", "2d-nh-phases-fext"):
+        mesh = MESHES[name]
+        z = fi.lift(mesh, fi.generic_state(mesh, 1))
+        prob = fem.Problem(mesh)
+        for bc in (False, True):
+            vals = prob.assemble_csr(dev(z), bc=bc, mode="rows")
+            assert rel(vals, oracle_mod.Oracle(mesh).assemble_alg2(z, bc=bc)) <= TOL
+
+
 def test_cg_graph_batches_match_direct_launches(fem, monkeypatch):
     """CG iterations between host checks run as a captured CUDA graph (check_every >= 2);
     with the deterministic CSR operator the iterates equal the directly launched ones bit

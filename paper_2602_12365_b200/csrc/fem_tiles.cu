@@ -492,7 +492,12 @@ __global__ void k_pack_meta(TileSet T, const uint8_t *node_bc, int64_t E) {
       __syncthreads();
       for (int i = threadIdx.x; i < nvalid; i += blockDim.x) inc[T.inc[t * T.maxe + i]] = (uint16_t)i;
     } else {
-      for (int i = threadIdx.x; i < kTile * 4; i += blockDim.x) inc[i] = i < nvalid ? T.inc[t * T.maxe + i] : 0;
+      // contribution offsets (a D kTile + el) of the incidences (el << 2 | a): the node sums
+      // add cb[w + c kTile] without unpacking; the bank (el mod 16) is w mod 16 as before
+      for (int i = threadIdx.x; i < kTile * 4; i += blockDim.x) {
+        const int e = i < nvalid ? T.inc[t * T.maxe + i] : 0;
+        inc[i] = (uint16_t)((e & 3) * D * kTile + (e >> 2));
+      }
     }
   }
   for (int i = threadIdx.x; i < T.um; i += blockDim.x) {
@@ -1393,14 +1398,14 @@ __device__ __forceinline__ void tile_phase2(const PipeArgs &A, const unsigned ch
         const int p0 = inc[w], p1 = inc[w + 1];
 #pragma unroll
         for (int cc = 0; cc < D; ++cc) {
-          s0[cc] += cb[((p0 & 3) * D + cc) * kTile + (p0 >> 2)];
-          s1[cc] += cb[((p1 & 3) * D + cc) * kTile + (p1 >> 2)];
+          s0[cc] += cb[p0 + cc * kTile];
+          s1[cc] += cb[p1 + cc * kTile];
         }
       }
       if (w < e) {
         const int pk = inc[w];
 #pragma unroll
-        for (int cc = 0; cc < D; ++cc) s0[cc] += cb[((pk & 3) * D + cc) * kTile + (pk >> 2)];
+        for (int cc = 0; cc < D; ++cc) s0[cc] += cb[pk + cc * kTile];
       }
     }
     double sacc[D];
@@ -1416,10 +1421,11 @@ __device__ __forceinline__ void tile_phase2(const PipeArgs &A, const unsigned ch
 #else
 template <int D, int OP, int SC>
 __device__ __forceinline__ void tile_phase2(const PipeArgs &A, const unsigned char *m, int U,
-                                            int64_t t, int tid, const double *cb) {
+                                            int64_t t, int tid, const double *cb,
+                                            int nth = kTile) {
   const uint16_t *ptr = reinterpret_cast<const uint16_t *>(m + A.off_ptr);
   const uint16_t *inc = reinterpret_cast<const uint16_t *>(m + A.off_inc);
-  for (int r = tid; r < U; r += kTile) {  // one thread per tile node, D components
+  for (int r = tid; r < U; r += nth) {  // one thread per tile node, D components
     const int lo = ptr[r], hi = ptr[r + 1];
     // two interleaved partial sums (even / odd incidences, combined in a fixed order):
     // halves the dependent shared-memory-load -> add chain of the node's sum (A/B at cfg 3:
@@ -1432,14 +1438,14 @@ __device__ __forceinline__ void tile_phase2(const PipeArgs &A, const unsigned ch
       const int p0 = inc[w], p1 = inc[w + 1];
 #pragma unroll
       for (int cc = 0; cc < D; ++cc) {
-        s0[cc] += cb[((p0 & 3) * D + cc) * kTile + (p0 >> 2)];
-        s1[cc] += cb[((p1 & 3) * D + cc) * kTile + (p1 >> 2)];
+        s0[cc] += cb[p0 + cc * kTile];
+        s1[cc] += cb[p1 + cc * kTile];
       }
     }
     if (w < hi) {
       const int pk = inc[w];
 #pragma unroll
-      for (int cc = 0; cc < D; ++cc) s0[cc] += cb[((pk & 3) * D + cc) * kTile + (pk >> 2)];
+      for (int cc = 0; cc < D; ++cc) s0[cc] += cb[pk + cc * kTile];
     }
     double sacc[D];
 #pragma unroll
@@ -1726,6 +1732,130 @@ __global__ void __launch_bounds__(kTile, pipe_minb(OP, MAT, D)) k_tile_pipe(Pipe
   }
 }
 
+
+// ------------------------------------------------------------------ warp-specialized tiles
+// FEM_WS: residual / HVP with the roles split by warpgroup (setmaxnreg): warpgroups 0-1 (one
+// element per thread) run only phase 1; warpgroup 2 (the producer) stages every tile — its
+// metadata block by one TMA bulk copy, its nodal data by cp.async gathers — and runs phase 2
+// (the node sums and writes) of tile k while the element warps compute tile k+1.  Hand-offs
+// are mbarriers: node[b] (data landed, 128 producer arrivals), full[b] (phase 1 done, 256),
+// empty[b] (contributions consumed, 128); contributions and node data double-buffered, the
+// metadata triple-buffered.  No CTA-wide barrier in the loop, so the element warps never
+// wait for the node sums (the ~24 % barrier stall of k_tile_pipe).  Registers: launch 80 x
+// 384; the producer gives back to 48, the element warps take 96.  Parity-tested; measured at
+// cfg 3 (r02, same box): HVP 0.984 / residual 0.845 ms against 0.925 / 0.795 for k_tile_pipe
+// (producer 32 / elements 104 registers: 1.155 / 1.037 — the node sums serialise their loads;
+// three contribution buffers: 1.123 / 0.930).  ncu: the element warps now wait on empty[b]
+// (25 % of stall samples): the producer's latency-bound node sums, stretched by issue
+// contention with 16 element warps, take longer than phase 1 — so off by default.
+#ifndef FEM_WS
+#define FEM_WS 0
+#endif
+#ifndef FEM_WS_RC
+#define FEM_WS_RC 96
+#endif
+#ifndef FEM_WS_RP
+#define FEM_WS_RP 48
+#endif
+#ifndef FEM_WS_CB
+#define FEM_WS_CB 2   // contribution buffers (the element warps run up to CB tiles ahead)
+#endif
+constexpr int kWsProd = 128;  // producer threads (one warpgroup)
+static_assert(kTile == 256, "FEM_WS: two element warpgroups per 256-element tile");
+
+template <int D, int MAT, int OP, bool MASK>
+__global__ void __launch_bounds__(kTile + kWsProd, 2) k_tile_ws(PipeArgs A) {
+  constexpr bool NEED_U = op_needs_u<OP, MAT>();
+  constexpr bool NEED_X = op_needs_x<OP, MAT>();
+  constexpr int NF = (NEED_X ? 1 : 0) + (NEED_U ? 1 : 0) + (op_is_hvp<OP>() ? 1 : 0);
+  constexpr int UOFF = NEED_X ? 1 : 0;
+  constexpr int CB = (D + 1) * D * kCbStride;
+  constexpr int NCB = FEM_WS_CB;
+  static_assert(!FEM_P2_BAL && !FEM_P2_NM && !FEM_P2_G8 && !FEM_P2_PAIR, "FEM_WS: default phase 2");
+  extern __shared__ __align__(128) unsigned char sm[];
+  __shared__ __align__(8) uint64_t mb_meta[3], mb_node[2], mb_full[NCB], mb_empty[NCB];
+  const int tid = threadIdx.x;
+  const int mb = A.mb, um = A.um;
+  const int nstride = um * D * NF;
+  unsigned char *metab = sm;
+  double *nodeb = reinterpret_cast<double *>(sm + 3 * mb);
+  double *contrib = nodeb + 2 * nstride;
+  const int64_t G = gridDim.x, t0 = blockIdx.x;
+  const int64_t nk = t0 < A.n_tiles ? (A.n_tiles - 1 - t0) / G + 1 : 0;  // tiles of this CTA
+  auto tile_id = [&](int64_t k) -> int64_t {
+    const int64_t i = t0 + k * G;
+    return A.list ? (int64_t)__ldg(A.list + i) : i;
+  };
+  if (tid == 0) {
+    for (int b = 0; b < 3; ++b) mb_init(&mb_meta[b], 1);
+    for (int b = 0; b < 2; ++b) mb_init(&mb_node[b], kWsProd);
+    for (int b = 0; b < NCB; ++b) {
+      mb_init(&mb_full[b], kTile);
+      mb_init(&mb_empty[b], kWsProd);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  if (tid >= kTile) {  // ---------------- producer warpgroup
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(FEM_WS_RP) : "memory");
+    const int pt = tid - kTile;
+    auto issue_meta = [&](int64_t k) {
+      if (pt == 0) {
+        uint64_t *bar = &mb_meta[k % 3];
+        mb_expect_tx(bar, (unsigned)mb);
+        bulk_g2s(metab + (k % 3) * mb, A.meta + tile_id(k) * (int64_t)mb, (unsigned)mb, bar);
+      }
+    };
+    auto issue_nodes = [&](int64_t k) {  // tile k's nodal data -> node buffer k & 1
+      const unsigned char *m = metab + (k % 3) * mb;
+      double *dst = nodeb + (k & 1) * nstride;
+      const int U = reinterpret_cast<const int *>(m)[0];
+      const int32_t *nodes = reinterpret_cast<const int32_t *>(m + A.off_nodes);
+      for (int r = pt; r < U; r += kWsProd) {
+        const int64_t g = (int64_t)nodes[r] * D;
+#pragma unroll
+        for (int c = 0; c < D; ++c) {
+          if constexpr (NEED_X) cp_async8(dst + r * D + c, A.coords + g + c);
+          if constexpr (NEED_U) cp_async8(dst + UOFF * um * D + r * D + c, A.u + g + c);
+          if constexpr (op_is_hvp<OP>()) cp_async8(dst + (NF - 1) * um * D + r * D + c, A.v + g + c);
+        }
+      }
+      mb_cp_arrive(&mb_node[k & 1]);
+    };
+    for (int64_t k = 0; k < 3 && k < nk; ++k) issue_meta(k);
+    for (int64_t k = 0; k < 2 && k < nk; ++k) {
+      mb_wait(&mb_meta[k % 3], (unsigned)(k / 3) & 1u);
+      issue_nodes(k);
+    }
+    for (int64_t k = 0; k < nk; ++k) {
+      mb_wait(&mb_full[k % NCB], (unsigned)(k / NCB) & 1u);  // phase 1 of tile k done
+      if (k + 2 < nk) {  // node buffer k & 1 is free: tile k + 2's data
+        mb_wait(&mb_meta[(k + 2) % 3], (unsigned)((k + 2) / 3) & 1u);
+        issue_nodes(k + 2);
+      }
+      const unsigned char *m = metab + (k % 3) * mb;
+      tile_phase2<D, OP, 0>(A, m, reinterpret_cast<const int *>(m)[0], tile_id(k), pt,
+                            contrib + (k % NCB) * CB, kWsProd);
+      mb_arrive(&mb_empty[k % NCB]);
+      asm volatile("bar.sync 1, %0;\n" ::"n"(kWsProd) : "memory");  // metadata k read by all
+      if (k + 3 < nk) issue_meta(k + 3);
+    }
+    asm volatile("cp.async.wait_all;\n" ::: "memory");
+  } else {  // ---------------- element warpgroups
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(FEM_WS_RC) : "memory");
+    double eacc = 0.0;
+    for (int64_t k = 0; k < nk; ++k) {
+      mb_wait(&mb_node[k & 1], (unsigned)(k >> 1) & 1u);                     // tile k staged
+      if (k >= NCB) mb_wait(&mb_empty[k % NCB], (unsigned)((k - NCB) / NCB) & 1u);  // buffer free
+      const unsigned char *m = metab + (k % 3) * mb;
+      const double *nb = nodeb + (k & 1) * nstride;
+      tile_phase1<D, MAT, OP, MASK>(A, m, nb, nb + UOFF * um * D, nb + (NF - 1) * um * D,
+                                    tile_id(k), tid, contrib + (k % NCB) * CB, eacc);
+      mb_arrive(&mb_full[k % NCB]);
+    }
+  }
+}
+
 // DET: y[node] = sum of its tile slots in tile order
 template <int D>
 __global__ void k_slot_gather(const int64_t *node_slot_ptr, const int32_t *node_slots,
@@ -1766,6 +1896,30 @@ static fem_status launch_pipe_t(Problem *p, const PipeArgs &a, cudaStream_t s) {
   kern<<<pipe_grid(p, OP, a.n_tiles), kTile, smem, s>>>(a);
   FEM_LAUNCH_CHECK("tile pipeline kernel");
   return FEM_OK;
+}
+
+template <int D, int MAT, int OP, bool MASK>
+static fem_status launch_ws_t(Problem *p, const PipeArgs &a, cudaStream_t s) {
+  const TileSet &T = p->tiles;
+  const int nf = (op_needs_x<OP, MAT>() ? 1 : 0) + (op_needs_u<OP, MAT>() ? 1 : 0) + (op_is_hvp<OP>() ? 1 : 0);
+  const size_t smem = (size_t)3 * T.mb + sizeof(double) * 2 * (size_t)T.um * D * nf +
+                      FEM_WS_CB * sizeof(double) * (size_t)(D + 1) * D * kCbStride;
+  auto kern = k_tile_ws<D, MAT, OP, MASK>;
+  FEM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(a.n_tiles, 148 * 2));
+  kern<<<grid, kTile + kWsProd, smem, s>>>(a);
+  FEM_LAUNCH_CHECK("warp-specialized tile kernel");
+  return FEM_OK;
+}
+
+template <int OP, bool MASK>
+static fem_status launch_ws_op(Problem *p, const PipeArgs &a, cudaStream_t s) {
+  if (p->dim == 2) {
+    if (p->material == FEM_LINEAR_ELASTIC) return launch_ws_t<2, FEM_LINEAR_ELASTIC, OP, MASK>(p, a, s);
+    return launch_ws_t<2, FEM_NEO_HOOKEAN, OP, MASK>(p, a, s);
+  }
+  if (p->material == FEM_LINEAR_ELASTIC) return launch_ws_t<3, FEM_LINEAR_ELASTIC, OP, MASK>(p, a, s);
+  return launch_ws_t<3, FEM_NEO_HOOKEAN, OP, MASK>(p, a, s);
 }
 
 template <int OP, bool MASK, int SC>
@@ -2004,6 +2158,10 @@ fem_status tile_pass(Problem *p, int op, const double *u, const double *v, doubl
   if (op == OP_RESIDUAL_R) return launch_pipe_op<OP_RESIDUAL_R, false, 0>(p, a, s);
   if (op == OP_HVP_R)
     return mask ? launch_pipe_op<OP_HVP_R, true, 0>(p, a, s) : launch_pipe_op<OP_HVP_R, false, 0>(p, a, s);
+  if (FEM_WS && (op == OP_RESIDUAL || op == OP_HVP) && !partials) {
+    if (op == OP_RESIDUAL) return launch_ws_op<OP_RESIDUAL, false>(p, a, s);
+    return mask ? launch_ws_op<OP_HVP, true>(p, a, s) : launch_ws_op<OP_HVP, false>(p, a, s);
+  }
   if (op == OP_RESIDUAL) return launch_pipe_op<OP_RESIDUAL, false, 0>(p, a, s);
   if (op == OP_HVP_LIN)
     return mask ? launch_pipe_op<OP_HVP_LIN, true, 0>(p, a, s) : launch_pipe_op<OP_HVP_LIN, false, 0>(p, a, s);

@@ -661,11 +661,12 @@ def main():
                     "peak_nominal": FP64_NOMINAL, "frac_nominal": pr["frac_fp64_nominal"],
                     "frac_hbm": pr["frac_hbm"]}
     traffic = None
-    try:
-        tj = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
-        traffic = tj["dram_bytes_per_launch"].get(dom)
-    except Exception:
-        pass
+    if args.config == 3 and world == 1 and not args.n and args.scaling != "strong":
+        try:  # ncu's DRAM bytes of the same launch configuration (profiled on cfg 3 only)
+            tj = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
+            traffic = tj["dram_bytes_per_launch"].get(dom)
+        except Exception:
+            pass
     roofline.update({"traffic": traffic, "kernel_phase": dom,
                      "note": "algorithmic bytes/flops per launch / CUDA-event time of the phase; "
                              "traffic from ncu in profiles/"})

@@ -82,6 +82,10 @@
 #ifndef FEM_P2_PAIR
 #define FEM_P2_PAIR 0
 #endif
+// unroll factor of the default node-sum loop (pairs of incidences per unrolled step)
+#ifndef FEM_P2_UNROLL
+#define FEM_P2_UNROLL 1
+#endif
 // Phase 0: one thread per tile node issues the node's D-vector copies (no div / mod by D;
 // A/B r02: neutral, 0.975 vs 0.972 ms HVP)
 // NH HVP in metric form (M_ab = c_a . c_b, D_ab = dv_b . cs_a): fewer FP64 operations than
@@ -98,6 +102,7 @@ namespace fem {
 // row stride of the per-tile contribution array cb[(a D + c)][kCbStride]: G8 appends 8 zero
 // columns (the pad entries of the incidence groups point there)
 constexpr int kCbStride = FEM_P2_G8 ? kTile + 8 : kTile;
+constexpr int kP2Unroll = FEM_P2_UNROLL;
 static_assert(!(FEM_P2_G8 && FEM_P2_BAL), "FEM_P2_G8 and FEM_P2_BAL are alternatives");
 static_assert(!(FEM_P2_NM && (FEM_P2_G8 || FEM_P2_BAL)), "FEM_P2_NM is an alternative phase 2");
 
@@ -1434,6 +1439,7 @@ __device__ __forceinline__ void tile_phase2(const PipeArgs &A, const unsigned ch
 #pragma unroll
     for (int cc = 0; cc < D; ++cc) s0[cc] = s1[cc] = 0.0;
     int w = lo;
+#pragma unroll kP2Unroll
     for (; w + 1 < hi; w += 2) {
       const int p0 = inc[w], p1 = inc[w + 1];
 #pragma unroll

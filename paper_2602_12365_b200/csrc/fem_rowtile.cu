@@ -33,6 +33,7 @@
 
 #include "element.cuh"
 #include "fem_internal.cuh"
+#include "pipe.cuh"
 
 #ifndef FEM_RT_DIAG_SMEM
 #define FEM_RT_DIAG_SMEM 1
@@ -62,6 +63,12 @@
 #endif
 #ifndef FEM_RT_NT
 #define FEM_RT_NT 16
+#endif
+// tile metadata blocks by one TMA bulk copy per tile (mbarrier completion) instead of 16-byte
+// cp.async per thread (the LDGSTS of the block took 38 M of the 711 M shared wavefronts per
+// launch at cfg 3, 11.5 per instruction against 4 conflict-free)
+#ifndef FEM_RT_TMA_META
+#define FEM_RT_TMA_META 1
 #endif
 // co-scheduled block lists (see k_rt_plan): 0 = each slot's run in ascending element order
 #ifndef FEM_RT_SCHED
@@ -496,9 +503,28 @@ __global__ void __launch_bounds__(kRtThreads, FEM_RT_MINB) k_rows_tile(RtArgs A)
   for (int q = tid; q < RS; q += kRtThreads) rec[(size_t)L.uem * RS + q] = 0.0;  // zero record
   const int64_t G = gridDim.x;
 
-  auto issue_meta = [&](int64_t t, unsigned char *dst) {
+  __shared__ __align__(8) uint64_t mb_meta[3];
+  if (FEM_RT_TMA_META && tid == 0) {
+    for (int b = 0; b < 3; ++b) mb_init(&mb_meta[b], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  // metadata of tile t into buffer b: one bulk copy (FEM_RT_TMA_META) or 16-byte cp.async
+  auto issue_meta = [&](int64_t t, int b) {
     const unsigned char *src = A.meta + t * (int64_t)mb;
-    for (int off = tid * 16; off < mb; off += kRtThreads * 16) rt_cp16(dst + off, src + off);
+    unsigned char *dst = metab + b * mb;
+    if (FEM_RT_TMA_META) {
+      if (tid == 0) {
+        mb_expect_tx(&mb_meta[b], (unsigned)mb);
+        bulk_g2s(dst, src, (unsigned)mb, &mb_meta[b]);
+      }
+    } else {
+      for (int off = tid * 16; off < mb; off += kRtThreads * 16) rt_cp16(dst + off, src + off);
+    }
+  };
+  // wait for the metadata of the k-th tile of this CTA (buffer k % 3, use k / 3)
+  auto wait_meta = [&](int k) {
+    if (FEM_RT_TMA_META) mb_wait(&mb_meta[k % 3], (unsigned)(k / 3) & 1u);
   };
   auto issue_nodes = [&](const unsigned char *m, double *dst) {
     const int un = reinterpret_cast<const int *>(m)[1];
@@ -512,12 +538,13 @@ __global__ void __launch_bounds__(kRtThreads, FEM_RT_MINB) k_rows_tile(RtArgs A)
 
   int64_t t = blockIdx.x;
   if (t < A.n_tiles) {
-    issue_meta(t, metab);
+    issue_meta(t, 0);
     rt_commit();
     rt_wait_all();
+    wait_meta(0);
     __syncthreads();
     issue_nodes(metab, nodeb);
-    if (t + G < A.n_tiles) issue_meta(t + G, metab + mb);
+    if (t + G < A.n_tiles) issue_meta(t + G, 1);
     rt_commit();
   }
   for (int k = 0; t < A.n_tiles; ++k, t += G) {
@@ -525,8 +552,11 @@ __global__ void __launch_bounds__(kRtThreads, FEM_RT_MINB) k_rows_tile(RtArgs A)
     __syncthreads();
     const unsigned char *m = metab + (k % 3) * mb;
     const double *xs = nodeb + (k & 1) * 2 * unm * D, *us = xs + unm * D;
-    if (t + G < A.n_tiles) issue_nodes(metab + ((k + 1) % 3) * mb, nodeb + ((k + 1) & 1) * 2 * unm * D);
-    if (t + 2 * G < A.n_tiles) issue_meta(t + 2 * G, metab + ((k + 2) % 3) * mb);
+    if (t + G < A.n_tiles) {
+      wait_meta(k + 1);
+      issue_nodes(metab + ((k + 1) % 3) * mb, nodeb + ((k + 1) & 1) * 2 * unm * D);
+    }
+    if (t + 2 * G < A.n_tiles) issue_meta(t + 2 * G, (k + 2) % 3);
     rt_commit();
     const int ue = reinterpret_cast<const int *>(m)[0];
     const int nn = reinterpret_cast<const int *>(m)[2];

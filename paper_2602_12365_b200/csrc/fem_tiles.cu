@@ -22,6 +22,7 @@
 
 #include "element.cuh"
 #include "fem_internal.cuh"
+#include "pipe.cuh"
 
 #ifndef FEM_PIPE_MINB2D
 #define FEM_PIPE_MINB2D 0
@@ -757,16 +758,8 @@ fem_status pack_tile_meta(Problem *p, cudaStream_t s) {
 // cp.async copies of tile k+1's nodal data (8-byte gathers of coordinates, u, v) and tile
 // k+2's metadata block (16-byte copies) are in flight: meta is triple-, node data
 // double-buffered in shared memory, so HBM/L2 latency overlaps the FP64 element math.
-__device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
-  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
-}
-__device__ __forceinline__ void cp_async8(void *smem, const void *gmem) {
-  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem));
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+// cp.async / mbarrier / TMA bulk-copy helpers: pipe.cuh
+
 
 // CTAs per SM the register budget targets (A/B on cfg 3, profiles/): the NH HVP is the
 // register-heaviest and runs fastest spill-free at 2; energy at 4; residual at 3.
@@ -1471,42 +1464,7 @@ __device__ __forceinline__ void tile_phase2(const PipeArgs &A, const unsigned ch
 // in phase 1 of k-1, before barrier k-1); tile k+2's metadata overwrites tile k-1's (read in
 // phase 2 of k-1, before barrier k) and is issued after barrier k.  A/B (profiles/): HVP
 // 1.13 -> 1.06 ms; residual / energy slower this way (smem of the second buffer, 3-4 CTAs/SM).
-__device__ __forceinline__ unsigned smem_addr(const void *p) {
-  return (unsigned)__cvta_generic_to_shared(p);
-}
-__device__ __forceinline__ void mb_init(uint64_t *m, unsigned count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_addr(m)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mb_arrive(uint64_t *m) {  // release.cta
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_addr(m)) : "memory");
-}
-__device__ __forceinline__ void mb_cp_arrive(uint64_t *m) {
-  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(smem_addr(m)) : "memory");
-}
-__device__ __forceinline__ void mb_wait(uint64_t *m, unsigned parity) {
-  asm volatile(
-      "{\n .reg .pred p;\n"
-      "WAIT_%=:\n"
-      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-      " @!p bra WAIT_%=;\n}\n" ::"r"(smem_addr(m)),
-      "r"(parity)
-      : "memory");
-}
-
-// TMA bulk copy (non-tensor) global -> shared, completing on an mbarrier with a byte count
-__device__ __forceinline__ void mb_expect_tx(uint64_t *m, unsigned bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_addr(m)),
-               "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned bytes, uint64_t *m) {
-  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
-          smem_addr(dst)),
-      "l"(src), "r"(bytes), "r"(smem_addr(m))
-      : "memory");
-}
+// (mbarrier and TMA bulk-copy helpers: pipe.cuh)
 
 #ifndef FEM_RES_DEC
 #define FEM_RES_DEC 0

@@ -1485,6 +1485,11 @@ __device__ __forceinline__ void tile_phase2(const PipeArgs &A, const unsigned ch
 #ifndef FEM_HVP_DEC
 #define FEM_HVP_DEC 1
 #endif
+// tile metadata blocks by one TMA bulk copy per tile (thread 0, mbarrier byte count) instead of
+// 16-byte cp.async by every thread
+#ifndef FEM_TMA_META
+#define FEM_TMA_META 1
+#endif
 #ifndef FEM_ENERGY_DEC
 #define FEM_ENERGY_DEC 0
 #endif
@@ -1530,8 +1535,15 @@ __global__ void __launch_bounds__(kTile, pipe_minb(OP, MAT, D)) k_tile_pipe(Pipe
   auto issue_meta = [&](int64_t t, int b) {
     unsigned char *dst = metab + b * mb;
     const unsigned char *src = A.meta + tile_id(t) * (int64_t)mb;
-    for (int off = tid * 16; off < mb; off += kTile * 16) cp_async16(dst + off, src + off);
-    if constexpr (DEC) mb_cp_arrive(&mb_meta[b]);
+    if (FEM_TMA_META) {  // one TMA bulk copy, completion on mb_meta[b] (byte count)
+      if (tid == 0) {
+        mb_expect_tx(&mb_meta[b], (unsigned)mb);
+        bulk_g2s(dst, src, (unsigned)mb, &mb_meta[b]);
+      }
+    } else {
+      for (int off = tid * 16; off < mb; off += kTile * 16) cp_async16(dst + off, src + off);
+      if constexpr (DEC) mb_cp_arrive(&mb_meta[b]);
+    }
   };
   auto issue_nodes = [&](const unsigned char *m, int b) {
     double *dst = nodeb + b * nstride;
@@ -1574,7 +1586,7 @@ __global__ void __launch_bounds__(kTile, pipe_minb(OP, MAT, D)) k_tile_pipe(Pipe
   if (t < A.n_tiles) prefetch_refm(t);
   if constexpr (DEC) {
     if (tid == 0) {
-      for (int b = 0; b < 3; ++b) mb_init(&mb_meta[b], kTile);
+      for (int b = 0; b < 3; ++b) mb_init(&mb_meta[b], FEM_TMA_META ? 1 : kTile);
       for (int b = 0; b < 2; ++b) mb_init(&mb_node[b], kTile);
       for (int b = 0; b < 2; ++b) mb_init(&mb_p1[b], kTile);
       for (int b = 0; b < 2; ++b) mb_init(&mb_p2[b], kTile);
@@ -1651,9 +1663,10 @@ __global__ void __launch_bounds__(kTile, pipe_minb(OP, MAT, D)) k_tile_pipe(Pipe
     }
     asm volatile("cp.async.wait_all;\n" ::: "memory");
   } else {
-    if constexpr (STREAM) {
+    if (STREAM || FEM_TMA_META) {
       if (tid == 0) {
         for (int b = 0; b < 2; ++b) mb_init(&mb_geom[b], 1);
+        for (int b = 0; b < 3; ++b) mb_init(&mb_meta[b], 1);
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
       }
       __syncthreads();
@@ -1662,6 +1675,7 @@ __global__ void __launch_bounds__(kTile, pipe_minb(OP, MAT, D)) k_tile_pipe(Pipe
       issue_meta(t, 0);
       cp_async_commit();
       cp_async_wait_all();
+      if (FEM_TMA_META) mb_wait(&mb_meta[0], 0);
       __syncthreads();
       issue_nodes(metab, 0);
       if constexpr (STREAM) issue_geom(t, 0);
@@ -1675,6 +1689,7 @@ __global__ void __launch_bounds__(kTile, pipe_minb(OP, MAT, D)) k_tile_pipe(Pipe
       const unsigned char *m = metab + (k % 3) * mb;
       const double *nb = nodeb + (k & 1) * nstride;
       if (t + G < A.n_tiles) {
+        if (FEM_TMA_META) mb_wait(&mb_meta[(k + 1) % 3], (unsigned)((k + 1) / 3) & 1u);
         issue_nodes(metab + ((k + 1) % 3) * mb, (k + 1) & 1);
         if constexpr (STREAM) issue_geom(t + G, (k + 1) & 1);
         prefetch_refm(t + G);

@@ -93,7 +93,8 @@ struct TileSet {
   // packed per-tile metadata blocks (fem_tiles.cu pack_tile_meta), mb bytes each
   uint8_t *meta = nullptr;
   int um = 0, mb = 0, off_nodes = 0, off_lconn = 0, off_ptr = 0, off_inc = 0, off_int = 0,
-      off_bc = 0, off_ph = 0, off_soff = 0, off_smeta = 0;
+      off_bc = 0, off_ph = 0, off_soff = 0, off_smeta = 0, off_perm = 0;
+  uint16_t *p2perm = nullptr;    // [n_tiles][maxe] phase-2 thread -> tile node (FEM_P2_SORT)
 };
 
 struct Workspace {

@@ -83,6 +83,15 @@
 #ifndef FEM_P2_PAIR
 #define FEM_P2_PAIR 0
 #endif
+// Phase-2 node order sorted by incidence count (FEM_P2_SORT): thread q of the node sums takes
+// the tile node with the q-th longest list, so each warp's lanes loop about as often as its
+// longest list and the short lists no longer idle in warps that hold a 24-incidence node.
+// Parity-tested; A/B r02 at cfg 3: HVP 0.944 vs 0.909 ms (the warp of the longest lists is
+// the critical path before the barrier either way, and the sorted groups lose the banks
+// spread), so off by default.
+#ifndef FEM_P2_SORT
+#define FEM_P2_SORT 0
+#endif
 // unroll factor of the default node-sum loop (pairs of incidences per unrolled step)
 #ifndef FEM_P2_UNROLL
 #define FEM_P2_UNROLL 1
@@ -513,6 +522,10 @@ __global__ void k_pack_meta(TileSet T, const uint8_t *node_bc, int64_t E) {
   if (T.phase)
     for (int i = threadIdx.x; i < kTile; i += blockDim.x)
       base[T.off_ph + i] = (e0 + i < E) ? T.phase[e0 + i] : 0;
+  if (T.p2perm) {
+    uint16_t *pp = reinterpret_cast<uint16_t *>(base + T.off_perm);
+    for (int i = threadIdx.x; i < T.um; i += blockDim.x) pp[i] = i < U ? T.p2perm[t * T.maxe + i] : 0;
+  }
 }
 
 // Phase-2 bank scheduling (FEM_TILE_SCHED): every tile node sums its incident contributions
@@ -526,17 +539,22 @@ __global__ void k_sched_inc(TileSet T) {
   const int U = T.U[t];
   const uint16_t *ptr = T.ptr + t * (T.maxe + 1);
   uint16_t *inc = T.inc + t * T.maxe;
+  const uint16_t *perm = T.p2perm ? T.p2perm + t * T.maxe : nullptr;  // phase-2 thread order
   for (int g = threadIdx.x; g * 32 < U; g += blockDim.x) {
-    const int r0 = g * 32, r1 = min(U, r0 + 32);
+    const int q0 = g * 32, q1 = min(U, q0 + 32);
     int len = 0;
-    for (int r = r0; r < r1; ++r) len = max(len, (int)ptr[r + 1] - (int)ptr[r]);
+    for (int q = q0; q < q1; ++q) {
+      const int r = perm ? perm[q] : q;
+      len = max(len, (int)ptr[r + 1] - (int)ptr[r]);
+    }
     for (int w = 0; w < len; ++w) {
       // a warp's 64-bit shared loads are served per half-warp: banks must differ within each
-      // group of 16 consecutive nodes
+      // group of 16 consecutive phase-2 threads
       int cnt[16];
-      for (int r = r0; r < r1; ++r) {
-        if (((r - r0) & 15) == 0)
+      for (int qq = q0; qq < q1; ++qq) {
+        if (((qq - q0) & 15) == 0)
           for (int b = 0; b < 16; ++b) cnt[b] = 0;
+        const int r = perm ? perm[qq] : qq;
         const int lo = ptr[r] + w, hi = ptr[r + 1];
         if (lo >= hi) continue;
         int best = lo, bc = 1 << 30;
@@ -551,6 +569,22 @@ __global__ void k_sched_inc(TileSet T) {
       }
     }
   }
+}
+
+// Phase-2 thread order (FEM_P2_SORT): tile nodes by descending incidence count, ties in node
+// order (counting sort per tile, one thread per tile).
+__global__ void k_p2_perm(TileSet T) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= T.n_tiles) return;
+  const int U = T.U[t];
+  const uint16_t *ptr = T.ptr + t * (T.maxe + 1);
+  uint16_t *perm = T.p2perm + t * T.maxe;
+  int maxlen = 0;
+  for (int r = 0; r < U; ++r) maxlen = max(maxlen, (int)ptr[r + 1] - (int)ptr[r]);
+  int pos = 0;
+  for (int len = maxlen; len >= 0; --len)
+    for (int r = 0; r < U; ++r)
+      if ((int)ptr[r + 1] - (int)ptr[r] == len) perm[pos++] = (uint16_t)r;
 }
 
 // Balanced phase-2 schedule (FEM_P2_BAL).  The tile's incidences (node r, element el, slot
@@ -695,6 +729,11 @@ fem_status pack_tile_meta(Problem *p, cudaStream_t s) {
     else k_build_sched<2><<<g, 128, 0, s>>>(T, T.sched_rounds);
     FEM_LAUNCH_CHECK("phase-2 schedule");
   }
+  if (FEM_P2_SORT && !FEM_P2_BAL && !FEM_P2_G8 && !FEM_P2_NM && !FEM_P2_PAIR) {
+    FEM_CUDA(cudaMalloc(&T.p2perm, sizeof(uint16_t) * (size_t)T.n_tiles * T.maxe));
+    k_p2_perm<<<(unsigned)((T.n_tiles + 127) / 128), 128, 0, s>>>(T);
+    FEM_LAUNCH_CHECK("phase-2 node order");
+  }
   if (FEM_TILE_SCHED && !FEM_P2_BAL) {
     k_sched_inc<<<(unsigned)T.n_tiles, 8, 0, s>>>(T);
     FEM_LAUNCH_CHECK("tile incidence scheduling");
@@ -735,7 +774,8 @@ fem_status pack_tile_meta(Problem *p, cudaStream_t s) {
   }
   T.off_bc = T.off_int + round_up(T.um, 16);
   T.off_ph = T.off_bc + round_up(T.um, 16);
-  T.mb = round_up(T.off_ph + (T.phase ? kTile : 0), 16);
+  T.off_perm = round_up(T.off_ph + (T.phase ? kTile : 0), 16);
+  T.mb = round_up(T.off_perm + (T.p2perm ? 2 * T.um : 0), 16);
   FEM_CUDA(cudaMalloc(&T.meta, (size_t)T.mb * T.n_tiles));
   if (p->dim == 2) k_pack_meta<2><<<(unsigned)T.n_tiles, 256, 0, s>>>(T, p->node_bc, p->n_elems);
   else k_pack_meta<3><<<(unsigned)T.n_tiles, 256, 0, s>>>(T, p->node_bc, p->n_elems);
@@ -794,8 +834,8 @@ __host__ __device__ constexpr int pipe_minb(int op, int mat, int dim = 3) {
 struct PipeArgs {
   const uint8_t *meta;
   int64_t n_tiles, E;
-  int mb, um, off_nodes, off_lconn, off_ptr, off_inc, off_int, off_bc, off_ph, off_soff, off_smeta;
-  bool has_phase;
+  int mb, um, off_nodes, off_lconn, off_ptr, off_inc, off_int, off_bc, off_ph, off_soff, off_smeta, off_perm;
+  bool has_phase, has_perm;
   const int64_t *slot_off;
   const double *coords, *u, *v;
   double lam, mu;
@@ -1423,7 +1463,9 @@ __device__ __forceinline__ void tile_phase2(const PipeArgs &A, const unsigned ch
                                             int nth = kTile) {
   const uint16_t *ptr = reinterpret_cast<const uint16_t *>(m + A.off_ptr);
   const uint16_t *inc = reinterpret_cast<const uint16_t *>(m + A.off_inc);
-  for (int r = tid; r < U; r += nth) {  // one thread per tile node, D components
+  const uint16_t *perm = reinterpret_cast<const uint16_t *>(m + A.off_perm);
+  for (int q = tid; q < U; q += nth) {  // one thread per tile node, D components
+    const int r = A.has_perm ? perm[q] : q;
     const int lo = ptr[r], hi = ptr[r + 1];
     // two interleaved partial sums (even / odd incidences, combined in a fixed order):
     // halves the dependent shared-memory-load -> add chain of the node's sum (A/B at cfg 3:
@@ -2081,7 +2123,9 @@ fem_status tile_pass(Problem *p, int op, const double *u, const double *v, doubl
   a.off_ph = T.off_ph;
   a.off_soff = T.off_soff;
   a.off_smeta = T.off_smeta;
+  a.off_perm = T.off_perm;
   a.has_phase = T.phase != nullptr;
+  a.has_perm = T.p2perm != nullptr;
   a.slot_off = T.slot_off;
   a.coords = p->coords;
   a.u = u;
@@ -2243,7 +2287,7 @@ fem_status morton_node_order(Problem *p, cudaStream_t s) {
 
 void free_tiles(TileSet &T) {
   void *bufs[] = {T.perm, T.nodes, T.U, T.ptr, T.inc, T.lconn, T.interior, T.phase, T.slot_off,
-                  T.node_slots, T.node_slot_ptr, T.epart, T.meta, T.list, T.geom, T.tcolor_list, T.refm};
+                  T.node_slots, T.node_slot_ptr, T.epart, T.meta, T.list, T.geom, T.tcolor_list, T.refm, T.p2perm};
   for (void *b : bufs)
     if (b) cudaFree(b);
   T = TileSet{};

@@ -28,6 +28,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <vector>
 
@@ -69,6 +70,19 @@
 // launch at cfg 3, 11.5 per instruction against 4 conflict-free)
 #ifndef FEM_RT_TMA_META
 #define FEM_RT_TMA_META 1
+#endif
+// bank-aware placement of the context records (16-lane tiles): a record's shared-memory
+// bank class is its slot mod 16, so each element is given the class whose banks collide
+// least with the elements the same node reads at the same co-scheduled step (greedy at setup,
+// k_rt_plan); the half-warp of a node then reads its g_b / M_ab / g_a / sc words from spread
+// banks (ncu r02: 4.8 wavefronts per slot-loop load against 2 conflict-free).  Measured (r02,
+// cfg 3): the greedy lowers the modelled g_b wavefronts per half-warp step by 15 % only
+// (FEM_RT_PLACE_DEBUG=1 prints the model: each element's four gradient banks are a rigid
+// pattern shared by all its node-steps), ncu shows 4.74 vs 4.82 per load, and the padded
+// record slots make the kernel slower (3.63 vs 3.54 ms) — off by default.  A micro-benchmark
+// (tools/micro/lds64.cu) confirms the model: 64-bit loads are served per half-warp.
+#ifndef FEM_RT_PLACE
+#define FEM_RT_PLACE 0
 #endif
 // co-scheduled block lists (see k_rt_plan): 0 = each slot's run in ascending element order
 #ifndef FEM_RT_SCHED
@@ -212,10 +226,15 @@ __global__ void __launch_bounds__(256) k_rt_plan(const int32_t *node_order, int6
   if (tid == 0) s_un = rt_unique(halo, ue * NEN);
   __syncthreads();
   const int un = s_un;
+  // bank-aware placement: records in 16 bank classes of ceil(ue / 16) slots each
+  const bool place = FEM_RT_PLACE && FEM_RT_SCHED && L.lpn == 16;
+  const int nslot = place ? (ue + 15) & ~15 : ue;
   if (!meta) {
-    if (tid == 0) { cnt[2 * t] = ue; cnt[2 * t + 1] = un; }
+    if (tid == 0) { cnt[2 * t] = nslot; cnt[2 * t + 1] = un; }
     return;
   }
+  __shared__ uint8_t s_best[64];   // co-schedule length per tile node (0: grouped runs)
+  for (int j = tid; j < 64; j += nthr) s_best[j] = 0;
   uint8_t *blk = meta + t * (int64_t)L.mb;
   if (tid == 0) {
     int *h = reinterpret_cast<int *>(blk);
@@ -354,6 +373,7 @@ __global__ void __launch_bounds__(256) k_rt_plan(const int32_t *node_order, int6
           }
         }
         for (int q = 0; q <= sno; ++q) so[j * L.ss + q] = (uint16_t)(q * best);
+        if (j < 64) s_best[j] = (uint8_t)best;
         ndw[j] = word;
         continue;
       }
@@ -370,6 +390,135 @@ __global__ void __launch_bounds__(256) k_rt_plan(const int32_t *node_order, int6
       }
     }
     ndw[j] = word;
+  }
+  if (!place) return;
+  // ---- bank-aware record placement (one thread; the per-node schedules are complete)
+  __syncthreads();
+  constexpr int RS = RtGeom<D>::RS;
+  uint32_t *occ = reinterpret_cast<uint32_t *>(halo);   // [ue][4] (j | k << 8 | a << 16)
+  int32_t *info = elems;                                  // [ue] count | slot << 8
+  // addresses per bank of each load type (g_b, M_ab, g_a, sc) at each (warp, step): a warp's
+  // 64-bit loads serve its two nodes' 32 lanes together (ncu: 2 wavefronts conflict-free)
+  __shared__ uint8_t mk[4][8][16][16];
+  if (tid == 0) {
+    for (int r = 0; r < ue; ++r) info[r] = 0;
+    for (int c = 0; c < 4 * 8 * 16 * 16; ++c) (&mk[0][0][0][0])[c] = 0;
+    for (int j = 0; j < nn && j < 16; ++j) {
+      const int best = s_best[j];
+      if (!best) continue;
+      const int sno = ndw[j].y & 0xff;
+      const uint16_t *ej = en + j * L.es;
+      for (int c = 0; c < sno * best; ++c) {
+        const int r = ej[c] & 1023;
+        if (r >= ue) continue;                            // zero record (idle step)
+        const int k = c % best, a = (ej[c] >> 10) & 3;
+        const int n = info[r] & 0xff;
+        bool seen = false;
+        for (int o = 0; o < n; ++o) seen |= (int)(occ[r * 4 + o] & 0xff) == j;
+        if (!seen && n < 4) {
+          occ[r * 4 + n] = (uint32_t)j | (uint32_t)k << 8 | (uint32_t)a << 16;
+          info[r] = n + 1;
+        }
+      }
+    }
+    // slot classes: bank(slot) = RS slot mod 16 (RS odd: a bijection of slot mod 16)
+    int cls_cnt[16];
+    for (int c = 0; c < 16; ++c) cls_cnt[c] = 0;
+    const int cap = (ue + 15) / 16;
+    int rs_inv = 1;
+    for (int x = 1; x < 16; x += 2) if (((RS * x) & 15) == 1) rs_inv = x;
+    for (int want = 4; want >= 0; --want)  // most-constrained elements first
+      for (int r = 0; r < ue; ++r) {
+        const int n = info[r] & 0xff;
+        if (n != want) continue;
+        int bestc = -1, bcost = 1 << 30;
+        for (int sg = 0; sg < 16; ++sg) {
+          if (cls_cnt[sg] >= cap) continue;
+          int cost = 0;
+          for (int o = 0; o < n; ++o) {
+            const uint32_t w = occ[r * 4 + o];
+            const int j = (w & 0xff) >> 1, k = (w >> 8) & 0xff, a = (w >> 16) & 3;
+            for (int b = 0; b < NEN; ++b) {
+              if (b == a) continue;
+              cost += 3 * mk[0][j][k][(sg + 3 * b) & 15];
+              cost += mk[1][j][k][(sg + RtGeom<D>::M0 + rt_pair<D>(a, b)) & 15];
+            }
+            cost += 3 * mk[2][j][k][(sg + 3 * a) & 15];
+            cost += 2 * mk[3][j][k][(sg + RtGeom<D>::S0) & 15];
+          }
+          if (cost < bcost) { bcost = cost; bestc = sg; }
+        }
+        for (int o = 0; o < n; ++o) {
+          const uint32_t w = occ[r * 4 + o];
+          const int j = (w & 0xff) >> 1, k = (w >> 8) & 0xff, a = (w >> 16) & 3;
+          for (int b = 0; b < NEN; ++b) {
+            if (b == a) continue;
+            ++mk[0][j][k][(bestc + 3 * b) & 15];
+            ++mk[1][j][k][(bestc + RtGeom<D>::M0 + rt_pair<D>(a, b)) & 15];
+          }
+          ++mk[2][j][k][(bestc + 3 * a) & 15];
+          ++mk[3][j][k][(bestc + RtGeom<D>::S0) & 15];
+        }
+        const int res = (rs_inv * bestc) & 15;         // slot residue of bank class bestc
+        info[r] = (info[r] & 0xff) | (res + 16 * cls_cnt[bestc]) << 8;
+        ++cls_cnt[bestc];
+      }
+    reinterpret_cast<int *>(blk)[0] = nslot;
+    if (cnt) {  // FEM_RT_PLACE_DEBUG: modelled g_b-load wavefronts per half-warp, before / after
+      int w0 = 0, w1 = 0;
+      for (int j = 0; j < nn && j < 16; ++j) {
+        const int best = s_best[j];
+        if (!best) continue;
+        const int sno = ndw[j].y & 0xff;
+        const uint16_t *ej = en + j * L.es;
+        for (int k = 0; k < best; ++k) {
+          int c0[16], c1[16];
+          for (int b = 0; b < 16; ++b) c0[b] = c1[b] = 0;
+          for (int q = 0; q < sno; ++q) {
+            const int e = ej[q * best + k], r = e & 1023, b = (e >> 12) & 3;
+            if (r >= ue) continue;
+            ++c0[(RS * r + 3 * b) & 15];
+            ++c1[(RS * (info[r] >> 8) + 3 * b) & 15];
+          }
+          int m0 = 0, m1 = 0;
+          for (int b = 0; b < 16; ++b) { m0 = max(m0, c0[b]); m1 = max(m1, c1[b]); }
+          w0 += m0; w1 += m1;
+        }
+      }
+      cnt[2 * t] = w0; cnt[2 * t + 1] = w1;
+    }
+  }
+  __syncthreads();
+  // remap the entries and move the element connectivity / phases to their slots (holes:
+  // lc.x = 0xffff, skipped by the context phase)
+  for (int j = 0; j < nn; ++j) {
+    const int sno = ndw[j].y & 0xff;
+    uint16_t *ej = en + j * L.es;
+    for (int c = tid; c < L.es; c += nthr) {
+      const int r = ej[c] & 1023;
+      if (r < ue && (c < sno * (s_best[j] ? s_best[j] : 1) || !s_best[j]))
+        ej[c] = (uint16_t)((ej[c] & ~1023) | (info[r] >> 8));
+    }
+  }
+  ushort4 keep[4];
+  uint8_t kph[4];
+  for (int i = 0; i < 4; ++i) {
+    const int r = tid + i * nthr;
+    if (r < ue) {
+      keep[i] = reinterpret_cast<const ushort4 *>(lc)[r];
+      kph[i] = phase ? blk[L.off_ph + r] : 0;
+    }
+  }
+  __syncthreads();
+  for (int q = tid; q < nslot; q += nthr) reinterpret_cast<ushort4 *>(lc)[q] = make_ushort4(0xffff, 0, 0, 0);
+  __syncthreads();
+  for (int i = 0; i < 4; ++i) {
+    const int r = tid + i * nthr;
+    if (r < ue) {
+      const int sl = info[r] >> 8;
+      reinterpret_cast<ushort4 *>(lc)[sl] = keep[i];
+      if (phase) blk[L.off_ph + sl] = kph[i];
+    }
   }
 }
 
@@ -440,7 +589,15 @@ fem_status build_row_tiles(Problem *p, cudaStream_t s) {
   }
   FEM_CUDA(cudaMalloc(&p->rt_meta, (size_t)L.mb * nt));
   if (D == 2) k_rt_plan<2><<<(unsigned)nt, 256, 0, s>>>(p->node_order, n, p->inc_ptr, p->inc, p->conn, p->phase, p->nadj_ptr, p->nadj, p->row_ptr, p->node_bc, L, cnt, p->rt_meta, d_bad);
-  else k_rt_plan<3><<<(unsigned)nt, 256, 0, s>>>(p->node_order, n, p->inc_ptr, p->inc, p->conn, p->phase, p->nadj_ptr, p->nadj, p->row_ptr, p->node_bc, L, cnt, p->rt_meta, d_bad);
+  else k_rt_plan<3><<<(unsigned)nt, 256, 0, s>>>(p->node_order, n, p->inc_ptr, p->inc, p->conn, p->phase, p->nadj_ptr, p->nadj, p->row_ptr, p->node_bc, L, getenv("FEM_RT_PLACE_DEBUG") ? cnt : nullptr, p->rt_meta, d_bad);
+  if (getenv("FEM_RT_PLACE_DEBUG")) {
+    std::vector<int32_t> hd(2 * nt);
+    FEM_CUDA(cudaMemcpyAsync(hd.data(), cnt, sizeof(int32_t) * 2 * nt, cudaMemcpyDeviceToHost, s));
+    FEM_CUDA(cudaStreamSynchronize(s));
+    long long a0 = 0, a1 = 0;
+    for (int64_t q = 0; q < nt; ++q) { a0 += hd[2 * q]; a1 += hd[2 * q + 1]; }
+    fprintf(stderr, "[rt place] modelled g_b wavefronts per half-warp step: identity %lld, placed %lld\n", a0, a1);
+  }
   FEM_LAUNCH_CHECK("row tiles (fill)");
   FEM_CUDA(cudaMemcpyAsync(&hbad, d_bad, sizeof(int), cudaMemcpyDeviceToHost, s));
   FEM_CUDA(cudaStreamSynchronize(s));
@@ -564,6 +721,7 @@ __global__ void __launch_bounds__(kRtThreads, FEM_RT_MINB) k_rows_tile(RtArgs A)
     const uint16_t *lc = reinterpret_cast<const uint16_t *>(m + L.off_lc);
     for (int e = tid; e < (FEM_RT_DIAG_SKIP == 1 ? 0 : ue); e += kRtThreads) {
       const ushort4 l4 = reinterpret_cast<const ushort4 *>(lc)[e];
+      if (l4.x == 0xffff) continue;  // placement hole (no entry reads it)
       const int li[4] = {l4.x, l4.y, l4.z, l4.w};
       double x[NEN][D], u[NEN][D], G[NEN][D], vol;
 #pragma unroll

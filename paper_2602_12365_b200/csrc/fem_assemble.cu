@@ -739,6 +739,11 @@ static fem_status assemble_colored(Problem *p, const double *z, double *vals, bo
     k_transpose_slots<<<grid_for(p->n_nodes), kThreads, 0, s>>>(p->nadj_ptr, p->nadj, p->n_nodes, p->tslot);
     FEM_LAUNCH_CHECK("transposed slots");
   }
+  // node tiles of one color each (contexts in shared memory, transposed stores); the warp
+  // pull over HBM context records below is the fallback for meshes the tile plan rejects
+  st = build_colored_tiles(p, s);
+  if (st) return st;
+  if (p->ct.state == 1 && !getenv("FEM_COLORED_PULL")) return launch_colored_tiles(p, z, vals, bc, s);
   RowArgs A{};
   A.node_bc = bc ? p->node_bc : nullptr; A.z = z;
   A.inc_ptr = p->inc_ptr; A.inc = p->inc; A.nadj_ptr = p->nadj_ptr; A.nadj = p->nadj;
@@ -806,7 +811,7 @@ static fem_status assemble(Problem *p, const double *z, double *vals, unsigned f
   if (rows) {
     fem_status st0 = build_row_tiles(p, s);
     if (st0) return st0;
-    if (p->rt_state == 1) {
+    if (p->rt.state == 1) {
       st0 = launch_row_tiles(p, z, vals, bc, s);
       if (st0) return st0;
       if (p->n_mpc) {  // the Lagrangian's B^T columns in the u rows and the multiplier rows

@@ -97,6 +97,16 @@ struct TileSet {
   uint16_t *p2perm = nullptr;    // [n_tiles][maxe] phase-2 thread -> tile node (FEM_P2_SORT)
 };
 
+// node-tile assembly plan (fem_rowtile.cu build_tile_plan)
+struct RtPlan {
+  int state = 0;                 // 0 not built, 1 built, -1 not eligible
+  uint8_t *meta = nullptr;
+  int64_t ntiles = 0;
+  int layout[16] = {0};          // RtLayout fields
+  int smem = 0;
+  std::vector<int64_t> seg_tiles;  // first tile of each node-list segment (colors for ct)
+};
+
 struct Workspace {
   void *ptr = nullptr;
   size_t bytes = 0;
@@ -155,12 +165,9 @@ struct Problem {
   uint32_t *rp_ent = nullptr;    // [n_pad*es] blocks (pos | a<<27 | b<<29) grouped by slot
   uint8_t *rp_soff = nullptr;    // [n_pad*ss] entry offsets of the off-diagonal slots
   uint8_t *rp_sbc = nullptr;     // [n_pad*ss] Dirichlet bits of each slot's node
-  // fused node-tile assembly (fem_rowtile.cu): packed per-tile metadata blocks
-  int rt_state = 0;              // 0 not built, 1 built, -1 not eligible
-  uint8_t *rt_meta = nullptr;
-  int64_t rt_ntiles = 0;
-  int rt_layout[14] = {0};       // RtLayout fields
-  int rt_smem = 0;
+  // fused node-tile assembly (fem_rowtile.cu): packed per-tile metadata blocks of the row
+  // form (rt) and of the colored form on node-color tiles (ct)
+  RtPlan rt, ct;
   // coloring
   bool have_colors = false;
   int32_t n_colors = -1;
@@ -283,6 +290,8 @@ fem_status launch_rows_pull(Problem *p, const double *ctx, double *vals, bool bc
 fem_status build_row_tiles(Problem *p, cudaStream_t s);                  // fem_rowtile.cu
 fem_status run_linearize(Problem *p, const double *z, cudaStream_t s);   // fem_core.cu
 fem_status launch_row_tiles(Problem *p, const double *z, double *vals, bool bc, cudaStream_t s);
+fem_status build_colored_tiles(Problem *p, cudaStream_t s);              // fem_rowtile.cu
+fem_status launch_colored_tiles(Problem *p, const double *z, double *vals, bool bc, cudaStream_t s);
 fem_status dist_setup(Problem *p, const fem_dist_desc *d, cudaStream_t s);
 void dist_free(Problem *p);
 fem_status allreduce(Problem *p, double *buf, int n, cudaStream_t s);

@@ -81,6 +81,9 @@
 // pattern shared by all its node-steps), ncu shows 4.74 vs 4.82 per load, and the padded
 // record slots make the kernel slower (3.63 vs 3.54 ms) — off by default.  A micro-benchmark
 // (tools/micro/lds64.cu) confirms the model: 64-bit loads are served per half-warp.
+#ifndef FEM_CT_NT
+#define FEM_CT_NT 4    // max seeds per colored node tile (FEM_ASSEMBLE_COLORED; A/B cfg 3: 2 / 4 / 6 / 8 / 16 -> 12.8 / 8.24 / 8.30 / 8.85 / 9.18 ms)
+#endif
 #ifndef FEM_RT_PLACE
 #define FEM_RT_PLACE 0
 #endif
@@ -122,11 +125,13 @@ __host__ __device__ constexpr int rt_pair(int a, int b) {
 struct RtLayout {
   int nt, lpn, uem, unm, es, ss, mb;
   int off_halo, off_lc, off_ph, off_nd, off_so, off_sb, off_en;
+  int off_tb, off_tsn;  // TR (colored Alg. 2): per (node, slot) transposed block base, neighbour row length
 };
 
 static inline int r16(int x) { return (x + 15) & ~15; }
 
-static RtLayout rt_layout(int nt, int lpn, int uem, int unm, int es, int ss, bool phase) {
+static RtLayout rt_layout(int nt, int lpn, int uem, int unm, int es, int ss, bool phase,
+                          bool tr = false) {
   RtLayout L{};
   L.nt = nt; L.lpn = lpn; L.uem = uem; L.unm = unm; L.es = es; L.ss = ss;
   L.off_halo = 16;
@@ -136,7 +141,9 @@ static RtLayout rt_layout(int nt, int lpn, int uem, int unm, int es, int ss, boo
   L.off_so = r16(L.off_nd + 16 * nt);
   L.off_sb = r16(L.off_so + 2 * nt * ss);   // slot offsets: uint16
   L.off_en = r16(L.off_sb + nt * ss);
-  L.mb = r16(L.off_en + 2 * nt * es);
+  L.off_tb = r16(L.off_en + 2 * nt * es);
+  L.off_tsn = L.off_tb + (tr ? 8 * nt * ss : 0);
+  L.mb = r16(L.off_tsn + (tr ? nt * ss : 0));
   return L;
 }
 
@@ -302,6 +309,22 @@ __global__ void __launch_bounds__(256) k_rt_plan(const int32_t *node_order, int6
     for (int q = 0; q < sno; ++q) c[q + 1] += c[q];
     for (int q = 0; q <= sno; ++q) so[j * L.ss + q] = c[q];
     for (int q = 0; q < sno; ++q) sb[j * L.ss + q] = node_bc ? node_bc[nadj[a0 + q + (q >= ds)]] : 0;
+    if (L.off_tsn > L.off_tb) {  // TR: where K[m, n] (the transpose of slot q's block) lives
+      int64_t *tb = reinterpret_cast<int64_t *>(blk + L.off_tb);
+      uint8_t *tsn = blk + L.off_tsn;
+      for (int q = 0; q < sno; ++q) {
+        const int32_t mm = nadj[a0 + q + (q >= ds)];
+        const int64_t b0 = nadj_ptr[mm];
+        const int snm = (int)(nadj_ptr[mm + 1] - b0);
+        int lo = 0, hi = snm;
+        while (lo < hi) {
+          const int mid = (lo + hi) >> 1;
+          if (nadj[b0 + mid] < n) lo = mid + 1; else hi = mid;
+        }
+        tb[j * L.ss + q] = row_ptr[(int64_t)mm * D] + (int64_t)lo * D;  // row (m, 0), column block n
+        tsn[j * L.ss + q] = (uint8_t)snm;
+      }
+    }
     uint16_t *ej = en + j * L.es;
     for (int q = 0; q < L.es; ++q) ej[q] = 0;
     const unsigned bcn = node_bc ? node_bc[n] : 0u;
@@ -522,12 +545,11 @@ __global__ void __launch_bounds__(256) k_rt_plan(const int32_t *node_order, int6
   }
 }
 
-fem_status build_row_tiles(Problem *p, cudaStream_t s) {
-  if (p->rt_state) return FEM_OK;
-  p->rt_state = -1;
-  if (p->n_nodes == 0 || p->n_elems == 0 || getenv("FEM_ROWS_PULL")) return FEM_OK;
-  fem_status st = morton_node_order(p, s);
-  if (st) return st;
+// Node-tile plan over segments of a node list (the row form: one segment, the Morton order;
+// the colored form, TR: one segment per node color, seeds in Morton order).  Tiles never
+// straddle segments; segment g's tiles start at tile seg_tiles[g].
+static fem_status build_tile_plan(Problem *p, const int32_t *order, const std::vector<int64_t> &seg,
+                                  bool tr, RtPlan &out, cudaStream_t s) {
   const int D = p->dim, NEN = D + 1;
   const int64_t n = p->n_nodes;
   // max degree -> entry stride; max off-diagonal slots -> lanes per node
@@ -549,21 +571,42 @@ fem_status build_row_tiles(Problem *p, cudaStream_t s) {
   const int LPN = force32 ? 32
                   : (D == 2 && SN - 1 <= 8 && !getenv("FEM_RT_LPN16")) ? 8
                   : (SN - 1 <= 16) ? 16 : 32;
-  const int NT = LPN == 8 ? 32 : LPN == 16 ? kRtNT : 8;
-  const int64_t nt = (n + NT - 1) / NT;
+  int NT = LPN == 8 ? 32 : LPN == 16 ? kRtNT : 8;
+  // colored tiles: seeds of one color share no element, so a tile's element set is the union
+  // of its seeds' stars (~24 per seed in 3D) — fewer seeds per tile keep the records small
+  if (tr && FEM_CT_NT > 0) NT = std::min(NT, FEM_CT_NT);
+  const int ng = (int)seg.size() - 1;
+  out.seg_tiles.assign(ng + 1, 0);
+  for (int g = 0; g < ng; ++g) out.seg_tiles[g + 1] = out.seg_tiles[g] + (seg[g + 1] - seg[g] + NT - 1) / NT;
+  const int64_t nt = out.seg_tiles[ng];
   const int MS = std::max(LPN, SN - 1);  // slots per node the layout holds
   const int ES = std::max((((NEN - 1) * IS) + 7) & ~7, FEM_RT_SCHED ? MS * (D == 3 ? 7 : 5) : 0),
             SS = (MS + 1 + 3) & ~3;
-  if (IS == 0 || ES > 65535) return FEM_OK;
+  if (IS == 0 || ES > 65535 || nt == 0) return FEM_OK;
   int *d_bad = nullptr;
   int32_t *cnt = nullptr;
   FEM_CUDA(cudaMalloc(&d_bad, sizeof(int)));
   FEM_CUDA(cudaMalloc(&cnt, sizeof(int32_t) * 2 * nt));
   FEM_CUDA(cudaMemsetAsync(d_bad, 0, sizeof(int), s));
-  RtLayout L0 = rt_layout(NT, LPN, 8, 8, ES, SS, p->phase != nullptr);
-  if (D == 2) k_rt_plan<2><<<(unsigned)nt, 256, 0, s>>>(p->node_order, n, p->inc_ptr, p->inc, p->conn, p->phase, p->nadj_ptr, p->nadj, p->row_ptr, p->node_bc, L0, cnt, nullptr, d_bad);
-  else k_rt_plan<3><<<(unsigned)nt, 256, 0, s>>>(p->node_order, n, p->inc_ptr, p->inc, p->conn, p->phase, p->nadj_ptr, p->nadj, p->row_ptr, p->node_bc, L0, cnt, nullptr, d_bad);
-  FEM_LAUNCH_CHECK("row tiles (count)");
+  const bool dbg = getenv("FEM_RT_PLACE_DEBUG") != nullptr;
+  auto plan = [&](const RtLayout &L, uint8_t *meta) -> fem_status {  // count (meta null) / fill
+    for (int g = 0; g < ng; ++g) {
+      const int64_t tiles = out.seg_tiles[g + 1] - out.seg_tiles[g];
+      if (!tiles) continue;
+      const int32_t *ord = order + seg[g];
+      const int64_t cnt_n = seg[g + 1] - seg[g];
+      int32_t *c = cnt + 2 * out.seg_tiles[g];
+      uint8_t *m = meta ? meta + out.seg_tiles[g] * (int64_t)L.mb : nullptr;
+      int32_t *cc = (meta && !dbg) ? nullptr : c;
+      if (D == 2) k_rt_plan<2><<<(unsigned)tiles, 256, 0, s>>>(ord, cnt_n, p->inc_ptr, p->inc, p->conn, p->phase, p->nadj_ptr, p->nadj, p->row_ptr, p->node_bc, L, cc, m, d_bad);
+      else k_rt_plan<3><<<(unsigned)tiles, 256, 0, s>>>(ord, cnt_n, p->inc_ptr, p->inc, p->conn, p->phase, p->nadj_ptr, p->nadj, p->row_ptr, p->node_bc, L, cc, m, d_bad);
+      FEM_LAUNCH_CHECK("node-tile plan");
+    }
+    return FEM_OK;
+  };
+  RtLayout L0 = rt_layout(NT, LPN, 8, 8, ES, SS, p->phase != nullptr, tr);
+  fem_status st = plan(L0, nullptr);
+  if (st) return st;
   std::vector<int32_t> hc(2 * nt);
   int hbad = 0;
   FEM_CUDA(cudaMemcpyAsync(hc.data(), cnt, sizeof(int32_t) * 2 * nt, cudaMemcpyDeviceToHost, s));
@@ -576,7 +619,7 @@ fem_status build_row_tiles(Problem *p, cudaStream_t s) {
   }
   uem = (uem + 7) & ~7;
   unm = (unm + 7) & ~7;
-  const RtLayout L = rt_layout(NT, LPN, uem, unm, ES, SS, p->phase != nullptr);
+  const RtLayout L = rt_layout(NT, LPN, uem, unm, ES, SS, p->phase != nullptr, tr);
   // shared memory of the assembly kernel: 3 metadata blocks, 2 node-data buffers, records
   const int RS = D == 3 ? RtGeom<3>::RS : RtGeom<2>::RS;
   const int BP = D == 3 ? RtGeom<3>::BP : RtGeom<2>::BP;
@@ -587,10 +630,10 @@ fem_status build_row_tiles(Problem *p, cudaStream_t s) {
     cudaFree(d_bad); cudaFree(cnt);
     return FEM_OK;
   }
-  FEM_CUDA(cudaMalloc(&p->rt_meta, (size_t)L.mb * nt));
-  if (D == 2) k_rt_plan<2><<<(unsigned)nt, 256, 0, s>>>(p->node_order, n, p->inc_ptr, p->inc, p->conn, p->phase, p->nadj_ptr, p->nadj, p->row_ptr, p->node_bc, L, cnt, p->rt_meta, d_bad);
-  else k_rt_plan<3><<<(unsigned)nt, 256, 0, s>>>(p->node_order, n, p->inc_ptr, p->inc, p->conn, p->phase, p->nadj_ptr, p->nadj, p->row_ptr, p->node_bc, L, getenv("FEM_RT_PLACE_DEBUG") ? cnt : nullptr, p->rt_meta, d_bad);
-  if (getenv("FEM_RT_PLACE_DEBUG")) {
+  FEM_CUDA(cudaMalloc(&out.meta, (size_t)L.mb * nt));
+  st = plan(L, out.meta);
+  if (st) return st;
+  if (dbg) {
     std::vector<int32_t> hd(2 * nt);
     FEM_CUDA(cudaMemcpyAsync(hd.data(), cnt, sizeof(int32_t) * 2 * nt, cudaMemcpyDeviceToHost, s));
     FEM_CUDA(cudaStreamSynchronize(s));
@@ -598,26 +641,41 @@ fem_status build_row_tiles(Problem *p, cudaStream_t s) {
     for (int64_t q = 0; q < nt; ++q) { a0 += hd[2 * q]; a1 += hd[2 * q + 1]; }
     fprintf(stderr, "[rt place] modelled g_b wavefronts per half-warp step: identity %lld, placed %lld\n", a0, a1);
   }
-  FEM_LAUNCH_CHECK("row tiles (fill)");
   FEM_CUDA(cudaMemcpyAsync(&hbad, d_bad, sizeof(int), cudaMemcpyDeviceToHost, s));
   FEM_CUDA(cudaStreamSynchronize(s));
   cudaFree(d_bad);
   cudaFree(cnt);
   if (hbad) {
-    cudaFree(p->rt_meta);
-    p->rt_meta = nullptr;
+    cudaFree(out.meta);
+    out.meta = nullptr;
     return FEM_OK;
   }
-  p->rt_ntiles = nt;
-  p->rt_layout[0] = L.nt; p->rt_layout[1] = L.uem; p->rt_layout[2] = L.unm;
-  p->rt_layout[3] = L.es; p->rt_layout[4] = L.ss; p->rt_layout[5] = L.mb;
-  p->rt_layout[6] = L.off_halo; p->rt_layout[7] = L.off_lc; p->rt_layout[8] = L.off_ph;
-  p->rt_layout[9] = L.off_nd; p->rt_layout[10] = L.off_so; p->rt_layout[11] = L.off_sb;
-  p->rt_layout[12] = L.off_en;
-  p->rt_layout[13] = L.lpn;
-  p->rt_smem = (int)smem;
-  p->rt_state = 1;
+  out.ntiles = nt;
+  int *l = out.layout;
+  l[0] = L.nt; l[1] = L.uem; l[2] = L.unm; l[3] = L.es; l[4] = L.ss; l[5] = L.mb;
+  l[6] = L.off_halo; l[7] = L.off_lc; l[8] = L.off_ph; l[9] = L.off_nd; l[10] = L.off_so;
+  l[11] = L.off_sb; l[12] = L.off_en; l[13] = L.lpn; l[14] = L.off_tb; l[15] = L.off_tsn;
+  out.smem = (int)smem;
+  out.state = 1;
   return FEM_OK;
+}
+
+fem_status build_row_tiles(Problem *p, cudaStream_t s) {
+  if (p->rt.state) return FEM_OK;
+  p->rt.state = -1;
+  if (p->n_nodes == 0 || p->n_elems == 0 || getenv("FEM_ROWS_PULL")) return FEM_OK;
+  fem_status st = morton_node_order(p, s);
+  if (st) return st;
+  return build_tile_plan(p, p->node_order, {0, p->n_nodes}, false, p->rt, s);
+}
+
+// fused colored Alg. 2 on node tiles: one segment per node color (p->ncolor_list / ncolor_off)
+fem_status build_colored_tiles(Problem *p, cudaStream_t s) {
+  if (p->ct.state) return FEM_OK;
+  p->ct.state = -1;
+  if (p->n_nodes == 0 || p->n_elems == 0 || p->n_mpc || !p->ncolor_list || getenv("FEM_ROWS_PULL"))
+    return FEM_OK;
+  return build_tile_plan(p, p->ncolor_list, p->ncolor_off, true, p->ct, s);
 }
 
 // ------------------------------------------------------------------ kernel
@@ -644,7 +702,10 @@ struct RtArgs {
   int *err;
 };
 
-template <int D, int MAT, int LPN>
+// TR: fused colored Alg. 2 (FEM_ASSEMBLE_COLORED, reading R13) on node tiles of one node color:
+// each seed's column blocks K[m, n] = K[n, m]^T are written at their decompressed CSR slots
+// (row m D + k, column n D + i), conflict-free within a color; the diagonal block as the row form.
+template <int D, int MAT, int LPN, bool TR = false>
 __global__ void __launch_bounds__(kRtThreads, FEM_RT_MINB) k_rows_tile(RtArgs A) {
   using Gm = RtGeom<D>;
   constexpr int NEN = Gm::NEN, BS = Gm::BS, RS = Gm::RS;
@@ -853,7 +914,23 @@ __global__ void __launch_bounds__(kRtThreads, FEM_RT_MINB) k_rows_tile(RtArgs A)
           }
         }
       }
-      if (live && q < sno) {
+      if (TR && live && q < sno) {  // K[m D + k, n D + i] = K[n D + i, m D + k]
+        const unsigned sbc = A.bc ? m[L.off_sb + j * L.ss + q] : 0u;
+        const int64_t tb = reinterpret_cast<const int64_t *>(m + L.off_tb)[j * L.ss + q];
+        const int snm = m[L.off_tsn + j * L.ss + q];
+#pragma unroll
+        for (int kk = 0; kk < D; ++kk) {
+          double *row = A.vals + tb + (int64_t)kk * D * snm;
+#pragma unroll
+          for (int i = 0; i < D; ++i) {
+            double v = acc[i * D + kk];
+            if ((sbc >> kk) & 1u) v = 0.0;   // identity row (m, kk), off-diagonal
+            if ((bcn >> i) & 1u) v = 0.0;    // masked column (n, i)
+            row[i] = v;
+          }
+        }
+      }
+      if (!TR && live && q < sno) {
         const unsigned sbc = A.bc ? m[L.off_sb + j * L.ss + q] : 0u;
         const int s = q + (q >= ds);
         double *row = A.vals + rp0 + s * D;
@@ -920,35 +997,52 @@ __global__ void __launch_bounds__(kRtThreads, FEM_RT_MINB) k_rows_tile(RtArgs A)
   }
 }
 
-fem_status launch_row_tiles(Problem *p, const double *z, double *vals, bool bc, cudaStream_t s) {
+template <bool TR>
+static fem_status launch_plan(Problem *p, const RtPlan &P, int64_t t0, int64_t tiles, const double *z,
+                              double *vals, bool bc, cudaStream_t s) {
   RtArgs A{};
-  const int *lay = p->rt_layout;
+  const int *lay = P.layout;
   A.L.nt = lay[0]; A.L.uem = lay[1]; A.L.unm = lay[2]; A.L.es = lay[3]; A.L.ss = lay[4];
   A.L.mb = lay[5]; A.L.off_halo = lay[6]; A.L.off_lc = lay[7]; A.L.off_ph = lay[8];
   A.L.off_nd = lay[9]; A.L.off_so = lay[10]; A.L.off_sb = lay[11]; A.L.off_en = lay[12];
-  A.L.lpn = lay[13];
-  A.meta = p->rt_meta; A.n_tiles = p->rt_ntiles; A.coords = p->coords; A.z = z;
+  A.L.lpn = lay[13]; A.L.off_tb = lay[14]; A.L.off_tsn = lay[15];
+  A.meta = P.meta + t0 * (int64_t)A.L.mb; A.n_tiles = tiles; A.coords = p->coords; A.z = z;
   A.lam = p->lam; A.mu = p->mu; A.lam_tab = p->lam_tab; A.mu_tab = p->mu_tab;
   A.has_phase = p->phase != nullptr; A.bc = bc ? 1 : 0; A.vals = vals; A.err = p->d_err;
   void (*kern)(RtArgs);
   const bool le = p->material == FEM_LINEAR_ELASTIC;
   const int lpn = A.L.lpn;
   if (p->dim == 2)
-    kern = le ? (lpn == 8 ? k_rows_tile<2, FEM_LINEAR_ELASTIC, 8> : lpn == 16 ? k_rows_tile<2, FEM_LINEAR_ELASTIC, 16> : k_rows_tile<2, FEM_LINEAR_ELASTIC, 32>)
-              : (lpn == 8 ? k_rows_tile<2, FEM_NEO_HOOKEAN, 8> : lpn == 16 ? k_rows_tile<2, FEM_NEO_HOOKEAN, 16> : k_rows_tile<2, FEM_NEO_HOOKEAN, 32>);
+    kern = le ? (lpn == 8 ? k_rows_tile<2, FEM_LINEAR_ELASTIC, 8, TR> : lpn == 16 ? k_rows_tile<2, FEM_LINEAR_ELASTIC, 16, TR> : k_rows_tile<2, FEM_LINEAR_ELASTIC, 32, TR>)
+              : (lpn == 8 ? k_rows_tile<2, FEM_NEO_HOOKEAN, 8, TR> : lpn == 16 ? k_rows_tile<2, FEM_NEO_HOOKEAN, 16, TR> : k_rows_tile<2, FEM_NEO_HOOKEAN, 32, TR>);
   else
-    kern = le ? (lpn == 16 ? k_rows_tile<3, FEM_LINEAR_ELASTIC, 16> : k_rows_tile<3, FEM_LINEAR_ELASTIC, 32>)
-              : (lpn == 16 ? k_rows_tile<3, FEM_NEO_HOOKEAN, 16> : k_rows_tile<3, FEM_NEO_HOOKEAN, 32>);
-  FEM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, p->rt_smem));
+    kern = le ? (lpn == 16 ? k_rows_tile<3, FEM_LINEAR_ELASTIC, 16, TR> : k_rows_tile<3, FEM_LINEAR_ELASTIC, 32, TR>)
+              : (lpn == 16 ? k_rows_tile<3, FEM_NEO_HOOKEAN, 16, TR> : k_rows_tile<3, FEM_NEO_HOOKEAN, 32, TR>);
+  FEM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, P.smem));
   int per_sm = 0;
-  FEM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kRtThreads, p->rt_smem));
+  FEM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kRtThreads, P.smem));
   int dev = 0, sms = 148;
   FEM_CUDA(cudaGetDevice(&dev));
   FEM_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   int64_t grid = (int64_t)sms * (per_sm > 0 ? per_sm : 1);
-  if (grid > p->rt_ntiles) grid = p->rt_ntiles;
-  kern<<<(int)grid, kRtThreads, p->rt_smem, s>>>(A);
+  if (grid > tiles) grid = tiles;
+  kern<<<(int)grid, kRtThreads, P.smem, s>>>(A);
   FEM_LAUNCH_CHECK("node-tile assembly");
+  return FEM_OK;
+}
+
+fem_status launch_row_tiles(Problem *p, const double *z, double *vals, bool bc, cudaStream_t s) {
+  return launch_plan<false>(p, p->rt, 0, p->rt.ntiles, z, vals, bc, s);
+}
+
+// one launch per node color (tiles of one color write disjoint slots)
+fem_status launch_colored_tiles(Problem *p, const double *z, double *vals, bool bc, cudaStream_t s) {
+  for (size_t g = 0; g + 1 < p->ct.seg_tiles.size(); ++g) {
+    const int64_t tiles = p->ct.seg_tiles[g + 1] - p->ct.seg_tiles[g];
+    if (!tiles) continue;
+    fem_status st = launch_plan<true>(p, p->ct, p->ct.seg_tiles[g], tiles, z, vals, bc, s);
+    if (st) return st;
+  }
   return FEM_OK;
 }
 

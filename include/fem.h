@@ -218,13 +218,16 @@ fem_status fem_color(fem_problem *p, int32_t *colors, int32_t *n_colors, fem_str
  *   FEM_ASSEMBLE_COLORED: C/D node-color passes; every seed node's D columns K e_j are
  *            gathered from its incident elements and stored at their decompressed slots
  *            (Alg. 2 fused: compress and decompress in one step, no J_comp; the columns of
- *            one color never share a slot, so no atomics);
+ *            one color never share a slot, so no atomics).  Each pass runs node tiles of 4
+ *            seeds of the color with their element contexts in shared memory (fallback for
+ *            meshes the tile plan rejects: a warp per seed over HBM context records);
  *   FEM_ASSEMBLE_ROWS: NOT Alg. 2: the row-owner gather form of the element-Hessian
  *            assembly (the sum of element Hessians, which
  *            Alg. 2 reproduces exactly).  Each node's D rows sum the tangent blocks
  *            K^e_nm of its incident elements and store them at the row's CSR slots; it reads
  *            neither the coloring nor a J_comp buffer, is atomic-free and bitwise
- *            reproducible.  Node tiles of 16 Morton-ordered nodes evaluate their elements'
+ *            reproducible.  Node tiles of 16 Morton-ordered nodes (8 when a node has more
+ *            than 16 off-diagonal slots: unstructured meshes) evaluate their elements'
  *            tangent contexts in shared memory (no context records in HBM); the diagonal
  *            block is minus the row's off-diagonal sum (element rows sum to zero);
  *   FEM_ASSEMBLE_SCATTER: not Alg. 2 but the assembly the paper compares it with (Fig. 4

@@ -20,7 +20,7 @@ for i in 0 1 2 3 4; do
 done
 mkdir -p /tmp/ncu_keep && mv gpurun_out/${T}_prof_full.ncu-rep /tmp/ncu_keep/   # > 64 MiB with the rest
 timeout 1200 ncu --set full --clock-control none --import-source on --profile-from-start off \
-   -k regex:"k_tile_pipe|k_rows_fused|k_elem_ctx" -c 12 -o gpurun_out/${T}_prof_var -f \
+   -k regex:"k_tile_pipe|k_rows_fused|k_elem_ctx|k_rows_tile" -c 12 -o gpurun_out/${T}_prof_var -f \
    python tools/profile_variants.py --variants hvp,hvp_lin,hvp_s,res,res_s,assemble_col > gpurun_out/${T}_ncu_var.log 2>&1
 ncu -i gpurun_out/${T}_prof_var.ncu-rep --page raw --csv > gpurun_out/${T}_prof_var_raw.csv 2>/dev/null
 mv gpurun_out/${T}_prof_var.ncu-rep /tmp/ncu_keep/

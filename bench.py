@@ -709,6 +709,16 @@ def main():
             solve["newton_csr_s"] = time.perf_counter() - t0
             solve["newton_csr"] = {k: infoc[k] for k in ("iters", "cg_iters", "converged", "res0", "res")}
             solve["newton_csr_vs_hvp_maxdiff"] = float((zc - zs).abs().max())
+            # inexact Newton-Krylov (Eisenstat-Walker forcing, reading R16): same outer target
+            for key, op, jac in (("newton_ew", 0, False), ("newton_csr_ew", 1, True)):
+                t0 = time.perf_counter()
+                ze, infoe = prob.newton_solve(z0, op=op, jacobi=jac, cg_rtol=1e-8, rtol=1e-10,
+                                              atol=1e-14, check_every=16, raise_on_fail=False,
+                                              forcing=0.9)
+                torch.cuda.synchronize()
+                solve[key + "_s"] = time.perf_counter() - t0
+                solve[key] = {k: infoe[k] for k in ("iters", "cg_iters", "converged", "res0", "res")}
+                solve[key + "_vs_fixed_maxdiff"] = float((ze - zs).abs().max())
 
     cpu = None
     if not args.no_cpu_baseline and rank == 0 and world == 1:

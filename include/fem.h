@@ -312,6 +312,15 @@ typedef struct {
   double atol, rtol; /* outer: ||r|| <= max(atol, rtol ||r0||)                 */
   int max_iter;
   fem_cg_opts cg;    /* inner solve; cg.op 0 = Newton-Krylov, 1 = colored CSR      */
+  double forcing;    /* inner tolerance of Newton step k (DESIGN reading R16):
+                      *   0: eta_k = cg.rtol at every step (fixed; the default);
+                      *   > 0: inexact Newton-Krylov with Eisenstat-Walker "choice 2" forcing
+                      *   terms, gamma = forcing (in (0, 1]; 0.9 typical), alpha = 2:
+                      *   eta_0 = 0.1, eta_k = min(0.1, gamma (||r_k|| / ||r_{k-1}||)^2),
+                      *   safeguarded by gamma eta_{k-1}^2 when that exceeds 0.1, never
+                      *   below cg.rtol, and at least 0.5 tau / ||r_k|| (tau = the outer
+                      *   target) so the last step does not over-solve.  The converged z
+                      *   satisfies the same outer test.  forcing > 1 or < 0: INVALID_ARG. */
 } fem_newton_opts;
 
 typedef struct {

@@ -102,7 +102,7 @@ struct RtPlan {
   int state = 0;                 // 0 not built, 1 built, -1 not eligible
   uint8_t *meta = nullptr;
   int64_t ntiles = 0;
-  int layout[16] = {0};          // RtLayout fields
+  int layout[20] = {0};          // RtLayout fields
   int smem = 0;
   std::vector<int64_t> seg_tiles;  // first tile of each node-list segment (colors for ct)
 };

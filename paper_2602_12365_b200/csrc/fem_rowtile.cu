@@ -87,6 +87,24 @@
 #ifndef FEM_RT_PLACE
 #define FEM_RT_PLACE 0
 #endif
+// Bank-conflict-free context records (3D, 16 lanes per node, row form): the records are
+// stored field-major (SoA) with a stride S = kRtSoaS = 4 (mod 16) words, so a 64-bit load
+// of field w of record r hits bank pair (4 w + r) mod 16: records of different r mod 4 (the
+// record's "color") never collide, g_b[i] of one record (field 3 b + i) covers four distinct
+// bank pairs over b, and M_ab sits at field 11 + (a ^ b) + 4 [0 not in {a, b}] (the three
+// pairs at a vertex have distinct a ^ b, i.e. K4's three perfect matchings).  The plan colors
+// each tile's elements with 4 colors (balanced per tile node), places element k of color c at
+// record 4 k + c, and co-schedules each node's slot runs so that the elements read at one step
+// have distinct colors: every load of the slot sums is then one wavefront per half-warp
+// (ncu r02: 4.8 wavefronts per warp-wide load against 2, LSU 73 % busy).  Idle steps are
+// entry 0xffff (no load).  0 = the odd-stride record layout (FEM_RT_RSODD).
+#ifndef FEM_RT_SOA
+#define FEM_RT_SOA 0
+#endif
+// visit budget of the plan's depth-first co-schedule search per node and length (0: first fit)
+#ifndef FEM_RT_SOA_DFS
+#define FEM_RT_SOA_DFS 4000
+#endif
 // co-scheduled block lists (see k_rt_plan): 0 = each slot's run in ascending element order
 #ifndef FEM_RT_SCHED
 #define FEM_RT_SCHED 1
@@ -105,6 +123,11 @@ constexpr int kRtLPNMax = 32;            // lanes per node: 8 (2D, <= 8 off-diag
                                          // <= 16) or 32 (unstructured, 8-node tiles)
 constexpr int kRtMaxSlots = 64;          // off-diagonal slots per node: a lane sums slots ql, ql + LPN, ...
 constexpr int kRtSortMax = 4096;         // plan: keys sorted per tile in shared memory
+constexpr int kRtSchedHist = 17;         // plan statistics: bad[1 + C] nodes with schedule length C, bad[1 + 17] grouped
+constexpr int kRtSoaS = 324;             // SoA record stride (= 4 mod 16; records per tile <= 324)
+constexpr int kRtSoaF = 20;              // SoA fields: g 0-11, M 12-14 / 16-18, sc1 15, sc2 19
+static_assert(kRtSoaS % 16 == 4, "SoA stride must be 4 mod 16");
+__host__ __device__ constexpr int rt_soa_m(int a, int b) { return 11 + (a ^ b) + ((a && b) ? 4 : 0); }
 
 template <int D>
 struct RtGeom {
@@ -124,6 +147,7 @@ __host__ __device__ constexpr int rt_pair(int a, int b) {
 
 struct RtLayout {
   int nt, lpn, uem, unm, es, ss, mb;
+  int soa;  // 1: SoA records (FEM_RT_SOA), uem = kRtSoaS
   int off_halo, off_lc, off_ph, off_nd, off_so, off_sb, off_en;
   int off_tb, off_tsn;  // TR (colored Alg. 2): per (node, slot) transposed block base, neighbour row length
 };
@@ -131,9 +155,9 @@ struct RtLayout {
 static inline int r16(int x) { return (x + 15) & ~15; }
 
 static RtLayout rt_layout(int nt, int lpn, int uem, int unm, int es, int ss, bool phase,
-                          bool tr = false) {
+                          bool tr = false, bool soa = false) {
   RtLayout L{};
-  L.nt = nt; L.lpn = lpn; L.uem = uem; L.unm = unm; L.es = es; L.ss = ss;
+  L.nt = nt; L.lpn = lpn; L.uem = uem; L.unm = unm; L.es = es; L.ss = ss; L.soa = soa ? 1 : 0;
   L.off_halo = 16;
   L.off_lc = r16(L.off_halo + 4 * unm);
   L.off_ph = r16(L.off_lc + 8 * uem);
@@ -233,9 +257,60 @@ __global__ void __launch_bounds__(256) k_rt_plan(const int32_t *node_order, int6
   if (tid == 0) s_un = rt_unique(halo, ue * NEN);
   __syncthreads();
   const int un = s_un;
+  // SoA records (FEM_RT_SOA): 4-coloring of the tile's elements, balanced per tile node;
+  // element k of color c at record 4 k + c (s_soa[0]: record of each element, s_soa[1]:
+  // element of each record or 0xffff, s_soa[2]: tile-node mask of each element)
+  __shared__ uint16_t s_soa[3][1024];
+  __shared__ int s_nslot;
+  const bool soa = L.soa != 0;
+  if (soa) {
+    if (ue > 1024) {
+      if (tid == 0) atomicOr(bad, 1);
+      return;
+    }
+    for (int e = tid; e < ue; e += nthr) {
+      unsigned mk = 0;
+      for (int a = 0; a < NEN; ++a) {
+        const int32_t nd = conn[(int64_t)elems[e] * NEN + a];
+        for (int j = 0; j < nn; ++j)
+          if (node_order[n0 + j] == nd) mk |= 1u << j;
+      }
+      s_soa[2][e] = (uint16_t)mk;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      uint8_t cn[16][4];
+      int csz[4] = {0, 0, 0, 0};
+      for (int j = 0; j < 16; ++j)
+        for (int c = 0; c < 4; ++c) cn[j][c] = 0;
+      for (int e = 0; e < ue; ++e) {
+        const unsigned mk = s_soa[2][e];
+        int bc = 0, bmax = 1 << 30, bsum = 1 << 30, bsz = 1 << 30;
+        for (int c = 0; c < 4; ++c) {
+          int mx = 0, sm = 0;
+          for (int j = 0; j < 16; ++j)
+            if (mk >> j & 1u) { mx = max(mx, cn[j][c] + 1); sm += cn[j][c]; }
+          if (mx < bmax || (mx == bmax && (sm < bsum || (sm == bsum && csz[c] < bsz)))) {
+            bc = c; bmax = mx; bsum = sm; bsz = csz[c];
+          }
+        }
+        for (int j = 0; j < 16; ++j)
+          if (mk >> j & 1u) ++cn[j][bc];
+        s_soa[0][e] = (uint16_t)(4 * csz[bc] + bc);
+        ++csz[bc];
+      }
+      const int ns = 4 * max(max(csz[0], csz[1]), max(csz[2], csz[3]));
+      s_nslot = ns;
+      for (int q = 0; q < ns && q < 1024; ++q) s_soa[1][q] = 0xffff;
+      for (int e = 0; e < ue; ++e)
+        if (s_soa[0][e] < 1024) s_soa[1][s_soa[0][e]] = (uint16_t)e;
+    }
+    __syncthreads();
+  }
   // bank-aware placement: records in 16 bank classes of ceil(ue / 16) slots each
-  const bool place = FEM_RT_PLACE && FEM_RT_SCHED && L.lpn == 16;
-  const int nslot = place ? (ue + 15) & ~15 : ue;
+  const bool place = !soa && FEM_RT_PLACE && FEM_RT_SCHED && L.lpn == 16;
+  const int nslot = soa ? s_nslot : place ? (ue + 15) & ~15 : ue;
+  auto rec_of = [&](int r) -> int { return soa ? (int)s_soa[0][r] : r; };  // sorted index -> record
   if (!meta) {
     if (tid == 0) { cnt[2 * t] = nslot; cnt[2 * t + 1] = un; }
     return;
@@ -245,20 +320,28 @@ __global__ void __launch_bounds__(256) k_rt_plan(const int32_t *node_order, int6
   uint8_t *blk = meta + t * (int64_t)L.mb;
   if (tid == 0) {
     int *h = reinterpret_cast<int *>(blk);
-    h[0] = ue; h[1] = un; h[2] = nn; h[3] = 0;
+    h[0] = soa ? nslot : ue; h[1] = un; h[2] = nn; h[3] = 0;
   }
   int32_t *hid = reinterpret_cast<int32_t *>(blk + L.off_halo);
   for (int q = tid; q < L.unm; q += nthr) hid[q] = q < un ? halo[q] : 0;
   uint16_t *lc = reinterpret_cast<uint16_t *>(blk + L.off_lc);
   for (int q = tid; q < L.uem * 4; q += nthr) {
-    const int e = q / 4, a = q % 4;
+    int e = q / 4;
+    const int a = q % 4;
     uint16_t v = 0;
+    if (soa) {  // records in slot order; holes marked lc.x = 0xffff
+      e = e < nslot ? (int)s_soa[1][e] : 0xffff;
+      if (e == 0xffff) v = a == 0 ? 0xffff : 0;
+    }
     if (e < ue && a < NEN) v = (uint16_t)rt_find(halo, un, conn[(int64_t)elems[e] * NEN + a]);
     lc[q] = v;
   }
   if (phase) {
     uint8_t *ph = blk + L.off_ph;
-    for (int q = tid; q < L.uem; q += nthr) ph[q] = q < ue ? phase[elems[q]] : 0;
+    for (int q = tid; q < L.uem; q += nthr) {
+      const int e = soa ? (q < nslot ? (int)s_soa[1][q] : 0xffff) : q;
+      ph[q] = e < ue ? phase[elems[e]] : 0;
+    }
   }
   // per tile node: row word, off-diagonal slots, block list
   int4 *ndw = reinterpret_cast<int4 *>(blk + L.off_nd);
@@ -344,6 +427,8 @@ __global__ void __launch_bounds__(256) k_rt_plan(const int32_t *node_order, int6
     for (int q = 0; q < sno; ++q) maxrun = max(maxrun, (int)(c[q + 1] - c[q]));
     if (deg <= kSchedMaxDeg && maxrun > 0) {
       uint64_t msk[kSchedMaxDeg];
+      uint8_t col[kSchedMaxDeg];   // SoA: record color (elements of one step: distinct colors)
+      int ncol[4] = {0, 0, 0, 0};
       for (int l = 0; l < deg; ++l) {
         const int32_t pk = inc[i0 + l];
         const int64_t e = pk / NEN;
@@ -351,7 +436,11 @@ __global__ void __launch_bounds__(256) k_rt_plan(const int32_t *node_order, int6
         uint64_t mm = 0;
         for (int k = 1; k < NEN; ++k) mm |= 1ull << q_of(slot_of(conn[e * NEN + (a + k) % NEN]));
         msk[l] = mm;
+        col[l] = soa ? (uint8_t)(rec_of(rt_find(elems, ue, (int32_t)e)) & 3) : 0;
+        ++ncol[col[l]];
       }
+      // lower bound of the schedule length: the longest run; SoA: also the largest color class
+      const int lb = soa ? max(maxrun, max(max(ncol[0], ncol[1]), max(ncol[2], ncol[3]))) : maxrun;
       uint8_t perm[kSchedMaxDeg], it[kSchedMaxDeg];
       auto attempt = [&](int seed) -> int {  // returns the schedule length (kSchedMaxC + 1: failed)
         for (int l = 0; l < deg; ++l) perm[l] = (uint8_t)l;
@@ -363,33 +452,77 @@ __global__ void __launch_bounds__(256) k_rt_plan(const int32_t *node_order, int6
             const uint8_t tmp = perm[l]; perm[l] = perm[k]; perm[k] = tmp;
           }
         uint64_t busy[kSchedMaxC];
-        for (int k = 0; k < kSchedMaxC; ++k) busy[k] = 0;
+        uint8_t cbusy[kSchedMaxC];
+        for (int k = 0; k < kSchedMaxC; ++k) { busy[k] = 0; cbusy[k] = 0; }
         int C = 0;
         for (int x = 0; x < deg; ++x) {
           const int l = perm[x];
+          const uint8_t cm = soa ? (uint8_t)(1u << col[l]) : 0;
           int k = 0;
-          while (k < kSchedMaxC && (busy[k] & msk[l])) ++k;
+          while (k < kSchedMaxC && ((busy[k] & msk[l]) || (cbusy[k] & cm))) ++k;
           if (k == kSchedMaxC) return kSchedMaxC + 1;
           busy[k] |= msk[l];
+          cbusy[k] |= cm;
           it[l] = (uint8_t)k;
           C = max(C, k + 1);
         }
         return C;
       };
       int best = kSchedMaxC + 1, bseed = 0;
-      for (int seed = 0; seed < 64 && best > maxrun; ++seed) {
+      for (int seed = 0; seed < 64 && best > lb; ++seed) {
         const int C = attempt(seed);
         if (C < best) { best = C; bseed = seed; }
       }
+      // SoA: the color constraint makes first fit leave ~1.5 steps on the table (Kuhn: 7.9
+      // steps against a bound of 6); a bounded depth-first search for C = lb .. best - 1
+      // (empty steps are interchangeable: only the first one is tried) usually finds 7
+      bool dfs_ok = false;
+      if (soa && FEM_RT_SOA_DFS && best > lb) {
+        int8_t st[kSchedMaxDeg];
+        uint64_t busy[kSchedMaxC];
+        uint8_t cbusy[kSchedMaxC];
+        for (int C = lb; C < best && C <= kSchedMaxC && !dfs_ok; ++C) {
+          for (int k = 0; k < C; ++k) { busy[k] = 0; cbusy[k] = 0; }
+          int i = 0, visits = 0;
+          st[0] = -1;
+          while (i >= 0 && i < deg && visits < FEM_RT_SOA_DFS) {
+            ++visits;
+            const uint8_t cm = (uint8_t)(1u << col[i]);
+            int k = st[i];
+            if (k >= 0) {  // undo the previous placement of item i
+              busy[k] &= ~msk[i];
+              cbusy[k] &= (uint8_t)~cm;
+              if (busy[k] == 0) { st[i] = -1; --i; continue; }  // it was an empty step
+            }
+            for (++k; k < C; ++k)
+              if (!(busy[k] & msk[i]) && !(cbusy[k] & cm)) break;
+            if (k < C) {
+              busy[k] |= msk[i];
+              cbusy[k] |= cm;
+              st[i] = (int8_t)k;
+              if (++i < deg) st[i] = -1;
+            } else {
+              st[i] = -1;
+              --i;
+            }
+          }
+          if (i == deg) {
+            dfs_ok = true;
+            best = C;
+            for (int l = 0; l < deg; ++l) it[l] = (uint8_t)st[l];
+          }
+        }
+      }
       if (best <= kSchedMaxC && sno * best <= L.es) {
-        attempt(bseed);
-        const uint16_t zero = (uint16_t)(L.uem | 0 << 10 | 1 << 12);
+        if (!dfs_ok) attempt(bseed);
+        // idle steps: the zero record (AoS) or 0xffff (SoA: predicated off, no load)
+        const uint16_t zero = soa ? (uint16_t)0xffff : (uint16_t)(L.uem | 0 << 10 | 1 << 12);
         for (int q = 0; q < sno * best; ++q) ej[q] = zero;
         for (int l = 0; l < deg; ++l) {
           const int32_t pk = inc[i0 + l];
           const int64_t e = pk / NEN;
           const int a = pk % NEN;
-          const int r = rt_find(elems, ue, (int32_t)e);
+          const int r = rec_of(rt_find(elems, ue, (int32_t)e));
           for (int k = 1; k < NEN; ++k) {
             const int b = (a + k) % NEN;
             ej[q_of(slot_of(conn[e * NEN + b])) * best + it[l]] = (uint16_t)(r | a << 10 | b << 12);
@@ -397,16 +530,18 @@ __global__ void __launch_bounds__(256) k_rt_plan(const int32_t *node_order, int6
         }
         for (int q = 0; q <= sno; ++q) so[j * L.ss + q] = (uint16_t)(q * best);
         if (j < 64) s_best[j] = (uint8_t)best;
+        atomicAdd(bad + 1 + best, 1);  // schedule-length histogram (FEM_RT_SCHED_STATS)
         ndw[j] = word;
         continue;
       }
     }
 #endif
+    atomicAdd(bad + 1 + kRtSchedHist, 1);  // nodes on grouped runs (no co-schedule)
     for (int l = 0; l < deg; ++l) {
       const int32_t pk = inc[i0 + l];
       const int64_t e = pk / NEN;
       const int a = pk % NEN;
-      const int r = rt_find(elems, ue, (int32_t)e);
+      const int r = rec_of(rt_find(elems, ue, (int32_t)e));
       for (int k = 1; k < NEN; ++k) {
         const int b = (a + k) % NEN;
         ej[c[q_of(slot_of(conn[e * NEN + b]))]++] = (uint16_t)(r | a << 10 | b << 12);
@@ -585,7 +720,8 @@ static fem_status build_tile_plan(Problem *p, const int32_t *order, const std::v
   if (IS == 0 || ES > 65535 || nt == 0) return FEM_OK;
   int *d_bad = nullptr;
   int32_t *cnt = nullptr;
-  FEM_CUDA(cudaMalloc(&d_bad, sizeof(int)));
+  FEM_CUDA(cudaMalloc(&d_bad, sizeof(int) * (2 + kRtSchedHist)));
+  FEM_CUDA(cudaMemsetAsync(d_bad, 0, sizeof(int) * (2 + kRtSchedHist), s));
   FEM_CUDA(cudaMalloc(&cnt, sizeof(int32_t) * 2 * nt));
   FEM_CUDA(cudaMemsetAsync(d_bad, 0, sizeof(int), s));
   const bool dbg = getenv("FEM_RT_PLACE_DEBUG") != nullptr;
@@ -604,34 +740,44 @@ static fem_status build_tile_plan(Problem *p, const int32_t *order, const std::v
     }
     return FEM_OK;
   };
-  RtLayout L0 = rt_layout(NT, LPN, 8, 8, ES, SS, p->phase != nullptr, tr);
-  fem_status st = plan(L0, nullptr);
-  if (st) return st;
+  // SoA records (FEM_RT_SOA): 3D row form with 16 lanes per <= 16-node tile; FEM_RT_SOA_OFF=1
+  // (environment) selects the odd-stride layout at run time (A/B)
+  bool soa = FEM_RT_SOA && D == 3 && LPN == 16 && NT <= 16 && !tr && !FEM_RT_PLACE &&
+             !getenv("FEM_RT_SOA_OFF");
   std::vector<int32_t> hc(2 * nt);
-  int hbad = 0;
-  FEM_CUDA(cudaMemcpyAsync(hc.data(), cnt, sizeof(int32_t) * 2 * nt, cudaMemcpyDeviceToHost, s));
-  FEM_CUDA(cudaMemcpyAsync(&hbad, d_bad, sizeof(int), cudaMemcpyDeviceToHost, s));
-  FEM_CUDA(cudaStreamSynchronize(s));
-  int uem = 0, unm = 0;
-  for (int64_t t = 0; t < nt; ++t) {
-    uem = std::max(uem, hc[2 * t]);
-    unm = std::max(unm, hc[2 * t + 1]);
+  int hbad = 0, uem = 0, unm = 0;
+  for (int pass = 0; pass < 2; ++pass) {
+    RtLayout L0 = rt_layout(NT, LPN, 8, 8, ES, SS, p->phase != nullptr, tr, soa);
+    FEM_CUDA(cudaMemsetAsync(d_bad, 0, sizeof(int), s));
+    fem_status st0 = plan(L0, nullptr);
+    if (st0) return st0;
+    FEM_CUDA(cudaMemcpyAsync(hc.data(), cnt, sizeof(int32_t) * 2 * nt, cudaMemcpyDeviceToHost, s));
+    FEM_CUDA(cudaMemcpyAsync(&hbad, d_bad, sizeof(int), cudaMemcpyDeviceToHost, s));
+    FEM_CUDA(cudaStreamSynchronize(s));
+    uem = unm = 0;
+    for (int64_t t = 0; t < nt; ++t) {
+      uem = std::max(uem, hc[2 * t]);
+      unm = std::max(unm, hc[2 * t + 1]);
+    }
+    if (!soa || (!hbad && uem <= kRtSoaS)) break;
+    soa = false;  // a tile's colored records exceed the SoA stride: odd-stride records
   }
-  uem = (uem + 7) & ~7;
+  uem = soa ? kRtSoaS : (uem + 7) & ~7;
   unm = (unm + 7) & ~7;
-  const RtLayout L = rt_layout(NT, LPN, uem, unm, ES, SS, p->phase != nullptr, tr);
+  const RtLayout L = rt_layout(NT, LPN, uem, unm, ES, SS, p->phase != nullptr, tr, soa);
   // shared memory of the assembly kernel: 3 metadata blocks, 2 node-data buffers, records
   const int RS = D == 3 ? RtGeom<3>::RS : RtGeom<2>::RS;
   const int BP = D == 3 ? RtGeom<3>::BP : RtGeom<2>::BP;
+  const size_t recw = soa ? (size_t)kRtSoaF * kRtSoaS : (size_t)RS * (uem + 1);
   const size_t smem = 3 * (size_t)L.mb + 2 * sizeof(double) * 2 * D * (size_t)unm +
-                      sizeof(double) * (size_t)RS * (uem + 1) +
+                      sizeof(double) * recw +
                       (FEM_RT_DIAG_SMEM ? sizeof(double) * (kRtThreads / 32) * 32 * BP : 0);
   if (hbad || uem >= 1024 || smem > 220 * 1024) {
     cudaFree(d_bad); cudaFree(cnt);
     return FEM_OK;
   }
   FEM_CUDA(cudaMalloc(&out.meta, (size_t)L.mb * nt));
-  st = plan(L, out.meta);
+  fem_status st = plan(L, out.meta);
   if (st) return st;
   if (dbg) {
     std::vector<int32_t> hd(2 * nt);
@@ -641,8 +787,21 @@ static fem_status build_tile_plan(Problem *p, const int32_t *order, const std::v
     for (int64_t q = 0; q < nt; ++q) { a0 += hd[2 * q]; a1 += hd[2 * q + 1]; }
     fprintf(stderr, "[rt place] modelled g_b wavefronts per half-warp step: identity %lld, placed %lld\n", a0, a1);
   }
-  FEM_CUDA(cudaMemcpyAsync(&hbad, d_bad, sizeof(int), cudaMemcpyDeviceToHost, s));
+  int hist[2 + kRtSchedHist];
+  FEM_CUDA(cudaMemcpyAsync(hist, d_bad, sizeof(hist), cudaMemcpyDeviceToHost, s));
   FEM_CUDA(cudaStreamSynchronize(s));
+  hbad = hist[0];
+  if (getenv("FEM_RT_SCHED_STATS")) {
+    long long n = 0, w = 0;
+    fprintf(stderr, "[rt plan] soa=%d tiles=%lld uem=%d schedule lengths:", L.soa, (long long)nt, L.uem);
+    for (int c = 0; c <= kRtSchedHist; ++c)
+      if (hist[1 + c]) {
+        if (c == kRtSchedHist) fprintf(stderr, " grouped:%d", hist[1 + c]);
+        else fprintf(stderr, " %d:%d", c, hist[1 + c]);
+        if (c < kRtSchedHist) { n += hist[1 + c]; w += (long long)c * hist[1 + c]; }
+      }
+    fprintf(stderr, "  mean %.3f\n", n ? (double)w / n : 0.0);
+  }
   cudaFree(d_bad);
   cudaFree(cnt);
   if (hbad) {
@@ -655,6 +814,7 @@ static fem_status build_tile_plan(Problem *p, const int32_t *order, const std::v
   l[0] = L.nt; l[1] = L.uem; l[2] = L.unm; l[3] = L.es; l[4] = L.ss; l[5] = L.mb;
   l[6] = L.off_halo; l[7] = L.off_lc; l[8] = L.off_ph; l[9] = L.off_nd; l[10] = L.off_so;
   l[11] = L.off_sb; l[12] = L.off_en; l[13] = L.lpn; l[14] = L.off_tb; l[15] = L.off_tsn;
+  l[16] = L.soa;
   out.smem = (int)smem;
   out.state = 1;
   return FEM_OK;
@@ -705,10 +865,12 @@ struct RtArgs {
 // TR: fused colored Alg. 2 (FEM_ASSEMBLE_COLORED, reading R13) on node tiles of one node color:
 // each seed's column blocks K[m, n] = K[n, m]^T are written at their decompressed CSR slots
 // (row m D + k, column n D + i), conflict-free within a color; the diagonal block as the row form.
-template <int D, int MAT, int LPN, bool TR = false>
+template <int D, int MAT, int LPN, bool TR = false, bool SOA = false>
 __global__ void __launch_bounds__(kRtThreads, FEM_RT_MINB) k_rows_tile(RtArgs A) {
   using Gm = RtGeom<D>;
   constexpr int NEN = Gm::NEN, BS = Gm::BS, RS = Gm::RS;
+  static_assert(!SOA || (D == 3 && LPN == 16 && !TR), "SoA records: 3D row form, 16 lanes");
+  constexpr int S = kRtSoaS;
   constexpr unsigned FULL = 0xffffffffu;
   extern __shared__ __align__(16) unsigned char sm_rt[];
   const RtLayout &L = A.L;
@@ -717,8 +879,10 @@ __global__ void __launch_bounds__(kRtThreads, FEM_RT_MINB) k_rows_tile(RtArgs A)
   unsigned char *metab = sm_rt;
   double *nodeb = reinterpret_cast<double *>(sm_rt + 3 * mb);  // [2][2][unm][D]: x | u
   double *rec = nodeb + 2 * 2 * unm * D;                         // [uem][RS]
-  double *scratch = rec + (size_t)(L.uem + 1) * RS;              // [8 warps][32][BP]
-  for (int q = tid; q < RS; q += kRtThreads) rec[(size_t)L.uem * RS + q] = 0.0;  // zero record
+  // AoS: [uem + 1][RS] (the last one the zero record of idle steps); SoA: [kRtSoaF][S]
+  double *scratch = rec + (SOA ? (size_t)kRtSoaF * S : (size_t)(L.uem + 1) * RS);  // [8 warps][32][BP]
+  if (!SOA)
+    for (int q = tid; q < RS; q += kRtThreads) rec[(size_t)L.uem * RS + q] = 0.0;  // zero record
   const int64_t G = gridDim.x;
 
   __shared__ __align__(8) uint64_t mb_meta[3];
@@ -807,14 +971,16 @@ __global__ void __launch_bounds__(kRtThreads, FEM_RT_MINB) k_rows_tile(RtArgs A)
         lam = A.lam_tab[ph];
         mu = A.mu_tab[ph];
       }
-      double *r = rec + e * RS;
+      // field f of this record: AoS r[f], SoA r[f * S]
+      double *r = rec + (SOA ? e : e * RS);
+      constexpr int FS = SOA ? S : 1;
       double c1 = mu;
       bool ok = true;
       if constexpr (MAT == FEM_LINEAR_ELASTIC) {
 #pragma unroll
         for (int a = 0; a < NEN; ++a)
 #pragma unroll
-          for (int i = 0; i < D; ++i) r[Gm::G0 + a * Gm::GP + i] = G[a][i];
+          for (int i = 0; i < D; ++i) r[(SOA ? a * D + i : Gm::G0 + a * Gm::GP + i) * FS] = G[a][i];
       } else {
         // g_a = F^-T G_a is the shape-function gradient in the deformed configuration, i.e.
         // the geometry of the element at x + u, and J = det F = det J(x + u) / det J(x): two
@@ -834,7 +1000,8 @@ __global__ void __launch_bounds__(kRtThreads, FEM_RT_MINB) k_rows_tile(RtArgs A)
 #pragma unroll
         for (int a = 0; a < NEN; ++a)
 #pragma unroll
-          for (int i = 0; i < D; ++i) r[Gm::G0 + a * Gm::GP + i] = ok ? g[a][i] : 0.0;
+          for (int i = 0; i < D; ++i)
+            r[(SOA ? a * D + i : Gm::G0 + a * Gm::GP + i) * FS] = ok ? g[a][i] : 0.0;
       }
       const double smu = ok ? vol * mu : 0.0;
 #pragma unroll
@@ -844,10 +1011,10 @@ __global__ void __launch_bounds__(kRtThreads, FEM_RT_MINB) k_rows_tile(RtArgs A)
           double gg = 0.0;
 #pragma unroll
           for (int j = 0; j < D; ++j) gg = fma(G[a][j], G[b][j], gg);
-          r[Gm::M0 + rt_pair<D>(a, b)] = smu * gg;
+          r[(SOA ? rt_soa_m(a, b) : Gm::M0 + rt_pair<D>(a, b)) * FS] = smu * gg;
         }
-      r[Gm::S0] = ok ? vol * c1 : 0.0;
-      r[Gm::S0 + 1] = ok ? vol * lam : 0.0;
+      r[(SOA ? 15 : Gm::S0) * FS] = ok ? vol * c1 : 0.0;
+      r[(SOA ? 19 : Gm::S0 + 1) * FS] = ok ? vol * lam : 0.0;
     }
     __syncthreads();
     // ---- 2: rows, LPN lanes per tile node (NPW nodes per warp)
@@ -880,6 +1047,36 @@ __global__ void __launch_bounds__(kRtThreads, FEM_RT_MINB) k_rows_tile(RtArgs A)
       double acc[BS];
 #pragma unroll
       for (int q = 0; q < BS; ++q) acc[q] = 0.0;
+      if constexpr (SOA) {
+        // SoA records: every load one wavefront per half-warp (the plan's colored records and
+        // color-distinct co-scheduled steps); idle steps (0xffff) load nothing
+#pragma unroll kRtUnroll
+        for (int c = lo; c < hi; ++c) {
+          const uint32_t en = ent[c];
+          if (en != 0xffffu) {
+            const int rr = en & 1023u, a = (en >> 10) & 3u, b = (en >> 12) & 3u;
+            const double *ra = rec + 3 * a * S + rr, *rb = rec + 3 * b * S + rr;
+            const double Mab = rec[rt_soa_m(a, b) * S + rr];
+            const double sc1 = rec[15 * S + rr], sc2 = rec[19 * S + rr];
+            double ga[3], gb[3];
+#pragma unroll
+            for (int i = 0; i < 3; ++i) {
+              ga[i] = ra[i * S];
+              gb[i] = rb[i * S];
+            }
+#pragma unroll
+            for (int i = 0; i < D; ++i) {
+              const double qi = sc2 * ga[i];
+#pragma unroll
+              for (int kk = 0; kk < D; ++kk) {
+                double v = fma(sc1 * ga[kk], gb[i], acc[i * D + kk]);
+                v = fma(qi, gb[kk], v);
+                acc[i * D + kk] = (i == kk) ? v + Mab : v;
+              }
+            }
+          }
+        }
+      } else
 #pragma unroll kRtUnroll
       for (int c = lo; c < hi; ++c) {
         const uint32_t en = ent[c];
@@ -1005,7 +1202,7 @@ static fem_status launch_plan(Problem *p, const RtPlan &P, int64_t t0, int64_t t
   A.L.nt = lay[0]; A.L.uem = lay[1]; A.L.unm = lay[2]; A.L.es = lay[3]; A.L.ss = lay[4];
   A.L.mb = lay[5]; A.L.off_halo = lay[6]; A.L.off_lc = lay[7]; A.L.off_ph = lay[8];
   A.L.off_nd = lay[9]; A.L.off_so = lay[10]; A.L.off_sb = lay[11]; A.L.off_en = lay[12];
-  A.L.lpn = lay[13]; A.L.off_tb = lay[14]; A.L.off_tsn = lay[15];
+  A.L.lpn = lay[13]; A.L.off_tb = lay[14]; A.L.off_tsn = lay[15]; A.L.soa = lay[16];
   A.meta = P.meta + t0 * (int64_t)A.L.mb; A.n_tiles = tiles; A.coords = p->coords; A.z = z;
   A.lam = p->lam; A.mu = p->mu; A.lam_tab = p->lam_tab; A.mu_tab = p->mu_tab;
   A.has_phase = p->phase != nullptr; A.bc = bc ? 1 : 0; A.vals = vals; A.err = p->d_err;
@@ -1015,6 +1212,8 @@ static fem_status launch_plan(Problem *p, const RtPlan &P, int64_t t0, int64_t t
   if (p->dim == 2)
     kern = le ? (lpn == 8 ? k_rows_tile<2, FEM_LINEAR_ELASTIC, 8, TR> : lpn == 16 ? k_rows_tile<2, FEM_LINEAR_ELASTIC, 16, TR> : k_rows_tile<2, FEM_LINEAR_ELASTIC, 32, TR>)
               : (lpn == 8 ? k_rows_tile<2, FEM_NEO_HOOKEAN, 8, TR> : lpn == 16 ? k_rows_tile<2, FEM_NEO_HOOKEAN, 16, TR> : k_rows_tile<2, FEM_NEO_HOOKEAN, 32, TR>);
+  else if (A.L.soa && !TR)
+    kern = le ? k_rows_tile<3, FEM_LINEAR_ELASTIC, 16, false, true> : k_rows_tile<3, FEM_NEO_HOOKEAN, 16, false, true>;
   else
     kern = le ? (lpn == 16 ? k_rows_tile<3, FEM_LINEAR_ELASTIC, 16, TR> : k_rows_tile<3, FEM_LINEAR_ELASTIC, 32, TR>)
               : (lpn == 16 ? k_rows_tile<3, FEM_NEO_HOOKEAN, 16, TR> : k_rows_tile<3, FEM_NEO_HOOKEAN, 32, TR>);

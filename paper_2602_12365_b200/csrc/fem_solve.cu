@@ -599,6 +599,7 @@ fem_status fem_newton_solve(fem_problem *h, double *z, const fem_newton_opts *o,
                             fem_newton_report *rep, fem_stream stream) {
   FEM_NVTX_RANGE("fem_newton_solve");
   FEM_ARG(h && z && o && rep, "fem_newton_solve: null argument");
+  FEM_ARG(o->forcing >= 0.0 && o->forcing <= 1.0, "fem_newton_solve: forcing must be in [0, 1]");
   Problem *p = &h->p;
   cudaStream_t s = (cudaStream_t)stream;
   const int64_t n = p->N;
@@ -613,7 +614,7 @@ fem_status fem_newton_solve(fem_problem *h, double *z, const fem_newton_opts *o,
   FEM_CUDA(cudaMalloc(&buf, bytes));
   double *r = buf, *dz = buf + n, *vals = csr ? buf + 2 * n : nullptr;
   rep->iters = rep->cg_iters = rep->converged = 0;
-  double r0 = 0.0;
+  double r0 = 0.0, r_prev = 0.0, eta_prev = 0.0;
   fem_status result = FEM_OK;
   for (int it = 0;; ++it) {
     st = run_residual(p, z, r, FEM_APPLY_BC, s);
@@ -639,6 +640,24 @@ fem_status fem_newton_solve(fem_problem *h, double *z, const fem_newton_opts *o,
     }
     fem_cg_report cr{};
     fem_cg_opts co = o->cg;
+    if (o->forcing > 0.0) {
+      // inexact Newton-Krylov (reading R16): Eisenstat-Walker choice 2 (alpha = 2)
+      constexpr double kEtaMax = 0.1;
+      const double g = o->forcing;
+      double eta = kEtaMax;
+      if (it > 0) {
+        const double q = nr / r_prev;
+        eta = std::fmin(kEtaMax, g * q * q);
+        const double sg = g * eta_prev * eta_prev;  // safeguard against a premature drop
+        if (sg > 0.1) eta = std::fmin(kEtaMax, std::fmax(eta, sg));
+      }
+      const double tau = std::fmax(o->atol, o->rtol * r0);
+      eta = std::fmin(kEtaMax, std::fmax(eta, 0.5 * tau / nr));  // no over-solving of the last step
+      eta = std::fmax(eta, o->cg.rtol);
+      co.rtol = eta;
+      eta_prev = eta;
+    }
+    r_prev = nr;
     // matrix-free CG on the linearized tangent (fem_linearize: the cached metric form; cfg 3
     // HVP 0.76 vs 0.94 ms recomputed); FEM_NEWTON_RECOMPUTE=1 recomputes the state per HVP
     if (!csr && p->material == FEM_NEO_HOOKEAN && !getenv("FEM_NEWTON_RECOMPUTE")) {

@@ -99,7 +99,7 @@ class GmresOpts(C.Structure):
 
 class NewtonOpts(C.Structure):
     _fields_ = [("atol", C.c_double), ("rtol", C.c_double), ("max_iter", C.c_int),
-                ("cg", CgOpts)]
+                ("cg", CgOpts), ("forcing", C.c_double)]
 
 
 class NewtonReport(C.Structure):
@@ -425,10 +425,13 @@ class Problem:
         return y
 
     def newton_solve(self, z0, atol=1e-12, rtol=1e-10, max_iter=50, op=0, cg_rtol=1e-10,
-                     cg_max_iter=100000, jacobi=False, check_every=1, raise_on_fail=True):
+                     cg_max_iter=100000, jacobi=False, check_every=1, raise_on_fail=True,
+                     forcing=0.0):
+        """forcing = 0: inner CG to cg_rtol at every step; in (0, 1]: Eisenstat-Walker
+        forcing terms with gamma = forcing (fem.h fem_newton_opts, DESIGN reading R16)."""
         z = self._vec(z0, "z0").clone()
         o = NewtonOpts(atol, rtol, max_iter, CgOpts(op, cg_rtol, 0.0, cg_max_iter, int(jacobi),
-                                                    check_every, 0))
+                                                    check_every, 0), float(forcing))
         rep = NewtonReport()
         st = load_library().fem_newton_solve(self._h, _ptr(z), C.byref(o), C.byref(rep), _stream())
         info = {"status": st, "iters": rep.iters, "cg_iters": rep.cg_iters,

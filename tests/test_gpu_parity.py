@@ -197,6 +197,34 @@ def test_newton(case):
         assert rel(zg, zr) <= 1e-10
 
 
+@pytest.mark.parametrize("dim", [2, 3])
+def test_newton_eisenstat_walker(fem, oracle_mod, dim):
+    """Inexact Newton-Krylov (fem_newton_opts.forcing, reading R16): the same converged
+    displacements as the oracle's exact-inner-solve Newton (<= 1e-10), with fewer CG
+    iterations than fixed inner tolerances at the same outer target; MF and CSR operators."""
+    if dim == 2:
+        mesh = fi.config_mesh(2, n=40)
+        eps = 0.1
+    else:
+        mesh = fi.config_mesh(3, n=10)
+        eps = 0.05
+    z0 = fi.lift(mesh, fi.affine_field(mesh, np.diag([eps] + [0.0] * (dim - 1))))
+    zr, rinfo = oracle_mod.Oracle(mesh).newton(z0, cg_rtol=1e-13)
+    assert rinfo["status"] == 0
+    prob = fem.Problem(mesh)
+    kw = dict(cg_rtol=1e-13, rtol=1e-12, atol=1e-16)
+    zf, info_f = prob.newton_solve(dev(z0), op=0, **kw)
+    for op, jac in ((0, 0), (1, 2)):
+        ze, info_e = prob.newton_solve(dev(z0), op=op, jacobi=jac, forcing=0.9, **kw)
+        assert info_e["converged"] and info_e["res"] <= 1e-12 * info_e["res0"]
+        assert rel(ze, zr) <= 1e-10
+    ze, info_e = prob.newton_solve(dev(z0), op=0, forcing=0.9, **kw)
+    assert info_f["converged"] and info_e["cg_iters"] < info_f["cg_iters"]
+    for bad in (-0.5, 1.5):
+        with pytest.raises(RuntimeError):
+            prob.newton_solve(dev(z0), op=0, forcing=bad, **kw)
+
+
 # ------------------------------------------------------------------ edge cases
 
 def test_single_element_and_empty(fem, oracle_mod):

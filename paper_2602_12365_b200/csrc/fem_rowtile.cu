@@ -101,6 +101,17 @@
 #ifndef FEM_RT_SOA
 #define FEM_RT_SOA 0
 #endif
+// node staging: one thread per halo node (D copies each of x and z) instead of one per
+// component (the i / D, i % D address math: ncu source counters r02, 172 M of the kernel's
+// 1.79 G warp instructions in the staging loop)
+// diagonal blocks: the sum over the node's slot lanes unrolled with predicated loads and two
+// partial sums (even / odd slots) instead of a counted loop of dependent adds
+#ifndef FEM_RT_DIAG_UNROLL
+#define FEM_RT_DIAG_UNROLL 1
+#endif
+#ifndef FEM_RT_ISSUE_NODE
+#define FEM_RT_ISSUE_NODE 1
+#endif
 // visit budget of the plan's depth-first co-schedule search per node and length (0: first fit)
 #ifndef FEM_RT_SOA_DFS
 #define FEM_RT_SOA_DFS 4000
@@ -139,10 +150,11 @@ struct RtGeom {
 };
 
 // index of the unordered node pair {a, b}: 3D (01 02 03 12 13 23), 2D (01 02 12)
+// (a != b): 3D a + b - [0 in {a, b}], 2D a + b - 1 — three integer ops per slot-loop entry
+// instead of the min / max / select chain
 template <int D>
 __host__ __device__ constexpr int rt_pair(int a, int b) {
-  return (a < b ? a : b) == 0 ? (a < b ? b : a) - 1
-                              : (D == 2 ? 2 : ((a < b ? a : b) == 1 ? (a < b ? b : a) + 1 : 5));
+  return D == 3 ? a + b - (a * b == 0 ? 1 : 0) : a + b - 1;
 }
 
 struct RtLayout {
@@ -740,10 +752,11 @@ static fem_status build_tile_plan(Problem *p, const int32_t *order, const std::v
     }
     return FEM_OK;
   };
-  // SoA records (FEM_RT_SOA): 3D row form with 16 lanes per <= 16-node tile; FEM_RT_SOA_OFF=1
-  // (environment) selects the odd-stride layout at run time (A/B)
-  bool soa = FEM_RT_SOA && D == 3 && LPN == 16 && NT <= 16 && !tr && !FEM_RT_PLACE &&
-             !getenv("FEM_RT_SOA_OFF");
+  // SoA records (FEM_RT_SOA): 3D row form with 16 lanes per <= 16-node tile; the environment
+  // variable FEM_RT_SOA=0/1 overrides the compiled default at run time (A/B)
+  const char *soa_env = getenv("FEM_RT_SOA");  // run-time override of the default (A/B)
+  bool soa = (soa_env ? atoi(soa_env) != 0 : FEM_RT_SOA) && D == 3 && LPN == 16 && NT <= 16 &&
+             !tr && !FEM_RT_PLACE && !getenv("FEM_RT_SOA_OFF");
   std::vector<int32_t> hc(2 * nt);
   int hbad = 0, uem = 0, unm = 0;
   for (int pass = 0; pass < 2; ++pass) {
@@ -911,10 +924,21 @@ __global__ void __launch_bounds__(kRtThreads, FEM_RT_MINB) k_rows_tile(RtArgs A)
   auto issue_nodes = [&](const unsigned char *m, double *dst) {
     const int un = reinterpret_cast<const int *>(m)[1];
     const int32_t *hid = reinterpret_cast<const int32_t *>(m + L.off_halo);
-    for (int i = tid; i < un * D; i += kRtThreads) {
-      const int64_t g = (int64_t)hid[i / D] * D + (i % D);
-      rt_cp8(dst + i, A.coords + g);
-      rt_cp8(dst + unm * D + i, A.z + g);
+    if (FEM_RT_ISSUE_NODE) {  // one thread per halo node: D copies of x and of z each
+      for (int r = tid; r < un; r += kRtThreads) {
+        const int64_t g = (int64_t)hid[r] * D;
+#pragma unroll
+        for (int c = 0; c < D; ++c) {
+          rt_cp8(dst + r * D + c, A.coords + g + c);
+          rt_cp8(dst + unm * D + r * D + c, A.z + g + c);
+        }
+      }
+    } else {
+      for (int i = tid; i < un * D; i += kRtThreads) {
+        const int64_t g = (int64_t)hid[i / D] * D + (i % D);
+        rt_cp8(dst + i, A.coords + g);
+        rt_cp8(dst + unm * D + i, A.z + g);
+      }
     }
   };
 
@@ -1157,7 +1181,17 @@ __global__ void __launch_bounds__(kRtThreads, FEM_RT_MINB) k_rows_tile(RtArgs A)
       if (live && ql < BS) {
         const double *sb = scratch + (w * 32 + h * LPN) * Gm::BP + ql;
         const int cnt = min(LPN, sno - pass * LPN);
-        for (int qq = 0; qq < cnt; ++qq) dacc += sb[qq * Gm::BP];
+        if (FEM_RT_DIAG_UNROLL) {  // predicated, fully unrolled; even / odd slots in two chains
+          double d0 = 0.0, d1 = 0.0;
+#pragma unroll
+          for (int qq = 0; qq < LPN; qq += 2) {
+            if (qq < cnt) d0 += sb[qq * Gm::BP];
+            if (qq + 1 < cnt) d1 += sb[(qq + 1) * Gm::BP];
+          }
+          dacc += d0 + d1;
+        } else {
+          for (int qq = 0; qq < cnt; ++qq) dacc += sb[qq * Gm::BP];
+        }
       }
       __syncwarp();
       }  // slot passes

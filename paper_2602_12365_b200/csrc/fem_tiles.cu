@@ -1535,6 +1535,19 @@ __device__ __forceinline__ void tile_phase2(const PipeArgs &A, const unsigned ch
 #ifndef FEM_ENERGY_DEC
 #define FEM_ENERGY_DEC 0
 #endif
+// metadata buffers of the decoupled (HVP) pipeline: 3 = tile k+2's block issued after barrier
+// k; 4 = tile k+3's (ncu r02 source counters: 6.5 % of the HVP's stall samples waiting on the
+// next tile's metadata at the top of an iteration — a TMA bulk copy with half an iteration
+// of lead time).  Measured (r02, cfg 3, same box, twice): HVP 0.923 / 0.924 ms with 4 buffers
+// against 0.910 / 0.911 with 3 (the extra 7 KB per CTA comes out of L1): 3 kept.
+#ifndef FEM_META_BUFS
+#define FEM_META_BUFS 3
+#endif
+static_assert(FEM_META_BUFS == 3 || FEM_META_BUFS == 4, "FEM_META_BUFS: 3 or 4");
+template <int OP>
+constexpr bool pipe_decoupled();
+template <int OP>
+constexpr int meta_bufs() { return pipe_decoupled<OP>() && !FEM_DEC2 ? FEM_META_BUFS : 3; }
 template <int OP>
 constexpr bool pipe_decoupled() {
   return (FEM_HVP_DEC && op_is_hvp<OP>() && !op_streams<OP>()) || (FEM_RES_DEC && OP == OP_RESIDUAL) ||
@@ -1552,12 +1565,13 @@ __global__ void __launch_bounds__(kTile, pipe_minb(OP, MAT, D)) k_tile_pipe(Pipe
   constexpr bool STREAM = op_streams<OP>();
   constexpr unsigned GBYTES = sizeof(double) * geom_words(D) * kTile;
   extern __shared__ __align__(16) unsigned char sm[];
-  __shared__ __align__(8) uint64_t mb_meta[3], mb_node[2], mb_geom[2], mb_p1[2], mb_p2[2];
+  constexpr int NMB = meta_bufs<OP>();
+  __shared__ __align__(8) uint64_t mb_meta[4], mb_node[2], mb_geom[2], mb_p1[2], mb_p2[2];
   const int tid = threadIdx.x;
   const int mb = A.mb, um = A.um;
   const int nstride = um * D * NF;
   unsigned char *metab = sm;
-  double *nodeb = reinterpret_cast<double *>(sm + 3 * mb);
+  double *nodeb = reinterpret_cast<double *>(sm + NMB * mb);
   double *contrib = nodeb + 2 * nstride;
   double *geomb = contrib + (DEC ? 2 : 1) * ((D + 1) * D * kCbStride);  // STREAM: 2 blocks
   const int64_t G = gridDim.x;
@@ -1628,15 +1642,15 @@ __global__ void __launch_bounds__(kTile, pipe_minb(OP, MAT, D)) k_tile_pipe(Pipe
   if (t < A.n_tiles) prefetch_refm(t);
   if constexpr (DEC) {
     if (tid == 0) {
-      for (int b = 0; b < 3; ++b) mb_init(&mb_meta[b], FEM_TMA_META ? 1 : kTile);
+      for (int b = 0; b < NMB; ++b) mb_init(&mb_meta[b], FEM_TMA_META ? 1 : kTile);
       for (int b = 0; b < 2; ++b) mb_init(&mb_node[b], kTile);
       for (int b = 0; b < 2; ++b) mb_init(&mb_p1[b], kTile);
       for (int b = 0; b < 2; ++b) mb_init(&mb_p2[b], kTile);
       asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
     __syncthreads();
-    if (t < A.n_tiles) issue_meta(t, 0);
-    if (t + G < A.n_tiles) issue_meta(t + G, 1);
+    for (int b = 0; b < NMB - 1; ++b)
+      if (t + b * G < A.n_tiles) issue_meta(t + b * G, b);
     if (t < A.n_tiles) {
       mb_wait(&mb_meta[0], 0);
       issue_nodes(metab, 0);
@@ -1677,12 +1691,12 @@ __global__ void __launch_bounds__(kTile, pipe_minb(OP, MAT, D)) k_tile_pipe(Pipe
       }
     } else {
       for (int k = 0; t < A.n_tiles; ++k, t += G) {
-        const int bm = k % 3, bn = k & 1;
+        const int bm = k % NMB, bn = k & 1;
         const unsigned char *m = metab + bm * mb;
         mb_wait(&mb_node[bn], (unsigned)(k >> 1) & 1u);  // node data of tile k
-        if (t + G < A.n_tiles) {  // node data of tile k+1 (its metadata issued after barrier k-1)
-          const int bm1 = (k + 1) % 3;
-          mb_wait(&mb_meta[bm1], (unsigned)((k + 1) / 3) & 1u);
+        if (t + G < A.n_tiles) {  // node data of tile k+1 (its metadata issued after barrier k+2-NMB)
+          const int bm1 = (k + 1) % NMB;
+          mb_wait(&mb_meta[bm1], (unsigned)((k + 1) / NMB) & 1u);
           issue_nodes(metab + bm1 * mb, bn ^ 1);
           if constexpr (OP == OP_HVP_LIN && MAT == FEM_NEO_HOOKEAN) {  // cache rows of tile k+1 -> L2
             if (tid < lin_words(D)) {
@@ -1698,7 +1712,7 @@ __global__ void __launch_bounds__(kTile, pipe_minb(OP, MAT, D)) k_tile_pipe(Pipe
         double *cb = contrib + (k & 1) * ((D + 1) * D * kCbStride);
         tile_phase1<D, MAT, OP, MASK>(A, m, nb, nb + UOFF * um * D, nb + (NF - 1) * um * D, tile_id(t), tid, cb, eacc);
         __syncthreads();  // phase 1 of tile k done; tile k-1 fully consumed
-        if (t + 2 * G < A.n_tiles) issue_meta(t + 2 * G, (k + 2) % 3);
+        if (t + (NMB - 1) * G < A.n_tiles) issue_meta(t + (NMB - 1) * G, (k + NMB - 1) % NMB);
         if constexpr (op_has_p2<OP>())
           tile_phase2<D, OP, SC>(A, m, reinterpret_cast<const int *>(m)[0], tile_id(t), tid, cb);
       }
@@ -1909,7 +1923,7 @@ static fem_status launch_pipe_t(Problem *p, const PipeArgs &a, cudaStream_t s) {
   const bool need_u = op_needs_u<OP, MAT>();
   const int nf = (op_needs_x<OP, MAT>() ? 1 : 0) + (need_u ? 1 : 0) + (op_is_hvp<OP>() ? 1 : 0);
   if constexpr (op_refm<OP>()) static_assert(MAT == FEM_NEO_HOOKEAN, "OP_*_R: neo-Hookean only");
-  const size_t smem = (size_t)3 * T.mb + sizeof(double) * 2 * (size_t)T.um * D * nf +
+  const size_t smem = (size_t)meta_bufs<OP>() * T.mb + sizeof(double) * 2 * (size_t)T.um * D * nf +
                       (!op_has_p2<OP>() ? 0 : (pipe_decoupled<OP>() ? 2 : 1) * sizeof(double) * (size_t)(D + 1) * D * kCbStride) +
                       (op_streams<OP>() ? 2 * sizeof(double) * geom_words(D) * kTile : 0);
   auto kern = k_tile_pipe<D, MAT, OP, MASK, SC>;

@@ -12,7 +12,11 @@ import sys
 
 def main(path, specs):
     rows = list(csv.reader(open(path)))
-    h, data = rows[1], rows[2:]
+    h, data = rows[1], []
+    for r in rows[2:]:  # the first kernel block only (a multi-kernel export repeats the header)
+        if not r or r[0] in ("Kernel Name", "Address"):
+            break
+        data.append(r)
     ia, isrc = h.index("Address"), h.index("Source")
     iss, iex = h.index("Warp Stall Sampling (All Samples)"), h.index("Instructions Executed")
     stalls = [c for c in h if c.startswith("stall_") and "Not Issued" not in c]

@@ -94,7 +94,9 @@ struct TileSet {
   uint8_t *meta = nullptr;
   int um = 0, mb = 0, off_nodes = 0, off_lconn = 0, off_ptr = 0, off_inc = 0, off_int = 0,
       off_bc = 0, off_ph = 0, off_soff = 0, off_smeta = 0, off_perm = 0;
-  uint16_t *p2perm = nullptr;    // [n_tiles][maxe] phase-2 thread -> tile node (FEM_P2_SORT)
+  uint16_t *p2perm = nullptr;    // [n_tiles][maxe] phase-2 thread -> tile node (FEM_P2_SORT) or task (FEM_P2_LSPLIT)
+  int32_t *p2n = nullptr;        // [n_tiles] phase-2 task count (FEM_P2_LSPLIT)
+  int pcap = 0;                  // phase-2 order / task entries per metadata block
 };
 
 // node-tile assembly plan (fem_rowtile.cu build_tile_plan)

@@ -93,6 +93,17 @@
 #define FEM_P2_SORT 0
 #endif
 // unroll factor of the default node-sum loop (pairs of incidences per unrolled step)
+// Phase-2 long-node split: nodes with more than FEM_P2_LSPLIT incidences are summed by two
+// adjacent lanes (halves of the list; the even lane adds the odd lane's partial by one
+// shuffle, fixed order), so the longest node-sum chain (24 incidences for an interior Kuhn
+// node) halves while the other nodes keep one lane each and most warps stay free to start the
+// next tile (two lanes for every node, FEM_P2_PAIR, kept all 8 warps busy: slower).  0 = off.
+// Measured (r02, cfg 3, two A/B pairs): HVP 0.958 / 0.957 ms at threshold 12 (0.943 at 8,
+// 0.957 at 16) against 0.923 / 0.922 off; residual 0.799 vs 0.793 — the extra phase-2 lanes
+// cost more than the halved chains save.  Off; the task branch is compiled only when on.
+#ifndef FEM_P2_LSPLIT
+#define FEM_P2_LSPLIT 0
+#endif
 #ifndef FEM_P2_UNROLL
 #define FEM_P2_UNROLL 1
 #endif
@@ -479,7 +490,7 @@ __global__ void k_pack_meta(TileSet T, const uint8_t *node_bc, int64_t E) {
     reinterpret_cast<int *>(base)[0] = U;
     reinterpret_cast<int *>(base)[1] = nvalid;
     reinterpret_cast<int *>(base)[2] = T.shdr ? (int)T.shdr[t] : 0;
-    reinterpret_cast<int *>(base)[3] = 0;
+    reinterpret_cast<int *>(base)[3] = T.p2n ? T.p2n[t] : 0;  // phase-2 tasks (FEM_P2_LSPLIT)
   }
   if (T.shdr) {
     const int cap = T.sched_rounds * kTile;
@@ -524,7 +535,8 @@ __global__ void k_pack_meta(TileSet T, const uint8_t *node_bc, int64_t E) {
       base[T.off_ph + i] = (e0 + i < E) ? T.phase[e0 + i] : 0;
   if (T.p2perm) {
     uint16_t *pp = reinterpret_cast<uint16_t *>(base + T.off_perm);
-    for (int i = threadIdx.x; i < T.um; i += blockDim.x) pp[i] = i < U ? T.p2perm[t * T.maxe + i] : 0;
+    const int n = T.p2n ? T.p2n[t] : U;
+    for (int i = threadIdx.x; i < T.pcap; i += blockDim.x) pp[i] = i < n ? T.p2perm[t * T.maxe + i] : 0;
   }
 }
 
@@ -585,6 +597,26 @@ __global__ void k_p2_perm(TileSet T) {
   for (int len = maxlen; len >= 0; --len)
     for (int r = 0; r < U; ++r)
       if ((int)ptr[r + 1] - (int)ptr[r] == len) perm[pos++] = (uint16_t)r;
+}
+
+// Phase-2 tasks (FEM_P2_LSPLIT): long nodes first as (first half, second half) lane pairs at
+// even positions, then the other nodes in node order; entry = r | 1 << 14 (first half) | 1 << 15
+// (second half).  One thread per tile.
+__global__ void k_p2_tasks(TileSet T, int th) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= T.n_tiles) return;
+  const int U = T.U[t];
+  const uint16_t *ptr = T.ptr + t * (T.maxe + 1);
+  uint16_t *task = T.p2perm + t * T.maxe;
+  int pos = 0;
+  for (int r = 0; r < U; ++r)
+    if ((int)ptr[r + 1] - (int)ptr[r] > th) {
+      task[pos++] = (uint16_t)(r | 1 << 14);
+      task[pos++] = (uint16_t)(r | 1 << 15);
+    }
+  for (int r = 0; r < U; ++r)
+    if ((int)ptr[r + 1] - (int)ptr[r] <= th) task[pos++] = (uint16_t)r;
+  T.p2n[t] = pos;
 }
 
 // Balanced phase-2 schedule (FEM_P2_BAL).  The tile's incidences (node r, element el, slot
@@ -729,7 +761,9 @@ fem_status pack_tile_meta(Problem *p, cudaStream_t s) {
     else k_build_sched<2><<<g, 128, 0, s>>>(T, T.sched_rounds);
     FEM_LAUNCH_CHECK("phase-2 schedule");
   }
-  if (FEM_P2_SORT && !FEM_P2_BAL && !FEM_P2_G8 && !FEM_P2_NM && !FEM_P2_PAIR) {
+  const bool lsplit = FEM_P2_LSPLIT > 0 && p->dim == 3 && !FEM_P2_BAL && !FEM_P2_G8 && !FEM_P2_NM && !FEM_P2_PAIR &&
+                      !getenv("FEM_P2_LSPLIT_OFF");
+  if (FEM_P2_SORT && !FEM_P2_BAL && !FEM_P2_G8 && !FEM_P2_NM && !FEM_P2_PAIR && !lsplit) {
     FEM_CUDA(cudaMalloc(&T.p2perm, sizeof(uint16_t) * (size_t)T.n_tiles * T.maxe));
     k_p2_perm<<<(unsigned)((T.n_tiles + 127) / 128), 128, 0, s>>>(T);
     FEM_LAUNCH_CHECK("phase-2 node order");
@@ -739,6 +773,14 @@ fem_status pack_tile_meta(Problem *p, cudaStream_t s) {
     FEM_LAUNCH_CHECK("tile incidence scheduling");
   }
   T.um = round_up(T.max_U > 0 ? T.max_U : 1, 8);
+  T.pcap = T.um;
+  if (lsplit) {  // tasks: <= 2 U per tile
+    FEM_CUDA(cudaMalloc(&T.p2perm, sizeof(uint16_t) * (size_t)T.n_tiles * T.maxe));
+    FEM_CUDA(cudaMalloc(&T.p2n, sizeof(int32_t) * (size_t)T.n_tiles));
+    k_p2_tasks<<<(unsigned)((T.n_tiles + 127) / 128), 128, 0, s>>>(T, FEM_P2_LSPLIT);
+    FEM_LAUNCH_CHECK("phase-2 tasks");
+    T.pcap = std::min(2 * T.um, T.maxe);
+  }
   if (FEM_P2_G8) {  // padded incidence groups (k_g8_fill), staged for k_pack_meta
     int *d_max = nullptr, h_max = 0;
     FEM_CUDA(cudaMalloc(&d_max, sizeof(int)));
@@ -775,7 +817,7 @@ fem_status pack_tile_meta(Problem *p, cudaStream_t s) {
   T.off_bc = T.off_int + round_up(T.um, 16);
   T.off_ph = T.off_bc + round_up(T.um, 16);
   T.off_perm = round_up(T.off_ph + (T.phase ? kTile : 0), 16);
-  T.mb = round_up(T.off_perm + (T.p2perm ? 2 * T.um : 0), 16);
+  T.mb = round_up(T.off_perm + (T.p2perm ? 2 * T.pcap : 0), 16);
   FEM_CUDA(cudaMalloc(&T.meta, (size_t)T.mb * T.n_tiles));
   if (p->dim == 2) k_pack_meta<2><<<(unsigned)T.n_tiles, 256, 0, s>>>(T, p->node_bc, p->n_elems);
   else k_pack_meta<3><<<(unsigned)T.n_tiles, 256, 0, s>>>(T, p->node_bc, p->n_elems);
@@ -1464,6 +1506,50 @@ __device__ __forceinline__ void tile_phase2(const PipeArgs &A, const unsigned ch
   const uint16_t *ptr = reinterpret_cast<const uint16_t *>(m + A.off_ptr);
   const uint16_t *inc = reinterpret_cast<const uint16_t *>(m + A.off_inc);
   const uint16_t *perm = reinterpret_cast<const uint16_t *>(m + A.off_perm);
+  const int ntask = FEM_P2_LSPLIT > 0 ? reinterpret_cast<const int *>(m)[3] : 0;
+  if (FEM_P2_LSPLIT > 0 && ntask > 0) {  // FEM_P2_LSPLIT tasks: long nodes on lane pairs (warp-uniform loop: shuffles)
+    const int nround = (ntask + 31) & ~31;
+    for (int q = tid; q < nround; q += nth) {
+      const bool act = q < ntask;
+      const unsigned tk = act ? perm[q] : 0u;
+      const int r = tk & 0xfff;
+      const bool first = (tk >> 14) & 1u, second = (tk >> 15) & 1u;
+      int lo = 0, hi = 0;
+      if (act) {
+        lo = ptr[r];
+        hi = ptr[r + 1];
+        const int mid = (lo + hi + 1) >> 1;
+        if (first) hi = mid;
+        if (second) lo = mid;
+      }
+      double s0[D], s1[D];
+#pragma unroll
+      for (int cc = 0; cc < D; ++cc) s0[cc] = s1[cc] = 0.0;
+      int w = lo;
+      for (; w + 1 < hi; w += 2) {
+        const int p0 = inc[w], p1 = inc[w + 1];
+#pragma unroll
+        for (int cc = 0; cc < D; ++cc) {
+          s0[cc] += cb[p0 + cc * kTile];
+          s1[cc] += cb[p1 + cc * kTile];
+        }
+      }
+      if (w < hi) {
+        const int pk = inc[w];
+#pragma unroll
+        for (int cc = 0; cc < D; ++cc) s0[cc] += cb[pk + cc * kTile];
+      }
+      double sacc[D];
+#pragma unroll
+      for (int cc = 0; cc < D; ++cc) {
+        sacc[cc] = s0[cc] + s1[cc];
+        const double oth = __shfl_down_sync(0xffffffffu, sacc[cc], 1);
+        if (first) sacc[cc] += oth;   // (first half) + (second half)
+      }
+      if (act && !second) node_write<D, SC>(A, m, r, t, sacc);
+    }
+    return;
+  }
   for (int q = tid; q < U; q += nth) {  // one thread per tile node, D components
     const int r = A.has_perm ? perm[q] : q;
     const int lo = ptr[r], hi = ptr[r + 1];
@@ -1685,7 +1771,9 @@ __global__ void __launch_bounds__(kTile, pipe_minb(OP, MAT, D)) k_tile_pipe(Pipe
           issue_meta(t + 2 * G, (k + 2) % 3);
         }
         const int U = reinterpret_cast<const int *>(m)[0];
-        if (tid < (FEM_P2_PAIR ? 2 * U : U)) mb_wait(&mb_p1[k & 1], (unsigned)(k >> 1) & 1u);  // all of tile k's phase 1
+        const int nt2 = FEM_P2_LSPLIT > 0 ? reinterpret_cast<const int *>(m)[3] : 0;  // FEM_P2_LSPLIT tasks
+        if (tid < (FEM_P2_PAIR ? 2 * U : nt2 > 0 ? ((nt2 + 31) & ~31) : U))
+          mb_wait(&mb_p1[k & 1], (unsigned)(k >> 1) & 1u);  // all of tile k's phase 1
         if constexpr (op_has_p2<OP>()) tile_phase2<D, OP, SC>(A, m, U, tile_id(t), tid, cb);
         mb_arrive(&mb_p2[k & 1]);
       }

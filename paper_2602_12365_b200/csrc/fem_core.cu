@@ -25,6 +25,25 @@ fem_status cuda_status(cudaError_t e, const char *what) {
   return e == cudaErrorMemoryAllocation ? FEM_ERR_OUT_OF_MEMORY : FEM_ERR_CUDA;
 }
 
+fem_status pool_alloc(void **ptr, size_t bytes, cudaStream_t s) {
+  static thread_local int configured = -1;  // device whose default pool was configured
+  int dev = 0;
+  FEM_CUDA(cudaGetDevice(&dev));
+  if (configured != dev) {
+    cudaMemPool_t pool;
+    FEM_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
+    uint64_t keep = (uint64_t)16 << 30;  // kPoolKeep: retain up to 16 GiB of freed memory
+    FEM_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
+    configured = dev;
+  }
+  FEM_CUDA(cudaMallocAsync(ptr, bytes > 0 ? bytes : 1, s));
+  return FEM_OK;
+}
+
+void pool_free(void *ptr, cudaStream_t s) {
+  if (ptr) cudaFreeAsync(ptr, s);
+}
+
 fem_status ensure(Workspace &w, size_t bytes) {
   if (w.bytes >= bytes) return FEM_OK;
   if (w.ptr) cudaFree(w.ptr);
@@ -815,6 +834,9 @@ fem_status fem_destroy(fem_problem *h) {
   FEM_NVTX_RANGE("fem_destroy");
   if (!h) return FEM_OK;
   Problem *p = &h->p;
+  // pattern / coloring buffers come from the stream-ordered pool (pool_alloc), for which
+  // cudaFree does not synchronize: finish all work that may still read them first
+  cudaDeviceSynchronize();
   void *bufs[] = {p->coords, p->conn, p->phase, p->lam_tab, p->mu_tab, p->node_bc, p->dir_dofs,
                   p->dir_vals, p->mpc_s, p->mpc_m, p->mpc_b, p->f_ext, p->partials, p->scal,
                   p->d_err, p->inc_ptr, p->inc, p->nadj_ptr, p->nadj, p->dmpc_ptr, p->dmpc,

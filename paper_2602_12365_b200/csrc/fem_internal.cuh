@@ -225,6 +225,18 @@ fem_status cuda_status(cudaError_t e, const char *what);
   } while (0)
 
 fem_status ensure(Workspace &w, size_t bytes);
+// Stream-ordered allocations from the device's default memory pool (cudaMallocAsync), which
+// keeps up to kPoolKeep bytes of freed memory mapped for reuse: the setup paths (pattern,
+// coloring) allocate and free GB-sized buffers per problem, and plain cudaMalloc / cudaFree
+// map and unmap them every time (bench setup medians of fresh problems varied 14-52 ms).
+// Memory from pool_alloc may be released with pool_free (stream-ordered) or cudaFree.
+fem_status pool_alloc(void **ptr, size_t bytes, cudaStream_t s);
+#define FEM_POOL(call)               \
+  do {                               \
+    fem_status fem_pool_st_ = (call); \
+    if (fem_pool_st_) return fem_pool_st_; \
+  } while (0)
+void pool_free(void *ptr, cudaStream_t s);
 fem_status read_error_word(Problem *p, cudaStream_t s);
 
 inline int grid_for(int64_t n, int threads = kThreads, int max_blocks = 148 * 64) {

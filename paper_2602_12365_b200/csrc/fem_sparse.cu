@@ -162,13 +162,13 @@ static fem_status build_incidence(Problem *p, cudaStream_t s) {
   const int64_t n = p->n_elems * p->nen;
   int32_t *idx = nullptr, *keys_out = nullptr;
   int64_t *cnt = nullptr;
-  FEM_CUDA(cudaMalloc(&p->inc_ptr, sizeof(int64_t) * (p->n_nodes + 1)));
-  FEM_CUDA(cudaMalloc(&p->inc, sizeof(int32_t) * (n > 0 ? n : 1)));
-  FEM_CUDA(cudaMalloc(&cnt, sizeof(int64_t) * (p->n_nodes + 1)));
+  FEM_POOL(pool_alloc((void **)&p->inc_ptr, sizeof(int64_t) * (p->n_nodes + 1), s));
+  FEM_POOL(pool_alloc((void **)&p->inc, sizeof(int32_t) * (n > 0 ? n : 1), s));
+  FEM_POOL(pool_alloc((void **)&cnt, sizeof(int64_t) * (p->n_nodes + 1), s));
   FEM_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int64_t) * (p->n_nodes + 1), s));
   if (n > 0) {
-    FEM_CUDA(cudaMalloc(&idx, sizeof(int32_t) * n));
-    FEM_CUDA(cudaMalloc(&keys_out, sizeof(int32_t) * n));
+    FEM_POOL(pool_alloc((void **)&idx, sizeof(int32_t) * n, s));
+    FEM_POOL(pool_alloc((void **)&keys_out, sizeof(int32_t) * n, s));
     k_iota_count<<<grid_for(n), kThreads, 0, s>>>(p->conn, n, idx, cnt);
     int bits = 1;
     while ((int64_t(1) << bits) < p->n_nodes) ++bits;
@@ -182,9 +182,9 @@ static fem_status build_incidence(Problem *p, cudaStream_t s) {
   }
   fem_status st = exclusive_scan(cnt, p->inc_ptr, p->n_nodes + 1, p->tmp, s);
   FEM_CUDA(cudaStreamSynchronize(s));
-  cudaFree(idx);
-  cudaFree(keys_out);
-  cudaFree(cnt);
+  pool_free(idx, s);
+  pool_free(keys_out, s);
+  pool_free(cnt, s);
   return st;
 }
 
@@ -194,58 +194,58 @@ fem_status build_pattern(Problem *p, cudaStream_t s) {
   if (st) return st;
   // node adjacency
   int64_t *cnt = nullptr;
-  FEM_CUDA(cudaMalloc(&cnt, sizeof(int64_t) * (p->n_nodes + 1)));
+  FEM_POOL(pool_alloc((void **)&cnt, sizeof(int64_t) * (p->n_nodes + 1), s));
   FEM_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int64_t) * (p->n_nodes + 1), s));
   k_nadj_count<<<grid_for(p->n_nodes, 128), 128, 0, s>>>(p->inc_ptr, p->inc, p->conn, p->nen,
                                                           p->n_nodes, cnt, p->d_err);
-  FEM_CUDA(cudaMalloc(&p->nadj_ptr, sizeof(int64_t) * (p->n_nodes + 1)));
+  FEM_POOL(pool_alloc((void **)&p->nadj_ptr, sizeof(int64_t) * (p->n_nodes + 1), s));
   st = exclusive_scan(cnt, p->nadj_ptr, p->n_nodes + 1, p->tmp, s);
   if (st) return st;
   int64_t total = 0;
   FEM_CUDA(cudaMemcpyAsync(&total, p->nadj_ptr + p->n_nodes, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
   FEM_CUDA(cudaStreamSynchronize(s));
   st = read_error_word(p, s);
-  if (st) { cudaFree(cnt); return st; }
-  FEM_CUDA(cudaMalloc(&p->nadj, sizeof(int32_t) * (total > 0 ? total : 1)));
+  if (st) { pool_free(cnt, s); return st; }
+  FEM_POOL(pool_alloc((void **)&p->nadj, sizeof(int32_t) * (total > 0 ? total : 1), s));
   k_nadj_fill<<<grid_for(p->n_nodes, 128), 128, 0, s>>>(p->inc_ptr, p->inc, p->conn, p->nen,
                                                          p->n_nodes, p->nadj_ptr, p->nadj);
   // dof -> constraint lists
   if (p->n_mpc) {
     int32_t *dcnt = nullptr, *cursor = nullptr;
-    FEM_CUDA(cudaMalloc(&dcnt, sizeof(int32_t) * (p->n_u + 1)));
-    FEM_CUDA(cudaMalloc(&cursor, sizeof(int32_t) * (p->n_u + 1)));
+    FEM_POOL(pool_alloc((void **)&dcnt, sizeof(int32_t) * (p->n_u + 1), s));
+    FEM_POOL(pool_alloc((void **)&cursor, sizeof(int32_t) * (p->n_u + 1), s));
     FEM_CUDA(cudaMemsetAsync(dcnt, 0, sizeof(int32_t) * (p->n_u + 1), s));
     FEM_CUDA(cudaMemsetAsync(cursor, 0, sizeof(int32_t) * (p->n_u + 1), s));
-    FEM_CUDA(cudaMalloc(&p->dmpc_ptr, sizeof(int32_t) * (p->n_u + 1)));
-    FEM_CUDA(cudaMalloc(&p->dmpc, sizeof(int32_t) * 2 * p->n_mpc));
+    FEM_POOL(pool_alloc((void **)&p->dmpc_ptr, sizeof(int32_t) * (p->n_u + 1), s));
+    FEM_POOL(pool_alloc((void **)&p->dmpc, sizeof(int32_t) * 2 * p->n_mpc, s));
     k_dmpc_count<<<grid_for(p->n_mpc), kThreads, 0, s>>>(p->mpc_s, p->mpc_m, p->n_mpc, dcnt);
     st = exclusive_scan(dcnt, p->dmpc_ptr, p->n_u + 1, p->tmp, s);
     if (st) return st;
     k_dmpc_fill<<<grid_for(p->n_mpc), kThreads, 0, s>>>(p->mpc_s, p->mpc_m, p->n_mpc, p->dmpc_ptr,
                                                         cursor, p->dmpc);
     FEM_CUDA(cudaStreamSynchronize(s));
-    cudaFree(dcnt);
-    cudaFree(cursor);
+    pool_free(dcnt, s);
+    pool_free(cursor, s);
   }
   // rows
   int64_t *len = nullptr;
-  FEM_CUDA(cudaMalloc(&len, sizeof(int64_t) * (p->N + 1)));
+  FEM_POOL(pool_alloc((void **)&len, sizeof(int64_t) * (p->N + 1), s));
   k_row_len<<<grid_for(p->N + 1), kThreads, 0, s>>>(p->nadj_ptr, p->dmpc_ptr, p->n_u, p->N,
                                                      p->dim, len);
-  FEM_CUDA(cudaMalloc(&p->row_ptr, sizeof(int64_t) * (p->N + 1)));
+  FEM_POOL(pool_alloc((void **)&p->row_ptr, sizeof(int64_t) * (p->N + 1), s));
   st = exclusive_scan(len, p->row_ptr, p->N + 1, p->tmp, s);
   if (st) return st;
   FEM_CUDA(cudaMemcpyAsync(&p->nnz, p->row_ptr + p->N, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
   FEM_CUDA(cudaStreamSynchronize(s));
-  FEM_CUDA(cudaMalloc(&p->col_idx, sizeof(int32_t) * (p->nnz > 0 ? p->nnz : 1)));
-  FEM_CUDA(cudaMalloc(&p->diag_pos, sizeof(int64_t) * (p->N > 0 ? p->N : 1)));
+  FEM_POOL(pool_alloc((void **)&p->col_idx, sizeof(int32_t) * (p->nnz > 0 ? p->nnz : 1), s));
+  FEM_POOL(pool_alloc((void **)&p->diag_pos, sizeof(int64_t) * (p->N > 0 ? p->N : 1), s));
   k_row_fill<<<grid_for(p->N), kThreads, 0, s>>>(p->nadj_ptr, p->nadj, p->dmpc_ptr, p->dmpc,
                                                   p->mpc_s, p->mpc_m, p->n_u, p->N, p->dim,
                                                   p->row_ptr, p->col_idx, p->diag_pos);
   FEM_LAUNCH_CHECK("pattern fill");
   FEM_CUDA(cudaStreamSynchronize(s));
-  cudaFree(cnt);
-  cudaFree(len);
+  pool_free(cnt, s);
+  pool_free(len, s);
   p->have_pattern = true;
   return FEM_OK;
 }
@@ -344,9 +344,9 @@ __global__ void k_expand_node_colors(const int32_t *nc, int64_t n_nodes, int dim
 static fem_status greedy_color(Problem *p, const int64_t *gp, const int32_t *gi, int64_t nv,
                                int32_t *colors, int32_t *n_colors, cudaStream_t s) {
   int32_t *cnt = nullptr, *f0 = nullptr, *aux = nullptr;
-  FEM_CUDA(cudaMalloc(&cnt, sizeof(int32_t) * (nv > 0 ? nv : 1)));
-  FEM_CUDA(cudaMalloc(&f0, sizeof(int32_t) * (nv > 0 ? nv : 1)));
-  FEM_CUDA(cudaMalloc(&aux, sizeof(int32_t) * 8));  // sizes[2], done, max_color
+  FEM_POOL(pool_alloc((void **)&cnt, sizeof(int32_t) * (nv > 0 ? nv : 1), s));
+  FEM_POOL(pool_alloc((void **)&f0, sizeof(int32_t) * (nv > 0 ? nv : 1), s));
+  FEM_POOL(pool_alloc((void **)&aux, sizeof(int32_t) * 8, s));  // sizes[2], done, max_color
   FEM_CUDA(cudaMemsetAsync(aux, 0, sizeof(int32_t) * 8, s));
   FEM_CUDA(cudaMemsetAsync(aux + 3, 0xff, sizeof(int32_t), s));  // max_color = -1
   int32_t *sizes = aux, *done = aux + 2, *maxc = aux + 3;
@@ -372,9 +372,9 @@ static fem_status greedy_color(Problem *p, const int64_t *gp, const int32_t *gi,
   int32_t hmax = -1;
   FEM_CUDA(cudaMemcpyAsync(&hmax, maxc, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
   FEM_CUDA(cudaStreamSynchronize(s));
-  cudaFree(cnt);
-  cudaFree(f0);
-  cudaFree(aux);
+  pool_free(cnt, s);
+  pool_free(f0, s);
+  pool_free(aux, s);
   *n_colors = hmax + 1;
   return read_error_word(p, s);
 }
@@ -383,15 +383,15 @@ fem_status build_colors(Problem *p, cudaStream_t s) {
   if (p->have_colors) return FEM_OK;
   fem_status st = build_pattern(p, s);
   if (st) return st;
-  FEM_CUDA(cudaMalloc(&p->colors, sizeof(int32_t) * (p->N > 0 ? p->N : 1)));
+  FEM_POOL(pool_alloc((void **)&p->colors, sizeof(int32_t) * (p->N > 0 ? p->N : 1), s));
   int32_t nc = 0;
   if (p->n_mpc == 0) {
     int32_t *node_colors = nullptr;
-    FEM_CUDA(cudaMalloc(&node_colors, sizeof(int32_t) * p->n_nodes));
+    FEM_POOL(pool_alloc((void **)&node_colors, sizeof(int32_t) * p->n_nodes, s));
     st = greedy_color(p, p->nadj_ptr, p->nadj, p->n_nodes, node_colors, &nc, s);
-    if (st) { cudaFree(node_colors); return st; }
+    if (st) { pool_free(node_colors, s); return st; }
     if (nc * p->dim > FEM_MAX_COLORS) {
-      cudaFree(node_colors);
+      pool_free(node_colors, s);
       set_error("coloring needs more than FEM_MAX_COLORS colors");
       return FEM_ERR_TOO_MANY_COLORS;
     }
@@ -399,7 +399,7 @@ fem_status build_colors(Problem *p, cudaStream_t s) {
                                                                 p->colors);
     FEM_LAUNCH_CHECK("expand colors");
     FEM_CUDA(cudaStreamSynchronize(s));
-    cudaFree(node_colors);
+    pool_free(node_colors, s);
     nc *= p->dim;
   } else {
     st = greedy_color(p, p->row_ptr, p->col_idx, p->N, p->colors, &nc, s);

@@ -130,6 +130,17 @@ namespace fem {
 constexpr int kRtNT = FEM_RT_NT;         // nodes per tile
 constexpr int kRtUnroll = FEM_RT_UNROLL; // entries per unrolled step of the slot sums
 constexpr int kRtThreads = 256;          // 8 warps, 2 nodes per warp per pass
+// threads per CTA of the colored (TR) node tiles.  256-thread CTAs leave 3/4 of the lanes at the
+// barrier with 4-seed tiles (ncu r02: 64 % barrier stalls), but smaller CTAs measured slower
+// (cfg 3, colored Alg. 2: 64 threads 8.65 ms, 128 threads 9.05 / 8.85 ms with 4 / 8 seeds,
+// 64 / 32 threads with 2 seeds 9.23 / 8.77 ms, against 8.28 ms at 256): 256 kept.
+#ifndef FEM_CT_THREADS
+#define FEM_CT_THREADS 256
+#endif
+#ifndef FEM_CT_MINB
+#define FEM_CT_MINB 2
+#endif
+constexpr int rt_threads(bool tr) { return tr ? FEM_CT_THREADS : kRtThreads; }
 constexpr int kRtLPNMax = 32;            // lanes per node: 8 (2D, <= 8 off-diagonal slots), 16 (3D Kuhn,
                                          // <= 16) or 32 (unstructured, 8-node tiles)
 constexpr int kRtMaxSlots = 64;          // off-diagonal slots per node: a lane sums slots ql, ql + LPN, ...
@@ -784,7 +795,7 @@ static fem_status build_tile_plan(Problem *p, const int32_t *order, const std::v
   const size_t recw = soa ? (size_t)kRtSoaF * kRtSoaS : (size_t)RS * (uem + 1);
   const size_t smem = 3 * (size_t)L.mb + 2 * sizeof(double) * 2 * D * (size_t)unm +
                       sizeof(double) * recw +
-                      (FEM_RT_DIAG_SMEM ? sizeof(double) * (kRtThreads / 32) * 32 * BP : 0);
+                      (FEM_RT_DIAG_SMEM ? sizeof(double) * (rt_threads(tr) / 32) * 32 * BP : 0);
   if (hbad || uem >= 1024 || smem > 220 * 1024) {
     cudaFree(d_bad); cudaFree(cnt);
     return FEM_OK;
@@ -879,7 +890,8 @@ struct RtArgs {
 // each seed's column blocks K[m, n] = K[n, m]^T are written at their decompressed CSR slots
 // (row m D + k, column n D + i), conflict-free within a color; the diagonal block as the row form.
 template <int D, int MAT, int LPN, bool TR = false, bool SOA = false>
-__global__ void __launch_bounds__(kRtThreads, FEM_RT_MINB) k_rows_tile(RtArgs A) {
+__global__ void __launch_bounds__(rt_threads(TR), TR ? FEM_CT_MINB : FEM_RT_MINB) k_rows_tile(RtArgs A) {
+  constexpr int NTH = rt_threads(TR);
   using Gm = RtGeom<D>;
   constexpr int NEN = Gm::NEN, BS = Gm::BS, RS = Gm::RS;
   static_assert(!SOA || (D == 3 && LPN == 16 && !TR), "SoA records: 3D row form, 16 lanes");
@@ -895,7 +907,7 @@ __global__ void __launch_bounds__(kRtThreads, FEM_RT_MINB) k_rows_tile(RtArgs A)
   // AoS: [uem + 1][RS] (the last one the zero record of idle steps); SoA: [kRtSoaF][S]
   double *scratch = rec + (SOA ? (size_t)kRtSoaF * S : (size_t)(L.uem + 1) * RS);  // [8 warps][32][BP]
   if (!SOA)
-    for (int q = tid; q < RS; q += kRtThreads) rec[(size_t)L.uem * RS + q] = 0.0;  // zero record
+    for (int q = tid; q < RS; q += NTH) rec[(size_t)L.uem * RS + q] = 0.0;  // zero record
   const int64_t G = gridDim.x;
 
   __shared__ __align__(8) uint64_t mb_meta[3];
@@ -914,7 +926,7 @@ __global__ void __launch_bounds__(kRtThreads, FEM_RT_MINB) k_rows_tile(RtArgs A)
         bulk_g2s(dst, src, (unsigned)mb, &mb_meta[b]);
       }
     } else {
-      for (int off = tid * 16; off < mb; off += kRtThreads * 16) rt_cp16(dst + off, src + off);
+      for (int off = tid * 16; off < mb; off += NTH * 16) rt_cp16(dst + off, src + off);
     }
   };
   // wait for the metadata of the k-th tile of this CTA (buffer k % 3, use k / 3)
@@ -925,7 +937,7 @@ __global__ void __launch_bounds__(kRtThreads, FEM_RT_MINB) k_rows_tile(RtArgs A)
     const int un = reinterpret_cast<const int *>(m)[1];
     const int32_t *hid = reinterpret_cast<const int32_t *>(m + L.off_halo);
     if (FEM_RT_ISSUE_NODE) {  // one thread per halo node: D copies of x and of z each
-      for (int r = tid; r < un; r += kRtThreads) {
+      for (int r = tid; r < un; r += NTH) {
         const int64_t g = (int64_t)hid[r] * D;
 #pragma unroll
         for (int c = 0; c < D; ++c) {
@@ -934,7 +946,7 @@ __global__ void __launch_bounds__(kRtThreads, FEM_RT_MINB) k_rows_tile(RtArgs A)
         }
       }
     } else {
-      for (int i = tid; i < un * D; i += kRtThreads) {
+      for (int i = tid; i < un * D; i += NTH) {
         const int64_t g = (int64_t)hid[i / D] * D + (i % D);
         rt_cp8(dst + i, A.coords + g);
         rt_cp8(dst + unm * D + i, A.z + g);
@@ -968,7 +980,7 @@ __global__ void __launch_bounds__(kRtThreads, FEM_RT_MINB) k_rows_tile(RtArgs A)
     const int nn = reinterpret_cast<const int *>(m)[2];
     // ---- 1: element contexts
     const uint16_t *lc = reinterpret_cast<const uint16_t *>(m + L.off_lc);
-    for (int e = tid; e < (FEM_RT_DIAG_SKIP == 1 ? 0 : ue); e += kRtThreads) {
+    for (int e = tid; e < (FEM_RT_DIAG_SKIP == 1 ? 0 : ue); e += NTH) {
       const ushort4 l4 = reinterpret_cast<const ushort4 *>(lc)[e];
       if (l4.x == 0xffff) continue;  // placement hole (no entry reads it)
       const int li[4] = {l4.x, l4.y, l4.z, l4.w};
@@ -1045,7 +1057,7 @@ __global__ void __launch_bounds__(kRtThreads, FEM_RT_MINB) k_rows_tile(RtArgs A)
     constexpr int NPW = 32 / LPN;
     const int h = lane / LPN, ql = lane % LPN;
     const int4 *ndw = reinterpret_cast<const int4 *>(m + L.off_nd);
-    for (int j = NPW * w + h; j < (FEM_RT_DIAG_SKIP == 2 ? 0 : L.nt); j += NPW * (kRtThreads / 32)) {
+    for (int j = NPW * w + h; j < (FEM_RT_DIAG_SKIP == 2 ? 0 : L.nt); j += NPW * (NTH / 32)) {
       const int4 nd = ndw[j];
       const int sno = nd.y & 0xff, sn = (nd.y >> 8) & 0xff, ds = (nd.y >> 16) & 0xff;
       const unsigned bcn = A.bc ? ((unsigned)nd.y >> 24) : 0u;
@@ -1253,13 +1265,13 @@ static fem_status launch_plan(Problem *p, const RtPlan &P, int64_t t0, int64_t t
               : (lpn == 16 ? k_rows_tile<3, FEM_NEO_HOOKEAN, 16, TR> : k_rows_tile<3, FEM_NEO_HOOKEAN, 32, TR>);
   FEM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, P.smem));
   int per_sm = 0;
-  FEM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kRtThreads, P.smem));
+  FEM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, rt_threads(TR), P.smem));
   int dev = 0, sms = 148;
   FEM_CUDA(cudaGetDevice(&dev));
   FEM_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   int64_t grid = (int64_t)sms * (per_sm > 0 ? per_sm : 1);
   if (grid > tiles) grid = tiles;
-  kern<<<(int)grid, kRtThreads, P.smem, s>>>(A);
+  kern<<<(int)grid, rt_threads(TR), P.smem, s>>>(A);
   FEM_LAUNCH_CHECK("node-tile assembly");
   return FEM_OK;
 }

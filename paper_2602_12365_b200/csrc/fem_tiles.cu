@@ -104,6 +104,12 @@
 #ifndef FEM_P2_LSPLIT
 #define FEM_P2_LSPLIT 0
 #endif
+// Experiment (A/B only): phase 1 RED-adds each element's nodal contributions straight to the
+// output (global fp64 atomics; the node data still staged per tile) and phase 2 is skipped —
+// measures the price of global REDs against the tile reduction's node sums and barrier.
+#ifndef FEM_P1_RED
+#define FEM_P1_RED 0
+#endif
 #ifndef FEM_P2_UNROLL
 #define FEM_P2_UNROLL 1
 #endif
@@ -909,7 +915,9 @@ __host__ __device__ constexpr int sym_idx(int a, int b, int D) {  // upper-trian
   return a <= b ? a * D - a * (a - 1) / 2 + (b - a) : b * D - b * (b - 1) / 2 + (a - b);
 }
 template <int OP>
-constexpr bool op_has_p2() { return base_op<OP>() == OP_RESIDUAL || op_is_hvp<OP>(); }
+constexpr bool op_has_p2() { return !FEM_P1_RED && (base_op<OP>() == OP_RESIDUAL || op_is_hvp<OP>()); }
+template <int OP>
+constexpr bool op_scatters() { return base_op<OP>() == OP_RESIDUAL || op_is_hvp<OP>(); }
 template <int OP, int MAT>
 constexpr bool op_needs_u() {
   return OP == OP_ENERGY || base_op<OP>() == OP_RESIDUAL || OP == OP_LIN ||
@@ -1305,19 +1313,27 @@ __device__ __forceinline__ void tile_phase1(const PipeArgs &A, const unsigned ch
       }
     }
     if (!ok) atomicOr(A.err, ERRW_INVERTED);
-    if constexpr (op_has_p2<OP>()) {
+    if constexpr (op_scatters<OP>()) {
       if constexpr (!SPATIAL && !SPATIAL_R && !NO_GEOM) nodal_from_c<D>(S, c, f);
+      if constexpr (FEM_P1_RED) {
+        const int32_t *nodes = reinterpret_cast<const int32_t *>(m + A.off_nodes);
 #pragma unroll
-      for (int a = 0; a < NEN; ++a)
+        for (int a = 0; a < NEN; ++a)
 #pragma unroll
-        for (int i = 0; i < D; ++i) {
-          if constexpr (FEM_P2_NM) {  // node-major: at the incidence's list position
-            const int q = reinterpret_cast<const uint16_t *>(m + A.off_inc)[tid * 4 + a];
-            cb[q * D + i] = ok ? f[a][i] : 0.0;
-          } else {
-            cb[(a * D + i) * kCbStride + tid] = ok ? f[a][i] : 0.0;
+          for (int i = 0; i < D; ++i) atomicAdd(A.out + (int64_t)nodes[lc[a]] * D + i, f[a][i]);
+      } else {
+#pragma unroll
+        for (int a = 0; a < NEN; ++a)
+#pragma unroll
+          for (int i = 0; i < D; ++i) {
+            if constexpr (FEM_P2_NM) {  // node-major: at the incidence's list position
+              const int q = reinterpret_cast<const uint16_t *>(m + A.off_inc)[tid * 4 + a];
+              cb[q * D + i] = ok ? f[a][i] : 0.0;
+            } else {
+              cb[(a * D + i) * kCbStride + tid] = ok ? f[a][i] : 0.0;
+            }
           }
-        }
+      }
     }
   }
 }

@@ -25,7 +25,16 @@ fem_status cuda_status(cudaError_t e, const char *what) {
   return e == cudaErrorMemoryAllocation ? FEM_ERR_OUT_OF_MEMORY : FEM_ERR_CUDA;
 }
 
+static bool pool_disabled() {  // FEM_NO_POOL=1: plain cudaMalloc / cudaFree (A/B)
+  static const bool off = getenv("FEM_NO_POOL") != nullptr;
+  return off;
+}
+
 fem_status pool_alloc(void **ptr, size_t bytes, cudaStream_t s) {
+  if (pool_disabled()) {
+    FEM_CUDA(cudaMalloc(ptr, bytes > 0 ? bytes : 1));
+    return FEM_OK;
+  }
   static thread_local int configured = -1;  // device whose default pool was configured
   int dev = 0;
   FEM_CUDA(cudaGetDevice(&dev));
@@ -41,7 +50,9 @@ fem_status pool_alloc(void **ptr, size_t bytes, cudaStream_t s) {
 }
 
 void pool_free(void *ptr, cudaStream_t s) {
-  if (ptr) cudaFreeAsync(ptr, s);
+  if (!ptr) return;
+  if (pool_disabled()) cudaFree(ptr);
+  else cudaFreeAsync(ptr, s);
 }
 
 fem_status ensure(Workspace &w, size_t bytes) {

@@ -334,6 +334,69 @@ __global__ void __launch_bounds__(128) k_color_apply(const int64_t *gp, const in
   }
 }
 
+// Push form (FEM_COLOR_PUSH): the thread whose decrement brings a higher neighbour's counter
+// to zero appends it to the next round's frontier, so no round rescans all vertices (the
+// select kernel above reads cnt and colors of every vertex every round).  Frontiers alternate
+// between two buffers; three size counters rotate (round t reads sizes[t % 3], appends to
+// sizes[(t + 1) % 3] and clears sizes[(t + 2) % 3], which no kernel of round t touches).  Each
+// counter reaches zero exactly once (decrements and the initial count use the same
+// multiplicities), and the colors are the same as the sequential greedy's: a vertex is colored
+// only after all its lower distance-2 neighbours, whatever the round.  Measured (r02, cfg 3,
+// 10.3M DOFs, bit-exact 90 colors): 34.4 ms against 33.1 ms for select + apply — the rounds
+// are bound by the distance-2 enumeration of the frontier, not by the scan; off.
+#ifndef FEM_COLOR_PUSH
+#define FEM_COLOR_PUSH 0
+#endif
+__global__ void __launch_bounds__(128) k_color_apply_push(const int64_t *gp, const int32_t *gi,
+                                                          int32_t *cnt, int32_t *colors,
+                                                          const int32_t *frontier, int32_t *next,
+                                                          int32_t *sizes, int t3, int32_t *done,
+                                                          int *err, int32_t *max_color) {
+  const int32_t n_cur = sizes[t3];
+  int32_t *n_next = sizes + (t3 + 1) % 3;
+  if (blockIdx.x == 0 && threadIdx.x == 0) sizes[(t3 + 2) % 3] = 0;
+  const int lane = threadIdx.x & 31;
+  const int32_t warps = gridDim.x * (blockDim.x >> 5);
+  for (int32_t w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < n_cur; w += warps) {
+    const int32_t j = frontier[w];
+    const int64_t p0 = gp[j], p1 = gp[j + 1];
+    uint32_t fb[FEM_MAX_COLORS / 32];
+#pragma unroll
+    for (int q = 0; q < FEM_MAX_COLORS / 32; ++q) fb[q] = 0u;
+    for (int64_t p = p0 + lane; p < p1; p += 32) {
+      const int32_t r = gi[p];
+      for (int64_t q = gp[r]; q < gp[r + 1]; ++q) {
+        const int32_t k = gi[q];
+        if (k < j) {
+          const int32_t c = colors[k];
+          fb[c >> 5] |= 1u << (c & 31);
+        }
+      }
+    }
+    int32_t c = -1;
+#pragma unroll
+    for (int q = 0; q < FEM_MAX_COLORS / 32; ++q) {
+      const uint32_t m = __reduce_or_sync(0xffffffffu, fb[q]);
+      if (c < 0 && m != 0xffffffffu) c = q * 32 + __ffs(~m) - 1;
+    }
+    if (lane == 0) {
+      if (c < 0) { atomicOr(err, ERRW_TOO_MANY_COLORS); c = FEM_MAX_COLORS - 1; }
+      colors[j] = c;
+      atomicMax(max_color, c);
+      atomicAdd(done, 1);
+    }
+    // the counters are decremented only after colors[j] is written: a vertex pushed by this
+    // warp reads colors[j] in a later round (kernel boundary), so no fence is needed
+    for (int64_t p = p0 + lane; p < p1; p += 32) {
+      const int32_t r = gi[p];
+      for (int64_t q = gp[r]; q < gp[r + 1]; ++q) {
+        const int32_t k = gi[q];
+        if (k > j && atomicSub(cnt + k, 1) == 1) next[atomicAdd(n_next, 1)] = k;
+      }
+    }
+  }
+}
+
 __global__ void k_expand_node_colors(const int32_t *nc, int64_t n_nodes, int dim, int32_t *colors) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_nodes * dim;
        i += (int64_t)gridDim.x * blockDim.x)
@@ -345,8 +408,9 @@ static fem_status greedy_color(Problem *p, const int64_t *gp, const int32_t *gi,
                                int32_t *colors, int32_t *n_colors, cudaStream_t s) {
   int32_t *cnt = nullptr, *f0 = nullptr, *aux = nullptr;
   FEM_POOL(pool_alloc((void **)&cnt, sizeof(int32_t) * (nv > 0 ? nv : 1), s));
-  FEM_POOL(pool_alloc((void **)&f0, sizeof(int32_t) * (nv > 0 ? nv : 1), s));
-  FEM_POOL(pool_alloc((void **)&aux, sizeof(int32_t) * 8, s));  // sizes[2], done, max_color
+  // select form: one frontier; push form: two alternating frontiers
+  FEM_POOL(pool_alloc((void **)&f0, sizeof(int32_t) * (FEM_COLOR_PUSH ? 2 : 1) * (nv > 0 ? nv : 1), s));
+  FEM_POOL(pool_alloc((void **)&aux, sizeof(int32_t) * 8, s));  // sizes[2], done, max_color, push sizes[3]
   FEM_CUDA(cudaMemsetAsync(aux, 0, sizeof(int32_t) * 8, s));
   FEM_CUDA(cudaMemsetAsync(aux + 3, 0xff, sizeof(int32_t), s));  // max_color = -1
   int32_t *sizes = aux, *done = aux + 2, *maxc = aux + 3;
@@ -355,11 +419,24 @@ static fem_status greedy_color(Problem *p, const int64_t *gp, const int32_t *gi,
   int32_t h_done = 0;
   const int kCheck = 32;
   const int sel_grid = grid_for(nv, kThreads, 148 * 16);
+  // push form: sizes[0..2] rotate (aux[0], aux[1], aux[4]); round 0's frontier by one select
+  int32_t *psz = aux + 4;  // [3]
+  if (FEM_COLOR_PUSH) {
+    FEM_CUDA(cudaMemsetAsync(psz, 0, sizeof(int32_t) * 3, s));
+    k_color_select<<<sel_grid, kThreads, 0, s>>>(cnt, colors, nv, f0, psz);
+  }
   for (int t = 0; h_done < nv;) {
     for (int q = 0; q < kCheck; ++q, ++t) {
-      const int slot = t & 1;
-      k_color_select<<<sel_grid, kThreads, 0, s>>>(cnt, colors, nv, f0, sizes + slot);
-      k_color_apply<<<148 * 4, 128, 0, s>>>(gp, gi, cnt, colors, f0, sizes, slot, done, p->d_err, maxc);
+      if (FEM_COLOR_PUSH) {
+        const int32_t *fin = f0 + (t & 1) * (nv > 0 ? nv : 1);
+        int32_t *fout = f0 + ((t + 1) & 1) * (nv > 0 ? nv : 1);
+        k_color_apply_push<<<148 * 4, 128, 0, s>>>(gp, gi, cnt, colors, fin, fout, psz, t % 3, done,
+                                                   p->d_err, maxc);
+      } else {
+        const int slot = t & 1;
+        k_color_select<<<sel_grid, kThreads, 0, s>>>(cnt, colors, nv, f0, sizes + slot);
+        k_color_apply<<<148 * 4, 128, 0, s>>>(gp, gi, cnt, colors, f0, sizes, slot, done, p->d_err, maxc);
+      }
     }
     FEM_LAUNCH_CHECK("color round");
     FEM_CUDA(cudaMemcpyAsync(&h_done, done, sizeof(int32_t), cudaMemcpyDeviceToHost, s));

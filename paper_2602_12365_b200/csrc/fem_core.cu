@@ -851,7 +851,7 @@ fem_status fem_destroy(fem_problem *h) {
   void *bufs[] = {p->coords, p->conn, p->phase, p->lam_tab, p->mu_tab, p->node_bc, p->dir_dofs,
                   p->dir_vals, p->mpc_s, p->mpc_m, p->mpc_b, p->f_ext, p->partials, p->scal,
                   p->d_err, p->inc_ptr, p->inc, p->nadj_ptr, p->nadj, p->dmpc_ptr, p->dmpc,
-                  p->row_ptr, p->col_idx, p->diag_pos, p->slot_list, p->slot_off, p->node_order, p->rp_node, p->epos, p->rp_ent, p->rt.meta, p->ct.meta, p->rp_soff, p->rp_sbc, p->colors, p->jcomp.ptr, p->cgbuf.ptr, p->slotbuf.ptr, p->ctxbuf.ptr,
+                  p->row_ptr, p->col_idx, p->diag_pos, p->slot_list, p->slot_off, p->node_order, p->rp_node, p->epos, p->rp_ent, p->rt.meta, p->ct.meta, p->rp_soff, p->rp_sbc, p->colors, p->jcomp.ptr, p->cgbuf.ptr, p->slotbuf.ptr, p->ctxbuf.ptr, p->nwbuf.ptr,
                   p->tmp.ptr};
   for (void *b : bufs)
     if (b) cudaFree(b);

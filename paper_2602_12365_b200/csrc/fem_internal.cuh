@@ -175,7 +175,7 @@ struct Problem {
   int32_t n_colors = -1;
   int32_t *colors = nullptr;    // [N]
   // workspaces
-  Workspace jcomp, cgbuf, tmp, slotbuf, ctxbuf;
+  Workspace jcomp, cgbuf, tmp, slotbuf, ctxbuf, nwbuf;  // nwbuf: Newton r, dz (+ CSR values)
   cudaStream_t cap_stream = nullptr;  // CUDA-graph capture of solver iterations
   int spmv_lpn = 0;             // node-block SpMV lanes per node (0 unset, -1 plain CSR)
   // element coloring for FEM_COLORED_SCATTER (fem_core.cu build_elem_colors): elements of

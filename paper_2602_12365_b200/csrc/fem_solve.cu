@@ -610,11 +610,14 @@ fem_status fem_newton_solve(fem_problem *h, double *z, const fem_newton_opts *o,
     st = build_colors(p, s);
     if (st) return st;
   }
-  // 2 vectors (+ the CSR values: 3.7 GB at cfg 3) from the stream-ordered pool: a plain
-  // cudaMalloc / cudaFree of that size per solve cost 0.1-1.3 s of host time (r02, cfg 3
-  // CSR Newton wall times 2.8-4.2 s for the same 2,800 CG iterations)
+  // 2 vectors (+ the CSR values: 3.7 GB at cfg 3) in a problem-owned workspace, allocated by the
+  // first solve and kept: a cudaMalloc / cudaFree of that size per solve cost 0.1-1.3 s of host
+  // time (r02, cfg 3 CSR Newton wall times 2.8-4.2 s for the same 2,800 CG iterations), and a
+  // pool allocation paid the pool's growth in the first CSR solve after other large buffers
   const size_t bytes = sizeof(double) * (2 * n + (csr ? p->nnz : 0));
-  FEM_POOL(pool_alloc((void **)&buf, bytes, s));
+  st = ensure(p->nwbuf, bytes);
+  if (st) return st;
+  buf = (double *)p->nwbuf.ptr;
   double *r = buf, *dz = buf + n, *vals = csr ? buf + 2 * n : nullptr;
   rep->iters = rep->cg_iters = rep->converged = 0;
   double r0 = 0.0, r_prev = 0.0, eta_prev = 0.0;
@@ -676,7 +679,6 @@ fem_status fem_newton_solve(fem_problem *h, double *z, const fem_newton_opts *o,
     k_add<<<grid_for(n), kThreads, 0, s>>>(z, dz, n);
   }
   rep->res0 = r0;
-  pool_free(buf, s);
   cudaStreamSynchronize(s);
   return result;
 }

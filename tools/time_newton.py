@@ -21,7 +21,7 @@ z0 = torch.as_tensor(fi.lift(mesh, fi.affine_field(mesh, np.diag([eps, 0.0, 0.0]
 prob.nnz()
 prob.color()
 out = []
-for op, jac, forcing in ((1, True, 0.9), (1, True, 0.0), (0, False, 0.9), (1, True, 0.9)):
+for op, jac, forcing in ((0, False, 0.0), (1, True, 0.0), (0, False, 0.9), (1, True, 0.9)):
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     z, info = prob.newton_solve(z0, op=op, jacobi=jac, cg_rtol=1e-8, rtol=1e-10, atol=1e-14,

@@ -431,6 +431,29 @@ def test_row_tiles_32_lanes(fem, oracle_mod, monkeypatch):
             assert rel(vals, oracle_mod.Oracle(mesh).assemble_alg2(z, bc=bc)) <= TOL
 
 
+def test_row_tiles_soa_records(fem, oracle_mod, monkeypatch):
+    """The conflict-free SoA record layout of the 3D node tiles (FEM_RT_SOA=1 at run time:
+    4-colored tile elements, color-distinct co-schedules from first fit or the plan's
+    depth-first search, idle steps without loads) against the oracle's Alg. 2 CSR, with and
+    without BC, on the structured, shuffled and LE 3D meshes; 2D meshes keep the odd-stride
+    records."""
+    monkeypatch.setenv("FEM_RT_SOA", "1")
+    for name in ("3d-nh", "3d-le", "3d-nh-shuffled", "2d-nh-roller"):
+        mesh = MESHES[name]
+        z = fi.lift(mesh, fi.generic_state(mesh, 1))
+        prob = fem.Problem(mesh)
+        for bc in (False, True):
+            vals = prob.assemble_csr(dev(z), bc=bc, mode="rows")
+            assert rel(vals, oracle_mod.Oracle(mesh).assemble_alg2(z, bc=bc)) <= TOL
+    mesh = fi.config_mesh(3, n=24)  # several hundred tiles: the plan's DFS co-schedules run
+    z = fi.lift(mesh, fi.generic_state(mesh, 2))
+    monkeypatch.setenv("FEM_RT_SOA", "0")
+    ref = fem.Problem(mesh).assemble_csr(dev(z), bc=True, mode="rows")
+    monkeypatch.setenv("FEM_RT_SOA", "1")
+    vals = fem.Problem(mesh).assemble_csr(dev(z), bc=True, mode="rows")
+    assert rel(vals, ref.cpu().numpy()) <= TOL
+
+
 def test_cg_graph_batches_match_direct_launches(fem, monkeypatch):
     """CG iterations between host checks run as a captured CUDA graph (check_every >= 2);
     with the deterministic CSR operator the iterates equal the directly launched ones bit

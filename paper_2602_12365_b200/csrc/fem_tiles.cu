@@ -1370,7 +1370,8 @@ __device__ __forceinline__ void node_write(const PipeArgs &A, const unsigned cha
 // node from precomputed offsets; the g lanes of a node combine by a shuffle tree.
 template <int D, int OP, int SC>
 __device__ __forceinline__ void tile_phase2(const PipeArgs &A, const unsigned char *m, int U,
-                                            int64_t t, int tid, const double *cb) {
+                                            int64_t t, int tid, const double *cb,
+                                            int /*nth: default variant only*/ = kTile) {
   const uint32_t hdr = reinterpret_cast<const uint32_t *>(m)[2];
   const int rounds = hdr & 0xff, steps = (hdr >> 8) & 0xff;
   const uint4 *so = reinterpret_cast<const uint4 *>(m + A.off_soff);
@@ -1413,7 +1414,8 @@ __device__ __forceinline__ void tile_phase2(const PipeArgs &A, const unsigned ch
 #elif FEM_P2_NM
 template <int D, int OP, int SC>
 __device__ __forceinline__ void tile_phase2(const PipeArgs &A, const unsigned char *m, int U,
-                                            int64_t t, int tid, const double *cb) {
+                                            int64_t t, int tid, const double *cb,
+                                            int /*nth: default variant only*/ = kTile) {
   const uint16_t *ptr = reinterpret_cast<const uint16_t *>(m + A.off_ptr);
   for (int r = tid; r < U; r += kTile) {  // one thread per tile node: a contiguous run
     const int lo = ptr[r], hi = ptr[r + 1];
@@ -1444,7 +1446,8 @@ __device__ __forceinline__ void tile_phase2(const PipeArgs &A, const unsigned ch
 // (16-byte loads), pad entries point at the zero columns; two interleaved partial sums.
 template <int D, int OP, int SC>
 __device__ __forceinline__ void tile_phase2(const PipeArgs &A, const unsigned char *m, int U,
-                                            int64_t t, int tid, const double *cb) {
+                                            int64_t t, int tid, const double *cb,
+                                            int /*nth: default variant only*/ = kTile) {
   const uint16_t *ptr = reinterpret_cast<const uint16_t *>(m + A.off_ptr);
   const uint4 *grp = reinterpret_cast<const uint4 *>(m + A.off_inc);
   for (int r = tid; r < U; r += kTile) {
@@ -1478,7 +1481,8 @@ __device__ __forceinline__ void tile_phase2(const PipeArgs &A, const unsigned ch
 // node sums instead of ceil(U / 32) of them (the critical path before the next tile's barrier).
 template <int D, int OP, int SC>
 __device__ __forceinline__ void tile_phase2(const PipeArgs &A, const unsigned char *m, int U,
-                                            int64_t t, int tid, const double *cb) {
+                                            int64_t t, int tid, const double *cb,
+                                            int /*nth: default variant only*/ = kTile) {
   const uint16_t *ptr = reinterpret_cast<const uint16_t *>(m + A.off_ptr);
   const uint16_t *inc = reinterpret_cast<const uint16_t *>(m + A.off_inc);
   for (int base = 0; base < 2 * U; base += kTile) {  // uniform over the CTA (shuffles)
@@ -1910,7 +1914,7 @@ __global__ void __launch_bounds__(kTile + kWsProd, 2) k_tile_ws(PipeArgs A) {
   constexpr int UOFF = NEED_X ? 1 : 0;
   constexpr int CB = (D + 1) * D * kCbStride;
   constexpr int NCB = FEM_WS_CB;
-  static_assert(!FEM_P2_BAL && !FEM_P2_NM && !FEM_P2_G8 && !FEM_P2_PAIR, "FEM_WS: default phase 2");
+  static_assert(!FEM_WS || (!FEM_P2_BAL && !FEM_P2_NM && !FEM_P2_G8 && !FEM_P2_PAIR), "FEM_WS: default phase 2");
   extern __shared__ __align__(128) unsigned char sm[];
   __shared__ __align__(8) uint64_t mb_meta[3], mb_node[2], mb_full[NCB], mb_empty[NCB];
   const int tid = threadIdx.x;

@@ -94,6 +94,10 @@ struct TileSet {
   uint8_t *meta = nullptr;
   int um = 0, mb = 0, off_nodes = 0, off_lconn = 0, off_ptr = 0, off_inc = 0, off_int = 0,
       off_bc = 0, off_ph = 0, off_soff = 0, off_smeta = 0, off_perm = 0;
+  // second metadata layout for the HVP kernels (FEM_HVP_G8): incidence offsets in padded groups
+  // of 8 (the G8 node sums); nodes / lconn / ptr at the default offsets
+  uint8_t *meta_g8 = nullptr;
+  int mb_g8 = 0, off_inc_g8 = 0, off_int_g8 = 0, off_bc_g8 = 0, off_ph_g8 = 0, off_perm_g8 = 0;
   uint16_t *p2perm = nullptr;    // [n_tiles][maxe] phase-2 thread -> tile node (FEM_P2_SORT) or task (FEM_P2_LSPLIT)
   int32_t *p2n = nullptr;        // [n_tiles] phase-2 task count (FEM_P2_LSPLIT)
   int pcap = 0;                  // phase-2 order / task entries per metadata block

@@ -110,6 +110,18 @@
 #ifndef FEM_P1_RED
 #define FEM_P1_RED 0
 #endif
+// G8 node sums (padded groups of 8 incidence offsets, 16-byte loads) for the HVP kernels only,
+// from a second metadata layout, the other operators keeping the default node sums.  Measured
+// (r02, cfg 3, device-timed medians): G8 everywhere gave HVP 0.901 vs 0.924 ms but residual
+// 0.842 vs 0.803 (the residual runs 3 CTAs/SM at 80 registers); HVP only: 0.902 / 0.903 vs
+// 0.927 / 0.926 ms, residual unchanged; the linearized HVP stays on the default sums (G8:
+// 0.961 vs 0.737 ms).
+#ifndef FEM_WS  // warp-specialized tile kernels (k_tile_ws below)
+#define FEM_WS 0
+#endif
+#ifndef FEM_HVP_G8
+#define FEM_HVP_G8 1
+#endif
 #ifndef FEM_P2_UNROLL
 #define FEM_P2_UNROLL 1
 #endif
@@ -129,6 +141,7 @@ namespace fem {
 // row stride of the per-tile contribution array cb[(a D + c)][kCbStride]: G8 appends 8 zero
 // columns (the pad entries of the incidence groups point there)
 constexpr int kCbStride = FEM_P2_G8 ? kTile + 8 : kTile;
+constexpr int kCbStrideG8 = kTile + 8;  // contribution rows of the G8 node sums (8 zero pad columns)
 constexpr int kP2Unroll = FEM_P2_UNROLL;
 static_assert(!(FEM_P2_G8 && FEM_P2_BAL), "FEM_P2_G8 and FEM_P2_BAL are alternatives");
 static_assert(!(FEM_P2_NM && (FEM_P2_G8 || FEM_P2_BAL)), "FEM_P2_NM is an alternative phase 2");
@@ -739,7 +752,7 @@ __global__ void k_g8_fill(TileSet T, int me8, uint16_t *inc8, uint16_t *ptr8) {
     const int lo = ptr[r], n = ptr[r + 1] - lo, n8 = (n + 7) & ~7;
     for (int q = 0; q < n8; ++q) {
       const int e = q < n ? inc[lo + q] : -1;
-      o[w + q] = e < 0 ? (uint16_t)kTile : (uint16_t)((e & 3) * D * kCbStride + (e >> 2));
+      o[w + q] = e < 0 ? (uint16_t)kTile : (uint16_t)((e & 3) * D * kCbStrideG8 + (e >> 2));
     }
     w += n8;
   }
@@ -828,6 +841,49 @@ fem_status pack_tile_meta(Problem *p, cudaStream_t s) {
   if (p->dim == 2) k_pack_meta<2><<<(unsigned)T.n_tiles, 256, 0, s>>>(T, p->node_bc, p->n_elems);
   else k_pack_meta<3><<<(unsigned)T.n_tiles, 256, 0, s>>>(T, p->node_bc, p->n_elems);
   FEM_LAUNCH_CHECK("pack tile meta");
+  if (FEM_HVP_G8 && !FEM_P2_G8 && !FEM_P2_BAL && !FEM_P2_NM && !FEM_P2_PAIR && !FEM_WS && !T.meta_g8) {
+    // HVP metadata with the incidences in padded groups of 8 (k_g8_fill), packed by
+    // k_pack_meta from a copy of the tile set carrying the G8 layout
+    int *d_max = nullptr, h_max = 0;
+    FEM_CUDA(cudaMalloc(&d_max, sizeof(int)));
+    FEM_CUDA(cudaMemsetAsync(d_max, 0, sizeof(int), s));
+    const unsigned g = (unsigned)((T.n_tiles + 127) / 128);
+    k_g8_count<<<g, 128, 0, s>>>(T, d_max);
+    FEM_CUDA(cudaMemcpyAsync(&h_max, d_max, sizeof(int), cudaMemcpyDeviceToHost, s));
+    FEM_CUDA(cudaStreamSynchronize(s));
+    cudaFree(d_max);
+    TileSet T2 = T;
+    T2.me8 = round_up(std::max(h_max, 8), 8);
+    FEM_CUDA(cudaMalloc(&T2.inc8, sizeof(uint16_t) * (size_t)T2.me8 * T.n_tiles));
+    FEM_CUDA(cudaMalloc(&T2.ptr8, sizeof(uint16_t) * (size_t)(T.um + 1) * T.n_tiles));
+    if (p->dim == 3) k_g8_fill<3><<<g, 128, 0, s>>>(T2, T2.me8, T2.inc8, T2.ptr8);
+    else k_g8_fill<2><<<g, 128, 0, s>>>(T2, T2.me8, T2.inc8, T2.ptr8);
+    FEM_LAUNCH_CHECK("phase-2 incidence groups (HVP)");
+    T2.p2perm = nullptr;
+    T2.p2n = nullptr;
+    T2.pcap = 0;
+    T2.shdr = nullptr;
+    T2.off_inc = T.off_ptr + round_up(2 * (T.um + 1), 16);
+    T2.off_int = T2.off_inc + round_up(2 * T2.me8, 16);
+    T2.off_bc = T2.off_int + round_up(T.um, 16);
+    T2.off_ph = T2.off_bc + round_up(T.um, 16);
+    T2.off_perm = round_up(T2.off_ph + (T.phase ? kTile : 0), 16);
+    T2.mb = round_up(T2.off_perm, 16);
+    FEM_CUDA(cudaMalloc(&T2.meta, (size_t)T2.mb * T.n_tiles));
+    if (p->dim == 2) k_pack_meta<2><<<(unsigned)T.n_tiles, 256, 0, s>>>(T2, p->node_bc, p->n_elems);
+    else k_pack_meta<3><<<(unsigned)T.n_tiles, 256, 0, s>>>(T2, p->node_bc, p->n_elems);
+    FEM_LAUNCH_CHECK("pack tile meta (HVP)");
+    FEM_CUDA(cudaStreamSynchronize(s));
+    cudaFree(T2.inc8);
+    cudaFree(T2.ptr8);
+    T.meta_g8 = T2.meta;
+    T.mb_g8 = T2.mb;
+    T.off_inc_g8 = T2.off_inc;
+    T.off_int_g8 = T2.off_int;
+    T.off_bc_g8 = T2.off_bc;
+    T.off_ph_g8 = T2.off_ph;
+    T.off_perm_g8 = T2.off_perm;
+  }
   if (T.inc8) {
     FEM_CUDA(cudaStreamSynchronize(s));
     cudaFree(T.inc8); cudaFree(T.ptr8);
@@ -918,6 +974,16 @@ template <int OP>
 constexpr bool op_has_p2() { return !FEM_P1_RED && (base_op<OP>() == OP_RESIDUAL || op_is_hvp<OP>()); }
 template <int OP>
 constexpr bool op_scatters() { return base_op<OP>() == OP_RESIDUAL || op_is_hvp<OP>(); }
+// the G8 node sums: every phase-2 op with FEM_P2_G8, else the HVP ops with FEM_HVP_G8 (their
+// metadata comes from TileSet::meta_g8)
+template <int OP>
+constexpr bool op_g8() {
+  return FEM_P2_G8 ? op_has_p2<OP>()
+                   : (FEM_HVP_G8 && !FEM_P2_BAL && !FEM_P2_NM && !FEM_P2_PAIR && !FEM_WS &&
+                      OP == OP_HVP);  // the linearized HVP measured slower with G8 (0.961 vs 0.737 ms)
+}
+template <int OP>
+constexpr int cb_stride() { return op_g8<OP>() ? kCbStrideG8 : kTile; }
 template <int OP, int MAT>
 constexpr bool op_needs_u() {
   return OP == OP_ENERGY || base_op<OP>() == OP_RESIDUAL || OP == OP_LIN ||
@@ -1330,7 +1396,7 @@ __device__ __forceinline__ void tile_phase1(const PipeArgs &A, const unsigned ch
               const int q = reinterpret_cast<const uint16_t *>(m + A.off_inc)[tid * 4 + a];
               cb[q * D + i] = ok ? f[a][i] : 0.0;
             } else {
-              cb[(a * D + i) * kCbStride + tid] = ok ? f[a][i] : 0.0;
+              cb[(a * D + i) * cb_stride<OP_>() + tid] = ok ? f[a][i] : 0.0;
             }
           }
       }
@@ -1365,6 +1431,37 @@ __device__ __forceinline__ void node_write(const PipeArgs &A, const unsigned cha
   }
 }
 
+// One thread per tile node; the node's entries come in groups of 8 contribution offsets
+// (16-byte loads), pad entries point at the zero columns; two interleaved partial sums.
+template <int D, int OP, int SC>
+__device__ __forceinline__ void tile_phase2_g8(const PipeArgs &A, const unsigned char *m, int U,
+                                            int64_t t, int tid, const double *cb) {
+  const uint16_t *ptr = reinterpret_cast<const uint16_t *>(m + A.off_ptr);
+  const uint4 *grp = reinterpret_cast<const uint4 *>(m + A.off_inc);
+  for (int r = tid; r < U; r += kTile) {
+    const int g0 = ptr[r], g1 = ptr[r + 1];
+    double s0[D], s1[D];
+#pragma unroll
+    for (int cc = 0; cc < D; ++cc) s0[cc] = s1[cc] = 0.0;
+    for (int g = g0; g < g1; ++g) {
+      const uint4 o4 = grp[g];
+      const uint32_t ow[4] = {o4.x, o4.y, o4.z, o4.w};
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const double *pq = cb + ((ow[q >> 1] >> ((q & 1) * 16)) & 0xffffu);
+#pragma unroll
+        for (int cc = 0; cc < D; ++cc) {
+          if (q & 1) s1[cc] += pq[cc * kCbStrideG8];
+          else s0[cc] += pq[cc * kCbStrideG8];
+        }
+      }
+    }
+    double sacc[D];
+#pragma unroll
+    for (int cc = 0; cc < D; ++cc) sacc[cc] = s0[cc] + s1[cc];
+    node_write<D, SC>(A, m, r, t, sacc);
+  }
+}
 #if FEM_P2_BAL
 // Balanced schedule (k_build_sched): every thread sums one task of <= 8 incidences of one
 // node from precomputed offsets; the g lanes of a node combine by a shuffle tree.
@@ -1442,37 +1539,11 @@ __device__ __forceinline__ void tile_phase2(const PipeArgs &A, const unsigned ch
   }
 }
 #elif FEM_P2_G8
-// One thread per tile node; the node's entries come in groups of 8 contribution offsets
-// (16-byte loads), pad entries point at the zero columns; two interleaved partial sums.
 template <int D, int OP, int SC>
 __device__ __forceinline__ void tile_phase2(const PipeArgs &A, const unsigned char *m, int U,
                                             int64_t t, int tid, const double *cb,
                                             int /*nth: default variant only*/ = kTile) {
-  const uint16_t *ptr = reinterpret_cast<const uint16_t *>(m + A.off_ptr);
-  const uint4 *grp = reinterpret_cast<const uint4 *>(m + A.off_inc);
-  for (int r = tid; r < U; r += kTile) {
-    const int g0 = ptr[r], g1 = ptr[r + 1];
-    double s0[D], s1[D];
-#pragma unroll
-    for (int cc = 0; cc < D; ++cc) s0[cc] = s1[cc] = 0.0;
-    for (int g = g0; g < g1; ++g) {
-      const uint4 o4 = grp[g];
-      const uint32_t ow[4] = {o4.x, o4.y, o4.z, o4.w};
-#pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        const double *pq = cb + ((ow[q >> 1] >> ((q & 1) * 16)) & 0xffffu);
-#pragma unroll
-        for (int cc = 0; cc < D; ++cc) {
-          if (q & 1) s1[cc] += pq[cc * kCbStride];
-          else s0[cc] += pq[cc * kCbStride];
-        }
-      }
-    }
-    double sacc[D];
-#pragma unroll
-    for (int cc = 0; cc < D; ++cc) sacc[cc] = s0[cc] + s1[cc];
-    node_write<D, SC>(A, m, r, t, sacc);
-  }
+  tile_phase2_g8<D, OP, SC>(A, m, U, t, tid, cb);
 }
 #elif FEM_P2_PAIR
 // Two lanes per tile node (lanes 2r, 2r+1 of the CTA): each sums half of the node's
@@ -1679,13 +1750,14 @@ __global__ void __launch_bounds__(kTile, pipe_minb(OP, MAT, D)) k_tile_pipe(Pipe
   unsigned char *metab = sm;
   double *nodeb = reinterpret_cast<double *>(sm + NMB * mb);
   double *contrib = nodeb + 2 * nstride;
-  double *geomb = contrib + (DEC ? 2 : 1) * ((D + 1) * D * kCbStride);  // STREAM: 2 blocks
+  constexpr int CBS = cb_stride<OP>();  // contribution row stride (G8: 8 zero pad columns)
+  double *geomb = contrib + (DEC ? 2 : 1) * ((D + 1) * D * CBS);  // STREAM: 2 blocks
   const int64_t G = gridDim.x;
 
   auto tile_id = [&](int64_t i) -> int64_t { return A.list ? (int64_t)__ldg(A.list + i) : i; };
-  if constexpr (FEM_P2_G8 && op_has_p2<OP>()) {  // the pad columns read by the G8 node sums
+  if constexpr (op_g8<OP>()) {  // the pad columns read by the G8 node sums
     for (int q = tid; q < (DEC ? 2 : 1) * (D + 1) * D * 8; q += kTile)
-      contrib[(q / 8) * kCbStride + kTile + (q % 8)] = 0.0;
+      contrib[(q / 8) * CBS + kTile + (q % 8)] = 0.0;
   }
   auto issue_geom = [&](int64_t t, int b) {  // one TMA bulk copy of the tile's geometry block
     if (tid == 0) {
@@ -1782,7 +1854,7 @@ __global__ void __launch_bounds__(kTile, pipe_minb(OP, MAT, D)) k_tile_pipe(Pipe
           prefetch_refm(t + G);
         }
         const double *nb = nodeb + bn * nstride;
-        double *cb = contrib + (k & 1) * ((D + 1) * D * kCbStride);
+        double *cb = contrib + (k & 1) * ((D + 1) * D * CBS);
         if (k >= 2) mb_wait(&mb_p2[k & 1], (unsigned)((k - 2) >> 1) & 1u);  // tile k-2 summed
         tile_phase1<D, MAT, OP, MASK>(A, m, nb, nb + UOFF * um * D, nb + (NF - 1) * um * D, tile_id(t), tid, cb, eacc);
         mb_arrive(&mb_p1[k & 1]);
@@ -1794,7 +1866,8 @@ __global__ void __launch_bounds__(kTile, pipe_minb(OP, MAT, D)) k_tile_pipe(Pipe
         const int nt2 = FEM_P2_LSPLIT > 0 ? reinterpret_cast<const int *>(m)[3] : 0;  // FEM_P2_LSPLIT tasks
         if (tid < (FEM_P2_PAIR ? 2 * U : nt2 > 0 ? ((nt2 + 31) & ~31) : U))
           mb_wait(&mb_p1[k & 1], (unsigned)(k >> 1) & 1u);  // all of tile k's phase 1
-        if constexpr (op_has_p2<OP>()) tile_phase2<D, OP, SC>(A, m, U, tile_id(t), tid, cb);
+        if constexpr (op_g8<OP>()) tile_phase2_g8<D, OP, SC>(A, m, U, tile_id(t), tid, cb);
+        else if constexpr (op_has_p2<OP>()) tile_phase2<D, OP, SC>(A, m, U, tile_id(t), tid, cb);
         mb_arrive(&mb_p2[k & 1]);
       }
     } else {
@@ -1817,11 +1890,13 @@ __global__ void __launch_bounds__(kTile, pipe_minb(OP, MAT, D)) k_tile_pipe(Pipe
           prefetch_refm(t + G);
         }
         const double *nb = nodeb + bn * nstride;
-        double *cb = contrib + (k & 1) * ((D + 1) * D * kCbStride);
+        double *cb = contrib + (k & 1) * ((D + 1) * D * CBS);
         tile_phase1<D, MAT, OP, MASK>(A, m, nb, nb + UOFF * um * D, nb + (NF - 1) * um * D, tile_id(t), tid, cb, eacc);
         __syncthreads();  // phase 1 of tile k done; tile k-1 fully consumed
         if (t + (NMB - 1) * G < A.n_tiles) issue_meta(t + (NMB - 1) * G, (k + NMB - 1) % NMB);
-        if constexpr (op_has_p2<OP>())
+        if constexpr (op_g8<OP>())
+          tile_phase2_g8<D, OP, SC>(A, m, reinterpret_cast<const int *>(m)[0], tile_id(t), tid, cb);
+        else if constexpr (op_has_p2<OP>())
           tile_phase2<D, OP, SC>(A, m, reinterpret_cast<const int *>(m)[0], tile_id(t), tid, cb);
       }
     }
@@ -1864,7 +1939,10 @@ __global__ void __launch_bounds__(kTile, pipe_minb(OP, MAT, D)) k_tile_pipe(Pipe
                                     STREAM ? geomb + (k & 1) * (GBYTES / 8) : nullptr);
       if constexpr (op_has_p2<OP>()) {
         __syncthreads();
-        tile_phase2<D, OP, SC>(A, m, reinterpret_cast<const int *>(m)[0], tile_id(t), tid, contrib);
+        if constexpr (op_g8<OP>())
+          tile_phase2_g8<D, OP, SC>(A, m, reinterpret_cast<const int *>(m)[0], tile_id(t), tid, contrib);
+        else
+          tile_phase2<D, OP, SC>(A, m, reinterpret_cast<const int *>(m)[0], tile_id(t), tid, contrib);
       }
       __syncthreads();
     }
@@ -1891,9 +1969,6 @@ __global__ void __launch_bounds__(kTile, pipe_minb(OP, MAT, D)) k_tile_pipe(Pipe
 // three contribution buffers: 1.123 / 0.930).  ncu: the element warps now wait on empty[b]
 // (25 % of stall samples): the producer's latency-bound node sums, stretched by issue
 // contention with 16 element warps, take longer than phase 1 — so off by default.
-#ifndef FEM_WS
-#define FEM_WS 0
-#endif
 #ifndef FEM_WS_RC
 #define FEM_WS_RC 96
 #endif
@@ -2031,8 +2106,8 @@ static fem_status launch_pipe_t(Problem *p, const PipeArgs &a, cudaStream_t s) {
   const bool need_u = op_needs_u<OP, MAT>();
   const int nf = (op_needs_x<OP, MAT>() ? 1 : 0) + (need_u ? 1 : 0) + (op_is_hvp<OP>() ? 1 : 0);
   if constexpr (op_refm<OP>()) static_assert(MAT == FEM_NEO_HOOKEAN, "OP_*_R: neo-Hookean only");
-  const size_t smem = (size_t)meta_bufs<OP>() * T.mb + sizeof(double) * 2 * (size_t)T.um * D * nf +
-                      (!op_has_p2<OP>() ? 0 : (pipe_decoupled<OP>() ? 2 : 1) * sizeof(double) * (size_t)(D + 1) * D * kCbStride) +
+  const size_t smem = (size_t)meta_bufs<OP>() * (op_g8<OP>() ? T.mb_g8 : T.mb) + sizeof(double) * 2 * (size_t)T.um * D * nf +
+                      (!op_has_p2<OP>() ? 0 : (pipe_decoupled<OP>() ? 2 : 1) * sizeof(double) * (size_t)(D + 1) * D * cb_stride<OP>()) +
                       (op_streams<OP>() ? 2 * sizeof(double) * geom_words(D) * kTile : 0);
   auto kern = k_tile_pipe<D, MAT, OP, MASK, SC>;
   FEM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -2248,6 +2323,21 @@ fem_status tile_pass(Problem *p, int op, const double *u, const double *v, doubl
   a.off_perm = T.off_perm;
   a.has_phase = T.phase != nullptr;
   a.has_perm = T.p2perm != nullptr;
+  // the HVP kernels read the G8 metadata layout (op_g8): same tiles, nodes and lconn offsets
+  if (!FEM_P2_G8 && op_g8<OP_HVP>() && op == OP_HVP) {
+    if (!T.meta_g8) {
+      set_error("HVP tile metadata (G8 layout) missing");
+      return FEM_ERR_CUDA;
+    }
+    a.meta = T.meta_g8;
+    a.mb = T.mb_g8;
+    a.off_inc = T.off_inc_g8;
+    a.off_int = T.off_int_g8;
+    a.off_bc = T.off_bc_g8;
+    a.off_ph = T.off_ph_g8;
+    a.off_perm = T.off_perm_g8;
+    a.has_perm = false;
+  }
   a.slot_off = T.slot_off;
   a.coords = p->coords;
   a.u = u;
@@ -2409,7 +2499,7 @@ fem_status morton_node_order(Problem *p, cudaStream_t s) {
 
 void free_tiles(TileSet &T) {
   void *bufs[] = {T.perm, T.nodes, T.U, T.ptr, T.inc, T.lconn, T.interior, T.phase, T.slot_off,
-                  T.node_slots, T.node_slot_ptr, T.epart, T.meta, T.list, T.geom, T.tcolor_list, T.refm, T.p2perm};
+                  T.node_slots, T.node_slot_ptr, T.epart, T.meta, T.list, T.geom, T.tcolor_list, T.refm, T.p2perm, T.meta_g8, T.p2n};
   for (void *b : bufs)
     if (b) cudaFree(b);
   T = TileSet{};

@@ -132,8 +132,13 @@
 #ifndef FEM_HVP_MD
 #define FEM_HVP_MD 1
 #endif
+// node-data staging of the tile kernels: 1 = one thread per tile node (D copies of each
+// array), 0 = one thread per component.  Re-measured on the end-of-round kernels (cfg 3,
+// device-timed, two pairs): per component HVP 0.886 / 0.885 vs 0.899 / 0.901 ms, residual
+// 0.785 / 0.785 vs 0.802 / 0.801, energy 0.378 / 0.379 vs 0.381 / 0.381 (was neutral in
+// round 1): 0.
 #ifndef FEM_ISSUE_NODE
-#define FEM_ISSUE_NODE 1
+#define FEM_ISSUE_NODE 0
 #endif
 
 namespace fem {
